@@ -1,0 +1,133 @@
+// ss_device.cuh -- device helpers shared by the sm_100a kernels.
+//
+// Numerics contract: the whole translation unit is compiled with
+// --fmad=false so that every `a * b + c` rounds twice, exactly like the
+// numpy float64 ufunc sequence of the reference; expression order below
+// follows the reference line by line (cited per helper). Only the
+// transcendental functions (sin, cos, exp, log, sqrt is exact) can differ
+// from numpy by an ulp; the parity tests carry a tolerance for that.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/stridesim_b200.h"
+
+namespace ss {
+
+// ---------------------------------------------------------------------------
+// splitmix64 counter streams (rng.py:21-41, :69-84)
+
+constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ull;
+constexpr uint64_t kMixA = 0xBF58476D1CE4E5B9ull;
+constexpr uint64_t kMixB = 0x94D049BB133111EBull;
+constexpr uint64_t kKeySalt = 0xD6E8FEB86659FD93ull;
+constexpr double kUnit = 1.1102230246251565e-16;  // 2**-53
+
+__host__ __device__ __forceinline__ uint64_t mix(uint64_t x) {
+    x = (x ^ (x >> 30)) * kMixA;
+    x = (x ^ (x >> 27)) * kMixB;
+    return x ^ (x >> 31);
+}
+
+// key = mix((id + 1) * SALT ^ mix(seed * GOLDEN ^ purpose_id))   (rng.py:64-65)
+__host__ __device__ __forceinline__ uint64_t stream_key(uint64_t base, uint64_t gid) {
+    return mix(((gid + 1ull) * kKeySalt) ^ base);
+}
+
+// word i of a draw starting at counter c   (rng.py:79)
+__device__ __forceinline__ uint64_t stream_word(uint64_t key, uint64_t c, uint64_t i) {
+    return mix(key + (c + i) * kGolden);
+}
+
+// (w >> 11) * 2**-53 in [0, 1)   (rng.py:102)
+__device__ __forceinline__ double unit_from_word(uint64_t w) {
+    return (double)(w >> 11) * kUnit;
+}
+
+// lo + u * (hi - lo)   (rng.py:111)
+__device__ __forceinline__ double uniform_from_word(uint64_t w, double lo, double hi) {
+    return lo + unit_from_word(w) * (hi - lo);
+}
+
+// std * sqrt(-2 log u1) * cos(2 pi u2); u1 in (0,1], u2 in [0,1)   (rng.py:114-119)
+__device__ __forceinline__ double normal_from_words(uint64_t w1, uint64_t w2, double std_) {
+    const double u1 = ((double)(w1 >> 11) + 1.0) * kUnit;
+    const double u2 = (double)(w2 >> 11) * kUnit;
+    const double two_pi = 6.283185307179586;  // 2.0 * np.pi, exactly as numpy forms it
+    return std_ * sqrt(-2.0 * log(u1)) * cos(two_pi * u2);
+}
+
+// ---------------------------------------------------------------------------
+// numpy semantics for NaN-propagating max / min / clip (numpy's _clip and
+// maximum ufunc loops: a NaN in any operand propagates).
+
+__device__ __forceinline__ bool isnan_(double x) { return x != x; }
+
+__device__ __forceinline__ double np_maximum(double a, double b) {
+    // numpy maximum: (a >= b || isnan(a)) ? a : b
+    return (a >= b || isnan_(a)) ? a : b;
+}
+__device__ __forceinline__ double np_minimum(double a, double b) {
+    return (a <= b || isnan_(a)) ? a : b;
+}
+__device__ __forceinline__ double np_clip(double x, double lo, double hi) {
+    // numpy _NPY_CLIP = min(max(x, lo), hi) with _NPY_MAX(a,b) = isnan(a) ? a : (a > b ? a : b)
+    double m = isnan_(x) ? x : (x > lo ? x : lo);
+    return isnan_(m) ? m : (m < hi ? m : hi);
+}
+
+// numpy add.reduce over a short contiguous axis: n < 8 is a sequential sum
+// from 0.0; n >= 8 uses the 8-lane pairwise block (numpy pairwise_sum).
+template <int NMAX>
+__device__ __forceinline__ double np_sum(const double* a, int n) {
+    if (n < 8) {
+        double r = 0.0;
+#pragma unroll
+        for (int i = 0; i < (NMAX < 8 ? NMAX : 7); ++i)
+            if (i < n) r += a[i];
+        return r;
+    }
+    double r[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = (j < NMAX) ? a[j] : 0.0;
+    int i = 8;
+#pragma unroll
+    for (int blk = 8; blk + 8 <= NMAX; blk += 8) {
+        if (blk + 8 <= n) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) r[j] += a[blk + j];
+            i = blk + 8;
+        }
+    }
+    double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+#pragma unroll
+    for (int t = 8; t < NMAX; ++t)
+        if (t >= i && t < n) res += a[t];
+    return res;
+}
+
+// ---------------------------------------------------------------------------
+// heightfield lookup (terrain.py:159-169)
+
+__device__ __forceinline__ double terrain_height(const ss_terrain& t, double x) {
+    if (t.flat) return 0.0;
+    const int64_t last = t.n_samples - 1;
+    double pos = (isfinite(x) ? x : 0.0) / t.spacing;
+    pos = np_clip(pos, 0.0, (double)last);
+    int64_t idx = (int64_t)pos;
+    if (idx > last - 1) idx = last - 1;
+    const double frac = pos - (double)idx;
+    const double s0 = __ldg(t.samples + idx);
+    const double s1 = __ldg(t.samples + idx + 1);
+    return s0 * (1.0 - frac) + s1 * frac;
+}
+
+// ---------------------------------------------------------------------------
+// field access (sim/model.py:26-38): shared -> ptr[c]; expanded -> ptr[c*N + w]
+
+__device__ __forceinline__ double field_at(const ss_field& f, int c, int w, int n) {
+    return f.expanded ? f.ptr[(int64_t)c * n + w] : f.ptr[c];
+}
+
+}  // namespace ss
