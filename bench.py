@@ -1,0 +1,406 @@
+"""Benchmark: env-steps/s of the batched ManagerBasedRlEnv.step on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--envs 4096] [--task Velocity-Rough]
+    python bench.py --impl reference ...      # the CPU implementation of the path (oracle port)
+
+Workload (BASELINE.json configs[1] restated): Velocity-Rough,
+the planar biped on the 5x6 curriculum heightfield, 4096 worlds per GPU,
+decimation 4, random actions from the per-world streams generated on device
+(policies.random_policy, inside the timed region like cli.py:163). One step
+= one control step of every world (4 physics substeps each). Multi-GPU: one
+process per GPU, world_id_offset = rank * N (weak scaling, no collective on
+the data path); time = max over ranks.
+
+Timing: W untimed warm-up steps; then K steps, each preceded by an L2 flush
+(a 512 MiB write, untimed) and bracketed by CUDA events on the launching
+stream; barrier + synchronize around the whole region. The JSON line adds the
+roofline of the fused step kernel, the CPU baseline (oracle port on the host
+cores), and an end-to-end figure through the public API with host buffers.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import multiprocessing as mp
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "env-steps/sec (physics, whole box) at 1/2/4/8 B200 vs host-CPU reference"
+UNIT = "env-steps/s"
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as fh:
+            j = json.load(fh)
+        return float(j["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def _ncu_traffic():
+    """dram bytes per launch of the step kernel from the committed ncu capture (or None)."""
+    p = os.path.join(ROOT, "profiles", "ncu_step_kernel.json")
+    try:
+        with open(p) as fh:
+            j = json.load(fh)
+        return j.get("dram_bytes_per_launch"), j.get("envs")
+    except Exception:
+        return None, None
+
+
+# ---------------------------------------------------------------------------
+# CPU side: the oracle port partitioned over host processes (world_id_offset)
+
+
+def _cpu_worker(conn, task, n_total, n_local, offset, seed):
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    sys.path.insert(0, ROOT)
+    from oracle import OracleEnv
+    from paper_2601_22074_b200.tasks import make_env_cfg
+    from paper_2601_22074_b200.terrain import generate_grid
+
+    cfg = make_env_cfg(task, num_envs=n_local, seed=seed)
+    cfg.scene.world_id_offset = offset
+    env = OracleEnv(cfg, generate_grid(cfg.scene.terrain, cfg.seed).samples)
+    env.reset()
+    conn.send("ready")
+    while True:
+        msg = conn.recv()
+        if msg == "stop":
+            break
+        n_steps = int(msg)
+        t0 = time.perf_counter()
+        for _ in range(n_steps):
+            env.step(env.random_actions())
+        conn.send(time.perf_counter() - t0)
+
+
+class CpuBaseline:
+    """Persistent worker pool; each step() runs one control step of all worlds."""
+
+    def __init__(self, task, n_total, seed=0, procs=None):
+        procs = procs or min(os.cpu_count() or 1, n_total)
+        self.procs = procs
+        ctx = mp.get_context("spawn")
+        self.conns, self.workers = [], []
+        split = np.array_split(np.arange(n_total), procs)
+        for part in split:
+            a, b = ctx.Pipe()
+            w = ctx.Process(target=_cpu_worker, args=(b, task, n_total, len(part), int(part[0]), seed), daemon=True)
+            w.start()
+            self.conns.append(a)
+            self.workers.append(w)
+        for c in self.conns:
+            assert c.recv() == "ready"
+
+    def run(self, n_steps: int) -> float:
+        """Wall seconds for n_steps control steps of all worlds (max over workers)."""
+        t0 = time.perf_counter()
+        for c in self.conns:
+            c.send(n_steps)
+        for c in self.conns:
+            c.recv()
+        return time.perf_counter() - t0
+
+    def close(self):
+        for c in self.conns:
+            c.send("stop")
+        for w in self.workers:
+            w.join(timeout=10)
+
+
+def cpu_model_name() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def measure_cpu(task, n, seconds=10.0, procs=None):
+    pool = CpuBaseline(task, n, procs=procs)
+    try:
+        pool.run(3)
+        steps, el = 0, 0.0
+        while el < seconds:
+            el += pool.run(5)
+            steps += 5
+    finally:
+        pool.close()
+    return {"value": n * steps / el, "unit": UNIT, "cores": pool.procs, "kind": "port",
+            "sample": f"{task} N={n} split over {pool.procs} processes (world_id_offset), {steps} control steps "
+                      f"({el:.1f} s wall), random actions, numpy oracle, CPU {cpu_model_name()}"}
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region
+
+
+class Clocks:
+    def __init__(self, index: int):
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_rank{index}.csv")
+        os.makedirs(os.path.dirname(self.path), exist_ok=True)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                          "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        self.proc.wait()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+
+
+def dist_setup(gpus):
+    import torch
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def allmax(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def run_ours(args):
+    import torch
+
+    import __graft_entry__
+
+    rank, world, local = dist_setup(args.gpus)
+    if rank == 0:
+        __graft_entry__.build()
+    barrier(world)
+    from paper_2601_22074_b200 import native
+    from paper_2601_22074_b200.env import ManagerBasedRlEnv
+    from paper_2601_22074_b200.policies import random_policy
+    from paper_2601_22074_b200.tasks import make_env_cfg
+    from paper_2601_22074_b200.traffic import policy_bytes_per_world, step_bytes_per_world
+
+    n = args.envs
+    cfg = make_env_cfg(args.task, num_envs=n, seed=args.seed)
+    cfg.scene.world_id_offset = rank * n
+    env = ManagerBasedRlEnv(cfg, args.task)
+    env.reset()
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+
+    for i in range(args.warmup):
+        env.step(random_policy(env, i))
+    torch.cuda.synchronize()
+
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+            torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    clocks = Clocks(local)
+    barrier(world)
+    torch.cuda.synchronize()
+    launches0 = native.LAUNCHES["count"]
+    for i in range(args.steps):
+        flush.fill_(float(i))  # evict L2 (126 MB) between timed iterations
+        torch.cuda._sleep(400000)  # ~0.2 ms: let the host run ahead so events time the GPU, not Python
+        e0, e1, e2 = evs[i]
+        e0.record(stream)
+        a = random_policy(env, args.warmup + i)
+        e1.record(stream)
+        env.step(a)
+        e2.record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    launches = native.LAUNCHES["count"] - launches0
+    clk = clocks.stop()
+    t_step = sum(e0.elapsed_time(e2) for e0, _, e2 in evs) / 1e3
+    t_kernel = sum(e1.elapsed_time(e2) for _, e1, e2 in evs) / 1e3
+    t_max = allmax(t_step, world)
+    value = n * world * args.steps / t_max
+
+    # roofline of the dominant kernel (the fused step)
+    per_world = step_bytes_per_world(env)
+    peak, peak_kind = _peaks()
+    achieved = per_world["total"] * n / (t_kernel / args.steps) / 1e9
+    traffic, traffic_envs = _ncu_traffic()
+    if traffic is not None and traffic_envs not in (None, n):
+        traffic = None
+
+    # end-to-end through the public API with host buffers
+    om = env.observation_manager
+    obs_dim = sum(om.group_dim(g) for g in om.groups)
+    A = env.action_manager.total_dim
+    rng = np.random.default_rng(rank)
+    host_actions = torch.from_numpy(rng.uniform(-1, 1, size=(args.steps, n, A))).pin_memory()
+    host_obs = {g: torch.empty((n, om.group_dim(g)), dtype=torch.float64).pin_memory() for g in om.groups}
+    host_rew = torch.empty(n, dtype=torch.float64).pin_memory()
+    host_done = torch.empty((2, n), dtype=torch.bool).pin_memory()
+    dev_actions = torch.empty((n, A), dtype=torch.float64, device="cuda")
+    barrier(world)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        dev_actions.copy_(host_actions[i], non_blocking=True)
+        obs, rew, term, trunc, _ = env.step(dev_actions)
+        for g in om.groups:
+            host_obs[g].copy_(obs[g], non_blocking=True)
+        host_rew.copy_(rew, non_blocking=True)
+        host_done[0].copy_(term, non_blocking=True)
+        host_done[1].copy_(trunc, non_blocking=True)
+        stream.synchronize()
+    e2e_t = allmax(time.perf_counter() - t0, world)
+    e2e = {"value": n * world * args.steps / e2e_t, "unit": UNIT, "h2d_bytes_per_step": n * A * 8,
+           "d2h_bytes_per_step": n * obs_dim * 8 + n * 8 + 2 * n}
+
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu:
+            cpu = measure_cpu(args.task, n, seconds=args.cpu_seconds)
+        line = {
+            "metric": METRIC,
+            "value": value,
+            "unit": UNIT,
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": 1e3 * t_max / args.steps,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic (random actions from the per-world device streams; random-init env, no checkpoint)",
+            "config": {"workload": f"{args.task} (planar biped restatement of BASELINE configs[1], SURVEY 0.1)",
+                       "task": args.task, "envs_per_gpu": n, "decimation": env.decimation,
+                       "substeps_per_step": env.decimation, "parallelism": f"dp{world} (world shards)",
+                       "l2": "flushed (512 MiB write) between timed iterations"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "peak_kind": peak_kind, "traffic": traffic,
+                         "algorithmic_bytes_per_env_step": per_world["total"],
+                         "kernel": "step_kernel<4,2> (fused control step)",
+                         "kernel_ms": 1e3 * t_kernel / args.steps},
+            "policy_bytes_per_env_step": policy_bytes_per_world(env),
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    n = args.envs
+    pool = CpuBaseline(args.task, n)
+    try:
+        pool.run(max(1, args.warmup))
+        el = pool.run(args.steps)
+    finally:
+        pool.close()
+    v = n * args.steps / el
+    line = {
+        "metric": METRIC,
+        "value": v,
+        "unit": UNIT,
+        "n_gpus": args.gpus,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": 1e3 * el / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (random actions from the per-world streams)",
+        "config": {"workload": f"{args.task} (planar biped restatement of BASELINE configs[1], SURVEY 0.1)",
+                   "task": args.task, "envs_per_gpu": n, "decimation": 4},
+        "impl": "reference",
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": pool.procs, "kind": "port",
+                         "sample": f"{args.task} N={n} over {pool.procs} host processes, {args.steps} control steps, "
+                                   f"numpy oracle port of the reference, CPU {cpu_model_name()}"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--envs", type=int, default=4096)
+    ap.add_argument("--task", default="Velocity-Rough")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -85,7 +85,10 @@ extern "C" {
 #define SS_ST_PREV_AFTER 8192u /* prev_lin_vel_b <- root_lin_vel_b after obs  */
 #define SS_ST_PREV_BEFORE 16384u /* ... before obs (env.reset order)          */
 #define SS_ST_RESET_EXT 32768u /* reset mask read from uniforms.reset_mask    */
-#define SS_ST_STEP_ALL 0x3FFFu /* ACTION..PREV_AFTER minus PREV_BEFORE        */
+#define SS_ST_STEP_ALL 0x3DFFu /* ACTION..PREV_AFTER, without RESET_ALL      */
+
+/* ss_uniforms.flags */
+#define SS_FLAG_NO_EPISODE 1u  /* TERM without the env.py:235-238 bookkeeping  */
 
 /* observation term function ids (mdp.py:26-89) */
 #define SS_OBS_BASE_LIN_VEL 1
@@ -398,6 +401,7 @@ typedef struct ss_env_desc {
     uint8_t* truncated;
     uint8_t* nonfinite;
     int64_t* trigger_counts;
+    uint32_t* nf_flags;
     /* rewards (managers/reward.py) */
     int32_t n_rewards;
     int32_t pad6;
@@ -442,6 +446,8 @@ typedef struct ss_env_desc {
 typedef struct ss_uniforms {
     uint32_t stages;
     int32_t nsub;
+    uint32_t flags;
+    int32_t nf_slot;
     int64_t global_step;
     int64_t sim_step;
     int32_t capture_slot0;

@@ -929,11 +929,15 @@ __global__ void __launch_bounds__(kBlock) step_kernel(const __grid_constant__ ss
         // ---- 3. episode bookkeeping + TerminationManager.compute (env.py:235-239)
         bool have_ep = false;
         if (st & SS_ST_TERM) {
-            s.ep_steps = d.episode_steps[w] + 1;
-            s.cmd_dist = d.commanded_distance[w] + fabs(s.cmd[0]) * d.dt_control;
+            s.ep_steps = d.episode_steps[w];
+            s.cmd_dist = d.commanded_distance[w];
+            if (!(u.flags & SS_FLAG_NO_EPISODE)) {
+                s.ep_steps += 1;
+                if (d.n_cmd > 0) s.cmd_dist = s.cmd_dist + fabs(s.cmd[0]) * d.dt_control;
+                d.episode_steps[w] = s.ep_steps;
+                d.commanded_distance[w] = s.cmd_dist;
+            }
             have_ep = true;
-            d.episode_steps[w] = s.ep_steps;
-            d.commanded_distance[w] = s.cmd_dist;
             bool term = false, trunc = false;
             for (int t = 0; t < d.n_terms; ++t) {
                 const ss_term_term& T = d.term[t];
@@ -981,14 +985,15 @@ __global__ void __launch_bounds__(kBlock) step_kernel(const __grid_constant__ ss
         }
 
         // ---- 5. curriculum on the finished episode, then masked reset (env.py:245-250)
-        bool do_reset = false;
-        if (st & SS_ST_RESET_ALL) do_reset = true;
-        else if (st & SS_ST_RESET) {
-            if (st & SS_ST_RESET_EXT) do_reset = u.reset_mask[w] != 0;
-            else if (st & SS_ST_TERM) do_reset = s.terminated || s.truncated;
-            else do_reset = d.terminated[w] || d.truncated[w];
+        bool selected = false;
+        if (st & SS_ST_RESET_ALL) selected = true;
+        else if (st & (SS_ST_RESET | SS_ST_CURRICULUM)) {
+            if (st & SS_ST_RESET_EXT) selected = u.reset_mask[w] != 0;
+            else if (st & SS_ST_TERM) selected = s.terminated || s.truncated;
+            else selected = d.terminated[w] || d.truncated[w];
         }
-        if (do_reset && (st & SS_ST_CURRICULUM)) {
+        const bool do_reset = selected && (st & (SS_ST_RESET | SS_ST_RESET_ALL));
+        if (selected && (st & SS_ST_CURRICULUM)) {
             if (!have_ep) {
                 s.ep_steps = d.episode_steps[w];
                 s.cmd_dist = d.commanded_distance[w];
@@ -1181,8 +1186,12 @@ __global__ void __launch_bounds__(kBlock) step_kernel(const __grid_constant__ ss
             if (lane == 0 && m) atomicAdd((unsigned long long*)&d.trigger_counts[t], (unsigned long long)__popc(m));
         }
         const unsigned m = __ballot_sync(0xffffffffu, (s.trig_bits >> 31) & 1u);
-        if (lane == 0 && m)
+        if (lane == 0 && m) {
             atomicAdd((unsigned long long*)&d.trigger_counts[d.n_terms], (unsigned long long)__popc(m));
+            // zero-copy flag in mapped pinned host memory: lets the host notice a
+            // nonfinite step without a per-step device->host copy (env.py:240-241)
+            if (d.nf_flags) *((volatile uint32_t*)&d.nf_flags[u.nf_slot]) = 1u;
+        }
     }
 }
 

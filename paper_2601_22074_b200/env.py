@@ -1,0 +1,446 @@
+"""ManagerBasedRlEnv on one B200: the reset/step state machine over N worlds.
+
+Drop-in for the reference env (env.py:95-305): same constructor, reset/step
+signatures, stage order and public attributes; state lives in HBM and a
+control step is ONE launch of the fused sm_100a kernel when every term is a
+built-in (act, d substeps, terminate, reward, curriculum + masked reset,
+command, events, observe -- env.py:219-259). With user-registered Python
+terms the same kernel runs stage by stage and the plugins are evaluated in
+between on the device tensors ("staged" mode), preserving the order.
+
+No step ever waits on the device: reset ids, trigger counts and extras are
+materialized lazily; nonfinite detection rides a zero-copy flag in pinned
+host memory and is processed at most ``NF_LAG`` steps later (the capture
+ring keeps that many spare steps of frames so the dump is exact).
+"""
+
+from __future__ import annotations
+
+import os
+from collections import deque
+from collections.abc import Mapping
+
+import numpy as np
+
+from . import mdp  # noqa: F401  (registers the built-in terms)
+from . import native
+from .capture import CaptureRing, dump_capture, load_capture, model_field_metadata
+from .config import ContactSensorCfg, EnvCfg, InitStateCfg, SceneCfg, config_hash, to_dict
+from .entity import DefaultState, Entity, EntityData
+from .managers import (
+    ActionManager,
+    CommandManager,
+    CurriculumManager,
+    EventManager,
+    ObservationManager,
+    RewardManager,
+    TerminationManager,
+)
+from .rng import StreamPack
+from .sensors import ContactSensor, RayScanner
+from .sim import BatchState, StepPipeline, compile_model, restore, snapshot
+from .terrain import generate_grid
+
+__all__ = ["EnvCfg", "SceneCfg", "InitStateCfg", "ManagerBasedRlEnv", "load_capture"]
+
+NF_LAG = 3  # control steps the host may run ahead before it must look at nonfinite flags
+
+_SIM = native.SS_ST_APPLY | native.SS_ST_PUSH | native.SS_ST_PHYS | native.SS_ST_SENSOR
+
+
+class _Extras(Mapping):
+    """Per-step extras (env.py:261-272), materialized on first access.
+
+    Values refer to this step's device buffers and are valid until the next
+    step (like the observation buffers)."""
+
+    def __init__(self, env, step: int):
+        self._env = env
+        self._step = step
+        self._data = None
+
+    def _build(self):
+        import torch
+
+        if self._data is None:
+            env = self._env
+            tm, rm = env.termination_manager, env.reward_manager
+            ids = torch.nonzero(tm.terminated | tm.truncated).reshape(-1)
+            d = {"reset_ids": ids}
+            if ids.numel():
+                for name in rm.terms:
+                    d[f"episode_reward/{name}"] = rm.finalized[name][ids]
+            for name in rm.terms:
+                d[f"reward/{name}"] = rm.last_values[name]
+            for name, c in tm.trigger_counts.items():
+                d[f"termination_count/{name}"] = np.int64(c)
+            d["curriculum/terrain_rows"] = env.terrain_rows
+            d["nonfinite_worlds"] = tm.last_nonfinite
+            self._data = d
+        return self._data
+
+    def __getitem__(self, k):
+        return self._build()[k]
+
+    def __iter__(self):
+        return iter(self._build())
+
+    def __len__(self):
+        return len(self._build())
+
+
+class ManagerBasedRlEnv:
+    def __init__(self, cfg: EnvCfg, task_id: str = "", device=None):
+        import torch
+
+        self.cfg = cfg
+        self.task_id = task_id
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        spec = cfg.scene.model
+        if cfg.physics_dt is not None:
+            spec.physics_dt = cfg.physics_dt
+        if cfg.decimation is not None:
+            spec.decimation = cfg.decimation
+        self.physics_dt = spec.physics_dt
+        self.decimation = spec.decimation
+        self.dt_control = self.physics_dt * self.decimation
+        self.max_episode_steps = int(np.ceil(cfg.episode_length_s / self.dt_control - 1e-9))
+        self.num_envs = n = cfg.scene.num_envs
+
+        self.config_hash = config_hash(cfg)
+        self.terrain = generate_grid(cfg.scene.terrain, cfg.seed)
+        self.model = compile_model(spec, n, self.device)
+        self.state = BatchState(self.model)
+        self.world_ids = cfg.scene.world_id_offset + np.arange(n)
+        self.streams = StreamPack(cfg.seed, cfg.scene.world_id_offset, n, self.device, self._invalidate)
+
+        init = cfg.scene.init_state
+        k = self.model.num_joints
+        self.default_joint_pos = np.asarray(init.joint_pos or (0.0,) * k, dtype=np.float64)
+        self.robot = Entity(
+            spec.name,
+            joint_names=self.model.joint_names,
+            default_state=DefaultState(base_pose=init.base_pose, base_vel=init.base_vel,
+                                       joint_pos=tuple(self.default_joint_pos),
+                                       joint_vel=tuple(init.joint_vel or (0.0,) * k)),
+            pos_limits=self.model.pos_limits,
+        )
+        self.entities = {spec.name: self.robot, "terrain": Entity("terrain", base_type="fixed")}
+        self.entity_data = EntityData(self.model, self.state)
+        self.contact_sensor = ContactSensor(ContactSensorCfg(history_length=cfg.scene.contact_history), n,
+                                            len(self.model.feet), self.device)
+        self.ray_scanner = RayScanner(cfg.scene.ray_scan, n, self.device)
+        self.pipeline = StepPipeline(self.model, self.terrain)
+        self.capture = CaptureRing(cfg.capture_len, n, self.model.nq, k, self.device,
+                                   spare=self.decimation * (NF_LAG + 1))
+
+        dev = self.device
+        self.terrain_rows = torch.zeros(n, dtype=torch.int64, device=dev)
+        self.terrain_cols = torch.as_tensor((self.world_ids % self.terrain.cols).astype(np.int64), device=dev)
+        self.episode_steps = torch.zeros(n, dtype=torch.int64, device=dev)
+        self.episode_start_x = torch.zeros(n, dtype=torch.float64, device=dev)
+        self.commanded_distance = torch.zeros(n, dtype=torch.float64, device=dev)
+        self._prev_lin_vel_b = torch.zeros((2, n), dtype=torch.float64, device=dev)
+        self.global_step = 0
+        self._dump_paths: list[str] = []
+        self._startup_done = False
+        self._desc = None
+        self._u = native.Uniforms()
+        self._launches = 0
+
+        # nonfinite bookkeeping: zero-copy flags + a ring of per-step world masks
+        self._nf_flags = torch.zeros(NF_LAG + 2, dtype=torch.int32).pin_memory()
+        self._nf_masks = torch.zeros((NF_LAG + 2, n), dtype=torch.bool, device=dev)
+        self._nf_slot = 0
+        self._nf_pending: deque = deque()
+
+        all_ids = torch.arange(n, device=dev)
+        self.robot.write_default_state(self.state, all_ids)
+        self._place_on_terrain(all_ids)
+
+        self.action_manager = ActionManager(cfg.actions, self)
+        self.command_manager = CommandManager(cfg.commands, self)
+        self.reward_manager = RewardManager(cfg.rewards, self)
+        self.termination_manager = TerminationManager(cfg.terminations, self)
+        self.termination_manager.last_nonfinite = self._nf_masks[0]
+        self.event_manager = EventManager(cfg.events, self)
+        self.curriculum_manager = CurriculumManager(cfg.curriculum, self)
+        self.observation_manager = ObservationManager(cfg.observations, self)
+        self.model.on_layout_change(self._invalidate)
+        self.staged = self._needs_staging()
+
+    # -- descriptor ---------------------------------------------------------------
+
+    prev_lin_vel_b = property(lambda self: self._prev_lin_vel_b.t())
+
+    def _invalidate(self, *_):
+        self._desc = None
+
+    def _needs_staging(self) -> bool:
+        return bool(self.termination_manager.external or self.reward_manager.external
+                    or self.curriculum_manager.has_external
+                    or any(self.event_manager.is_external(nm) and self.cfg.events[nm].mode != "startup"
+                           for nm in self.event_manager.terms)
+                    or self.observation_manager.has_external)
+
+    def _get_desc(self):
+        if self._desc is None:
+            d = native.EnvDesc()
+            d.abi_version = native.SS_ABI_VERSION
+            d.n_worlds = self.num_envs
+            d.decimation = self.decimation
+            d.max_episode_steps = self.max_episode_steps
+            d.dt_control = self.dt_control
+            self.model.native_into(d)
+            d.terrain = self.terrain.native(self.device)
+            self.state.native_into(d.state)
+            r = self.streams
+            d.rng.world_id_offset = r.world_id_offset
+            for s, base in enumerate(r.bases):
+                d.rng.base[s] = base
+                d.rng.counter[s] = r.counters[s].data_ptr()
+            ds = self.robot.default_state
+            for i in range(3):
+                d.base_pose[i] = float(ds.base_pose[i])
+                d.base_vel[i] = float(ds.base_vel[i])
+            for j in range(self.model.num_joints):
+                d.joint_pos[j] = float(ds.joint_pos[j])
+                d.joint_vel[j] = float(ds.joint_vel[j])
+            d.spawn_offset = float(self.cfg.scene.spawn_offset)
+            self.action_manager.native_into(d)
+            self.capture.native_into(d)
+            self.contact_sensor.native_into(d)
+            self.ray_scanner.native_into(d)
+            self.termination_manager.native_into(d)
+            self.reward_manager.native_into(d)
+            self.command_manager.native_into(d)
+            self.event_manager.native_into(d)
+            self.curriculum_manager.native_into(d)
+            d.episode_steps = self.episode_steps.data_ptr()
+            d.episode_start_x = self.episode_start_x.data_ptr()
+            d.commanded_distance = self.commanded_distance.data_ptr()
+            d.terrain_rows = self.terrain_rows.data_ptr()
+            d.terrain_cols = self.terrain_cols.data_ptr()
+            d.prev_lin_vel_b = self._prev_lin_vel_b.data_ptr()
+            self.observation_manager.native_into(d)
+            d.nf_flags = self._nf_flags.data_ptr()
+            # the descriptor may have allocated new stream slots: refresh their pointers
+            for s, base in enumerate(r.bases):
+                d.rng.base[s] = base
+                d.rng.counter[s] = r.counters[s].data_ptr()
+            self._desc = d
+        return self._desc
+
+    def _launch(self, stages: int, nsub: int = 0, actions=None, reset_mask=None, groups_mask: int = 0,
+                flags: int = 0) -> None:
+        """One ss_env_step launch with every host-tracked per-step scalar."""
+        d = self._get_desc()
+        if self._desc is None:  # a slot was allocated while building
+            d = self._get_desc()
+        u = self._u
+        u.stages = stages
+        u.nsub = nsub
+        u.flags = flags
+        u.global_step = self.global_step
+        sim_step = self.state.sim_step
+        u.sim_step = sim_step
+        if stages & native.SS_ST_PUSH:
+            u.capture_slot0 = self.capture.reserve(nsub, sim_step)
+        if stages & native.SS_ST_SENSOR:
+            u.sensor_mask = self.contact_sensor.enabled_mask(sim_step, nsub, bool(stages & native.SS_ST_PHYS))
+        if stages & native.SS_ST_APPLY:
+            self.action_manager.advance_heads(u, nsub)
+        om = self.observation_manager
+        u.groups_mask = groups_mask
+        u.any_pending = int(om.any_pending)
+        if stages & native.SS_ST_OBS:
+            om.fill_heads(u)
+        if stages & native.SS_ST_REWARD:
+            self.reward_manager.fill_weights(u)
+        u.actions = None if actions is None else actions.data_ptr()
+        u.reset_mask = None if reset_mask is None else reset_mask.data_ptr()
+        if stages & native.SS_ST_TERM:
+            slot = self._nf_slot
+            d.nonfinite = self._nf_masks[slot].data_ptr()
+            self.termination_manager.last_nonfinite = self._nf_masks[slot]
+            self._nf_flags[slot] = 0
+            u.nf_slot = slot
+        native.call("ss_env_step", native.byref(d), native.byref(u), native.current_stream(self.device))
+        self._launches += 1
+        if stages & native.SS_ST_PHYS:
+            self.state.sim_step += nsub
+        if stages & native.SS_ST_OBS and (groups_mask + 1) == (1 << len(om.groups)):
+            om.any_pending = False
+        if stages & (native.SS_ST_RESET | native.SS_ST_RESET_ALL) and not stages & native.SS_ST_OBS:
+            om.any_pending = True
+        if stages & native.SS_ST_TERM:
+            self._nf_note()
+
+    # -- nonfinite detection (deferred, no per-step sync) ----------------------------
+
+    def _nf_note(self) -> None:
+        import torch
+
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(self.device))
+        self._nf_pending.append((ev, self._nf_slot, self.capture.pushes, self.capture.count, self.state.sim_step))
+        self._nf_slot = (self._nf_slot + 1) % self._nf_flags.numel()
+        self._nf_drain(NF_LAG)
+
+    def _nf_drain(self, keep: int) -> None:
+        while self._nf_pending:
+            ev, slot, pushes, count, sim_step = self._nf_pending[0]
+            if len(self._nf_pending) > keep:
+                ev.synchronize()
+            elif not ev.query():
+                break
+            self._nf_pending.popleft()
+            if int(self._nf_flags[slot]):
+                self._dump_on_nonfinite(slot, pushes, count, sim_step)
+
+    @property
+    def dump_paths(self) -> list[str]:
+        self._nf_drain(0)
+        return self._dump_paths
+
+    def _dump_on_nonfinite(self, slot: int, pushes: int, count: int, sim_step: int) -> None:
+        os.makedirs(self.cfg.capture_dir, exist_ok=True)
+        path = os.path.join(self.cfg.capture_dir, f"capture_step{sim_step}.bin")
+        self._write_dump(path, pushes, count, self._nf_masks[slot])
+        self._dump_paths.append(path)
+
+    def _write_dump(self, path: str, pushes=None, count=None, nonfinite=None) -> None:
+        import torch
+
+        nf = self.termination_manager.last_nonfinite if nonfinite is None else nonfinite
+        meta = {
+            "offending_observation_terms": sorted(self.observation_manager.nonfinite_report),
+            "offending_reward_terms": sorted(self.reward_manager.nonfinite_report),
+            "nonfinite_worlds": torch.nonzero(nf).reshape(-1).cpu().tolist(),
+            "fields": model_field_metadata(self.model),
+        }
+        dump_capture(path, self.capture, self.config_hash, task_id=self.task_id, config_json=to_dict(self.cfg),
+                     metadata=meta, pushes=pushes, count=count)
+
+    def dump_capture(self, path: str) -> None:
+        self._nf_drain(0)
+        self._write_dump(path)
+
+    # -- reset --------------------------------------------------------------------------
+
+    def _place_on_terrain(self, ids) -> None:
+        """Spawn on the world's curriculum patch + terrain height (env.py:171-180)."""
+        import torch
+
+        rows, cols = self.terrain_rows[ids], self.terrain_cols[ids]
+        origin = (rows * self.terrain.cols + cols).to(torch.float64) * self.terrain.patch_length
+        spawn_x = origin + self.cfg.scene.spawn_offset
+        self.state.q[ids, 0] += spawn_x
+        self.state.q[ids, 1] += self.terrain.heights(spawn_x)
+
+    def _reset_worlds(self, ids) -> None:
+        """Standalone masked reset of the listed worlds (env.py:182-200)."""
+        import torch
+
+        ids_t = torch.as_tensor(np.asarray(ids) if not torch.is_tensor(ids) else ids, device=self.device)
+        mask = torch.zeros(self.num_envs, dtype=torch.uint8, device=self.device)
+        mask[ids_t] = 1
+        self.event_manager.prepare_fields()
+        self._launch(native.SS_ST_RESET | native.SS_ST_RESET_EXT, reset_mask=mask)
+        self.event_manager.run_external_reset(ids_t)
+        self.ray_scanner._cached_step = -1
+
+    def reset(self, seed: int | None = None) -> dict:
+        """Start fresh episodes in every world and return the first obs (env.py:202-215)."""
+        import torch
+
+        if seed is not None:
+            self.streams = StreamPack(seed, self.cfg.scene.world_id_offset, self.num_envs, self.device,
+                                      self._invalidate)
+            self._invalidate()
+            self._startup_done = False
+        if not self._startup_done:
+            self.event_manager.apply_startup()
+            self._startup_done = True
+        self.event_manager.prepare_fields()
+        om = self.observation_manager
+        ext_reset = any(self.event_manager.is_external(nm) and tc.mode == "reset"
+                        for nm, tc in self.cfg.events.items())
+        all_ids = torch.arange(self.num_envs, device=self.device)
+        om._cache.clear()
+        if ext_reset or om.has_external:
+            self._launch(native.SS_ST_RESET_ALL)
+            self.event_manager.run_external_reset(all_ids)
+            self._launch(native.SS_ST_PREV_BEFORE)
+            om.eval_external(list(om.groups))
+            mask = om.begin(list(om.groups))
+            self._launch(native.SS_ST_OBS, groups_mask=mask)
+        else:
+            mask = om.begin(list(om.groups))
+            self._launch(native.SS_ST_RESET_ALL | native.SS_ST_PREV_BEFORE | native.SS_ST_OBS, groups_mask=mask)
+        self.ray_scanner._cached_step = -1
+        return om.outputs()
+
+    # -- step -------------------------------------------------------------------------------
+
+    def step(self, actions):
+        """One control step through the fixed eight-stage pipeline.
+
+        Returns (obs groups, reward, terminated, truncated, extras); all device
+        tensors, valid until the next step."""
+        a = self.action_manager.check_actions(actions)
+        if not self._startup_done:
+            self.event_manager.prepare_fields()
+        self.global_step += 1
+        om = self.observation_manager
+        om._cache.clear()
+        if not self.staged:
+            mask = om.begin(list(om.groups))
+            self._launch(native.SS_ST_STEP_ALL, nsub=self.decimation, actions=a, groups_mask=mask)
+            self.curriculum_manager.run_host(None)
+        else:
+            self._step_staged(a)
+        self.ray_scanner._cached_step = -1
+        tm = self.termination_manager
+        return om.outputs(), self.reward_manager.reward, tm.terminated, tm.truncated, _Extras(self, self.global_step)
+
+    def _step_staged(self, a) -> None:
+        import torch
+
+        om, em, cm = self.observation_manager, self.event_manager, self.curriculum_manager
+        self._launch(native.SS_ST_ACTION | _SIM, nsub=self.decimation, actions=a)
+        self.termination_manager.eval_external()
+        self._launch(native.SS_ST_TERM)
+        self.reward_manager.eval_external()
+        self._launch(native.SS_ST_REWARD)
+        ext_reset = any(em.is_external(nm) and tc.mode == "reset" for nm, tc in self.cfg.events.items())
+        if cm.has_external or ext_reset:
+            tm = self.termination_manager
+            ids = torch.nonzero(tm.terminated | tm.truncated).reshape(-1)
+            self._launch(native.SS_ST_CURRICULUM)
+            cm.run_external(ids)
+            cm.run_host(ids)
+            self._launch(native.SS_ST_RESET)
+            em.run_external_reset(ids)
+        else:
+            self._launch(native.SS_ST_CURRICULUM | native.SS_ST_RESET)
+            cm.run_host(None)
+        self._launch(native.SS_ST_COMMAND | native.SS_ST_EVENTS)
+        em.run_external_interval()
+        om.eval_external(list(om.groups))
+        mask = om.begin(list(om.groups))
+        self._launch(native.SS_ST_OBS | native.SS_ST_PREV_AFTER, groups_mask=mask)
+
+    # -- convenience passthroughs (tests, replay) ---------------------------------------------
+
+    def snapshot(self):
+        return snapshot(self.state)
+
+    def restore(self, frame) -> None:
+        restore(self.state, frame)
+
+    def synchronize(self) -> None:
+        import torch
+
+        torch.cuda.synchronize(self.device)
+        self._nf_drain(0)

@@ -140,7 +140,11 @@ def lib():
     return _LIB
 
 
+LAUNCHES = {"count": 0}  # kernel launches issued through the C-ABI (bench.py reports them)
+
+
 def call(name: str, *args) -> None:
+    LAUNCHES["count"] += 1
     rc = getattr(lib(), name)(*args)
     if rc != 0:
         msg = lib().ss_last_error().decode(errors="replace")
