@@ -27,6 +27,7 @@
  *   ss_heights       Heightfield.heights                terrain.py:159-169
  *   ss_randomize     randomize_field (startup/explicit) managers/event.py:19-52
  *   ss_actuator_eval pd_torque / dc_motor_torque        actuators.py:104-117
+ *   ss_jit_*         StepPipeline._rebuild (re-specialize to the layout) sim/physics.py:158-237
  *
  * Layout: every per-world array is structure-of-arrays, component-major,
  * i.e. element (world w, component c) of an (N, C) logical array lives at
@@ -41,8 +42,18 @@
 #ifndef STRIDESIM_B200_H
 #define STRIDESIM_B200_H
 
+#ifdef __CUDACC_RTC__
+/* NVRTC (the per-env JIT specialization of the step) has no libc headers */
+typedef signed char int8_t;
+typedef unsigned char uint8_t;
+typedef int int32_t;
+typedef unsigned int uint32_t;
+typedef long long int64_t;
+typedef unsigned long long uint64_t;
+#else
 #include <stddef.h>
 #include <stdint.h>
+#endif
 
 #ifdef __cplusplus
 extern "C" {
@@ -482,6 +493,7 @@ typedef struct ss_rng_draw_args {
     double* out;
 } ss_rng_draw_args;
 
+#ifndef __CUDACC_RTC__ /* host entry points (not part of the JIT translation unit) */
 int ss_abi_version(void);
 size_t ss_sizeof(int which); /* 0 env_desc, 1 uniforms, 2 rng_draw_args */
 const char* ss_last_error(void);
@@ -495,10 +507,20 @@ int ss_heights(const ss_terrain* terrain, const double* x, double* out, int64_t 
 int ss_randomize(const ss_env_desc* desc, int32_t field, int32_t distribution,
                  double r0, double r1, int32_t operation, int32_t slot,
                  const int64_t* sel, int32_t n_sel, void* stream);
+/* Per-env specialization: NVRTC-compile the step body with the env's term
+ * tables as compile-time constants (csrc/ss_cfg.cuh), load it, launch it.
+ * Same semantics and results as ss_env_step. */
+int ss_jit_compile(const char* src, int n_headers, const char* const* header_src,
+                   const char* const* header_names, int n_opts, const char* const* opts,
+                   void* out, size_t* size, char* log, size_t log_size);
+int ss_jit_load(const void* cubin, size_t size, const char* kernel_name, void** handle);
+int ss_jit_unload(void* handle);
+int ss_env_step_jit(void* handle, const ss_env_desc* desc, const ss_uniforms* u, void* stream);
 int ss_actuator_eval(int32_t kind, const double* kp, const double* kd, double effort,
                      double saturation, double vel_limit, const double* q_des,
                      const double* q, const double* qd, double* out, int64_t n,
                      void* stream);
+#endif /* __CUDACC_RTC__ */
 
 #ifdef __cplusplus
 }

@@ -8,10 +8,12 @@
 // from numpy by an ulp; the parity tests carry a tolerance for that.
 #pragma once
 
+#ifndef __CUDACC_RTC__
 #include <cstdint>
 #include <cuda_runtime.h>
 
 #include "../../include/stridesim_b200.h"
+#endif
 
 namespace ss {
 

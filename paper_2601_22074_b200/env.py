@@ -17,13 +17,14 @@ ring keeps that many spare steps of frames so the dump is exact).
 from __future__ import annotations
 
 import os
+import warnings
 from collections import deque
 from collections.abc import Mapping
 
 import numpy as np
 
 from . import mdp  # noqa: F401  (registers the built-in terms)
-from . import native
+from . import jit, native
 from .capture import CaptureRing, dump_capture, load_capture, model_field_metadata
 from .config import ContactSensorCfg, EnvCfg, InitStateCfg, SceneCfg, config_hash, to_dict
 from .entity import DefaultState, Entity, EntityData
@@ -145,6 +146,8 @@ class ManagerBasedRlEnv:
         self._dump_paths: list[str] = []
         self._startup_done = False
         self._desc = None
+        self._jit_handle = None
+        self.use_jit = jit.enabled()
         self._u = native.Uniforms()
         self._launches = 0
 
@@ -175,6 +178,7 @@ class ManagerBasedRlEnv:
 
     def _invalidate(self, *_):
         self._desc = None
+        self._jit_handle = None
 
     def _needs_staging(self) -> bool:
         return bool(self.termination_manager.external or self.reward_manager.external
@@ -265,7 +269,17 @@ class ManagerBasedRlEnv:
             self.termination_manager.last_nonfinite = self._nf_masks[slot]
             self._nf_flags[slot] = 0
             u.nf_slot = slot
-        native.call("ss_env_step", native.byref(d), native.byref(u), native.current_stream(self.device))
+        stream = native.current_stream(self.device)
+        if self.use_jit and self._jit_handle is None:
+            try:
+                self._jit_handle = jit.module_for(d)
+            except jit.JitUnsupported as err:
+                warnings.warn(f"per-env specialization unavailable ({err}); using the generic sm_100a kernel")
+                self.use_jit = False
+        if self.use_jit:
+            native.call("ss_env_step_jit", self._jit_handle, native.byref(d), native.byref(u), stream)
+        else:
+            native.call("ss_env_step", native.byref(d), native.byref(u), stream)
         self._launches += 1
         if stages & native.SS_ST_PHYS:
             self.state.sim_step += nsub

@@ -1,0 +1,183 @@
+"""Per-env specialization of the fused step kernel (NVRTC, sm_100a).
+
+The reference re-specializes its substep whenever the model layout changes
+(StepPipeline._rebuild, sim/physics.py:158-237). Here the analogous step is
+a compile: every value the kernel reads from the term tables is turned into
+a compile-time constant (the X-lists of csrc/ss_cfg.cuh, evaluated against
+the env's descriptor), so NVRTC unrolls every term loop, folds topology and
+parameters into immediates and keeps each world's arrays in registers. The
+kernel source is the same ss_kernel.cuh the generic AOT build uses, so the
+two agree bit for bit; device pointers and RNG keys stay runtime values.
+
+Compiled cubins are cached in memory by source hash (and on disk under
+$XDG_CACHE_HOME/paper_2601_22074_b200/jit, an optional speed-up only).
+SS_JIT=0 in the environment selects the generic kernel.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import hashlib
+import math
+import os
+import re
+
+from . import native
+
+_CSRC = os.path.join(os.path.dirname(os.path.abspath(__file__)), "csrc")
+_HEADERS = {
+    "stridesim_b200.h": native.HEADER,
+    "ss_device.cuh": os.path.join(_CSRC, "ss_device.cuh"),
+    "ss_cfg.cuh": os.path.join(_CSRC, "ss_cfg.cuh"),
+    "ss_kernel.cuh": os.path.join(_CSRC, "ss_kernel.cuh"),
+}
+OPTIONS = ["--gpu-architecture=sm_100a", "--fmad=false", "-std=c++17", "-lineinfo", "-DSS_JIT=1"]
+KERNEL = "ss_step_jit"
+
+
+class JitUnsupported(RuntimeError):
+    pass
+
+
+def enabled() -> bool:
+    return os.environ.get("SS_JIT", "1") != "0"
+
+
+def _parse_lists():
+    text = open(_HEADERS["ss_cfg.cuh"]).read()
+    out = {}
+    for macro, arity in (("SS_CFG_SCALARS", 3), ("SS_CFG_ARRAYS", 4), ("SS_CFG_ARRAYS2", 5)):
+        body = text.split(f"#define {macro}(")[1].split("\n\n")[0]
+        items = []
+        for m in re.finditer(r"X[AB]?\(([^()]*(?:\([^()]*\)[^()]*)*)\)", body):
+            parts = [p.strip() for p in m.group(1).split(",")]
+            if len(parts) != arity:
+                continue
+            items.append(parts)
+        out[macro] = items
+    return out
+
+
+_LISTS = _parse_lists()
+
+
+def _bound(name: str) -> int:
+    return int(name) if name.isdigit() else getattr(native, name)
+
+
+def _lit(typ: str, v) -> str:
+    if typ == "double":
+        v = float(v)
+        if not math.isfinite(v):
+            raise JitUnsupported(f"non-finite constant {v}")
+        return v.hex()
+    if typ == "unsigned":
+        return f"{int(v) & 0xFFFFFFFF}u"
+    return str(int(v))
+
+
+def config_source(d) -> str:
+    """C++ source of the constexpr config struct for descriptor ``d``."""
+    lines = ["struct JitCfg {", "  static constexpr bool kJit = true;", "  static constexpr int kUnroll = 64;"]
+    head = "  static __device__ __forceinline__"
+    for typ, name, expr in _LISTS["SS_CFG_SCALARS"]:
+        val = eval(expr, {"d": d})  # noqa: S307 -- expressions come from ss_cfg.cuh
+        lines.append(f"{head} {typ} {name}(const ss_env_desc&) {{ return {_lit(typ, val)}; }}")
+    for typ, name, bound, expr in _LISTS["SS_CFG_ARRAYS"]:
+        n = _bound(bound)
+        vals = [_lit(typ, eval(expr, {"d": d, "i": i})) for i in range(n)]  # noqa: S307
+        lines.append(f"{head} {typ} {name}(const ss_env_desc&, int i) {{ constexpr {typ} a[{n}] = {{"
+                     f"{', '.join(vals)}}}; return a[i]; }}")
+    for typ, name, bt, bi, expr in _LISTS["SS_CFG_ARRAYS2"]:
+        nt, ni = _bound(bt), _bound(bi)
+        rows = []
+        for t in range(nt):
+            rows.append("{" + ", ".join(_lit(typ, eval(expr, {"d": d, "t": t, "i": i})) for i in range(ni)) + "}")  # noqa: S307
+        lines.append(f"{head} {typ} {name}(const ss_env_desc&, int t, int i) {{ constexpr {typ} a[{nt}][{ni}] = {{"
+                     f"{', '.join(rows)}}}; return a[t][i]; }}")
+    lines.append("};")
+    return "\n".join(lines)
+
+
+def kernel_source(d) -> str:
+    k, f = int(d.model.n_joints), int(d.model.n_feet)
+    return "\n".join([
+        '#include "stridesim_b200.h"',
+        '#include "ss_kernel.cuh"',
+        config_source(d),
+        f"extern \"C\" __global__ void __launch_bounds__(ss::kBlock) {KERNEL}(",
+        "    const __grid_constant__ ss_env_desc d, const __grid_constant__ ss_uniforms u) {",
+        f"  ss::step_body<JitCfg, {max(k, 1)}, {max(f, 1)}>(d, u);",
+        "}",
+    ]) + "\n"
+
+
+def _headers():
+    names, srcs = [], []
+    for name, path in _HEADERS.items():
+        names.append(name.encode())
+        srcs.append(open(path, "rb").read())
+    return names, srcs
+
+
+def compile_cubin(src: str) -> bytes:
+    """NVRTC: source -> sm_100a cubin (no GPU needed)."""
+    names, srcs = _headers()
+    c_names = (ctypes.c_char_p * len(names))(*names)
+    c_srcs = (ctypes.c_char_p * len(srcs))(*srcs)
+    opts = [o.encode() for o in OPTIONS]
+    c_opts = (ctypes.c_char_p * len(opts))(*opts)
+    size = ctypes.c_size_t(0)
+    log = ctypes.create_string_buffer(1 << 16)
+    so = native.lib()
+    rc = so.ss_jit_compile(src.encode(), len(names), c_srcs, c_names, len(opts), c_opts, None, ctypes.byref(size),
+                           log, len(log))
+    if rc != 0:
+        raise native.NativeError(f"NVRTC failed: {so.ss_last_error().decode()}\n{log.value.decode()[:4000]}")
+    buf = ctypes.create_string_buffer(size.value)
+    rc = so.ss_jit_compile(src.encode(), len(names), c_srcs, c_names, len(opts), c_opts, buf, ctypes.byref(size),
+                           log, len(log))
+    if rc != 0:
+        raise native.NativeError(f"NVRTC failed: {so.ss_last_error().decode()}")
+    return buf.raw[: size.value]
+
+
+def _cache_dir() -> str:
+    base = os.environ.get("XDG_CACHE_HOME", os.path.join(os.path.expanduser("~"), ".cache"))
+    return os.path.join(base, "paper_2601_22074_b200", "jit")
+
+
+_MODULES: dict[str, int] = {}
+STATS = {"compiled": 0, "disk_hits": 0, "memory_hits": 0}
+
+
+def module_for(d) -> int:
+    """Loaded kernel handle specialized for descriptor ``d`` (compiled on first use)."""
+    src = kernel_source(d)
+    key = hashlib.sha256((src + "|".join(OPTIONS) + "".join(open(p).read() for p in _HEADERS.values())).encode()).hexdigest()
+    h = _MODULES.get(key)
+    if h is not None:
+        STATS["memory_hits"] += 1
+        return h
+    path = os.path.join(_cache_dir(), key + ".cubin")
+    cubin = None
+    try:
+        with open(path, "rb") as fh:
+            cubin = fh.read()
+        STATS["disk_hits"] += 1
+    except OSError:
+        pass
+    if cubin is None:
+        cubin = compile_cubin(src)
+        STATS["compiled"] += 1
+        try:
+            os.makedirs(os.path.dirname(path), exist_ok=True)
+            with open(path + ".tmp", "wb") as fh:
+                fh.write(cubin)
+            os.replace(path + ".tmp", path)
+        except OSError:
+            pass
+    handle = ctypes.c_void_p()
+    native.call("ss_jit_load", cubin, len(cubin), KERNEL.encode(), ctypes.byref(handle))
+    _MODULES[key] = handle.value
+    return handle.value

@@ -105,6 +105,14 @@ _SIGNATURES = {
          ctypes.c_int32, ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p],
         ctypes.c_int,
     ),
+    "ss_jit_compile": (
+        [ctypes.c_char_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p,
+         ctypes.c_void_p, ctypes.POINTER(ctypes.c_size_t), ctypes.c_char_p, ctypes.c_size_t],
+        ctypes.c_int,
+    ),
+    "ss_jit_load": ([ctypes.c_void_p, ctypes.c_size_t, ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
+    "ss_jit_unload": ([ctypes.c_void_p], ctypes.c_int),
+    "ss_env_step_jit": ([ctypes.c_void_p] * 4, ctypes.c_int),
     "ss_actuator_eval": (
         [ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double, ctypes.c_double, ctypes.c_double,
          ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p],

@@ -663,3 +663,29 @@ def test_dc_motor_envelope_on_device(rng):
                           torch.as_tensor(q_des, device="cuda"), 0.0, torch.as_tensor(q, device="cuda"),
                           torch.as_tensor(qd, device="cuda"))
     assert np.array_equal(host, _np(dev))
+
+
+@pytest.mark.parametrize("task", ["Velocity-Rough", "Velocity-Flat"])
+def test_jit_specialization_bitwise_equals_generic_kernel(task):
+    """The per-env NVRTC specialization and the generic AOT kernel run the same
+    source; they must agree bit for bit (no reassociation, --fmad=false)."""
+    from paper_2601_22074_b200 import jit
+    from paper_2601_22074_b200.env import ManagerBasedRlEnv
+    from paper_2601_22074_b200.policies import random_policy
+    from paper_2601_22074_b200.tasks import make_env_cfg
+
+    a = ManagerBasedRlEnv(make_env_cfg(task, num_envs=300, seed=4))
+    b = ManagerBasedRlEnv(make_env_cfg(task, num_envs=300, seed=4))
+    assert a.use_jit
+    b.use_jit = False
+    oa, ob = a.reset(), b.reset()
+    for i in range(40):
+        act = random_policy(a, i)
+        random_policy(b, i)
+        oa, ra, ta, _, _ = a.step(act)
+        ob, rb, tb, _, _ = b.step(act)
+        for k in oa:
+            assert torch.equal(oa[k], ob[k]), (i, k)
+        assert torch.equal(ra, rb) and torch.equal(ta, tb)
+        assert torch.equal(a.state.q, b.state.q)
+    assert jit.STATS["compiled"] + jit.STATS["disk_hits"] + jit.STATS["memory_hits"] > 0
