@@ -256,14 +256,18 @@ def run_ours(args):
     torch.cuda.synchronize()
     launches0 = native.LAUNCHES["count"]
     for i in range(args.steps):
-        flush.fill_(float(i))  # evict L2 (126 MB) between timed iterations
-        torch.cuda._sleep(400000)  # ~0.2 ms: let the host run ahead so events time the GPU, not Python
+        flush.fill_(float(i))  # evict L2 (126 MB) between timed iterations (untimed)
         e0, e1, e2 = evs[i]
         e0.record(stream)
         a = random_policy(env, args.warmup + i)
         e1.record(stream)
         env.step(a)
         e2.record(stream)
+        if i >= 2:
+            # bound the host's lead to two iterations: the flush of the next
+            # iteration gives the host time to enqueue the step before the GPU
+            # reaches e0, so the events time GPU work only
+            evs[i - 2][2].synchronize()
     torch.cuda.synchronize()
     barrier(world)
     launches = native.LAUNCHES["count"] - launches0

@@ -27,6 +27,7 @@
  *   ss_heights       Heightfield.heights                terrain.py:159-169
  *   ss_randomize     randomize_field (startup/explicit) managers/event.py:19-52
  *   ss_actuator_eval pd_torque / dc_motor_torque        actuators.py:104-117
+ *   ss_rt_*          ManagerBasedRlEnv.step bookkeeping (env.py:219-259)
  *   ss_jit_*         StepPipeline._rebuild (re-specialize to the layout) sim/physics.py:158-237
  *
  * Layout: every per-world array is structure-of-arrays, component-major,
@@ -473,6 +474,56 @@ typedef struct ss_uniforms {
     const uint8_t* reset_mask;
 } ss_uniforms;
 
+/* Host-side runtime state of one env: every per-launch uniform (step
+ * counters, ring heads, reward weights) is derived and advanced here by
+ * ss_rt_launch, so a control step costs the host one C call. The struct is
+ * shared memory between Python (ctypes) and C: Python reads the counters
+ * directly, C advances them. */
+#define SS_RT_SLOTS 8
+typedef struct ss_rt_state {
+    int64_t global_step;
+    int64_t sim_step;
+    int64_t cap_pushes;
+    int64_t* cap_sim_steps;
+    int32_t cap_count;
+    int32_t cap_capacity;
+    int32_t cap_phys;
+    int32_t n_act;
+    int64_t sensor_last_update;
+    int32_t act_head[SS_MAX_ACTUATORS];
+    int32_t act_cap[SS_MAX_ACTUATORS];
+    int32_t n_obs;
+    int32_t n_groups;
+    int32_t obs_group[SS_MAX_OBS_TERMS];
+    int32_t obs_delay_head[SS_MAX_OBS_TERMS];
+    int32_t obs_delay_len[SS_MAX_OBS_TERMS];
+    int32_t obs_hist_head[SS_MAX_OBS_TERMS];
+    int32_t obs_hist_len[SS_MAX_OBS_TERMS];
+    int32_t any_pending;
+    int32_t n_rewards;
+    double weight[SS_MAX_REWARDS];
+    uint32_t* nf_flags;
+    int32_t nf_slots;
+    int32_t nf_slot;
+    int32_t nf_head;
+    int32_t nf_pending;
+    int64_t nf_pushes[SS_RT_SLOTS];
+    int64_t nf_sim_step[SS_RT_SLOTS];
+    int32_t nf_count[SS_RT_SLOTS];
+    uint64_t nf_event[SS_RT_SLOTS];
+    int64_t launches;
+} ss_rt_state;
+
+/* One launch request for ss_rt_launch. */
+typedef struct ss_launch {
+    uint32_t stages;
+    int32_t nsub;
+    uint32_t flags;
+    uint32_t groups_mask;
+    const double* actions;
+    const uint8_t* reset_mask;
+} ss_launch;
+
 /* One draw call of StreamPack.uniform/normal (rng.py:69-119). sel == NULL
  * means all N streams; otherwise n_sel world indices (int64). lo/hi are
  * broadcast per `lohi_mode`: 0 scalar, 1 per selected row (n_sel), 2 per
@@ -495,7 +546,7 @@ typedef struct ss_rng_draw_args {
 
 #ifndef __CUDACC_RTC__ /* host entry points (not part of the JIT translation unit) */
 int ss_abi_version(void);
-size_t ss_sizeof(int which); /* 0 env_desc, 1 uniforms, 2 rng_draw_args */
+size_t ss_sizeof(int which); /* 0 env_desc, 1 uniforms, 2 rng_draw_args, 3 rt_state, 4 launch */
 const char* ss_last_error(void);
 
 int ss_env_step(const ss_env_desc* desc, const ss_uniforms* u, void* stream);
@@ -510,12 +561,20 @@ int ss_randomize(const ss_env_desc* desc, int32_t field, int32_t distribution,
 /* Per-env specialization: NVRTC-compile the step body with the env's term
  * tables as compile-time constants (csrc/ss_cfg.cuh), load it, launch it.
  * Same semantics and results as ss_env_step. */
-int ss_jit_compile(const char* src, int n_headers, const char* const* header_src,
+int ss_jit_compile(const char* src, const char* name, int n_headers, const char* const* header_src,
                    const char* const* header_names, int n_opts, const char* const* opts,
                    void* out, size_t* size, char* log, size_t log_size);
 int ss_jit_load(const void* cubin, size_t size, const char* kernel_name, void** handle);
 int ss_jit_unload(void* handle);
 int ss_env_step_jit(void* handle, const ss_env_desc* desc, const ss_uniforms* u, void* stream);
+/* Runtime: derive the uniforms from *st, launch (JIT module when jit != NULL,
+ * else the generic kernel), advance *st. ss_rt_poll retires completed TERM
+ * launches (blocking on the oldest while more than `keep` are pending) and
+ * returns the slots whose nonfinite flag was raised; ss_rt_release frees the
+ * runtime's CUDA events. */
+int ss_rt_launch(const ss_env_desc* desc, ss_rt_state* st, const ss_launch* l, void* jit, void* stream);
+int ss_rt_poll(ss_rt_state* st, int32_t keep, int32_t* out_slots, int32_t max_out);
+int ss_rt_release(ss_rt_state* st);
 int ss_actuator_eval(int32_t kind, const double* kp, const double* kd, double effort,
                      double saturation, double vel_limit, const double* q_des,
                      const double* q, const double* qd, double* out, int64_t n,

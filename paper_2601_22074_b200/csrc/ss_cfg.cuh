@@ -149,6 +149,9 @@ namespace ss {
 struct RuntimeCfg {
     static constexpr bool kJit = false;
     static constexpr int kUnroll = 1;  // term-table loops stay loops in the generic build
+    static constexpr int kCapAct = SS_MAX_ACTUATORS, kCapActTerms = SS_MAX_ACTION_TERMS;
+    static constexpr int kCapTerms = SS_MAX_TERMINATIONS, kCapRewards = SS_MAX_REWARDS;
+    static constexpr int kCapEvents = SS_MAX_EVENTS, kCapGroups = SS_MAX_GROUPS, kCapObs = SS_MAX_OBS_TERMS;
 #define SS_RT_X(T, name, expr) \
     static __device__ __forceinline__ T name(const ss_env_desc& d) { return (T)(expr); }
 #define SS_RT_XA(T, name, bound, expr) \

@@ -48,6 +48,38 @@ __device__ __forceinline__ void sel_store(double (&a)[M], int j, double v) {
         if (i == j) a[i] = v;
 }
 
+// Term-table loops. In the per-env JIT build the trip counts are constants
+// and static_for instantiates the body once per term with the index as a
+// compile-time constant (Ic<I>), so every table lookup folds to an
+// immediate; the generic build runs an ordinary loop.
+template <int V>
+struct Ic {
+    static constexpr int value = V;
+};
+__device__ __forceinline__ constexpr int ival(int t) { return t; }
+template <int V>
+__device__ __forceinline__ constexpr int ival(Ic<V>) { return V; }
+
+template <int I, int N, class F>
+__device__ __forceinline__ void static_for(F& f) {
+    if constexpr (I < N) {
+        f(Ic<I>{});
+        static_for<I + 1, N>(f);
+    }
+}
+
+template <class C, int MAX, class F>
+__device__ __forceinline__ void for_terms(int lo, int hi, F f) {
+    if constexpr (C::kJit) {
+        auto g = [&](auto I) {
+            if (ival(I) >= lo && ival(I) < hi) f(I);
+        };
+        static_for<0, MAX>(g);
+    } else {
+        for (int t = lo; t < hi; ++t) f(t);
+    }
+}
+
 template <class C>
 __device__ __forceinline__ double fld(const ss_env_desc& d, int f, int c, int w) {
     const double* p = d.field[f].ptr;
@@ -105,6 +137,20 @@ struct World {
     double cmd_dist;
     bool terminated, truncated, nonfinite, was_reset;
     unsigned trig_bits;
+    // per-step state prefetched at kernel entry (one round trip, see step_body)
+    double ep_sum[SS_MAX_REWARDS], ep_rw[SS_MAX_REWARDS];
+    long long countdown;
+    double ev_el[SS_MAX_EVENTS], ev_tg[SS_MAX_EVENTS];
+    uint64_t nctr[SS_MAX_OBS_TERMS];
+    double plv0, plv1;
+};
+
+// model fields hoisted out of the substep loop (they cannot change within a launch)
+template <int KM>
+struct Params {
+    double base_mass, base_inertia, friction;
+    double lm[KM], rot[KM], dmp[KM];
+    double kp[SS_MAX_ACTUATORS][KM], kd[SS_MAX_ACTUATORS][KM];
 };
 
 __device__ __forceinline__ uint64_t rng_begin(const ss_env_desc& d, int slot, int w, uint64_t& key) {
@@ -206,19 +252,41 @@ __device__ __forceinline__ void refresh(World<KM, FM>& s) {
 // ---------------------------------------------------------------------------
 // StepPipeline.substep (sim/physics.py:178-249)
 
-template <class C, int KM, int FM>
-__device__ __forceinline__ void phys_substep(const ss_env_desc& d, int w, World<KM, FM>& s) {
-    const int K = C::K(d), F = C::F(d);
-    const double base_mass = fld<C>(d, C::f_base_mass(d), 0, w);
-    const double base_inertia = fld<C>(d, C::f_base_inertia(d), 0, w);
-    const double friction = fld<C>(d, C::f_friction(d), 0, w);
-    double lm[KM], rot[KM], dmp[KM];
+template <class C, int KM>
+__device__ __forceinline__ void load_params(const ss_env_desc& d, int w, Params<KM>& P, bool actuators) {
+    const int K = C::K(d);
+    P.base_mass = fld<C>(d, C::f_base_mass(d), 0, w);
+    P.base_inertia = fld<C>(d, C::f_base_inertia(d), 0, w);
+    P.friction = fld<C>(d, C::f_friction(d), 0, w);
 #pragma unroll
     for (int j = 0; j < KM; ++j) {
-        lm[j] = (j < K) ? fld<C>(d, C::f_link_mass(d), j, w) : 0.0;
-        rot[j] = (j < K) ? fld<C>(d, C::f_rotor(d), j, w) : 1.0;
-        dmp[j] = (j < K) ? fld<C>(d, C::f_damping(d), j, w) : 0.0;
+        P.lm[j] = (j < K) ? fld<C>(d, C::f_link_mass(d), j, w) : 0.0;
+        P.rot[j] = (j < K) ? fld<C>(d, C::f_rotor(d), j, w) : 1.0;
+        P.dmp[j] = (j < K) ? fld<C>(d, C::f_damping(d), j, w) : 0.0;
     }
+    if (actuators) {
+        for_terms<C, C::kCapAct>(0, C::n_act(d), [&](auto aa) {
+            const int a = ival(aa);
+            if (C::act_kind(d, a) != SS_ACT_MLP) {
+#pragma unroll
+                for (int i = 0; i < KM; ++i) {
+                    if (i < C::act_dim(d, a)) {
+                        P.kp[a][i] = fld<C>(d, C::act_f_kp(d, a), i, w);
+                        P.kd[a][i] = fld<C>(d, C::act_f_kd(d, a), i, w);
+                    }
+                }
+            }
+        });
+    }
+}
+
+template <class C, int KM, int FM>
+__device__ __forceinline__ void phys_substep(const ss_env_desc& d, int w, World<KM, FM>& s, const Params<KM>& P) {
+    const int K = C::K(d), F = C::F(d);
+    const double base_mass = P.base_mass, base_inertia = P.base_inertia, friction = P.friction;
+    const double(&lm)[KM] = P.lm;
+    const double(&rot)[KM] = P.rot;
+    const double(&dmp)[KM] = P.dmp;
 
     // forward kinematics (fk_batch_trig, sim/physics.py:22-57)
     double sp, cp;
@@ -416,11 +484,10 @@ __device__ __noinline__ double mlp_torque(const ss_env_desc& d, int a, int i, in
 
 template <class C, int KM, int FM>
 __device__ __forceinline__ void apply_actuators(const ss_env_desc& d, const ss_uniforms& u, int w, int sub,
-                                                World<KM, FM>& s) {
+                                                World<KM, FM>& s, const Params<KM>& P) {
     const int N = d.n_worlds;
-#pragma unroll(C::kUnroll)
-    for (int a = 0; a < SS_MAX_ACTUATORS; ++a) {
-        if (a >= C::n_act(d)) break;
+    for_terms<C, C::kCapAct>(0, C::n_act(d), [&](auto aa) {
+        const int a = ival(aa);
         long long delay = 0;
         int head = 0;
         const int cap = C::act_cap(d, a);
@@ -449,8 +516,7 @@ __device__ __forceinline__ void apply_actuators(const ss_env_desc& d, const ss_u
             if (kind == SS_ACT_MLP) {
                 tau = mlp_torque<KM, FM>(d, a, i, w, qdes, qj, qdj);
             } else {
-                const double kp = fld<C>(d, C::act_f_kp(d, a), i, w);
-                const double kd = fld<C>(d, C::act_f_kd(d, a), i, w);
+                const double kp = P.kp[a][i], kd = P.kd[a][i];
                 tau = kp * (qdes - qj) + kd * (0.0 - qdj);
                 if (kind == SS_ACT_PD) {
                     tau = np_clip(tau, -eff, eff);
@@ -464,7 +530,7 @@ __device__ __forceinline__ void apply_actuators(const ss_env_desc& d, const ss_u
             }
             sel_store(s.ctrl, j, tau);
         }
-    }
+    });
 }
 
 // Actuator.reset (actuators.py:269-277) for one world
@@ -608,8 +674,8 @@ __device__ __forceinline__ void obs_raw(const ss_env_desc& d, int t, int w, cons
             v[0] = s.eqd[2];
             break;
         case SS_OBS_BASE_LIN_ACC:
-            v[0] = (s.lvb0 - d.prev_lin_vel_b[w]) / C::dt_control(d);
-            v[1] = (s.lvb1 - d.prev_lin_vel_b[N + w]) / C::dt_control(d);
+            v[0] = (s.lvb0 - s.plv0) / C::dt_control(d);
+            v[1] = (s.lvb1 - s.plv1) / C::dt_control(d);
             break;
         case SS_OBS_PROJECTED_GRAVITY:
             v[0] = s.pg0;
@@ -663,48 +729,42 @@ __device__ __forceinline__ void obs_raw(const ss_env_desc& d, int t, int w, cons
     }
 }
 
-// ObservationManager.compute for one group, one world (managers/observation.py:99-137)
+// ObservationManager.compute, one term of one world (managers/observation.py:99-137)
 template <class C, int KM, int FM>
-__device__ __forceinline__ void compute_group(const ss_env_desc& d, const ss_uniforms& u, int g, int w,
-                                              const World<KM, FM>& s, bool pending, unsigned& bad_bits) {
+__device__ __forceinline__ void obs_term(const ss_env_desc& d, const ss_uniforms& u, int t, int w,
+                                         World<KM, FM>& s, bool pending, double* out, unsigned& bad_bits) {
     const int N = d.n_worlds;
-    double* out = d.group[g].out + (int64_t)w * C::g_dim(d, g);
-    const int first = C::g_first(d, g), last = first + C::g_n(d, g);
-#pragma unroll(C::kUnroll)
-    for (int t = first; t < last; ++t) {
-        double v[kObsMax];
-        obs_raw<C>(d, t, w, s, v);
-        const int dim = C::obs_dim(d, t);
-        const int col = C::obs_col(d, t);
-        bool bad = false;
+    double v[kObsMax];
+    obs_raw<C>(d, t, w, s, v);
+    const int dim = C::obs_dim(d, t);
+    const int col = C::obs_col(d, t);
+    bool bad = false;
+#pragma unroll
+    for (int k = 0; k < kObsMax; ++k)
+        if (k < dim) bad |= !finite_(v[k]);
+    if (bad) bad_bits |= 1u << t;
+    if (C::obs_has_clip(d, t)) {
 #pragma unroll
         for (int k = 0; k < kObsMax; ++k)
-            if (k < dim) bad |= !finite_(v[k]);
-        if (bad) bad_bits |= 1u << t;
-        if (C::obs_has_clip(d, t)) {
+            if (k < dim) v[k] = np_clip(v[k], C::obs_clip_lo(d, t), C::obs_clip_hi(d, t));
+    }
+    if (C::obs_has_scale(d, t)) {
 #pragma unroll
-            for (int k = 0; k < kObsMax; ++k)
-                if (k < dim) v[k] = np_clip(v[k], C::obs_clip_lo(d, t), C::obs_clip_hi(d, t));
-        }
-        if (C::obs_has_scale(d, t)) {
-#pragma unroll
-            for (int k = 0; k < kObsMax; ++k)
-                if (k < dim) v[k] = v[k] * C::obs_scale(d, t);
-        }
-        const int noise = C::obs_noise(d, t);
+        for (int k = 0; k < kObsMax; ++k)
+            if (k < dim) v[k] = v[k] * C::obs_scale(d, t);
+    }
+    const int noise = C::obs_noise(d, t);
+    if (noise != SS_NOISE_NONE) {
+        const int slot = C::obs_noise_slot(d, t);
+        const uint64_t key = stream_key(d.rng.base[slot], (uint64_t)(d.rng.world_id_offset + w));
+        const uint64_t c = s.nctr[t];  // prefetched at kernel entry
         if (noise == SS_NOISE_UNIFORM) {
-            uint64_t key;
-            const int slot = C::obs_noise_slot(d, t);
-            const uint64_t c = rng_begin(d, slot, w, key);
             const double hi = C::obs_noise_scale(d, t), lo = -hi;
 #pragma unroll
             for (int k = 0; k < kObsMax; ++k)
                 if (k < dim) v[k] = v[k] + uniform_from_word(stream_word(key, c, k), lo, hi);
             rng_end(d, slot, w, c + (uint64_t)dim);
-        } else if (noise == SS_NOISE_GAUSSIAN) {
-            uint64_t key;
-            const int slot = C::obs_noise_slot(d, t);
-            const uint64_t c = rng_begin(d, slot, w, key);
+        } else {
 #pragma unroll
             for (int k = 0; k < kObsMax; ++k)
                 if (k < dim)
@@ -712,62 +772,62 @@ __device__ __forceinline__ void compute_group(const ss_env_desc& d, const ss_uni
                                                     C::obs_noise_scale(d, t));
             rng_end(d, slot, w, c + (uint64_t)(2 * dim));
         }
-        const int D = C::obs_delay(d, t), H = C::obs_history(d, t);
-        if (D == 0 && H == 1) {
+    }
+    const int D = C::obs_delay(d, t), H = C::obs_history(d, t);
+    if (D == 0 && H == 1) {
 #pragma unroll
-            for (int k = 0; k < kObsMax; ++k)
-                if (k < dim) out[col + k] = v[k];
-            continue;
-        }
-        // delay ring: push, then read D pushes back (flood on reset)
-        if (D > 0) {
-            double* ring = d.obs[t].delay_ring;
-            const int D1 = D + 1;
-            const int head = u.obs_delay_head[t];
-            if (pending) {
-                for (int h = 0; h < D1; ++h)
-#pragma unroll
-                    for (int k = 0; k < kObsMax; ++k)
-                        if (k < dim) ring[((int64_t)h * dim + k) * N + w] = v[k];
-            } else {
-#pragma unroll
-                for (int k = 0; k < kObsMax; ++k)
-                    if (k < dim) ring[((int64_t)head * dim + k) * N + w] = v[k];
-                int slot = (head - D) % D1;
-                if (slot < 0) slot += D1;
-#pragma unroll
-                for (int k = 0; k < kObsMax; ++k)
-                    if (k < dim) v[k] = ring[((int64_t)slot * dim + k) * N + w];
-            }
-        }
-        // history ring, oldest-first output (newest at the host-tracked head)
-        if (H == 1) {
-#pragma unroll
-            for (int k = 0; k < kObsMax; ++k)
-                if (k < dim) out[col + k] = v[k];
-            continue;
-        }
-        double* hr = d.obs[t].hist_ring;
-        const int hh = u.obs_hist_head[t];
+        for (int k = 0; k < kObsMax; ++k)
+            if (k < dim) out[col + k] = v[k];
+        return;
+    }
+    // delay ring: push, then read D pushes back (flood on reset)
+    if (D > 0) {
+        double* ring = d.obs[t].delay_ring;
+        const int D1 = D + 1;
+        const int head = u.obs_delay_head[t];
         if (pending) {
-            for (int h = 0; h < H; ++h)
+            for (int h = 0; h < D1; ++h)
 #pragma unroll
                 for (int k = 0; k < kObsMax; ++k)
-                    if (k < dim) {
-                        hr[((int64_t)h * dim + k) * N + w] = v[k];
-                        out[col + h * dim + k] = v[k];
-                    }
+                    if (k < dim) ring[((int64_t)h * dim + k) * N + w] = v[k];
         } else {
 #pragma unroll
             for (int k = 0; k < kObsMax; ++k)
-                if (k < dim) hr[((int64_t)hh * dim + k) * N + w] = v[k];
-            for (int h = 0; h < H; ++h) {
-                const int slot = (hh + 1 + h) % H;
+                if (k < dim) ring[((int64_t)head * dim + k) * N + w] = v[k];
+            int slot = (head - D) % D1;
+            if (slot < 0) slot += D1;
 #pragma unroll
-                for (int k = 0; k < kObsMax; ++k)
-                    if (k < dim)
-                        out[col + h * dim + k] = (slot == hh) ? v[k] : hr[((int64_t)slot * dim + k) * N + w];
-            }
+            for (int k = 0; k < kObsMax; ++k)
+                if (k < dim) v[k] = ring[((int64_t)slot * dim + k) * N + w];
+        }
+    }
+    // history ring, oldest-first output (newest at the host-tracked head)
+    if (H == 1) {
+#pragma unroll
+        for (int k = 0; k < kObsMax; ++k)
+            if (k < dim) out[col + k] = v[k];
+        return;
+    }
+    double* hr = d.obs[t].hist_ring;
+    const int hh = u.obs_hist_head[t];
+    if (pending) {
+        for (int h = 0; h < H; ++h)
+#pragma unroll
+            for (int k = 0; k < kObsMax; ++k)
+                if (k < dim) {
+                    hr[((int64_t)h * dim + k) * N + w] = v[k];
+                    out[col + h * dim + k] = v[k];
+                }
+    } else {
+#pragma unroll
+        for (int k = 0; k < kObsMax; ++k)
+            if (k < dim) hr[((int64_t)hh * dim + k) * N + w] = v[k];
+        for (int h = 0; h < H; ++h) {
+            const int slot = (hh + 1 + h) % H;
+#pragma unroll
+            for (int k = 0; k < kObsMax; ++k)
+                if (k < dim)
+                    out[col + h * dim + k] = (slot == hh) ? v[k] : hr[((int64_t)slot * dim + k) * N + w];
         }
     }
 }
@@ -857,17 +917,51 @@ __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniform
     if (active) {
         const bool sim = (st & (SS_ST_APPLY | SS_ST_PUSH | SS_ST_PHYS | SS_ST_SENSOR)) && u.nsub > 0;
         const bool phys = (st & SS_ST_PHYS) && u.nsub > 0;
-        load_phys<C>(d, w, s, /*load_cache=*/!phys);
-        if (!phys) refresh(s);  // staged launch: entity data from the stored state
+        const bool resets = st & (SS_ST_RESET | SS_ST_RESET_ALL);
 
+        // ---- prefetch: every per-step array this launch will read, issued up
+        // front so their DRAM latency overlaps (the stores that follow would
+        // otherwise pin each load behind them: the pointers may alias)
+        load_phys<C>(d, w, s, /*load_cache=*/!phys);
 #pragma unroll
         for (int c = 0; c < SS_MAX_CMD; ++c) s.cmd[c] = (c < C::n_cmd(d)) ? d.command[(int64_t)c * N + w] : 0.0;
-        s.have_action = false;
-        s.have_sensor = false;
-
         const bool need_targets = st & (SS_ST_ACTION | SS_ST_APPLY | SS_ST_RESET | SS_ST_RESET_ALL);
 #pragma unroll
         for (int j = 0; j < KM; ++j) s.targets[j] = (need_targets && j < K) ? d.targets[(int64_t)j * N + w] : 0.0;
+        s.have_action = false;
+        s.have_sensor = false;
+        if (st & (SS_ST_TERM | SS_ST_CURRICULUM)) {
+            s.ep_steps = d.episode_steps[w];
+            s.cmd_dist = d.commanded_distance[w];
+        }
+        if (st & (SS_ST_REWARD | SS_ST_CURRICULUM | SS_ST_RESET | SS_ST_RESET_ALL)) {
+            for_terms<C, C::kCapRewards>(0, C::n_rewards(d), [&](auto rr) {
+                const int r = ival(rr);
+                s.ep_sum[r] = d.ep_sums[(int64_t)r * N + w];
+                s.ep_rw[r] = d.ep_raw[(int64_t)r * N + w];
+            });
+        }
+        if ((st & SS_ST_COMMAND) && C::n_cmd(d) > 0) s.countdown = d.countdown[w];
+        if (st & SS_ST_EVENTS) {
+            for_terms<C, C::kCapEvents>(0, C::n_events(d), [&](auto ee) {
+                const int e = ival(ee);
+                if (C::ev_mode(d, e) == SS_MODE_INTERVAL) {
+                    s.ev_el[e] = d.event[e].elapsed[w];
+                    s.ev_tg[e] = d.event[e].target[w];
+                }
+            });
+        }
+        if (st & SS_ST_OBS) {
+            for_terms<C, C::kCapObs>(0, C::n_obs(d), [&](auto tt) {
+                const int t = ival(tt);
+                if (C::obs_noise(d, t) != SS_NOISE_NONE) s.nctr[t] = d.rng.counter[C::obs_noise_slot(d, t)][w];
+            });
+            s.plv0 = d.prev_lin_vel_b[w];
+            s.plv1 = d.prev_lin_vel_b[N + w];
+        }
+        Params<KM> P;
+        if (sim && (st & (SS_ST_PHYS | SS_ST_APPLY))) load_params<C>(d, w, P, st & SS_ST_APPLY);
+        if (!phys) refresh(s);  // staged launch: entity data from the stored state
 
         // ---- 1. ActionManager.process (managers/action.py:68-82)
         if (st & SS_ST_ACTION) {
@@ -877,13 +971,17 @@ __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniform
                 if (k < A) {
                     s.prev_action[k] = d.action[(int64_t)k * N + w];
                     s.action[k] = a[k];
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < SS_MAX_ACTION; ++k) {
+                if (k < A) {
                     d.prev_action[(int64_t)k * N + w] = s.prev_action[k];
                     d.action[(int64_t)k * N + w] = s.action[k];
                 }
             }
-#pragma unroll(C::kUnroll)
-            for (int t = 0; t < SS_MAX_ACTION_TERMS; ++t) {
-                if (t >= C::n_action_terms(d)) break;
+            for_terms<C, C::kCapActTerms>(0, C::n_action_terms(d), [&](auto tt) {
+                const int t = ival(tt);
 #pragma unroll
                 for (int i = 0; i < KM; ++i) {
                     if (i >= C::at_dim(d, t)) break;
@@ -891,7 +989,7 @@ __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniform
                     if (C::at_has_clip(d, t)) x = np_clip(x, C::at_clip_lo(d, t), C::at_clip_hi(d, t));
                     sel_store(s.targets, C::at_joint(d, t, i), C::at_offset(d, t, i) + C::at_scale(d, t) * x);
                 }
-            }
+            });
 #pragma unroll
             for (int j = 0; j < KM; ++j)
                 if (j < K) d.targets[(int64_t)j * N + w] = s.targets[j];
@@ -925,7 +1023,7 @@ __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniform
             const int nsub = u.nsub;
 #pragma unroll 1
             for (int sub = 0; sub < nsub; ++sub) {
-                if (st & SS_ST_APPLY) apply_actuators<C>(d, u, w, sub, s);
+                if (st & SS_ST_APPLY) apply_actuators<C>(d, u, w, sub, s, P);
                 if (st & SS_ST_PUSH) {
                     // CaptureRing.push (capture.py:53-59): ctrl written, pre-integration
                     const int slot = (u.capture_slot0 + sub) % d.capture_phys;
@@ -942,7 +1040,7 @@ __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniform
                         if (j < K) d.cap_ctrl[((int64_t)slot * K + j) * N + w] = s.ctrl[j];
                 }
                 if (phys) {
-                    phys_substep<C>(d, w, s);
+                    phys_substep<C>(d, w, s, P);
                     refresh(s);
                 }
                 if (sensor && ((u.sensor_mask >> sub) & 1u)) {
@@ -993,21 +1091,16 @@ __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniform
         const long long sim_step_now = u.sim_step + (phys ? u.nsub : 0);
 
         // ---- 3. episode bookkeeping + TerminationManager.compute (env.py:235-239)
-        bool have_ep = false;
         if (st & SS_ST_TERM) {
-            s.ep_steps = d.episode_steps[w];
-            s.cmd_dist = d.commanded_distance[w];
             if (!(u.flags & SS_FLAG_NO_EPISODE)) {
                 s.ep_steps += 1;
                 if (C::n_cmd(d) > 0) s.cmd_dist = s.cmd_dist + fabs(s.cmd[0]) * C::dt_control(d);
                 d.episode_steps[w] = s.ep_steps;
                 d.commanded_distance[w] = s.cmd_dist;
             }
-            have_ep = true;
             bool term = false, trunc = false;
-#pragma unroll(C::kUnroll)
-            for (int t = 0; t < SS_MAX_TERMINATIONS; ++t) {
-                if (t >= C::n_terms(d)) break;
+            for_terms<C, C::kCapTerms>(0, C::n_terms(d), [&](auto tt) {
+                const int t = ival(tt);
                 const int f = C::term_func(d, t);
                 bool m;
                 if (f == SS_TERM_BASE_HEIGHT_BELOW) m = s.q[1] < C::term_p0(d, t);
@@ -1017,7 +1110,7 @@ __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniform
                 if (m) s.trig_bits |= 1u << t;
                 if (C::term_time_out(d, t)) trunc |= m;
                 else term |= m;
-            }
+            });
             // detect_nonfinite over q, qd, ctrl (sim/state.py:69-74)
             bool bad = false;
 #pragma unroll
@@ -1033,7 +1126,7 @@ __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniform
             s.nonfinite = bad;
             d.terminated[w] = term;
             d.truncated[w] = trunc;
-            d.nonfinite[w] = bad;
+            d.nonfinite[(int64_t)u.nf_slot * N + w] = bad;  // per-step slot of the lag ring
         }
 
         auto ensure_action = [&]() {
@@ -1062,16 +1155,15 @@ __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniform
             ensure_action();
             ensure_sensor();
             double total = 0.0;
-#pragma unroll(C::kUnroll)
-            for (int r = 0; r < SS_MAX_REWARDS; ++r) {
-                if (r >= C::n_rewards(d)) break;
+            for_terms<C, C::kCapRewards>(0, C::n_rewards(d), [&](auto rr) {
+                const int r = ival(rr);
                 const double v = reward_value<C>(d, r, w, s, sim_step_now);
                 const double contribution = u.weight[r] * v * C::dt_control(d);
                 total += contribution;
-                d.ep_sums[(int64_t)r * N + w] += contribution;
-                d.ep_raw[(int64_t)r * N + w] += v;
+                s.ep_sum[r] = s.ep_sum[r] + contribution;
+                s.ep_rw[r] = s.ep_rw[r] + v;
                 d.last_values[(int64_t)r * N + w] = v;
-            }
+            });
             d.reward_out[w] = total;
         }
 
@@ -1083,13 +1175,8 @@ __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniform
             else if (st & SS_ST_TERM) selected = s.terminated || s.truncated;
             else selected = d.terminated[w] || d.truncated[w];
         }
-        const bool do_reset = selected && (st & (SS_ST_RESET | SS_ST_RESET_ALL));
+        const bool do_reset = selected && resets;
         if (selected && (st & SS_ST_CURRICULUM)) {
-            if (!have_ep) {
-                s.ep_steps = d.episode_steps[w];
-                s.cmd_dist = d.commanded_distance[w];
-                have_ep = true;
-            }
             for (int c = 0; c < C::n_curr(d); ++c) {
                 if (C::cur_func(d, c) == SS_CUR_TERRAIN_LEVELS) {
                     // terrain_levels (mdp.py:227-243)
@@ -1104,7 +1191,11 @@ __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniform
                 } else if (C::cur_func(d, c) == SS_CUR_COMMAND_WIDEN) {
                     // command_widen (mdp.py:246-259) -> CommandManager.widen (command.py:47-50)
                     const double steps = (double)s.ep_steps;
-                    const double mean = d.ep_raw[(int64_t)C::cur_term(d, c) * N + w] / (steps > 1.0 ? steps : 1.0);
+                    double raw = 0.0;
+                    for_terms<C, C::kCapRewards>(0, C::n_rewards(d), [&](auto rr) {
+                        if (ival(rr) == C::cur_term(d, c)) raw = s.ep_rw[ival(rr)];
+                    });
+                    const double mean = raw / (steps > 1.0 ? steps : 1.0);
                     if (mean > C::cur_p0(d, c)) {
                         for (int ch = 0; ch < C::n_cmd(d); ++ch) {
                             const double blo = fabs(C::init_lo(d, ch)) * C::cap_scale(d);
@@ -1141,17 +1232,25 @@ __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniform
                 s.q[1] = s.q[1] + height_raw(d, spawn_x);
             }
             // EventManager.apply_reset (managers/event.py:92-101)
-            for (int e = 0; e < C::n_events(d); ++e) {
+            for_terms<C, C::kCapEvents>(0, C::n_events(d), [&](auto ee) {
+                const int e = ival(ee);
                 const int mode = C::ev_mode(d, e);
                 if (mode == SS_MODE_RESET && C::ev_func(d, e) != SS_EVT_EXTERNAL) {
                     apply_event<C>(d, e, w, s);
                 } else if (mode == SS_MODE_INTERVAL) {
-                    d.event[e].elapsed[w] = 0.0;
-                    d.event[e].target[w] = draw_interval_target<C>(d, e, w);
+                    s.ev_el[e] = 0.0;
+                    s.ev_tg[e] = draw_interval_target<C>(d, e, w);
+                    if (!(st & SS_ST_EVENTS)) {
+                        d.event[e].elapsed[w] = 0.0;
+                        d.event[e].target[w] = s.ev_tg[e];
+                    }
                 }
-            }
+            });
             // CommandManager.resample
-            if (C::n_cmd(d) > 0) resample_command<C>(d, w, s);
+            if (C::n_cmd(d) > 0) {
+                resample_command<C>(d, w, s);
+                s.countdown = C::period_steps(d);
+            }
             // ActionManager.reset (managers/action.py:92-97)
 #pragma unroll
             for (int k = 0; k < SS_MAX_ACTION; ++k) {
@@ -1163,15 +1262,14 @@ __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniform
                 }
             }
             s.have_action = true;
-#pragma unroll
-            for (int t = 0; t < SS_MAX_ACTION_TERMS; ++t) {
-                if (t >= C::n_action_terms(d)) break;
+            for_terms<C, C::kCapActTerms>(0, C::n_action_terms(d), [&](auto tt) {
+                const int t = ival(tt);
 #pragma unroll
                 for (int i = 0; i < KM; ++i) {
                     if (i >= C::at_dim(d, t)) break;
                     sel_store(s.targets, C::at_joint(d, t, i), C::at_offset(d, t, i));
                 }
-            }
+            });
 #pragma unroll
             for (int j = 0; j < KM; ++j)
                 if (j < K) d.targets[(int64_t)j * N + w] = s.targets[j];
@@ -1203,14 +1301,14 @@ __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniform
                 s.fin[i] = false;
             }
             // RewardManager.reset (managers/reward.py:55-62)
-            for (int r = 0; r < C::n_rewards(d); ++r) {
-                d.finalized[(int64_t)r * N + w] = d.ep_sums[(int64_t)r * N + w];
-                d.ep_sums[(int64_t)r * N + w] = 0.0;
-                d.ep_raw[(int64_t)r * N + w] = 0.0;
-            }
+            for_terms<C, C::kCapRewards>(0, C::n_rewards(d), [&](auto rr) {
+                const int r = ival(rr);
+                d.finalized[(int64_t)r * N + w] = s.ep_sum[r];
+                s.ep_sum[r] = 0.0;
+                s.ep_rw[r] = 0.0;
+            });
             s.ep_steps = 0;
             s.cmd_dist = 0.0;
-            have_ep = true;
             d.episode_steps[w] = 0;
             d.episode_start_x[w] = s.q[0];
             d.commanded_distance[w] = 0.0;
@@ -1218,53 +1316,68 @@ __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniform
             if (!(st & SS_ST_OBS))
                 for (int g = 0; g < C::n_groups(d); ++g) d.group[g].pending[w] = 1;
         }
+        if (st & (SS_ST_REWARD | SS_ST_RESET | SS_ST_RESET_ALL)) {
+            // episodic sums: one store each, after the reward update and the reset finalize
+            for_terms<C, C::kCapRewards>(0, C::n_rewards(d), [&](auto rr) {
+                const int r = ival(rr);
+                if ((st & SS_ST_REWARD) || do_reset) {
+                    d.ep_sums[(int64_t)r * N + w] = s.ep_sum[r];
+                    d.ep_raw[(int64_t)r * N + w] = s.ep_rw[r];
+                }
+            });
+        }
 
         // ---- 6. CommandManager.update (managers/command.py:41-45)
         if ((st & SS_ST_COMMAND) && C::n_cmd(d) > 0) {
-            const long long cd = d.countdown[w] - 1;
+            const long long cd = s.countdown - 1;
             if (cd <= 0) resample_command<C>(d, w, s);
             else d.countdown[w] = cd;
         }
 
         // ---- 7. EventManager.apply_interval (managers/event.py:103-114)
         if (st & SS_ST_EVENTS) {
-#pragma unroll(C::kUnroll)
-            for (int e = 0; e < SS_MAX_EVENTS; ++e) {
-                if (e >= C::n_events(d)) break;
-                if (C::ev_mode(d, e) != SS_MODE_INTERVAL) continue;
-                double el = d.event[e].elapsed[w] + C::dt_control(d);
-                const double tgt = d.event[e].target[w];
+            for_terms<C, C::kCapEvents>(0, C::n_events(d), [&](auto ee) {
+                const int e = ival(ee);
+                if (C::ev_mode(d, e) != SS_MODE_INTERVAL) return;
+                double el = s.ev_el[e] + C::dt_control(d);
+                const double tgt = s.ev_tg[e];
                 const bool fire = el >= tgt - 0.5 * C::dt_control(d);
                 if (fire) {
                     // registered Python terms run on the host for the fired ids
                     if (C::ev_func(d, e) != SS_EVT_EXTERNAL) apply_event<C>(d, e, w, s);
                     el = 0.0;
-                    d.event[e].target[w] = draw_interval_target<C>(d, e, w);
+                    s.ev_tg[e] = draw_interval_target<C>(d, e, w);
                 }
+                if (fire || s.was_reset) d.event[e].target[w] = s.ev_tg[e];
                 if (d.event[e].fired) d.event[e].fired[w] = fire;
                 d.event[e].elapsed[w] = el;
-            }
+            });
         }
 
         // ---- 8. observations (post-reset state) (managers/observation.py:139-141)
         if (st & SS_ST_PREV_BEFORE) {
             d.prev_lin_vel_b[w] = s.lvb0;
             d.prev_lin_vel_b[N + w] = s.lvb1;
+            s.plv0 = s.lvb0;
+            s.plv1 = s.lvb1;
         }
         if (st & SS_ST_OBS) {
             ensure_action();
             unsigned bad_bits = 0;
-#pragma unroll(C::kUnroll)
-            for (int g = 0; g < SS_MAX_GROUPS; ++g) {
-                if (g >= C::n_groups(d)) break;
-                if (!((u.groups_mask >> g) & 1u)) continue;
+            for_terms<C, C::kCapGroups>(0, C::n_groups(d), [&](auto gg) {
+                const int g = ival(gg);
+                if (!((u.groups_mask >> g) & 1u)) return;
                 bool pending = s.was_reset;
                 if (u.any_pending) {
                     pending |= d.group[g].pending[w] != 0;
                     d.group[g].pending[w] = 0;
                 }
-                compute_group<C>(d, u, g, w, s, pending, bad_bits);
-            }
+                double* out = d.group[g].out + (int64_t)w * C::g_dim(d, g);
+                const int first = C::g_first(d, g);
+                for_terms<C, C::kCapObs>(first, first + C::g_n(d, g), [&](auto tt) {
+                    obs_term<C>(d, u, ival(tt), w, s, pending, out, bad_bits);
+                });
+            });
             d.obs_bad[w] = bad_bits;
         }
         if (st & SS_ST_PREV_AFTER) {

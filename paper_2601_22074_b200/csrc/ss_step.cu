@@ -54,6 +54,8 @@ extern "C" size_t ss_sizeof(int which) {
         case 0: return sizeof(ss_env_desc);
         case 1: return sizeof(ss_uniforms);
         case 2: return sizeof(ss_rng_draw_args);
+        case 3: return sizeof(ss_rt_state);
+        case 4: return sizeof(ss_launch);
         default: return 0;
     }
 }
@@ -99,11 +101,12 @@ struct JitModule {
 
 // Compile `src` (with named headers) for sm_100a. Returns the cubin through
 // a two-call protocol: with out == NULL, *size receives the byte count.
-extern "C" int ss_jit_compile(const char* src, int n_headers, const char* const* header_src,
+extern "C" int ss_jit_compile(const char* src, const char* name, int n_headers, const char* const* header_src,
                               const char* const* header_names, int n_opts, const char* const* opts, void* out,
                               size_t* size, char* log, size_t log_size) {
     nvrtcProgram prog;
-    nvrtcResult r = nvrtcCreateProgram(&prog, src, "ss_step_jit.cu", n_headers, header_src, header_names);
+    nvrtcResult r = nvrtcCreateProgram(&prog, src, name ? name : "ss_step_jit.cu", n_headers, header_src,
+                                       header_names);
     if (r != NVRTC_SUCCESS) {
         ss_set_error("nvrtcCreateProgram", nvrtcGetErrorString(r));
         return -10;

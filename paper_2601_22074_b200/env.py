@@ -16,9 +16,9 @@ ring keeps that many spare steps of frames so the dump is exact).
 
 from __future__ import annotations
 
+import ctypes
 import os
 import warnings
-from collections import deque
 from collections.abc import Mapping
 
 import numpy as np
@@ -44,7 +44,7 @@ from .terrain import generate_grid
 
 __all__ = ["EnvCfg", "SceneCfg", "InitStateCfg", "ManagerBasedRlEnv", "load_capture"]
 
-NF_LAG = 3  # control steps the host may run ahead before it must look at nonfinite flags
+NF_LAG = 4  # control steps the host may run ahead before it must look at nonfinite flags
 
 _SIM = native.SS_ST_APPLY | native.SS_ST_PUSH | native.SS_ST_PHYS | native.SS_ST_SENSOR
 
@@ -142,20 +142,30 @@ class ManagerBasedRlEnv:
         self.episode_start_x = torch.zeros(n, dtype=torch.float64, device=dev)
         self.commanded_distance = torch.zeros(n, dtype=torch.float64, device=dev)
         self._prev_lin_vel_b = torch.zeros((2, n), dtype=torch.float64, device=dev)
-        self.global_step = 0
         self._dump_paths: list[str] = []
         self._startup_done = False
         self._desc = None
+        self._desc_ref = None
         self._jit_handle = None
         self.use_jit = jit.enabled()
-        self._u = native.Uniforms()
-        self._launches = 0
+        self._lib = native.lib()
 
-        # nonfinite bookkeeping: zero-copy flags + a ring of per-step world masks
-        self._nf_flags = torch.zeros(NF_LAG + 2, dtype=torch.int32).pin_memory()
-        self._nf_masks = torch.zeros((NF_LAG + 2, n), dtype=torch.bool, device=dev)
-        self._nf_slot = 0
-        self._nf_pending: deque = deque()
+        # native runtime state shared with ss_rt_launch (counters, heads, weights)
+        self._rt = native.RtState()
+        self._rt_ref = ctypes.byref(self._rt)
+        self._la = native.Launch()
+        self._la_ref = ctypes.byref(self._la)
+        self._rt.global_step = 0
+        self._rt.sensor_last_update = -1
+        # nonfinite bookkeeping: zero-copy flags (mapped pinned memory) + a ring of
+        # per-step world masks, NF_LAG + 2 slots
+        slots = NF_LAG + 2
+        self._nf_flags = torch.zeros(native.SS_RT_SLOTS, dtype=torch.int32).pin_memory()
+        self._nf_masks = torch.zeros((slots, n), dtype=torch.bool, device=dev)
+        self._rt.nf_flags = self._nf_flags.data_ptr()
+        self._rt.nf_slots = slots
+        self._nf_out = (ctypes.c_int32 * slots)()
+        self._nf_views = [self._nf_masks[i] for i in range(slots)]
 
         all_ids = torch.arange(n, device=dev)
         self.robot.write_default_state(self.state, all_ids)
@@ -171,6 +181,25 @@ class ManagerBasedRlEnv:
         self.observation_manager = ObservationManager(cfg.observations, self)
         self.model.on_layout_change(self._invalidate)
         self.staged = self._needs_staging()
+        self.capture.bind(self._rt)
+        self.contact_sensor.bind(self._rt)
+        self.action_manager.bind(self._rt)
+        self.observation_manager.bind(self._rt)
+        self.reward_manager.weights.bind(self._rt)
+
+    def __del__(self):
+        try:
+            self._lib.ss_rt_release(self._rt_ref)
+        except Exception:
+            pass
+
+    @property
+    def global_step(self) -> int:
+        return self._rt.global_step
+
+    @global_step.setter
+    def global_step(self, v: int) -> None:
+        self._rt.global_step = int(v)
 
     # -- descriptor ---------------------------------------------------------------
 
@@ -228,89 +257,60 @@ class ManagerBasedRlEnv:
             d.prev_lin_vel_b = self._prev_lin_vel_b.data_ptr()
             self.observation_manager.native_into(d)
             d.nf_flags = self._nf_flags.data_ptr()
+            d.nonfinite = self._nf_masks.data_ptr()
             # the descriptor may have allocated new stream slots: refresh their pointers
             for s, base in enumerate(r.bases):
                 d.rng.base[s] = base
                 d.rng.counter[s] = r.counters[s].data_ptr()
             self._desc = d
+            self._desc_ref = ctypes.byref(d)
         return self._desc
 
     def _launch(self, stages: int, nsub: int = 0, actions=None, reset_mask=None, groups_mask: int = 0,
                 flags: int = 0) -> None:
-        """One ss_env_step launch with every host-tracked per-step scalar."""
-        d = self._get_desc()
-        if self._desc is None:  # a slot was allocated while building
+        """One launch through the native runtime (ss_rt_launch): it derives the
+        per-step uniforms from the shared ss_rt_state, launches the
+        specialized (or generic) kernel and advances the counters."""
+        d = self._desc if self._desc is not None else self._get_desc()
+        if self._desc is None:  # a stream slot was allocated while building
             d = self._get_desc()
-        u = self._u
-        u.stages = stages
-        u.nsub = nsub
-        u.flags = flags
-        u.global_step = self.global_step
-        sim_step = self.state.sim_step
-        u.sim_step = sim_step
-        if stages & native.SS_ST_PUSH:
-            u.capture_slot0 = self.capture.reserve(nsub, sim_step)
-        if stages & native.SS_ST_SENSOR:
-            u.sensor_mask = self.contact_sensor.enabled_mask(sim_step, nsub, bool(stages & native.SS_ST_PHYS))
-        if stages & native.SS_ST_APPLY:
-            self.action_manager.advance_heads(u, nsub)
-        om = self.observation_manager
-        u.groups_mask = groups_mask
-        u.any_pending = int(om.any_pending)
-        if stages & native.SS_ST_OBS:
-            om.fill_heads(u)
-        if stages & native.SS_ST_REWARD:
-            self.reward_manager.fill_weights(u)
-        u.actions = None if actions is None else actions.data_ptr()
-        u.reset_mask = None if reset_mask is None else reset_mask.data_ptr()
-        if stages & native.SS_ST_TERM:
-            slot = self._nf_slot
-            d.nonfinite = self._nf_masks[slot].data_ptr()
-            self.termination_manager.last_nonfinite = self._nf_masks[slot]
-            self._nf_flags[slot] = 0
-            u.nf_slot = slot
-        stream = native.current_stream(self.device)
         if self.use_jit and self._jit_handle is None:
             try:
                 self._jit_handle = jit.module_for(d)
             except jit.JitUnsupported as err:
                 warnings.warn(f"per-env specialization unavailable ({err}); using the generic sm_100a kernel")
                 self.use_jit = False
-        if self.use_jit:
-            native.call("ss_env_step_jit", self._jit_handle, native.byref(d), native.byref(u), stream)
-        else:
-            native.call("ss_env_step", native.byref(d), native.byref(u), stream)
-        self._launches += 1
-        if stages & native.SS_ST_PHYS:
-            self.state.sim_step += nsub
-        if stages & native.SS_ST_OBS and (groups_mask + 1) == (1 << len(om.groups)):
-            om.any_pending = False
-        if stages & (native.SS_ST_RESET | native.SS_ST_RESET_ALL) and not stages & native.SS_ST_OBS:
-            om.any_pending = True
-        if stages & native.SS_ST_TERM:
-            self._nf_note()
+        rt = self._rt
+        term = stages & native.SS_ST_TERM
+        if term:
+            self._nf_drain(NF_LAG)
+            self.termination_manager.last_nonfinite = self._nf_views[rt.nf_slot]
+        la = self._la
+        la.stages = stages
+        la.nsub = nsub
+        la.flags = flags
+        la.groups_mask = groups_mask
+        la.actions = None if actions is None else actions.data_ptr()
+        la.reset_mask = None if reset_mask is None else reset_mask.data_ptr()
+        rt.sim_step = self.state.sim_step
+        native.LAUNCHES["count"] += 1
+        rc = self._lib.ss_rt_launch(self._desc_ref, self._rt_ref, self._la_ref,
+                                    self._jit_handle if self.use_jit else None,
+                                    native.current_stream(self.device))
+        if rc != 0:
+            raise native.NativeError(f"ss_rt_launch failed ({rc}): {self._lib.ss_last_error().decode()}")
+        self.state.sim_step = rt.sim_step
 
     # -- nonfinite detection (deferred, no per-step sync) ----------------------------
 
-    def _nf_note(self) -> None:
-        import torch
-
-        ev = torch.cuda.Event()
-        ev.record(torch.cuda.current_stream(self.device))
-        self._nf_pending.append((ev, self._nf_slot, self.capture.pushes, self.capture.count, self.state.sim_step))
-        self._nf_slot = (self._nf_slot + 1) % self._nf_flags.numel()
-        self._nf_drain(NF_LAG)
-
     def _nf_drain(self, keep: int) -> None:
-        while self._nf_pending:
-            ev, slot, pushes, count, sim_step = self._nf_pending[0]
-            if len(self._nf_pending) > keep:
-                ev.synchronize()
-            elif not ev.query():
-                break
-            self._nf_pending.popleft()
-            if int(self._nf_flags[slot]):
-                self._dump_on_nonfinite(slot, pushes, count, sim_step)
+        n = self._lib.ss_rt_poll(self._rt_ref, keep, self._nf_out, len(self._nf_out))
+        if n < 0:
+            raise native.NativeError(f"ss_rt_poll failed: {self._lib.ss_last_error().decode()}")
+        rt = self._rt
+        for i in range(n):
+            slot = self._nf_out[i]
+            self._dump_on_nonfinite(slot, rt.nf_pushes[slot], rt.nf_count[slot], rt.nf_sim_step[slot])
 
     @property
     def dump_paths(self) -> list[str]:

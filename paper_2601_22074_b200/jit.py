@@ -31,7 +31,8 @@ _HEADERS = {
     "ss_cfg.cuh": os.path.join(_CSRC, "ss_cfg.cuh"),
     "ss_kernel.cuh": os.path.join(_CSRC, "ss_kernel.cuh"),
 }
-OPTIONS = ["--gpu-architecture=sm_100a", "--fmad=false", "-std=c++17", "-lineinfo", "-DSS_JIT=1"]
+OPTIONS = ["--gpu-architecture=sm_100a", "--fmad=false", "-std=c++17", "-lineinfo", "-DSS_JIT=1", "-default-device",
+           f"--include-path={_CSRC}", f"--include-path={os.path.dirname(native.HEADER)}"]
 KERNEL = "ss_step_jit"
 
 
@@ -78,7 +79,10 @@ def _lit(typ: str, v) -> str:
 
 def config_source(d) -> str:
     """C++ source of the constexpr config struct for descriptor ``d``."""
+    caps = {"kCapAct": d.n_actuators, "kCapActTerms": d.n_action_terms, "kCapTerms": d.n_terms,
+            "kCapRewards": d.n_rewards, "kCapEvents": d.n_events, "kCapGroups": d.n_groups, "kCapObs": d.n_obs_terms}
     lines = ["struct JitCfg {", "  static constexpr bool kJit = true;", "  static constexpr int kUnroll = 64;"]
+    lines += [f"  static constexpr int {k} = {int(v)};" for k, v in caps.items()]
     head = "  static __device__ __forceinline__"
     for typ, name, expr in _LISTS["SS_CFG_SCALARS"]:
         val = eval(expr, {"d": d})  # noqa: S307 -- expressions come from ss_cfg.cuh
@@ -120,22 +124,35 @@ def _headers():
     return names, srcs
 
 
+def _source_file(src: str) -> str:
+    """Write the generated translation unit next to the cache so -lineinfo
+    (and ncu --import-source) can resolve it; headers resolve to csrc/."""
+    key = hashlib.sha256(src.encode()).hexdigest()[:16]
+    path = os.path.join(_cache_dir(), f"ss_step_jit_{key}.cu")
+    try:
+        os.makedirs(os.path.dirname(path), exist_ok=True)
+        if not os.path.exists(path):
+            with open(path, "w") as fh:
+                fh.write(src)
+    except OSError:
+        return "ss_step_jit.cu"
+    return path
+
+
 def compile_cubin(src: str) -> bytes:
     """NVRTC: source -> sm_100a cubin (no GPU needed)."""
-    names, srcs = _headers()
-    c_names = (ctypes.c_char_p * len(names))(*names)
-    c_srcs = (ctypes.c_char_p * len(srcs))(*srcs)
     opts = [o.encode() for o in OPTIONS]
     c_opts = (ctypes.c_char_p * len(opts))(*opts)
     size = ctypes.c_size_t(0)
     log = ctypes.create_string_buffer(1 << 16)
     so = native.lib()
-    rc = so.ss_jit_compile(src.encode(), len(names), c_srcs, c_names, len(opts), c_opts, None, ctypes.byref(size),
+    name = _source_file(src).encode()
+    rc = so.ss_jit_compile(src.encode(), name, 0, None, None, len(opts), c_opts, None, ctypes.byref(size),
                            log, len(log))
     if rc != 0:
         raise native.NativeError(f"NVRTC failed: {so.ss_last_error().decode()}\n{log.value.decode()[:4000]}")
     buf = ctypes.create_string_buffer(size.value)
-    rc = so.ss_jit_compile(src.encode(), len(names), c_srcs, c_names, len(opts), c_opts, buf, ctypes.byref(size),
+    rc = so.ss_jit_compile(src.encode(), name, 0, None, None, len(opts), c_opts, buf, ctypes.byref(size),
                            log, len(log))
     if rc != 0:
         raise native.NativeError(f"NVRTC failed: {so.ss_last_error().decode()}")

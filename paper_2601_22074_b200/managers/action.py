@@ -117,11 +117,16 @@ class ActionManager:
 
     # -- host-side ring bookkeeping for the fused kernel ------------------------
 
-    def advance_heads(self, u, nsub: int) -> None:
-        for i, a in enumerate(self.actuators):
+    def bind(self, rt) -> None:
+        """Hand the delay-ring heads to the native runtime (ss_rt_launch advances them)."""
+        acts = self.actuators
+        rt.n_act = len(acts)
+        for i, a in enumerate(acts):
             if a.delay is not None:
-                u.act_head0[i] = a.delay.head
-                a.delay.head = (a.delay.head + nsub) % a.delay.capacity
+                a.delay.bind(rt, i)
+            else:
+                rt.act_head[i] = 0
+                rt.act_cap[i] = 0
 
     def native_into(self, d) -> None:
         d.n_action_terms = len(self.terms)

@@ -83,8 +83,9 @@ class _ObsTerm:
         if self.dim > max_dim:
             raise ManagerError(f"obs term {name!r}: dim {self.dim} exceeds the sm_100a build ({max_dim})")
         self.noise_purpose = f"obs.{group}.{name}"
-        self.delay_head = 0
-        self.hist_head = cfg.history - 1
+        self._heads = [0, cfg.history - 1]
+        self._rt = None
+        self._rt_idx = 0
         dev = env.device
         self._dring = (torch.zeros((cfg.delay_steps + 1, self.dim, n), dtype=torch.float64, device=dev)
                        if cfg.delay_steps > 0 else None)
@@ -93,9 +94,21 @@ class _ObsTerm:
         self.ext = torch.zeros((n, self.dim), dtype=torch.float64, device=dev) if self.sid is None else None
         self.out_dim = self.dim * cfg.history
 
-    def advance(self) -> None:
-        self.delay_head = (self.delay_head + 1) % (self.cfg.delay_steps + 1)
-        self.hist_head = (self.hist_head + 1) % self.cfg.history
+    def bind(self, rt, idx: int, group_idx: int) -> None:
+        self._rt, self._rt_idx = rt, idx
+        rt.obs_group[idx] = group_idx
+        rt.obs_delay_len[idx] = self.cfg.delay_steps + 1
+        rt.obs_hist_len[idx] = self.cfg.history
+        rt.obs_delay_head[idx] = self._heads[0]
+        rt.obs_hist_head[idx] = self._heads[1]
+
+    @property
+    def delay_head(self) -> int:
+        return self._rt.obs_delay_head[self._rt_idx] if self._rt is not None else self._heads[0]
+
+    @property
+    def hist_head(self) -> int:
+        return self._rt.obs_hist_head[self._rt_idx] if self._rt is not None else self._heads[1]
 
 
 class ObservationManager:
@@ -118,10 +131,35 @@ class ObservationManager:
             self._pending[g] = torch.zeros(n, dtype=torch.uint8, device=dev)
         if sum(len(t) for t in self.groups.values()) > native.SS_MAX_OBS_TERMS:
             raise ManagerError(f"more than {native.SS_MAX_OBS_TERMS} observation terms")
-        self.any_pending = False
+        self._any_pending = False
+        self._rt = None
         self._bad = torch.zeros(n, dtype=torch.int32, device=dev)
         self._cache: dict[str, int] = {}
         self._report_terms: list[str] = []
+
+    def bind(self, rt) -> None:
+        """Hand the ring heads and the pending flag to the native runtime."""
+        self._rt = rt
+        names = list(self.groups)
+        rt.n_groups = len(names)
+        i = 0
+        for g, terms in self.groups.items():
+            for t in terms:
+                t.bind(rt, i, names.index(g))
+                i += 1
+        rt.n_obs = i
+        rt.any_pending = int(self._any_pending)
+
+    @property
+    def any_pending(self) -> bool:
+        return bool(self._rt.any_pending) if self._rt is not None else self._any_pending
+
+    @any_pending.setter
+    def any_pending(self, v: bool) -> None:
+        if self._rt is not None:
+            self._rt.any_pending = int(v)
+        else:
+            self._any_pending = bool(v)
 
     def group_dim(self, group: str) -> int:
         return sum(t.out_dim for t in self.groups[group])
@@ -149,20 +187,15 @@ class ObservationManager:
                     t.ext.copy_(_as_rows(t.func(self.env, **t.cfg.params), self.env.num_envs, self.env.device))
 
     def begin(self, groups) -> int:
-        """Host bookkeeping before an OBS launch: advance ring heads, return the group mask."""
+        """Host bookkeeping before an OBS launch (the runtime advances the ring
+        heads of the masked groups); returns the group mask."""
         mask = 0
         names = list(self.groups)
+        step = self.env.global_step
         for g in groups:
             mask |= 1 << names.index(g)
-            for t in self.groups[g]:
-                t.advance()
-            self._cache[g] = self.env.global_step
+            self._cache[g] = step
         return mask
-
-    def fill_heads(self, u) -> None:
-        for i, t in enumerate(self.all_terms()):
-            u.obs_delay_head[i] = t.delay_head
-            u.obs_hist_head[i] = t.hist_head
 
     def compute(self, group: str):
         """Group output (N, sum of term dims x history) (managers/observation.py:99-137)."""

@@ -20,6 +20,27 @@ class _Rows(dict):
     """name -> (N,) row view of a (T, N) device array (dict API of the reference)."""
 
 
+class _Weights(dict):
+    """Host float weights (a dict, like the reference) mirrored into the
+    native runtime's per-launch uniforms on every write."""
+
+    def __init__(self, items, order):
+        super().__init__(items)
+        self._order = list(order)
+        self._rt = None
+
+    def bind(self, rt) -> None:
+        self._rt = rt
+        rt.n_rewards = len(self._order)
+        for i, k in enumerate(self._order):
+            rt.weight[i] = float(dict.__getitem__(self, k))
+
+    def __setitem__(self, k, v) -> None:
+        super().__setitem__(k, v)
+        if self._rt is not None and k in self._order:
+            self._rt.weight[self._order.index(k)] = float(v)
+
+
 class RewardManager:
     def __init__(self, cfg: dict[str, RewardTermCfg], env):
         import torch
@@ -33,7 +54,7 @@ class RewardManager:
             self.terms[name] = resolve(REWARD_TERMS, tc.func, "reward")
         if len(self.terms) > native.SS_MAX_REWARDS:
             raise ManagerError(f"more than {native.SS_MAX_REWARDS} reward terms")
-        self.weights = {name: c.weight for name, c in cfg.items()}
+        self.weights = _Weights(((name, c.weight) for name, c in cfg.items()), cfg)
         n, t, dev = env.num_envs, max(1, len(cfg)), env.device
         z = lambda: torch.zeros((t, n), dtype=torch.float64, device=dev)  # noqa: E731
         self._sums, self._raw, self._last, self._final = z(), z(), z(), z()
@@ -118,6 +139,3 @@ class RewardManager:
         d.last_values = self._last.data_ptr()
         d.finalized = self._final.data_ptr()
 
-    def fill_weights(self, u) -> None:
-        for i, name in enumerate(self.terms):
-            u.weight[i] = float(self.weights[name])

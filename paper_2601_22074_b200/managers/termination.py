@@ -95,5 +95,4 @@ class TerminationManager:
                     t.p0 = float(p.get("max_pitch", 1.0))
         d.terminated = self.terminated.data_ptr()
         d.truncated = self.truncated.data_ptr()
-        d.nonfinite = self.last_nonfinite.data_ptr()
         d.trigger_counts = self._counts.data_ptr()

@@ -86,6 +86,8 @@ EnvDesc = _TYPES["ss_env_desc"]
 Uniforms = _TYPES["ss_uniforms"]
 RngDrawArgs = _TYPES["ss_rng_draw_args"]
 Terrain = _TYPES["ss_terrain"]
+RtState = _TYPES["ss_rt_state"]
+Launch = _TYPES["ss_launch"]
 
 # ---------------------------------------------------------------------------
 # library
@@ -106,13 +108,16 @@ _SIGNATURES = {
         ctypes.c_int,
     ),
     "ss_jit_compile": (
-        [ctypes.c_char_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p,
+        [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p,
          ctypes.c_void_p, ctypes.POINTER(ctypes.c_size_t), ctypes.c_char_p, ctypes.c_size_t],
         ctypes.c_int,
     ),
     "ss_jit_load": ([ctypes.c_void_p, ctypes.c_size_t, ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
     "ss_jit_unload": ([ctypes.c_void_p], ctypes.c_int),
     "ss_env_step_jit": ([ctypes.c_void_p] * 4, ctypes.c_int),
+    "ss_rt_launch": ([ctypes.c_void_p] * 5, ctypes.c_int),
+    "ss_rt_poll": ([ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_int32], ctypes.c_int),
+    "ss_rt_release": ([ctypes.c_void_p], ctypes.c_int),
     "ss_actuator_eval": (
         [ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double, ctypes.c_double, ctypes.c_double,
          ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p],
@@ -138,7 +143,7 @@ def lib():
             fn.restype = res
         if so.ss_abi_version() != SS_ABI_VERSION:  # noqa: F821
             raise NativeError("stale extension: ABI version mismatch, rebuild it")
-        for which, cls in ((0, EnvDesc), (1, Uniforms), (2, RngDrawArgs)):
+        for which, cls in ((0, EnvDesc), (1, Uniforms), (2, RngDrawArgs), (3, RtState), (4, Launch)):
             if so.ss_sizeof(which) != ctypes.sizeof(cls):
                 raise NativeError(
                     f"struct layout mismatch for {cls.__name__}: C {so.ss_sizeof(which)} vs "

@@ -155,14 +155,21 @@ class StreamPack:
         args.counter = self.counters[s].data_ptr()
         args.sel = sel_t.data_ptr() if sel_t is not None else None
         keep = []
-        if kind == 0:
+        if kind == 0 and not torch.is_tensor(lo) and not torch.is_tensor(hi) and np.ndim(lo) == 0 and np.ndim(hi) == 0:
+            # scalar bounds: no device tensors, no synchronization
+            args.lohi_mode = 0
+            args.lo = float(lo)
+            args.hi = float(hi)
+        elif kind == 0:
             lo_t = torch.as_tensor(lo, dtype=torch.float64, device=self.device)
             hi_t = torch.as_tensor(hi, dtype=torch.float64, device=self.device)
             lo_t, hi_t = torch.broadcast_tensors(lo_t, hi_t)
             if lo_t.dim() == 0:
-                args.lohi_mode = 0
-                args.lo = float(lo_t.item()) if not torch.is_tensor(lo) else float(lo_t.item())
-                args.hi = float(hi_t.item()) if not torch.is_tensor(hi) else float(hi_t.item())
+                args.lohi_mode = 1
+                lo_t = lo_t.expand(n_sel).contiguous()
+                hi_t = hi_t.expand(n_sel).contiguous()
+                args.lo_arr, args.hi_arr = lo_t.data_ptr(), hi_t.data_ptr()
+                keep = [lo_t, hi_t]
             elif lo_t.dim() == 1:
                 args.lohi_mode = 1
                 lo_t, hi_t = lo_t.contiguous(), hi_t.contiguous()

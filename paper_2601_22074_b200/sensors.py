@@ -73,7 +73,23 @@ class ContactSensor:
         self._last_air = z(n_feet, n_worlds)
         self._contact = z(n_feet, n_worlds)
         self._td = torch.full((n_feet, n_worlds), NEVER_TOUCHED, dtype=torch.int64, device=device)
-        self._last_update_step = -1
+        self._last_local = -1
+        self._rt = None
+
+    def bind(self, rt) -> None:
+        self._rt = rt
+        rt.sensor_last_update = self._last_local
+
+    @property
+    def _last_update_step(self) -> int:
+        return self._rt.sensor_last_update if self._rt is not None else self._last_local
+
+    @_last_update_step.setter
+    def _last_update_step(self, v: int) -> None:
+        if self._rt is not None:
+            self._rt.sensor_last_update = v
+        else:
+            self._last_local = v
 
     in_contact = property(lambda self: self._in.t())
     normal_force = property(lambda self: self._normal.t())

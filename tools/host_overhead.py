@@ -1,0 +1,47 @@
+"""Measure host-side (Python) cost per env.step vs GPU time; cProfile the step."""
+import cProfile
+import os
+import pstats
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+from paper_2601_22074_b200.env import ManagerBasedRlEnv  # noqa: E402
+from paper_2601_22074_b200.policies import random_policy  # noqa: E402
+from paper_2601_22074_b200.tasks import make_env_cfg  # noqa: E402
+
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
+env = ManagerBasedRlEnv(make_env_cfg("Velocity-Rough", num_envs=n))
+env.reset()
+for i in range(20):
+    env.step(random_policy(env, i))
+torch.cuda.synchronize()
+K = 500
+t0 = time.perf_counter()
+for i in range(K):
+    env.step(random_policy(env, i))
+t1 = time.perf_counter()
+torch.cuda.synchronize()
+t2 = time.perf_counter()
+print(f"N={n}: host enqueue {1e6*(t1-t0)/K:.1f} us/step, wall incl. drain {1e6*(t2-t0)/K:.1f} us/step, "
+      f"{n*K/(t2-t0)/1e6:.1f} M env-steps/s back-to-back")
+a = random_policy(env, 0)
+t0 = time.perf_counter()
+for i in range(K):
+    env.step(a)
+torch.cuda.synchronize()
+print(f"step only: {1e6*(time.perf_counter()-t0)/K:.1f} us/step")
+t0 = time.perf_counter()
+for i in range(K):
+    random_policy(env, i)
+torch.cuda.synchronize()
+print(f"policy only: {1e6*(time.perf_counter()-t0)/K:.1f} us/call")
+pr = cProfile.Profile()
+pr.enable()
+for i in range(200):
+    env.step(random_policy(env, i))
+pr.disable()
+torch.cuda.synchronize()
+pstats.Stats(pr).sort_stats("tottime").print_stats(18)
