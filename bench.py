@@ -335,7 +335,8 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_kind": peak_kind, "traffic": traffic,
                          "algorithmic_bytes_per_env_step": per_world["total"],
-                         "kernel": "step_kernel<4,2> (fused control step)",
+                         "kernel": "ss_step_jit (fused control step, per-env NVRTC specialization)"
+                         if env.use_jit else "step_kernel<4,2> (fused control step, generic)",
                          "kernel_ms": 1e3 * t_kernel / args.steps},
             "policy_bytes_per_env_step": policy_bytes_per_world(env),
             "cpu_baseline": cpu,
