@@ -564,7 +564,7 @@ int ss_randomize(const ss_env_desc* desc, int32_t field, int32_t distribution,
 int ss_jit_compile(const char* src, const char* name, int n_headers, const char* const* header_src,
                    const char* const* header_names, int n_opts, const char* const* opts,
                    void* out, size_t* size, char* log, size_t log_size);
-int ss_jit_load(const void* cubin, size_t size, const char* kernel_name, void** handle);
+int ss_jit_load(const void* cubin, size_t size, const char* kernel_name, int block, void** handle);
 int ss_jit_unload(void* handle);
 int ss_env_step_jit(void* handle, const ss_env_desc* desc, const ss_uniforms* u, void* stream);
 /* Runtime: derive the uniforms from *st, launch (JIT module when jit != NULL,

@@ -74,10 +74,14 @@ __device__ __forceinline__ double np_minimum(double a, double b) {
     return (a <= b || isnan_(a)) ? a : b;
 }
 __device__ __forceinline__ double np_clip(double x, double lo, double hi) {
-    // numpy _NPY_CLIP = min(max(x, lo), hi) with _NPY_MAX(a,b) = isnan(a) ? a : (a > b ? a : b)
-    double m = isnan_(x) ? x : (x > lo ? x : lo);
-    return isnan_(m) ? m : (m < hi ? m : hi);
+    // numpy _NPY_CLIP = min(max(x, lo), hi) with NaN propagation from x.
+    // "!(x <= lo)" is one unordered compare (true for x > lo or x NaN);
+    // bounds are finite wherever the step uses clip with state-dependent x.
+    const double m = !(x <= lo) ? x : lo;
+    return !(m >= hi) ? m : hi;
 }
+// numpy maximum(0.0, x): NaN in x propagates
+__device__ __forceinline__ double np_max0(double x) { return !(x <= 0.0) ? x : 0.0; }
 
 // numpy add.reduce over a short contiguous axis: n < 8 is a sequential sum
 // from 0.0; n >= 8 uses the 8-lane pairwise block (numpy pairwise_sum).

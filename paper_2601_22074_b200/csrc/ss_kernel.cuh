@@ -359,7 +359,7 @@ __device__ __forceinline__ void phys_substep(const ss_env_desc& d, int w, World<
             }
             const double phi = height<C>(d, px) - pz;
             const bool touching = phi > 0.0;
-            double normal = np_maximum(0.0, C::k_n(d) * phi - C::c_n(d) * vz);
+            double normal = np_max0(C::k_n(d) * phi - C::c_n(d) * vz);
             normal = touching ? normal : 0.0;
             const double bound = friction * normal;
             double tangent = np_clip(-C::k_t(d) * vx, -bound, bound);
@@ -873,7 +873,7 @@ __device__ __forceinline__ double reward_value(const ss_env_desc& d, int r, int 
                     const double lo = C::pos_lo(d, j), hi = C::pos_hi(d, j);
                     const double mid = 0.5 * (lo + hi);
                     const double soft_half = 0.5 * (hi - lo) * C::soft_frac(d, j);
-                    ex[j] = np_maximum(0.0, fabs(s.eq[3 + j] - mid) - soft_half);
+                    ex[j] = np_max0(fabs(s.eq[3 + j] - mid) - soft_half);
                 }
             }
             return np_sum<KM>(ex, K);

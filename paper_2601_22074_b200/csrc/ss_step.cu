@@ -132,10 +132,10 @@ extern "C" int ss_jit_compile(const char* src, const char* name, int n_headers, 
     return 0;
 }
 
-extern "C" int ss_jit_load(const void* cubin, size_t size, const char* kernel_name, void** handle) {
+extern "C" int ss_jit_load(const void* cubin, size_t size, const char* kernel_name, int block, void** handle) {
     (void)size;
     JitModule* m = new JitModule();
-    m->block = kBlock;
+    m->block = block > 0 ? block : kBlock;
     cudaError_t e = cudaLibraryLoadData(&m->lib, cubin, nullptr, nullptr, 0, nullptr, nullptr, 0);
     if (e != cudaSuccess) {
         delete m;

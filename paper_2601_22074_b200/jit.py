@@ -84,15 +84,28 @@ def config_source(d) -> str:
     lines = ["struct JitCfg {", "  static constexpr bool kJit = true;", "  static constexpr int kUnroll = 64;"]
     lines += [f"  static constexpr int {k} = {int(v)};" for k, v in caps.items()]
     head = "  static __device__ __forceinline__"
+    # Integers (counts, ids, flags, indices) become immediates: they drive the
+    # unrolling and fold the term tables. Doubles stay kernel-parameter loads:
+    # FP64 instructions read constant-bank operands directly, whereas a 64-bit
+    # immediate costs two uniform moves per use.
     for typ, name, expr in _LISTS["SS_CFG_SCALARS"]:
+        if typ == "double":
+            lines.append(f"{head} {typ} {name}(const ss_env_desc& d) {{ return {expr}; }}")
+            continue
         val = eval(expr, {"d": d})  # noqa: S307 -- expressions come from ss_cfg.cuh
         lines.append(f"{head} {typ} {name}(const ss_env_desc&) {{ return {_lit(typ, val)}; }}")
     for typ, name, bound, expr in _LISTS["SS_CFG_ARRAYS"]:
+        if typ == "double":
+            lines.append(f"{head} {typ} {name}(const ss_env_desc& d, int i) {{ return {expr}; }}")
+            continue
         n = _bound(bound)
         vals = [_lit(typ, eval(expr, {"d": d, "i": i})) for i in range(n)]  # noqa: S307
         lines.append(f"{head} {typ} {name}(const ss_env_desc&, int i) {{ constexpr {typ} a[{n}] = {{"
                      f"{', '.join(vals)}}}; return a[i]; }}")
     for typ, name, bt, bi, expr in _LISTS["SS_CFG_ARRAYS2"]:
+        if typ == "double":
+            lines.append(f"{head} {typ} {name}(const ss_env_desc& d, int t, int i) {{ return {expr}; }}")
+            continue
         nt, ni = _bound(bt), _bound(bi)
         rows = []
         for t in range(nt):
@@ -103,13 +116,18 @@ def config_source(d) -> str:
     return "\n".join(lines)
 
 
+def block_size() -> int:
+    """Threads per block of the specialized kernel (one world per thread)."""
+    return int(os.environ.get("SS_BLOCK", "128"))
+
+
 def kernel_source(d) -> str:
     k, f = int(d.model.n_joints), int(d.model.n_feet)
     return "\n".join([
         '#include "stridesim_b200.h"',
         '#include "ss_kernel.cuh"',
         config_source(d),
-        f"extern \"C\" __global__ void __launch_bounds__(ss::kBlock) {KERNEL}(",
+        f"extern \"C\" __global__ void __launch_bounds__({block_size()}) {KERNEL}(",
         "    const __grid_constant__ ss_env_desc d, const __grid_constant__ ss_uniforms u) {",
         f"  ss::step_body<JitCfg, {max(k, 1)}, {max(f, 1)}>(d, u);",
         "}",
@@ -195,6 +213,6 @@ def module_for(d) -> int:
         except OSError:
             pass
     handle = ctypes.c_void_p()
-    native.call("ss_jit_load", cubin, len(cubin), KERNEL.encode(), ctypes.byref(handle))
+    native.call("ss_jit_load", cubin, len(cubin), KERNEL.encode(), block_size(), ctypes.byref(handle))
     _MODULES[key] = handle.value
     return handle.value

@@ -112,7 +112,8 @@ _SIGNATURES = {
          ctypes.c_void_p, ctypes.POINTER(ctypes.c_size_t), ctypes.c_char_p, ctypes.c_size_t],
         ctypes.c_int,
     ),
-    "ss_jit_load": ([ctypes.c_void_p, ctypes.c_size_t, ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
+    "ss_jit_load": ([ctypes.c_void_p, ctypes.c_size_t, ctypes.c_char_p, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)],
+                    ctypes.c_int),
     "ss_jit_unload": ([ctypes.c_void_p], ctypes.c_int),
     "ss_env_step_jit": ([ctypes.c_void_p] * 4, ctypes.c_int),
     "ss_rt_launch": ([ctypes.c_void_p] * 5, ctypes.c_int),
