@@ -286,30 +286,27 @@ def run_ours(args):
         traffic = None
 
     # end-to-end through the public API with host buffers
-    om = env.observation_manager
-    obs_dim = sum(om.group_dim(g) for g in om.groups)
     A = env.action_manager.total_dim
     rng = np.random.default_rng(rank)
     host_actions = torch.from_numpy(rng.uniform(-1, 1, size=(args.steps, n, A))).pin_memory()
-    host_obs = {g: torch.empty((n, om.group_dim(g)), dtype=torch.float64).pin_memory() for g in om.groups}
-    host_rew = torch.empty(n, dtype=torch.float64).pin_memory()
-    host_done = torch.empty((2, n), dtype=torch.bool).pin_memory()
+    # one pinned block receives every per-step result (obs groups, reward,
+    # terminated, truncated) with a single copy (env.step_outputs)
+    host_out = torch.empty(env.step_outputs.numel(), dtype=torch.uint8).pin_memory()
+    host_views = env.unpack_outputs(host_out)
     dev_actions = torch.empty((n, A), dtype=torch.float64, device="cuda")
     barrier(world)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for i in range(args.steps):
         dev_actions.copy_(host_actions[i], non_blocking=True)
-        obs, rew, term, trunc, _ = env.step(dev_actions)
-        for g in om.groups:
-            host_obs[g].copy_(obs[g], non_blocking=True)
-        host_rew.copy_(rew, non_blocking=True)
-        host_done[0].copy_(term, non_blocking=True)
-        host_done[1].copy_(trunc, non_blocking=True)
+        env.step(dev_actions)
+        host_out.copy_(env.step_outputs, non_blocking=True)
         stream.synchronize()
     e2e_t = allmax(time.perf_counter() - t0, world)
+    assert host_views["reward"].shape == (n,)
     e2e = {"value": n * world * args.steps / e2e_t, "unit": UNIT, "h2d_bytes_per_step": n * A * 8,
-           "d2h_bytes_per_step": n * obs_dim * 8 + n * 8 + 2 * n}
+           "d2h_bytes_per_step": int(env.step_outputs.numel()),
+           "path": "pinned actions -> env.step -> one copy of env.step_outputs (obs groups, reward, dones)"}
 
     if rank == 0:
         cpu = None

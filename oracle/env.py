@@ -29,6 +29,28 @@ from .rng import OracleStreams
 NEVER = -(1 << 40)  # sensors.py:51
 
 
+def _load_mlp(path):
+    """SSMLP1 container reader restated (actuators.py:140-174)."""
+    import struct
+
+    raw = open(path, "rb").read()
+    assert raw[:6] == b"SSMLP1"
+    _, n_layers = struct.unpack_from("<II", raw, 6)
+    off, layers = 14, []
+    for _ in range(n_layers):
+        (ln,) = struct.unpack_from("<B", raw, off)
+        act = raw[off + 1 : off + 1 + ln].decode()
+        off += 1 + ln
+        n_in, n_out = struct.unpack_from("<II", raw, off)
+        off += 8
+        w = np.frombuffer(raw, "<f8", n_in * n_out, off).reshape(n_out, n_in).copy()
+        off += 8 * n_in * n_out
+        b = np.frombuffer(raw, "<f8", n_out, off).copy()
+        off += 8 * n_out
+        layers.append((w, b, act))
+    return layers
+
+
 class OracleEnv:
     def __init__(self, cfg, samples=None, custom=None, capture=True):
         self.cfg = cfg
@@ -196,7 +218,7 @@ class OracleEnv:
             self.m.add_field(f"actuator.{name}.kp", np.full(len(ids), inner.kp))
             self.m.add_field(f"actuator.{name}.kd", np.full(len(ids), inner.kd))
         if inner.kind == "mlp":
-            a["mlp"] = self.custom["__mlp_layers__"][inner.weights_path]
+            a["mlp"] = _load_mlp(inner.weights_path)
             a["err"] = np.zeros((inner.error_history, self.n, len(ids)))
             a["vel"] = np.zeros((inner.velocity_history, self.n, len(ids)))
         return a

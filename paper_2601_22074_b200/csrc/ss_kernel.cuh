@@ -930,35 +930,40 @@ __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniform
         for (int j = 0; j < KM; ++j) s.targets[j] = (need_targets && j < K) ? d.targets[(int64_t)j * N + w] : 0.0;
         s.have_action = false;
         s.have_sensor = false;
-        if (st & (SS_ST_TERM | SS_ST_CURRICULUM)) {
-            s.ep_steps = d.episode_steps[w];
-            s.cmd_dist = d.commanded_distance[w];
-        }
-        if (st & (SS_ST_REWARD | SS_ST_CURRICULUM | SS_ST_RESET | SS_ST_RESET_ALL)) {
-            for_terms<C, C::kCapRewards>(0, C::n_rewards(d), [&](auto rr) {
-                const int r = ival(rr);
-                s.ep_sum[r] = d.ep_sums[(int64_t)r * N + w];
-                s.ep_rw[r] = d.ep_raw[(int64_t)r * N + w];
-            });
-        }
-        if ((st & SS_ST_COMMAND) && C::n_cmd(d) > 0) s.countdown = d.countdown[w];
-        if (st & SS_ST_EVENTS) {
-            for_terms<C, C::kCapEvents>(0, C::n_events(d), [&](auto ee) {
-                const int e = ival(ee);
-                if (C::ev_mode(d, e) == SS_MODE_INTERVAL) {
-                    s.ev_el[e] = d.event[e].elapsed[w];
-                    s.ev_tg[e] = d.event[e].target[w];
-                }
-            });
-        }
-        if (st & SS_ST_OBS) {
-            for_terms<C, C::kCapObs>(0, C::n_obs(d), [&](auto tt) {
-                const int t = ival(tt);
-                if (C::obs_noise(d, t) != SS_NOISE_NONE) s.nctr[t] = d.rng.counter[C::obs_noise_slot(d, t)][w];
-            });
-            s.plv0 = d.prev_lin_vel_b[w];
-            s.plv1 = d.prev_lin_vel_b[N + w];
-        }
+        // per-step arrays used only after the substeps: loaded just before the
+        // last substep (latency hidden behind it, registers not held through
+        // the whole physics loop)
+        auto late_prefetch = [&]() {
+            if (st & (SS_ST_TERM | SS_ST_CURRICULUM)) {
+                s.ep_steps = d.episode_steps[w];
+                s.cmd_dist = d.commanded_distance[w];
+            }
+            if (st & (SS_ST_REWARD | SS_ST_CURRICULUM | SS_ST_RESET | SS_ST_RESET_ALL)) {
+                for_terms<C, C::kCapRewards>(0, C::n_rewards(d), [&](auto rr) {
+                    const int r = ival(rr);
+                    s.ep_sum[r] = d.ep_sums[(int64_t)r * N + w];
+                    s.ep_rw[r] = d.ep_raw[(int64_t)r * N + w];
+                });
+            }
+            if ((st & SS_ST_COMMAND) && C::n_cmd(d) > 0) s.countdown = d.countdown[w];
+            if (st & SS_ST_EVENTS) {
+                for_terms<C, C::kCapEvents>(0, C::n_events(d), [&](auto ee) {
+                    const int e = ival(ee);
+                    if (C::ev_mode(d, e) == SS_MODE_INTERVAL) {
+                        s.ev_el[e] = d.event[e].elapsed[w];
+                        s.ev_tg[e] = d.event[e].target[w];
+                    }
+                });
+            }
+            if (st & SS_ST_OBS) {
+                for_terms<C, C::kCapObs>(0, C::n_obs(d), [&](auto tt) {
+                    const int t = ival(tt);
+                    if (C::obs_noise(d, t) != SS_NOISE_NONE) s.nctr[t] = d.rng.counter[C::obs_noise_slot(d, t)][w];
+                });
+                s.plv0 = d.prev_lin_vel_b[w];
+                s.plv1 = d.prev_lin_vel_b[N + w];
+            }
+        };
         Params<KM> P;
         if (sim && (st & (SS_ST_PHYS | SS_ST_APPLY))) load_params<C>(d, w, P, st & SS_ST_APPLY);
         if (!phys) refresh(s);  // staged launch: entity data from the stored state
@@ -1021,8 +1026,7 @@ __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniform
                         s.s_hist[h][i] = (need_hist && h < H && i < F) ? d.s_force_hist[((int64_t)h * F + i) * N + w] : 0.0;
             }
             const int nsub = u.nsub;
-#pragma unroll 1
-            for (int sub = 0; sub < nsub; ++sub) {
+            auto substep = [&](int sub) {
                 if (st & SS_ST_APPLY) apply_actuators<C>(d, u, w, sub, s, P);
                 if (st & SS_ST_PUSH) {
                     // CaptureRing.push (capture.py:53-59): ctrl written, pre-integration
@@ -1063,11 +1067,16 @@ __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniform
 #pragma unroll
                     for (int h = SS_MAX_HIST - 1; h >= 1; --h)
 #pragma unroll
-                        for (int i = 0; i < FM; ++i) s.s_hist[h][i] = s.s_hist[h - 1][i];
+                        for (int i = 0; i < FM; ++i)
+                            if (h < H) s.s_hist[h][i] = s.s_hist[h - 1][i];
 #pragma unroll
                     for (int i = 0; i < FM; ++i) s.s_hist[0][i] = s.fn[i];
                 }
-            }
+            };
+#pragma unroll 1
+            for (int sub = 0; sub < nsub - 1; ++sub) substep(sub);
+            late_prefetch();
+            substep(nsub - 1);
             if (sensor) {
 #pragma unroll
                 for (int i = 0; i < FM; ++i) {
@@ -1088,6 +1097,7 @@ __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniform
                         if (h < H && i < F) d.s_force_hist[((int64_t)h * F + i) * N + w] = s.s_hist[h][i];
             }
         }
+        if (!sim) late_prefetch();
         const long long sim_step_now = u.sim_step + (phys ? u.nsub : 0);
 
         // ---- 3. episode bookkeeping + TerminationManager.compute (env.py:235-239)

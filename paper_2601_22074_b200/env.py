@@ -181,11 +181,49 @@ class ManagerBasedRlEnv:
         self.observation_manager = ObservationManager(cfg.observations, self)
         self.model.on_layout_change(self._invalidate)
         self.staged = self._needs_staging()
+        self._build_output_arena()
         self.capture.bind(self._rt)
         self.contact_sensor.bind(self._rt)
         self.action_manager.bind(self._rt)
         self.observation_manager.bind(self._rt)
         self.reward_manager.weights.bind(self._rt)
+
+    def _build_output_arena(self) -> None:
+        """Place every per-step output -- the observation groups, reward,
+        terminated, truncated -- in ONE contiguous device block, so a consumer
+        on the host moves a step's results with a single copy (see
+        ``step_outputs`` / ``unpack_outputs``)."""
+        import torch
+
+        n = self.num_envs
+        om, rm, tm = self.observation_manager, self.reward_manager, self.termination_manager
+        layout = []
+        off = 0
+        for g in om.groups:
+            nbytes = n * om.group_dim(g) * 8
+            layout.append((f"obs/{g}", off, nbytes, torch.float64, (n, om.group_dim(g))))
+            off += nbytes
+        layout.append(("reward", off, n * 8, torch.float64, (n,)))
+        off += n * 8
+        layout.append(("terminated", off, n, torch.bool, (n,)))
+        off += n
+        layout.append(("truncated", off, n, torch.bool, (n,)))
+        off += n
+        self.step_outputs = torch.zeros(off, dtype=torch.uint8, device=self.device)
+        self.step_output_layout = layout
+        views = self.unpack_outputs(self.step_outputs)
+        for g in om.groups:
+            om._out[g] = views[f"obs/{g}"]
+        rm.reward = views["reward"]
+        tm.terminated = views["terminated"]
+        tm.truncated = views["truncated"]
+
+    def unpack_outputs(self, block) -> dict:
+        """Typed views into a copy of ``step_outputs`` (device or host)."""
+        out = {}
+        for name, off, nbytes, dtype, shape in self.step_output_layout:
+            out[name] = block[off : off + nbytes].view(dtype).view(shape)
+        return out
 
     def __del__(self):
         try:

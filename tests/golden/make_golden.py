@@ -142,6 +142,25 @@ def soup_cfg(n: int, seed: int):
     return cfg
 
 
+def mlp_cfg(n: int, seed: int):
+    """Velocity-Flat with an MLP actuator on the knees (actuators.py:124-180, 302-316)."""
+    from stridesim.actuators import MlpActuatorCfg, save_mlp_weights
+
+    path = os.path.join(OUT, "mlp_knee.ssmlp")
+    r = np.random.default_rng(11)
+    layers = [(r.normal(0, 0.8, (16, 4)), r.normal(0, 0.1, 16), "tanh"),
+              (r.normal(0, 0.5, (16, 16)), r.normal(0, 0.1, 16), "relu"),
+              (r.normal(0, 2.0, (1, 16)), r.normal(0, 0.1, 1), "identity")]
+    save_mlp_weights(path, layers)
+    cfg = make_env_cfg("Velocity-Flat", num_envs=n, seed=seed)
+    cfg.actions["joint_targets"].actuators = {
+        "hips": IdealPdCfg(joint_patterns=[".*_hip"], kp=40.0, kd=2.0, effort_limit=30.0),
+        "knees": MlpActuatorCfg(joint_patterns=[".*_knee"], weights_path="tests/golden/mlp_knee.ssmlp",
+                                error_history=2, velocity_history=2, effort_limit=25.0),
+    }
+    return cfg
+
+
 def physics_cases():
     out = {}
     rng = np.random.default_rng(2601)
@@ -204,6 +223,12 @@ def main():
     np.savez_compressed(os.path.join(OUT, "rollout_rough.npz"),
                         **rollout(make_env_cfg("Velocity-Rough", num_envs=16, seed=7), 60, "Velocity-Rough"))
     np.savez_compressed(os.path.join(OUT, "rollout_soup.npz"), **rollout(soup_cfg(12, 123), 60))
+    cwd = os.getcwd()
+    os.chdir(os.path.dirname(os.path.dirname(OUT)))  # weights path is repo-relative
+    try:
+        np.savez_compressed(os.path.join(OUT, "rollout_mlp.npz"), **rollout(mlp_cfg(10, 5), 40))
+    finally:
+        os.chdir(cwd)
     qcfg = make_env_cfg("Velocity-Flat", num_envs=6, seed=1)
     qcfg.scene.model = quad_spec()
     qcfg.scene.init_state.joint_pos = (0.3, -0.6, 0.3) * 4

@@ -689,3 +689,19 @@ def test_jit_specialization_bitwise_equals_generic_kernel(task):
         assert torch.equal(ra, rb) and torch.equal(ta, tb)
         assert torch.equal(a.state.q, b.state.q)
     assert jit.STATS["compiled"] + jit.STATS["disk_hits"] + jit.STATS["memory_hits"] > 0
+
+
+def test_step_outputs_arena_holds_every_result():
+    """One contiguous block (obs groups, reward, dones) for a single D2H copy."""
+    from paper_2601_22074_b200.env import ManagerBasedRlEnv
+    from paper_2601_22074_b200.policies import random_policy
+    from paper_2601_22074_b200.tasks import make_env_cfg
+
+    env = ManagerBasedRlEnv(make_env_cfg("Velocity-Rough", num_envs=64, seed=2))
+    env.reset()
+    obs, rew, term, trunc, _ = env.step(random_policy(env, 0))
+    host = env.unpack_outputs(env.step_outputs.cpu())
+    for g in obs:
+        assert torch.equal(host[f"obs/{g}"], obs[g].cpu())
+    assert torch.equal(host["reward"], rew.cpu())
+    assert torch.equal(host["terminated"], term.cpu()) and torch.equal(host["truncated"], trunc.cpu())

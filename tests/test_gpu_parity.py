@@ -73,7 +73,8 @@ FP32_ATOL = 1e-6
 SHORT = 10  # control steps of free-running "short rollout" parity
 
 
-@pytest.mark.parametrize("name", ["rollout_flat.npz", "rollout_rough.npz", "rollout_soup.npz", "rollout_quad.npz"])
+@pytest.mark.parametrize("name", ["rollout_flat.npz", "rollout_rough.npz", "rollout_soup.npz", "rollout_quad.npz",
+                                  "rollout_mlp.npz"])
 def test_short_rollout_matches_reference(name):
     """Free-running GPU env vs the reference's recorded rollout: flags exact,
     floats within the north star's fp32 tolerance for SHORT control steps
@@ -97,7 +98,8 @@ def test_short_rollout_matches_reference(name):
             _close(obs[k], g[f"obs/{k}"][i], f"obs/{k} step {i}", FP32_RTOL, FP32_ATOL)
 
 
-@pytest.mark.parametrize("name", ["rollout_flat.npz", "rollout_rough.npz", "rollout_soup.npz", "rollout_quad.npz"])
+@pytest.mark.parametrize("name", ["rollout_flat.npz", "rollout_rough.npz", "rollout_soup.npz", "rollout_quad.npz",
+                                  "rollout_mlp.npz"])
 def test_single_step_parity_every_step(name):
     """Teacher-forced lockstep with the oracle over the whole rollout: before
     each step the GPU env is loaded with the oracle's exact state, so every

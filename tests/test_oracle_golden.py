@@ -9,7 +9,7 @@ from oracle import OracleEnv, OracleModel, OracleStreams
 from oracle.physics import heights_fn, new_state, oracle_substep
 from paper_2601_22074_b200 import config as C
 
-ROLLOUTS = ["rollout_flat.npz", "rollout_rough.npz", "rollout_soup.npz", "rollout_quad.npz"]
+ROLLOUTS = ["rollout_flat.npz", "rollout_rough.npz", "rollout_soup.npz", "rollout_quad.npz", "rollout_mlp.npz"]
 
 
 def test_terrain_generation_matches_reference():
