@@ -705,3 +705,17 @@ def test_step_outputs_arena_holds_every_result():
         assert torch.equal(host[f"obs/{g}"], obs[g].cpu())
     assert torch.equal(host["reward"], rew.cpu())
     assert torch.equal(host["terminated"], term.cpu()) and torch.equal(host["truncated"], trunc.cpu())
+
+
+def test_ppo_trainer_runs_on_device():
+    from paper_2601_22074_b200.env import ManagerBasedRlEnv
+    from paper_2601_22074_b200.ppo import PpoCfg, PpoTrainer
+    from paper_2601_22074_b200.tasks import make_env_cfg
+
+    env = ManagerBasedRlEnv(make_env_cfg("Velocity-Flat", num_envs=256, seed=1))
+    tr = PpoTrainer(env, PpoCfg(hidden=(64, 64), steps_per_env=8, epochs=2, minibatches=2))
+    for _ in range(3):
+        tr.collect()
+        st = tr.update()
+    assert st["allreduces"] == 4 and np.isfinite(st["loss"])
+    assert tr.buf["obs_p"].is_cuda and tr.reducer.numel > 0

@@ -1,0 +1,80 @@
+"""Learner-side algebra on CPU (no oracle exists for PPO -- parity unpinned):
+the flat-bucket all-reduce across 2 gloo ranks equals the gradient of the
+concatenated batch on one process, and GAE matches a scalar recurrence."""
+
+import os
+import socket
+
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as tmp
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _data(seed, n):
+    g = torch.Generator().manual_seed(seed)
+    return (torch.randn(n, 6, generator=g), torch.randn(n, 8, generator=g), torch.randn(n, 3, generator=g),
+            torch.randn(n, generator=g), torch.randn(n, generator=g), torch.randn(n, generator=g))
+
+
+def _model():
+    from paper_2601_22074_b200.ppo import ActorCritic, PpoCfg
+
+    torch.manual_seed(0)
+    cfg = PpoCfg(hidden=(16, 16))
+    return ActorCritic(6, 8, 3, cfg), cfg
+
+
+def _worker(rank, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=2)
+    from paper_2601_22074_b200.ppo import FlatGradReducer, ppo_loss
+
+    model, cfg = _model()
+    loss = ppo_loss(model, cfg, *_data(rank, 32))
+    loss.backward()
+    FlatGradReducer(model).reduce()
+    if rank == 0:
+        torch.save([p.grad.clone() for p in model.parameters()], out)
+    dist.destroy_process_group()
+
+
+def test_flat_bucket_allreduce_equals_concatenated_batch(tmp_path):
+    from paper_2601_22074_b200.ppo import ppo_loss
+
+    out = str(tmp_path / "g.pt")
+    tmp.spawn(_worker, args=(_port(), out), nprocs=2, join=True)
+    got = torch.load(out)
+    model, cfg = _model()
+    # mean over two equal halves == mean of the two per-rank means
+    a, b = _data(0, 32), _data(1, 32)
+    loss = 0.5 * (ppo_loss(model, cfg, *a) + ppo_loss(model, cfg, *b))
+    loss.backward()
+    for g, p in zip(got, model.parameters()):
+        assert torch.allclose(g, p.grad, atol=1e-6, rtol=1e-5)
+
+
+def test_gae_matches_scalar_recurrence():
+    from paper_2601_22074_b200.ppo import gae
+
+    g = torch.Generator().manual_seed(3)
+    T, n = 7, 3
+    r, v = torch.randn(T, n, generator=g), torch.randn(T, n, generator=g)
+    d = (torch.rand(T, n, generator=g) < 0.2).float()
+    lv = torch.randn(n, generator=g)
+    adv, ret = gae(r, v, d, lv, 0.99, 0.95)
+    for j in range(n):
+        last = 0.0
+        for t in reversed(range(T)):
+            nv = lv[j] if t == T - 1 else v[t + 1, j]
+            delta = r[t, j] + 0.99 * nv * (1 - d[t, j]) - v[t, j]
+            last = delta + 0.99 * 0.95 * (1 - d[t, j]) * last
+            assert abs(float(adv[t, j]) - float(last)) < 1e-5
+    assert torch.allclose(ret, adv + v)
