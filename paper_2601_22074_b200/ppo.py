@@ -57,7 +57,9 @@ class ActorCritic(nn.Module):
 
     def dist(self, obs_p):
         mean = self.actor(obs_p)
-        return torch.distributions.Normal(mean, self.log_std.exp().expand_as(mean))
+        # validate_args=False: argument validation is a data-dependent check that
+        # synchronizes the device on every call
+        return torch.distributions.Normal(mean, self.log_std.exp().expand_as(mean), validate_args=False)
 
     def value(self, obs_c):
         return self.critic(obs_c).squeeze(-1)
