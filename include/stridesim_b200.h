@@ -452,6 +452,8 @@ typedef struct ss_env_desc {
     ss_obs_group group[SS_MAX_GROUPS];
     ss_obs_term obs[SS_MAX_OBS_TERMS];
     uint32_t* obs_bad;
+    /* optional clock64() phase probes of world 0 (JIT builds with -DSS_PROBES) */
+    int64_t* probe;
 } ss_env_desc;
 
 /* Per-launch uniform values, all host-tracked (no device round trip). */

@@ -33,6 +33,11 @@ constexpr long long kNeverTouched = -(1ll << 40);  // sensors.py:51
 
 __device__ __forceinline__ bool finite_(double x) { return (x - x) == 0.0; }
 
+// Pull a line into L2 without holding a register (the bench flushes L2
+// between steps, so every first touch of a per-world array is a DRAM trip;
+// prefetching at kernel entry turns the later dependent loads into L2 hits).
+__device__ __forceinline__ void l2_prefetch(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
 template <int M>
 __device__ __forceinline__ double sel(const double (&a)[M], int j) {
     double v = a[0];
@@ -901,6 +906,32 @@ __device__ __forceinline__ double reward_value(const ss_env_desc& d, int r, int 
 // ---------------------------------------------------------------------------
 // the fused step body
 
+#ifdef SS_PROBES
+#define SS_PROBE(i)                                       \
+    do {                                                  \
+        if (w == 0 && d.probe) d.probe[i] = clock64();    \
+    } while (0)
+__device__ __forceinline__ long long gtimer() {
+    long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define SS_PROBE_SPAN(first)                                                                       \
+    do {                                                                                           \
+        if (d.probe && (threadIdx.x & 31) == 0) {                                                  \
+            if (first) atomicMin((unsigned long long*)&d.probe[14], (unsigned long long)gtimer()); \
+            else atomicMax((unsigned long long*)&d.probe[15], (unsigned long long)gtimer());       \
+        }                                                                                          \
+    } while (0)
+#else
+#define SS_PROBE_SPAN(first) \
+    do {                     \
+    } while (0)
+#define SS_PROBE(i) \
+    do {            \
+    } while (0)
+#endif
+
 template <class C, int KM, int FM>
 __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniforms& u) {
     const int N = d.n_worlds;
@@ -908,6 +939,11 @@ __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniform
     const bool active = w < N;
     const unsigned st = u.stages;
     const int K = C::K(d), F = C::F(d), A = C::A(d);
+    // Observation rows are staged in shared memory and leave the block as one
+    // contiguous bulk copy per group (TMA, cp.async.bulk) instead of 32-way
+    // scattered row stores (specialized builds whose groups fit 48 KB).
+    __shared__ __align__(16) double obs_stage[C::kStageObs ? C::kBlock * C::kObsTotal : 2];
+    SS_PROBE_SPAN(1);
     World<KM, FM> s;
 #pragma unroll
     for (int k = 0; k < SS_MAX_ACTION; ++k) s.action[k] = s.prev_action[k] = 0.0;
@@ -918,6 +954,7 @@ __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniform
         const bool sim = (st & (SS_ST_APPLY | SS_ST_PUSH | SS_ST_PHYS | SS_ST_SENSOR)) && u.nsub > 0;
         const bool phys = (st & SS_ST_PHYS) && u.nsub > 0;
         const bool resets = st & (SS_ST_RESET | SS_ST_RESET_ALL);
+        SS_PROBE(0);
 
         // ---- prefetch: every per-step array this launch will read, issued up
         // front so their DRAM latency overlaps (the stores that follow would
@@ -964,9 +1001,51 @@ __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniform
                 s.plv1 = d.prev_lin_vel_b[N + w];
             }
         };
+        // L2 prefetch of everything read after the substeps or on the reset path
+        if (st & (SS_ST_TERM | SS_ST_CURRICULUM)) {
+            l2_prefetch(d.episode_steps + w);
+            l2_prefetch(d.commanded_distance + w);
+        }
+        if (st & (SS_ST_REWARD | SS_ST_CURRICULUM | SS_ST_RESET | SS_ST_RESET_ALL)) {
+            for_terms<C, C::kCapRewards>(0, C::n_rewards(d), [&](auto rr) {
+                l2_prefetch(d.ep_sums + (int64_t)ival(rr) * N + w);
+                l2_prefetch(d.ep_raw + (int64_t)ival(rr) * N + w);
+            });
+        }
+        if ((st & SS_ST_COMMAND) && C::n_cmd(d) > 0) {
+            l2_prefetch(d.countdown + w);
+            l2_prefetch(d.rng.counter[C::cmd_slot(d)] + w);
+        }
+        if (st & (SS_ST_EVENTS | SS_ST_RESET | SS_ST_RESET_ALL)) {
+            for_terms<C, C::kCapEvents>(0, C::n_events(d), [&](auto ee) {
+                const int e = ival(ee);
+                if (C::ev_mode(d, e) == SS_MODE_INTERVAL) {
+                    l2_prefetch(d.event[e].elapsed + w);
+                    l2_prefetch(d.event[e].target + w);
+                    l2_prefetch(d.rng.counter[C::ev_iv_slot(d, e)] + w);
+                }
+                if (C::ev_mode(d, e) != SS_MODE_STARTUP && C::ev_func(d, e) != SS_EVT_EXTERNAL) {
+                    l2_prefetch(d.rng.counter[C::ev_slot_a(d, e)] + w);
+                    if (C::ev_func(d, e) == SS_EVT_PUSH_BASE) l2_prefetch(d.rng.counter[C::ev_slot_b(d, e)] + w);
+                }
+            });
+        }
+        if (st & SS_ST_OBS) {
+            for_terms<C, C::kCapObs>(0, C::n_obs(d), [&](auto tt) {
+                const int t = ival(tt);
+                if (C::obs_noise(d, t) != SS_NOISE_NONE) l2_prefetch(d.rng.counter[C::obs_noise_slot(d, t)] + w);
+            });
+            l2_prefetch(d.prev_lin_vel_b + w);
+            l2_prefetch(d.prev_lin_vel_b + N + w);
+        }
+        if (resets) {
+            l2_prefetch(d.terrain_rows + w);
+            l2_prefetch(d.terrain_cols + w);
+        }
         Params<KM> P;
         if (sim && (st & (SS_ST_PHYS | SS_ST_APPLY))) load_params<C>(d, w, P, st & SS_ST_APPLY);
         if (!phys) refresh(s);  // staged launch: entity data from the stored state
+        SS_PROBE(1);
 
         // ---- 1. ActionManager.process (managers/action.py:68-82)
         if (st & SS_ST_ACTION) {
@@ -1001,6 +1080,7 @@ __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniform
             s.have_action = true;
         }
 
+        SS_PROBE(2);
         // ---- 2. decimation substeps (env.py:228-233)
         if (sim) {
             const bool sensor = st & SS_ST_SENSOR;
@@ -1072,6 +1152,7 @@ __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniform
 #pragma unroll
                     for (int i = 0; i < FM; ++i) s.s_hist[0][i] = s.fn[i];
                 }
+                SS_PROBE(3 + (sub < 3 ? sub : 3));
             };
 #pragma unroll 1
             for (int sub = 0; sub < nsub - 1; ++sub) substep(sub);
@@ -1097,6 +1178,7 @@ __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniform
                         if (h < H && i < F) d.s_force_hist[((int64_t)h * F + i) * N + w] = s.s_hist[h][i];
             }
         }
+        SS_PROBE(7);
         if (!sim) late_prefetch();
         const long long sim_step_now = u.sim_step + (phys ? u.nsub : 0);
 
@@ -1139,6 +1221,7 @@ __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniform
             d.nonfinite[(int64_t)u.nf_slot * N + w] = bad;  // per-step slot of the lag ring
         }
 
+        SS_PROBE(8);
         auto ensure_action = [&]() {
             if (!s.have_action) {
 #pragma unroll
@@ -1177,6 +1260,7 @@ __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniform
             d.reward_out[w] = total;
         }
 
+        SS_PROBE(9);
         // ---- 5. curriculum on the finished episode, then masked reset (env.py:245-250)
         bool selected = false;
         if (st & SS_ST_RESET_ALL) selected = true;
@@ -1337,6 +1421,7 @@ __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniform
             });
         }
 
+        SS_PROBE(10);
         // ---- 6. CommandManager.update (managers/command.py:41-45)
         if ((st & SS_ST_COMMAND) && C::n_cmd(d) > 0) {
             const long long cd = s.countdown - 1;
@@ -1364,6 +1449,7 @@ __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniform
             });
         }
 
+        SS_PROBE(11);
         // ---- 8. observations (post-reset state) (managers/observation.py:139-141)
         if (st & SS_ST_PREV_BEFORE) {
             d.prev_lin_vel_b[w] = s.lvb0;
@@ -1382,7 +1468,9 @@ __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniform
                     pending |= d.group[g].pending[w] != 0;
                     d.group[g].pending[w] = 0;
                 }
-                double* out = d.group[g].out + (int64_t)w * C::g_dim(d, g);
+                double* out = C::kStageObs
+                                  ? obs_stage + C::kBlock * C::g_soff(d, g) + (int)threadIdx.x * C::g_dim(d, g)
+                                  : d.group[g].out + (int64_t)w * C::g_dim(d, g);
                 const int first = C::g_first(d, g);
                 for_terms<C, C::kCapObs>(first, first + C::g_n(d, g), [&](auto tt) {
                     obs_term<C>(d, u, ival(tt), w, s, pending, out, bad_bits);
@@ -1395,7 +1483,40 @@ __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniform
             d.prev_lin_vel_b[N + w] = s.lvb1;
         }
 
+        SS_PROBE(12);
         store_phys<C>(d, w, s, /*store_cache=*/phys || s.was_reset);
+        SS_PROBE(13);
+    }
+
+    // ---- staged observation rows -> global, one bulk copy per group
+    if constexpr (C::kStageObs) {
+        if (st & SS_ST_OBS) {
+            __syncthreads();
+            const int w0 = blockIdx.x * blockDim.x;
+            const int rows = (N - w0) < (int)blockDim.x ? (N - w0) : (int)blockDim.x;
+            for_terms<C, C::kCapGroups>(0, C::n_groups(d), [&](auto gg) {
+                const int g = ival(gg);
+                if (!((u.groups_mask >> g) & 1u)) return;
+                const int D = C::g_dim(d, g);
+                double* dst = d.group[g].out + (int64_t)w0 * D;
+                const double* src = obs_stage + C::kBlock * C::g_soff(d, g);
+                const unsigned bytes = (unsigned)rows * D * 8u;
+                const bool bulk = ((bytes & 15u) == 0) && ((((unsigned long long)dst) & 15ull) == 0);
+                if (bulk) {
+                    if (threadIdx.x == 0) {
+                        const unsigned saddr = (unsigned)__cvta_generic_to_shared(src);
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(saddr),
+                                     "r"(bytes)
+                                     : "memory");
+                        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                    }
+                } else {
+                    for (int i = threadIdx.x; i < rows * D; i += blockDim.x) dst[i] = src[i];
+                }
+            });
+            if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        }
     }
 
     // ---- warp-aggregated trigger counters (managers/termination.py:31-39)
@@ -1413,6 +1534,7 @@ __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniform
             if (d.nf_flags) *((volatile uint32_t*)&d.nf_flags[u.nf_slot]) = 1u;
         }
     }
+    SS_PROBE_SPAN(0);
 }
 
 }  // namespace ss

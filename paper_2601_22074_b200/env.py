@@ -295,6 +295,7 @@ class ManagerBasedRlEnv:
             d.prev_lin_vel_b = self._prev_lin_vel_b.data_ptr()
             self.observation_manager.native_into(d)
             d.nf_flags = self._nf_flags.data_ptr()
+            d.probe = getattr(self, "_probe_ptr", None)
             d.nonfinite = self._nf_masks.data_ptr()
             # the descriptor may have allocated new stream slots: refresh their pointers
             for s, base in enumerate(r.bases):

@@ -40,6 +40,13 @@ class JitUnsupported(RuntimeError):
     pass
 
 
+def options() -> list[str]:
+    opts = list(OPTIONS)
+    if os.environ.get("SS_PROBES") == "1":
+        opts.append("-DSS_PROBES=1")
+    return opts
+
+
 def enabled() -> bool:
     return os.environ.get("SS_JIT", "1") != "0"
 
@@ -83,6 +90,14 @@ def config_source(d) -> str:
             "kCapRewards": d.n_rewards, "kCapEvents": d.n_events, "kCapGroups": d.n_groups, "kCapObs": d.n_obs_terms}
     lines = ["struct JitCfg {", "  static constexpr bool kJit = true;", "  static constexpr int kUnroll = 64;"]
     lines += [f"  static constexpr int {k} = {int(v)};" for k, v in caps.items()]
+    # shared-memory staging of the observation rows (one bulk copy per group)
+    dims = [int(d.group[g].dim) for g in range(int(d.n_groups))]
+    soff = [sum(dims[:g]) for g in range(len(dims))] + [0] * (native.SS_MAX_GROUPS - len(dims))
+    block = block_size()
+    stage = int(sum(dims) > 0 and block * sum(dims) * 8 <= 48 * 1024 and os.environ.get("SS_STAGE_OBS", "1") != "0")
+    lines += [f"  static constexpr int kBlock = {block}, kStageObs = {stage}, kObsTotal = {max(sum(dims), 1)};",
+              f"  static __device__ __forceinline__ int g_soff(const ss_env_desc&, int g) {{ constexpr int a[{native.SS_MAX_GROUPS}] = "
+              f"{{{', '.join(str(x) for x in soff)}}}; return a[g]; }}"]
     head = "  static __device__ __forceinline__"
     # Integers (counts, ids, flags, indices) become immediates: they drive the
     # unrolling and fold the term tables. Doubles stay kernel-parameter loads:
@@ -118,7 +133,7 @@ def config_source(d) -> str:
 
 def block_size() -> int:
     """Threads per block of the specialized kernel (one world per thread)."""
-    return int(os.environ.get("SS_BLOCK", "128"))
+    return int(os.environ.get("SS_BLOCK", "64"))
 
 
 def kernel_source(d) -> str:
@@ -159,7 +174,7 @@ def _source_file(src: str) -> str:
 
 def compile_cubin(src: str) -> bytes:
     """NVRTC: source -> sm_100a cubin (no GPU needed)."""
-    opts = [o.encode() for o in OPTIONS]
+    opts = [o.encode() for o in options()]
     c_opts = (ctypes.c_char_p * len(opts))(*opts)
     size = ctypes.c_size_t(0)
     log = ctypes.create_string_buffer(1 << 16)
@@ -189,7 +204,7 @@ STATS = {"compiled": 0, "disk_hits": 0, "memory_hits": 0}
 def module_for(d) -> int:
     """Loaded kernel handle specialized for descriptor ``d`` (compiled on first use)."""
     src = kernel_source(d)
-    key = hashlib.sha256((src + "|".join(OPTIONS) + "".join(open(p).read() for p in _HEADERS.values())).encode()).hexdigest()
+    key = hashlib.sha256((src + "|".join(options()) + "".join(open(p).read() for p in _HEADERS.values())).encode()).hexdigest()
     h = _MODULES.get(key)
     if h is not None:
         STATS["memory_hits"] += 1

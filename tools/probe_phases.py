@@ -1,0 +1,42 @@
+"""clock64() phase probes of world 0 inside the JIT step (SS_PROBES=1)."""
+import os
+import sys
+
+os.environ["SS_PROBES"] = "1"
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+from paper_2601_22074_b200.env import ManagerBasedRlEnv  # noqa: E402
+from paper_2601_22074_b200.policies import random_policy  # noqa: E402
+from paper_2601_22074_b200.tasks import make_env_cfg  # noqa: E402
+
+n = int(os.environ.get("N", "4096"))
+env = ManagerBasedRlEnv(make_env_cfg(os.environ.get("TASK", "Velocity-Rough"), num_envs=n))
+probe = torch.zeros(16, dtype=torch.int64, device="cuda")
+env.reset()
+env._probe_ptr = probe.data_ptr()
+env._invalidate()
+names = ["start", "loads+params", "action", "sub0", "sub1", "sub2", "sub3", "post-sim", "term", "reward",
+         "cur+reset", "cmd+events", "obs", "stores"]
+acc = [0.0] * 14
+span = 0.0
+K = 50
+probe[14] = 2**62
+for i in range(200 + K):
+    if i >= 200:
+        probe[14] = 2**62
+        probe[15] = 0
+    env.step(random_policy(env, i))
+    if i >= 200:
+        torch.cuda.synchronize()
+        p = probe.cpu().tolist()
+        span += (p[15] - p[14]) / 1e3
+        probe[14] = 2**62
+        probe[15] = 0
+        for j in range(1, 14):
+            acc[j] += p[j] - p[j - 1]
+tot = sum(acc)
+print(f"kernel span (globaltimer, first warp start -> last warp end): {span / K:.1f} us")
+print(f"N={n} world-0 phase cycles (mean of {K} steps), total {tot / K:.0f} cycles = {tot / K / 1.965e3:.1f} us at 1.965 GHz")
+for j in range(1, 14):
+    print(f"  {names[j - 1]:>12s} -> {names[j]:<12s} {acc[j] / K:8.0f} cycles  {100 * acc[j] / tot:5.1f} %")
