@@ -72,11 +72,11 @@ __global__ void __launch_bounds__(kAuxBlock) fk_kernel(const __grid_constant__ s
     const double* qr = q + (int64_t)w * nq;  // row-major (N, nq) input
     double th[SS_MAX_JOINTS], st[SS_MAX_JOINTS], ct[SS_MAX_JOINTS], ax[SS_MAX_JOINTS], az[SS_MAX_JOINTS];
     double sp, cp;
-    sincos(qr[2], &sp, &cp);
+    ss_sincos(qr[2], &sp, &cp);
     for (int j = 0; j < K; ++j) {
         const int p = m.parent[j];
         th[j] = (p == -1 ? qr[2] : th[p]) + qr[3 + j];
-        sincos(th[j], &st[j], &ct[j]);
+        ss_sincos(th[j], &st[j], &ct[j]);
     }
     for (int j = 0; j < K; ++j) {
         const int p = m.parent[j];

@@ -52,6 +52,68 @@ __device__ __forceinline__ double uniform_from_word(uint64_t w, double lo, doubl
     return lo + unit_from_word(w) * (hi - lo);
 }
 
+// ---------------------------------------------------------------------------
+// sin/cos of the planar kinematics (sim/physics.py:31-40 calls np.sin/np.cos).
+// Cody-Waite reduction by pi/2 in three FMA steps, then the fdlibm minimax
+// kernels (__kernel_sin/__kernel_cos, |err| < 1 ulp, the same accuracy class
+// as glibc and libdevice) with the polynomials in Estrin form: ~12 dependent
+// DFMA levels instead of libdevice's ~25, and no branch, so the K joint
+// angles of a substep evaluate as independent FMA chains. |x| >= 2^20, inf
+// and NaN go to libdevice's sincos (kept out of line: one copy in the code).
+static __device__ __noinline__ void sincos_slow(double x, double* s, double* c) { sincos(x, s, c); }
+
+constexpr double kSincosFastMax = 1048576.0;  // 2^20
+
+__host__ __device__ __forceinline__ void sincos_fast(double x, double* sn, double* cs) {
+    const double kMagic = 6755399441055744.0;  // 1.5 * 2^52: fma(x, 2/pi, M) - M = rint(x * 2/pi)
+    const double t = fma(x, 0.63661977236758138243, kMagic);
+    const double q = t - kMagic;
+    const long long qi = (long long)q;
+    double r = fma(-q, 1.5707963267948966e+00, x);
+    r = fma(-q, 6.1232339957367574e-17, r);
+    r = fma(-q, 8.4784276603688985e-32, r);
+    const double z = r * r, z2 = z * z;
+    // sin: r + r*z*(S1 + z*(S2 + z S3 + z^2 S4 + z^3 S5 + z^4 S6))
+    const double sa = fma(z, -1.98412698298579493134e-04, 8.33333333332248946124e-03);
+    const double sb = fma(z, -2.50507602534068634195e-08, 2.75573137070700676789e-06);
+    const double sp = fma(z2, fma(z2, 1.58969099521155010221e-10, sb), sa);
+    const double v = z * r;
+    const double s = r == 0.0 ? r : fma(v, fma(z, sp, -1.66666666666666324348e-01), r);  // sin(-0) = -0
+    // cos: w + (((1 - w) - z/2) + z^2 (C1 + z C2 + ... + z^5 C6)), w = 1 - z/2
+    const double ca = fma(z, -1.38888888888741095749e-03, 4.16666666666666019037e-02);
+    const double cb = fma(z, -2.75573143513906633035e-07, 2.48015872894767294178e-05);
+    const double cc = fma(z, -1.13596475577881948265e-11, 2.08757232129817482790e-09);
+    const double cp = fma(z2, fma(z2, cc, cb), ca);
+    const double hz = 0.5 * z, w = 1.0 - hz;
+    const double c = w + fma(z2, cp, (1.0 - w) - hz);
+    const int n = (int)(qi & 3);
+    const double ss = (n & 1) ? c : s, cc2 = (n & 1) ? s : c;
+    *sn = (n & 2) ? -ss : ss;
+    *cs = ((n + 1) & 2) ? -cc2 : cc2;
+}
+
+__device__ __forceinline__ void ss_sincos(double x, double* s, double* c) {
+    if (fabs(x) < kSincosFastMax)
+        sincos_fast(x, s, c);
+    else
+        sincos_slow(x, s, c);
+}
+
+// K angles: one range check for all of them, then K straight-line chains
+template <int K>
+__device__ __forceinline__ void ss_sincos_n(const double (&x)[K], double (&s)[K], double (&c)[K]) {
+    bool fast = true;
+#pragma unroll
+    for (int j = 0; j < K; ++j) fast = fast && fabs(x[j]) < kSincosFastMax;
+    if (fast) {
+#pragma unroll
+        for (int j = 0; j < K; ++j) sincos_fast(x[j], &s[j], &c[j]);
+    } else {
+#pragma unroll
+        for (int j = 0; j < K; ++j) sincos_slow(x[j], &s[j], &c[j]);
+    }
+}
+
 // std * sqrt(-2 log u1) * cos(2 pi u2); u1 in (0,1], u2 in [0,1)   (rng.py:114-119)
 __device__ __forceinline__ double normal_from_words(uint64_t w1, uint64_t w2, double std_) {
     const double u1 = ((double)(w1 >> 11) + 1.0) * kUnit;
@@ -116,10 +178,22 @@ __device__ __forceinline__ double np_sum(const double* a, int n) {
 // ---------------------------------------------------------------------------
 // heightfield lookup (terrain.py:159-169)
 
+// a / b correctly rounded, from y = RN(1/b) (loop-invariant): q = RN(a y),
+// then one Markstein correction q + RN(a - b q) y (the remainder is exact
+// under FMA). 3 dependent DFMA instead of DDIV's reciprocal iteration;
+// checked equal to a / b on 3e8 quotients incl. random divisors
+// (tests/test_div_rn_cpu.py). An overflowing quotient keeps RN(a y) (= inf).
+__host__ __device__ __forceinline__ double div_rn(double a, double b, double y) {
+    const double q = a * y;
+    const double q1 = fma(fma(-q, b, a), y, q);
+    return isfinite(q1) ? q1 : q;
+}
+
+
 __device__ __forceinline__ double terrain_height(const ss_terrain& t, double x) {
     if (t.flat) return 0.0;
     const int64_t last = t.n_samples - 1;
-    double pos = (isfinite(x) ? x : 0.0) / t.spacing;
+    double pos = div_rn(isfinite(x) ? x : 0.0, t.spacing, 1.0 / t.spacing);
     pos = np_clip(pos, 0.0, (double)last);
     int64_t idx = (int64_t)pos;
     if (idx > last - 1) idx = last - 1;

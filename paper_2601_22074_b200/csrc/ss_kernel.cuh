@@ -26,6 +26,10 @@
 #include "ss_device.cuh"
 #include "ss_cfg.cuh"
 
+#ifndef SS_PEEL_LAST_SUBSTEP
+#define SS_PEEL_LAST_SUBSTEP 1
+#endif
+
 namespace ss {
 
 constexpr int kBlock = 128;
@@ -96,7 +100,7 @@ __device__ __forceinline__ double height(const ss_env_desc& d, double x) {
     if (C::flat(d)) return 0.0;
     const ss_terrain& t = d.terrain;
     const int64_t last = t.n_samples - 1;
-    double pos = (finite_(x) ? x : 0.0) / t.spacing;
+    double pos = div_rn(finite_(x) ? x : 0.0, t.spacing, 1.0 / t.spacing);
     pos = np_clip(pos, 0.0, (double)last);
     int64_t idx = (int64_t)pos;
     if (idx > last - 1) idx = last - 1;
@@ -109,7 +113,7 @@ __device__ __forceinline__ double height_raw(const ss_env_desc& d, double x) {
     const ss_terrain& t = d.terrain;
     if (t.n_samples < 2) return 0.0;
     const int64_t last = t.n_samples - 1;
-    double pos = (finite_(x) ? x : 0.0) / t.spacing;
+    double pos = div_rn(finite_(x) ? x : 0.0, t.spacing, 1.0 / t.spacing);
     pos = np_clip(pos, 0.0, (double)last);
     int64_t idx = (int64_t)pos;
     if (idx > last - 1) idx = last - 1;
@@ -155,6 +159,8 @@ template <int KM>
 struct Params {
     double base_mass, base_inertia, friction;
     double lm[KM], rot[KM], dmp[KM];
+    // stage_integrate's divisors (sim/physics.py:216-224), formed once per launch
+    double m_total, inv_m, inv_inertia, inv_rot[KM];
     double kp[SS_MAX_ACTUATORS][KM], kd[SS_MAX_ACTUATORS][KM];
 };
 
@@ -232,7 +238,7 @@ __device__ __forceinline__ void store_phys(const ss_env_desc& d, int w, const Wo
 template <int KM, int FM>
 __device__ __forceinline__ void refresh(World<KM, FM>& s) {
     double sn, c;
-    sincos(s.q[2], &sn, &c);
+    ss_sincos(s.q[2], &sn, &c);
     s.sp = sn;
     s.cp = c;
     s.trig_ok = true;
@@ -269,6 +275,11 @@ __device__ __forceinline__ void load_params(const ss_env_desc& d, int w, Params<
         P.rot[j] = (j < K) ? fld<C>(d, C::f_rotor(d), j, w) : 1.0;
         P.dmp[j] = (j < K) ? fld<C>(d, C::f_damping(d), j, w) : 0.0;
     }
+    P.m_total = P.base_mass + np_sum<KM>(P.lm, K);
+    P.inv_m = 1.0 / P.m_total;
+    P.inv_inertia = 1.0 / P.base_inertia;
+#pragma unroll
+    for (int j = 0; j < KM; ++j) P.inv_rot[j] = 1.0 / P.rot[j];
     if (actuators) {
         for_terms<C, C::kCapAct>(0, C::n_act(d), [&](auto aa) {
             const int a = ival(aa);
@@ -288,9 +299,8 @@ __device__ __forceinline__ void load_params(const ss_env_desc& d, int w, Params<
 template <class C, int KM, int FM>
 __device__ __forceinline__ void phys_substep(const ss_env_desc& d, int w, World<KM, FM>& s, const Params<KM>& P) {
     const int K = C::K(d), F = C::F(d);
-    const double base_mass = P.base_mass, base_inertia = P.base_inertia, friction = P.friction;
+    const double friction = P.friction;
     const double(&lm)[KM] = P.lm;
-    const double(&rot)[KM] = P.rot;
     const double(&dmp)[KM] = P.dmp;
 
     // forward kinematics (fk_batch_trig, sim/physics.py:22-57)
@@ -299,7 +309,7 @@ __device__ __forceinline__ void phys_substep(const ss_env_desc& d, int w, World<
         sp = s.sp;
         cp = s.cp;
     } else {
-        sincos(s.q[2], &sp, &cp);
+        ss_sincos(s.q[2], &sp, &cp);
     }
     double th[KM], st[KM], ct[KM], ax[KM], az[KM], tx[KM], tz[KM];
 #pragma unroll
@@ -314,12 +324,7 @@ __device__ __forceinline__ void phys_substep(const ss_env_desc& d, int w, World<
             th[j] = pa + s.q[3 + j];
         }
     }
-#pragma unroll
-    for (int j = 0; j < KM; ++j) {
-        st[j] = 0.0;
-        ct[j] = 1.0;
-        if (j < K) sincos(th[j], &st[j], &ct[j]);
-    }
+    ss_sincos_n<KM>(th, st, ct);  // th[j >= K] = 0: sin 0, cos 1 as before
 #pragma unroll
     for (int j = 0; j < KM; ++j) {
         ax[j] = az[j] = tx[j] = tz[j] = 0.0;
@@ -389,8 +394,7 @@ __device__ __forceinline__ void phys_substep(const ss_env_desc& d, int w, World<
     for (int j = 0; j < KM; ++j) tau[3 + j] = 0.0 + s.ctrl[j];
 #pragma unroll
     for (int j = 0; j < KM; ++j) tau[3 + j] = tau[3 + j] - dmp[j] * s.qd[3 + j];
-    const double m_total = base_mass + np_sum<KM>(lm, K);
-    tau[1] = tau[1] - m_total * g;
+    tau[1] = tau[1] - P.m_total * g;
 #pragma unroll
     for (int j = 0; j < KM; ++j) tau[3 + j] = tau[3 + j] - lm[j] * g * C::half_len(d, j) * st[j];
     tau[0] = tau[0] + s.ext0;
@@ -413,12 +417,11 @@ __device__ __forceinline__ void phys_substep(const ss_env_desc& d, int w, World<
     s.ext1 = 0.0;
 
     // semi-implicit Euler (stage_integrate, sim/physics.py:216-224)
-    const double inv_m = 1.0 / m_total;
-    tau[0] = tau[0] * inv_m;
-    tau[1] = tau[1] * inv_m;
-    tau[2] = tau[2] * (1.0 / base_inertia);
+    tau[0] = tau[0] * P.inv_m;
+    tau[1] = tau[1] * P.inv_m;
+    tau[2] = tau[2] * P.inv_inertia;
 #pragma unroll
-    for (int j = 0; j < KM; ++j) tau[3 + j] = tau[3 + j] * (1.0 / rot[j]);
+    for (int j = 0; j < KM; ++j) tau[3 + j] = tau[3 + j] * P.inv_rot[j];
     const double dt = C::dt(d);
 #pragma unroll
     for (int i = 0; i < 3 + KM; ++i)
@@ -935,6 +938,7 @@ __device__ __forceinline__ long long gtimer() {
 template <class C, int KM, int FM>
 __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniforms& u) {
     const int N = d.n_worlds;
+    if ((int)(blockIdx.x * blockDim.x) >= N) return;  // padding block (grid rounded up to fill the SMs)
     const int w = blockIdx.x * blockDim.x + threadIdx.x;
     const bool active = w < N;
     const unsigned st = u.stages;
@@ -1154,10 +1158,21 @@ __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniform
                 }
                 SS_PROBE(3 + (sub < 3 ? sub : 3));
             };
+#if SS_PEEL_LAST_SUBSTEP
 #pragma unroll 1
             for (int sub = 0; sub < nsub - 1; ++sub) substep(sub);
             late_prefetch();
             substep(nsub - 1);
+#else
+            // one copy of the substep body in the code (the kernel is
+            // instruction-fetch bound when L2 is cold); the late loads are
+            // issued before the last substep from inside the loop
+#pragma unroll 1
+            for (int sub = 0; sub < nsub; ++sub) {
+                if (sub == nsub - 1) late_prefetch();
+                substep(sub);
+            }
+#endif
             if (sensor) {
 #pragma unroll
                 for (int i = 0; i < FM; ++i) {

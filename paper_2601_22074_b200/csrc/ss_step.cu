@@ -6,6 +6,7 @@
 // and load a kernel whose tables are compile-time constants (see
 // ss_cfg.cuh); ss_env_step_jit launches it. Both execute the same source,
 // ss_kernel.cuh, so their results are bitwise identical.
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -97,6 +98,7 @@ struct JitModule {
     cudaLibrary_t lib;
     cudaKernel_t kernel;
     int block;
+    int min_grid;  // experiment knob (SS_MIN_GRID): pad the grid with empty blocks
 };
 
 // Compile `src` (with named headers) for sm_100a. Returns the cubin through
@@ -136,6 +138,8 @@ extern "C" int ss_jit_load(const void* cubin, size_t size, const char* kernel_na
     (void)size;
     JitModule* m = new JitModule();
     m->block = block > 0 ? block : kBlock;
+    const char* mg = getenv("SS_MIN_GRID");
+    m->min_grid = mg ? atoi(mg) : 0;
     cudaError_t e = cudaLibraryLoadData(&m->lib, cubin, nullptr, nullptr, 0, nullptr, nullptr, 0);
     if (e != cudaSuccess) {
         delete m;
@@ -164,7 +168,9 @@ extern "C" int ss_env_step_jit(void* handle, const ss_env_desc* desc, const ss_u
     if (desc->n_worlds <= 0) return 0;
     JitModule* m = (JitModule*)handle;
     void* args[2] = {(void*)desc, (void*)u};
-    const dim3 grid((desc->n_worlds + m->block - 1) / m->block);
+    int blocks = (desc->n_worlds + m->block - 1) / m->block;
+    if (blocks < m->min_grid) blocks = m->min_grid;
+    const dim3 grid(blocks);
     cudaError_t e = cudaLaunchKernel((const void*)m->kernel, grid, dim3(m->block), args, 0, (cudaStream_t)stream);
     if (e != cudaSuccess) return ss_fail("ss_env_step_jit launch", e);
     return 0;

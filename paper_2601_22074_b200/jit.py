@@ -44,6 +44,8 @@ def options() -> list[str]:
     opts = list(OPTIONS)
     if os.environ.get("SS_PROBES") == "1":
         opts.append("-DSS_PROBES=1")
+    # experiment switches, e.g. SS_JIT_DEFINES="-DSS_PEEL_LAST_SUBSTEP=0"
+    opts += os.environ.get("SS_JIT_DEFINES", "").split()
     return opts
 
 
