@@ -5,9 +5,12 @@
 
 Workload (BASELINE.json configs[1] restated): Velocity-Rough,
 the planar biped on the 5x6 curriculum heightfield, 4096 worlds per GPU,
-decimation 4, random actions from the per-world streams generated on device
-(policies.random_policy, inside the timed region like cli.py:163). One step
-= one control step of every world (4 physics substeps each). Multi-GPU: one
+decimation 4, random actions from the per-world policy.random streams, drawn
+inside the timed region like cli.py:163 -- by the step kernel itself
+(policies.RandomActions; the same values as random_policy's separate draw,
+tests/test_gpu_env_api.py). One step = one control step of every world (4
+physics substeps each) = one kernel launch. --scale-envs adds the same step
+at 262144 worlds, where the working set streams from HBM. Multi-GPU: one
 process per GPU, world_id_offset = rank * N (weak scaling, no collective on
 the data path); time = max over ranks.
 
@@ -222,6 +225,52 @@ def allmax(x: float, world: int) -> float:
     return float(t.item())
 
 
+def timed_steps(env, steps: int, flush, stream, policy) -> float:
+    """Seconds of GPU time for `steps` env steps, each preceded by an L2 flush
+    (untimed) and bracketed by CUDA events on the launching stream."""
+    import torch
+
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    torch.cuda.synchronize()
+    for i in range(steps):
+        flush.fill_(float(i))  # evict L2 (126 MB) between timed iterations (untimed)
+        e0, e1 = evs[i]
+        e0.record(stream)
+        env.step(policy(i))
+        e1.record(stream)
+        if i >= 2:
+            # bound the host's lead to two iterations: the flush of the next
+            # iteration gives the host time to enqueue the step before the GPU
+            # reaches e0, so the events time GPU work only
+            evs[i - 2][1].synchronize()
+    torch.cuda.synchronize()
+    return sum(e0.elapsed_time(e1) for e0, e1 in evs) / 1e3
+
+
+def at_scale(args, flush, stream) -> dict:
+    """The same step at a world count past the L2 (the roofline
+    fraction is quoted where the working set streams from HBM)."""
+    from paper_2601_22074_b200.env import ManagerBasedRlEnv
+    from paper_2601_22074_b200.policies import random_policy
+    from paper_2601_22074_b200.tasks import make_env_cfg
+    from paper_2601_22074_b200.traffic import step_bytes_per_world
+
+    n = args.scale_envs
+    env = ManagerBasedRlEnv(make_env_cfg(args.task, num_envs=n, seed=args.seed), args.task)
+    env.reset()
+    for i in range(5):
+        env.step(random_policy(env, i, fused=True))
+    steps = 20
+    t = timed_steps(env, steps, flush, stream, lambda i: random_policy(env, 5 + i, fused=True))
+    per_world = step_bytes_per_world(env, fused_policy=True)["total"]
+    peak, _ = _peaks()
+    gbs = per_world * n * steps / t / 1e9
+    out = {"envs": n, "value": n * steps / t, "unit": UNIT, "ms_per_step": 1e3 * t / steps,
+           "achieved_gbs": gbs, "frac": gbs / peak, "bytes_per_env_step": per_world}
+    del env
+    return out
+
+
 def run_ours(args):
     import torch
 
@@ -235,7 +284,7 @@ def run_ours(args):
     from paper_2601_22074_b200.env import ManagerBasedRlEnv
     from paper_2601_22074_b200.policies import random_policy
     from paper_2601_22074_b200.tasks import make_env_cfg
-    from paper_2601_22074_b200.traffic import policy_bytes_per_world, step_bytes_per_world
+    from paper_2601_22074_b200.traffic import step_bytes_per_world
 
     n = args.envs
     cfg = make_env_cfg(args.task, num_envs=n, seed=args.seed)
@@ -245,40 +294,25 @@ def run_ours(args):
     stream = torch.cuda.current_stream()
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
+    # the benchmark loop of the reference (cli.py:163): env.step(random_policy(env));
+    # fused=True draws the same actions (stream policy.random) inside the step kernel
     for i in range(args.warmup):
-        env.step(random_policy(env, i))
+        env.step(random_policy(env, i, fused=True))
     torch.cuda.synchronize()
 
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
-            torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     clocks = Clocks(local)
     barrier(world)
-    torch.cuda.synchronize()
     launches0 = native.LAUNCHES["count"]
-    for i in range(args.steps):
-        flush.fill_(float(i))  # evict L2 (126 MB) between timed iterations (untimed)
-        e0, e1, e2 = evs[i]
-        e0.record(stream)
-        a = random_policy(env, args.warmup + i)
-        e1.record(stream)
-        env.step(a)
-        e2.record(stream)
-        if i >= 2:
-            # bound the host's lead to two iterations: the flush of the next
-            # iteration gives the host time to enqueue the step before the GPU
-            # reaches e0, so the events time GPU work only
-            evs[i - 2][2].synchronize()
-    torch.cuda.synchronize()
+    t_step = timed_steps(env, args.steps, flush, stream, lambda i: random_policy(env, args.warmup + i, fused=True))
     barrier(world)
     launches = native.LAUNCHES["count"] - launches0
     clk = clocks.stop()
-    t_step = sum(e0.elapsed_time(e2) for e0, _, e2 in evs) / 1e3
-    t_kernel = sum(e1.elapsed_time(e2) for _, e1, e2 in evs) / 1e3
+    t_kernel = t_step  # one launch per step: the fused step kernel is the whole step
     t_max = allmax(t_step, world)
     value = n * world * args.steps / t_max
 
     # roofline of the dominant kernel (the fused step)
-    per_world = step_bytes_per_world(env)
+    per_world = step_bytes_per_world(env, fused_policy=True)
     peak, peak_kind = _peaks()
     achieved = per_world["total"] * n / (t_kernel / args.steps) / 1e9
     traffic, traffic_envs = _ncu_traffic()
@@ -308,6 +342,8 @@ def run_ours(args):
            "d2h_bytes_per_step": int(env.step_outputs.numel()),
            "path": "pinned actions -> env.step -> one copy of env.step_outputs (obs groups, reward, dones)"}
 
+    scale = at_scale(args, flush, stream) if (world == 1 and args.scale_envs > 0) else None
+
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu:
@@ -335,7 +371,8 @@ def run_ours(args):
                          "kernel": "ss_step_jit (fused control step, per-env NVRTC specialization)"
                          if env.use_jit else "step_kernel<4,2> (fused control step, generic)",
                          "kernel_ms": 1e3 * t_kernel / args.steps},
-            "policy_bytes_per_env_step": policy_bytes_per_world(env),
+            "policy": "random_policy fused into the step kernel (policies.RandomActions: same stream and values)",
+            "at_scale": scale,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
@@ -395,6 +432,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--scale-envs", type=int, default=262144,
+                    help="also time the step at this many worlds (HBM-bound regime); 0 disables")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -60,7 +60,7 @@ typedef unsigned long long uint64_t;
 extern "C" {
 #endif
 
-#define SS_ABI_VERSION 1
+#define SS_ABI_VERSION 2
 
 #define SS_MAX_JOINTS 16
 #define SS_MAX_FEET 8
@@ -474,6 +474,13 @@ typedef struct ss_uniforms {
     double weight[SS_MAX_REWARDS];
     const double* actions;
     const uint8_t* reset_mask;
+    /* fused random policy (policies.py:14-16): policy_slot >= 0 makes the
+     * ACTION stage draw U[policy_lo, policy_hi) from that stream slot instead
+     * of reading `actions` */
+    int32_t policy_slot;
+    int32_t policy_pad;
+    double policy_lo;
+    double policy_hi;
 } ss_uniforms;
 
 /* Host-side runtime state of one env: every per-launch uniform (step
@@ -524,6 +531,10 @@ typedef struct ss_launch {
     uint32_t groups_mask;
     const double* actions;
     const uint8_t* reset_mask;
+    int32_t policy_slot;
+    int32_t policy_pad;
+    double policy_lo;
+    double policy_hi;
 } ss_launch;
 
 /* One draw call of StreamPack.uniform/normal (rng.py:69-119). sel == NULL

@@ -1053,14 +1053,24 @@ __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniform
 
         // ---- 1. ActionManager.process (managers/action.py:68-82)
         if (st & SS_ST_ACTION) {
-            const double* a = u.actions + (int64_t)w * A;
+            if (u.policy_slot >= 0) {
+                // fused random_policy (policies.py:14-16): U[lo, hi) from the
+                // policy stream, the same words ss_rng_draw would produce
+                uint64_t key;
+                const uint64_t c = rng_begin(d, u.policy_slot, w, key);
 #pragma unroll
-            for (int k = 0; k < SS_MAX_ACTION; ++k) {
-                if (k < A) {
-                    s.prev_action[k] = d.action[(int64_t)k * N + w];
-                    s.action[k] = a[k];
-                }
+                for (int k = 0; k < SS_MAX_ACTION; ++k)
+                    if (k < A) s.action[k] = uniform_from_word(stream_word(key, c, k), u.policy_lo, u.policy_hi);
+                rng_end(d, u.policy_slot, w, c + (uint64_t)A);
+            } else {
+                const double* a = u.actions + (int64_t)w * A;
+#pragma unroll
+                for (int k = 0; k < SS_MAX_ACTION; ++k)
+                    if (k < A) s.action[k] = a[k];
             }
+#pragma unroll
+            for (int k = 0; k < SS_MAX_ACTION; ++k)
+                if (k < A) s.prev_action[k] = d.action[(int64_t)k * N + w];
 #pragma unroll
             for (int k = 0; k < SS_MAX_ACTION; ++k) {
                 if (k < A) {

@@ -69,6 +69,10 @@ extern "C" int ss_rt_launch(const ss_env_desc* d, ss_rt_state* st, const ss_laun
     for (int r = 0; r < st->n_rewards; ++r) u.weight[r] = st->weight[r];
     u.actions = l->actions;
     u.reset_mask = l->reset_mask;
+    u.policy_slot = l->policy_slot;
+    u.policy_pad = 0;
+    u.policy_lo = l->policy_lo;
+    u.policy_hi = l->policy_hi;
     int slot = -1;
     if (stages & SS_ST_TERM) {
         if (st->nf_pending >= st->nf_slots) {

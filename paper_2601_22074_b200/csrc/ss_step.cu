@@ -75,6 +75,15 @@ static int check_desc(const ss_env_desc* desc, const ss_uniforms* u, const char*
         snprintf(g_err, sizeof(g_err), "%s: model exceeds compiled limits", who);
         return -4;
     }
+    if ((u->stages & SS_ST_ACTION) && u->policy_slot < 0 && !u->actions) {
+        snprintf(g_err, sizeof(g_err), "%s: ACTION stage without actions or a policy stream", who);
+        return -5;
+    }
+    if (u->policy_slot >= SS_MAX_SLOTS || ((u->stages & SS_ST_ACTION) && u->policy_slot >= 0 &&
+                                           !desc->rng.counter[u->policy_slot])) {
+        snprintf(g_err, sizeof(g_err), "%s: policy stream slot %d not allocated", who, u->policy_slot);
+        return -6;
+    }
     return 0;
 }
 

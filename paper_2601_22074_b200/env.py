@@ -26,6 +26,7 @@ import numpy as np
 from . import mdp  # noqa: F401  (registers the built-in terms)
 from . import jit, native
 from .capture import CaptureRing, dump_capture, load_capture, model_field_metadata
+from .policies import RandomActions
 from .config import ContactSensorCfg, EnvCfg, InitStateCfg, SceneCfg, config_hash, to_dict
 from .entity import DefaultState, Entity, EntityData
 from .managers import (
@@ -310,6 +311,8 @@ class ManagerBasedRlEnv:
         """One launch through the native runtime (ss_rt_launch): it derives the
         per-step uniforms from the shared ss_rt_state, launches the
         specialized (or generic) kernel and advances the counters."""
+        if isinstance(actions, RandomActions):
+            slot = self.streams.slot("policy.random")  # first use invalidates the descriptor
         d = self._desc if self._desc is not None else self._get_desc()
         if self._desc is None:  # a stream slot was allocated while building
             d = self._get_desc()
@@ -329,7 +332,12 @@ class ManagerBasedRlEnv:
         la.nsub = nsub
         la.flags = flags
         la.groups_mask = groups_mask
-        la.actions = None if actions is None else actions.data_ptr()
+        if isinstance(actions, RandomActions):
+            la.actions = None
+            la.policy_slot, la.policy_lo, la.policy_hi = slot, float(actions.low), float(actions.high)
+        else:
+            la.actions = None if actions is None else actions.data_ptr()
+            la.policy_slot = -1
         la.reset_mask = None if reset_mask is None else reset_mask.data_ptr()
         rt.sim_step = self.state.sim_step
         native.LAUNCHES["count"] += 1

@@ -138,13 +138,19 @@ def block_size() -> int:
     return int(os.environ.get("SS_BLOCK", "64"))
 
 
+def min_blocks() -> int:
+    """__launch_bounds__ min blocks per SM (0: let ptxas use every register)."""
+    return int(os.environ.get("SS_MINB", "0"))
+
+
 def kernel_source(d) -> str:
     k, f = int(d.model.n_joints), int(d.model.n_feet)
     return "\n".join([
         '#include "stridesim_b200.h"',
         '#include "ss_kernel.cuh"',
         config_source(d),
-        f"extern \"C\" __global__ void __launch_bounds__({block_size()}) {KERNEL}(",
+        f"extern \"C\" __global__ void __launch_bounds__({block_size()}"
+        f"{', ' + str(min_blocks()) if min_blocks() else ''}) {KERNEL}(",
         "    const __grid_constant__ ss_env_desc d, const __grid_constant__ ss_uniforms u) {",
         f"  ss::step_body<JitCfg, {max(k, 1)}, {max(f, 1)}>(d, u);",
         "}",

@@ -81,6 +81,10 @@ class ActionManager:
         """Validate and stage a (N, total_dim) float64 CUDA tensor."""
         import torch
 
+        from ..policies import RandomActions
+
+        if isinstance(actions, RandomActions):
+            return actions
         if torch.is_tensor(actions):
             a = actions
         else:

@@ -13,7 +13,9 @@ from __future__ import annotations
 F64, I64, U8, U32, U64 = 8, 8, 1, 4, 8
 
 
-def step_bytes_per_world(env) -> dict:
+def step_bytes_per_world(env, fused_policy: bool = False) -> dict:
+    """``fused_policy``: the step draws its actions from stream policy.random
+    (policies.RandomActions) instead of reading an (N, A) action row."""
     m = env.model
     k, nq, nf = m.num_joints, m.nq, len(m.feet)
     d = env.decimation
@@ -32,7 +34,11 @@ def step_bytes_per_world(env) -> dict:
     n_exp = sum(f.size for f in m._fields.values() if f.expanded)
     rd["expanded fields"] = F64 * n_exp
     # actions: input row, previous action -> prev, action; targets
-    rd["actions in + action"] = F64 * (2 * A)
+    if fused_policy:
+        rd["policy counter + action"] = U64 + F64 * A
+        wr["policy counter"] = U64
+    else:
+        rd["actions in + action"] = F64 * (2 * A)
     wr["action, prev, targets"] = F64 * (2 * A + k)
     # delayed actuators: ring push + read per substep, delays
     for a in am.actuators:

@@ -719,3 +719,42 @@ def test_ppo_trainer_runs_on_device():
         st = tr.update()
     assert st["allreduces"] == 4 and np.isfinite(st["loss"])
     assert tr.buf["obs_p"].is_cuda and tr.reducer.numel > 0
+
+
+@pytest.mark.parametrize("mode", ["jit", "generic", "staged"])
+def test_fused_random_policy_equals_separate_draw(mode):
+    """env.step(RandomActions()) draws policy.random inside the step kernel:
+    actions, stream counters and every output equal the two-launch form
+    env.step(random_policy(env)) bit for bit (policies.py:14-16)."""
+    from paper_2601_22074_b200.config import RewardTermCfg
+    from paper_2601_22074_b200.env import ManagerBasedRlEnv
+    from paper_2601_22074_b200.managers import reward_term
+    from paper_2601_22074_b200.policies import random_policy
+    from paper_2601_22074_b200.tasks import make_env_cfg
+
+    @reward_term("test_host_const_reward")
+    def _const(env):
+        return np.full(env.num_envs, 0.5)
+
+    def make():
+        cfg = make_env_cfg("Velocity-Rough", num_envs=257, seed=11)
+        if mode == "staged":
+            cfg.rewards["host"] = RewardTermCfg(func="test_host_const_reward", weight=1.0)
+        e = ManagerBasedRlEnv(cfg)
+        if mode == "generic":
+            e.use_jit = False
+        return e
+
+    a, b = make(), make()
+    assert a.staged == (mode == "staged")
+    a.reset()
+    b.reset()
+    for i in range(30):
+        oa, ra, ta, xa, _ = a.step(random_policy(a, i))
+        ob, rb, tb, xb, _ = b.step(random_policy(b, i, fused=True))
+        assert torch.equal(a.action_manager.action, b.action_manager.action), i
+        for k in oa:
+            assert torch.equal(oa[k], ob[k]), (i, k)
+        assert torch.equal(ra, rb) and torch.equal(ta, tb) and torch.equal(xa, xb)
+    assert torch.equal(a.streams.counter("policy.random"), b.streams.counter("policy.random"))
+    assert torch.equal(a.state.q, b.state.q) and torch.equal(a.state.qd, b.state.qd)

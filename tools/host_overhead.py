@@ -45,3 +45,37 @@ for i in range(200):
 pr.disable()
 torch.cuda.synchronize()
 pstats.Stats(pr).sort_stats("tottime").print_stats(18)
+
+# ---- end-to-end loop breakdown (bench.py e2e: pinned H2D -> step -> one D2H of step_outputs)
+import numpy as np  # noqa: E402
+
+A = env.action_manager.total_dim
+host_actions = torch.from_numpy(np.random.default_rng(0).uniform(-1, 1, size=(n, A))).pin_memory()
+host_out = torch.empty(env.step_outputs.numel(), dtype=torch.uint8).pin_memory()
+dev_actions = torch.empty((n, A), dtype=torch.float64, device="cuda")
+stream = torch.cuda.current_stream()
+
+
+def timed(label, fn, k=300):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(k):
+        fn()
+    torch.cuda.synchronize()
+    print(f"{label:<40s} {1e6 * (time.perf_counter() - t0) / k:7.1f} us")
+
+
+timed("H2D actions + sync", lambda: (dev_actions.copy_(host_actions, non_blocking=True), stream.synchronize()))
+timed("D2H step_outputs + sync", lambda: (host_out.copy_(env.step_outputs, non_blocking=True), stream.synchronize()))
+timed("step + sync", lambda: (env.step(dev_actions), stream.synchronize()))
+timed("e2e (H2D, step, D2H, sync)", lambda: (dev_actions.copy_(host_actions, non_blocking=True), env.step(dev_actions),
+                                             host_out.copy_(env.step_outputs, non_blocking=True), stream.synchronize()))
+t0 = time.perf_counter()
+for _ in range(300):
+    dev_actions.copy_(host_actions, non_blocking=True)
+    env.step(dev_actions)
+    host_out.copy_(env.step_outputs, non_blocking=True)
+t1 = time.perf_counter()
+torch.cuda.synchronize()
+print(f"{'e2e host enqueue only':<40s} {1e6 * (t1 - t0) / 300:7.1f} us")
+print("D2H bytes", env.step_outputs.numel())

@@ -22,7 +22,10 @@ acc = [0.0] * 14
 span = 0.0
 K = 50
 probe[14] = 2**62
+flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda") if os.environ.get("FLUSH") else None
 for i in range(200 + K):
+    if flush is not None:
+        flush.fill_(float(i))  # cold L2 (as bench.py): code and data come from HBM
     if i >= 200:
         probe[14] = 2**62
         probe[15] = 0
