@@ -10,6 +10,7 @@
 
 #ifndef __CUDACC_RTC__
 #include <cstdint>
+#include <cstring>
 #include <cuda_runtime.h>
 
 #include "../../include/stridesim_b200.h"
@@ -64,11 +65,33 @@ static __device__ __noinline__ void sincos_slow(double x, double* s, double* c) 
 
 constexpr double kSincosFastMax = 1048576.0;  // 2^20
 
+__host__ __device__ __forceinline__ unsigned lo_word(double v) {
+#ifdef __CUDA_ARCH__
+    return (unsigned)__double2loint(v);
+#else
+    unsigned long long b;
+    memcpy(&b, &v, 8);
+    return (unsigned)b;
+#endif
+}
+
+// v with its sign bit xor-ed by `flip` (0 or 0x80000000 on the high word)
+__host__ __device__ __forceinline__ double flip_sign(double v, unsigned flip) {
+#ifdef __CUDA_ARCH__
+    return __hiloint2double(__double2hiint(v) ^ (int)flip, __double2loint(v));
+#else
+    unsigned long long b;
+    memcpy(&b, &v, 8);
+    b ^= (unsigned long long)flip << 32;
+    memcpy(&v, &b, 8);
+    return v;
+#endif
+}
+
 __host__ __device__ __forceinline__ void sincos_fast(double x, double* sn, double* cs) {
     const double kMagic = 6755399441055744.0;  // 1.5 * 2^52: fma(x, 2/pi, M) - M = rint(x * 2/pi)
     const double t = fma(x, 0.63661977236758138243, kMagic);
     const double q = t - kMagic;
-    const long long qi = (long long)q;
     double r = fma(-q, 1.5707963267948966e+00, x);
     r = fma(-q, 6.1232339957367574e-17, r);
     r = fma(-q, 8.4784276603688985e-32, r);
@@ -86,10 +109,12 @@ __host__ __device__ __forceinline__ void sincos_fast(double x, double* sn, doubl
     const double cp = fma(z2, fma(z2, cc, cb), ca);
     const double hz = 0.5 * z, w = 1.0 - hz;
     const double c = w + fma(z2, cp, (1.0 - w) - hz);
-    const int n = (int)(qi & 3);
-    const double ss = (n & 1) ? c : s, cc2 = (n & 1) ? s : c;
-    *sn = (n & 2) ? -ss : ss;
-    *cs = ((n + 1) & 2) ? -cc2 : cc2;
+    // quadrant q mod 4 sits in the low bits of t (its ulp is 1); the result is
+    // a swap plus sign-bit flips on the high words (no FP negations/selects)
+    const unsigned n = lo_word(t) & 3u;
+    const bool swap = n & 1u;
+    *sn = flip_sign(swap ? c : s, (n & 2u) << 30);
+    *cs = flip_sign(swap ? s : c, ((n + 1u) & 2u) << 30);
 }
 
 __device__ __forceinline__ void ss_sincos(double x, double* s, double* c) {

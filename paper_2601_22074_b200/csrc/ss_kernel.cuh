@@ -92,7 +92,7 @@ __device__ __forceinline__ void for_terms(int lo, int hi, F f) {
 template <class C>
 __device__ __forceinline__ double fld(const ss_env_desc& d, int f, int c, int w) {
     const double* p = d.field[f].ptr;
-    return C::fexp(d, f) ? p[(int64_t)c * d.n_worlds + w] : p[c];
+    return C::fexp(d, f) ? p[(int64_t)c * C::NW(d) + w] : p[c];
 }
 
 template <class C>
@@ -177,7 +177,7 @@ __device__ __forceinline__ void rng_end(const ss_env_desc& d, int slot, int w, u
 
 template <class C, int KM, int FM>
 __device__ __forceinline__ void load_phys(const ss_env_desc& d, int w, World<KM, FM>& s, bool load_cache) {
-    const int N = d.n_worlds, K = C::K(d), F = C::F(d);
+    const int N = C::NW(d), K = C::K(d), F = C::F(d);
 #pragma unroll
     for (int i = 0; i < 3 + KM; ++i) {
         s.q[i] = (i < 3 + K) ? d.state.q[(int64_t)i * N + w] : 0.0;
@@ -204,7 +204,7 @@ __device__ __forceinline__ void load_phys(const ss_env_desc& d, int w, World<KM,
 
 template <class C, int KM, int FM>
 __device__ __forceinline__ void store_phys(const ss_env_desc& d, int w, const World<KM, FM>& s, bool store_cache) {
-    const int N = d.n_worlds, K = C::K(d), F = C::F(d);
+    const int N = C::NW(d), K = C::K(d), F = C::F(d);
 #pragma unroll
     for (int i = 0; i < 3 + KM; ++i) {
         if (i < 3 + K) {
@@ -493,7 +493,7 @@ __device__ __noinline__ double mlp_torque(const ss_env_desc& d, int a, int i, in
 template <class C, int KM, int FM>
 __device__ __forceinline__ void apply_actuators(const ss_env_desc& d, const ss_uniforms& u, int w, int sub,
                                                 World<KM, FM>& s, const Params<KM>& P) {
-    const int N = d.n_worlds;
+    const int N = C::NW(d);
     for_terms<C, C::kCapAct>(0, C::n_act(d), [&](auto aa) {
         const int a = ival(aa);
         long long delay = 0;
@@ -544,7 +544,7 @@ __device__ __forceinline__ void apply_actuators(const ss_env_desc& d, const ss_u
 // Actuator.reset (actuators.py:269-277) for one world
 template <class C, int KM>
 __device__ __forceinline__ void reset_actuators(const ss_env_desc& d, int w, const double (&targets)[KM]) {
-    const int N = d.n_worlds;
+    const int N = C::NW(d);
     for (int a = 0; a < C::n_act(d); ++a) {
         const ss_actuator& A = d.actuator[a];
         if (C::act_delayed(d, a)) {
@@ -583,7 +583,7 @@ __device__ __forceinline__ void reset_actuators(const ss_env_desc& d, int w, con
 template <class C>
 __device__ __forceinline__ void randomize_world(const ss_env_desc& d, int w, int field, int dist, double r0,
                                                 double r1, int op, int slot) {
-    const int N = d.n_worlds;
+    const int N = C::NW(d);
     const int size = C::fsize(d, field);
     double* ptr = d.field[field].ptr;
     uint64_t key;
@@ -647,7 +647,7 @@ __device__ __forceinline__ void apply_event(const ss_env_desc& d, int e, int w, 
 // CommandManager.resample for one world (managers/command.py:33-39)
 template <class C, int KM, int FM>
 __device__ __forceinline__ void resample_command(const ss_env_desc& d, int w, World<KM, FM>& s) {
-    const int N = d.n_worlds;
+    const int N = C::NW(d);
     uint64_t key;
     const int slot = C::cmd_slot(d);
     const uint64_t c = rng_begin(d, slot, w, key);
@@ -672,7 +672,7 @@ constexpr int kObsMax = SS_MAX_JOINTS > 2 * SS_MAX_FEET ? SS_MAX_JOINTS : 2 * SS
 template <class C, int KM, int FM>
 __device__ __forceinline__ void obs_raw(const ss_env_desc& d, int t, int w, const World<KM, FM>& s,
                                         double (&v)[kObsMax]) {
-    const int N = d.n_worlds, K = C::K(d), F = C::F(d);
+    const int N = C::NW(d), K = C::K(d), F = C::F(d);
     switch (C::obs_func(d, t)) {
         case SS_OBS_BASE_LIN_VEL:
             v[0] = s.lvb0;
@@ -741,7 +741,7 @@ __device__ __forceinline__ void obs_raw(const ss_env_desc& d, int t, int w, cons
 template <class C, int KM, int FM>
 __device__ __forceinline__ void obs_term(const ss_env_desc& d, const ss_uniforms& u, int t, int w,
                                          World<KM, FM>& s, bool pending, double* out, unsigned& bad_bits) {
-    const int N = d.n_worlds;
+    const int N = C::NW(d);
     double v[kObsMax];
     obs_raw<C>(d, t, w, s, v);
     const int dim = C::obs_dim(d, t);
@@ -937,7 +937,7 @@ __device__ __forceinline__ long long gtimer() {
 
 template <class C, int KM, int FM>
 __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniforms& u) {
-    const int N = d.n_worlds;
+    const int N = C::NW(d);
     if ((int)(blockIdx.x * blockDim.x) >= N) return;  // padding block (grid rounded up to fill the SMs)
     const int w = blockIdx.x * blockDim.x + threadIdx.x;
     const bool active = w < N;
@@ -1046,6 +1046,42 @@ __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniform
             l2_prefetch(d.terrain_rows + w);
             l2_prefetch(d.terrain_cols + w);
         }
+        // action inputs and contact-sensor state: loaded here, ahead of the
+        // ACTION stage's stores (which would otherwise order them behind)
+        uint64_t pol_key = 0, pol_c = 0;
+        if (st & SS_ST_ACTION) {
+#pragma unroll
+            for (int k = 0; k < SS_MAX_ACTION; ++k)
+                if (k < A) s.prev_action[k] = d.action[(int64_t)k * N + w];
+            if (u.policy_slot >= 0) {
+                pol_c = rng_begin(d, u.policy_slot, w, pol_key);
+            } else {
+                const double* a = u.actions + (int64_t)w * A;
+#pragma unroll
+                for (int k = 0; k < SS_MAX_ACTION; ++k)
+                    if (k < A) s.action[k] = a[k];
+            }
+        }
+        if (sim && (st & SS_ST_SENSOR)) {
+#pragma unroll
+            for (int i = 0; i < FM; ++i) {
+                const bool ok = i < F;
+                s.s_in[i] = ok ? d.s_in_contact[(int64_t)i * N + w] != 0 : false;
+                s.s_air[i] = ok ? d.s_cur_air[(int64_t)i * N + w] : 0.0;
+                s.s_last_air[i] = ok ? d.s_last_air[(int64_t)i * N + w] : 0.0;
+                s.s_contact[i] = ok ? d.s_cur_contact[(int64_t)i * N + w] : 0.0;
+                s.s_td[i] = ok ? d.s_last_td[(int64_t)i * N + w] : kNeverTouched;
+            }
+            // the force history is fully overwritten when >= H updates run
+            const int H = C::hist_len(d);
+            const int n_upd = __popc(u.sensor_mask & ((1u << u.nsub) - 1u));
+            const bool need_hist = n_upd < H;
+#pragma unroll
+            for (int h = 0; h < SS_MAX_HIST; ++h)
+#pragma unroll
+                for (int i = 0; i < FM; ++i)
+                    s.s_hist[h][i] = (need_hist && h < H && i < F) ? d.s_force_hist[((int64_t)h * F + i) * N + w] : 0.0;
+        }
         Params<KM> P;
         if (sim && (st & (SS_ST_PHYS | SS_ST_APPLY))) load_params<C>(d, w, P, st & SS_ST_APPLY);
         if (!phys) refresh(s);  // staged launch: entity data from the stored state
@@ -1056,21 +1092,11 @@ __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniform
             if (u.policy_slot >= 0) {
                 // fused random_policy (policies.py:14-16): U[lo, hi) from the
                 // policy stream, the same words ss_rng_draw would produce
-                uint64_t key;
-                const uint64_t c = rng_begin(d, u.policy_slot, w, key);
 #pragma unroll
                 for (int k = 0; k < SS_MAX_ACTION; ++k)
-                    if (k < A) s.action[k] = uniform_from_word(stream_word(key, c, k), u.policy_lo, u.policy_hi);
-                rng_end(d, u.policy_slot, w, c + (uint64_t)A);
-            } else {
-                const double* a = u.actions + (int64_t)w * A;
-#pragma unroll
-                for (int k = 0; k < SS_MAX_ACTION; ++k)
-                    if (k < A) s.action[k] = a[k];
+                    if (k < A) s.action[k] = uniform_from_word(stream_word(pol_key, pol_c, k), u.policy_lo, u.policy_hi);
+                rng_end(d, u.policy_slot, w, pol_c + (uint64_t)A);
             }
-#pragma unroll
-            for (int k = 0; k < SS_MAX_ACTION; ++k)
-                if (k < A) s.prev_action[k] = d.action[(int64_t)k * N + w];
 #pragma unroll
             for (int k = 0; k < SS_MAX_ACTION; ++k) {
                 if (k < A) {
@@ -1099,32 +1125,15 @@ __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniform
         if (sim) {
             const bool sensor = st & SS_ST_SENSOR;
             const int H = C::hist_len(d);
-            if (sensor) {
-                s.have_sensor = true;
-#pragma unroll
-                for (int i = 0; i < FM; ++i) {
-                    const bool ok = i < F;
-                    s.s_in[i] = ok ? d.s_in_contact[(int64_t)i * N + w] != 0 : false;
-                    s.s_air[i] = ok ? d.s_cur_air[(int64_t)i * N + w] : 0.0;
-                    s.s_last_air[i] = ok ? d.s_last_air[(int64_t)i * N + w] : 0.0;
-                    s.s_contact[i] = ok ? d.s_cur_contact[(int64_t)i * N + w] : 0.0;
-                    s.s_td[i] = ok ? d.s_last_td[(int64_t)i * N + w] : kNeverTouched;
-                }
-                // the force history is fully overwritten when >= H updates run
-                const int n_upd = __popc(u.sensor_mask & ((1u << u.nsub) - 1u));
-                const bool need_hist = n_upd < H;
-#pragma unroll
-                for (int h = 0; h < SS_MAX_HIST; ++h)
-#pragma unroll
-                    for (int i = 0; i < FM; ++i)
-                        s.s_hist[h][i] = (need_hist && h < H && i < F) ? d.s_force_hist[((int64_t)h * F + i) * N + w] : 0.0;
-            }
+            if (sensor) s.have_sensor = true;  // state loaded with the prefetch block
             const int nsub = u.nsub;
             auto substep = [&](int sub) {
                 if (st & SS_ST_APPLY) apply_actuators<C>(d, u, w, sub, s, P);
                 if (st & SS_ST_PUSH) {
                     // CaptureRing.push (capture.py:53-59): ctrl written, pre-integration
-                    const int slot = (u.capture_slot0 + sub) % d.capture_phys;
+                    // capture_slot0 < capture_phys and sub < nsub <= capture_phys
+                    int slot = u.capture_slot0 + sub;
+                    if (slot >= C::cap_phys(d)) slot -= C::cap_phys(d);
                     const int nq = 3 + K;
 #pragma unroll
                     for (int i = 0; i < 3 + KM; ++i) {

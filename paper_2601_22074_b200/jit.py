@@ -110,6 +110,11 @@ def config_source(d) -> str:
             lines.append(f"{head} {typ} {name}(const ss_env_desc& d) {{ return {expr}; }}")
             continue
         val = eval(expr, {"d": d})  # noqa: S307 -- expressions come from ss_cfg.cuh
+        if name == "NW" and int(val) < const_worlds_min():
+            # small envs share one build across world counts (tests, tools);
+            # large ones fold N into every SoA offset (ptr[c*N + w])
+            lines.append(f"{head} {typ} {name}(const ss_env_desc& d) {{ return {expr}; }}")
+            continue
         lines.append(f"{head} {typ} {name}(const ss_env_desc&) {{ return {_lit(typ, val)}; }}")
     for typ, name, bound, expr in _LISTS["SS_CFG_ARRAYS"]:
         if typ == "double":
@@ -131,6 +136,11 @@ def config_source(d) -> str:
                      f"{', '.join(rows)}}}; return a[t][i]; }}")
     lines.append("};")
     return "\n".join(lines)
+
+
+def const_worlds_min() -> int:
+    """World count from which N is compiled in as a constant (SS_CONST_N_MIN)."""
+    return int(os.environ.get("SS_CONST_N_MIN", "1024"))
 
 
 def block_size() -> int:

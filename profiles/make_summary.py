@@ -1,6 +1,6 @@
 """Turn gpurun_out/ ncu artifacts into committed profile summaries.
 
-    python profiles/make_summary.py <round> <launches.csv> <full.ncu-rep> <envs>
+    python profiles/make_summary.py <round> <launches.csv> <full.ncu-rep> <envs> [alg_bytes_per_world]
 
 Writes profiles/<round>_launches.md (per-kernel launch list stats),
 profiles/<round>_step_kernel.md (full-set summary of the fused step kernel)
@@ -14,6 +14,7 @@ import sys
 from collections import defaultdict
 
 rnd, launches, rep, envs = sys.argv[1], sys.argv[2], sys.argv[3], int(sys.argv[4])
+alg = int(sys.argv[5]) if len(sys.argv) > 5 else 2197
 here = os.path.dirname(os.path.abspath(__file__))
 
 rows = list(csv.reader(open(launches)))
@@ -26,7 +27,7 @@ for r in rows[h + 1:]:
         v = float(r[vi].replace(",", ""))
         v = v / 1e3 if r[ui] == "ns" else (v * 1e3 if r[ui] == "ms" else v)  # -> us
         agg[r[ki].split("(")[0][:70]].append(v)
-lines = [f"# {rnd}: launch list of `python bench.py --steps 10 --warmup 3 --no-cpu` (N=4096)",
+lines = [f"# {rnd}: launch list of `python bench.py --steps 10 --warmup 3 --no-cpu --scale-envs 0` (N=4096)",
          "", "ncu `--metrics gpu__time_duration.sum --clock-control none` (cold-cache, serialised: compare shares).", "",
          "| kernel | launches | mean us | total us | share |", "|---|---|---|---|---|"]
 tot = sum(sum(v) for v in agg.values())
@@ -69,7 +70,9 @@ for k in want:
     if k in vals:
         md.append(f"| {k} | {vals[k][0]} {vals[k][1]} |")
 md.append(f"| dram bytes read+write | {dram:.0f} B ({dram/envs:.0f} B per world) |")
-md.append(f"| algorithmic bytes (traffic.py) | {2213*envs} B (2213 B per world) |")
+md.append(f"| algorithmic bytes (traffic.py) | {alg*envs} B ({alg} B per world) |")
+st = subprocess.run([sys.executable, os.path.join(here, "ncu_stalls.py"), rep, "12"], capture_output=True, text=True).stdout
+md += ["", "Warp-state samples (ncu source counters; `profiles/ncu_stalls.py`):", "", "```", st.rstrip(), "```"]
 open(os.path.join(here, f"{rnd}_step_kernel.md"), "w").write("\n".join(md) + "\n")
 json.dump({"round": rnd, "envs": envs, "dram_bytes_per_launch": dram, "ncu_duration_us": dur,
            "report": os.path.basename(rep)}, open(os.path.join(here, "ncu_step_kernel.json"), "w"), indent=1)

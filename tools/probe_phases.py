@@ -29,7 +29,7 @@ for i in range(200 + K):
     if i >= 200:
         probe[14] = 2**62
         probe[15] = 0
-    env.step(random_policy(env, i))
+    env.step(random_policy(env, i, fused=True))
     if i >= 200:
         torch.cuda.synchronize()
         p = probe.cpu().tolist()
