@@ -27,7 +27,7 @@
 #include "ss_cfg.cuh"
 
 #ifndef SS_PEEL_LAST_SUBSTEP
-#define SS_PEEL_LAST_SUBSTEP 1
+#define SS_PEEL_LAST_SUBSTEP 0
 #endif
 
 namespace ss {
@@ -1183,14 +1183,11 @@ __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniform
             late_prefetch();
             substep(nsub - 1);
 #else
-            // one copy of the substep body in the code (the kernel is
-            // instruction-fetch bound when L2 is cold); the late loads are
-            // issued before the last substep from inside the loop
+            // one copy of the substep body in the code; the late loads follow
+            // the loop (their lines were pulled into L2 at kernel entry)
 #pragma unroll 1
-            for (int sub = 0; sub < nsub; ++sub) {
-                if (sub == nsub - 1) late_prefetch();
-                substep(sub);
-            }
+            for (int sub = 0; sub < nsub; ++sub) substep(sub);
+            late_prefetch();
 #endif
             if (sensor) {
 #pragma unroll
