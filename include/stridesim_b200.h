@@ -60,7 +60,7 @@ typedef unsigned long long uint64_t;
 extern "C" {
 #endif
 
-#define SS_ABI_VERSION 2
+#define SS_ABI_VERSION 3
 
 #define SS_MAX_JOINTS 16
 #define SS_MAX_FEET 8
@@ -454,6 +454,11 @@ typedef struct ss_env_desc {
     uint32_t* obs_bad;
     /* optional clock64() phase probes of world 0 (JIT builds with -DSS_PROBES) */
     int64_t* probe;
+    /* host mirror of the output arena (obs groups, reward, terminated,
+     * truncated): when nonzero, every output store is repeated at
+     * address + out_mirror, a mapped pinned host buffer, so the step's results
+     * cross PCIe from the kernel itself (no separate device->host copy) */
+    int64_t out_mirror;
 } ss_env_desc;
 
 /* Per-launch uniform values, all host-tracked (no device round trip). */

@@ -22,6 +22,7 @@
 #define SS_CFG_SCALARS(X) \
     X(int, NW, d.n_worlds) \
     X(int, cap_phys, d.capture_phys) \
+    X(int, mirror_on, (d.out_mirror != 0)) \
     X(int, K, d.model.n_joints) \
     X(int, F, d.model.n_feet) \
     X(double, gravity, d.model.gravity) \

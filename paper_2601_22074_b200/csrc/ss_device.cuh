@@ -75,6 +75,18 @@ __host__ __device__ __forceinline__ unsigned lo_word(double v) {
 #endif
 }
 
+// finite <=> exponent field not all ones: two integer ops on the high word
+// instead of an FP64 subtract + compare (the FP64 pipe is the scarce one)
+__host__ __device__ __forceinline__ bool finite_bits(double v) {
+#ifdef __CUDA_ARCH__
+    return (__double2hiint(v) & 0x7ff00000) != 0x7ff00000;
+#else
+    unsigned long long b;
+    memcpy(&b, &v, 8);
+    return ((b >> 32) & 0x7ff00000ull) != 0x7ff00000ull;
+#endif
+}
+
 // v with its sign bit xor-ed by `flip` (0 or 0x80000000 on the high word)
 __host__ __device__ __forceinline__ double flip_sign(double v, unsigned flip) {
 #ifdef __CUDA_ARCH__
@@ -211,14 +223,14 @@ __device__ __forceinline__ double np_sum(const double* a, int n) {
 __host__ __device__ __forceinline__ double div_rn(double a, double b, double y) {
     const double q = a * y;
     const double q1 = fma(fma(-q, b, a), y, q);
-    return isfinite(q1) ? q1 : q;
+    return finite_bits(q1) ? q1 : q;
 }
 
 
 __device__ __forceinline__ double terrain_height(const ss_terrain& t, double x) {
     if (t.flat) return 0.0;
     const int64_t last = t.n_samples - 1;
-    double pos = div_rn(isfinite(x) ? x : 0.0, t.spacing, 1.0 / t.spacing);
+    double pos = div_rn(finite_bits(x) ? x : 0.0, t.spacing, 1.0 / t.spacing);
     pos = np_clip(pos, 0.0, (double)last);
     int64_t idx = (int64_t)pos;
     if (idx > last - 1) idx = last - 1;

@@ -35,7 +35,13 @@ namespace ss {
 constexpr int kBlock = 128;
 constexpr long long kNeverTouched = -(1ll << 40);  // sensors.py:51
 
-__device__ __forceinline__ bool finite_(double x) { return (x - x) == 0.0; }
+__device__ __forceinline__ bool finite_(double x) { return finite_bits(x); }
+
+// the host-mirror twin of an output-arena address (ss_env_desc.out_mirror)
+template <class T>
+__device__ __forceinline__ T* mirror_of(const ss_env_desc& d, T* p) {
+    return (T*)((char*)p + d.out_mirror);
+}
 
 // Pull a line into L2 without holding a register (the bench flushes L2
 // between steps, so every first touch of a per-world array is a DRAM trip;
@@ -1249,6 +1255,10 @@ __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniform
             s.nonfinite = bad;
             d.terminated[w] = term;
             d.truncated[w] = trunc;
+            if (C::mirror_on(d)) {
+                *mirror_of(d, d.terminated + w) = term;
+                *mirror_of(d, d.truncated + w) = trunc;
+            }
             d.nonfinite[(int64_t)u.nf_slot * N + w] = bad;  // per-step slot of the lag ring
         }
 
@@ -1289,6 +1299,7 @@ __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniform
                 d.last_values[(int64_t)r * N + w] = v;
             });
             d.reward_out[w] = total;
+            if (C::mirror_on(d)) *mirror_of(d, d.reward_out + w) = total;
         }
 
         SS_PROBE(9);
@@ -1508,6 +1519,17 @@ __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniform
                 });
             });
             d.obs_bad[w] = bad_bits;
+            if (!C::kStageObs && C::mirror_on(d)) {
+                // unstaged rows: repeat them into the host mirror
+                for_terms<C, C::kCapGroups>(0, C::n_groups(d), [&](auto gg) {
+                    const int g = ival(gg);
+                    if (!((u.groups_mask >> g) & 1u)) return;
+                    const int D = C::g_dim(d, g);
+                    const double* row = d.group[g].out + (int64_t)w * D;
+                    double* mrow = mirror_of(d, d.group[g].out) + (int64_t)w * D;
+                    for (int k = 0; k < D; ++k) mrow[k] = row[k];
+                });
+            }
         }
         if (st & SS_ST_PREV_AFTER) {
             d.prev_lin_vel_b[w] = s.lvb0;
@@ -1533,6 +1555,8 @@ __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniform
                 const double* src = obs_stage + C::kBlock * C::g_soff(d, g);
                 const unsigned bytes = (unsigned)rows * D * 8u;
                 const bool bulk = ((bytes & 15u) == 0) && ((((unsigned long long)dst) & 15ull) == 0);
+                double* mdst = C::mirror_on(d) ? mirror_of(d, dst) : nullptr;
+                const bool mbulk = ((((unsigned long long)mdst) & 15ull) == 0);
                 if (bulk) {
                     if (threadIdx.x == 0) {
                         const unsigned saddr = (unsigned)__cvta_generic_to_shared(src);
@@ -1540,10 +1564,18 @@ __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniform
                         asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(saddr),
                                      "r"(bytes)
                                      : "memory");
+                        if (mdst && mbulk)  // the same rows straight into the host mirror over PCIe
+                            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(mdst),
+                                         "r"(saddr), "r"(bytes)
+                                         : "memory");
                         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                     }
+                    if (mdst && !mbulk)
+                        for (int i = threadIdx.x; i < rows * D; i += blockDim.x) mdst[i] = src[i];
                 } else {
                     for (int i = threadIdx.x; i < rows * D; i += blockDim.x) dst[i] = src[i];
+                    if (mdst)
+                        for (int i = threadIdx.x; i < rows * D; i += blockDim.x) mdst[i] = src[i];
                 }
             });
             if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");

@@ -219,6 +219,24 @@ class ManagerBasedRlEnv:
         tm.terminated = views["terminated"]
         tm.truncated = views["truncated"]
 
+    def enable_host_outputs(self) -> dict:
+        """Mirror every step's outputs into pinned host memory from the kernel.
+
+        After this call each launch repeats its output-arena stores (the obs
+        groups, reward, terminated, truncated) into a mapped pinned host block
+        of the same layout, so the results cross PCIe while the kernel runs
+        instead of through a separate device->host copy. Returns the typed
+        host views (also ``host_outputs``); they hold a step's results once
+        the launching stream has been synchronized. Device outputs are
+        unchanged."""
+        import torch
+
+        if getattr(self, "_host_mirror", None) is None:
+            self._host_mirror = torch.zeros(self.step_outputs.numel(), dtype=torch.uint8).pin_memory()
+            self.host_outputs = self.unpack_outputs(self._host_mirror)
+            self._invalidate()
+        return self.host_outputs
+
     def unpack_outputs(self, block) -> dict:
         """Typed views into a copy of ``step_outputs`` (device or host)."""
         out = {}
@@ -297,6 +315,10 @@ class ManagerBasedRlEnv:
             self.observation_manager.native_into(d)
             d.nf_flags = self._nf_flags.data_ptr()
             d.probe = getattr(self, "_probe_ptr", None)
+            hm = getattr(self, "_host_mirror", None)
+            if hm is not None:
+                delta = hm.data_ptr() - self.step_outputs.data_ptr()
+                d.out_mirror = ctypes.c_int64(delta).value  # two's complement wrap
             d.nonfinite = self._nf_masks.data_ptr()
             # the descriptor may have allocated new stream slots: refresh their pointers
             for s, base in enumerate(r.bases):

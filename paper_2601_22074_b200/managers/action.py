@@ -94,6 +94,11 @@ class ActionManager:
                 f"action shape {tuple(a.shape)} does not match expected "
                 f"{(self.env.num_envs, self.total_dim)} (sum of term dims)"
             )
+        if a.device.type == "cpu" and a.dtype == torch.float64 and a.is_contiguous() and a.is_pinned():
+            # pinned host rows are read by the step kernel in place over PCIe
+            # (mapped memory): no separate host->device copy. Keep the buffer
+            # unchanged until the step has completed on the stream.
+            return a
         if a.dtype != torch.float64 or a.device != self.env.device or not a.is_contiguous():
             a = a.to(device=self.env.device, dtype=torch.float64).contiguous()
         return a

@@ -758,3 +758,33 @@ def test_fused_random_policy_equals_separate_draw(mode):
         assert torch.equal(ra, rb) and torch.equal(ta, tb) and torch.equal(xa, xb)
     assert torch.equal(a.streams.counter("policy.random"), b.streams.counter("policy.random"))
     assert torch.equal(a.state.q, b.state.q) and torch.equal(a.state.qd, b.state.qd)
+
+
+@pytest.mark.parametrize("generic", [False, True])
+def test_host_io_zero_copy_equals_device_path(generic):
+    """Pinned host actions read in place by the kernel and outputs mirrored
+    into pinned host memory by the kernel (enable_host_outputs) give the same
+    bits as device actions + device outputs."""
+    from paper_2601_22074_b200.env import ManagerBasedRlEnv
+    from paper_2601_22074_b200.tasks import make_env_cfg
+
+    a = ManagerBasedRlEnv(make_env_cfg("Velocity-Rough", num_envs=300, seed=5))
+    b = ManagerBasedRlEnv(make_env_cfg("Velocity-Rough", num_envs=300, seed=5))
+    if generic:
+        a.use_jit = b.use_jit = False
+    host = b.enable_host_outputs()
+    a.reset()
+    b.reset()
+    rng = np.random.default_rng(3)
+    pinned = torch.empty((300, a.action_manager.total_dim), dtype=torch.float64).pin_memory()
+    for i in range(25):
+        pinned.copy_(torch.from_numpy(rng.uniform(-1, 1, size=tuple(pinned.shape))))
+        oa, ra, ta, xa, _ = a.step(pinned.cuda())
+        b.step(pinned)
+        torch.cuda.synchronize()
+        for g in oa:
+            assert torch.equal(oa[g].cpu(), host[f"obs/{g}"]), (i, g)
+        assert torch.equal(ra.cpu(), host["reward"]) and torch.equal(ta.cpu(), host["terminated"])
+        assert torch.equal(xa.cpu(), host["truncated"])
+    assert torch.equal(a.state.q, b.state.q)
+    assert torch.equal(a.step_outputs, b.step_outputs)

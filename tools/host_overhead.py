@@ -79,3 +79,25 @@ t1 = time.perf_counter()
 torch.cuda.synchronize()
 print(f"{'e2e host enqueue only':<40s} {1e6 * (t1 - t0) / 300:7.1f} us")
 print("D2H bytes", env.step_outputs.numel())
+
+# ---- zero-copy host I/O (enable_host_outputs + pinned actions read in place)
+host_views = env.enable_host_outputs()
+pinned = host_actions
+env.step(pinned)
+torch.cuda.synchronize()
+timed("zero-copy e2e (step(pinned), sync)", lambda: (env.step(pinned), stream.synchronize()))
+t0 = time.perf_counter()
+for _ in range(300):
+    env.step(pinned)
+t1 = time.perf_counter()
+torch.cuda.synchronize()
+print(f"{'zero-copy host enqueue only':<40s} {1e6 * (t1 - t0) / 300:7.1f} us")
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+tot = 0.0
+for _ in range(100):
+    e0.record()
+    env.step(pinned)
+    e1.record()
+    e1.synchronize()
+    tot += e0.elapsed_time(e1)
+print(f"{'zero-copy step GPU time (events, host-bound)':<40s} {10 * tot:7.1f} us")

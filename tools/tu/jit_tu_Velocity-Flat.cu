@@ -14,6 +14,7 @@ struct JitCfg {
   static __device__ __forceinline__ int g_soff(const ss_env_desc&, int g) { constexpr int a[4] = {0, 19, 0, 0}; return a[g]; }
   static __device__ __forceinline__ int NW(const ss_env_desc&) { return 4096; }
   static __device__ __forceinline__ int cap_phys(const ss_env_desc&) { return 220; }
+  static __device__ __forceinline__ int mirror_on(const ss_env_desc&) { return 0; }
   static __device__ __forceinline__ int K(const ss_env_desc&) { return 4; }
   static __device__ __forceinline__ int F(const ss_env_desc&) { return 2; }
   static __device__ __forceinline__ double gravity(const ss_env_desc& d) { return d.model.gravity; }
