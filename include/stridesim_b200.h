@@ -60,7 +60,7 @@ typedef unsigned long long uint64_t;
 extern "C" {
 #endif
 
-#define SS_ABI_VERSION 3
+#define SS_ABI_VERSION 4
 
 #define SS_MAX_JOINTS 16
 #define SS_MAX_FEET 8
@@ -526,6 +526,10 @@ typedef struct ss_rt_state {
     int32_t nf_count[SS_RT_SLOTS];
     uint64_t nf_event[SS_RT_SLOTS];
     int64_t launches;
+    /* slots retired by the poll folded into the last ss_rt_launch that were
+     * flagged nonfinite (ss_launch.poll_keep >= 0) */
+    int32_t nf_ready_n;
+    int32_t nf_ready[SS_RT_SLOTS];
 } ss_rt_state;
 
 /* One launch request for ss_rt_launch. */
@@ -537,7 +541,9 @@ typedef struct ss_launch {
     const double* actions;
     const uint8_t* reset_mask;
     int32_t policy_slot;
-    int32_t policy_pad;
+    /* >= 0: retire nonfinite slots first (ss_rt_poll with this keep), results
+     * in ss_rt_state.nf_ready -- one host call per step instead of two */
+    int32_t poll_keep;
     double policy_lo;
     double policy_hi;
 } ss_launch;

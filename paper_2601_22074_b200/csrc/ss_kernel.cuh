@@ -26,6 +26,9 @@
 #include "ss_device.cuh"
 #include "ss_cfg.cuh"
 
+#ifndef SS_MIRROR_TMA
+#define SS_MIRROR_TMA 1
+#endif
 #ifndef SS_PEEL_LAST_SUBSTEP
 #define SS_PEEL_LAST_SUBSTEP 0
 #endif
@@ -1556,7 +1559,7 @@ __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniform
                 const unsigned bytes = (unsigned)rows * D * 8u;
                 const bool bulk = ((bytes & 15u) == 0) && ((((unsigned long long)dst) & 15ull) == 0);
                 double* mdst = C::mirror_on(d) ? mirror_of(d, dst) : nullptr;
-                const bool mbulk = ((((unsigned long long)mdst) & 15ull) == 0);
+                const bool mbulk = SS_MIRROR_TMA && ((((unsigned long long)mdst) & 15ull) == 0);
                 if (bulk) {
                     if (threadIdx.x == 0) {
                         const unsigned saddr = (unsigned)__cvta_generic_to_shared(src);

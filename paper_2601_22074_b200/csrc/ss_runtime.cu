@@ -20,7 +20,15 @@
 
 void ss_set_error(const char* what, const char* msg);  // ss_step.cu
 
+extern "C" int ss_rt_poll(ss_rt_state* st, int32_t keep, int32_t* out_slots, int32_t max_out);
+
 extern "C" int ss_rt_launch(const ss_env_desc* d, ss_rt_state* st, const ss_launch* l, void* jit, void* stream) {
+    st->nf_ready_n = 0;
+    if ((l->stages & SS_ST_TERM) && l->poll_keep >= 0) {
+        const int n = ss_rt_poll(st, l->poll_keep, st->nf_ready, SS_RT_SLOTS);
+        if (n < 0) return n;
+        st->nf_ready_n = n;
+    }
     ss_uniforms u;
     memset(&u, 0, sizeof(u));
     const uint32_t stages = l->stages;

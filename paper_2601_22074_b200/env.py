@@ -111,6 +111,7 @@ class ManagerBasedRlEnv:
 
         self.config_hash = config_hash(cfg)
         self.terrain = generate_grid(cfg.scene.terrain, cfg.seed)
+        self._dev_index = self.device.index if self.device.index is not None else torch.cuda.current_device()
         self.model = compile_model(spec, n, self.device)
         self.state = BatchState(self.model)
         self.world_ids = cfg.scene.world_id_offset + np.arange(n)
@@ -347,7 +348,7 @@ class ManagerBasedRlEnv:
         rt = self._rt
         term = stages & native.SS_ST_TERM
         if term:
-            self._nf_drain(NF_LAG)
+            # the launch retires old nonfinite slots itself (poll_keep)
             self.termination_manager.last_nonfinite = self._nf_views[rt.nf_slot]
         la = self._la
         la.stages = stages
@@ -361,14 +362,21 @@ class ManagerBasedRlEnv:
             la.actions = None if actions is None else actions.data_ptr()
             la.policy_slot = -1
         la.reset_mask = None if reset_mask is None else reset_mask.data_ptr()
+        la.poll_keep = NF_LAG if term else -1
         rt.sim_step = self.state.sim_step
         native.LAUNCHES["count"] += 1
         rc = self._lib.ss_rt_launch(self._desc_ref, self._rt_ref, self._la_ref,
                                     self._jit_handle if self.use_jit else None,
-                                    native.current_stream(self.device))
+                                    native.current_stream(self._dev_index))
         if rc != 0:
             raise native.NativeError(f"ss_rt_launch failed ({rc}): {self._lib.ss_last_error().decode()}")
         self.state.sim_step = rt.sim_step
+        if term and rt.nf_ready_n:
+            # retired slots are never the one this launch used (ring of
+            # NF_LAG + 2), so their metadata and masks are still intact
+            for i in range(rt.nf_ready_n):
+                slot = rt.nf_ready[i]
+                self._dump_on_nonfinite(slot, rt.nf_pushes[slot], rt.nf_count[slot], rt.nf_sim_step[slot])
 
     # -- nonfinite detection (deferred, no per-step sync) ----------------------------
 

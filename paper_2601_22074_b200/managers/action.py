@@ -94,7 +94,7 @@ class ActionManager:
                 f"action shape {tuple(a.shape)} does not match expected "
                 f"{(self.env.num_envs, self.total_dim)} (sum of term dims)"
             )
-        if a.device.type == "cpu" and a.dtype == torch.float64 and a.is_contiguous() and a.is_pinned():
+        if a.device.type == "cpu" and a.dtype == torch.float64 and a.is_contiguous() and self._pinned(a):
             # pinned host rows are read by the step kernel in place over PCIe
             # (mapped memory): no separate host->device copy. Keep the buffer
             # unchanged until the step has completed on the stream.
@@ -102,6 +102,22 @@ class ActionManager:
         if a.dtype != torch.float64 or a.device != self.env.device or not a.is_contiguous():
             a = a.to(device=self.env.device, dtype=torch.float64).contiguous()
         return a
+
+    def _pinned(self, a) -> bool:
+        """is_pinned() with a small cache of known pinned storages (the query
+        is a driver call); cached entries hold a reference, so a cached range
+        cannot be freed and reused by pageable memory."""
+        p = a.data_ptr()
+        cache = self.__dict__.setdefault("_pinned_cache", [])
+        for lo, hi, _ref in cache:
+            if lo <= p and p + a.numel() * 8 <= hi:
+                return True
+        if not a.is_pinned():
+            return False
+        st = a.untyped_storage()
+        cache.insert(0, (st.data_ptr(), st.data_ptr() + st.nbytes(), a))
+        del cache[4:]
+        return True
 
     def process(self, actions) -> None:
         """Stage 1: history update, optional clip, per-term targets (managers/action.py:68-82)."""

@@ -166,8 +166,11 @@ def call(name: str, *args) -> None:
 
 
 def current_stream(device=None) -> int:
+    """Raw cudaStream_t of the current stream (an int device index is the fast path)."""
     import torch
 
+    if isinstance(device, int):
+        return torch._C._cuda_getCurrentRawStream(device)
     return torch.cuda.current_stream(device).cuda_stream
 
 

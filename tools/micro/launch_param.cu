@@ -1,5 +1,6 @@
 // Launch cost vs kernel-parameter size, warm and after an L2 flush.
 //   nvcc -O2 -gencode arch=compute_100a,code=sm_100a tools/micro/launch_param.cu -o /tmp/lp && /tmp/lp
+#include <chrono>
 #include <cstdio>
 #include <cuda_runtime.h>
 
@@ -54,6 +55,23 @@ int main() {
     P<4096> p4k{};
     P<13312> p13k{};
     P<32000> p32k{};
+    // host-side cost of one launch (queue depth kept low by periodic syncs)
+    auto host_cost = [&](auto launch) {
+        cudaDeviceSynchronize();
+        double tot = 0;
+        for (int r = 0; r < 20; ++r) {
+            auto t0 = std::chrono::steady_clock::now();
+            for (int i = 0; i < 100; ++i) launch();
+            auto t1 = std::chrono::steady_clock::now();
+            cudaDeviceSynchronize();
+            tot += std::chrono::duration<double, std::micro>(t1 - t0).count();
+        }
+        return tot / 2000;
+    };
+    printf("host launch cost: 16 B %.2f us, 1 KB %.2f us, 4 KB %.2f us, 13 KB %.2f us, 32 KB %.2f us\n",
+           host_cost([&] { k_param<16><<<64, 64>>>(p16, out); }), host_cost([&] { k_param<1024><<<64, 64>>>(p1k, out); }),
+           host_cost([&] { k_param<4096><<<64, 64>>>(p4k, out); }), host_cost([&] { k_param<13312><<<64, 64>>>(p13k, out); }),
+           host_cost([&] { k_param<32000><<<64, 64>>>(p32k, out); }));
     for (int fl = 0; fl < 2; ++fl) {
         printf("%s\n", fl ? "after L2 flush:" : "warm:");
         printf("  param 16 B   : %6.2f us\n", time_it([&] { k_param<16><<<64, 64>>>(p16, out); }, fl, fbuf, fn));
