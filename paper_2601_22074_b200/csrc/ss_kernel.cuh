@@ -1014,6 +1014,12 @@ __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniform
                 s.plv1 = d.prev_lin_vel_b[N + w];
             }
         };
+        // the heightfield (38 KB for the rough grid): one 128 B line per thread
+        // of the first threads, so the feet's first lookups hit L2
+        if (!C::flat(d) && (st & (SS_ST_PHYS | SS_ST_OBS | SS_ST_RESET | SS_ST_RESET_ALL))) {
+            const int line = w;  // w < N here
+            if ((int64_t)line * 16 < d.terrain.n_samples) l2_prefetch(d.terrain.samples + (int64_t)line * 16);
+        }
         // L2 prefetch of everything read after the substeps or on the reset path
         if (st & (SS_ST_TERM | SS_ST_CURRICULUM)) {
             l2_prefetch(d.episode_steps + w);
