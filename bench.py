@@ -392,7 +392,9 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    n = args.envs
+    # the whole job of our arm: envs per GPU x GPUs (weak scaling), on the host cores
+    world = int(os.environ.get("WORLD_SIZE", str(max(1, args.gpus))))
+    n = args.envs * world
     pool = CpuBaseline(args.task, n)
     try:
         pool.run(max(1, args.warmup))
@@ -404,7 +406,7 @@ def run_reference(args):
         "metric": METRIC,
         "value": v,
         "unit": UNIT,
-        "n_gpus": args.gpus,
+        "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
         "ms_per_step": 1e3 * el / args.steps,
@@ -414,7 +416,7 @@ def run_reference(args):
         "dtype": "f64",
         "data": "synthetic (random actions from the per-world streams)",
         "config": {"workload": f"{args.task} (planar biped restatement of BASELINE configs[1], SURVEY 0.1)",
-                   "task": args.task, "envs_per_gpu": n, "decimation": 4},
+                   "task": args.task, "envs_per_gpu": args.envs, "total_envs": n, "decimation": 4},
         "impl": "reference",
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": pool.procs, "kind": "port",
                          "sample": f"{args.task} N={n} over {pool.procs} host processes, {args.steps} control steps, "
