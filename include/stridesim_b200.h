@@ -60,7 +60,7 @@ typedef unsigned long long uint64_t;
 extern "C" {
 #endif
 
-#define SS_ABI_VERSION 4
+#define SS_ABI_VERSION 5
 
 #define SS_MAX_JOINTS 16
 #define SS_MAX_FEET 8
@@ -79,6 +79,58 @@ extern "C" {
 #define SS_MAX_SLOTS 48
 #define SS_MAX_MLP_LAYERS 4
 #define SS_MAX_HIST 8
+
+/* Array bounds of the descriptor structs. The ABI (this header as compiled
+ * by the library and parsed by the Python binding) uses the SS_MAX_* caps;
+ * a per-env specialized kernel (jit.py) defines them to the env's actual
+ * counts before including this header, so its descriptor parameter block
+ * holds only the entries that exist (ss_launch.jit_desc carries that packed
+ * copy). */
+#ifndef SS_DCAP_JOINTS
+#define SS_DCAP_JOINTS SS_MAX_JOINTS
+#endif
+#ifndef SS_DCAP_FEET
+#define SS_DCAP_FEET SS_MAX_FEET
+#endif
+#ifndef SS_DCAP_ACTION_TERMS
+#define SS_DCAP_ACTION_TERMS SS_MAX_ACTION_TERMS
+#endif
+#ifndef SS_DCAP_ACTUATORS
+#define SS_DCAP_ACTUATORS SS_MAX_ACTUATORS
+#endif
+#ifndef SS_DCAP_CMD
+#define SS_DCAP_CMD SS_MAX_CMD
+#endif
+#ifndef SS_DCAP_RAYS
+#define SS_DCAP_RAYS SS_MAX_RAYS
+#endif
+#ifndef SS_DCAP_GROUPS
+#define SS_DCAP_GROUPS SS_MAX_GROUPS
+#endif
+#ifndef SS_DCAP_OBS_TERMS
+#define SS_DCAP_OBS_TERMS SS_MAX_OBS_TERMS
+#endif
+#ifndef SS_DCAP_REWARDS
+#define SS_DCAP_REWARDS SS_MAX_REWARDS
+#endif
+#ifndef SS_DCAP_TERMINATIONS
+#define SS_DCAP_TERMINATIONS SS_MAX_TERMINATIONS
+#endif
+#ifndef SS_DCAP_EVENTS
+#define SS_DCAP_EVENTS SS_MAX_EVENTS
+#endif
+#ifndef SS_DCAP_CURRICULUM
+#define SS_DCAP_CURRICULUM SS_MAX_CURRICULUM
+#endif
+#ifndef SS_DCAP_FIELDS
+#define SS_DCAP_FIELDS SS_MAX_FIELDS
+#endif
+#ifndef SS_DCAP_SLOTS
+#define SS_DCAP_SLOTS SS_MAX_SLOTS
+#endif
+#ifndef SS_DCAP_MLP_LAYERS
+#define SS_DCAP_MLP_LAYERS SS_MAX_MLP_LAYERS
+#endif
 
 /* stage bits for ss_uniforms.stages (reference order: env.py:219-259) */
 #define SS_ST_ACTION 1u        /* ActionManager.process                      */
@@ -172,23 +224,23 @@ typedef struct ss_field {
     double* ptr;
     int32_t expanded;
     int32_t size;
-    double base[SS_MAX_JOINTS];
+    double base[SS_DCAP_JOINTS];
 } ss_field;
 
 /* Compiled chain structure (sim/model.py:43-92) + contact constants. */
 typedef struct ss_model {
     int32_t n_joints;
     int32_t n_feet;
-    int32_t parent[SS_MAX_JOINTS];
-    int32_t foot_joint[SS_MAX_FEET];
-    uint32_t chain_mask[SS_MAX_FEET];
-    double attach_x[SS_MAX_JOINTS];
-    double attach_z[SS_MAX_JOINTS];
-    double link_len[SS_MAX_JOINTS];
-    double half_len[SS_MAX_JOINTS];
-    double pos_lo[SS_MAX_JOINTS];
-    double pos_hi[SS_MAX_JOINTS];
-    double soft_frac[SS_MAX_JOINTS];
+    int32_t parent[SS_DCAP_JOINTS];
+    int32_t foot_joint[SS_DCAP_FEET];
+    uint32_t chain_mask[SS_DCAP_FEET];
+    double attach_x[SS_DCAP_JOINTS];
+    double attach_z[SS_DCAP_JOINTS];
+    double link_len[SS_DCAP_JOINTS];
+    double half_len[SS_DCAP_JOINTS];
+    double pos_lo[SS_DCAP_JOINTS];
+    double pos_hi[SS_DCAP_JOINTS];
+    double soft_frac[SS_DCAP_JOINTS];
     double gravity;
     double dt;
     double k_n;
@@ -232,8 +284,8 @@ typedef struct ss_state {
  * on device from base[slot] and the global world id; counters are (N,). */
 typedef struct ss_rng {
     int64_t world_id_offset;
-    uint64_t base[SS_MAX_SLOTS];
-    uint64_t* counter[SS_MAX_SLOTS];
+    uint64_t base[SS_DCAP_SLOTS];
+    uint64_t* counter[SS_DCAP_SLOTS];
 } ss_rng;
 
 typedef struct ss_action_term {
@@ -241,8 +293,8 @@ typedef struct ss_action_term {
     int32_t start;
     int32_t has_clip;
     int32_t pad0;
-    int32_t joint[SS_MAX_JOINTS];
-    double offset[SS_MAX_JOINTS];
+    int32_t joint[SS_DCAP_JOINTS];
+    double offset[SS_DCAP_JOINTS];
     double scale;
     double clip_lo;
     double clip_hi;
@@ -270,7 +322,7 @@ typedef struct ss_actuator {
     int32_t n_layers;
     int32_t err_hist;
     int32_t vel_hist;
-    int32_t joint[SS_MAX_JOINTS];
+    int32_t joint[SS_DCAP_JOINTS];
     double effort;
     double saturation;
     double vel_limit;
@@ -280,7 +332,7 @@ typedef struct ss_actuator {
     int64_t* delay_steps;
     double* err_buf;
     double* vel_buf;
-    ss_mlp_layer layer[SS_MAX_MLP_LAYERS];
+    ss_mlp_layer layer[SS_DCAP_MLP_LAYERS];
 } ss_actuator;
 
 typedef struct ss_obs_term {
@@ -366,24 +418,24 @@ typedef struct ss_env_desc {
     ss_model model;
     ss_terrain terrain;
     ss_state state;
-    ss_field field[SS_MAX_FIELDS];
+    ss_field field[SS_DCAP_FIELDS];
     ss_rng rng;
     /* default state (entity.py:91-105, env.py:121-135) and spawn */
     double base_pose[3];
     double base_vel[3];
-    double joint_pos[SS_MAX_JOINTS];
-    double joint_vel[SS_MAX_JOINTS];
+    double joint_pos[SS_DCAP_JOINTS];
+    double joint_vel[SS_DCAP_JOINTS];
     double spawn_offset;
     /* actions */
     int32_t n_action_terms;
     int32_t action_dim;
-    ss_action_term action_term[SS_MAX_ACTION_TERMS];
+    ss_action_term action_term[SS_DCAP_ACTION_TERMS];
     double* action;
     double* prev_action;
     double* targets;
     int32_t n_actuators;
     int32_t pad1;
-    ss_actuator actuator[SS_MAX_ACTUATORS];
+    ss_actuator actuator[SS_DCAP_ACTUATORS];
     /* capture ring (capture.py:41-59), physical capacity capture_phys */
     int32_t capture_phys;
     int32_t pad2;
@@ -404,11 +456,11 @@ typedef struct ss_env_desc {
     /* ray scanner (sensors.py:20-46) */
     int32_t n_rays;
     int32_t pad4;
-    double ray_offset[SS_MAX_RAYS];
+    double ray_offset[SS_DCAP_RAYS];
     /* terminations (managers/termination.py) */
     int32_t n_terms;
     int32_t pad5;
-    ss_term_term term[SS_MAX_TERMINATIONS];
+    ss_term_term term[SS_DCAP_TERMINATIONS];
     uint8_t* terminated;
     uint8_t* truncated;
     uint8_t* nonfinite;
@@ -417,7 +469,7 @@ typedef struct ss_env_desc {
     /* rewards (managers/reward.py) */
     int32_t n_rewards;
     int32_t pad6;
-    ss_reward_term reward[SS_MAX_REWARDS];
+    ss_reward_term reward[SS_DCAP_REWARDS];
     double* reward_out;
     double* ep_sums;
     double* ep_raw;
@@ -429,16 +481,16 @@ typedef struct ss_env_desc {
     int32_t cmd_slot;
     int32_t pad7;
     double cap_scale;
-    double init_lo[SS_MAX_CMD];
-    double init_hi[SS_MAX_CMD];
+    double init_lo[SS_DCAP_CMD];
+    double init_hi[SS_DCAP_CMD];
     double* command;
     double* ranges;
     int64_t* countdown;
     /* events + curriculum */
     int32_t n_events;
     int32_t n_curriculum;
-    ss_event_term event[SS_MAX_EVENTS];
-    ss_curriculum_term curriculum[SS_MAX_CURRICULUM];
+    ss_event_term event[SS_DCAP_EVENTS];
+    ss_curriculum_term curriculum[SS_DCAP_CURRICULUM];
     /* episode bookkeeping (env.py:146-151) */
     int64_t* episode_steps;
     double* episode_start_x;
@@ -449,8 +501,8 @@ typedef struct ss_env_desc {
     /* observations */
     int32_t n_groups;
     int32_t n_obs_terms;
-    ss_obs_group group[SS_MAX_GROUPS];
-    ss_obs_term obs[SS_MAX_OBS_TERMS];
+    ss_obs_group group[SS_DCAP_GROUPS];
+    ss_obs_term obs[SS_DCAP_OBS_TERMS];
     uint32_t* obs_bad;
     /* optional clock64() phase probes of world 0 (JIT builds with -DSS_PROBES) */
     int64_t* probe;
@@ -546,6 +598,10 @@ typedef struct ss_launch {
     int32_t poll_keep;
     double policy_lo;
     double policy_hi;
+    /* the descriptor packed with the specialized kernel's SS_DCAP_* bounds
+     * (NULL: the kernel takes the full ss_env_desc); its size in bytes */
+    const void* jit_desc;
+    int64_t jit_desc_bytes;
 } ss_launch;
 
 /* One draw call of StreamPack.uniform/normal (rng.py:69-119). sel == NULL
@@ -591,6 +647,12 @@ int ss_jit_compile(const char* src, const char* name, int n_headers, const char*
 int ss_jit_load(const void* cubin, size_t size, const char* kernel_name, int block, void** handle);
 int ss_jit_unload(void* handle);
 int ss_env_step_jit(void* handle, const ss_env_desc* desc, const ss_uniforms* u, void* stream);
+/* A module compiled with SS_DCAP_* bounds takes the packed descriptor:
+ * declare its size once, then launch with the full descriptor (validated)
+ * plus the packed copy that becomes the kernel parameter block. */
+int ss_jit_set_desc_bytes(void* handle, int64_t bytes);
+int ss_env_step_jit_packed(void* handle, const ss_env_desc* desc, const void* packed, int64_t packed_bytes,
+                           const ss_uniforms* u, void* stream);
 /* Runtime: derive the uniforms from *st, launch (JIT module when jit != NULL,
  * else the generic kernel), advance *st. ss_rt_poll retires completed TERM
  * launches (blocking on the oldest while more than `keep` are pending) and

@@ -91,7 +91,9 @@ extern "C" int ss_rt_launch(const ss_env_desc* d, ss_rt_state* st, const ss_laun
         u.nf_slot = slot;
         st->nf_flags[slot] = 0;
     }
-    const int rc = jit ? ss_env_step_jit(jit, d, &u, stream) : ss_env_step(d, &u, stream);
+    const int rc = !jit ? ss_env_step(d, &u, stream)
+                   : l->jit_desc ? ss_env_step_jit_packed(jit, d, l->jit_desc, l->jit_desc_bytes, &u, stream)
+                                 : ss_env_step_jit(jit, d, &u, stream);
     if (rc != 0) return rc;
     st->launches += 1;
     if ((stages & SS_ST_PHYS) && nsub > 0) st->sim_step += nsub;

@@ -108,6 +108,7 @@ struct JitModule {
     cudaKernel_t kernel;
     int block;
     int min_grid;  // experiment knob (SS_MIN_GRID): pad the grid with empty blocks
+    int64_t desc_bytes;  // size of the kernel's descriptor parameter (packed when < sizeof(ss_env_desc))
 };
 
 // Compile `src` (with named headers) for sm_100a. Returns the cubin through
@@ -147,6 +148,7 @@ extern "C" int ss_jit_load(const void* cubin, size_t size, const char* kernel_na
     (void)size;
     JitModule* m = new JitModule();
     m->block = block > 0 ? block : kBlock;
+    m->desc_bytes = (int64_t)sizeof(ss_env_desc);
     const char* mg = getenv("SS_MIN_GRID");
     m->min_grid = mg ? atoi(mg) : 0;
     cudaError_t e = cudaLibraryLoadData(&m->lib, cubin, nullptr, nullptr, 0, nullptr, nullptr, 0);
@@ -172,15 +174,45 @@ extern "C" int ss_jit_unload(void* handle) {
     return 0;
 }
 
-extern "C" int ss_env_step_jit(void* handle, const ss_env_desc* desc, const ss_uniforms* u, void* stream) {
-    if (int rc = check_desc(desc, u, "ss_env_step_jit")) return rc;
-    if (desc->n_worlds <= 0) return 0;
-    JitModule* m = (JitModule*)handle;
-    void* args[2] = {(void*)desc, (void*)u};
+static int jit_launch(JitModule* m, const ss_env_desc* desc, const void* param, const ss_uniforms* u, void* stream) {
+    void* args[2] = {(void*)param, (void*)u};
     int blocks = (desc->n_worlds + m->block - 1) / m->block;
     if (blocks < m->min_grid) blocks = m->min_grid;
     const dim3 grid(blocks);
     cudaError_t e = cudaLaunchKernel((const void*)m->kernel, grid, dim3(m->block), args, 0, (cudaStream_t)stream);
     if (e != cudaSuccess) return ss_fail("ss_env_step_jit launch", e);
     return 0;
+}
+
+extern "C" int ss_env_step_jit(void* handle, const ss_env_desc* desc, const ss_uniforms* u, void* stream) {
+    if (int rc = check_desc(desc, u, "ss_env_step_jit")) return rc;
+    if (desc->n_worlds <= 0) return 0;
+    JitModule* m = (JitModule*)handle;
+    if (m->desc_bytes != (int64_t)sizeof(ss_env_desc)) {
+        ss_set_error("ss_env_step_jit", "module takes a packed descriptor: use ss_env_step_jit_packed");
+        return -13;
+    }
+    return jit_launch(m, desc, desc, u, stream);
+}
+
+extern "C" int ss_jit_set_desc_bytes(void* handle, int64_t bytes) {
+    JitModule* m = (JitModule*)handle;
+    if (!m || bytes <= 0 || bytes > (int64_t)sizeof(ss_env_desc)) {
+        ss_set_error("ss_jit_set_desc_bytes", "bad handle or size");
+        return -14;
+    }
+    m->desc_bytes = bytes;
+    return 0;
+}
+
+extern "C" int ss_env_step_jit_packed(void* handle, const ss_env_desc* desc, const void* packed, int64_t packed_bytes,
+                                      const ss_uniforms* u, void* stream) {
+    if (int rc = check_desc(desc, u, "ss_env_step_jit_packed")) return rc;
+    if (desc->n_worlds <= 0) return 0;
+    JitModule* m = (JitModule*)handle;
+    if (!packed || packed_bytes != m->desc_bytes) {
+        ss_set_error("ss_env_step_jit_packed", "packed descriptor size does not match the module");
+        return -15;
+    }
+    return jit_launch(m, desc, packed, u, stream);
 }

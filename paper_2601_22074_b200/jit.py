@@ -153,10 +153,32 @@ def min_blocks() -> int:
     return int(os.environ.get("SS_MINB", "0"))
 
 
+def desc_caps(d) -> dict:
+    """SS_DCAP_* bounds of the packed descriptor for ``d``: the counts that
+    exist (>= 1); stream slots rounded up to 8 so a new purpose rarely
+    changes the layout."""
+    k, f = int(d.model.n_joints), int(d.model.n_feet)
+    fields = max([i + 1 for i in range(native.SS_MAX_FIELDS) if d.field[i].ptr] + [1])
+    fsize = max([int(d.field[i].size) for i in range(fields)] + [1])
+    slots = max([i + 1 for i in range(native.SS_MAX_SLOTS) if d.rng.counter[i]] + [1])
+    slots = min(native.SS_MAX_SLOTS, -(-slots // 8) * 8)
+    layers = max([int(d.actuator[a].n_layers) for a in range(int(d.n_actuators))] + [1])
+    return {"JOINTS": max(k, fsize, 1), "FEET": max(f, 1), "ACTION_TERMS": max(int(d.n_action_terms), 1),
+            "ACTUATORS": max(int(d.n_actuators), 1), "CMD": max(int(d.n_cmd), 1), "RAYS": max(int(d.n_rays), 1),
+            "GROUPS": max(int(d.n_groups), 1), "OBS_TERMS": max(int(d.n_obs_terms), 1),
+            "REWARDS": max(int(d.n_rewards), 1), "TERMINATIONS": max(int(d.n_terms), 1),
+            "EVENTS": max(int(d.n_events), 1), "CURRICULUM": max(int(d.n_curriculum), 1), "FIELDS": fields,
+            "SLOTS": slots, "MLP_LAYERS": layers}
+
+
 def kernel_source(d) -> str:
     k, f = int(d.model.n_joints), int(d.model.n_feet)
+    caps = desc_caps(d)
+    packed = ctypes.sizeof(native.packed_desc_type(caps))
     return "\n".join([
+        *[f"#define SS_DCAP_{c} {v}" for c, v in caps.items()],
         '#include "stridesim_b200.h"',
+        f'static_assert(sizeof(ss_env_desc) == {packed}, "packed descriptor layout differs from the host packing");',
         '#include "ss_kernel.cuh"',
         config_source(d),
         f"extern \"C\" __global__ void __launch_bounds__({block_size()}"
@@ -247,5 +269,6 @@ def module_for(d) -> int:
             pass
     handle = ctypes.c_void_p()
     native.call("ss_jit_load", cubin, len(cubin), KERNEL.encode(), block_size(), ctypes.byref(handle))
+    native.call("ss_jit_set_desc_bytes", handle, ctypes.sizeof(native.packed_desc_type(desc_caps(d))))
     _MODULES[key] = handle.value
     return handle.value

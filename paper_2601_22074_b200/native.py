@@ -28,13 +28,22 @@ class NativeError(RuntimeError):
 # header -> ctypes
 
 
-def _parse_header(path: str):
+def _parse_header(path: str, overrides: dict | None = None):
+    """Macros + struct field lists of the header. ``overrides`` pins macros
+    (the SS_DCAP_* bounds of a specialized kernel's packed descriptor)."""
     text = open(path).read()
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
     text = re.sub(r"//[^\n]*", "", text)
-    macros: dict[str, int] = {}
-    for name, val in re.findall(r"#define\s+(\w+)\s+(0x[0-9A-Fa-f]+|-?\d+)u?\b", text):
-        macros[name] = int(val, 0)
+    macros: dict[str, int] = dict(overrides or {})
+    for name, val in re.findall(r"#define\s+(\w+)[ \t]+(0x[0-9A-Fa-f]+|-?\d+|[A-Za-z_]\w*)u?[ \t]*$", text,
+                                flags=re.M):
+        if name in macros:
+            continue  # overridden, or an #ifndef default already seen
+        if val[0].isalpha() or val[0] == "_":
+            if val in macros:
+                macros[name] = macros[val]  # alias of an earlier macro
+        else:
+            macros[name] = int(val, 0)
     structs: dict[str, list[tuple[str, str, list[int]]]] = {}
     order: list[str] = []
     for m in re.finditer(r"typedef\s+struct\s+(\w+)\s*\{(.*?)\}\s*(\w+)\s*;", text, flags=re.S):
@@ -67,20 +76,25 @@ _SCALARS = {
 MACROS, _STRUCTS, _ORDER = _parse_header(HEADER)
 globals().update({k: v for k, v in MACROS.items() if k.startswith("SS_")})
 
-_TYPES: dict[str, type] = {}
-for _name in _ORDER:
-    _fields = []
-    for _fname, _ftype, _shape in _STRUCTS[_name]:
-        if _ftype.endswith("*"):
-            t = ctypes.c_void_p
-        elif _ftype in _SCALARS:
-            t = _SCALARS[_ftype]
-        else:
-            t = _TYPES[_ftype]
-        for dim in reversed(_shape):
-            t = t * dim
-        _fields.append((_fname, t))
-    _TYPES[_name] = type(_name, (ctypes.Structure,), {"_fields_": _fields})
+def _build_types(structs, order) -> dict[str, type]:
+    types: dict[str, type] = {}
+    for name in order:
+        fields = []
+        for fname, ftype, shape in structs[name]:
+            if ftype.endswith("*"):
+                t = ctypes.c_void_p
+            elif ftype in _SCALARS:
+                t = _SCALARS[ftype]
+            else:
+                t = types[ftype]
+            for dim in reversed(shape):
+                t = t * dim
+            fields.append((fname, t))
+        types[name] = type(name, (ctypes.Structure,), {"_fields_": fields})
+    return types
+
+
+_TYPES = _build_types(_STRUCTS, _ORDER)
 
 EnvDesc = _TYPES["ss_env_desc"]
 Uniforms = _TYPES["ss_uniforms"]
@@ -88,6 +102,54 @@ RngDrawArgs = _TYPES["ss_rng_draw_args"]
 Terrain = _TYPES["ss_terrain"]
 RtState = _TYPES["ss_rt_state"]
 Launch = _TYPES["ss_launch"]
+
+DCAPS = ("JOINTS", "FEET", "ACTION_TERMS", "ACTUATORS", "CMD", "RAYS", "GROUPS", "OBS_TERMS", "REWARDS",
+         "TERMINATIONS", "EVENTS", "CURRICULUM", "FIELDS", "SLOTS", "MLP_LAYERS")
+_PACKED: dict[tuple, type] = {}
+
+
+def packed_desc_type(caps: dict) -> type:
+    """ctypes class of ss_env_desc with SS_DCAP_<k> = caps[k] (a specialized
+    kernel's parameter block)."""
+    key = tuple(sorted(caps.items()))
+    t = _PACKED.get(key)
+    if t is None:
+        _, structs, order = _parse_header(HEADER, {f"SS_DCAP_{k}": int(v) for k, v in caps.items()})
+        t = _PACKED[key] = _build_types(structs, order)["ss_env_desc"]
+    return t
+
+
+def _copy_into(dst, src) -> None:
+    """Field-by-field copy between two layouts of one struct; arrays are
+    truncated to the destination's bounds (ctypes objects)."""
+    for name, t in dst._fields_:
+        sv = getattr(src, name)
+        if isinstance(sv, ctypes.Structure):
+            _copy_into(getattr(dst, name), sv)
+        elif isinstance(sv, ctypes.Array):
+            _copy_array(getattr(dst, name), sv)
+        else:
+            setattr(dst, name, sv)
+
+
+def _copy_array(dst, src) -> None:
+    n = len(dst)
+    if n and isinstance(dst[0], (ctypes.Structure, ctypes.Array)):
+        for i in range(n):
+            if isinstance(dst[i], ctypes.Structure):
+                _copy_into(dst[i], src[i])
+            else:
+                _copy_array(dst[i], src[i])
+    else:
+        dst[:n] = src[:n]
+
+
+def pack_desc(desc, caps: dict):
+    """The descriptor re-laid-out with the given SS_DCAP_* bounds."""
+    out = packed_desc_type(caps)()
+    _copy_into(out, desc)
+    return out
+
 
 # ---------------------------------------------------------------------------
 # library
@@ -116,6 +178,9 @@ _SIGNATURES = {
                     ctypes.c_int),
     "ss_jit_unload": ([ctypes.c_void_p], ctypes.c_int),
     "ss_env_step_jit": ([ctypes.c_void_p] * 4, ctypes.c_int),
+    "ss_jit_set_desc_bytes": ([ctypes.c_void_p, ctypes.c_int64], ctypes.c_int),
+    "ss_env_step_jit_packed": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
+                                ctypes.c_void_p], ctypes.c_int),
     "ss_rt_launch": ([ctypes.c_void_p] * 5, ctypes.c_int),
     "ss_rt_poll": ([ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_int32], ctypes.c_int),
     "ss_rt_release": ([ctypes.c_void_p], ctypes.c_int),

@@ -1,4 +1,20 @@
+#define SS_DCAP_JOINTS 10
+#define SS_DCAP_FEET 2
+#define SS_DCAP_ACTION_TERMS 1
+#define SS_DCAP_ACTUATORS 1
+#define SS_DCAP_CMD 2
+#define SS_DCAP_RAYS 5
+#define SS_DCAP_GROUPS 2
+#define SS_DCAP_OBS_TERMS 16
+#define SS_DCAP_REWARDS 7
+#define SS_DCAP_TERMINATIONS 3
+#define SS_DCAP_EVENTS 3
+#define SS_DCAP_CURRICULUM 2
+#define SS_DCAP_FIELDS 8
+#define SS_DCAP_SLOTS 16
+#define SS_DCAP_MLP_LAYERS 1
 #include "stridesim_b200.h"
+static_assert(sizeof(ss_env_desc) == 5144, "packed descriptor layout differs from the host packing");
 #include "ss_kernel.cuh"
 struct JitCfg {
   static constexpr bool kJit = true;
