@@ -326,10 +326,10 @@ def run_ours(args):
     # transfers cross PCIe inside the one launch; the host then synchronizes.
     A = env.action_manager.total_dim
     rng = np.random.default_rng(rank)
-    e2e_steps = max(args.steps, 200)  # ~70 us each: a longer sample smooths host/PCIe jitter
+    e2e_steps = 0 if args.no_e2e else max(args.steps, 200)  # ~70 us each: a longer sample smooths host/PCIe jitter
     host_actions = torch.from_numpy(rng.uniform(-1, 1, size=(e2e_steps, n, A))).pin_memory()
     host_views = env.enable_host_outputs()
-    for i in range(max(args.warmup, 3)):  # descriptor rebuild with the mirror + warm-up (untimed)
+    for i in range(min(max(args.warmup, 3), e2e_steps)):  # descriptor rebuild with the mirror + warm-up (untimed)
         env.step(host_actions[i])
         stream.synchronize()
     barrier(world)
@@ -340,7 +340,7 @@ def run_ours(args):
         stream.synchronize()
     e2e_t = allmax(time.perf_counter() - t0, world)
     assert host_views["reward"].shape == (n,) and host_views["reward"].device.type == "cpu"
-    e2e = {"value": n * world * e2e_steps / e2e_t, "unit": UNIT, "steps": e2e_steps, "h2d_bytes_per_step": n * A * 8,
+    e2e = None if not e2e_steps else {"value": n * world * e2e_steps / e2e_t, "unit": UNIT, "steps": e2e_steps, "h2d_bytes_per_step": n * A * 8,
            "d2h_bytes_per_step": int(env.step_outputs.numel()),
            "path": "pinned host actions -> env.step (kernel reads them over PCIe, writes obs/reward/dones "
                    "into pinned host memory) -> stream sync"}
@@ -436,6 +436,7 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the end-to-end leg (profiling runs)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--scale-envs", type=int, default=262144,
                     help="also time the step at this many worlds (HBM-bound regime); 0 disables")

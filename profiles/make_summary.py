@@ -27,7 +27,7 @@ for r in rows[h + 1:]:
         v = float(r[vi].replace(",", ""))
         v = v / 1e3 if r[ui] == "ns" else (v * 1e3 if r[ui] == "ms" else v)  # -> us
         agg[r[ki].split("(")[0][:70]].append(v)
-lines = [f"# {rnd}: launch list of `python bench.py --steps 10 --warmup 3 --no-cpu --scale-envs 0` (N=4096)",
+lines = [f"# {rnd}: launch list of `python bench.py --steps 10 --warmup 3 --no-cpu --scale-envs 0 --no-e2e` (N=4096)",
          "", "ncu `--metrics gpu__time_duration.sum --clock-control none` (cold-cache, serialised: compare shares).", "",
          "| kernel | launches | mean us | total us | share |", "|---|---|---|---|---|"]
 tot = sum(sum(v) for v in agg.values())
@@ -35,8 +35,8 @@ for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
     lines.append(f"| `{k}` | {len(v)} | {sum(v)/len(v):.1f} | {sum(v):.1f} | {100*sum(v)/tot:.1f} % |")
 ours = {k: v for k, v in agg.items() if k.startswith(("ss_step", "rng_draw", "ss::", "randomize", "heights", "fk_"))}
 t_ours = sum(sum(v) for v in ours.values())
-lines += ["", f"Own kernels: {t_ours:.1f} us of {tot:.1f} us total (the rest is the bench's L2 flush fills, "
-          "torch fills/copies of the e2e leg and the spin used to keep the host ahead)."]
+lines += ["", f"Own kernels: {t_ours:.1f} us of {tot:.1f} us total; the rest is the bench's 512 MiB L2-flush "
+          "fills before every timed step and torch fills/indexing at env setup and reset."]
 open(os.path.join(here, f"{rnd}_launches.md"), "w").write("\n".join(lines) + "\n")
 
 out = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True, text=True).stdout

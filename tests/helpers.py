@@ -55,7 +55,7 @@ def sync_from_oracle(env, ref):
     dev = env.device
 
     def put(dst, src):
-        dst.copy_(torch.as_tensor(np.ascontiguousarray(src), device=dev).to(dst.dtype).reshape(dst.shape))
+        dst.copy_(torch.as_tensor(np.array(src, copy=True), device=dev).to(dst.dtype).reshape(dst.shape))
 
     S = ref.S
     st = env.state

@@ -665,8 +665,9 @@ def test_dc_motor_envelope_on_device(rng):
     assert np.array_equal(host, _np(dev))
 
 
-@pytest.mark.parametrize("task", ["Velocity-Rough", "Velocity-Flat"])
-def test_jit_specialization_bitwise_equals_generic_kernel(task):
+@pytest.mark.parametrize("task,n", [("Velocity-Rough", 300), ("Velocity-Flat", 300), ("Velocity-Rough", 2048),
+                                    ("Velocity-Flat-Quad12", 300), ("Velocity-Rough-Humanoid10", 1100)])
+def test_jit_specialization_bitwise_equals_generic_kernel(task, n):
     """The per-env NVRTC specialization and the generic AOT kernel run the same
     source; they must agree bit for bit (no reassociation, --fmad=false)."""
     from paper_2601_22074_b200 import jit
@@ -674,8 +675,8 @@ def test_jit_specialization_bitwise_equals_generic_kernel(task):
     from paper_2601_22074_b200.policies import random_policy
     from paper_2601_22074_b200.tasks import make_env_cfg
 
-    a = ManagerBasedRlEnv(make_env_cfg(task, num_envs=300, seed=4))
-    b = ManagerBasedRlEnv(make_env_cfg(task, num_envs=300, seed=4))
+    a = ManagerBasedRlEnv(make_env_cfg(task, num_envs=n, seed=4))
+    b = ManagerBasedRlEnv(make_env_cfg(task, num_envs=n, seed=4))
     assert a.use_jit
     b.use_jit = False
     oa, ob = a.reset(), b.reset()

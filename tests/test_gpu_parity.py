@@ -147,7 +147,11 @@ def test_random_policy_bit_exact():
         env.step(a)
 
 
-@pytest.mark.parametrize("task,n,seed", [("Velocity-Rough", 257, 11), ("Velocity-Flat", 64, 0)])
+@pytest.mark.parametrize("task,n,seed", [("Velocity-Rough", 257, 11), ("Velocity-Flat", 64, 0),
+                                         # N >= 1024: the world count is folded into the specialized kernel
+                                         ("Velocity-Rough", 1536, 7),
+                                         # planar surrogates of BASELINE configs 0/1
+                                         ("Velocity-Flat-Quad12", 96, 2), ("Velocity-Rough-Humanoid10", 129, 5)])
 def test_env_matches_oracle_lockstep(task, n, seed):
     """Random-action lockstep vs the oracle on non-golden sizes: 10 free steps
     within fp32 tolerance, then 60 teacher-forced steps bit-exact in flags."""
