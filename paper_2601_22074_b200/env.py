@@ -157,6 +157,7 @@ class ManagerBasedRlEnv:
         self._rt_ref = ctypes.byref(self._rt)
         self._la = native.Launch()
         self._la_ref = ctypes.byref(self._la)
+        self._la_key = None  # (stages, nsub, flags, groups_mask) last written into _la
         self._rt.global_step = 0
         self._rt.sensor_last_update = -1
         # nonfinite bookkeeping: zero-copy flags (mapped pinned memory) + a ring of
@@ -329,16 +330,13 @@ class ManagerBasedRlEnv:
             self._desc_ref = ctypes.byref(d)
         return self._desc
 
-    def _launch(self, stages: int, nsub: int = 0, actions=None, reset_mask=None, groups_mask: int = 0,
-                flags: int = 0) -> None:
-        """One launch through the native runtime (ss_rt_launch): it derives the
-        per-step uniforms from the shared ss_rt_state, launches the
-        specialized (or generic) kernel and advances the counters."""
-        if isinstance(actions, RandomActions):
-            slot = self.streams.slot("policy.random")  # first use invalidates the descriptor
+    def _prepare_launch(self) -> None:
+        """(Re)build the descriptor and, for the specialized kernel, its module
+        handle and packed parameter block."""
         d = self._desc if self._desc is not None else self._get_desc()
         if self._desc is None:  # a stream slot was allocated while building
             d = self._get_desc()
+        la = self._la
         if self.use_jit and self._jit_handle is None:
             try:
                 self._jit_handle = jit.module_for(d)
@@ -348,29 +346,41 @@ class ManagerBasedRlEnv:
             except jit.JitUnsupported as err:
                 warnings.warn(f"per-env specialization unavailable ({err}); using the generic sm_100a kernel")
                 self.use_jit = False
+        if self.use_jit:
+            la.jit_desc = ctypes.addressof(self._jit_packed)
+            la.jit_desc_bytes = ctypes.sizeof(self._jit_packed)
+        else:
+            la.jit_desc = None
+            la.jit_desc_bytes = 0
+
+    def _launch(self, stages: int, nsub: int = 0, actions=None, reset_mask=None, groups_mask: int = 0,
+                flags: int = 0) -> None:
+        """One launch through the native runtime (ss_rt_launch): it derives the
+        per-step uniforms from the shared ss_rt_state, launches the
+        specialized (or generic) kernel and advances the counters."""
+        fused = actions.__class__ is RandomActions
+        if fused:
+            slot = self.streams.slot("policy.random")  # first use invalidates the descriptor
+        if self._desc is None or (self.use_jit and self._jit_handle is None):
+            self._prepare_launch()
         rt = self._rt
         term = stages & native.SS_ST_TERM
         if term:
             # the launch retires old nonfinite slots itself (poll_keep)
             self.termination_manager.last_nonfinite = self._nf_views[rt.nf_slot]
         la = self._la
-        la.stages = stages
-        la.nsub = nsub
-        la.flags = flags
-        la.groups_mask = groups_mask
-        if isinstance(actions, RandomActions):
+        key = (stages, nsub, flags, groups_mask)
+        if key != self._la_key:  # the fused step repeats one signature: skip the ctypes writes
+            la.stages, la.nsub, la.flags, la.groups_mask = key
+            la.poll_keep = NF_LAG if term else -1
+            self._la_key = key
+        if fused:
             la.actions = None
             la.policy_slot, la.policy_lo, la.policy_hi = slot, float(actions.low), float(actions.high)
         else:
             la.actions = None if actions is None else actions.data_ptr()
             la.policy_slot = -1
         la.reset_mask = None if reset_mask is None else reset_mask.data_ptr()
-        la.poll_keep = NF_LAG if term else -1
-        if self.use_jit:
-            la.jit_desc = ctypes.addressof(self._jit_packed)
-            la.jit_desc_bytes = ctypes.sizeof(self._jit_packed)
-        else:
-            la.jit_desc = None
         rt.sim_step = self.state.sim_step
         native.LAUNCHES["count"] += 1
         rc = self._lib.ss_rt_launch(self._desc_ref, self._rt_ref, self._la_ref,
@@ -494,7 +504,7 @@ class ManagerBasedRlEnv:
         om = self.observation_manager
         om._cache.clear()
         if not self.staged:
-            mask = om.begin(list(om.groups))
+            mask = om.begin_all()
             self._launch(native.SS_ST_STEP_ALL, nsub=self.decimation, actions=a, groups_mask=mask)
             self.curriculum_manager.run_host(None)
         else:

@@ -83,6 +83,13 @@ class ActionManager:
 
         from ..policies import RandomActions
 
+        if actions.__class__ is torch.Tensor:
+            # fast path: the common well-formed inputs (a few C-level checks)
+            a = actions
+            if a.dtype is torch.float64 and a.shape == self._shape and a.is_contiguous():
+                dev = a.get_device()
+                if dev == self._dev_index or (dev < 0 and self._pinned(a)):
+                    return a
         if isinstance(actions, RandomActions):
             return actions
         if torch.is_tensor(actions):
@@ -102,6 +109,14 @@ class ActionManager:
         if a.dtype != torch.float64 or a.device != self.env.device or not a.is_contiguous():
             a = a.to(device=self.env.device, dtype=torch.float64).contiguous()
         return a
+
+    @property
+    def _shape(self):
+        return (self.env.num_envs, self.total_dim)
+
+    @property
+    def _dev_index(self) -> int:
+        return self.env._dev_index
 
     def _pinned(self, a) -> bool:
         """is_pinned() with a small cache of known pinned storages (the query

@@ -51,9 +51,12 @@ class CurriculumManager:
 
     def run_host(self, reset_ids=None) -> None:
         """Host-side terms after a fused step (their result feeds the next step)."""
-        for name, fn in self.terms.items():
-            if self.kind(name) == "host":
-                fn(self.env, reset_ids, **self.cfg[name].params)
+        host = self.__dict__.get("_host_terms")
+        if host is None:  # the term set is fixed at construction
+            host = self._host_terms = [(fn, self.cfg[name].params) for name, fn in self.terms.items()
+                                       if self.kind(name) == "host"]
+        for fn, params in host:
+            fn(self.env, reset_ids, **params)
 
     def run_external(self, reset_ids) -> None:
         for name, fn in self.terms.items():

@@ -197,6 +197,13 @@ class ObservationManager:
             self._cache[g] = step
         return mask
 
+    def begin_all(self) -> int:
+        """begin() for every group (the fused step)."""
+        step = self.env.global_step
+        for g in self.groups:
+            self._cache[g] = step
+        return (1 << len(self.groups)) - 1
+
     def compute(self, group: str):
         """Group output (N, sum of term dims x history) (managers/observation.py:99-137)."""
         if group not in self.groups:
