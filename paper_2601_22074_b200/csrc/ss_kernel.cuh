@@ -130,6 +130,39 @@ __device__ __forceinline__ double height_raw(const ss_env_desc& d, double x) {
     return __ldg(t.samples + idx) * (1.0 - frac) + __ldg(t.samples + idx + 1) * frac;
 }
 
+// the ray scan: all NR lookups' indices first, then every sample load, then
+// the interpolations -- one L2 round trip for the whole scan instead of one
+// per ray (height_raw's result, ray by ray)
+template <class C, int NR>
+__device__ __forceinline__ void height_raw_n(const ss_env_desc& d, const double (&x)[NR], double (&out)[NR]) {
+    const ss_terrain& t = d.terrain;
+    if (t.n_samples < 2) {
+#pragma unroll
+        for (int r = 0; r < NR; ++r) out[r] = 0.0;
+        return;
+    }
+    const int64_t last = t.n_samples - 1;
+    const double inv = 1.0 / t.spacing;
+    int64_t idx[NR];
+    double frac[NR], a[NR], b[NR];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+        double pos = div_rn(finite_(x[r]) ? x[r] : 0.0, t.spacing, inv);
+        pos = np_clip(pos, 0.0, (double)last);
+        int64_t i = (int64_t)pos;
+        i = i > last - 1 ? last - 1 : i;
+        idx[r] = i;
+        frac[r] = pos - (double)i;
+    }
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+        a[r] = __ldg(t.samples + idx[r]);
+        b[r] = __ldg(t.samples + idx[r] + 1);
+    }
+#pragma unroll
+    for (int r = 0; r < NR; ++r) out[r] = a[r] * (1.0 - frac[r]) + b[r] * frac[r];
+}
+
 template <int KM, int FM>
 struct World {
     double q[3 + KM], qd[3 + KM], ctrl[KM];
@@ -724,12 +757,18 @@ __device__ __forceinline__ void obs_raw(const ss_env_desc& d, int t, int w, cons
         case SS_OBS_SIM_TIME:
             v[0] = s.time;
             break;
-        case SS_OBS_HEIGHT_SCAN:
+        case SS_OBS_HEIGHT_SCAN: {
             // RayScanner.read (sensors.py:36-46): h(x_base + off) - z_base
+            constexpr int NR = C::kJit ? C::kRays : SS_MAX_RAYS;
+            double xr[NR], hr[NR];
 #pragma unroll
-            for (int r = 0; r < SS_MAX_RAYS; ++r)
-                if (r < C::n_rays(d)) v[r] = height_raw(d, s.eq[0] + C::ray_offset(d, r)) - s.eq[1];
+            for (int r = 0; r < NR; ++r) xr[r] = s.eq[0] + (r < C::n_rays(d) ? C::ray_offset(d, r) : 0.0);
+            height_raw_n<C, NR>(d, xr, hr);
+#pragma unroll
+            for (int r = 0; r < NR; ++r)
+                if (r < C::n_rays(d)) v[r] = hr[r] - s.eq[1];
             break;
+        }
         case SS_OBS_FOOT_CONTACT_FORCES:
 #pragma unroll
             for (int i = 0; i < FM; ++i) {

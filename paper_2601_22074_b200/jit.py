@@ -97,7 +97,8 @@ def config_source(d) -> str:
     soff = [sum(dims[:g]) for g in range(len(dims))] + [0] * (native.SS_MAX_GROUPS - len(dims))
     block = block_size()
     stage = int(sum(dims) > 0 and block * sum(dims) * 8 <= 48 * 1024 and os.environ.get("SS_STAGE_OBS", "1") != "0")
-    lines += [f"  static constexpr int kBlock = {block}, kStageObs = {stage}, kObsTotal = {max(sum(dims), 1)};",
+    lines += [f"  static constexpr int kBlock = {block}, kStageObs = {stage}, kObsTotal = {max(sum(dims), 1)}, "
+              f"kRays = {max(int(d.n_rays), 1)};",
               f"  static __device__ __forceinline__ int g_soff(const ss_env_desc&, int g) {{ constexpr int a[{native.SS_MAX_GROUPS}] = "
               f"{{{', '.join(str(x) for x in soff)}}}; return a[g]; }}"]
     head = "  static __device__ __forceinline__"

@@ -11,7 +11,17 @@ from paper_2601_22074_b200.policies import random_policy  # noqa: E402
 from paper_2601_22074_b200.tasks import make_env_cfg  # noqa: E402
 
 n = int(os.environ.get("N", "4096"))
-env = ManagerBasedRlEnv(make_env_cfg(os.environ.get("TASK", "Velocity-Rough"), num_envs=n))
+cfg = make_env_cfg(os.environ.get("TASK", "Velocity-Rough"), num_envs=n)
+if os.environ.get("NO_NOISE"):  # experiment: observation noise off
+    from paper_2601_22074_b200.config import NoiseCfg
+    for g in cfg.observations.values():
+        for t in g.terms.values():
+            t.noise = NoiseCfg()
+if os.environ.get("NO_SCAN"):  # experiment: no height scan term
+    cfg.observations["critic"].terms.pop("height_scan", None)
+if os.environ.get("NO_CRITIC"):  # experiment: policy group only
+    cfg.observations.pop("critic", None)
+env = ManagerBasedRlEnv(cfg)
 probe = torch.zeros(16, dtype=torch.int64, device="cuda")
 env.reset()
 env._probe_ptr = probe.data_ptr()

@@ -26,7 +26,7 @@ struct JitCfg {
   static constexpr int kCapEvents = 3;
   static constexpr int kCapGroups = 2;
   static constexpr int kCapObs = 16;
-  static constexpr int kBlock = 64, kStageObs = 1, kObsTotal = 47;
+  static constexpr int kBlock = 64, kStageObs = 1, kObsTotal = 47, kRays = 5;
   static __device__ __forceinline__ int g_soff(const ss_env_desc&, int g) { constexpr int a[4] = {0, 19, 0, 0}; return a[g]; }
   static __device__ __forceinline__ int NW(const ss_env_desc&) { return 4096; }
   static __device__ __forceinline__ int cap_phys(const ss_env_desc&) { return 220; }
