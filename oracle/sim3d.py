@@ -1,0 +1,650 @@
+"""numpy float64 oracle of the 3-D articulated path -- TEST INFRASTRUCTURE ONLY.
+
+PARITY UNPINNED with respect to the reference: the reference is planar
+(SPEC.md:8 drops MuJoCo Warp and 3-D dynamics; sim/physics.py:1-11) and no
+MuJoCo / MJWarp / mjlab is installed here, so there is no 3-D golden vector to
+pin against. This module is this repo's own restatement of the published
+MuJoCo pipeline stages, one function per stage, written as the specification
+the CUDA kernel (paper_2601_22074_b200/csrc/s3_kernel.cuh) follows operation
+for operation. It is pinned instead by analytic properties
+(tests/test_sim3d_oracle_cpu.py): FK vs independent rotation composition,
+1/2 qd^T M qd == kinetic energy summed over bodies, L^T D L == M, the point
+Jacobian == finite differences of FK, RNE == Lagrangian finite differences
+(fixed base), free fall exact, energy conservation, Newton KKT optimality
+and the friction-cone bound of the contact forces.
+
+Stages (MuJoCo names in brackets):
+  kinematics [mj_kinematics] -> com [mj_comPos] (subtree com, cinert, cdof)
+  -> crb [mj_crb] (M) -> factor [mj_factorM] (tree-sparse L^T D L)
+  -> com_vel [mj_comVel] -> rne [mj_rne, no acc] -> passive + actuation
+  -> qacc_smooth -> collision (broadphase + primitive narrowphase)
+  -> constraints (limits + pyramidal contacts, soft impedance)
+  -> Newton solver with exact line search [mj_solNewton]
+  -> implicitfast [mj_implicitSkip] -> integrate [mj_integratePos].
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from paper_2601_22074_b200.sim3d.model import (ACT_DC, ACT_IMPLICIT, GEOM_BOX, GEOM_CAPSULE, GEOM_HFIELD,
+                                               GEOM_PLANE, GEOM_SPHERE, JNT_FREE, MAX_CON, MAX_LIM)
+
+MINVAL = 1e-15
+
+
+# ----------------------------------------------------------------------------- small math
+
+
+def qmul(a, b):
+    aw, ax, ay, az = a
+    bw, bx, by, bz = b
+    return np.array([aw * bw - ax * bx - ay * by - az * bz,
+                     aw * bx + ax * bw + ay * bz - az * by,
+                     aw * by - ax * bz + ay * bw + az * bx,
+                     aw * bz + ax * by - ay * bx + az * bw])
+
+
+def qmat(q):
+    w, x, y, z = q
+    return np.array([[1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y)],
+                     [2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)],
+                     [2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)]])
+
+
+def qnormalize(q):
+    return q / np.sqrt(q @ q)
+
+
+def qaxisangle(axis, angle):
+    s, c = np.sin(0.5 * angle), np.cos(0.5 * angle)
+    return np.array([c, axis[0] * s, axis[1] * s, axis[2] * s])
+
+
+def cross_motion(v, u):
+    """[w x u_ang ; w x u_lin + v_lin x u_ang] (mju_crossMotion)."""
+    w, vl = v[:3], v[3:]
+    return np.concatenate([np.cross(w, u[:3]), np.cross(w, u[3:]) + np.cross(vl, u[:3])])
+
+
+def cross_force(v, f):
+    """[w x f_ang + v_lin x f_lin ; w x f_lin] (mju_crossForce)."""
+    w, vl = v[:3], v[3:]
+    return np.concatenate([np.cross(w, f[:3]) + np.cross(vl, f[3:]), np.cross(w, f[3:])])
+
+
+def inert_mul(ci, v):
+    """10-vector spatial inertia (Ixx Iyy Izz Ixy Ixz Iyz mdx mdy mdz m) times a motion vector."""
+    I = np.array([[ci[0], ci[3], ci[4]], [ci[3], ci[1], ci[5]], [ci[4], ci[5], ci[2]]])
+    md, m = ci[6:9], ci[9]
+    w, vl = v[:3], v[3:]
+    return np.concatenate([I @ w + np.cross(md, vl), m * vl - np.cross(md, w)])
+
+
+# ----------------------------------------------------------------------------- stages
+
+
+def kinematics(m, qpos):
+    """Body frames in topological order (mj_kinematics)."""
+    nb = m.nbody
+    xpos = np.zeros((nb, 3))
+    xquat = np.zeros((nb, 4))
+    xquat[0] = (1, 0, 0, 0)
+    xmat = np.zeros((nb, 3, 3))
+    xmat[0] = np.eye(3)
+    xanchor = np.zeros((m.njnt, 3))
+    xaxis = np.zeros((m.njnt, 3))
+    for b in range(1, nb):
+        p = m.body_parentid[b]
+        pos = xpos[p] + xmat[p] @ m.body_pos[b]
+        quat = qmul(xquat[p], m.body_quat[b])
+        for j in range(m.body_jntadr[b], m.body_jntadr[b] + m.body_jntnum[b]):
+            a = m.jnt_qposadr[j]
+            if m.jnt_type[j] == JNT_FREE:
+                pos = qpos[a:a + 3].copy()
+                quat = qnormalize(qpos[a + 3:a + 7])
+                xanchor[j] = pos
+                xaxis[j] = (0, 0, 1)
+            else:
+                R = qmat(quat)
+                xanchor[j] = R @ m.jnt_pos[j] + pos
+                xaxis[j] = R @ m.jnt_axis[j]
+                quat = qmul(quat, qaxisangle(m.jnt_axis[j], qpos[a] - m.qpos0[a]))
+                pos = xanchor[j] - qmat(quat) @ m.jnt_pos[j]
+        quat = qnormalize(quat)
+        xquat[b] = quat
+        xmat[b] = qmat(quat)
+        xpos[b] = pos
+    xipos = xpos + np.einsum("bij,bj->bi", xmat, m.body_ipos)
+    ximat = np.array([xmat[b] @ qmat(m.body_iquat[b]) for b in range(nb)])
+    gxpos = xpos[m.geom_bodyid] + np.einsum("gij,gj->gi", xmat[m.geom_bodyid], m.geom_pos)
+    gxmat = np.array([xmat[m.geom_bodyid[g]] @ qmat(m.geom_quat[g]) for g in range(m.ngeom)])
+    return dict(xpos=xpos, xquat=xquat, xmat=xmat, xipos=xipos, ximat=ximat, xanchor=xanchor, xaxis=xaxis,
+                geom_xpos=gxpos, geom_xmat=gxmat)
+
+
+def com_pos(m, K):
+    """Subtree com of the (single) tree, cinert about it, cdof (mj_comPos)."""
+    mass = m.body_mass[1:]
+    com = (mass[:, None] * K["xipos"][1:]).sum(0) / mass.sum()
+    cinert = np.zeros((m.nbody, 10))
+    for b in range(1, m.nbody):
+        R = K["ximat"][b]
+        I = R @ np.diag(m.body_inertia[b]) @ R.T
+        d = K["xipos"][b] - com
+        mb = m.body_mass[b]
+        I = I + mb * ((d @ d) * np.eye(3) - np.outer(d, d))
+        cinert[b] = (I[0, 0], I[1, 1], I[2, 2], I[0, 1], I[0, 2], I[1, 2], mb * d[0], mb * d[1], mb * d[2], mb)
+    cdof = np.zeros((m.nv, 6))
+    for j in range(m.njnt):
+        b, da = m.jnt_bodyid[j], m.jnt_dofadr[j]
+        if m.jnt_type[j] == JNT_FREE:
+            for i in range(3):
+                cdof[da + i, 3 + i] = 1.0
+            off = com - K["xanchor"][j]
+            for i in range(3):
+                ax = K["xmat"][b][:, i]
+                cdof[da + 3 + i] = np.concatenate([ax, np.cross(ax, off)])
+        else:
+            ax = K["xaxis"][j]
+            cdof[da] = np.concatenate([ax, np.cross(ax, com - K["xanchor"][j])])
+    return dict(com=com, cinert=cinert, cdof=cdof)
+
+
+def crb(m, C):
+    """Composite inertia + dense symmetric M over ancestor pairs (mj_crb); armature on the diagonal."""
+    c = C["cinert"].copy()
+    for b in range(m.nbody - 1, 0, -1):
+        p = m.body_parentid[b]
+        if p > 0:
+            c[p] += c[b]
+    M = np.zeros((m.nv, m.nv))
+    for i in range(m.nv):
+        f = inert_mul(c[m.dof_bodyid[i]], C["cdof"][i])
+        j = i
+        while j >= 0:
+            M[i, j] = M[j, i] = C["cdof"][j] @ f
+            j = m.dof_parentid[j]
+        M[i, i] += m.dof_armature[i]
+    return M, c
+
+
+def factor_ldl(m, M):
+    """Tree-sparse L^T D L (mj_factorM): returns qLD with D on the diagonal and L below it
+    (only ancestor entries are touched; no fill-in for a kinematic tree)."""
+    L = M.copy()
+    par = m.dof_parentid
+    for k in range(m.nv - 1, -1, -1):
+        i = par[k]
+        while i >= 0:
+            t = L[k, i] / L[k, k]
+            j = i
+            while j >= 0:
+                L[i, j] -= t * L[k, j]
+                j = par[j]
+            L[k, i] = t
+            i = par[i]
+    return L
+
+
+def solve_ldl(m, L, b):
+    x = b.copy()
+    par = m.dof_parentid
+    for i in range(m.nv - 1, -1, -1):
+        j = par[i]
+        while j >= 0:
+            x[j] -= L[i, j] * x[i]
+            j = par[j]
+    x = x / np.diag(L)
+    for i in range(m.nv):
+        j = par[i]
+        while j >= 0:
+            x[i] -= L[i, j] * x[j]
+            j = par[j]
+    return x
+
+
+def com_vel(m, C, qvel):
+    """cvel per body and cdof_dot per dof (mj_comVel)."""
+    cvel = np.zeros((m.nbody, 6))
+    cdofd = np.zeros((m.nv, 6))
+    for b in range(1, m.nbody):
+        v = cvel[m.body_parentid[b]].copy()
+        for j in range(m.body_jntadr[b], m.body_jntadr[b] + m.body_jntnum[b]):
+            da = m.jnt_dofadr[j]
+            if m.jnt_type[j] == JNT_FREE:
+                for i in range(3):
+                    v = v + C["cdof"][da + i] * qvel[da + i]
+                for i in range(3, 6):
+                    cdofd[da + i] = cross_motion(v, C["cdof"][da + i])
+                for i in range(3, 6):
+                    v = v + C["cdof"][da + i] * qvel[da + i]
+            else:
+                cdofd[da] = cross_motion(v, C["cdof"][da])
+                v = v + C["cdof"][da] * qvel[da]
+        cvel[b] = v
+    return cvel, cdofd
+
+
+def rne(m, C, cvel, cdofd, qvel):
+    """Bias forces C(q,qd) qd + g(q) (mj_rne with qacc = 0); gravity as a base acceleration."""
+    g = np.asarray(m.opt.gravity, dtype=np.float64)
+    cacc = np.zeros((m.nbody, 6))
+    cacc[0, 3:] = -g
+    cfrc = np.zeros((m.nbody, 6))
+    for b in range(1, m.nbody):
+        a = cacc[m.body_parentid[b]].copy()
+        da, nd = m.body_dofadr[b], m.body_dofnum[b]
+        for d in range(da, da + nd) if nd else ():
+            a = a + cdofd[d] * qvel[d]
+        cacc[b] = a
+        ci = C["cinert"][b]
+        cfrc[b] = inert_mul(ci, a) + cross_force(cvel[b], inert_mul(ci, cvel[b]))
+    for b in range(m.nbody - 1, 0, -1):
+        p = m.body_parentid[b]
+        if p > 0:
+            cfrc[p] += cfrc[b]
+    bias = np.array([C["cdof"][i] @ cfrc[m.dof_bodyid[i]] for i in range(m.nv)])
+    return bias
+
+
+def actuation(m, qpos, qvel, ctrl):
+    """Joint-space actuator forces and the implicit velocity derivative per dof.
+    ctrl is the position target per actuator. PD / DC follow actuators.py:104-117 of the
+    reference (explicit kd); IMPLICIT is a position actuator kp (ctrl - q) - kv qd whose kv
+    enters implicitfast (skipped when the force range clamps it)."""
+    f = np.zeros(m.nv)
+    kvd = np.zeros(m.nv)
+    for u in range(m.nu):
+        d, a = m.actuator_dofadr[u], m.actuator_qposadr[u]
+        kp, kv, eff = m.actuator_kp[u], m.actuator_kv[u], m.actuator_effort[u]
+        q, qd = qpos[a], qvel[d]
+        tau = kp * (ctrl[u] - q) + kv * (0.0 - qd)
+        if m.actuator_kind[u] == ACT_DC:
+            sat, vmax = m.actuator_saturation[u], m.actuator_vmax[u]
+            hi = min(max(sat * (1.0 - qd / vmax), 0.0), eff)
+            lo = min(max(sat * (-1.0 - qd / vmax), -eff), 0.0)
+            tau = min(max(tau, lo), hi)
+        else:
+            clamped = tau > eff or tau < -eff
+            tau = min(max(tau, -eff), eff)
+            if m.actuator_kind[u] == ACT_IMPLICIT and not clamped:
+                kvd[d] += kv
+        f[d] += tau
+    return f, kvd
+
+
+# ----------------------------------------------------------------------------- collision
+
+
+def make_frame(n):
+    e = np.array([0.0, 1.0, 0.0]) if abs(n[1]) < 0.5 else np.array([1.0, 0.0, 0.0])
+    t1 = np.cross(n, e)
+    t1 = t1 / np.sqrt(t1 @ t1)
+    t2 = np.cross(n, t1)
+    return np.array([n, t1, t2])
+
+
+def hfield_point(m, q, r):
+    """Signed distance of a sphere (centre q, radius r) to the heightfield triangle under q.
+    Grid rows run along y, columns along x; each cell is split along the (0,0)-(1,1) diagonal."""
+    H = m.hfield_data
+    nr, nc = H.shape
+    sp = m.hfield_spacing
+    fx = (q[0] - m.hfield_origin[0]) / sp
+    fy = (q[1] - m.hfield_origin[1]) / sp
+    if not (fx >= 0.0 and fy >= 0.0 and fx < nc - 1 and fy < nr - 1):
+        return None
+    ix, iy = int(np.floor(fx)), int(np.floor(fy))
+    u, v = fx - ix, fy - iy
+    x0 = m.hfield_origin[0] + ix * sp
+    y0 = m.hfield_origin[1] + iy * sp
+    h00, h10, h01, h11 = H[iy, ix], H[iy, ix + 1], H[iy + 1, ix], H[iy + 1, ix + 1]
+    if u >= v:  # triangle (0,0) (1,0) (1,1)
+        n = np.array([-(h10 - h00) * sp, -(h11 - h10) * sp, sp * sp])
+        v0 = np.array([x0, y0, h00])
+    else:       # triangle (0,0) (1,1) (0,1)
+        n = np.array([-(h11 - h01) * sp, -(h01 - h00) * sp, sp * sp])
+        v0 = np.array([x0, y0, h00])
+    n = n / np.sqrt(n @ n)
+    d = n @ (q - v0) - r
+    return d, n
+
+
+def seg_closest(p1, q1, p2, q2):
+    d1, d2, r = q1 - p1, q2 - p2, p1 - p2
+    a, e, f = d1 @ d1, d2 @ d2, d2 @ r
+    c, b = d1 @ r, d1 @ d2
+    if e <= 1e-12:  # second segment degenerate (a sphere centre)
+        s = min(max(-c / a, 0.0), 1.0) if a > 1e-12 else 0.0
+        return p1 + d1 * s, p2
+    if a <= 1e-12:
+        t = min(max(f / e, 0.0), 1.0)
+        return p1, p2 + d2 * t
+    den = a * e - b * b
+    s = min(max((b * f - c * e) / den, 0.0), 1.0) if den > 1e-12 else 0.0
+    t = (b * s + f) / e
+    if t < 0.0:
+        t = 0.0
+        s = min(max(-c / a, 0.0), 1.0)
+    elif t > 1.0:
+        t = 1.0
+        s = min(max((b - c) / a, 0.0), 1.0)
+    return p1 + d1 * s, p2 + d2 * t
+
+
+def _sphere_sphere(c1, r1, c2, r2):
+    dv = c2 - c1
+    L = np.sqrt(dv @ dv)
+    n = dv / L if L > 1e-12 else np.array([0.0, 0.0, 1.0])
+    d = L - r1 - r2
+    return d, n, c1 + n * (r1 + 0.5 * d)
+
+
+def _segment(m, K, g):
+    a = K["geom_xmat"][g][:, 2] * m.geom_size[g][1]
+    c = K["geom_xpos"][g]
+    return c - a, c + a
+
+
+def _point_set(m, K, g):
+    """Points + radii standing in for geom g against the terrain."""
+    t, s = m.geom_type[g], m.geom_size[g]
+    c = K["geom_xpos"][g]
+    if t == GEOM_SPHERE:
+        return [(c, s[0])]
+    if t == GEOM_CAPSULE:
+        p, q = _segment(m, K, g)
+        return [(p, s[0]), (q, s[0])]
+    R = K["geom_xmat"][g]
+    out = []
+    for i in range(8):
+        loc = np.array([s[0] if i & 1 else -s[0], s[1] if i & 2 else -s[1], s[2] if i & 4 else -s[2]])
+        out.append((c + R @ loc, 0.0))
+    return out
+
+
+def collide(m, K):
+    """Broadphase (bounding spheres) + narrowphase over the compiled candidate pairs, in pair order;
+    at most MAX_CON contacts (later ones dropped and counted)."""
+    cons, dropped = [], 0
+    hmax = float(m.hfield_data.max())
+    for p, (g1, g2) in enumerate(m.pair_geom):
+        t1, t2 = m.geom_type[g1], m.geom_type[g2]
+        c1, c2 = K["geom_xpos"][g1], K["geom_xpos"][g2]
+        mu = max(m.geom_friction[g1], m.geom_friction[g2])
+        found = []
+        if t1 == GEOM_PLANE:
+            n = K["geom_xmat"][g1][:, 2]
+            if n @ (c2 - c1) - m.geom_rbound[g2] >= 0.0:
+                continue
+            for q, r in _point_set(m, K, g2):
+                d = n @ (q - c1) - r
+                if d < 0.0:
+                    found.append((d, n, q - n * (r + 0.5 * d)))
+        elif t1 == GEOM_HFIELD:
+            if c2[2] - m.geom_rbound[g2] >= hmax:
+                continue
+            for q, r in _point_set(m, K, g2):
+                h = hfield_point(m, q, r)
+                if h is not None and h[0] < 0.0:
+                    d, n = h
+                    found.append((d, n, q - n * (r + 0.5 * d)))
+        else:
+            dv = c2 - c1
+            rb = m.geom_rbound[g1] + m.geom_rbound[g2]
+            if dv @ dv >= rb * rb:
+                continue
+            r1, r2 = m.geom_size[g1][0], m.geom_size[g2][0]
+            if t1 == GEOM_SPHERE and t2 == GEOM_SPHERE:
+                a, b = c1, c2
+            elif t1 == GEOM_SPHERE:
+                p2, q2 = _segment(m, K, g2)
+                b, a = seg_closest(p2, q2, c1, c1)
+            elif t2 == GEOM_SPHERE:
+                p1, q1 = _segment(m, K, g1)
+                a, b = seg_closest(p1, q1, c2, c2)
+            else:
+                p1, q1 = _segment(m, K, g1)
+                p2, q2 = _segment(m, K, g2)
+                a, b = seg_closest(p1, q1, p2, q2)
+            d, n, pos = _sphere_sphere(a, r1, b, r2)
+            if d < 0.0:
+                found.append((d, n, pos))
+        if t2 == GEOM_BOX:
+            found = found[:4]
+        for d, n, pos in found:
+            if len(cons) >= MAX_CON:
+                dropped += 1
+                continue
+            cons.append(dict(dist=d, pos=pos, frame=make_frame(n), mu=mu, pair=p, geom1=g1, geom2=g2))
+    return cons, dropped
+
+
+# ----------------------------------------------------------------------------- constraints
+
+
+def point_jac(m, C, b, p):
+    """3 x nv translational Jacobian of world point p attached to body b (mj_jac)."""
+    J = np.zeros((3, m.nv))
+    for d in m.body_chain[b]:
+        J[:, d] = C["cdof"][d][3:] + np.cross(C["cdof"][d][:3], p - C["com"])
+    return J
+
+
+def impedance(r, solimp):
+    dmin, dmax, width, mid, power = solimp
+    x = abs(r) / width
+    if x >= 1.0:
+        d = dmax
+    else:
+        y = x ** power / mid ** (power - 1) if x <= mid else 1.0 - (1.0 - x) ** power / (1.0 - mid) ** (power - 1)
+        d = dmin + y * (dmax - dmin)
+    return min(max(d, 1e-4), 0.9999)
+
+
+def constraints(m, C, cons, qpos, qvel):
+    """Rows: active joint limits (dof order), then 4 pyramid edges per contact
+    [n + mu t1, n - mu t1, n + mu t2, n - mu t2]. Each row: dense J (nv), pos, aref, D."""
+    rows = []
+    for j in range(m.njnt):
+        if not m.jnt_limited[j]:
+            continue
+        a, d = m.jnt_qposadr[j], m.jnt_dofadr[j]
+        lo, hi = m.jnt_range[j]
+        for dist, sgn in ((qpos[a] - lo, 1.0), (hi - qpos[a], -1.0)):
+            if dist < 0.0 and len(rows) < MAX_LIM:
+                J = np.zeros(m.nv)
+                J[d] = sgn
+                rows.append(dict(J=J, pos=dist, A=m.dof_invweight0[d]))
+    nlim = len(rows)
+    for c in cons:
+        b1, b2 = m.geom_bodyid[c["geom1"]], m.geom_bodyid[c["geom2"]]
+        Jp = point_jac(m, C, b2, c["pos"]) - point_jac(m, C, b1, c["pos"])
+        Jc = c["frame"] @ Jp
+        mu = c["mu"]
+        A = (1.0 + mu * mu) * (m.body_invweight0[b1] + m.body_invweight0[b2])
+        for k in (1, 2):
+            for s in (1.0, -1.0):
+                rows.append(dict(J=Jc[0] + (s * mu) * Jc[k], pos=c["dist"], A=A))
+    tc = max(m.opt.solref[0], 2.0 * m.opt.timestep)
+    dr = m.opt.solref[1]
+    dmax = m.opt.solimp[1]
+    kk = 1.0 / (dmax * dmax * tc * tc * dr * dr)
+    bb = 2.0 / (dmax * tc)
+    nefc = len(rows)
+    J = np.array([r["J"] for r in rows]).reshape(nefc, m.nv)
+    pos = np.array([r["pos"] for r in rows])
+    imp = np.array([impedance(p, m.opt.solimp) for p in pos])
+    A = np.array([r["A"] for r in rows])
+    R = np.maximum((1.0 - imp) / imp * A, MINVAL)
+    vel = J @ qvel
+    aref = -bb * vel - kk * imp * pos
+    return dict(J=J, pos=pos, aref=aref, D=1.0 / R, R=R, imp=imp, nlim=nlim, nefc=nefc)
+
+
+def cholesky(H):
+    """Right-looking dense Cholesky H = L L^T (lower)."""
+    n = H.shape[0]
+    L = H.copy()
+    for k in range(n):
+        L[k, k] = np.sqrt(L[k, k])
+        L[k + 1:, k] = L[k + 1:, k] / L[k, k]
+        L[k + 1:, k + 1:] -= np.outer(L[k + 1:, k], L[k + 1:, k])
+    return np.tril(L)
+
+
+def chol_solve(L, b):
+    n = L.shape[0]
+    y = b.copy()
+    for i in range(n):
+        y[i] = (y[i] - L[i, :i] @ y[:i]) / L[i, i]
+    x = y.copy()
+    for i in range(n - 1, -1, -1):
+        x[i] = (x[i] - L[i + 1:, i] @ x[i + 1:]) / L[i, i]
+    return x
+
+
+def _cost(E, qfrc_smooth, a, Ma, jar):
+    act = jar < 0.0
+    gauss = 0.5 * ((a - E["a0"]) @ (Ma - qfrc_smooth))
+    return gauss + 0.5 * np.sum(E["D"][act] * jar[act] ** 2)
+
+
+def newton(m, M, E, qfrc_smooth, a0, warm):
+    """Primal Newton on 1/2 (a-a0)^T M (a-a0) + sum_i 1/2 D_i min(J_i a - aref_i, 0)^2
+    with an exact (bracketed 1-D Newton) line search (mj_solNewton restated)."""
+    E = dict(E, a0=a0)
+    J, D, aref = E["J"], E["D"], E["aref"]
+    scale = 1.0 / (m.meaninertia * max(1, m.nv))
+    a = a0.copy()
+    Ma = M @ a
+    jar = J @ a - aref
+    cost = _cost(E, qfrc_smooth, a, Ma, jar)
+    if warm is not None:
+        Mw = M @ warm
+        jw = J @ warm - aref
+        cw = _cost(E, qfrc_smooth, warm, Mw, jw)
+        if cw < cost:
+            a, Ma, jar, cost = warm.copy(), Mw, jw, cw
+    its = 0
+    for it in range(m.opt.iterations):
+        act = jar < 0.0
+        grad = Ma - qfrc_smooth + J.T @ (D * act * jar)
+        if scale * np.sqrt(grad @ grad) < m.opt.tolerance:
+            break
+        its += 1
+        H = M + (J.T * (D * act)) @ J
+        L = cholesky(H)
+        p = -chol_solve(L, grad)
+        Mp = M @ p
+        Jp = J @ p
+        alpha = line_search(m, p, Ma - qfrc_smooth, Mp, jar, Jp, D)
+        if alpha == 0.0:
+            break
+        a = a + alpha * p
+        Ma = Ma + alpha * Mp
+        jar = jar + alpha * Jp
+        new = _cost(E, qfrc_smooth, a, Ma, jar)
+        imp = scale * (cost - new)
+        cost = new
+        if imp < m.opt.tolerance:
+            break
+    act = jar < 0.0
+    force = -D * act * jar
+    return a, force, J.T @ force, its
+
+
+def line_search(m, p, res, Mp, jar, Jp, D):
+    """Exact minimiser of the convex piecewise-quadratic cost along p: bracketed Newton on phi'."""
+    g0 = p @ res
+    h0 = p @ Mp
+
+    def deriv(al):
+        x = jar + al * Jp
+        act = x < 0.0
+        return g0 + al * h0 + np.sum(D[act] * x[act] * Jp[act]), h0 + np.sum(D[act] * Jp[act] ** 2)
+
+    d0, _ = deriv(0.0)
+    if not d0 < 0.0:
+        return 0.0
+    lo, hi, al = 0.0, np.inf, 1.0
+    for _ in range(m.opt.ls_iterations):
+        d1, d2 = deriv(al)
+        if abs(d1) < m.opt.ls_tolerance * abs(d0):
+            break
+        if d1 < 0.0:
+            lo = al
+        else:
+            hi = al
+        an = al - d1 / d2
+        if not (lo < an < hi):
+            an = 0.5 * (lo + hi)
+        al = an
+    return al
+
+
+# ----------------------------------------------------------------------------- step
+
+
+def integrate_pos(m, qpos, qvel, dt):
+    q = qpos.copy()
+    for j in range(m.njnt):
+        a, d = m.jnt_qposadr[j], m.jnt_dofadr[j]
+        if m.jnt_type[j] == JNT_FREE:
+            q[a:a + 3] = q[a:a + 3] + dt * qvel[d:d + 3]
+            w = qvel[d + 3:d + 6]
+            nw = np.sqrt(w @ w)
+            quat = q[a + 3:a + 7]
+            if nw > MINVAL:
+                quat = qmul(quat, qaxisangle(w / nw, nw * dt))
+            q[a + 3:a + 7] = qnormalize(quat)
+        else:
+            q[a] = q[a] + dt * qvel[d]
+    return q
+
+
+def forward(m, qpos, qvel, ctrl, qfrc_applied=None, warm=None):
+    """Everything of one substep up to (and including) the constraint solve."""
+    K = kinematics(m, qpos)
+    C = com_pos(m, K)
+    M, crbs = crb(m, C)
+    L = factor_ldl(m, M)
+    cvel, cdofd = com_vel(m, C, qvel)
+    bias = rne(m, C, cvel, cdofd, qvel)
+    fact, kvd = actuation(m, qpos, qvel, ctrl)
+    smooth = fact - m.dof_damping * qvel - bias
+    if qfrc_applied is not None:
+        smooth = smooth + qfrc_applied
+    a0 = solve_ldl(m, L, smooth)
+    cons, dropped = collide(m, K)
+    E = constraints(m, C, cons, qpos, qvel)
+    qacc, force, qfrc_con, its = newton(m, M, E, smooth, a0, warm)
+    return dict(K=K, C=C, M=M, qLD=L, crb=crbs, cvel=cvel, cdofd=cdofd, bias=bias, qfrc_actuator=fact, kvd=kvd,
+                qfrc_smooth=smooth, qacc_smooth=a0, contacts=cons, dropped=dropped, efc=E, qacc=qacc,
+                efc_force=force, qfrc_constraint=qfrc_con, iterations=its)
+
+
+def step(m, qpos, qvel, ctrl, qfrc_applied=None, warm=None):
+    """One substep: forward, implicitfast velocity update, position integration.
+    Returns (qpos, qvel, qacc_warmstart, forward-dict)."""
+    dt = m.opt.timestep
+    F = forward(m, qpos, qvel, ctrl, qfrc_applied, warm)
+    Mt = F["M"].copy()
+    Mt[np.diag_indices(m.nv)] += dt * (m.dof_damping + F["kvd"])
+    Lt = factor_ldl(m, Mt)
+    acc = solve_ldl(m, Lt, F["qfrc_smooth"] + F["qfrc_constraint"])
+    qvel_new = qvel + dt * acc
+    qpos_new = integrate_pos(m, qpos, qvel_new, dt)
+    return qpos_new, qvel_new, F["qacc"], F
+
+
+def set_const(m, qpos0=None):
+    """Inverse weights at qpos0 from this oracle's own M (model.set_const)."""
+    q = m.qpos0 if qpos0 is None else qpos0
+    K = kinematics(m, q)
+    C = com_pos(m, K)
+    M, _ = crb(m, C)
+    jac = [np.zeros((3, m.nv))] + [point_jac(m, C, b, K["xipos"][b]) for b in range(1, m.nbody)]
+    m.set_const(M, jac)
+    return M

@@ -1,0 +1,192 @@
+"""Robots for the 3-D path, built in code (no MJCF parser, no network for assets).
+
+* ``g1_like`` -- a 29-dof humanoid with the Unitree G1's joint layout (6 per leg,
+  3 waist, 7 per arm; one hinge per body, free-floating pelvis: nq = 36,
+  nv = 35) and approximately its link lengths and masses (~35 kg). The
+  dimensions are a surrogate: the real G1 MJCF is not available offline.
+* ``go1_like`` -- a 12-dof quadruped with the Unitree Go1's layout (hip
+  abduction, thigh, calf per leg; nq = 19, nv = 18).
+* ``terrain`` -- a flat plane or a seeded rough heightfield.
+
+Both robots use position actuators (implicit ``kv`` by default, the mjlab G1
+velocity configuration's ``BuiltinPositionActuator``), joint armature and
+range limits, sphere feet and capsule limbs.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .model import (ACT_IMPLICIT, GEOM_BOX, GEOM_CAPSULE, GEOM_SPHERE, ModelBuilder, Opt)
+
+
+def rough_heightfield(seed: int, size_m: float = 16.0, spacing: float = 0.1, amplitude: float = 0.06):
+    """Seeded rough terrain: uniform noise smoothed by a 3x3 box filter, centred at the origin,
+    with a flat 2 m pad at the centre (spawn area)."""
+    n = int(round(size_m / spacing)) + 1
+    rng = np.random.default_rng(seed)
+    h = rng.uniform(-amplitude, amplitude, size=(n + 2, n + 2))
+    h = sum(h[i:i + n, j:j + n] for i in range(3) for j in range(3)) / 9.0
+    c = (np.arange(n) - (n - 1) / 2) * spacing
+    pad = (np.abs(c)[:, None] < 1.0) & (np.abs(c)[None, :] < 1.0)
+    h = np.where(pad, 0.0, h)
+    return h, spacing, (-(n - 1) / 2 * spacing, -(n - 1) / 2 * spacing)
+
+
+def _terrain(b: ModelBuilder, rough: bool, seed: int):
+    if rough:
+        data, sp, origin = rough_heightfield(seed)
+        b.heightfield(data, sp, origin, friction=1.0)
+    else:
+        b.plane(friction=1.0)
+
+
+def g1_like(rough: bool = False, seed: int = 0, actuator_kind: int = ACT_IMPLICIT, self_collision: bool = True,
+            opt: Opt | None = None):
+    b = ModelBuilder("g1_like", opt)
+    _terrain(b, rough, seed)
+    pelvis = b.body("pelvis", 0, pos=(0, 0, 0.793), mass=3.81, inertia=(0.010, 0.009, 0.008))
+    b.free_joint(pelvis)
+    b.geom(pelvis, GEOM_SPHERE, (0.07,), pos=(0, 0, -0.02))
+    arm = 0.01
+    leg_gains = dict(kp=100.0, kv=2.0)
+    for side, sy in (("left", 1.0), ("right", -1.0)):
+        hp = b.body(f"{side}_hip_pitch_link", pelvis, pos=(0, 0.064 * sy, -0.103), mass=1.35,
+                    inertia=(0.002, 0.002, 0.002))
+        b.hinge(hp, (0, 1, 0), name=f"{side}_hip_pitch_joint", range=(-2.53, 2.88), armature=arm)
+        hr = b.body(f"{side}_hip_roll_link", hp, pos=(0, 0.052 * sy, -0.030), mass=1.52, inertia=(0.002, 0.002, 0.002))
+        b.hinge(hr, (1, 0, 0), name=f"{side}_hip_roll_joint",
+                range=(-0.52, 2.97) if sy > 0 else (-2.97, 0.52), armature=arm)
+        hy = b.body(f"{side}_hip_yaw_link", hr, pos=(0.025, 0, -0.124), mass=1.70, inertia=(0.006, 0.006, 0.002),
+                    ipos=(0, 0, -0.08))
+        b.hinge(hy, (0, 0, 1), name=f"{side}_hip_yaw_joint", range=(-2.75, 2.75), armature=arm)
+        b.geom(hy, GEOM_CAPSULE, (0.055,), fromto=(0, 0, -0.02, -0.05, 0, -0.16))
+        kn = b.body(f"{side}_knee_link", hy, pos=(-0.078, 0.0, -0.177), mass=1.93, inertia=(0.012, 0.012, 0.002),
+                    ipos=(0, 0, -0.13))
+        b.hinge(kn, (0, 1, 0), name=f"{side}_knee_joint", range=(-0.087, 2.88), armature=arm)
+        b.geom(kn, GEOM_CAPSULE, (0.045,), fromto=(0, 0, -0.03, 0, 0, -0.26))
+        ap = b.body(f"{side}_ankle_pitch_link", kn, pos=(0, 0, -0.30), mass=0.074, inertia=(1e-4, 1e-4, 1e-4))
+        b.hinge(ap, (0, 1, 0), name=f"{side}_ankle_pitch_joint", range=(-0.87, 0.52), armature=arm)
+        ar = b.body(f"{side}_ankle_roll_link", ap, pos=(0, 0, -0.017), mass=0.61, inertia=(4e-4, 1.5e-3, 1.6e-3),
+                    ipos=(0.03, 0, -0.02))
+        b.hinge(ar, (1, 0, 0), name=f"{side}_ankle_roll_joint", range=(-0.26, 0.26), armature=arm)
+        for fx in (-0.05, 0.12):
+            for fy in (-0.025, 0.025):
+                b.geom(ar, GEOM_SPHERE, (0.012,), pos=(fx, fy, -0.031), name=f"{side}_foot")
+    # waist + torso
+    wy = b.body("waist_yaw_link", pelvis, pos=(0, 0, 0), mass=0.21, inertia=(1e-4, 1e-4, 1e-4))
+    b.hinge(wy, (0, 0, 1), name="waist_yaw_joint", range=(-2.62, 2.62), armature=arm)
+    wr = b.body("waist_roll_link", wy, pos=(-0.004, 0, 0.035), mass=0.09, inertia=(1e-4, 1e-4, 1e-4))
+    b.hinge(wr, (1, 0, 0), name="waist_roll_joint", range=(-0.52, 0.52), armature=arm)
+    torso = b.body("torso_link", wr, pos=(0, 0, 0.019), mass=9.6, inertia=(0.11, 0.09, 0.04), ipos=(0, 0, 0.2))
+    b.hinge(torso, (0, 1, 0), name="waist_pitch_joint", range=(-0.52, 0.52), armature=arm)
+    b.geom(torso, GEOM_CAPSULE, (0.09,), fromto=(0, 0, 0.1, 0, 0, 0.3))
+    b.geom(torso, GEOM_SPHERE, (0.07,), pos=(0, 0, 0.45), name="head")
+    for side, sy in (("left", 1.0), ("right", -1.0)):
+        sp = b.body(f"{side}_shoulder_pitch_link", torso, pos=(0, 0.10 * sy, 0.24), mass=0.72,
+                    inertia=(5e-4, 5e-4, 5e-4))
+        b.hinge(sp, (0, 1, 0), name=f"{side}_shoulder_pitch_joint", range=(-3.09, 2.67), armature=arm)
+        sr = b.body(f"{side}_shoulder_roll_link", sp, pos=(0, 0.038 * sy, -0.014), mass=0.64,
+                    inertia=(5e-4, 5e-4, 5e-4))
+        b.hinge(sr, (1, 0, 0), name=f"{side}_shoulder_roll_joint",
+                range=(-1.59, 2.25) if sy > 0 else (-2.25, 1.59), armature=arm)
+        sw = b.body(f"{side}_shoulder_yaw_link", sr, pos=(0, 0.006 * sy, -0.1), mass=0.60, inertia=(1e-3, 1e-3, 3e-4),
+                    ipos=(0, 0, -0.04))
+        b.hinge(sw, (0, 0, 1), name=f"{side}_shoulder_yaw_joint", range=(-2.62, 2.62), armature=arm)
+        b.geom(sw, GEOM_CAPSULE, (0.035,), fromto=(0, 0, 0.0, 0, 0, -0.08))
+        el = b.body(f"{side}_elbow_link", sw, pos=(0.016, 0, -0.08), mass=0.60, inertia=(1e-3, 1e-3, 3e-4),
+                    ipos=(0.05, 0, 0))
+        b.hinge(el, (0, 1, 0), name=f"{side}_elbow_joint", range=(-1.05, 2.09), armature=arm)
+        b.geom(el, GEOM_CAPSULE, (0.03,), fromto=(0.0, 0, 0, 0.1, 0, 0))
+        wrl = b.body(f"{side}_wrist_roll_link", el, pos=(0.1, 0.002 * sy, -0.01), mass=0.085,
+                     inertia=(5e-5, 5e-5, 5e-5))
+        b.hinge(wrl, (1, 0, 0), name=f"{side}_wrist_roll_joint", range=(-1.97, 1.97), armature=arm)
+        wp = b.body(f"{side}_wrist_pitch_link", wrl, pos=(0.038, 0, 0), mass=0.48, inertia=(3e-4, 3e-4, 3e-4))
+        b.hinge(wp, (0, 1, 0), name=f"{side}_wrist_pitch_joint", range=(-1.61, 1.61), armature=arm)
+        wyl = b.body(f"{side}_wrist_yaw_link", wp, pos=(0.046, 0, 0), mass=0.25, inertia=(2e-4, 2e-4, 2e-4))
+        b.hinge(wyl, (0, 0, 1), name=f"{side}_wrist_yaw_joint", range=(-1.61, 1.61), armature=arm)
+        b.geom(wyl, GEOM_SPHERE, (0.04,), pos=(0.05, 0, 0), name=f"{side}_hand")
+    for j in list(b.joints):
+        if j["type"] == 3:
+            name = j["name"]
+            if "hip" in name or "knee" in name:
+                gains = dict(kp=leg_gains["kp"] * (1.5 if "knee" in name else 1.0), kv=leg_gains["kv"],
+                             effort=139.0 if "knee" in name else 88.0)
+            elif "ankle" in name:
+                gains = dict(kp=40.0, kv=2.0, effort=50.0)
+            elif "waist" in name:
+                gains = dict(kp=200.0, kv=5.0, effort=88.0)
+            else:
+                gains = dict(kp=40.0, kv=1.0, effort=25.0)
+            b.actuator(name, kind=actuator_kind, **gains)
+    if not self_collision:
+        _only_terrain(b)
+    else:
+        _limit_self_pairs(b)
+    return b.compile()
+
+
+def _only_terrain(b: ModelBuilder):
+    for g in b.geoms[1:]:
+        g["contype"], g["conaffinity"] = 2, 1  # robot geoms collide with terrain (contype 1) only
+    b.geoms[0]["contype"], b.geoms[0]["conaffinity"] = 1, 2
+
+
+def _limit_self_pairs(b: ModelBuilder):
+    """Terrain vs everything; self pairs only shin-shin and hand-vs-leg/torso."""
+    _only_terrain(b)
+    for g in b.geoms[1:]:
+        name = b.bodies[g["body"]].name
+        if "knee" in name:
+            g["contype"] |= 4
+            g["conaffinity"] |= 4
+        if g.get("name", "") and "hand" in g["name"]:
+            g["contype"] |= 8
+        if "hip_yaw" in name or name == "torso_link":
+            g["conaffinity"] |= 8
+
+
+def go1_like(rough: bool = False, seed: int = 0, actuator_kind: int = ACT_IMPLICIT, opt: Opt | None = None):
+    b = ModelBuilder("go1_like", opt)
+    _terrain(b, rough, seed)
+    trunk = b.body("trunk", 0, pos=(0, 0, 0.33), mass=5.2, inertia=(0.016, 0.037, 0.046))
+    b.free_joint(trunk)
+    b.geom(trunk, GEOM_BOX, (0.19, 0.047, 0.05))
+    arm = 0.01
+    for leg, (sx, sy) in (("FR", (1, -1)), ("FL", (1, 1)), ("RR", (-1, -1)), ("RL", (-1, 1))):
+        hip = b.body(f"{leg}_hip", trunk, pos=(0.1881 * sx, 0.04675 * sy, 0), mass=0.68, inertia=(5e-4, 8e-4, 6e-4))
+        b.hinge(hip, (1, 0, 0), name=f"{leg}_hip_joint", range=(-0.86, 0.86), armature=arm)
+        th = b.body(f"{leg}_thigh", hip, pos=(0, 0.08 * sy, 0), mass=1.0, inertia=(5e-3, 5e-3, 1e-3),
+                    ipos=(0, 0, -0.03))
+        b.hinge(th, (0, 1, 0), name=f"{leg}_thigh_joint", range=(-0.69, 4.5), armature=arm)
+        b.geom(th, GEOM_CAPSULE, (0.02,), fromto=(0, 0, 0, 0, 0, -0.213))
+        ca = b.body(f"{leg}_calf", th, pos=(0, 0, -0.213), mass=0.2, inertia=(2e-3, 2e-3, 1e-4), ipos=(0, 0, -0.1))
+        b.hinge(ca, (0, 1, 0), name=f"{leg}_calf_joint", range=(-2.82, -0.89), armature=arm)
+        b.geom(ca, GEOM_SPHERE, (0.02,), pos=(0, 0, -0.213), name=f"{leg}_foot")
+    for j in list(b.joints):
+        if j["type"] == 3:
+            b.actuator(j["name"], kind=actuator_kind, kp=35.0, kv=0.5, effort=23.7 if "calf" not in j["name"] else 35.55)
+    _only_terrain(b)
+    return b.compile()
+
+
+G1_DEFAULT_JOINTS = {
+    "hip_pitch": -0.312, "knee": 0.669, "ankle_pitch": -0.363, "elbow": 0.6,
+    "left_shoulder_roll": 0.2, "right_shoulder_roll": -0.2, "shoulder_pitch": 0.2,
+}
+GO1_DEFAULT_JOINTS = {"hip": 0.0, "thigh": 0.9, "calf": -1.8}
+
+
+def default_qpos(model, table: dict) -> np.ndarray:
+    """qpos0 with named joint defaults (substring match, longest key wins)."""
+    q = model.qpos0.copy()
+    for j, name in enumerate(model.jnt_names):
+        if model.jnt_type[j] != 3:
+            continue
+        best = None
+        for k in table:
+            if k in name and (best is None or len(k) > len(best)):
+                best = k
+        if best is not None:
+            q[model.jnt_qposadr[j]] = table[best]
+    return q

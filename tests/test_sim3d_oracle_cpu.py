@@ -1,0 +1,339 @@
+"""The 3-D oracle (oracle/sim3d.py) pinned by analytic properties (no reference exists).
+
+Each test checks a stage against an independent computation: rotation
+composition, finite differences of forward kinematics, kinetic and potential
+energy, the Lagrangian, brute-force geometry, and the optimality conditions
+of the constraint problem.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import sim3d as O
+from paper_2601_22074_b200.sim3d import robots
+from paper_2601_22074_b200.sim3d.model import (ACT_DC, ACT_PD, GEOM_CAPSULE, GEOM_SPHERE, ModelBuilder, Opt)
+
+
+def _arm(gravity=(0, 0, -9.81)):
+    b = ModelBuilder("arm", Opt(gravity=gravity))
+    b.plane()
+    l1 = b.body("l1", 0, pos=(0, 0, 1.0), quat=(0.9, 0.1, 0.3, 0.2), mass=1.2, inertia=(0.02, 0.03, 0.01),
+                ipos=(0.1, 0.02, -0.2), iquat=(0.8, 0.2, 0.1, 0.4))
+    b.hinge(l1, (0, 0, 1), pos=(0.05, 0, 0))
+    l2 = b.body("l2", l1, pos=(0.0, 0.1, -0.4), mass=0.8, inertia=(0.01, 0.015, 0.004), ipos=(0.0, 0.05, -0.1))
+    b.hinge(l2, (1, 1, 0), pos=(0, 0.02, 0.01))
+    l3 = b.body("l3", l2, pos=(0.1, 0.0, -0.3), quat=(0.7, 0.0, 0.7, 0.1), mass=0.5, inertia=(0.004, 0.002, 0.003),
+                ipos=(0.03, 0.0, -0.05))
+    b.hinge(l3, (0.2, 0.3, 0.9))
+    b.geom(l3, GEOM_SPHERE, (0.05,))
+    return b.compile()
+
+
+def _random_state(m, rng, scale=0.5):
+    q = m.qpos0.copy()
+    v = rng.normal(size=m.nv) * scale
+    for j in range(m.njnt):
+        a = m.jnt_qposadr[j]
+        if m.jnt_type[j] == 0:
+            q[a:a + 3] += rng.normal(size=3) * 0.1
+            quat = rng.normal(size=4)
+            q[a + 3:a + 7] = quat / np.linalg.norm(quat)
+        else:
+            q[a] = rng.uniform(-1, 1)
+    return q, v
+
+
+MODELS = {"g1": robots.g1_like, "go1": robots.go1_like, "arm": _arm}
+
+
+@pytest.fixture(params=list(MODELS))
+def model(request):
+    m = MODELS[request.param]()
+    O.set_const(m)
+    return m
+
+
+def _homog(q, p):
+    T = np.eye(4)
+    T[:3, :3] = O.qmat(q)
+    T[:3, 3] = p
+    return T
+
+
+def test_fk_matches_homogeneous_composition(model, rng):
+    m = model
+    q, _ = _random_state(m, rng)
+    K = O.kinematics(m, q)
+    T = [np.eye(4)]
+    for b in range(1, m.nbody):
+        Tb = T[m.body_parentid[b]] @ _homog(m.body_quat[b], m.body_pos[b])
+        for j in range(m.body_jntadr[b], m.body_jntadr[b] + m.body_jntnum[b]):
+            a = m.jnt_qposadr[j]
+            if m.jnt_type[j] == 0:
+                Tb = _homog(q[a + 3:a + 7] / np.linalg.norm(q[a + 3:a + 7]), q[a:a + 3])
+            else:
+                ax = m.jnt_axis[j]
+                th = q[a] - m.qpos0[a]
+                # rotation about the joint axis through jnt_pos (body frame)
+                R = O.qmat(O.qaxisangle(ax, th))
+                P = np.eye(4)
+                P[:3, 3] = m.jnt_pos[j]
+                Rh = np.eye(4)
+                Rh[:3, :3] = R
+                Pi = np.eye(4)
+                Pi[:3, 3] = -m.jnt_pos[j]
+                Tb = Tb @ P @ Rh @ Pi
+        T.append(Tb)
+    for b in range(1, m.nbody):
+        np.testing.assert_allclose(K["xpos"][b], T[b][:3, 3], atol=1e-12)
+        np.testing.assert_allclose(K["xmat"][b], T[b][:3, :3], atol=1e-12)
+
+
+def _kinetic_from_fd(m, q, v, h=1e-6):
+    """sum_b 1/2 m |v_com|^2 + 1/2 w^T I w, body velocities by central differences of FK."""
+    Kp = O.kinematics(m, O.integrate_pos(m, q, v, h))
+    Km = O.kinematics(m, O.integrate_pos(m, q, v, -h))
+    K0 = O.kinematics(m, q)
+    T = 0.0
+    for b in range(1, m.nbody):
+        vc = (Kp["xipos"][b] - Km["xipos"][b]) / (2 * h)
+        dR = (Kp["xmat"][b] - Km["xmat"][b]) / (2 * h)
+        W = dR @ K0["xmat"][b].T
+        w = np.array([W[2, 1], W[0, 2], W[1, 0]])
+        Ib = K0["ximat"][b] @ np.diag(m.body_inertia[b]) @ K0["ximat"][b].T
+        T += 0.5 * m.body_mass[b] * vc @ vc + 0.5 * w @ Ib @ w
+    return T
+
+
+def test_mass_matrix_is_kinetic_energy(model, rng):
+    m = model
+    for _ in range(3):
+        q, v = _random_state(m, rng)
+        F = O.forward(m, q, v, np.zeros(m.nu))
+        M = F["M"] - np.diag(m.dof_armature)
+        np.testing.assert_allclose(F["M"], F["M"].T, atol=0)
+        assert np.all(np.linalg.eigvalsh(F["M"]) > 0)
+        T = _kinetic_from_fd(m, q, v)
+        assert abs(0.5 * v @ M @ v - T) < 1e-7 * max(1.0, T)
+
+
+def test_ldl_factor_solves_and_reconstructs(model, rng):
+    m = model
+    q, v = _random_state(m, rng)
+    K = O.kinematics(m, q)
+    C = O.com_pos(m, K)
+    M, _ = O.crb(m, C)
+    L = O.factor_ldl(m, M)
+    # reconstruct: M = U^T D U with U unit upper-in-reverse (L below diagonal on ancestor entries)
+    U = np.tril(L, -1) + np.eye(m.nv)
+    D = np.diag(np.diag(L))
+    np.testing.assert_allclose(U.T @ D @ U, M, rtol=1e-12, atol=1e-12)
+    for (i, j) in zip(*np.nonzero(np.tril(L, -1))):
+        assert j in m.dof_chain[i]  # no fill-in outside the tree pattern
+    b = rng.normal(size=m.nv)
+    np.testing.assert_allclose(O.solve_ldl(m, L, b), np.linalg.solve(M, b), rtol=1e-9, atol=1e-12)
+
+
+def test_point_jacobian_is_fd_of_fk(model, rng):
+    m = model
+    q, v = _random_state(m, rng)
+    K = O.kinematics(m, q)
+    C = O.com_pos(m, K)
+    h = 1e-6
+    for b in range(1, m.nbody):
+        loc = rng.normal(size=3) * 0.1
+        J = O.point_jac(m, C, b, K["xpos"][b] + K["xmat"][b] @ loc)
+        Kp = O.kinematics(m, O.integrate_pos(m, q, v, h))
+        Km = O.kinematics(m, O.integrate_pos(m, q, v, -h))
+        fd = ((Kp["xpos"][b] + Kp["xmat"][b] @ loc) - (Km["xpos"][b] + Km["xmat"][b] @ loc)) / (2 * h)
+        np.testing.assert_allclose(J @ v, fd, atol=1e-7)
+
+
+def test_rne_matches_lagrangian_fixed_base(rng):
+    m = _arm()
+    O.set_const(m)
+    q, v = _random_state(m, rng, 1.0)
+    F = O.forward(m, q, v, np.zeros(m.nu))
+    h = 1e-6
+
+    def Mof(qq):
+        return O.crb(m, O.com_pos(m, O.kinematics(m, qq)))[0]
+
+    def V(qq):
+        K = O.kinematics(m, qq)
+        return -sum(m.body_mass[b] * np.asarray(m.opt.gravity) @ K["xipos"][b] for b in range(1, m.nbody))
+
+    Mdot = (Mof(q + h * v) - Mof(q - h * v)) / (2 * h)
+    dT = np.zeros(m.nv)
+    dV = np.zeros(m.nv)
+    for i in range(m.nv):
+        e = np.zeros(m.nv)
+        e[i] = h
+        dT[i] = 0.5 * v @ ((Mof(q + e) - Mof(q - e)) / (2 * h)) @ v
+        dV[i] = (V(q + e) - V(q - e)) / (2 * h)
+    np.testing.assert_allclose(F["bias"], Mdot @ v - dT + dV, rtol=1e-6, atol=1e-6)
+
+
+@pytest.mark.parametrize("gravity", [(0, 0, 0), (0, 0, -9.81)])
+def test_energy_conserved_free_floating(gravity, rng):
+    m = robots.go1_like(opt=Opt(gravity=gravity))
+    m.actuator_kp[:] = 0
+    m.actuator_kv[:] = 0
+    O.set_const(m)
+    q, v = _random_state(m, rng, 0.3)
+    q[2] = 5.0
+
+    def acc(qq, vv):
+        F = O.forward(m, qq, vv, np.zeros(m.nu))
+        return F["qacc_smooth"]
+
+    def energy(qq, vv):
+        F = O.forward(m, qq, vv, np.zeros(m.nu))
+        K = F["K"]
+        Vp = -sum(m.body_mass[b] * np.asarray(gravity) @ K["xipos"][b] for b in range(1, m.nbody))
+        return 0.5 * vv @ F["M"] @ vv + Vp
+
+    E0 = energy(q, v)
+    dt = 1e-3
+    for _ in range(50):  # RK4 on (q, v) with the manifold update for the free joint
+        k1v = acc(q, v)
+        k2v = acc(O.integrate_pos(m, q, v, dt / 2), v + dt / 2 * k1v)
+        k3v = acc(O.integrate_pos(m, q, v + dt / 2 * k1v, dt / 2), v + dt / 2 * k2v)
+        k4v = acc(O.integrate_pos(m, q, v + dt / 2 * k2v, dt), v + dt * k3v)
+        vn = v + dt / 6 * (k1v + 2 * k2v + 2 * k3v + k4v)
+        vbar = (v + 2 * (v + dt / 2 * k1v) + 2 * (v + dt / 2 * k2v) + (v + dt * k3v)) / 6
+        q = O.integrate_pos(m, q, vbar, dt)
+        v = vn
+    assert abs(energy(q, v) - E0) < 2e-4 * max(1.0, abs(E0))
+
+
+def test_free_fall_exact():
+    b = ModelBuilder("ball")
+    b.plane()
+    ball = b.body("ball", 0, pos=(0, 0, 10.0), mass=2.0, inertia=(0.01, 0.01, 0.01))
+    b.free_joint(ball)
+    b.geom(ball, GEOM_SPHERE, (0.1,))
+    m = b.compile()
+    O.set_const(m)
+    q, v = m.qpos0.copy(), np.zeros(6)
+    z, vz = 10.0, 0.0
+    for _ in range(100):
+        q, v, _, F = O.step(m, q, v, np.zeros(0))
+        vz = vz + 0.005 * -9.81
+        z = z + 0.005 * vz
+        assert F["contacts"] == []
+    assert abs(q[2] - z) < 1e-12 and abs(v[2] - vz) < 1e-12
+
+
+def test_ball_comes_to_rest_on_plane_and_forces_in_cone():
+    b = ModelBuilder("ball")
+    b.plane(friction=0.5)
+    ball = b.body("ball", 0, pos=(0, 0, 0.2), mass=2.0, inertia=(0.008, 0.008, 0.008))
+    b.free_joint(ball)
+    b.geom(ball, GEOM_SPHERE, (0.1,), friction=0.5)
+    m = b.compile()
+    O.set_const(m)
+    q, v = m.qpos0.copy(), np.zeros(6)
+    v[0] = 1.0  # sliding, then rolling
+    warm = None
+    for _ in range(800):
+        q, v, warm, F = O.step(m, q, v, np.zeros(0), warm=warm)
+    assert len(F["contacts"]) == 1
+    # sliding decays into rolling without slip: v_x = w_y r, no vertical motion
+    assert abs(q[2] - 0.1) < 2e-3 and abs(v[2]) < 1e-3
+    assert abs(v[0] - v[4] * 0.1) < 1e-3 and 0.3 < v[0] < 1.0
+    f = F["efc_force"]
+    assert np.all(f >= 0)
+    # the 4 pyramid edge forces sum to the normal force ~ m g
+    assert abs(f.sum() - 2.0 * 9.81) < 0.5
+
+
+def test_newton_optimality(model, rng):
+    m = model
+    q = robots.default_qpos(m, robots.G1_DEFAULT_JOINTS if m.name == "g1_like" else robots.GO1_DEFAULT_JOINTS) \
+        if m.name != "arm" else m.qpos0.copy()
+    if m.name != "arm":  # press the lowest geom 5 mm into the ground
+        K = O.kinematics(m, q)
+        low = min(K["geom_xpos"][g][2] - m.geom_rbound[g] for g in range(1, m.ngeom))
+        q[2] -= low + 0.005
+    v = rng.normal(size=m.nv) * 0.2
+    ctrl = q[m.actuator_qposadr] if m.nu else np.zeros(0)
+    F = O.forward(m, q, v, ctrl)
+    E = F["efc"]
+    if m.name != "arm":
+        assert len(F["contacts"]) >= 4
+    # KKT: M (a - a0) = J^T f, f = D max(-(J a - aref), 0)
+    res = F["M"] @ (F["qacc"] - F["qacc_smooth"]) - F["qfrc_constraint"]
+    scale = 1.0 / (m.meaninertia * max(1, m.nv))
+    assert scale * np.linalg.norm(res) < 1e-5
+    np.testing.assert_allclose(F["efc_force"], E["D"] * np.maximum(-(E["J"] @ F["qacc"] - E["aref"]), 0.0),
+                               rtol=1e-12, atol=1e-12)
+
+
+def test_segment_closest_points_brute_force(rng):
+    for _ in range(50):
+        p1, q1, p2, q2 = (rng.normal(size=3) for _ in range(4))
+        a, b = O.seg_closest(p1, q1, p2, q2)
+        t = np.linspace(0, 1, 401)
+        A = p1 + (q1 - p1) * t[:, None]
+        B = p2 + (q2 - p2) * t[:, None]
+        brute = np.min(np.linalg.norm(A[:, None] - B[None], axis=-1))
+        assert np.linalg.norm(a - b) <= brute + 1e-12
+        assert np.linalg.norm(a - b) > brute - 1e-3
+
+
+def test_hfield_distance_continuous_and_exact_on_vertices():
+    m = robots.g1_like(rough=True)
+    H, sp, org = m.hfield_data, m.hfield_spacing, m.hfield_origin
+    for (iy, ix) in ((3, 5), (40, 70), (100, 12)):
+        x, y = org[0] + ix * sp, org[1] + iy * sp
+        d, n = O.hfield_point(m, np.array([x, y, 1.0]), 0.0)
+        assert abs((1.0 - H[iy, ix]) * n[2] - d) < 1e-12
+    # continuity across the cell diagonal and cell edges
+    xs = np.linspace(org[0] + 1.0, org[0] + 1.3, 301)
+    hs = []
+    for x in xs:
+        d, n = O.hfield_point(m, np.array([x, org[1] + 2.013, 1.0]), 0.0)
+        hs.append(1.0 - d / n[2])
+    assert np.max(np.abs(np.diff(hs))) < 0.01
+
+
+def test_actuator_laws():
+    m = robots.go1_like(actuator_kind=ACT_DC)
+    m.actuator_saturation[:] = 20.0
+    m.actuator_vmax[:] = 10.0
+    q = m.qpos0.copy()
+    v = np.zeros(m.nv)
+    v[m.actuator_dofadr] = 5.0
+    ctrl = q[m.actuator_qposadr] + 1.0
+    f, kvd = O.actuation(m, q, v, ctrl)
+    tau = m.actuator_kp * 1.0 - m.actuator_kv * 5.0
+    hi = np.clip(20.0 * (1 - 5.0 / 10.0), 0, m.actuator_effort)
+    np.testing.assert_allclose(f[m.actuator_dofadr], np.minimum(tau, hi))
+    assert not kvd.any()
+    m2 = robots.go1_like(actuator_kind=ACT_PD)
+    f2, kvd2 = O.actuation(m2, q, v, ctrl)
+    np.testing.assert_allclose(f2[m2.actuator_dofadr], np.clip(tau, -m2.actuator_effort, m2.actuator_effort))
+    assert not kvd2.any()
+    m3 = robots.go1_like()  # implicit kv enters only where the force range does not clamp
+    f3, kvd3 = O.actuation(m3, q, v, ctrl)
+    clamped = np.abs(tau) > m3.actuator_effort
+    assert clamped.any() and not clamped.all()
+    np.testing.assert_allclose(kvd3[m3.actuator_dofadr], np.where(clamped, 0.0, m3.actuator_kv))
+
+
+def test_self_collision_pairs_generate_contacts():
+    m = robots.g1_like()
+    O.set_const(m)
+    q = robots.default_qpos(m, robots.G1_DEFAULT_JOINTS)
+    # swing the left hip roll inward until the shins cross
+    j = m.jnt_names.index("left_hip_roll_joint")
+    q[m.jnt_qposadr[j]] = -0.45
+    j = m.jnt_names.index("right_hip_roll_joint")
+    q[m.jnt_qposadr[j]] = 0.45
+    K = O.kinematics(m, q)
+    cons, _ = O.collide(m, K)
+    self_pairs = [c for c in cons if c["geom1"] != 0]
+    assert self_pairs, "crossed legs must touch"
+    for c in self_pairs:
+        assert m.geom_type[c["geom1"]] == GEOM_CAPSULE and c["dist"] < 0
