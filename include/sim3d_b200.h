@@ -1,0 +1,188 @@
+/* sim3d_b200.h -- C-ABI of the 3-D articulated-body path.
+ *
+ * The reference (stridesim) is planar and has no 3-D engine; in
+ * mjlab this path is MuJoCo Warp's mjwarp.step over an MjModel/MjData pair
+ * (PAPER.md:111-118, 171-177). These entry points are what a host binding of
+ * that step would call: plain pointers and sizes, everything asynchronous on
+ * the given CUDA stream, no allocation inside. Arrays are device pointers,
+ * row-major with the world index outermost ((N, nq) qpos, (N, nv) qvel ...),
+ * in the element type selected by `dtype` (S3_F64 or S3_F32); the model
+ * tables are packed by the host in the same element type.
+ *
+ * Style: one field per line (paper_2601_22074_b200/sim3d/native.py parses
+ * the structs into ctypes; s3_sizeof cross-checks them).
+ */
+#ifndef SIM3D_B200_H
+#define SIM3D_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define S3_ABI_VERSION 1
+#define S3_F64 0
+#define S3_F32 1
+
+#define S3_MAX_NV 64
+#define S3_MAX_NBODY 64
+#define S3_MAX_CHAIN 32
+#define S3_MAX_CON 16
+#define S3_MAX_LIM 32
+#define S3_MAX_ROWS 96
+
+#define S3_OK 0
+#define S3_ERR_ARG 1
+#define S3_ERR_CUDA 2
+#define S3_ERR_BOUNDS 3
+
+/* Model tables (device pointers). Float tables hold `dtype` elements. */
+typedef struct s3_model {
+    int32_t dtype;
+    int32_t nbody;
+    int32_t njnt;
+    int32_t nq;
+    int32_t nv;
+    int32_t ngeom;
+    int32_t npair;
+    int32_t nu;
+    int32_t nlimjnt;
+    int32_t nlevel;
+    int32_t chain_stride;
+    int32_t terrain_hfield;
+    int32_t hf_nrow;
+    int32_t hf_ncol;
+    int32_t iterations;
+    int32_t ls_iterations;
+    double timestep;
+    double gravity[3];
+    double tolerance;
+    double ls_tolerance;
+    double solref[2];
+    double solimp[5];
+    double scale;
+    double total_mass;
+    double hf_spacing;
+    double hf_origin[2];
+    double hf_max;
+    /* bodies */
+    const int32_t* body_parentid;
+    const int32_t* body_jntadr;
+    const int32_t* body_jntnum;
+    const int32_t* body_dofadr;
+    const int32_t* body_dofnum;
+    const uint64_t* body_dofmask;
+    const int32_t* level_ptr;
+    const int32_t* level_body;
+    const int32_t* child_ptr;
+    const int32_t* child_idx;
+    const void* body_pos;
+    const void* body_quat;
+    const void* body_ipos;
+    const void* body_ilmat;
+    const void* body_mass;
+    const void* body_inertia;
+    const void* body_invweight0;
+    /* joints */
+    const int32_t* jnt_type;
+    const int32_t* jnt_qposadr;
+    const int32_t* jnt_dofadr;
+    const void* jnt_pos;
+    const void* jnt_axis;
+    const void* qpos0;
+    /* dofs */
+    const int32_t* dof_bodyid;
+    const int32_t* dof_parentid;
+    const uint64_t* dof_descmask;
+    const uint8_t* dof_chain;
+    const int32_t* dof_chainlen;
+    const void* dof_damping;
+    const void* dof_armature;
+    const void* dof_invweight0;
+    /* limited joints */
+    const int32_t* lim_qposadr;
+    const int32_t* lim_dofadr;
+    const void* lim_range;
+    /* geoms */
+    const int32_t* geom_type;
+    const int32_t* geom_bodyid;
+    const void* geom_pos;
+    const void* geom_lmat;
+    const void* geom_size;
+    const void* geom_friction;
+    const void* geom_rbound;
+    /* collision pairs */
+    const int32_t* pair_geom;
+    const uint8_t* pair_chain;
+    const int32_t* pair_chainlen;
+    /* actuators */
+    const int32_t* act_dofadr;
+    const int32_t* act_qposadr;
+    const int32_t* act_kind;
+    const void* act_gain;
+    /* heightfield samples (hf_nrow, hf_ncol) */
+    const void* hfield;
+} s3_model;
+
+/* Per-world state and optional per-substep outputs (NULL = not written). */
+typedef struct s3_data {
+    int64_t nworld;
+    void* qpos;
+    void* qvel;
+    void* ctrl;
+    void* qacc_warmstart;
+    void* qfrc_applied;
+    void* time;
+    /* outputs of the LAST substep of a launch (for parity tests / sensors) */
+    void* xpos;
+    void* xquat;
+    void* com;
+    void* cdof;
+    void* qM;
+    void* qLD;
+    void* qfrc_bias;
+    void* qfrc_smooth;
+    void* qacc_smooth;
+    void* qacc;
+    void* qfrc_constraint;
+    void* geom_xpos;
+    void* geom_xmat;
+    int32_t* ncon;
+    int32_t* ndropped;
+    int32_t* nefc;
+    int32_t* con_pair;
+    void* con_dist;
+    void* con_pos;
+    void* con_frame;
+    void* efc_force;
+    int32_t* solver_niter;
+} s3_data;
+
+/* Workspace layout: offsets (in elements) inside one world's shared-memory block. */
+typedef struct s3_layout {
+    int32_t warps_per_block;
+    int32_t elems_per_world;
+    int32_t bytes_per_block;
+    int32_t off[40];
+} s3_layout;
+
+int s3_abi_version(void);
+size_t s3_sizeof(int which); /* 0 model, 1 data, 2 layout */
+const char* s3_last_error(void);
+
+/* Fill the shared-memory layout for this model; warps_per_block = 0 picks the largest
+ * count that fits the per-block shared-memory limit. */
+int s3_plan(const s3_model* m, int32_t warps_per_block, s3_layout* out);
+
+/* `nsub` physics substeps of every world (mj_step x nsub: kinematics, com, CRB + L^T D L,
+ * RNE, actuation, collision, constraints, Newton, implicitfast), ctrl held fixed.
+ * Replaces, for the 3-D path, StepPipeline.substep x decimation (sim/physics.py:239-249,
+ * env.py:228-233 of the reference; mjwarp.step in mjlab). */
+int s3_step(const s3_model* m, const s3_data* d, const s3_layout* l, int32_t nsub, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SIM3D_B200_H */

@@ -1,0 +1,1317 @@
+// s3_kernel.cu -- 3-D articulated-body step for sm_100a.
+//
+// One warp owns one world for the whole launch: its state and every
+// per-world intermediate (frames, cinert/crb, cdof, the packed mass matrix and
+// its factor, contacts, contact Jacobians, constraint rows) live in that
+// warp's slice of shared memory; lanes split the work inside each stage
+// (bodies of one tree level, dofs, geom pairs, ancestor pairs of the
+// factorization, rows of the constraint problem) and __syncwarp() orders the
+// stages. No block-level synchronisation: warps are independent worlds.
+//
+// The stages follow oracle/sim3d.py operation for operation (that file is the
+// written specification; parity: tests/test_gpu_sim3d.py):
+//   kinematics -> com/cinert/cdof -> CRB -> M (packed lower) -> tree-sparse
+//   L^T D L -> comVel/RNE -> actuation -> qacc_smooth -> broadphase +
+//   narrowphase -> limit + pyramidal contact rows -> Newton (dense Cholesky of
+//   H = M + J^T D J, exact bracketed line search) -> implicitfast -> integrate.
+// Templated on the element type (double: parity build; float: throughput).
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "../../include/sim3d_b200.h"
+
+namespace s3 {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int kGeomPlane = 0, kGeomHfield = 1, kGeomSphere = 2, kGeomCapsule = 3, kGeomBox = 6;
+constexpr int kJntFree = 0;
+constexpr int kActDC = 1, kActImplicit = 2;  // 0 = PD (the default branch)
+constexpr int kConStride = 14;  // dist, pos[3], frame[9], mu
+
+// layout slots (s3_layout.off)
+enum {
+    O_XPOS, O_XQUAT, O_XIPOS, O_CINERT, O_CRB, O_CDOF, O_CDOFD, O_CVEL, O_CACC, O_JANC, O_JAX,
+    O_M, O_LD, O_QPOS, O_QVEL, O_SMOOTH, O_A0, O_A, O_MA, O_GRAD, O_P, O_MP, O_KVD, O_GPOS, O_GMAT,
+    O_CON, O_JC, O_RAREF, O_RD, O_RJAR, O_RJP, O_CDOT, O_BIAS, O_FCON, O_CTRL, O_COM, O_INT, O_END
+};
+
+__host__ __device__ inline int tri(int i, int j) { return i * (i + 1) / 2 + j; }  // packed lower, i >= j
+
+__device__ inline void tri_decode(int t, int& a, int& b) {
+    int x = (int)((sqrtf(8.0f * (float)t + 1.0f) - 1.0f) * 0.5f);
+    while ((x + 1) * (x + 2) / 2 <= t) ++x;
+    while (x * (x + 1) / 2 > t) --x;
+    a = x;
+    b = t - x * (x + 1) / 2;
+}
+
+template <class T> __device__ inline T wsum(T v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+    return v;
+}
+
+template <class T> __device__ inline T rsqrt_t(T x);
+template <> __device__ inline double rsqrt_t(double x) { return 1.0 / sqrt(x); }
+template <> __device__ inline float rsqrt_t(float x) { return 1.0f / sqrtf(x); }
+
+template <class T> __device__ inline void sincos_t(T x, T* s, T* c);
+template <> __device__ inline void sincos_t(double x, double* s, double* c) { sincos(x, s, c); }
+template <> __device__ inline void sincos_t(float x, float* s, float* c) { sincosf(x, s, c); }
+
+// ---------------------------------------------------------------- small 3-D math (oracle/sim3d.py helpers)
+
+template <class T> __device__ inline void qmul(const T* a, const T* b, T* r) {
+    T w = a[0] * b[0] - a[1] * b[1] - a[2] * b[2] - a[3] * b[3];
+    T x = a[0] * b[1] + a[1] * b[0] + a[2] * b[3] - a[3] * b[2];
+    T y = a[0] * b[2] - a[1] * b[3] + a[2] * b[0] + a[3] * b[1];
+    T z = a[0] * b[3] + a[1] * b[2] - a[2] * b[1] + a[3] * b[0];
+    r[0] = w; r[1] = x; r[2] = y; r[3] = z;
+}
+
+template <class T> __device__ inline void qmat(const T* q, T* R) {
+    T w = q[0], x = q[1], y = q[2], z = q[3];
+    R[0] = T(1) - T(2) * (y * y + z * z); R[1] = T(2) * (x * y - w * z); R[2] = T(2) * (x * z + w * y);
+    R[3] = T(2) * (x * y + w * z); R[4] = T(1) - T(2) * (x * x + z * z); R[5] = T(2) * (y * z - w * x);
+    R[6] = T(2) * (x * z - w * y); R[7] = T(2) * (y * z + w * x); R[8] = T(1) - T(2) * (x * x + y * y);
+}
+
+template <class T> __device__ inline void mv3(const T* R, const T* v, T* r) {
+    T a = R[0] * v[0] + R[1] * v[1] + R[2] * v[2];
+    T b = R[3] * v[0] + R[4] * v[1] + R[5] * v[2];
+    T c = R[6] * v[0] + R[7] * v[1] + R[8] * v[2];
+    r[0] = a; r[1] = b; r[2] = c;
+}
+
+template <class T> __device__ inline void mm3(const T* A, const T* B, T* C) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) C[3 * i + j] = A[3 * i] * B[j] + A[3 * i + 1] * B[3 + j] + A[3 * i + 2] * B[6 + j];
+}
+
+template <class T> __device__ inline void cross3(const T* a, const T* b, T* r) {
+    T x = a[1] * b[2] - a[2] * b[1];
+    T y = a[2] * b[0] - a[0] * b[2];
+    T z = a[0] * b[1] - a[1] * b[0];
+    r[0] = x; r[1] = y; r[2] = z;
+}
+
+template <class T> __device__ inline T dot3(const T* a, const T* b) { return a[0] * b[0] + a[1] * b[1] + a[2] * b[2]; }
+
+template <class T> __device__ inline T dot6(const T* a, const T* b) {
+    return a[0] * b[0] + a[1] * b[1] + a[2] * b[2] + a[3] * b[3] + a[4] * b[4] + a[5] * b[5];
+}
+
+template <class T> __device__ inline void qnormalize(T* q) {
+    T r = rsqrt_t(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+    q[0] *= r; q[1] *= r; q[2] *= r; q[3] *= r;
+}
+
+// motion x motion: [w x u_ang ; w x u_lin + v_lin x u_ang]
+template <class T> __device__ inline void cross_motion(const T* v, const T* u, T* r) {
+    T a[3], b[3], c[3];
+    cross3(v, u, a);
+    cross3(v, u + 3, b);
+    cross3(v + 3, u, c);
+    r[0] = a[0]; r[1] = a[1]; r[2] = a[2];
+    r[3] = b[0] + c[0]; r[4] = b[1] + c[1]; r[5] = b[2] + c[2];
+}
+
+// motion x force: [w x f_ang + v_lin x f_lin ; w x f_lin]
+template <class T> __device__ inline void cross_force(const T* v, const T* f, T* r) {
+    T a[3], b[3], c[3];
+    cross3(v, f, a);
+    cross3(v + 3, f + 3, b);
+    cross3(v, f + 3, c);
+    r[0] = a[0] + b[0]; r[1] = a[1] + b[1]; r[2] = a[2] + b[2];
+    r[3] = c[0]; r[4] = c[1]; r[5] = c[2];
+}
+
+// 10-vector spatial inertia times motion
+template <class T> __device__ inline void inert_mul(const T* ci, const T* v, T* r) {
+    const T* w = v;
+    const T* vl = v + 3;
+    T md[3] = {ci[6], ci[7], ci[8]};
+    T a[3], b[3];
+    cross3(md, vl, a);
+    cross3(md, w, b);
+    r[0] = ci[0] * w[0] + ci[3] * w[1] + ci[4] * w[2] + a[0];
+    r[1] = ci[3] * w[0] + ci[1] * w[1] + ci[5] * w[2] + a[1];
+    r[2] = ci[4] * w[0] + ci[5] * w[1] + ci[2] * w[2] + a[2];
+    r[3] = ci[9] * vl[0] - b[0];
+    r[4] = ci[9] * vl[1] - b[1];
+    r[5] = ci[9] * vl[2] - b[2];
+}
+
+template <class T> __device__ inline T clampt(T x, T lo, T hi) { return x < lo ? lo : (x > hi ? hi : x); }
+
+// ---------------------------------------------------------------- per-warp workspace
+
+template <class T> struct WS {
+    T *xpos, *xquat, *xipos, *cinert, *crb, *cdof, *cdofd, *cvel, *cacc, *janc, *jax, *M, *LD, *qpos, *qvel,
+        *smooth, *a0, *a, *Ma, *grad, *p, *Mp, *kvd, *gpos, *gmat, *con, *Jc, *raref, *rD, *rjar, *rJp, *cdot,
+        *bias, *fcon, *ctrl, *com;
+    int *con_pair, *lim_dof, *lim_sign, *misc;
+};
+
+template <class T> __device__ inline WS<T> make_ws(T* base, const s3_layout& l) {
+    WS<T> s;
+    const int* o = l.off;
+    s.xpos = base + o[O_XPOS]; s.xquat = base + o[O_XQUAT]; s.xipos = base + o[O_XIPOS];
+    s.cinert = base + o[O_CINERT]; s.crb = base + o[O_CRB]; s.cdof = base + o[O_CDOF]; s.cdofd = base + o[O_CDOFD];
+    s.cvel = base + o[O_CVEL]; s.cacc = base + o[O_CACC]; s.janc = base + o[O_JANC]; s.jax = base + o[O_JAX];
+    s.M = base + o[O_M]; s.LD = base + o[O_LD]; s.qpos = base + o[O_QPOS]; s.qvel = base + o[O_QVEL];
+    s.smooth = base + o[O_SMOOTH]; s.a0 = base + o[O_A0]; s.a = base + o[O_A]; s.Ma = base + o[O_MA];
+    s.grad = base + o[O_GRAD]; s.p = base + o[O_P]; s.Mp = base + o[O_MP]; s.kvd = base + o[O_KVD];
+    s.gpos = base + o[O_GPOS]; s.gmat = base + o[O_GMAT]; s.con = base + o[O_CON]; s.Jc = base + o[O_JC];
+    s.raref = base + o[O_RAREF]; s.rD = base + o[O_RD]; s.rjar = base + o[O_RJAR]; s.rJp = base + o[O_RJP];
+    s.cdot = base + o[O_CDOT]; s.bias = base + o[O_BIAS]; s.fcon = base + o[O_FCON]; s.ctrl = base + o[O_CTRL];
+    s.com = base + o[O_COM];
+    int* ib = reinterpret_cast<int*>(base + o[O_INT]);
+    s.con_pair = ib;
+    s.lim_dof = ib + S3_MAX_CON;
+    s.lim_sign = ib + S3_MAX_CON + S3_MAX_LIM;
+    s.misc = ib + S3_MAX_CON + 2 * S3_MAX_LIM;
+    return s;
+}
+
+template <class T> __device__ inline const T* F(const void* p) { return static_cast<const T*>(p); }
+
+// ---------------------------------------------------------------- stages
+
+// mj_kinematics: body frames level by level (oracle kinematics)
+template <class T> __device__ void kinematics(const s3_model& m, WS<T>& s, int lane) {
+    const T* bpos = F<T>(m.body_pos);
+    const T* bquat = F<T>(m.body_quat);
+    const T* jpos = F<T>(m.jnt_pos);
+    const T* jaxis = F<T>(m.jnt_axis);
+    const T* q0 = F<T>(m.qpos0);
+    if (lane == 0) {
+        s.xpos[0] = s.xpos[1] = s.xpos[2] = T(0);
+        s.xquat[0] = T(1); s.xquat[1] = s.xquat[2] = s.xquat[3] = T(0);
+    }
+    __syncwarp();
+    for (int L = 1; L < m.nlevel; ++L) {
+        for (int idx = m.level_ptr[L] + lane; idx < m.level_ptr[L + 1]; idx += 32) {
+            int b = m.level_body[idx];
+            int par = m.body_parentid[b];
+            T pq[4] = {s.xquat[4 * par], s.xquat[4 * par + 1], s.xquat[4 * par + 2], s.xquat[4 * par + 3]};
+            T R[9], pos[3], quat[4], v[3];
+            qmat(pq, R);
+            T bp[3] = {bpos[3 * b], bpos[3 * b + 1], bpos[3 * b + 2]};
+            mv3(R, bp, v);
+            pos[0] = s.xpos[3 * par] + v[0]; pos[1] = s.xpos[3 * par + 1] + v[1]; pos[2] = s.xpos[3 * par + 2] + v[2];
+            T bq[4] = {bquat[4 * b], bquat[4 * b + 1], bquat[4 * b + 2], bquat[4 * b + 3]};
+            qmul(pq, bq, quat);
+            int j0 = m.body_jntadr[b], jn = m.body_jntnum[b];
+            for (int j = j0; j < j0 + jn; ++j) {
+                int a = m.jnt_qposadr[j];
+                if (m.jnt_type[j] == kJntFree) {
+                    pos[0] = s.qpos[a]; pos[1] = s.qpos[a + 1]; pos[2] = s.qpos[a + 2];
+                    quat[0] = s.qpos[a + 3]; quat[1] = s.qpos[a + 4]; quat[2] = s.qpos[a + 5]; quat[3] = s.qpos[a + 6];
+                    qnormalize(quat);
+                    s.janc[3 * j] = pos[0]; s.janc[3 * j + 1] = pos[1]; s.janc[3 * j + 2] = pos[2];
+                    s.jax[3 * j] = T(0); s.jax[3 * j + 1] = T(0); s.jax[3 * j + 2] = T(1);
+                } else {
+                    T jp[3] = {jpos[3 * j], jpos[3 * j + 1], jpos[3 * j + 2]};
+                    T ja[3] = {jaxis[3 * j], jaxis[3 * j + 1], jaxis[3 * j + 2]};
+                    T anc[3], ax[3];
+                    qmat(quat, R);
+                    mv3(R, jp, anc);
+                    anc[0] += pos[0]; anc[1] += pos[1]; anc[2] += pos[2];
+                    mv3(R, ja, ax);
+                    s.janc[3 * j] = anc[0]; s.janc[3 * j + 1] = anc[1]; s.janc[3 * j + 2] = anc[2];
+                    s.jax[3 * j] = ax[0]; s.jax[3 * j + 1] = ax[1]; s.jax[3 * j + 2] = ax[2];
+                    T sn, cs;
+                    sincos_t(T(0.5) * (s.qpos[a] - q0[a]), &sn, &cs);
+                    T qa[4] = {cs, ja[0] * sn, ja[1] * sn, ja[2] * sn};
+                    T nq[4];
+                    qmul(quat, qa, nq);
+                    quat[0] = nq[0]; quat[1] = nq[1]; quat[2] = nq[2]; quat[3] = nq[3];
+                    qmat(quat, R);
+                    mv3(R, jp, v);
+                    pos[0] = anc[0] - v[0]; pos[1] = anc[1] - v[1]; pos[2] = anc[2] - v[2];
+                }
+            }
+            qnormalize(quat);
+            s.xquat[4 * b] = quat[0]; s.xquat[4 * b + 1] = quat[1]; s.xquat[4 * b + 2] = quat[2];
+            s.xquat[4 * b + 3] = quat[3];
+            s.xpos[3 * b] = pos[0]; s.xpos[3 * b + 1] = pos[1]; s.xpos[3 * b + 2] = pos[2];
+        }
+        __syncwarp();
+    }
+}
+
+// mj_comPos: xipos, subtree com (single tree), cinert, cdof; geom frames
+template <class T> __device__ void com_pos(const s3_model& m, WS<T>& s, int lane) {
+    const T* ipos = F<T>(m.body_ipos);
+    const T* ilmat = F<T>(m.body_ilmat);
+    const T* mass = F<T>(m.body_mass);
+    const T* inertia = F<T>(m.body_inertia);
+    T cx = T(0), cy = T(0), cz = T(0);
+    for (int b = 1 + lane; b < m.nbody; b += 32) {
+        T R[9], v[3];
+        qmat(s.xquat + 4 * b, R);
+        T ip[3] = {ipos[3 * b], ipos[3 * b + 1], ipos[3 * b + 2]};
+        mv3(R, ip, v);
+        T x = s.xpos[3 * b] + v[0], y = s.xpos[3 * b + 1] + v[1], z = s.xpos[3 * b + 2] + v[2];
+        s.xipos[3 * b] = x; s.xipos[3 * b + 1] = y; s.xipos[3 * b + 2] = z;
+        cx += mass[b] * x; cy += mass[b] * y; cz += mass[b] * z;
+    }
+    T inv = T(1) / T(m.total_mass);
+    T com[3] = {wsum(cx) * inv, wsum(cy) * inv, wsum(cz) * inv};
+    if (lane == 0) { s.com[0] = com[0]; s.com[1] = com[1]; s.com[2] = com[2]; }
+    for (int b = 1 + lane; b < m.nbody; b += 32) {
+        T R[9], Ri[9], IL[9];
+        qmat(s.xquat + 4 * b, R);
+        for (int k = 0; k < 9; ++k) IL[k] = ilmat[9 * b + k];
+        mm3(R, IL, Ri);
+        T i0 = inertia[3 * b], i1 = inertia[3 * b + 1], i2 = inertia[3 * b + 2];
+        // I = Ri diag(i) Ri^T
+        T I[9];
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) I[3 * r + c] = Ri[3 * r] * i0 * Ri[3 * c] + Ri[3 * r + 1] * i1 * Ri[3 * c + 1] +
+                                                     Ri[3 * r + 2] * i2 * Ri[3 * c + 2];
+        T d[3] = {s.xipos[3 * b] - com[0], s.xipos[3 * b + 1] - com[1], s.xipos[3 * b + 2] - com[2]};
+        T mb = mass[b];
+        T dd = dot3(d, d);
+        T* ci = s.cinert + 10 * b;
+        ci[0] = I[0] + mb * (dd - d[0] * d[0]);
+        ci[1] = I[4] + mb * (dd - d[1] * d[1]);
+        ci[2] = I[8] + mb * (dd - d[2] * d[2]);
+        ci[3] = I[1] + mb * (T(0) - d[0] * d[1]);
+        ci[4] = I[2] + mb * (T(0) - d[0] * d[2]);
+        ci[5] = I[5] + mb * (T(0) - d[1] * d[2]);
+        ci[6] = mb * d[0]; ci[7] = mb * d[1]; ci[8] = mb * d[2]; ci[9] = mb;
+    }
+    // cdof, per joint
+    for (int j = lane; j < m.njnt; j += 32) {
+        int da = m.jnt_dofadr[j];
+        T off[3] = {com[0] - s.janc[3 * j], com[1] - s.janc[3 * j + 1], com[2] - s.janc[3 * j + 2]};
+        if (m.jnt_type[j] == kJntFree) {
+            int b = m.dof_bodyid[da];
+            T R[9];
+            qmat(s.xquat + 4 * b, R);
+            for (int i = 0; i < 3; ++i) {
+                T* c = s.cdof + 6 * (da + i);
+                c[0] = c[1] = c[2] = T(0);
+                c[3] = T(i == 0); c[4] = T(i == 1); c[5] = T(i == 2);
+                T ax[3] = {R[i], R[3 + i], R[6 + i]};
+                T lin[3];
+                cross3(ax, off, lin);
+                T* r = s.cdof + 6 * (da + 3 + i);
+                r[0] = ax[0]; r[1] = ax[1]; r[2] = ax[2]; r[3] = lin[0]; r[4] = lin[1]; r[5] = lin[2];
+            }
+        } else {
+            T ax[3] = {s.jax[3 * j], s.jax[3 * j + 1], s.jax[3 * j + 2]};
+            T lin[3];
+            cross3(ax, off, lin);
+            T* r = s.cdof + 6 * da;
+            r[0] = ax[0]; r[1] = ax[1]; r[2] = ax[2]; r[3] = lin[0]; r[4] = lin[1]; r[5] = lin[2];
+        }
+    }
+    // geom frames
+    const T* gp = F<T>(m.geom_pos);
+    const T* gl = F<T>(m.geom_lmat);
+    for (int g = lane; g < m.ngeom; g += 32) {
+        int b = m.geom_bodyid[g];
+        T R[9], v[3], L[9];
+        qmat(s.xquat + 4 * b, R);
+        T p[3] = {gp[3 * g], gp[3 * g + 1], gp[3 * g + 2]};
+        mv3(R, p, v);
+        s.gpos[3 * g] = s.xpos[3 * b] + v[0]; s.gpos[3 * g + 1] = s.xpos[3 * b + 1] + v[1];
+        s.gpos[3 * g + 2] = s.xpos[3 * b + 2] + v[2];
+        for (int k = 0; k < 9; ++k) L[k] = gl[9 * g + k];
+        mm3(R, L, s.gmat + 9 * g);
+    }
+    __syncwarp();
+}
+
+// mj_crb: composite inertias (levels, deepest first, children in descending index) + packed M
+template <class T> __device__ void crb_mass(const s3_model& m, WS<T>& s, int lane) {
+    for (int L = m.nlevel - 1; L >= 1; --L) {
+        int n0 = m.level_ptr[L], nl = m.level_ptr[L + 1] - n0;
+        for (int t = lane; t < nl * 10; t += 32) {
+            int b = m.level_body[n0 + t / 10], c = t % 10;
+            T acc = s.cinert[10 * b + c];
+            for (int k = m.child_ptr[b]; k < m.child_ptr[b + 1]; ++k) acc += s.crb[10 * m.child_idx[k] + c];
+            s.crb[10 * b + c] = acc;
+        }
+        __syncwarp();
+    }
+    const T* arm = F<T>(m.dof_armature);
+    int nv = m.nv;
+    int np = nv * (nv + 1) / 2;
+    for (int t = lane; t < np; t += 32) s.M[t] = T(0);
+    __syncwarp();
+    for (int i = lane; i < nv; i += 32) {
+        T f[6];
+        inert_mul(s.crb + 10 * m.dof_bodyid[i], s.cdof + 6 * i, f);
+        int j = i;
+        while (j >= 0) {
+            s.M[tri(i, j)] = dot6(s.cdof + 6 * j, f);
+            j = m.dof_parentid[j];
+        }
+        s.M[tri(i, i)] += arm[i];
+    }
+    __syncwarp();
+}
+
+// mj_factorM: tree-sparse L^T D L in place on packed-lower A (oracle factor_ldl)
+template <class T> __device__ void factor_ldl(const s3_model& m, T* A, int lane) {
+    for (int k = m.nv - 1; k >= 0; --k) {
+        int len = m.dof_chainlen[k] - 1;  // strict ancestors
+        if (len <= 0) continue;
+        const uint8_t* ch = m.dof_chain + k * S3_MAX_CHAIN;
+        T dk = A[tri(k, k)];
+        int npair = len * (len + 1) / 2;
+        for (int t = lane; t < npair; t += 32) {
+            int a, b;
+            tri_decode(t, a, b);
+            int i = ch[a], j = ch[b];
+            T tk = A[tri(k, i)] / dk;
+            A[tri(i, j)] -= tk * A[tri(k, j)];
+        }
+        __syncwarp();
+        for (int a = lane; a < len; a += 32) {
+            int i = ch[a];
+            A[tri(k, i)] = A[tri(k, i)] / dk;
+        }
+        __syncwarp();
+    }
+}
+
+// x <- M^-1 x with the L^T D L factor (oracle solve_ldl; column-oriented forward pass)
+template <class T> __device__ void solve_ldl(const s3_model& m, const T* A, T* x, int lane) {
+    int nv = m.nv;
+    for (int i = nv - 1; i >= 0; --i) {
+        int len = m.dof_chainlen[i] - 1;
+        const uint8_t* ch = m.dof_chain + i * S3_MAX_CHAIN;
+        T xi = x[i];
+        for (int a = lane; a < len; a += 32) {
+            int j = ch[a];
+            x[j] -= A[tri(i, j)] * xi;
+        }
+        __syncwarp();
+    }
+    for (int i = lane; i < nv; i += 32) x[i] = x[i] / A[tri(i, i)];
+    __syncwarp();
+    for (int j = 0; j < nv; ++j) {
+        uint64_t dm = m.dof_descmask[j];
+        if (!dm) continue;
+        T xj = x[j];
+        for (int i = lane; i < nv; i += 32)
+            if ((dm >> i) & 1ull) x[i] -= A[tri(i, j)] * xj;
+        __syncwarp();
+    }
+}
+
+// dense Cholesky H = L L^T on packed lower (oracle cholesky), then x <- H^-1 x
+template <class T> __device__ void cholesky(int nv, T* H, int lane) {
+    for (int k = 0; k < nv; ++k) {
+        T d = sqrt(H[tri(k, k)]);
+        for (int i = k + 1 + lane; i < nv; i += 32) H[tri(i, k)] = H[tri(i, k)] / d;
+        __syncwarp();
+        if (lane == 0) H[tri(k, k)] = d;
+        int n = nv - k - 1;
+        int npair = n * (n + 1) / 2;
+        for (int t = lane; t < npair; t += 32) {
+            int a, b;
+            tri_decode(t, a, b);
+            int i = k + 1 + a, j = k + 1 + b;
+            H[tri(i, j)] -= H[tri(i, k)] * H[tri(j, k)];
+        }
+        __syncwarp();
+    }
+}
+
+template <class T> __device__ void chol_solve(int nv, const T* L, T* x, int lane) {
+    for (int i = 0; i < nv; ++i) {
+        T xi = x[i] / L[tri(i, i)];
+        __syncwarp();
+        if (lane == 0) x[i] = xi;
+        for (int r = i + 1 + lane; r < nv; r += 32) x[r] -= L[tri(r, i)] * xi;
+        __syncwarp();
+    }
+    for (int i = nv - 1; i >= 0; --i) {
+        T xi = x[i] / L[tri(i, i)];
+        __syncwarp();
+        if (lane == 0) x[i] = xi;
+        for (int r = lane; r < i; r += 32) x[r] -= L[tri(i, r)] * xi;
+        __syncwarp();
+    }
+}
+
+// y = M x with packed-lower symmetric M
+template <class T> __device__ void sym_mul(int nv, const T* M, const T* x, T* y, int lane) {
+    for (int i = lane; i < nv; i += 32) {
+        T acc = T(0);
+        for (int j = 0; j < nv; ++j) acc += (i >= j ? M[tri(i, j)] : M[tri(j, i)]) * x[j];
+        y[i] = acc;
+    }
+    __syncwarp();
+}
+
+// mj_comVel + mj_rne (qacc = 0): bias forces
+template <class T> __device__ void rne(const s3_model& m, WS<T>& s, int lane) {
+    if (lane < 6) {
+        s.cvel[lane] = T(0);
+        s.cacc[lane] = lane < 3 ? T(0) : T(-m.gravity[lane - 3]);
+    }
+    __syncwarp();
+    for (int L = 1; L < m.nlevel; ++L) {
+        for (int idx = m.level_ptr[L] + lane; idx < m.level_ptr[L + 1]; idx += 32) {
+            int b = m.level_body[idx];
+            int par = m.body_parentid[b];
+            T v[6], a[6];
+            for (int k = 0; k < 6; ++k) { v[k] = s.cvel[6 * par + k]; a[k] = s.cacc[6 * par + k]; }
+            int j0 = m.body_jntadr[b], jn = m.body_jntnum[b];
+            for (int j = j0; j < j0 + jn; ++j) {
+                int da = m.jnt_dofadr[j];
+                if (m.jnt_type[j] == kJntFree) {
+                    for (int i = 0; i < 3; ++i)
+                        for (int k = 0; k < 6; ++k) v[k] += s.cdof[6 * (da + i) + k] * s.qvel[da + i];
+                    for (int i = 0; i < 3; ++i) {
+                        s.cdofd[6 * (da + i)] = s.cdofd[6 * (da + i) + 1] = s.cdofd[6 * (da + i) + 2] = T(0);
+                        s.cdofd[6 * (da + i) + 3] = s.cdofd[6 * (da + i) + 4] = s.cdofd[6 * (da + i) + 5] = T(0);
+                        cross_motion(v, s.cdof + 6 * (da + 3 + i), s.cdofd + 6 * (da + 3 + i));
+                    }
+                    for (int i = 3; i < 6; ++i)
+                        for (int k = 0; k < 6; ++k) v[k] += s.cdof[6 * (da + i) + k] * s.qvel[da + i];
+                } else {
+                    cross_motion(v, s.cdof + 6 * da, s.cdofd + 6 * da);
+                    for (int k = 0; k < 6; ++k) v[k] += s.cdof[6 * da + k] * s.qvel[da];
+                }
+            }
+            int d0 = m.body_dofadr[b], dn = m.body_dofnum[b];
+            for (int d = d0; d < d0 + dn; ++d)
+                for (int k = 0; k < 6; ++k) a[k] += s.cdofd[6 * d + k] * s.qvel[d];
+            for (int k = 0; k < 6; ++k) { s.cvel[6 * b + k] = v[k]; s.cacc[6 * b + k] = a[k]; }
+        }
+        __syncwarp();
+    }
+    // body forces (overwrite cacc with cfrc)
+    for (int b = 1 + lane; b < m.nbody; b += 32) {
+        T f1[6], iv[6], f2[6];
+        const T* ci = s.cinert + 10 * b;
+        inert_mul(ci, s.cacc + 6 * b, f1);
+        inert_mul(ci, s.cvel + 6 * b, iv);
+        cross_force(s.cvel + 6 * b, iv, f2);
+        for (int k = 0; k < 6; ++k) s.cacc[6 * b + k] = f1[k] + f2[k];
+    }
+    __syncwarp();
+    // backward accumulation (children in descending index, like the oracle's reverse sweep)
+    for (int L = m.nlevel - 1; L >= 1; --L) {
+        int n0 = m.level_ptr[L], nl = m.level_ptr[L + 1] - n0;
+        for (int t = lane; t < nl * 6; t += 32) {
+            int b = m.level_body[n0 + t / 6], c = t % 6;
+            T acc = s.cacc[6 * b + c];
+            for (int k = m.child_ptr[b]; k < m.child_ptr[b + 1]; ++k) acc += s.cacc[6 * m.child_idx[k] + c];
+            s.cacc[6 * b + c] = acc;
+        }
+        __syncwarp();
+    }
+    for (int i = lane; i < m.nv; i += 32) s.bias[i] = dot6(s.cdof + 6 * i, s.cacc + 6 * m.dof_bodyid[i]);
+    __syncwarp();
+}
+
+// actuation + passive + smooth force (oracle actuation / forward)
+template <class T> __device__ void smooth_force(const s3_model& m, WS<T>& s, const T* applied, int lane) {
+    for (int i = lane; i < m.nv; i += 32) { s.fcon[i] = T(0); s.kvd[i] = T(0); }
+    __syncwarp();
+    const T* gain = F<T>(m.act_gain);
+    for (int u = lane; u < m.nu; u += 32) {
+        int d = m.act_dofadr[u], a = m.act_qposadr[u], kind = m.act_kind[u];
+        T kp = gain[5 * u], kv = gain[5 * u + 1], eff = gain[5 * u + 2];
+        T q = s.qpos[a], qd = s.qvel[d];
+        T tau = kp * (s.ctrl[u] - q) + kv * (T(0) - qd);
+        if (kind == kActDC) {
+            T sat = gain[5 * u + 3], vmax = gain[5 * u + 4];
+            T hi = fmin(fmax(sat * (T(1) - qd / vmax), T(0)), eff);
+            T lo = fmin(fmax(sat * (T(-1) - qd / vmax), -eff), T(0));
+            tau = fmin(fmax(tau, lo), hi);
+        } else {
+            bool clamped = tau > eff || tau < -eff;
+            tau = fmin(fmax(tau, -eff), eff);
+            if (kind == kActImplicit && !clamped) s.kvd[d] += kv;
+        }
+        s.fcon[d] += tau;  // fcon doubles as qfrc_actuator scratch here
+    }
+    __syncwarp();
+    const T* damp = F<T>(m.dof_damping);
+    for (int i = lane; i < m.nv; i += 32) {
+        T f = s.fcon[i] - damp[i] * s.qvel[i] - s.bias[i];
+        if (applied) f += applied[i];
+        s.smooth[i] = f;
+        s.a0[i] = f;
+    }
+    __syncwarp();
+}
+
+// ---------------------------------------------------------------- collision
+
+template <class T> struct Hit { T d, n[3], pos[3]; };
+
+template <class T> __device__ bool hfield_point(const s3_model& m, const T* q, T r, T& d, T* n) {
+    const T* H = F<T>(m.hfield);
+    T sp = T(m.hf_spacing);
+    T fx = (q[0] - T(m.hf_origin[0])) / sp;
+    T fy = (q[1] - T(m.hf_origin[1])) / sp;
+    if (!(fx >= T(0) && fy >= T(0) && fx < T(m.hf_ncol - 1) && fy < T(m.hf_nrow - 1))) return false;
+    int ix = (int)floor(fx), iy = (int)floor(fy);
+    T u = fx - T(ix), v = fy - T(iy);
+    T x0 = T(m.hf_origin[0]) + T(ix) * sp;
+    T y0 = T(m.hf_origin[1]) + T(iy) * sp;
+    int nc = m.hf_ncol;
+    T h00 = H[iy * nc + ix], h10 = H[iy * nc + ix + 1], h01 = H[(iy + 1) * nc + ix], h11 = H[(iy + 1) * nc + ix + 1];
+    if (u >= v) {
+        n[0] = -(h10 - h00) * sp; n[1] = -(h11 - h10) * sp;
+    } else {
+        n[0] = -(h11 - h01) * sp; n[1] = -(h01 - h00) * sp;
+    }
+    n[2] = sp * sp;
+    T rn = rsqrt_t(n[0] * n[0] + n[1] * n[1] + n[2] * n[2]);
+    n[0] *= rn; n[1] *= rn; n[2] *= rn;
+    T dq[3] = {q[0] - x0, q[1] - y0, q[2] - h00};
+    d = dot3(n, dq) - r;
+    return true;
+}
+
+template <class T> __device__ void seg_closest(const T* p1, const T* q1, const T* p2, const T* q2, T* A, T* B) {
+    T d1[3] = {q1[0] - p1[0], q1[1] - p1[1], q1[2] - p1[2]};
+    T d2[3] = {q2[0] - p2[0], q2[1] - p2[1], q2[2] - p2[2]};
+    T r[3] = {p1[0] - p2[0], p1[1] - p2[1], p1[2] - p2[2]};
+    T a = dot3(d1, d1), e = dot3(d2, d2), f = dot3(d2, r);
+    T c = dot3(d1, r), b = dot3(d1, d2);
+    T sN, tN;
+    if (e <= T(1e-12)) {
+        sN = a > T(1e-12) ? clampt(-c / a, T(0), T(1)) : T(0);
+        tN = T(0);
+    } else if (a <= T(1e-12)) {
+        sN = T(0);
+        tN = clampt(f / e, T(0), T(1));
+    } else {
+        T den = a * e - b * b;
+        sN = den > T(1e-12) ? clampt((b * f - c * e) / den, T(0), T(1)) : T(0);
+        tN = (b * sN + f) / e;
+        if (tN < T(0)) {
+            tN = T(0);
+            sN = clampt(-c / a, T(0), T(1));
+        } else if (tN > T(1)) {
+            tN = T(1);
+            sN = clampt((b - c) / a, T(0), T(1));
+        }
+    }
+    for (int k = 0; k < 3; ++k) { A[k] = p1[k] + d1[k] * sN; B[k] = p2[k] + d2[k] * tN; }
+}
+
+template <class T> __device__ inline void segment(const s3_model& m, const WS<T>& s, int g, T* p, T* q) {
+    T hl = F<T>(m.geom_size)[3 * g + 1];
+    const T* R = s.gmat + 9 * g;
+    const T* c = s.gpos + 3 * g;
+    for (int k = 0; k < 3; ++k) {
+        T a = R[3 * k + 2] * hl;
+        p[k] = c[k] - a;
+        q[k] = c[k] + a;
+    }
+}
+
+// point k (0..7) of geom g's terrain point set (sphere: centre; capsule: 2 ends; box: 8 corners)
+template <class T> __device__ inline int point_count(int type) {
+    return type == kGeomSphere ? 1 : (type == kGeomCapsule ? 2 : 8);
+}
+
+template <class T> __device__ inline void point_of(const s3_model& m, const WS<T>& s, int g, int type, int k, T* q,
+                                                   T& r) {
+    const T* sz = F<T>(m.geom_size) + 3 * g;
+    const T* c = s.gpos + 3 * g;
+    if (type == kGeomSphere) {
+        q[0] = c[0]; q[1] = c[1]; q[2] = c[2];
+        r = sz[0];
+    } else if (type == kGeomCapsule) {
+        T p0[3], p1[3];
+        segment(m, s, g, p0, p1);
+        const T* pp = k == 0 ? p0 : p1;
+        q[0] = pp[0]; q[1] = pp[1]; q[2] = pp[2];
+        r = sz[0];
+    } else {
+        T loc[3] = {(k & 1) ? sz[0] : -sz[0], (k & 2) ? sz[1] : -sz[1], (k & 4) ? sz[2] : -sz[2]};
+        T v[3];
+        mv3(s.gmat + 9 * g, loc, v);
+        q[0] = c[0] + v[0]; q[1] = c[1] + v[1]; q[2] = c[2] + v[2];
+        r = T(0);
+    }
+}
+
+// Narrowphase of one pair; emits up to 4 contacts through `emit(hit)` in the oracle's order.
+template <class T, class Emit> __device__ int narrow(const s3_model& m, const WS<T>& s, int p, Emit emit) {
+    int g1 = m.pair_geom[2 * p], g2 = m.pair_geom[2 * p + 1];
+    int t1 = m.geom_type[g1], t2 = m.geom_type[g2];
+    const T* c1 = s.gpos + 3 * g1;
+    const T* c2 = s.gpos + 3 * g2;
+    const T* rb = F<T>(m.geom_rbound);
+    int cnt = 0, cap = t2 == kGeomBox ? 4 : 8;
+    if (t1 == kGeomPlane) {
+        T n[3] = {s.gmat[9 * g1 + 2], s.gmat[9 * g1 + 5], s.gmat[9 * g1 + 8]};
+        T dc[3] = {c2[0] - c1[0], c2[1] - c1[1], c2[2] - c1[2]};
+        if (!(dot3(n, dc) - rb[g2] < T(0))) return 0;
+        int np = point_count<T>(t2);
+        for (int k = 0; k < np && cnt < cap; ++k) {
+            T q[3], r;
+            point_of(m, s, g2, t2, k, q, r);
+            T dq[3] = {q[0] - c1[0], q[1] - c1[1], q[2] - c1[2]};
+            T d = dot3(n, dq) - r;
+            if (d < T(0)) {
+                Hit<T> h;
+                h.d = d;
+                for (int i = 0; i < 3; ++i) { h.n[i] = n[i]; h.pos[i] = q[i] - n[i] * (r + T(0.5) * d); }
+                emit(h);
+                ++cnt;
+            }
+        }
+    } else if (t1 == kGeomHfield) {
+        if (!(c2[2] - rb[g2] < T(m.hf_max))) return 0;
+        int np = point_count<T>(t2);
+        for (int k = 0; k < np && cnt < cap; ++k) {
+            T q[3], r, d, n[3];
+            point_of(m, s, g2, t2, k, q, r);
+            if (hfield_point(m, q, r, d, n) && d < T(0)) {
+                Hit<T> h;
+                h.d = d;
+                for (int i = 0; i < 3; ++i) { h.n[i] = n[i]; h.pos[i] = q[i] - n[i] * (r + T(0.5) * d); }
+                emit(h);
+                ++cnt;
+            }
+        }
+    } else {
+        T dv[3] = {c2[0] - c1[0], c2[1] - c1[1], c2[2] - c1[2]};
+        T rr = rb[g1] + rb[g2];
+        if (!(dot3(dv, dv) < rr * rr)) return 0;
+        const T* sz = F<T>(m.geom_size);
+        T r1 = sz[3 * g1], r2 = sz[3 * g2];
+        T A[3], B[3];
+        if (t1 == kGeomSphere && t2 == kGeomSphere) {
+            for (int k = 0; k < 3; ++k) { A[k] = c1[k]; B[k] = c2[k]; }
+        } else if (t1 == kGeomSphere) {
+            T p2[3], q2[3];
+            segment(m, s, g2, p2, q2);
+            seg_closest(p2, q2, c1, c1, B, A);
+        } else if (t2 == kGeomSphere) {
+            T p1[3], q1[3];
+            segment(m, s, g1, p1, q1);
+            seg_closest(p1, q1, c2, c2, A, B);
+        } else {
+            T p1[3], q1[3], p2[3], q2[3];
+            segment(m, s, g1, p1, q1);
+            segment(m, s, g2, p2, q2);
+            seg_closest(p1, q1, p2, q2, A, B);
+        }
+        T e[3] = {B[0] - A[0], B[1] - A[1], B[2] - A[2]};
+        T L = sqrt(dot3(e, e));
+        T n[3];
+        if (L > T(1e-12)) { n[0] = e[0] / L; n[1] = e[1] / L; n[2] = e[2] / L; }
+        else { n[0] = T(0); n[1] = T(0); n[2] = T(1); }
+        T d = L - r1 - r2;
+        if (d < T(0)) {
+            Hit<T> h;
+            h.d = d;
+            for (int i = 0; i < 3; ++i) { h.n[i] = n[i]; h.pos[i] = A[i] + n[i] * (r1 + T(0.5) * d); }
+            emit(h);
+            ++cnt;
+        }
+    }
+    return cnt;
+}
+
+template <class T> __device__ inline void make_frame(const T* n, T* fr) {
+    T e[3];
+    if (fabs(n[1]) < T(0.5)) { e[0] = T(0); e[1] = T(1); e[2] = T(0); }
+    else { e[0] = T(1); e[1] = T(0); e[2] = T(0); }
+    T t1[3], t2[3];
+    cross3(n, e, t1);
+    T r = rsqrt_t(dot3(t1, t1));
+    t1[0] *= r; t1[1] *= r; t1[2] *= r;
+    cross3(n, t1, t2);
+    for (int k = 0; k < 3; ++k) { fr[k] = n[k]; fr[3 + k] = t1[k]; fr[6 + k] = t2[k]; }
+}
+
+// broadphase + narrowphase over all pairs, compacted in pair order; returns ncon (warp-uniform)
+template <class T> __device__ int collide(const s3_model& m, WS<T>& s, int lane, int& dropped) {
+    int base = 0;
+    dropped = 0;
+    const T* fric = F<T>(m.geom_friction);
+    for (int p0 = 0; p0 < m.npair; p0 += 32) {
+        int p = p0 + lane;
+        int cnt = p < m.npair ? narrow(m, s, p, [](const Hit<T>&) {}) : 0;
+        int incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int y = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += y;
+        }
+        int total = __shfl_sync(FULL, incl, 31);
+        int off = base + incl - cnt;
+        if (cnt) {
+            int g1 = m.pair_geom[2 * p], g2 = m.pair_geom[2 * p + 1];
+            T mu = fmax(fric[g1], fric[g2]);
+            int slot = off;
+            narrow(m, s, p, [&](const Hit<T>& h) {
+                if (slot < S3_MAX_CON) {
+                    T* c = s.con + kConStride * slot;
+                    c[0] = h.d;
+                    c[1] = h.pos[0]; c[2] = h.pos[1]; c[3] = h.pos[2];
+                    make_frame(h.n, c + 4);
+                    c[13] = mu;
+                    s.con_pair[slot] = p;
+                }
+                ++slot;
+            });
+        }
+        base += total;
+    }
+    __syncwarp();
+    if (base > S3_MAX_CON) {
+        dropped = base - S3_MAX_CON;
+        base = S3_MAX_CON;
+    }
+    return base;
+}
+
+// ---------------------------------------------------------------- constraints
+
+template <class T> __device__ inline T impedance(const s3_model& m, T r) {
+    T dmin = T(m.solimp[0]), dmax = T(m.solimp[1]), width = T(m.solimp[2]), mid = T(m.solimp[3]),
+      power = T(m.solimp[4]);
+    T x = fabs(r) / width;
+    T d;
+    if (x >= T(1)) d = dmax;
+    else {
+        T y = x <= mid ? pow(x, power) / pow(mid, power - T(1))
+                       : T(1) - pow(T(1) - x, power) / pow(T(1) - mid, power - T(1));
+        d = dmin + y * (dmax - dmin);
+    }
+    return fmin(fmax(d, T(1e-4)), T(0.9999));
+}
+
+// Contact Jacobians Jc[c][3][stride] (frame rows over the pair's chain), limit rows, aref, D.
+template <class T> __device__ int build_rows(const s3_model& m, WS<T>& s, int ncon, int& nlim, int lane) {
+    // limits: ballot-compact the violated sides
+    const T* rng = F<T>(m.lim_range);
+    nlim = 0;
+    for (int l0 = 0; l0 < m.nlimjnt; l0 += 32) {
+        int l = l0 + lane;
+        T dlo = T(1), dhi = T(1);
+        if (l < m.nlimjnt) {
+            T q = s.qpos[m.lim_qposadr[l]];
+            dlo = q - rng[2 * l];
+            dhi = rng[2 * l + 1] - q;
+        }
+        bool lo = dlo < T(0), hi = dhi < T(0);
+        // oracle order per joint: lower then upper (at most one is violated)
+        unsigned mk = __ballot_sync(FULL, lo || hi);
+        int rank = __popc(mk & ((1u << lane) - 1));
+        int slot = nlim + rank;
+        if ((lo || hi) && slot < S3_MAX_LIM) {
+            s.lim_dof[slot] = m.lim_dofadr[l];
+            s.lim_sign[slot] = lo ? 1 : -1;
+            s.rjar[slot] = lo ? dlo : dhi;  // pos, stashed until aref below
+        }
+        nlim += __popc(mk);
+    }
+    if (nlim > S3_MAX_LIM) nlim = S3_MAX_LIM;
+    __syncwarp();
+    // contact Jacobians: serial over contacts, lanes over chain columns
+    const T* iw = F<T>(m.body_invweight0);
+    int stride = m.chain_stride;
+    for (int c = 0; c < ncon; ++c) {
+        int p = s.con_pair[c];
+        int len = m.pair_chainlen[p];
+        int b1 = m.geom_bodyid[m.pair_geom[2 * p]], b2 = m.geom_bodyid[m.pair_geom[2 * p + 1]];
+        uint64_t m1 = m.body_dofmask[b1], m2 = m.body_dofmask[b2];
+        const T* cc = s.con + kConStride * c;
+        T dp[3] = {cc[1] - s.com[0], cc[2] - s.com[1], cc[3] - s.com[2]};
+        for (int k = lane; k < len; k += 32) {
+            int d = m.pair_chain[p * S3_MAX_CHAIN + k];
+            const T* cd = s.cdof + 6 * d;
+            T w[3];
+            cross3(cd, dp, w);
+            T jv[3] = {cd[3] + w[0], cd[4] + w[1], cd[5] + w[2]};
+            T sg = T(((m2 >> d) & 1ull) ? 1 : 0) - T(((m1 >> d) & 1ull) ? 1 : 0);
+            T* J = s.Jc + (3 * c) * stride;
+            J[k] = sg * dot3(cc + 4, jv);
+            J[stride + k] = sg * dot3(cc + 7, jv);
+            J[2 * stride + k] = sg * dot3(cc + 10, jv);
+        }
+    }
+    __syncwarp();
+    int nefc = nlim + 4 * ncon;
+    // J qvel per row (contact frame dots first)
+    for (int t = lane; t < 3 * ncon; t += 32) {
+        int c = t / 3, r = t % 3;
+        int p = s.con_pair[c];
+        int len = m.pair_chainlen[p];
+        const T* J = s.Jc + (3 * c + r) * stride;
+        T acc = T(0);
+        for (int k = 0; k < len; ++k) acc += J[k] * s.qvel[m.pair_chain[p * S3_MAX_CHAIN + k]];
+        s.cdot[t] = acc;
+    }
+    __syncwarp();
+    T tc = fmax(T(m.solref[0]), T(2) * T(m.timestep));
+    T dr = T(m.solref[1]);
+    T dmax = T(m.solimp[1]);
+    T kk = T(1) / (dmax * dmax * tc * tc * dr * dr);
+    T bb = T(2) / (dmax * tc);
+    const T* diw = F<T>(m.dof_invweight0);
+    for (int r = lane; r < nefc; r += 32) {
+        T pos, vel, A;
+        if (r < nlim) {
+            int d = s.lim_dof[r];
+            pos = s.rjar[r];
+            vel = T(s.lim_sign[r]) * s.qvel[d];
+            A = diw[d];
+        } else {
+            int c = (r - nlim) >> 2, e = (r - nlim) & 3;
+            const T* cc = s.con + kConStride * c;
+            T mu = cc[13];
+            T sg = (e & 1) ? -mu : mu;
+            pos = cc[0];
+            vel = s.cdot[3 * c] + sg * s.cdot[3 * c + 1 + (e >> 1)];
+            int p = s.con_pair[c];
+            int b1 = m.geom_bodyid[m.pair_geom[2 * p]], b2 = m.geom_bodyid[m.pair_geom[2 * p + 1]];
+            A = (T(1) + mu * mu) * (iw[b1] + iw[b2]);
+        }
+        T imp = impedance(m, pos);
+        T R = fmax((T(1) - imp) / imp * A, T(1e-15));
+        s.rD[r] = T(1) / R;
+        s.raref[r] = -bb * vel - kk * imp * pos;
+    }
+    __syncwarp();
+    return nefc;
+}
+
+// out[r] = J_r x for all rows
+template <class T> __device__ void rows_mul(const s3_model& m, WS<T>& s, int ncon, int nlim, const T* x, T* out,
+                                            int lane) {
+    int stride = m.chain_stride;
+    for (int t = lane; t < 3 * ncon; t += 32) {
+        int c = t / 3, r = t % 3;
+        int p = s.con_pair[c];
+        int len = m.pair_chainlen[p];
+        const T* J = s.Jc + (3 * c + r) * stride;
+        T acc = T(0);
+        for (int k = 0; k < len; ++k) acc += J[k] * x[m.pair_chain[p * S3_MAX_CHAIN + k]];
+        s.cdot[t] = acc;
+    }
+    __syncwarp();
+    int nefc = nlim + 4 * ncon;
+    for (int r = lane; r < nefc; r += 32) {
+        T v;
+        if (r < nlim) v = T(s.lim_sign[r]) * x[s.lim_dof[r]];
+        else {
+            int c = (r - nlim) >> 2, e = (r - nlim) & 3;
+            T mu = s.con[kConStride * c + 13];
+            T sg = (e & 1) ? -mu : mu;
+            v = s.cdot[3 * c] + sg * s.cdot[3 * c + 1 + (e >> 1)];
+        }
+        out[r] = v;
+    }
+    __syncwarp();
+}
+
+// y += J^T (coef) where coef[r] is per row
+template <class T> __device__ void rows_tmul_add(const s3_model& m, WS<T>& s, int ncon, int nlim, const T* coef, T* y,
+                                                 int lane) {
+    int stride = m.chain_stride;
+    for (int r = lane; r < nlim; r += 32) y[s.lim_dof[r]] += T(s.lim_sign[r]) * coef[r];
+    __syncwarp();
+    for (int c = 0; c < ncon; ++c) {
+        const T* w = coef + nlim + 4 * c;
+        T mu = s.con[kConStride * c + 13];
+        T cn = ((w[0] + w[1]) + w[2]) + w[3];
+        T c1 = mu * (w[0] - w[1]);
+        T c2 = mu * (w[2] - w[3]);
+        int p = s.con_pair[c];
+        int len = m.pair_chainlen[p];
+        const T* J = s.Jc + (3 * c) * stride;
+        for (int k = lane; k < len; k += 32)
+            y[m.pair_chain[p * S3_MAX_CHAIN + k]] += cn * J[k] + c1 * J[stride + k] + c2 * J[2 * stride + k];
+        __syncwarp();
+    }
+}
+
+template <class T> __device__ T total_cost(const s3_model& m, WS<T>& s, int nefc, const T* a, const T* Ma,
+                                           const T* jar, int lane) {
+    T g = T(0);
+    for (int i = lane; i < m.nv; i += 32) g += (a[i] - s.a0[i]) * (Ma[i] - s.smooth[i]);
+    T c = T(0);
+    for (int r = lane; r < nefc; r += 32)
+        if (jar[r] < T(0)) c += s.rD[r] * jar[r] * jar[r];
+    return T(0.5) * wsum(g) + T(0.5) * wsum(c);
+}
+
+// mj_solNewton restated (oracle newton / line_search)
+template <class T> __device__ int newton(const s3_model& m, WS<T>& s, int ncon, int nlim, bool warm_ok, int lane) {
+    int nv = m.nv;
+    int nefc = nlim + 4 * ncon;
+    T scale = T(m.scale);
+    T tol = T(m.tolerance);
+    // a = a0 (a0 currently holds qacc_smooth)
+    for (int i = lane; i < nv; i += 32) s.a[i] = s.a0[i];
+    __syncwarp();
+    sym_mul(nv, s.M, s.a, s.Ma, lane);
+    rows_mul(m, s, ncon, nlim, s.a, s.rjar, lane);
+    for (int r = lane; r < nefc; r += 32) s.rjar[r] -= s.raref[r];
+    __syncwarp();
+    T cost = total_cost(m, s, nefc, s.a, s.Ma, s.rjar, lane);
+    if (warm_ok) {
+        // candidate: qacc_warmstart staged in s.p; Mw -> s.Mp, jw -> s.rJp
+        sym_mul(nv, s.M, s.p, s.Mp, lane);
+        rows_mul(m, s, ncon, nlim, s.p, s.rJp, lane);
+        for (int r = lane; r < nefc; r += 32) s.rJp[r] -= s.raref[r];
+        __syncwarp();
+        T cw = total_cost(m, s, nefc, s.p, s.Mp, s.rJp, lane);
+        if (cw < cost) {
+            for (int i = lane; i < nv; i += 32) { s.a[i] = s.p[i]; s.Ma[i] = s.Mp[i]; }
+            for (int r = lane; r < nefc; r += 32) s.rjar[r] = s.rJp[r];
+            cost = cw;
+            __syncwarp();
+        }
+    }
+    int its = 0;
+    for (int it = 0; it < m.iterations; ++it) {
+        // gradient
+        for (int r = lane; r < nefc; r += 32) s.rJp[r] = s.rjar[r] < T(0) ? s.rD[r] * s.rjar[r] : T(0);
+        for (int i = lane; i < nv; i += 32) s.grad[i] = s.Ma[i] - s.smooth[i];
+        __syncwarp();
+        rows_tmul_add(m, s, ncon, nlim, s.rJp, s.grad, lane);
+        T gn = T(0);
+        for (int i = lane; i < nv; i += 32) gn += s.grad[i] * s.grad[i];
+        gn = wsum(gn);
+        if (scale * sqrt(gn) < tol) break;
+        ++its;
+        // H = M + J^T diag(D act) J on the packed lower LD buffer
+        int np = nv * (nv + 1) / 2;
+        for (int t = lane; t < np; t += 32) s.LD[t] = s.M[t];
+        __syncwarp();
+        for (int r = lane; r < nlim; r += 32)
+            if (s.rjar[r] < T(0)) s.LD[tri(s.lim_dof[r], s.lim_dof[r])] += s.rD[r];
+        __syncwarp();
+        int stride = m.chain_stride;
+        for (int c = 0; c < ncon; ++c) {
+            const T* jr = s.rjar + nlim + 4 * c;
+            const T* D = s.rD + nlim + 4 * c;
+            T w0 = jr[0] < T(0) ? D[0] : T(0), w1 = jr[1] < T(0) ? D[1] : T(0);
+            T w2 = jr[2] < T(0) ? D[2] : T(0), w3 = jr[3] < T(0) ? D[3] : T(0);
+            if (w0 == T(0) && w1 == T(0) && w2 == T(0) && w3 == T(0)) continue;
+            T mu = s.con[kConStride * c + 13];
+            T W00 = ((w0 + w1) + w2) + w3, W01 = mu * (w0 - w1), W02 = mu * (w2 - w3);
+            T W11 = mu * mu * (w0 + w1), W22 = mu * mu * (w2 + w3);
+            int p = s.con_pair[c];
+            int len = m.pair_chainlen[p];
+            const uint8_t* ch = m.pair_chain + p * S3_MAX_CHAIN;
+            const T* J0 = s.Jc + (3 * c) * stride;
+            const T* J1 = J0 + stride;
+            const T* J2 = J1 + stride;
+            int npair = len * (len + 1) / 2;
+            for (int t = lane; t < npair; t += 32) {
+                int a, b;
+                tri_decode(t, a, b);
+                T x0 = J0[a], x1 = J1[a], x2 = J2[a];
+                T y0 = J0[b], y1 = J1[b], y2 = J2[b];
+                T v = x0 * (W00 * y0 + W01 * y1 + W02 * y2) + x1 * (W01 * y0 + W11 * y1) + x2 * (W02 * y0 + W22 * y2);
+                s.LD[tri(ch[a], ch[b])] += v;
+            }
+            __syncwarp();
+        }
+        cholesky(nv, s.LD, lane);
+        for (int i = lane; i < nv; i += 32) s.p[i] = -s.grad[i];
+        __syncwarp();
+        chol_solve(nv, s.LD, s.p, lane);
+        sym_mul(nv, s.M, s.p, s.Mp, lane);
+        rows_mul(m, s, ncon, nlim, s.p, s.rJp, lane);
+        // exact line search along p: bracketed Newton on phi'
+        T g0 = T(0), h0 = T(0);
+        for (int i = lane; i < nv; i += 32) {
+            g0 += s.p[i] * (s.Ma[i] - s.smooth[i]);
+            h0 += s.p[i] * s.Mp[i];
+        }
+        g0 = wsum(g0);
+        h0 = wsum(h0);
+        auto deriv = [&](T al, T& d1, T& d2) {
+            T x1 = T(0), x2 = T(0);
+            for (int r = lane; r < nefc; r += 32) {
+                T x = s.rjar[r] + al * s.rJp[r];
+                if (x < T(0)) {
+                    x1 += s.rD[r] * x * s.rJp[r];
+                    x2 += s.rD[r] * s.rJp[r] * s.rJp[r];
+                }
+            }
+            d1 = g0 + al * h0 + wsum(x1);
+            d2 = h0 + wsum(x2);
+        };
+        T d0, dd;
+        deriv(T(0), d0, dd);
+        T alpha = T(0);
+        if (d0 < T(0)) {
+            T lo = T(0), hi = T(INFINITY), al = T(1);
+            for (int li = 0; li < m.ls_iterations; ++li) {
+                T d1, d2;
+                deriv(al, d1, d2);
+                if (fabs(d1) < T(m.ls_tolerance) * fabs(d0)) break;
+                if (d1 < T(0)) lo = al;
+                else hi = al;
+                T an = al - d1 / d2;
+                if (!(lo < an && an < hi)) an = T(0.5) * (lo + hi);
+                al = an;
+            }
+            alpha = al;
+        }
+        if (alpha == T(0)) break;
+        for (int i = lane; i < nv; i += 32) {
+            s.a[i] += alpha * s.p[i];
+            s.Ma[i] += alpha * s.Mp[i];
+        }
+        for (int r = lane; r < nefc; r += 32) s.rjar[r] += alpha * s.rJp[r];
+        __syncwarp();
+        T nc = total_cost(m, s, nefc, s.a, s.Ma, s.rjar, lane);
+        T impv = scale * (cost - nc);
+        cost = nc;
+        if (impv < tol) break;
+    }
+    // forces and qfrc_constraint
+    for (int r = lane; r < nefc; r += 32) s.rJp[r] = s.rjar[r] < T(0) ? -s.rD[r] * s.rjar[r] : T(0);
+    for (int i = lane; i < nv; i += 32) s.fcon[i] = T(0);
+    __syncwarp();
+    rows_tmul_add(m, s, ncon, nlim, s.rJp, s.fcon, lane);
+    return its;
+}
+
+// ---------------------------------------------------------------- the step kernel
+
+template <class T>
+__global__ void __launch_bounds__(32 * 8) step_kernel(const __grid_constant__ s3_model m, const __grid_constant__ s3_data d,
+                                                      const __grid_constant__ s3_layout l, int nsub) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    int lane = threadIdx.x & 31;
+    int wib = threadIdx.x >> 5;
+    int64_t w = (int64_t)blockIdx.x * l.warps_per_block + wib;
+    if (w >= d.nworld) return;
+    T* base = reinterpret_cast<T*>(smem_raw) + (size_t)wib * l.elems_per_world;
+    WS<T> s = make_ws(base, l);
+    const int nq = m.nq, nv = m.nv, nu = m.nu;
+    T* gq = static_cast<T*>(d.qpos) + w * nq;
+    T* gv = static_cast<T*>(d.qvel) + w * nv;
+    T* gw = d.qacc_warmstart ? static_cast<T*>(d.qacc_warmstart) + w * nv : nullptr;
+    const T* gapp = d.qfrc_applied ? static_cast<const T*>(d.qfrc_applied) + w * nv : nullptr;
+    for (int i = lane; i < nq; i += 32) s.qpos[i] = gq[i];
+    for (int i = lane; i < nv; i += 32) s.qvel[i] = gv[i];
+    for (int i = lane; i < nu; i += 32) s.ctrl[i] = static_cast<const T*>(d.ctrl)[w * nu + i];
+    __syncwarp();
+    T dt = T(m.timestep);
+    int ncon = 0, nlim = 0, dropped = 0, its = 0;
+    for (int sub = 0; sub < nsub; ++sub) {
+        kinematics(m, s, lane);
+        com_pos(m, s, lane);
+        crb_mass(m, s, lane);
+        int np = nv * (nv + 1) / 2;
+        for (int t = lane; t < np; t += 32) s.LD[t] = s.M[t];
+        __syncwarp();
+        factor_ldl(m, s.LD, lane);
+        rne(m, s, lane);
+        smooth_force(m, s, gapp, lane);
+        if (sub == nsub - 1 && d.qM) {  // parity outputs of the factor before it is overwritten
+            T* o = static_cast<T*>(d.qLD) + w * np;
+            for (int t = lane; t < np; t += 32) o[t] = s.LD[t];
+        }
+        solve_ldl(m, s.LD, s.a0, lane);
+        ncon = collide(m, s, lane, dropped);
+        int nefc = build_rows(m, s, ncon, nlim, lane);
+        (void)nefc;
+        if (gw) {
+            for (int i = lane; i < nv; i += 32) s.p[i] = gw[i];
+            __syncwarp();
+        }
+        its = newton(m, s, ncon, nlim, gw != nullptr, lane);
+        if (gw) {
+            for (int i = lane; i < nv; i += 32) gw[i] = s.a[i];
+        }
+        // implicitfast: (M + dt diag(damping + kv)) acc = smooth + constraint
+        const T* damp = F<T>(m.dof_damping);
+        for (int t = lane; t < np; t += 32) s.LD[t] = s.M[t];
+        __syncwarp();
+        for (int i = lane; i < nv; i += 32) s.LD[tri(i, i)] += dt * (damp[i] + s.kvd[i]);
+        for (int i = lane; i < nv; i += 32) s.grad[i] = s.smooth[i] + s.fcon[i];
+        __syncwarp();
+        if (sub == nsub - 1 && d.qM) {  // parity outputs (pre-integration quantities)
+            T* oM = static_cast<T*>(d.qM) + w * np;
+            for (int t = lane; t < np; t += 32) oM[t] = s.M[t];
+            for (int i = lane; i < nv; i += 32) {
+                static_cast<T*>(d.qfrc_bias)[w * nv + i] = s.bias[i];
+                static_cast<T*>(d.qfrc_smooth)[w * nv + i] = s.smooth[i];
+                static_cast<T*>(d.qacc_smooth)[w * nv + i] = s.a0[i];
+                static_cast<T*>(d.qacc)[w * nv + i] = s.a[i];
+                static_cast<T*>(d.qfrc_constraint)[w * nv + i] = s.fcon[i];
+                for (int k = 0; k < 6; ++k) static_cast<T*>(d.cdof)[(w * nv + i) * 6 + k] = s.cdof[6 * i + k];
+            }
+            for (int b = lane; b < m.nbody; b += 32) {
+                for (int k = 0; k < 3; ++k) static_cast<T*>(d.xpos)[(w * m.nbody + b) * 3 + k] = s.xpos[3 * b + k];
+                for (int k = 0; k < 4; ++k) static_cast<T*>(d.xquat)[(w * m.nbody + b) * 4 + k] = s.xquat[4 * b + k];
+            }
+            if (lane < 3) static_cast<T*>(d.com)[w * 3 + lane] = s.com[lane];
+            for (int c = lane; c < ncon; c += 32) {
+                const T* cc = s.con + kConStride * c;
+                static_cast<T*>(d.con_dist)[w * S3_MAX_CON + c] = cc[0];
+                for (int k = 0; k < 3; ++k) static_cast<T*>(d.con_pos)[(w * S3_MAX_CON + c) * 3 + k] = cc[1 + k];
+                for (int k = 0; k < 9; ++k) static_cast<T*>(d.con_frame)[(w * S3_MAX_CON + c) * 9 + k] = cc[4 + k];
+                d.con_pair[w * S3_MAX_CON + c] = s.con_pair[c];
+            }
+            for (int r = lane; r < nlim + 4 * ncon; r += 32)
+                static_cast<T*>(d.efc_force)[w * S3_MAX_ROWS + r] = s.rJp[r];
+            if (lane == 0) {
+                d.ncon[w] = ncon;
+                d.ndropped[w] = dropped;
+                d.nefc[w] = nlim + 4 * ncon;
+                d.solver_niter[w] = its;
+            }
+        }
+        factor_ldl(m, s.LD, lane);
+        solve_ldl(m, s.LD, s.grad, lane);
+        for (int i = lane; i < nv; i += 32) s.qvel[i] += dt * s.grad[i];
+        __syncwarp();
+        // integrate positions (oracle integrate_pos)
+        for (int j = lane; j < m.njnt; j += 32) {
+            int a = m.jnt_qposadr[j], dd = m.jnt_dofadr[j];
+            if (m.jnt_type[j] == kJntFree) {
+                for (int k = 0; k < 3; ++k) s.qpos[a + k] = s.qpos[a + k] + dt * s.qvel[dd + k];
+                T wv[3] = {s.qvel[dd + 3], s.qvel[dd + 4], s.qvel[dd + 5]};
+                T nw = sqrt(dot3(wv, wv));
+                T qt[4] = {s.qpos[a + 3], s.qpos[a + 4], s.qpos[a + 5], s.qpos[a + 6]};
+                if (nw > T(1e-15)) {
+                    T sn, cs;
+                    sincos_t(T(0.5) * (nw * dt), &sn, &cs);
+                    T inv = T(1) / nw;
+                    T qa[4] = {cs, wv[0] * inv * sn, wv[1] * inv * sn, wv[2] * inv * sn};
+                    T r[4];
+                    qmul(qt, qa, r);
+                    qt[0] = r[0]; qt[1] = r[1]; qt[2] = r[2]; qt[3] = r[3];
+                }
+                qnormalize(qt);
+                for (int k = 0; k < 4; ++k) s.qpos[a + 3 + k] = qt[k];
+            } else {
+                s.qpos[a] = s.qpos[a] + dt * s.qvel[dd];
+            }
+        }
+        __syncwarp();
+        if (d.time && lane == 0) static_cast<T*>(d.time)[w] += dt;
+    }
+    if (d.geom_xpos) {  // frames of the last substep's kinematics (sensors)
+        for (int g = lane; g < m.ngeom; g += 32) {
+            for (int k = 0; k < 3; ++k) static_cast<T*>(d.geom_xpos)[(w * m.ngeom + g) * 3 + k] = s.gpos[3 * g + k];
+            for (int k = 0; k < 9; ++k) static_cast<T*>(d.geom_xmat)[(w * m.ngeom + g) * 9 + k] = s.gmat[9 * g + k];
+        }
+    }
+    for (int i = lane; i < nq; i += 32) gq[i] = s.qpos[i];
+    for (int i = lane; i < nv; i += 32) gv[i] = s.qvel[i];
+}
+
+}  // namespace s3
+
+// ---------------------------------------------------------------- C-ABI
+
+namespace {
+thread_local char g_err[512] = "";
+int fail(int code, const char* msg) {
+    snprintf(g_err, sizeof(g_err), "%s", msg);
+    return code;
+}
+}  // namespace
+
+extern "C" {
+
+int s3_abi_version(void) { return S3_ABI_VERSION; }
+
+size_t s3_sizeof(int which) {
+    switch (which) {
+        case 0: return sizeof(s3_model);
+        case 1: return sizeof(s3_data);
+        case 2: return sizeof(s3_layout);
+        default: return 0;
+    }
+}
+
+const char* s3_last_error(void) { return g_err; }
+
+int s3_plan(const s3_model* m, int32_t warps_per_block, s3_layout* out) {
+    using namespace s3;
+    if (!m || !out) return fail(S3_ERR_ARG, "null argument");
+    if (m->nv > S3_MAX_NV || m->nbody > S3_MAX_NBODY || m->chain_stride > S3_MAX_CHAIN || m->nlimjnt > 64)
+        return fail(S3_ERR_BOUNDS, "model exceeds kernel bounds");
+    int nb = m->nbody, nv = m->nv, nj = m->njnt, ng = m->ngeom, nq = m->nq, nu = m->nu;
+    int np = nv * (nv + 1) / 2;
+    int sizes[O_END] = {};
+    sizes[O_XPOS] = 3 * nb; sizes[O_XQUAT] = 4 * nb; sizes[O_XIPOS] = 3 * nb; sizes[O_CINERT] = 10 * nb;
+    sizes[O_CRB] = 10 * nb; sizes[O_CDOF] = 6 * nv; sizes[O_CDOFD] = 6 * nv; sizes[O_CVEL] = 6 * nb;
+    sizes[O_CACC] = 6 * nb; sizes[O_JANC] = 3 * nj; sizes[O_JAX] = 3 * nj; sizes[O_M] = np; sizes[O_LD] = np;
+    sizes[O_QPOS] = nq; sizes[O_QVEL] = nv; sizes[O_SMOOTH] = nv; sizes[O_A0] = nv; sizes[O_A] = nv;
+    sizes[O_MA] = nv; sizes[O_GRAD] = nv; sizes[O_P] = nv; sizes[O_MP] = nv; sizes[O_KVD] = nv;
+    sizes[O_GPOS] = 3 * ng; sizes[O_GMAT] = 9 * ng; sizes[O_CON] = kConStride * S3_MAX_CON;
+    sizes[O_JC] = 3 * S3_MAX_CON * m->chain_stride; sizes[O_RAREF] = S3_MAX_ROWS; sizes[O_RD] = S3_MAX_ROWS;
+    sizes[O_RJAR] = S3_MAX_ROWS; sizes[O_RJP] = S3_MAX_ROWS; sizes[O_CDOT] = 3 * S3_MAX_CON; sizes[O_BIAS] = nv;
+    sizes[O_FCON] = nv; sizes[O_CTRL] = nu; sizes[O_COM] = 4;
+    int esz = m->dtype == S3_F64 ? 8 : 4;
+    int ints = S3_MAX_CON + 2 * S3_MAX_LIM + 8;
+    sizes[O_INT] = (ints * 4 + esz - 1) / esz;
+    int off = 0;
+    for (int k = 0; k < O_END; ++k) {
+        out->off[k] = off;
+        off += (sizes[k] + 1) & ~1;  // keep 8-byte alignment for the float build's int region
+    }
+    out->elems_per_world = off;
+    int per = off * esz;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int maxsm = 0;
+    if (cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess || maxsm <= 0)
+        maxsm = 227 * 1024;
+    int wpb = warps_per_block > 0 ? warps_per_block : maxsm / per;
+    if (wpb > 8) wpb = 8;
+    if (wpb < 1 || wpb * per > maxsm) return fail(S3_ERR_BOUNDS, "one world does not fit in shared memory");
+    out->warps_per_block = wpb;
+    out->bytes_per_block = wpb * per;
+    return S3_OK;
+}
+
+int s3_step(const s3_model* m, const s3_data* d, const s3_layout* l, int32_t nsub, void* stream) {
+    using namespace s3;
+    if (!m || !d || !l || nsub < 0) return fail(S3_ERR_ARG, "null argument");
+    if (d->nworld == 0 || nsub == 0) return S3_OK;
+    if (!d->qpos || !d->qvel || !d->ctrl) return fail(S3_ERR_ARG, "qpos/qvel/ctrl required");
+    if (d->qM && (!d->qLD || !d->qfrc_bias || !d->qfrc_smooth || !d->qacc_smooth || !d->qacc || !d->qfrc_constraint ||
+                  !d->cdof || !d->xpos || !d->xquat || !d->com || !d->ncon || !d->ndropped || !d->nefc ||
+                  !d->con_pair || !d->con_dist || !d->con_pos || !d->con_frame || !d->efc_force || !d->solver_niter))
+        return fail(S3_ERR_ARG, "qM set: every parity output is required");
+    if (d->geom_xpos && !d->geom_xmat) return fail(S3_ERR_ARG, "geom_xmat required with geom_xpos");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    int wpb = l->warps_per_block;
+    unsigned grid = (unsigned)((d->nworld + wpb - 1) / wpb);
+    size_t smem = (size_t)l->bytes_per_block;
+    cudaError_t e;
+    if (m->dtype == S3_F64) {
+        e = cudaFuncSetAttribute(step_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e == cudaSuccess) step_kernel<double><<<grid, 32 * wpb, smem, st>>>(*m, *d, *l, nsub);
+    } else {
+        e = cudaFuncSetAttribute(step_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e == cudaSuccess) step_kernel<float><<<grid, 32 * wpb, smem, st>>>(*m, *d, *l, nsub);
+    }
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(S3_ERR_CUDA, cudaGetErrorString(e));
+    return S3_OK;
+}
+
+}  // extern "C"
