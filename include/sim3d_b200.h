@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define S3_ABI_VERSION 1
+#define S3_ABI_VERSION 2
 #define S3_F64 0
 #define S3_F32 1
 
@@ -122,6 +122,14 @@ typedef struct s3_model {
     const int32_t* act_qposadr;
     const int32_t* act_kind;
     const void* act_gain;
+    /* derived tables: per-dof (i, j) update lists of the tree-sparse factorization (ldl_ptr[nv+1],
+     * ldl_pair = i << 8 | j), Jacobian class per pair (pairs with identical column lists), 1 when a
+     * pair's J^T J keeps the tree sparsity pattern, and the (a, b) decode of packed-lower index t */
+    const int32_t* ldl_ptr;
+    const uint16_t* ldl_pair;
+    const int32_t* pair_class;
+    const int32_t* pair_tree;
+    const uint16_t* tri_tab;
     /* heightfield samples (hf_nrow, hf_ncol) */
     const void* hfield;
 } s3_model;

@@ -38,15 +38,7 @@ enum {
     O_CON, O_JC, O_RAREF, O_RD, O_RJAR, O_RJP, O_CDOT, O_BIAS, O_FCON, O_CTRL, O_COM, O_INT, O_END
 };
 
-__host__ __device__ inline int tri(int i, int j) { return i * (i + 1) / 2 + j; }  // packed lower, i >= j
-
-__device__ inline void tri_decode(int t, int& a, int& b) {
-    int x = (int)((sqrtf(8.0f * (float)t + 1.0f) - 1.0f) * 0.5f);
-    while ((x + 1) * (x + 2) / 2 <= t) ++x;
-    while (x * (x + 1) / 2 > t) --x;
-    a = x;
-    b = t - x * (x + 1) / 2;
-}
+__host__ __device__ inline int tri(int i, int j) { return ((i * (i + 1)) >> 1) + j; }  // packed lower, i >= j
 
 template <class T> __device__ inline T wsum(T v) {
 #pragma unroll
@@ -154,7 +146,7 @@ template <class T> __device__ inline T clampt(T x, T lo, T hi) { return x < lo ?
 template <class T> struct WS {
     T *xpos, *xquat, *xipos, *cinert, *crb, *cdof, *cdofd, *cvel, *cacc, *janc, *jax, *M, *LD, *qpos, *qvel,
         *smooth, *a0, *a, *Ma, *grad, *p, *Mp, *kvd, *gpos, *gmat, *con, *Jc, *raref, *rD, *rjar, *rJp, *cdot,
-        *bias, *fcon, *ctrl, *com;
+        *bias, *fcon, *ctrl, *com, *tk, *u;
     int *con_pair, *lim_dof, *lim_sign, *misc;
 };
 
@@ -162,8 +154,11 @@ template <class T> __device__ inline WS<T> make_ws(T* base, const s3_layout& l) 
     WS<T> s;
     const int* o = l.off;
     s.xpos = base + o[O_XPOS]; s.xquat = base + o[O_XQUAT]; s.xipos = base + o[O_XIPOS];
-    s.cinert = base + o[O_CINERT]; s.crb = base + o[O_CRB]; s.cdof = base + o[O_CDOF]; s.cdofd = base + o[O_CDOFD];
-    s.cvel = base + o[O_CVEL]; s.cacc = base + o[O_CACC]; s.janc = base + o[O_JANC]; s.jax = base + o[O_JAX];
+    s.cinert = base + o[O_CINERT]; s.crb = s.cinert; s.cdof = base + o[O_CDOF];
+    s.tk = base + o[O_CRB]; s.u = s.tk + S3_MAX_NV;
+    s.janc = base + o[O_JANC]; s.jax = base + o[O_JAX];
+    // RNE scratch lives in the contact-Jacobian region (dead until build_rows)
+    s.cdofd = base + o[O_JC]; s.cvel = s.cdofd + o[O_CDOFD]; s.cacc = s.cvel + o[O_CVEL];
     s.M = base + o[O_M]; s.LD = base + o[O_LD]; s.qpos = base + o[O_QPOS]; s.qvel = base + o[O_QVEL];
     s.smooth = base + o[O_SMOOTH]; s.a0 = base + o[O_A0]; s.a = base + o[O_A]; s.Ma = base + o[O_MA];
     s.grad = base + o[O_GRAD]; s.p = base + o[O_P]; s.Mp = base + o[O_MP]; s.kvd = base + o[O_KVD];
@@ -333,14 +328,17 @@ template <class T> __device__ void com_pos(const s3_model& m, WS<T>& s, int lane
     __syncwarp();
 }
 
-// mj_crb: composite inertias (levels, deepest first, children in descending index) + packed M
+// mj_crb: composite inertias (levels, deepest first, children in descending index) + packed M.
+// Accumulates in place over cinert (RNE, the only other reader of cinert, has already run).
 template <class T> __device__ void crb_mass(const s3_model& m, WS<T>& s, int lane) {
-    for (int L = m.nlevel - 1; L >= 1; --L) {
+    for (int L = m.nlevel - 2; L >= 1; --L) {
         int n0 = m.level_ptr[L], nl = m.level_ptr[L + 1] - n0;
         for (int t = lane; t < nl * 10; t += 32) {
             int b = m.level_body[n0 + t / 10], c = t % 10;
-            T acc = s.cinert[10 * b + c];
-            for (int k = m.child_ptr[b]; k < m.child_ptr[b + 1]; ++k) acc += s.crb[10 * m.child_idx[k] + c];
+            int k0 = m.child_ptr[b], k1 = m.child_ptr[b + 1];
+            if (k0 == k1) continue;
+            T acc = s.crb[10 * b + c];
+            for (int k = k0; k < k1; ++k) acc += s.crb[10 * m.child_idx[k] + c];
             s.crb[10 * b + c] = acc;
         }
         __syncwarp();
@@ -364,24 +362,27 @@ template <class T> __device__ void crb_mass(const s3_model& m, WS<T>& s, int lan
 }
 
 // mj_factorM: tree-sparse L^T D L in place on packed-lower A (oracle factor_ldl)
-template <class T> __device__ void factor_ldl(const s3_model& m, T* A, int lane) {
+// Row k is normalised first (tk[i] = L[k,i] / D[k], u keeps the unnormalised values), then the
+// (i, j) updates of step k run from the precomputed list, one pair per lane.
+template <class T> __device__ void factor_ldl(const s3_model& m, T* A, T* tk, T* u, int lane) {
     for (int k = m.nv - 1; k >= 0; --k) {
         int len = m.dof_chainlen[k] - 1;  // strict ancestors
         if (len <= 0) continue;
         const uint8_t* ch = m.dof_chain + k * S3_MAX_CHAIN;
         T dk = A[tri(k, k)];
-        int npair = len * (len + 1) / 2;
-        for (int t = lane; t < npair; t += 32) {
-            int a, b;
-            tri_decode(t, a, b);
-            int i = ch[a], j = ch[b];
-            T tk = A[tri(k, i)] / dk;
-            A[tri(i, j)] -= tk * A[tri(k, j)];
-        }
-        __syncwarp();
         for (int a = lane; a < len; a += 32) {
             int i = ch[a];
-            A[tri(k, i)] = A[tri(k, i)] / dk;
+            T v = A[tri(k, i)];
+            T t = v / dk;
+            u[i] = v;
+            tk[i] = t;
+            A[tri(k, i)] = t;
+        }
+        __syncwarp();
+        for (int t = m.ldl_ptr[k] + lane; t < m.ldl_ptr[k + 1]; t += 32) {
+            int pr = m.ldl_pair[t];
+            int i = pr >> 8, j = pr & 255;
+            A[tri(i, j)] -= tk[i] * u[j];
         }
         __syncwarp();
     }
@@ -419,13 +420,10 @@ template <class T> __device__ void cholesky(int nv, T* H, int lane) {
         for (int i = k + 1 + lane; i < nv; i += 32) H[tri(i, k)] = H[tri(i, k)] / d;
         __syncwarp();
         if (lane == 0) H[tri(k, k)] = d;
-        int n = nv - k - 1;
-        int npair = n * (n + 1) / 2;
-        for (int t = lane; t < npair; t += 32) {
-            int a, b;
-            tri_decode(t, a, b);
-            int i = k + 1 + a, j = k + 1 + b;
-            H[tri(i, j)] -= H[tri(i, k)] * H[tri(j, k)];
+        for (int i = k + 1 + lane; i < nv; i += 32) {
+            T lik = H[tri(i, k)];
+            int ri = tri(i, 0);
+            for (int j = k + 1; j <= i; ++j) H[ri + j] -= lik * H[tri(j, k)];
         }
         __syncwarp();
     }
@@ -829,14 +827,16 @@ template <class T> __device__ int build_rows(const s3_model& m, WS<T>& s, int nc
     // contact Jacobians: serial over contacts, lanes over chain columns
     const T* iw = F<T>(m.body_invweight0);
     int stride = m.chain_stride;
-    for (int c = 0; c < ncon; ++c) {
+    for (int t = lane; t < ncon * S3_MAX_CHAIN; t += 32) {
+        int c = t / S3_MAX_CHAIN, k = t % S3_MAX_CHAIN;
         int p = s.con_pair[c];
         int len = m.pair_chainlen[p];
+        if (k >= len) continue;
         int b1 = m.geom_bodyid[m.pair_geom[2 * p]], b2 = m.geom_bodyid[m.pair_geom[2 * p + 1]];
         uint64_t m1 = m.body_dofmask[b1], m2 = m.body_dofmask[b2];
         const T* cc = s.con + kConStride * c;
         T dp[3] = {cc[1] - s.com[0], cc[2] - s.com[1], cc[3] - s.com[2]};
-        for (int k = lane; k < len; k += 32) {
+        {
             int d = m.pair_chain[p * S3_MAX_CHAIN + k];
             const T* cd = s.cdof + 6 * d;
             T w[3];
@@ -930,18 +930,27 @@ template <class T> __device__ void rows_tmul_add(const s3_model& m, WS<T>& s, in
     int stride = m.chain_stride;
     for (int r = lane; r < nlim; r += 32) y[s.lim_dof[r]] += T(s.lim_sign[r]) * coef[r];
     __syncwarp();
-    for (int c = 0; c < ncon; ++c) {
-        const T* w = coef + nlim + 4 * c;
-        T mu = s.con[kConStride * c + 13];
-        T cn = ((w[0] + w[1]) + w[2]) + w[3];
-        T c1 = mu * (w[0] - w[1]);
-        T c2 = mu * (w[2] - w[3]);
-        int p = s.con_pair[c];
-        int len = m.pair_chainlen[p];
-        const T* J = s.Jc + (3 * c) * stride;
-        for (int k = lane; k < len; k += 32)
-            y[m.pair_chain[p * S3_MAX_CHAIN + k]] += cn * J[k] + c1 * J[stride + k] + c2 * J[2 * stride + k];
+    for (int c0 = 0; c0 < ncon;) {
+        int p0 = s.con_pair[c0];
+        int cls = m.pair_class[p0];
+        int c1e = c0 + 1;
+        while (c1e < ncon && m.pair_class[s.con_pair[c1e]] == cls) ++c1e;
+        int len = m.pair_chainlen[p0];
+        for (int k = lane; k < len; k += 32) {
+            T acc = T(0);
+            for (int c = c0; c < c1e; ++c) {
+                const T* w = coef + nlim + 4 * c;
+                T mu = s.con[kConStride * c + 13];
+                T cn = ((w[0] + w[1]) + w[2]) + w[3];
+                T ca = mu * (w[0] - w[1]);
+                T cb = mu * (w[2] - w[3]);
+                const T* J = s.Jc + (3 * c) * stride;
+                acc += cn * J[k] + ca * J[stride + k] + cb * J[2 * stride + k];
+            }
+            y[m.pair_chain[p0 * S3_MAX_CHAIN + k]] += acc;
+        }
         __syncwarp();
+        c0 = c1e;
     }
 }
 
@@ -983,6 +992,9 @@ template <class T> __device__ int newton(const s3_model& m, WS<T>& s, int ncon, 
             __syncwarp();
         }
     }
+    // H = M + J^T D J keeps the tree pattern unless a contact couples two branches
+    bool tree = true;
+    for (int c = 0; c < ncon; ++c) tree = tree && m.pair_tree[s.con_pair[c]] != 0;
     int its = 0;
     for (int it = 0; it < m.iterations; ++it) {
         // gradient
@@ -1003,36 +1015,48 @@ template <class T> __device__ int newton(const s3_model& m, WS<T>& s, int ncon, 
             if (s.rjar[r] < T(0)) s.LD[tri(s.lim_dof[r], s.lim_dof[r])] += s.rD[r];
         __syncwarp();
         int stride = m.chain_stride;
-        for (int c = 0; c < ncon; ++c) {
-            const T* jr = s.rjar + nlim + 4 * c;
-            const T* D = s.rD + nlim + 4 * c;
-            T w0 = jr[0] < T(0) ? D[0] : T(0), w1 = jr[1] < T(0) ? D[1] : T(0);
-            T w2 = jr[2] < T(0) ? D[2] : T(0), w3 = jr[3] < T(0) ? D[3] : T(0);
-            if (w0 == T(0) && w1 == T(0) && w2 == T(0) && w3 == T(0)) continue;
-            T mu = s.con[kConStride * c + 13];
-            T W00 = ((w0 + w1) + w2) + w3, W01 = mu * (w0 - w1), W02 = mu * (w2 - w3);
-            T W11 = mu * mu * (w0 + w1), W22 = mu * mu * (w2 + w3);
-            int p = s.con_pair[c];
-            int len = m.pair_chainlen[p];
-            const uint8_t* ch = m.pair_chain + p * S3_MAX_CHAIN;
-            const T* J0 = s.Jc + (3 * c) * stride;
-            const T* J1 = J0 + stride;
-            const T* J2 = J1 + stride;
+        for (int c0 = 0; c0 < ncon;) {
+            int p0 = s.con_pair[c0];
+            int cls = m.pair_class[p0];
+            int c1e = c0 + 1;
+            while (c1e < ncon && m.pair_class[s.con_pair[c1e]] == cls) ++c1e;
+            int len = m.pair_chainlen[p0];
+            const uint8_t* ch = m.pair_chain + p0 * S3_MAX_CHAIN;
             int npair = len * (len + 1) / 2;
             for (int t = lane; t < npair; t += 32) {
-                int a, b;
-                tri_decode(t, a, b);
-                T x0 = J0[a], x1 = J1[a], x2 = J2[a];
-                T y0 = J0[b], y1 = J1[b], y2 = J2[b];
-                T v = x0 * (W00 * y0 + W01 * y1 + W02 * y2) + x1 * (W01 * y0 + W11 * y1) + x2 * (W02 * y0 + W22 * y2);
+                int ab = m.tri_tab[t];
+                int a = ab >> 8, b = ab & 255;
+                T v = T(0);
+                for (int c = c0; c < c1e; ++c) {
+                    const T* jr = s.rjar + nlim + 4 * c;
+                    const T* D = s.rD + nlim + 4 * c;
+                    T w0 = jr[0] < T(0) ? D[0] : T(0), w1 = jr[1] < T(0) ? D[1] : T(0);
+                    T w2 = jr[2] < T(0) ? D[2] : T(0), w3 = jr[3] < T(0) ? D[3] : T(0);
+                    T mu = s.con[kConStride * c + 13];
+                    T W00 = ((w0 + w1) + w2) + w3, W01 = mu * (w0 - w1), W02 = mu * (w2 - w3);
+                    T W11 = mu * mu * (w0 + w1), W22 = mu * mu * (w2 + w3);
+                    const T* J0 = s.Jc + (3 * c) * stride;
+                    const T* J1 = J0 + stride;
+                    const T* J2 = J1 + stride;
+                    T x0 = J0[a], x1 = J1[a], x2 = J2[a];
+                    T y0 = J0[b], y1 = J1[b], y2 = J2[b];
+                    v += x0 * (W00 * y0 + W01 * y1 + W02 * y2) + x1 * (W01 * y0 + W11 * y1) +
+                         x2 * (W02 * y0 + W22 * y2);
+                }
                 s.LD[tri(ch[a], ch[b])] += v;
             }
             __syncwarp();
+            c0 = c1e;
         }
-        cholesky(nv, s.LD, lane);
         for (int i = lane; i < nv; i += 32) s.p[i] = -s.grad[i];
         __syncwarp();
-        chol_solve(nv, s.LD, s.p, lane);
+        if (tree) {
+            factor_ldl(m, s.LD, s.tk, s.u, lane);
+            solve_ldl(m, s.LD, s.p, lane);
+        } else {
+            cholesky(nv, s.LD, lane);
+            chol_solve(nv, s.LD, s.p, lane);
+        }
         sym_mul(nv, s.M, s.p, s.Mp, lane);
         rows_mul(m, s, ncon, nlim, s.p, s.rJp, lane);
         // exact line search along p: bracketed Newton on phi'
@@ -1095,7 +1119,7 @@ template <class T> __device__ int newton(const s3_model& m, WS<T>& s, int ncon, 
 // ---------------------------------------------------------------- the step kernel
 
 template <class T>
-__global__ void __launch_bounds__(32 * 8) step_kernel(const __grid_constant__ s3_model m, const __grid_constant__ s3_data d,
+__global__ void __launch_bounds__(32 * 16) step_kernel(const __grid_constant__ s3_model m, const __grid_constant__ s3_data d,
                                                       const __grid_constant__ s3_layout l, int nsub) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     int lane = threadIdx.x & 31;
@@ -1118,12 +1142,12 @@ __global__ void __launch_bounds__(32 * 8) step_kernel(const __grid_constant__ s3
     for (int sub = 0; sub < nsub; ++sub) {
         kinematics(m, s, lane);
         com_pos(m, s, lane);
+        rne(m, s, lane);
         crb_mass(m, s, lane);
         int np = nv * (nv + 1) / 2;
         for (int t = lane; t < np; t += 32) s.LD[t] = s.M[t];
         __syncwarp();
-        factor_ldl(m, s.LD, lane);
-        rne(m, s, lane);
+        factor_ldl(m, s.LD, s.tk, s.u, lane);
         smooth_force(m, s, gapp, lane);
         if (sub == nsub - 1 && d.qM) {  // parity outputs of the factor before it is overwritten
             T* o = static_cast<T*>(d.qLD) + w * np;
@@ -1180,7 +1204,7 @@ __global__ void __launch_bounds__(32 * 8) step_kernel(const __grid_constant__ s3
                 d.solver_niter[w] = its;
             }
         }
-        factor_ldl(m, s.LD, lane);
+        factor_ldl(m, s.LD, s.tk, s.u, lane);
         solve_ldl(m, s.LD, s.grad, lane);
         for (int i = lane; i < nv; i += 32) s.qvel[i] += dt * s.grad[i];
         __syncwarp();
@@ -1256,12 +1280,12 @@ int s3_plan(const s3_model* m, int32_t warps_per_block, s3_layout* out) {
     int np = nv * (nv + 1) / 2;
     int sizes[O_END] = {};
     sizes[O_XPOS] = 3 * nb; sizes[O_XQUAT] = 4 * nb; sizes[O_XIPOS] = 3 * nb; sizes[O_CINERT] = 10 * nb;
-    sizes[O_CRB] = 10 * nb; sizes[O_CDOF] = 6 * nv; sizes[O_CDOFD] = 6 * nv; sizes[O_CVEL] = 6 * nb;
-    sizes[O_CACC] = 6 * nb; sizes[O_JANC] = 3 * nj; sizes[O_JAX] = 3 * nj; sizes[O_M] = np; sizes[O_LD] = np;
+    sizes[O_CRB] = 2 * S3_MAX_NV; sizes[O_CDOF] = 6 * nv; sizes[O_JANC] = 3 * nj; sizes[O_JAX] = 3 * nj; sizes[O_M] = np; sizes[O_LD] = np;
     sizes[O_QPOS] = nq; sizes[O_QVEL] = nv; sizes[O_SMOOTH] = nv; sizes[O_A0] = nv; sizes[O_A] = nv;
     sizes[O_MA] = nv; sizes[O_GRAD] = nv; sizes[O_P] = nv; sizes[O_MP] = nv; sizes[O_KVD] = nv;
     sizes[O_GPOS] = 3 * ng; sizes[O_GMAT] = 9 * ng; sizes[O_CON] = kConStride * S3_MAX_CON;
-    sizes[O_JC] = 3 * S3_MAX_CON * m->chain_stride; sizes[O_RAREF] = S3_MAX_ROWS; sizes[O_RD] = S3_MAX_ROWS;
+    int jc = 3 * S3_MAX_CON * m->chain_stride, rne = 6 * nv + 12 * nb;
+    sizes[O_JC] = jc > rne ? jc : rne; sizes[O_RAREF] = S3_MAX_ROWS; sizes[O_RD] = S3_MAX_ROWS;
     sizes[O_RJAR] = S3_MAX_ROWS; sizes[O_RJP] = S3_MAX_ROWS; sizes[O_CDOT] = 3 * S3_MAX_CON; sizes[O_BIAS] = nv;
     sizes[O_FCON] = nv; sizes[O_CTRL] = nu; sizes[O_COM] = 4;
     int esz = m->dtype == S3_F64 ? 8 : 4;
@@ -1272,6 +1296,9 @@ int s3_plan(const s3_model* m, int32_t warps_per_block, s3_layout* out) {
         out->off[k] = off;
         off += (sizes[k] + 1) & ~1;  // keep 8-byte alignment for the float build's int region
     }
+    out->off[O_CDOFD] = 6 * nv;  // RNE scratch offsets relative to the Jacobian region
+    out->off[O_CVEL] = 6 * nb;
+    out->off[O_CACC] = 0;
     out->elems_per_world = off;
     int per = off * esz;
     int dev = 0;
@@ -1280,7 +1307,7 @@ int s3_plan(const s3_model* m, int32_t warps_per_block, s3_layout* out) {
     if (cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess || maxsm <= 0)
         maxsm = 227 * 1024;
     int wpb = warps_per_block > 0 ? warps_per_block : maxsm / per;
-    if (wpb > 8) wpb = 8;
+    if (wpb > 16) wpb = 16;
     if (wpb < 1 || wpb * per > maxsm) return fail(S3_ERR_BOUNDS, "one world does not fit in shared memory");
     out->warps_per_block = wpb;
     out->bytes_per_block = wpb * per;

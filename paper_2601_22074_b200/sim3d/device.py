@@ -74,6 +74,21 @@ class DeviceModel:
             pair_chain[p, :len(c)] = c
             pair_chainlen[p] = len(c)
         self.chain_stride = int(max([len(c) for c in m.pair_chain] + [1]))
+        # factorization update lists: for each k, pairs (i in anc(k), j in chain(i))
+        ldl_ptr, ldl_pair = [0], []
+        for k in range(m.nv):
+            for i in m.dof_chain[k][:-1]:
+                for j in m.dof_chain[i]:
+                    ldl_pair.append((i << 8) | j)
+            ldl_ptr.append(len(ldl_pair))
+        classes, pair_class, pair_tree = {}, [], []
+        for p, (g1, g2) in enumerate(m.pair_geom):
+            key = tuple(m.pair_chain[p])
+            pair_class.append(classes.setdefault(key, len(classes)))
+            b1, b2 = int(m.geom_bodyid[g1]), int(m.geom_bodyid[g2])
+            c1, c2 = set(m.body_chain[b1]), set(m.body_chain[b2])
+            pair_tree.append(int(c1 <= c2 or c2 <= c1))
+        tri_tab = np.array([(a << 8) | b for a in range(MAX_CHAIN) for b in range(a + 1)], dtype=np.uint16)
         lim = np.nonzero(m.jnt_limited)[0]
         geom_lmat = np.array([quat2mat(q) for q in m.geom_quat]).reshape(-1, 9)
         body_ilmat = np.array([quat2mat(q) for q in m.body_iquat]).reshape(-1, 9)
@@ -92,7 +107,10 @@ class DeviceModel:
             pair_chain=pair_chain, pair_chainlen=pair_chainlen,
             act_dofadr=np.append(m.actuator_dofadr, 0).astype(np.int32),
             act_qposadr=np.append(m.actuator_qposadr, 0).astype(np.int32),
-            act_kind=np.append(m.actuator_kind, 0).astype(np.int32))
+            act_kind=np.append(m.actuator_kind, 0).astype(np.int32),
+            ldl_ptr=np.array(ldl_ptr, dtype=np.int32), ldl_pair=np.array(ldl_pair + [0], dtype=np.uint16),
+            pair_class=np.array(pair_class + [0], dtype=np.int32), pair_tree=np.array(pair_tree + [1], dtype=np.int32),
+            tri_tab=tri_tab)
         floats = dict(
             body_pos=m.body_pos, body_quat=m.body_quat, body_ipos=m.body_ipos, body_ilmat=body_ilmat,
             body_mass=m.body_mass, body_inertia=m.body_inertia, body_invweight0=m.body_invweight0,
@@ -103,7 +121,7 @@ class DeviceModel:
             hfield=m.hfield_data)
         # one device buffer, 16-byte aligned slices
         chunks, offs, pos = [], {}, 0
-        ints = {k: (v if np.asarray(v).dtype in (np.uint8, np.uint64) else np.asarray(v).astype(np.int32))
+        ints = {k: (v if np.asarray(v).dtype in (np.uint8, np.uint16, np.uint64) else np.asarray(v).astype(np.int32))
                 for k, v in ints.items()}
         fields = {f for f, _ in N.ModelT._fields_}
         missing = {f for f, t in N.ModelT._fields_ if t is ctypes.c_void_p} - set(ints) - set(floats)
