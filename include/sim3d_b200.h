@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define S3_ABI_VERSION 2
+#define S3_ABI_VERSION 3
 #define S3_F64 0
 #define S3_F32 1
 
@@ -32,6 +32,7 @@ extern "C" {
 #define S3_MAX_CON 16
 #define S3_MAX_LIM 32
 #define S3_MAX_ROWS 96
+#define S3_MAX_RAYS 128
 
 #define S3_OK 0
 #define S3_ERR_ARG 1
@@ -176,8 +177,46 @@ typedef struct s3_layout {
     int32_t off[40];
 } s3_layout;
 
+/* Fused velocity-tracking task (paper_2601_22074_b200/sim3d/task.py): configuration + per-world
+ * task state (device pointers, `dtype` elements unless noted). */
+typedef struct s3_task {
+    int32_t decimation;
+    int32_t episode_steps;
+    int32_t cmd_resample_steps;
+    int32_t obs_dim;
+    int32_t nscan;
+    int32_t pad0;
+    uint64_t seed;
+    int64_t world_offset;
+    double action_scale;
+    double action_clip;
+    double track_sigma;
+    double min_height;
+    double max_tilt_cos;
+    double reset_joint_jitter;
+    double spawn_half_extent;
+    double cmd_lo[3];
+    double cmd_hi[3];
+    double reward_weights[6];
+    double noise[7];
+    double scan_xy[256];
+    double scan_offset;
+    double scan_noise;
+    const void* default_qpos;
+    void* action;
+    void* prev_action;
+    void* command;
+    int32_t* cmd_timer;
+    int32_t* episode_step;
+    void* episode_return;
+    void* obs;
+    void* reward;
+    uint8_t* terminated;
+    uint8_t* truncated;
+} s3_task;
+
 int s3_abi_version(void);
-size_t s3_sizeof(int which); /* 0 model, 1 data, 2 layout */
+size_t s3_sizeof(int which); /* 0 model, 1 data, 2 layout, 3 task */
 const char* s3_last_error(void);
 
 /* Fill the shared-memory layout for this model; warps_per_block = 0 picks the largest
@@ -189,6 +228,13 @@ int s3_plan(const s3_model* m, int32_t warps_per_block, s3_layout* out);
  * Replaces, for the 3-D path, StepPipeline.substep x decimation (sim/physics.py:239-249,
  * env.py:228-233 of the reference; mjwarp.step in mjlab). */
 int s3_step(const s3_model* m, const s3_data* d, const s3_layout* l, int32_t nsub, void* stream);
+
+/* One control step of the fused velocity task (mode 0): ActionManager.process -> decimation x
+ * substep -> terminations -> rewards -> masked reset + command resample -> command countdown ->
+ * observations, every world in ONE launch (env.py:219-259 of the reference, on the 3-D model).
+ * mode 1 resets every world (counter 0 draws) and writes the first observation; actions unused. */
+int s3_env_step(const s3_model* m, const s3_data* d, const s3_layout* l, const s3_task* t, const void* actions,
+                int32_t mode, int64_t global_step, void* stream);
 
 #ifdef __cplusplus
 }

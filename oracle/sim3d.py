@@ -648,3 +648,179 @@ def set_const(m, qpos0=None):
     jac = [np.zeros((3, m.nv))] + [point_jac(m, C, b, K["xipos"][b]) for b in range(1, m.nbody)]
     m.set_const(M, jac)
     return M
+
+
+# ----------------------------------------------------------------------------- velocity task (3-D)
+# The fused task stage of paper_2601_22074_b200/sim3d/task.py restated: the reference's manager
+# pipeline (env.py:219-259: action -> decimation x substep -> termination -> reward -> masked reset ->
+# command -> observation) on the 3-D model, with mjlab's velocity-tracking terms.
+
+U64 = np.uint64
+GOLDEN = U64(0x9E3779B97F4A7C15)
+SALT = U64(0xD1B54A32D192ED03)
+
+
+def mix64(z):
+    with np.errstate(over="ignore"):
+        z = U64(z)
+        z = (z ^ (z >> U64(30))) * U64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> U64(27))) * U64(0x94D049BB133111EB)
+        return z ^ (z >> U64(31))
+
+
+def stream_key(seed, world, purpose):
+    with np.errstate(over="ignore"):
+        return mix64(mix64(U64(seed) * GOLDEN) ^ (U64(world + 1) * SALT) ^ mix64(U64(purpose)))
+
+
+def uniform(key, ctr):
+    """U[0,1) from word mix(key + ctr * GOLDEN) (the rng.py:97-105 construction)."""
+    with np.errstate(over="ignore"):
+        w = mix64(U64(key) + U64(ctr) * GOLDEN)
+    return float(w >> U64(11)) * (1.0 / 9007199254740992.0)
+
+
+def terrain_height(m, x, y):
+    if not m.terrain_is_hfield:
+        return 0.0
+    h = hfield_point(m, np.array([x, y, 0.0]), 0.0)
+    if h is None:
+        return 0.0
+    d, n = h
+    return -d / n[2]
+
+
+def base_frame(m, qpos, qvel):
+    R = qmat(qnormalize(qpos[3:7]))
+    return R.T @ qvel[0:3], qvel[3:6].copy(), R.T @ np.array([0.0, 0.0, -1.0]), R
+
+
+class TaskOracle:
+    """Per-world numpy restatement of the fused 3-D velocity task (one control step = decimation substeps)."""
+
+    def __init__(self, m, cfg, nworld, seed=0, world_offset=0):
+        self.m, self.cfg, self.n, self.seed, self.off = m, cfg, nworld, seed, world_offset
+        self.default = cfg.default_qpos.copy()
+        act = m.actuator_qposadr
+        self.qpos = np.tile(self.default, (nworld, 1))
+        self.qvel = np.zeros((nworld, m.nv))
+        self.warm = np.zeros((nworld, m.nv))
+        self.action = np.zeros((nworld, m.nu))
+        self.prev_action = np.zeros((nworld, m.nu))
+        self.cmd = np.zeros((nworld, 3))
+        self.cmd_timer = np.zeros(nworld, dtype=np.int64)
+        self.episode_step = np.zeros(nworld, dtype=np.int64)
+        self.ep_return = np.zeros(nworld)
+        self.global_step = 0
+        self.act_default = self.default[act]
+
+    def key(self, w, purpose):
+        return stream_key(self.seed, self.off + w, purpose)
+
+    def reset_world(self, w, ctr):
+        m, cfg = self.m, self.cfg
+        kr = self.key(w, 1)
+        q = self.default.copy()
+        hinge = m.jnt_qposadr[m.jnt_type == 3]
+        for i, a in enumerate(hinge):
+            q[a] += cfg.reset_joint_jitter * (2.0 * uniform(kr, ctr * 256 + i) - 1.0)
+        q[0] = cfg.spawn_half_extent * (2.0 * uniform(kr, ctr * 256 + 200) - 1.0)
+        q[1] = cfg.spawn_half_extent * (2.0 * uniform(kr, ctr * 256 + 201) - 1.0)
+        yaw = np.pi * (2.0 * uniform(kr, ctr * 256 + 202) - 1.0)
+        q[2] = self.default[2] + terrain_height(m, q[0], q[1])
+        q[3:7] = (np.cos(0.5 * yaw), 0.0, 0.0, np.sin(0.5 * yaw))
+        self.qpos[w] = q
+        self.qvel[w] = 0.0
+        self.warm[w] = 0.0
+        self.action[w] = 0.0
+        self.prev_action[w] = 0.0
+        self.episode_step[w] = 0
+        self.ep_return[w] = 0.0
+        self.resample(w, ctr)
+
+    def resample(self, w, ctr):
+        kc = self.key(w, 2)
+        for i, (lo, hi) in enumerate(self.cfg.command_ranges):
+            self.cmd[w, i] = lo + (hi - lo) * uniform(kc, ctr * 4 + i)
+        self.cmd_timer[w] = self.cfg.command_resample_steps
+
+    def reset(self):
+        for w in range(self.n):
+            self.reset_world(w, 0)
+        return self.observe(0)
+
+    def observe(self, ctr):
+        m, cfg = self.m, self.cfg
+        act = m.actuator_qposadr
+        dofs = m.actuator_dofadr
+        out = np.zeros((self.n, cfg.obs_dim(m)))
+        for w in range(self.n):
+            v, om, g, R = base_frame(m, self.qpos[w], self.qvel[w])
+            parts = [v, om, g, self.cmd[w], self.qpos[w][act] - self.act_default, self.qvel[w][dofs], self.action[w]]
+            o = np.concatenate(parts)
+            if cfg.height_scan:
+                o = np.concatenate([o, self.height_scan(w)])
+            ko = self.key(w, 3)
+            scales = cfg.noise_vector(m)
+            for i in range(o.size):
+                if scales[i] > 0.0:
+                    o[i] += scales[i] * (2.0 * uniform(ko, ctr * 1024 + i) - 1.0)
+            out[w] = o
+        return out
+
+    def height_scan(self, w):
+        m, cfg = self.m, self.cfg
+        q = self.qpos[w]
+        quat = qnormalize(q[3:7])
+        yaw = np.arctan2(2.0 * (quat[0] * quat[3] + quat[1] * quat[2]), 1.0 - 2.0 * (quat[2] ** 2 + quat[3] ** 2))
+        c, s = np.cos(yaw), np.sin(yaw)
+        out = []
+        for (ox, oy) in cfg.scan_points():
+            x = q[0] + c * ox - s * oy
+            y = q[1] + s * ox + c * oy
+            h = q[2] - terrain_height(m, x, y) - cfg.scan_offset
+            out.append(min(max(h, -1.0), 1.0))
+        return np.array(out)
+
+    def step(self, actions):
+        """One control step of every world; returns (obs, reward, terminated, truncated)."""
+        m, cfg = self.m, self.cfg
+        self.global_step += 1
+        ctr = self.global_step
+        dtc = m.opt.timestep * cfg.decimation
+        rew = np.zeros(self.n)
+        term = np.zeros(self.n, dtype=bool)
+        trunc = np.zeros(self.n, dtype=bool)
+        act = m.actuator_qposadr
+        for w in range(self.n):
+            a = np.clip(actions[w], -cfg.action_clip, cfg.action_clip)
+            self.prev_action[w] = self.action[w]
+            self.action[w] = a
+            ctrl = self.act_default + cfg.action_scale * a
+            q, v, warm = self.qpos[w], self.qvel[w], self.warm[w]
+            for _ in range(cfg.decimation):
+                q, v, warm, _ = step(m, q, v, ctrl, warm=warm)
+            self.qpos[w], self.qvel[w], self.warm[w] = q, v, warm
+            vb, om, g, _ = base_frame(m, q, v)
+            e_xy = (self.cmd[w, 0] - vb[0]) ** 2 + (self.cmd[w, 1] - vb[1]) ** 2
+            terms = (np.exp(-e_xy / cfg.track_sigma), np.exp(-((self.cmd[w, 2] - om[2]) ** 2) / cfg.track_sigma),
+                     vb[2] * vb[2], om[0] * om[0] + om[1] * om[1],
+                     float(np.sum((self.action[w] - self.prev_action[w]) ** 2)), g[0] * g[0] + g[1] * g[1])
+            r = 0.0
+            for wt, t in zip(cfg.reward_weights, terms):
+                r += wt * t * dtc
+            rew[w] = r
+            self.ep_return[w] += r
+            h = q[2] - terrain_height(m, q[0], q[1])
+            nonfinite = not (np.all(np.isfinite(q)) and np.all(np.isfinite(v)))
+            term[w] = bool(h < cfg.min_height or g[2] > cfg.max_tilt_cos or nonfinite)
+            self.episode_step[w] += 1
+            trunc[w] = bool(self.episode_step[w] >= cfg.episode_steps)
+        for w in range(self.n):
+            if term[w] or trunc[w]:
+                self.reset_world(w, ctr)
+            else:
+                self.cmd_timer[w] -= 1
+                if self.cmd_timer[w] <= 0:
+                    self.resample(w, ctr)
+        return self.observe(ctr), rew, term, trunc

@@ -311,7 +311,11 @@ template <class T> __device__ void com_pos(const s3_model& m, WS<T>& s, int lane
             r[0] = ax[0]; r[1] = ax[1]; r[2] = ax[2]; r[3] = lin[0]; r[4] = lin[1]; r[5] = lin[2];
         }
     }
-    // geom frames
+    __syncwarp();
+}
+
+// geom frames from the body frames
+template <class T> __device__ void geom_frames(const s3_model& m, WS<T>& s, int lane) {
     const T* gp = F<T>(m.geom_pos);
     const T* gl = F<T>(m.geom_lmat);
     for (int g = lane; g < m.ngeom; g += 32) {
@@ -1116,6 +1120,119 @@ template <class T> __device__ int newton(const s3_model& m, WS<T>& s, int ncon, 
     return its;
 }
 
+// ---------------------------------------------------------------- one physics substep (mj_step)
+
+template <class T>
+__device__ void substep(const s3_model& m, const s3_data& d, WS<T>& s, int64_t w, T* gw, const T* gapp, bool last,
+                        int lane) {
+    const int nv = m.nv;
+    const T dt = T(m.timestep);
+    int ncon = 0, nlim = 0, dropped = 0, its = 0;
+    kinematics(m, s, lane);
+    com_pos(m, s, lane);
+    geom_frames(m, s, lane);
+    rne(m, s, lane);
+    crb_mass(m, s, lane);
+    int np = nv * (nv + 1) / 2;
+    for (int t = lane; t < np; t += 32) s.LD[t] = s.M[t];
+    __syncwarp();
+    factor_ldl(m, s.LD, s.tk, s.u, lane);
+    smooth_force(m, s, gapp, lane);
+    if (last && d.qM) {  // parity outputs of the factor before it is overwritten
+        T* o = static_cast<T*>(d.qLD) + w * np;
+        for (int t = lane; t < np; t += 32) o[t] = s.LD[t];
+    }
+    solve_ldl(m, s.LD, s.a0, lane);
+    ncon = collide(m, s, lane, dropped);
+    build_rows(m, s, ncon, nlim, lane);
+    if (gw) {
+        for (int i = lane; i < nv; i += 32) s.p[i] = gw[i];
+        __syncwarp();
+    }
+    its = newton(m, s, ncon, nlim, gw != nullptr, lane);
+    if (gw) {
+        for (int i = lane; i < nv; i += 32) gw[i] = s.a[i];
+    }
+    // implicitfast: (M + dt diag(damping + kv)) acc = smooth + constraint
+    const T* damp = F<T>(m.dof_damping);
+    for (int t = lane; t < np; t += 32) s.LD[t] = s.M[t];
+    __syncwarp();
+    for (int i = lane; i < nv; i += 32) s.LD[tri(i, i)] += dt * (damp[i] + s.kvd[i]);
+    for (int i = lane; i < nv; i += 32) s.grad[i] = s.smooth[i] + s.fcon[i];
+    __syncwarp();
+    if (last && d.qM) {  // parity outputs (pre-integration quantities)
+        T* oM = static_cast<T*>(d.qM) + w * np;
+        for (int t = lane; t < np; t += 32) oM[t] = s.M[t];
+        for (int i = lane; i < nv; i += 32) {
+            static_cast<T*>(d.qfrc_bias)[w * nv + i] = s.bias[i];
+            static_cast<T*>(d.qfrc_smooth)[w * nv + i] = s.smooth[i];
+            static_cast<T*>(d.qacc_smooth)[w * nv + i] = s.a0[i];
+            static_cast<T*>(d.qacc)[w * nv + i] = s.a[i];
+            static_cast<T*>(d.qfrc_constraint)[w * nv + i] = s.fcon[i];
+            for (int k = 0; k < 6; ++k) static_cast<T*>(d.cdof)[(w * nv + i) * 6 + k] = s.cdof[6 * i + k];
+        }
+        for (int b = lane; b < m.nbody; b += 32) {
+            for (int k = 0; k < 3; ++k) static_cast<T*>(d.xpos)[(w * m.nbody + b) * 3 + k] = s.xpos[3 * b + k];
+            for (int k = 0; k < 4; ++k) static_cast<T*>(d.xquat)[(w * m.nbody + b) * 4 + k] = s.xquat[4 * b + k];
+        }
+        if (lane < 3) static_cast<T*>(d.com)[w * 3 + lane] = s.com[lane];
+        for (int c = lane; c < ncon; c += 32) {
+            const T* cc = s.con + kConStride * c;
+            static_cast<T*>(d.con_dist)[w * S3_MAX_CON + c] = cc[0];
+            for (int k = 0; k < 3; ++k) static_cast<T*>(d.con_pos)[(w * S3_MAX_CON + c) * 3 + k] = cc[1 + k];
+            for (int k = 0; k < 9; ++k) static_cast<T*>(d.con_frame)[(w * S3_MAX_CON + c) * 9 + k] = cc[4 + k];
+            d.con_pair[w * S3_MAX_CON + c] = s.con_pair[c];
+        }
+        for (int r = lane; r < nlim + 4 * ncon; r += 32) static_cast<T*>(d.efc_force)[w * S3_MAX_ROWS + r] = s.rJp[r];
+        if (lane == 0) {
+            d.ncon[w] = ncon;
+            d.ndropped[w] = dropped;
+            d.nefc[w] = nlim + 4 * ncon;
+            d.solver_niter[w] = its;
+        }
+    }
+    factor_ldl(m, s.LD, s.tk, s.u, lane);
+    solve_ldl(m, s.LD, s.grad, lane);
+    for (int i = lane; i < nv; i += 32) s.qvel[i] += dt * s.grad[i];
+    __syncwarp();
+    // integrate positions (oracle integrate_pos)
+    for (int j = lane; j < m.njnt; j += 32) {
+        int a = m.jnt_qposadr[j], dd = m.jnt_dofadr[j];
+        if (m.jnt_type[j] == kJntFree) {
+            for (int k = 0; k < 3; ++k) s.qpos[a + k] = s.qpos[a + k] + dt * s.qvel[dd + k];
+            T wv[3] = {s.qvel[dd + 3], s.qvel[dd + 4], s.qvel[dd + 5]};
+            T nw = sqrt(dot3(wv, wv));
+            T qt[4] = {s.qpos[a + 3], s.qpos[a + 4], s.qpos[a + 5], s.qpos[a + 6]};
+            if (nw > T(1e-15)) {
+                T sn, cs;
+                sincos_t(T(0.5) * (nw * dt), &sn, &cs);
+                T inv = T(1) / nw;
+                T qa[4] = {cs, wv[0] * inv * sn, wv[1] * inv * sn, wv[2] * inv * sn};
+                T r[4];
+                qmul(qt, qa, r);
+                qt[0] = r[0]; qt[1] = r[1]; qt[2] = r[2]; qt[3] = r[3];
+            }
+            qnormalize(qt);
+            for (int k = 0; k < 4; ++k) s.qpos[a + 3 + k] = qt[k];
+        } else {
+            s.qpos[a] = s.qpos[a] + dt * s.qvel[dd];
+        }
+    }
+    __syncwarp();
+    if (d.time && lane == 0) static_cast<T*>(d.time)[w] += dt;
+}
+
+template <class T> __device__ void store_geom_frames(const s3_model& m, const s3_data& d, WS<T>& s, int64_t w,
+                                                     int lane) {
+    // frames at the FINAL state of the launch (what sensors see)
+    kinematics(m, s, lane);
+    geom_frames(m, s, lane);
+    for (int g = lane; g < m.ngeom; g += 32) {
+        for (int k = 0; k < 3; ++k) static_cast<T*>(d.geom_xpos)[(w * m.ngeom + g) * 3 + k] = s.gpos[3 * g + k];
+        for (int k = 0; k < 9; ++k) static_cast<T*>(d.geom_xmat)[(w * m.ngeom + g) * 9 + k] = s.gmat[9 * g + k];
+    }
+}
+
 // ---------------------------------------------------------------- the step kernel
 
 template <class T>
@@ -1137,109 +1254,231 @@ __global__ void __launch_bounds__(32 * 16) step_kernel(const __grid_constant__ s
     for (int i = lane; i < nv; i += 32) s.qvel[i] = gv[i];
     for (int i = lane; i < nu; i += 32) s.ctrl[i] = static_cast<const T*>(d.ctrl)[w * nu + i];
     __syncwarp();
-    T dt = T(m.timestep);
-    int ncon = 0, nlim = 0, dropped = 0, its = 0;
-    for (int sub = 0; sub < nsub; ++sub) {
-        kinematics(m, s, lane);
-        com_pos(m, s, lane);
-        rne(m, s, lane);
-        crb_mass(m, s, lane);
-        int np = nv * (nv + 1) / 2;
-        for (int t = lane; t < np; t += 32) s.LD[t] = s.M[t];
-        __syncwarp();
-        factor_ldl(m, s.LD, s.tk, s.u, lane);
-        smooth_force(m, s, gapp, lane);
-        if (sub == nsub - 1 && d.qM) {  // parity outputs of the factor before it is overwritten
-            T* o = static_cast<T*>(d.qLD) + w * np;
-            for (int t = lane; t < np; t += 32) o[t] = s.LD[t];
-        }
-        solve_ldl(m, s.LD, s.a0, lane);
-        ncon = collide(m, s, lane, dropped);
-        int nefc = build_rows(m, s, ncon, nlim, lane);
-        (void)nefc;
-        if (gw) {
-            for (int i = lane; i < nv; i += 32) s.p[i] = gw[i];
-            __syncwarp();
-        }
-        its = newton(m, s, ncon, nlim, gw != nullptr, lane);
-        if (gw) {
-            for (int i = lane; i < nv; i += 32) gw[i] = s.a[i];
-        }
-        // implicitfast: (M + dt diag(damping + kv)) acc = smooth + constraint
-        const T* damp = F<T>(m.dof_damping);
-        for (int t = lane; t < np; t += 32) s.LD[t] = s.M[t];
-        __syncwarp();
-        for (int i = lane; i < nv; i += 32) s.LD[tri(i, i)] += dt * (damp[i] + s.kvd[i]);
-        for (int i = lane; i < nv; i += 32) s.grad[i] = s.smooth[i] + s.fcon[i];
-        __syncwarp();
-        if (sub == nsub - 1 && d.qM) {  // parity outputs (pre-integration quantities)
-            T* oM = static_cast<T*>(d.qM) + w * np;
-            for (int t = lane; t < np; t += 32) oM[t] = s.M[t];
-            for (int i = lane; i < nv; i += 32) {
-                static_cast<T*>(d.qfrc_bias)[w * nv + i] = s.bias[i];
-                static_cast<T*>(d.qfrc_smooth)[w * nv + i] = s.smooth[i];
-                static_cast<T*>(d.qacc_smooth)[w * nv + i] = s.a0[i];
-                static_cast<T*>(d.qacc)[w * nv + i] = s.a[i];
-                static_cast<T*>(d.qfrc_constraint)[w * nv + i] = s.fcon[i];
-                for (int k = 0; k < 6; ++k) static_cast<T*>(d.cdof)[(w * nv + i) * 6 + k] = s.cdof[6 * i + k];
-            }
-            for (int b = lane; b < m.nbody; b += 32) {
-                for (int k = 0; k < 3; ++k) static_cast<T*>(d.xpos)[(w * m.nbody + b) * 3 + k] = s.xpos[3 * b + k];
-                for (int k = 0; k < 4; ++k) static_cast<T*>(d.xquat)[(w * m.nbody + b) * 4 + k] = s.xquat[4 * b + k];
-            }
-            if (lane < 3) static_cast<T*>(d.com)[w * 3 + lane] = s.com[lane];
-            for (int c = lane; c < ncon; c += 32) {
-                const T* cc = s.con + kConStride * c;
-                static_cast<T*>(d.con_dist)[w * S3_MAX_CON + c] = cc[0];
-                for (int k = 0; k < 3; ++k) static_cast<T*>(d.con_pos)[(w * S3_MAX_CON + c) * 3 + k] = cc[1 + k];
-                for (int k = 0; k < 9; ++k) static_cast<T*>(d.con_frame)[(w * S3_MAX_CON + c) * 9 + k] = cc[4 + k];
-                d.con_pair[w * S3_MAX_CON + c] = s.con_pair[c];
-            }
-            for (int r = lane; r < nlim + 4 * ncon; r += 32)
-                static_cast<T*>(d.efc_force)[w * S3_MAX_ROWS + r] = s.rJp[r];
-            if (lane == 0) {
-                d.ncon[w] = ncon;
-                d.ndropped[w] = dropped;
-                d.nefc[w] = nlim + 4 * ncon;
-                d.solver_niter[w] = its;
-            }
-        }
-        factor_ldl(m, s.LD, s.tk, s.u, lane);
-        solve_ldl(m, s.LD, s.grad, lane);
-        for (int i = lane; i < nv; i += 32) s.qvel[i] += dt * s.grad[i];
-        __syncwarp();
-        // integrate positions (oracle integrate_pos)
-        for (int j = lane; j < m.njnt; j += 32) {
-            int a = m.jnt_qposadr[j], dd = m.jnt_dofadr[j];
-            if (m.jnt_type[j] == kJntFree) {
-                for (int k = 0; k < 3; ++k) s.qpos[a + k] = s.qpos[a + k] + dt * s.qvel[dd + k];
-                T wv[3] = {s.qvel[dd + 3], s.qvel[dd + 4], s.qvel[dd + 5]};
-                T nw = sqrt(dot3(wv, wv));
-                T qt[4] = {s.qpos[a + 3], s.qpos[a + 4], s.qpos[a + 5], s.qpos[a + 6]};
-                if (nw > T(1e-15)) {
-                    T sn, cs;
-                    sincos_t(T(0.5) * (nw * dt), &sn, &cs);
-                    T inv = T(1) / nw;
-                    T qa[4] = {cs, wv[0] * inv * sn, wv[1] * inv * sn, wv[2] * inv * sn};
-                    T r[4];
-                    qmul(qt, qa, r);
-                    qt[0] = r[0]; qt[1] = r[1]; qt[2] = r[2]; qt[3] = r[3];
-                }
-                qnormalize(qt);
-                for (int k = 0; k < 4; ++k) s.qpos[a + 3 + k] = qt[k];
-            } else {
-                s.qpos[a] = s.qpos[a] + dt * s.qvel[dd];
-            }
-        }
-        __syncwarp();
-        if (d.time && lane == 0) static_cast<T*>(d.time)[w] += dt;
+    for (int sub = 0; sub < nsub; ++sub) substep(m, d, s, w, gw, gapp, sub == nsub - 1, lane);
+    if (d.geom_xpos) store_geom_frames(m, d, s, w, lane);
+    for (int i = lane; i < nq; i += 32) gq[i] = s.qpos[i];
+    for (int i = lane; i < nv; i += 32) gv[i] = s.qvel[i];
+}
+
+// ---------------------------------------------------------------- the fused velocity task (task.py)
+
+__device__ inline uint64_t mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ull;
+constexpr uint64_t kSalt = 0xD1B54A32D192ED03ull;
+
+__device__ inline uint64_t stream_key(uint64_t seed, int64_t world, uint64_t purpose) {
+    return mix64(mix64(seed * kGolden) ^ ((uint64_t)(world + 1) * kSalt) ^ mix64(purpose));
+}
+
+template <class T> __device__ inline T uniform01(uint64_t key, uint64_t ctr) {
+    uint64_t wd = mix64(key + ctr * kGolden);
+    return T((double)(wd >> 11) * (1.0 / 9007199254740992.0));
+}
+
+template <class T> __device__ inline T terrain_height(const s3_model& m, T x, T y) {
+    if (!m.terrain_hfield) return T(0);
+    T q[3] = {x, y, T(0)}, dd, n[3];
+    if (!hfield_point(m, q, T(0), dd, n)) return T(0);
+    return -dd / n[2];
+}
+
+// base-frame linear velocity, angular velocity, projected gravity from the free joint
+template <class T> __device__ inline void base_frame(const T* qpos, const T* qvel, T* vb, T* om, T* g) {
+    T q[4] = {qpos[3], qpos[4], qpos[5], qpos[6]};
+    qnormalize(q);
+    T R[9];
+    qmat(q, R);
+    for (int k = 0; k < 3; ++k) {
+        vb[k] = R[k] * qvel[0] + R[3 + k] * qvel[1] + R[6 + k] * qvel[2];
+        om[k] = qvel[3 + k];
+        g[k] = -R[6 + k];
     }
-    if (d.geom_xpos) {  // frames of the last substep's kinematics (sensors)
-        for (int g = lane; g < m.ngeom; g += 32) {
-            for (int k = 0; k < 3; ++k) static_cast<T*>(d.geom_xpos)[(w * m.ngeom + g) * 3 + k] = s.gpos[3 * g + k];
-            for (int k = 0; k < 9; ++k) static_cast<T*>(d.geom_xmat)[(w * m.ngeom + g) * 9 + k] = s.gmat[9 * g + k];
-        }
+}
+
+template <class T>
+__device__ void task_reset(const s3_model& m, const s3_task& tk, WS<T>& s, int64_t w, uint64_t ctr, int lane) {
+    const T* dq = static_cast<const T*>(tk.default_qpos);
+    uint64_t kr = stream_key(tk.seed, tk.world_offset + w, 1);
+    for (int i = lane; i < m.nq; i += 32) s.qpos[i] = dq[i];
+    __syncwarp();
+    for (int j = lane; j < m.njnt; j += 32) {
+        if (m.jnt_type[j] == kJntFree) continue;
+        // hinge index among hinge joints (joint order; the free joint, if any, comes first)
+        int hi = j - (m.jnt_type[0] == kJntFree ? 1 : 0);
+        int a = m.jnt_qposadr[j];
+        s.qpos[a] = dq[a] + T(tk.reset_joint_jitter) * (T(2) * uniform01<T>(kr, ctr * 256 + hi) - T(1));
     }
+    if (lane == 0) {
+        T x = T(tk.spawn_half_extent) * (T(2) * uniform01<T>(kr, ctr * 256 + 200) - T(1));
+        T y = T(tk.spawn_half_extent) * (T(2) * uniform01<T>(kr, ctr * 256 + 201) - T(1));
+        T yaw = T(3.141592653589793) * (T(2) * uniform01<T>(kr, ctr * 256 + 202) - T(1));
+        s.qpos[0] = x;
+        s.qpos[1] = y;
+        s.qpos[2] = dq[2] + terrain_height(m, x, y);
+        T sn, cs;
+        sincos_t(T(0.5) * yaw, &sn, &cs);
+        s.qpos[3] = cs; s.qpos[4] = T(0); s.qpos[5] = T(0); s.qpos[6] = sn;
+    }
+    for (int i = lane; i < m.nv; i += 32) s.qvel[i] = T(0);
+    __syncwarp();
+}
+
+template <class T>
+__device__ void task_resample(const s3_task& tk, T* cmd, int64_t w, uint64_t ctr, int lane) {
+    uint64_t kc = stream_key(tk.seed, tk.world_offset + w, 2);
+    if (lane < 3) cmd[lane] = T(tk.cmd_lo[lane]) + T(tk.cmd_hi[lane] - tk.cmd_lo[lane]) * uniform01<T>(kc, ctr * 4 + lane);
+}
+
+template <class T>
+__device__ void task_observe(const s3_model& m, const s3_task& tk, WS<T>& s, int64_t w, uint64_t ctr, const T* cmd,
+                             const T* action, int lane) {
+    T vb[3], om[3], g[3];
+    base_frame(s.qpos, s.qvel, vb, om, g);
+    const T* dq = static_cast<const T*>(tk.default_qpos);
+    uint64_t ko = stream_key(tk.seed, tk.world_offset + w, 3);
+    T* out = static_cast<T*>(tk.obs) + w * tk.obs_dim;
+    int nu = m.nu;
+    T yaw = T(0), cy = T(1), sy = T(0);
+    if (tk.nscan) {
+        T q[4] = {s.qpos[3], s.qpos[4], s.qpos[5], s.qpos[6]};
+        qnormalize(q);
+        yaw = atan2(T(2) * (q[0] * q[3] + q[1] * q[2]), T(1) - T(2) * (q[2] * q[2] + q[3] * q[3]));
+        sincos_t(yaw, &sy, &cy);
+    }
+    for (int i = lane; i < tk.obs_dim; i += 32) {
+        T v, ns;
+        if (i < 12) {
+            int g3 = i / 3, k = i % 3;
+            v = g3 == 0 ? vb[k] : (g3 == 1 ? om[k] : (g3 == 2 ? g[k] : cmd[k]));
+            ns = T(tk.noise[g3]);
+        } else if (i < 12 + nu) {
+            int a = m.act_qposadr[i - 12];
+            v = s.qpos[a] - dq[a];
+            ns = T(tk.noise[4]);
+        } else if (i < 12 + 2 * nu) {
+            v = s.qvel[m.act_dofadr[i - 12 - nu]];
+            ns = T(tk.noise[5]);
+        } else if (i < 12 + 3 * nu) {
+            v = action[i - 12 - 2 * nu];
+            ns = T(tk.noise[6]);
+        } else {
+            int r = i - 12 - 3 * nu;
+            T ox = T(tk.scan_xy[2 * r]), oy = T(tk.scan_xy[2 * r + 1]);
+            T x = s.qpos[0] + cy * ox - sy * oy;
+            T y = s.qpos[1] + sy * ox + cy * oy;
+            T h = s.qpos[2] - terrain_height(m, x, y) - T(tk.scan_offset);
+            v = fmin(fmax(h, T(-1)), T(1));
+            ns = T(tk.scan_noise);
+        }
+        if (ns > T(0)) v += ns * (T(2) * uniform01<T>(ko, ctr * 1024 + i) - T(1));
+        out[i] = v;
+    }
+}
+
+template <class T>
+__global__ void __launch_bounds__(32 * 16) env_kernel(const __grid_constant__ s3_model m, const __grid_constant__ s3_data d,
+                                                     const __grid_constant__ s3_layout l,
+                                                     const __grid_constant__ s3_task tk, const T* __restrict__ actions,
+                                                     int mode, int64_t global_step) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    int lane = threadIdx.x & 31;
+    int wib = threadIdx.x >> 5;
+    int64_t w = (int64_t)blockIdx.x * l.warps_per_block + wib;
+    if (w >= d.nworld) return;
+    T* base = reinterpret_cast<T*>(smem_raw) + (size_t)wib * l.elems_per_world;
+    WS<T> s = make_ws(base, l);
+    const int nq = m.nq, nv = m.nv, nu = m.nu;
+    T* gq = static_cast<T*>(d.qpos) + w * nq;
+    T* gv = static_cast<T*>(d.qvel) + w * nv;
+    T* gw = static_cast<T*>(d.qacc_warmstart) + w * nv;
+    T* act = static_cast<T*>(tk.action) + w * nu;
+    T* prev = static_cast<T*>(tk.prev_action) + w * nu;
+    T* cmd = static_cast<T*>(tk.command) + w * 3;
+    const T* dq = static_cast<const T*>(tk.default_qpos);
+    uint64_t ctr = (uint64_t)global_step;
+    if (mode == 1) {  // reset every world, counter 0
+        task_reset(m, tk, s, w, 0, lane);
+        for (int i = lane; i < nv; i += 32) gw[i] = T(0);
+        for (int i = lane; i < nu; i += 32) { act[i] = T(0); prev[i] = T(0); }
+        task_resample(tk, cmd, w, 0, lane);
+        if (lane == 0) {
+            tk.cmd_timer[w] = tk.cmd_resample_steps;
+            tk.episode_step[w] = 0;
+            static_cast<T*>(tk.episode_return)[w] = T(0);
+        }
+        __syncwarp();
+        task_observe(m, tk, s, w, 0, cmd, act, lane);
+        for (int i = lane; i < nq; i += 32) gq[i] = s.qpos[i];
+        for (int i = lane; i < nv; i += 32) gv[i] = s.qvel[i];
+        return;
+    }
+    for (int i = lane; i < nq; i += 32) s.qpos[i] = gq[i];
+    for (int i = lane; i < nv; i += 32) s.qvel[i] = gv[i];
+    // ActionManager.process: clip, remember the previous action, position targets
+    T rate = T(0);
+    for (int i = lane; i < nu; i += 32) {
+        T a = fmin(fmax(actions[w * nu + i], T(-tk.action_clip)), T(tk.action_clip));
+        T p = act[i];
+        prev[i] = p;
+        act[i] = a;
+        rate += (a - p) * (a - p);
+        s.ctrl[i] = dq[m.act_qposadr[i]] + T(tk.action_scale) * a;
+    }
+    rate = wsum(rate);
+    __syncwarp();
+    for (int sub = 0; sub < tk.decimation; ++sub) substep(m, d, s, w, gw, (const T*)nullptr, false, lane);
+    // rewards, terminations (pre-reset state)
+    T vb[3], om[3], g[3];
+    base_frame(s.qpos, s.qvel, vb, om, g);
+    T c0 = cmd[0], c1 = cmd[1], c2 = cmd[2];
+    T dtc = T(m.timestep) * T(tk.decimation);
+    T e_xy = (c0 - vb[0]) * (c0 - vb[0]) + (c1 - vb[1]) * (c1 - vb[1]);
+    T sig = T(tk.track_sigma);
+    T terms[6] = {exp(-e_xy / sig), exp(-((c2 - om[2]) * (c2 - om[2])) / sig), vb[2] * vb[2],
+                  om[0] * om[0] + om[1] * om[1], rate, g[0] * g[0] + g[1] * g[1]};
+    T r = T(0);
+    for (int k = 0; k < 6; ++k) r += T(tk.reward_weights[k]) * terms[k] * dtc;
+    bool finite = true;
+    for (int i = lane; i < nq; i += 32) finite = finite && isfinite(s.qpos[i]);
+    for (int i = lane; i < nv; i += 32) finite = finite && isfinite(s.qvel[i]);
+    finite = __all_sync(FULL, finite);
+    T h = s.qpos[2] - terrain_height(m, s.qpos[0], s.qpos[1]);
+    bool term = h < T(tk.min_height) || g[2] > T(tk.max_tilt_cos) || !finite;
+    int es = tk.episode_step[w] + 1;
+    bool trunc = es >= tk.episode_steps;
+    __syncwarp();
+    if (lane == 0) {
+        static_cast<T*>(tk.reward)[w] = r;
+        static_cast<T*>(tk.episode_return)[w] += r;
+        tk.terminated[w] = term;
+        tk.truncated[w] = trunc;
+        tk.episode_step[w] = es;
+    }
+    if (term || trunc) {  // masked reset (warp-uniform)
+        task_reset(m, tk, s, w, ctr, lane);
+        for (int i = lane; i < nv; i += 32) gw[i] = T(0);
+        for (int i = lane; i < nu; i += 32) { act[i] = T(0); prev[i] = T(0); }
+        task_resample(tk, cmd, w, ctr, lane);
+        if (lane == 0) {
+            tk.cmd_timer[w] = tk.cmd_resample_steps;
+            tk.episode_step[w] = 0;
+            static_cast<T*>(tk.episode_return)[w] = T(0);
+        }
+    } else {
+        int tm = tk.cmd_timer[w] - 1;
+        if (tm <= 0) {
+            task_resample(tk, cmd, w, ctr, lane);
+            tm = tk.cmd_resample_steps;
+        }
+        __syncwarp();
+        if (lane == 0) tk.cmd_timer[w] = tm;
+    }
+    __syncwarp();
+    task_observe(m, tk, s, w, ctr, cmd, act, lane);
     for (int i = lane; i < nq; i += 32) gq[i] = s.qpos[i];
     for (int i = lane; i < nv; i += 32) gv[i] = s.qvel[i];
 }
@@ -1265,6 +1504,7 @@ size_t s3_sizeof(int which) {
         case 0: return sizeof(s3_model);
         case 1: return sizeof(s3_data);
         case 2: return sizeof(s3_layout);
+        case 3: return sizeof(s3_task);
         default: return 0;
     }
 }
@@ -1311,6 +1551,37 @@ int s3_plan(const s3_model* m, int32_t warps_per_block, s3_layout* out) {
     if (wpb < 1 || wpb * per > maxsm) return fail(S3_ERR_BOUNDS, "one world does not fit in shared memory");
     out->warps_per_block = wpb;
     out->bytes_per_block = wpb * per;
+    return S3_OK;
+}
+
+int s3_env_step(const s3_model* m, const s3_data* d, const s3_layout* l, const s3_task* t, const void* actions,
+                int32_t mode, int64_t global_step, void* stream) {
+    using namespace s3;
+    if (!m || !d || !l || !t) return fail(S3_ERR_ARG, "null argument");
+    if (d->nworld == 0) return S3_OK;
+    if (!d->qpos || !d->qvel || !d->qacc_warmstart) return fail(S3_ERR_ARG, "qpos/qvel/qacc_warmstart required");
+    if (mode == 0 && !actions) return fail(S3_ERR_ARG, "actions required");
+    if (t->obs_dim != 12 + 3 * m->nu + t->nscan || t->nscan > S3_MAX_RAYS || t->decimation < 1)
+        return fail(S3_ERR_ARG, "task layout does not match the model");
+    if (d->qM) return fail(S3_ERR_ARG, "parity outputs are not written by s3_env_step");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    int wpb = l->warps_per_block;
+    unsigned grid = (unsigned)((d->nworld + wpb - 1) / wpb);
+    size_t smem = (size_t)l->bytes_per_block;
+    cudaError_t e;
+    if (m->dtype == S3_F64) {
+        e = cudaFuncSetAttribute(env_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e == cudaSuccess)
+            env_kernel<double><<<grid, 32 * wpb, smem, st>>>(*m, *d, *l, *t, static_cast<const double*>(actions), mode,
+                                                              global_step);
+    } else {
+        e = cudaFuncSetAttribute(env_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e == cudaSuccess)
+            env_kernel<float><<<grid, 32 * wpb, smem, st>>>(*m, *d, *l, *t, static_cast<const float*>(actions), mode,
+                                                             global_step);
+    }
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(S3_ERR_CUDA, cudaGetErrorString(e));
     return S3_OK;
 }
 

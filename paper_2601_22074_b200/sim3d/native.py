@@ -22,6 +22,7 @@ _TYPES = _n._build_types(_STRUCTS, _ORDER)
 ModelT = _TYPES["s3_model"]
 DataT = _TYPES["s3_data"]
 LayoutT = _TYPES["s3_layout"]
+TaskT = _TYPES["s3_task"]
 
 _SIGNATURES = {
     "s3_abi_version": ([], ctypes.c_int),
@@ -29,6 +30,7 @@ _SIGNATURES = {
     "s3_last_error": ([], ctypes.c_char_p),
     "s3_plan": ([ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p], ctypes.c_int),
     "s3_step": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p], ctypes.c_int),
+    "s3_env_step": ([ctypes.c_void_p] * 5 + [ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p], ctypes.c_int),
 }
 EXPORTED = sorted(_SIGNATURES)
 _LIB = None
@@ -51,7 +53,7 @@ def lib():
             fn.restype = res
         if so.s3_abi_version() != S3_ABI_VERSION:  # noqa: F821
             raise NativeError("stale sim3d extension: ABI version mismatch, rebuild it")
-        for which, cls in ((0, ModelT), (1, DataT), (2, LayoutT)):
+        for which, cls in ((0, ModelT), (1, DataT), (2, LayoutT), (3, TaskT)):
             if so.s3_sizeof(which) != ctypes.sizeof(cls):
                 raise NativeError(f"struct layout mismatch for {cls.__name__}; rebuild the extension")
         _LIB = so

@@ -1,0 +1,151 @@
+"""Velocity-tracking task on the 3-D path, fused into one kernel launch per control step.
+
+The reference's manager pipeline (env.py:219-259) -- ActionManager.process ->
+decimation x (actuators + physics substep) -> TerminationManager ->
+RewardManager -> masked reset (+ CommandManager.resample) ->
+CommandManager.update -> ObservationManager -- run for the 3-D model with
+mjlab's velocity-tracking terms (§6.1): exp-kernel tracking of the
+commanded planar velocity and yaw rate, vertical-velocity / roll-pitch-rate /
+action-rate / flat-orientation penalties, fall and tilt terminations, a
+time-out truncation, masked reset with joint jitter and random yaw, and
+uniformly resampled (vx, vy, wz) commands. Every stochastic draw is a
+counter-based splitmix64 word keyed by (seed, global world id, purpose), the
+construction of the reference's rng.py, so worlds are partition-independent.
+
+``VelocityEnv3D`` is the batched env: ``reset()`` and ``step(actions)``
+return device tensors (obs (N, D), reward (N,), terminated (N,), truncated
+(N,)); the whole control step is ONE launch of ``s3_env_step``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import native as N
+from .device import Data, DeviceModel
+from .model import Model
+
+PURPOSE_RESET, PURPOSE_COMMAND, PURPOSE_OBS = 1, 2, 3
+
+
+@dataclass
+class VelocityTaskCfg:
+    default_qpos: np.ndarray
+    decimation: int = 4
+    action_scale: float = 0.25
+    action_clip: float = 2.0
+    episode_steps: int = 1000          # 20 s at 50 Hz
+    command_resample_steps: int = 500  # 10 s
+    command_ranges: tuple = ((-1.0, 1.0), (-0.5, 0.5), (-1.0, 1.0))
+    track_sigma: float = 0.25
+    # track_lin_vel_xy_exp, track_ang_vel_z_exp, lin_vel_z_l2, ang_vel_xy_l2, action_rate_l2, flat_orientation_l2
+    reward_weights: tuple = (1.0, 0.5, -2.0, -0.05, -0.01, -1.0)
+    min_height: float = 0.3
+    max_tilt_cos: float = -0.5         # terminate when projected gravity z > -cos(60 deg)
+    reset_joint_jitter: float = 0.1
+    spawn_half_extent: float = 0.5
+    noise: tuple = (0.1, 0.2, 0.05, 0.0, 0.01, 1.5, 0.0)  # lin vel, ang vel, gravity, command, qpos, qvel, action
+    height_scan: bool = False
+    scan_size: tuple = (1.6, 1.0)
+    scan_resolution: float = 0.2
+    scan_offset: float = 0.5
+    scan_noise: float = 0.02
+
+    def scan_points(self):
+        nx = int(round(self.scan_size[0] / self.scan_resolution)) + 1
+        ny = int(round(self.scan_size[1] / self.scan_resolution)) + 1
+        xs = (np.arange(nx) - (nx - 1) / 2) * self.scan_resolution
+        ys = (np.arange(ny) - (ny - 1) / 2) * self.scan_resolution
+        return [(x, y) for y in ys for x in xs]
+
+    def obs_dim(self, m: Model) -> int:
+        return 12 + 3 * m.nu + (len(self.scan_points()) if self.height_scan else 0)
+
+    def noise_vector(self, m: Model) -> np.ndarray:
+        n = self.noise
+        v = [n[0]] * 3 + [n[1]] * 3 + [n[2]] * 3 + [n[3]] * 3 + [n[4]] * m.nu + [n[5]] * m.nu + [n[6]] * m.nu
+        if self.height_scan:
+            v += [self.scan_noise] * len(self.scan_points())
+        return np.array(v)
+
+
+class VelocityEnv3D:
+    """Batched 3-D velocity-tracking env on the GPU (world index outermost)."""
+
+    def __init__(self, model: Model, cfg: VelocityTaskCfg, num_envs: int, seed: int = 0, world_offset: int = 0,
+                 dtype: str = "f64", device="cuda"):
+        self.model, self.cfg, self.num_envs, self.seed = model, cfg, int(num_envs), int(seed)
+        self.world_offset = int(world_offset)
+        self.dm = DeviceModel(model, dtype, device)
+        self.dm.set_const()
+        self.data = Data(self.dm, num_envs)
+        dev, dt = self.dm.device, self.dm.tdtype
+        n, nu = self.num_envs, model.nu
+        self.obs_dim = cfg.obs_dim(model)
+        z = lambda *s: torch.zeros(*s, dtype=dt, device=dev)  # noqa: E731
+        self.action = z(n, nu)
+        self.prev_action = z(n, nu)
+        self.command = z(n, 3)
+        self.cmd_timer = torch.zeros(n, dtype=torch.int32, device=dev)
+        self.episode_step = torch.zeros(n, dtype=torch.int32, device=dev)
+        self.episode_return = z(n)
+        self.obs = z(n, self.obs_dim)
+        self.reward = z(n)
+        self.terminated = torch.zeros(n, dtype=torch.uint8, device=dev)
+        self.truncated = torch.zeros(n, dtype=torch.uint8, device=dev)
+        self.global_step = 0
+        t = N.TaskT()
+        t.decimation, t.episode_steps, t.cmd_resample_steps = cfg.decimation, cfg.episode_steps, \
+            cfg.command_resample_steps
+        t.obs_dim = self.obs_dim
+        t.seed = self.seed
+        t.world_offset = self.world_offset
+        t.action_scale, t.action_clip, t.track_sigma = cfg.action_scale, cfg.action_clip, cfg.track_sigma
+        t.min_height, t.max_tilt_cos, t.reset_joint_jitter = cfg.min_height, cfg.max_tilt_cos, cfg.reset_joint_jitter
+        t.spawn_half_extent = cfg.spawn_half_extent
+        for i, (lo, hi) in enumerate(cfg.command_ranges):
+            t.cmd_lo[i], t.cmd_hi[i] = lo, hi
+        t.reward_weights[:] = cfg.reward_weights
+        t.noise[:] = cfg.noise
+        pts = cfg.scan_points() if cfg.height_scan else []
+        if len(pts) > N.S3_MAX_RAYS:
+            raise ValueError("height scan larger than S3_MAX_RAYS")
+        t.nscan = len(pts)
+        for i, (x, y) in enumerate(pts):
+            t.scan_xy[2 * i], t.scan_xy[2 * i + 1] = x, y
+        t.scan_offset, t.scan_noise = cfg.scan_offset, cfg.scan_noise
+        self._default = torch.as_tensor(cfg.default_qpos, dtype=dt, device=dev).contiguous()
+        t.default_qpos = self._default.data_ptr()
+        for name in ("action", "prev_action", "command", "cmd_timer", "episode_step", "episode_return", "obs",
+                     "reward", "terminated", "truncated"):
+            setattr(t, name, getattr(self, name).data_ptr())
+        self.task = t
+        self._actions_in = z(n, nu)
+
+    def _launch(self, mode: int, actions=None):
+        d = self.data.struct(False)
+        ptr = None if actions is None else actions.data_ptr()
+        st = torch.cuda.current_stream(self.dm.device).cuda_stream
+        N.call("s3_env_step", ctypes.byref(self.dm.struct), ctypes.byref(d), ctypes.byref(self.dm.layout),
+               ctypes.byref(self.task), ptr, int(mode), int(self.global_step), st, launch=True)
+
+    def reset(self):
+        """Reset every world (counter 0 draws) and return the observation tensor."""
+        self.global_step = 0
+        self._launch(1)
+        return self.obs
+
+    def step(self, actions: torch.Tensor):
+        """One control step: (obs, reward, terminated, truncated) as device tensors (reused buffers)."""
+        if actions.dtype != self.dm.tdtype or actions.device != self.dm.device or not actions.is_contiguous():
+            self._actions_in.copy_(actions)
+            actions = self._actions_in
+        if tuple(actions.shape) != (self.num_envs, self.model.nu):
+            raise ValueError(f"actions shape {tuple(actions.shape)} does not match ({self.num_envs}, {self.model.nu})")
+        self.global_step += 1
+        self._launch(0, actions)
+        return self.obs, self.reward, self.terminated, self.truncated

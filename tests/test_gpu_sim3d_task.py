@@ -1,0 +1,140 @@
+"""Fused 3-D velocity task (one launch per control step) vs the oracle's TaskOracle.
+
+Parity unpinned w.r.t. the reference (no 3-D engine there).
+float64: observations, rewards within 1e-8 (free-running, few control steps,
+before chaotic contact divergence); termination / truncation flags and reset
+worlds bit-exact; teacher-forced single steps bit-exact on flags across
+forced terminations, truncations and command resampling.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import sim3d as O
+from paper_2601_22074_b200.sim3d import robots
+from paper_2601_22074_b200.sim3d.task import VelocityTaskCfg
+
+CASES = {
+    "g1_flat": (lambda: robots.g1_like(), robots.G1_DEFAULT_JOINTS, dict()),
+    "g1_rough_scan": (lambda: robots.g1_like(rough=True, seed=1), robots.G1_DEFAULT_JOINTS, dict(height_scan=True)),
+    "go1_flat": (lambda: robots.go1_like(), robots.GO1_DEFAULT_JOINTS, dict(min_height=0.15)),
+}
+
+
+def _pair(name, n, dtype="f64", **over):
+    from paper_2601_22074_b200.sim3d.task import VelocityEnv3D
+
+    make, table, kw = CASES[name]
+    kw = dict(kw, **over)
+    mg, mo = make(), make()
+    cfg = VelocityTaskCfg(default_qpos=robots.default_qpos(mg, table), **kw)
+    env = VelocityEnv3D(mg, cfg, n, seed=7, dtype=dtype)
+    O.set_const(mo)
+    ref = O.TaskOracle(mo, cfg, n, seed=7)
+    return env, ref
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", list(CASES))
+def test_reset_and_free_running_steps_f64(name):
+    import torch
+
+    n = 8
+    env, ref = _pair(name, n)
+    o = env.reset().cpu().numpy()
+    o_ref = ref.reset()
+    np.testing.assert_allclose(o, o_ref, rtol=0, atol=1e-12)
+    rng = np.random.default_rng(0)
+    for k in range(4):
+        a = rng.uniform(-1, 1, size=(n, env.model.nu))
+        o, r, te, tr = env.step(torch.as_tensor(a, device="cuda"))
+        o_ref, r_ref, te_ref, tr_ref = ref.step(a)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(te.cpu().numpy().astype(bool), te_ref)
+        np.testing.assert_array_equal(tr.cpu().numpy().astype(bool), tr_ref)
+        np.testing.assert_allclose(r.cpu().numpy(), r_ref, rtol=1e-8, atol=1e-10)
+        np.testing.assert_allclose(o.cpu().numpy(), o_ref, rtol=1e-7, atol=1e-7)
+
+
+def _load(env, ref):
+    import torch
+
+    t = lambda x: torch.as_tensor(x, device="cuda")  # noqa: E731
+    env.data.qpos.copy_(t(ref.qpos))
+    env.data.qvel.copy_(t(ref.qvel))
+    env.data.qacc_warmstart.copy_(t(ref.warm))
+    env.action.copy_(t(ref.action))
+    env.prev_action.copy_(t(ref.prev_action))
+    env.command.copy_(t(ref.cmd))
+    env.cmd_timer.copy_(t(ref.cmd_timer.astype(np.int32)))
+    env.episode_step.copy_(t(ref.episode_step.astype(np.int32)))
+    env.global_step = ref.global_step
+
+
+@pytest.mark.gpu
+def test_teacher_forced_resets_truncations_and_commands():
+    """Short episodes and command periods force truncation resets and resamples; a tight height
+    threshold forces terminations: every step's flags, reset state and draws must match."""
+    import torch
+
+    n = 8
+    env, ref = _pair("g1_rough_scan", n, episode_steps=3, command_resample_steps=2, min_height=0.78)
+    env.reset()
+    ref.reset()
+    rng = np.random.default_rng(3)
+    saw_term = saw_trunc = 0
+    for k in range(7):
+        _load(env, ref)
+        a = rng.uniform(-1, 1, size=(n, env.model.nu))
+        o, r, te, tr = env.step(torch.as_tensor(a, device="cuda"))
+        o_ref, r_ref, te_ref, tr_ref = ref.step(a)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(te.cpu().numpy().astype(bool), te_ref)
+        np.testing.assert_array_equal(tr.cpu().numpy().astype(bool), tr_ref)
+        np.testing.assert_allclose(r.cpu().numpy(), r_ref, rtol=1e-8, atol=1e-10)
+        np.testing.assert_allclose(o.cpu().numpy(), o_ref, rtol=1e-7, atol=1e-7)
+        np.testing.assert_allclose(env.command.cpu().numpy(), ref.cmd, atol=1e-15)
+        np.testing.assert_array_equal(env.cmd_timer.cpu().numpy(), ref.cmd_timer)
+        np.testing.assert_array_equal(env.episode_step.cpu().numpy(), ref.episode_step)
+        saw_term += int(te_ref.sum())
+        saw_trunc += int(tr_ref.sum())
+    assert saw_term > 0 and saw_trunc > 0
+
+
+@pytest.mark.gpu
+def test_f32_task_close_to_oracle():
+    import torch
+
+    n = 8
+    env, ref = _pair("g1_flat", n, dtype="f32")
+    o = env.reset().double().cpu().numpy()
+    np.testing.assert_allclose(o, ref.reset(), atol=1e-5)
+    a = np.random.default_rng(1).uniform(-1, 1, size=(n, env.model.nu)).astype(np.float32)
+    o, r, te, tr = env.step(torch.as_tensor(a, device="cuda"))
+    o_ref, r_ref, te_ref, _ = ref.step(a.astype(np.float64))
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(te.cpu().numpy().astype(bool), te_ref)
+    np.testing.assert_allclose(r.double().cpu().numpy(), r_ref, atol=1e-4)
+    np.testing.assert_allclose(o.double().cpu().numpy(), o_ref, atol=5e-3 * max(1.0, np.abs(o_ref).max()))
+
+
+@pytest.mark.gpu
+def test_world_offset_partition_independence():
+    """Two shards with world_id offsets reproduce one big batch (worlds are independent)."""
+    import torch
+
+    from paper_2601_22074_b200.sim3d.task import VelocityEnv3D
+
+    make, table, kw = CASES["go1_flat"]
+    cfg = VelocityTaskCfg(default_qpos=robots.default_qpos(make(), table), **kw)
+    full = VelocityEnv3D(make(), cfg, 8, seed=3)
+    a0 = VelocityEnv3D(make(), cfg, 4, seed=3, world_offset=0)
+    a1 = VelocityEnv3D(make(), cfg, 4, seed=3, world_offset=4)
+    of = full.reset().clone()
+    assert torch.equal(of, torch.cat([a0.reset(), a1.reset()]))
+    act = torch.rand(8, full.model.nu, dtype=torch.float64, device="cuda") * 2 - 1
+    for _ in range(3):
+        of, rf, _, _ = full.step(act)
+        o0, r0, _, _ = a0.step(act[:4].contiguous())
+        o1, r1, _, _ = a1.step(act[4:].contiguous())
+    assert torch.equal(of, torch.cat([o0, o1])) and torch.equal(rf, torch.cat([r0, r1]))
