@@ -236,6 +236,19 @@ int s3_step(const s3_model* m, const s3_data* d, const s3_layout* l, int32_t nsu
 int s3_env_step(const s3_model* m, const s3_data* d, const s3_layout* l, const s3_task* t, const void* actions,
                 int32_t mode, int64_t global_step, void* stream);
 
+/* Ray casting against every geom of each world (frames from s3_step / s3_env_step geom outputs):
+ * nearest hit distance along o + t d (|d| = 1, t <= max_dist), -1 and geom -1 on a miss; geoms on
+ * `exclude_body` are skipped. Height scanners pass vertical rays; s3_depth builds pinhole rays of a
+ * camera fixed to geom `cam_geom` (forward +x, right -y, up +z of the geom frame, vertical field of
+ * view `fovy` radians) and writes an (N, height, width) range image. Replaces, for the 3-D path,
+ * RayScanner.read (sensors.py:26-46 of the reference; mjlab's RayCastSensor / depth camera). */
+int s3_raycast(const s3_model* m, const void* geom_xpos, const void* geom_xmat, int64_t nworld, int32_t nray,
+               const void* origin, const void* dir, double max_dist, int32_t exclude_body, void* dist, int32_t* geom,
+               void* stream);
+int s3_depth(const s3_model* m, const void* geom_xpos, const void* geom_xmat, int64_t nworld, int32_t cam_geom,
+             const double* offset, int32_t width, int32_t height, double fovy, double max_dist, int32_t exclude_body,
+             void* dist, int32_t* geom, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

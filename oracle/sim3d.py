@@ -824,3 +824,147 @@ class TaskOracle:
                 if self.cmd_timer[w] <= 0:
                     self.resample(w, ctr)
         return self.observe(ctr), rew, term, trunc
+
+
+# ----------------------------------------------------------------------------- ray casting (sensors)
+# Specification of s3_raycast / s3_depth: nearest hit along o + t d (|d| = 1, 0 < t <= max_dist)
+# over every geom of the world except those on `exclude_body`; -1 / geom -1 when nothing is hit.
+
+HF_MARCH = 0.5     # march step in units of the heightfield spacing
+HF_BISECT = 24     # bisection steps after a sign change
+
+
+def ray_plane(n, p0, o, d):
+    den = n @ d
+    if not den < 0.0:
+        return np.inf
+    t = (n @ (p0 - o)) / den
+    return t if t > 0.0 else np.inf
+
+
+def ray_sphere(c, r, o, d):
+    oc = o - c
+    b = oc @ d
+    cc = oc @ oc - r * r
+    disc = b * b - cc
+    if disc < 0.0:
+        return np.inf
+    sq = np.sqrt(disc)
+    t = -b - sq
+    if t > 0.0:
+        return t
+    t = -b + sq
+    return t if t > 0.0 else np.inf
+
+
+def ray_capsule(c, ax, hl, r, o, d):
+    best = min(ray_sphere(c - ax * hl, r, o, d), ray_sphere(c + ax * hl, r, o, d))
+    # cylinder part
+    oc = o - c
+    dd = d - ax * (d @ ax)
+    oo = oc - ax * (oc @ ax)
+    a = dd @ dd
+    if a > 1e-12:
+        b = oo @ dd
+        cc = oo @ oo - r * r
+        disc = b * b - a * cc
+        if disc >= 0.0:
+            sq = np.sqrt(disc)
+            for t in ((-b - sq) / a, (-b + sq) / a):
+                if t > 0.0:
+                    z = (oc + d * t) @ ax
+                    if -hl <= z <= hl and t < best:
+                        best = t
+                    break
+    return best
+
+
+def ray_box(c, R, size, o, d):
+    ol = R.T @ (o - c)
+    dl = R.T @ d
+    tmin, tmax = -np.inf, np.inf
+    for k in range(3):
+        if abs(dl[k]) < 1e-12:
+            if ol[k] < -size[k] or ol[k] > size[k]:
+                return np.inf
+            continue
+        t1 = (-size[k] - ol[k]) / dl[k]
+        t2 = (size[k] - ol[k]) / dl[k]
+        if t1 > t2:
+            t1, t2 = t2, t1
+        tmin = max(tmin, t1)
+        tmax = min(tmax, t2)
+    if tmax < tmin or tmax <= 0.0:
+        return np.inf
+    return tmin if tmin > 0.0 else tmax
+
+
+def _hf_f(m, p):
+    h = hfield_point(m, p, 0.0)
+    if h is None:
+        return 1.0  # outside the grid: no terrain
+    return h[0]
+
+
+def ray_hfield(m, o, d, tmax):
+    step = HF_MARCH * m.hfield_spacing
+    t0 = 0.0
+    f0 = _hf_f(m, o)
+    if f0 < 0.0:
+        return np.inf  # starts below the terrain
+    nstep = int(np.ceil(tmax / step))
+    for i in range(1, nstep + 1):
+        t1 = min(i * step, tmax)
+        f1 = _hf_f(m, o + d * t1)
+        if f1 < 0.0:
+            a, b = t0, t1
+            for _ in range(HF_BISECT):
+                mid = 0.5 * (a + b)
+                if _hf_f(m, o + d * mid) < 0.0:
+                    b = mid
+                else:
+                    a = mid
+            return b
+        t0 = t1
+    return np.inf
+
+
+def raycast(m, K, o, d, max_dist, exclude_body=-1):
+    best, gid = np.inf, -1
+    for g in range(m.ngeom):
+        if m.geom_bodyid[g] == exclude_body:
+            continue
+        t = m.geom_type[g]
+        c, R, s = K["geom_xpos"][g], K["geom_xmat"][g], m.geom_size[g]
+        if t == GEOM_PLANE:
+            tt = ray_plane(R[:, 2], c, o, d)
+        elif t == GEOM_HFIELD:
+            tt = ray_hfield(m, o, d, max_dist)
+        elif t == GEOM_SPHERE:
+            tt = ray_sphere(c, s[0], o, d)
+        elif t == GEOM_CAPSULE:
+            tt = ray_capsule(c, R[:, 2], s[1], s[0], o, d)
+        else:
+            tt = ray_box(c, R, s, o, d)
+        if tt < best:
+            best, gid = tt, g
+    if not best <= max_dist:
+        return -1.0, -1
+    return best, gid
+
+
+def camera_rays(K, cam_geom, width, height, fovy, offset=np.zeros(3)):
+    """Pinhole rays of a camera fixed to geom `cam_geom`: forward +x, right -y, up +z of the geom frame."""
+    R, c = K["geom_xmat"][cam_geom], K["geom_xpos"][cam_geom]
+    ty = np.tan(0.5 * fovy)
+    tx = ty * width / height
+    o = c + R @ offset
+    dirs = np.zeros((height, width, 3))
+    for i in range(height):
+        for j in range(width):
+            a = (2.0 * (j + 0.5) / width - 1.0) * tx
+            b = (1.0 - 2.0 * (i + 0.5) / height) * ty
+            dl = np.array([1.0, -a, b])
+            dl = dl / np.sqrt(dl @ dl)
+            dirs[i, j] = R @ dl
+    return o, dirs

@@ -1412,6 +1412,7 @@ __global__ void __launch_bounds__(32 * 16) env_kernel(const __grid_constant__ s3
         }
         __syncwarp();
         task_observe(m, tk, s, w, 0, cmd, act, lane);
+        if (d.geom_xpos) store_geom_frames(m, d, s, w, lane);
         for (int i = lane; i < nq; i += 32) gq[i] = s.qpos[i];
         for (int i = lane; i < nv; i += 32) gv[i] = s.qvel[i];
         return;
@@ -1479,8 +1480,190 @@ __global__ void __launch_bounds__(32 * 16) env_kernel(const __grid_constant__ s3
     }
     __syncwarp();
     task_observe(m, tk, s, w, ctr, cmd, act, lane);
+    if (d.geom_xpos) store_geom_frames(m, d, s, w, lane);  // sensors see the post-reset state, like obs
     for (int i = lane; i < nq; i += 32) gq[i] = s.qpos[i];
     for (int i = lane; i < nv; i += 32) gv[i] = s.qvel[i];
+}
+
+// ---------------------------------------------------------------- ray casting (oracle raycast)
+
+constexpr double kHfMarch = 0.5;
+constexpr int kHfBisect = 24;
+
+template <class T> __device__ inline T ray_plane(const T* n, const T* p0, const T* o, const T* d) {
+    T den = dot3(n, d);
+    if (!(den < T(0))) return T(INFINITY);
+    T dp[3] = {p0[0] - o[0], p0[1] - o[1], p0[2] - o[2]};
+    T t = dot3(n, dp) / den;
+    return t > T(0) ? t : T(INFINITY);
+}
+
+template <class T> __device__ inline T ray_sphere(const T* c, T r, const T* o, const T* d) {
+    T oc[3] = {o[0] - c[0], o[1] - c[1], o[2] - c[2]};
+    T b = dot3(oc, d);
+    T cc = dot3(oc, oc) - r * r;
+    T disc = b * b - cc;
+    if (disc < T(0)) return T(INFINITY);
+    T sq = sqrt(disc);
+    T t = -b - sq;
+    if (t > T(0)) return t;
+    t = -b + sq;
+    return t > T(0) ? t : T(INFINITY);
+}
+
+template <class T> __device__ inline T ray_capsule(const T* c, const T* ax, T hl, T r, const T* o, const T* d) {
+    T e0[3] = {c[0] - ax[0] * hl, c[1] - ax[1] * hl, c[2] - ax[2] * hl};
+    T e1[3] = {c[0] + ax[0] * hl, c[1] + ax[1] * hl, c[2] + ax[2] * hl};
+    T best = fmin(ray_sphere(e0, r, o, d), ray_sphere(e1, r, o, d));
+    T oc[3] = {o[0] - c[0], o[1] - c[1], o[2] - c[2]};
+    T da = dot3(d, ax), oa = dot3(oc, ax);
+    T dd[3] = {d[0] - ax[0] * da, d[1] - ax[1] * da, d[2] - ax[2] * da};
+    T oo[3] = {oc[0] - ax[0] * oa, oc[1] - ax[1] * oa, oc[2] - ax[2] * oa};
+    T a = dot3(dd, dd);
+    if (a > T(1e-12)) {
+        T b = dot3(oo, dd);
+        T cc = dot3(oo, oo) - r * r;
+        T disc = b * b - a * cc;
+        if (disc >= T(0)) {
+            T sq = sqrt(disc);
+            T ts[2] = {(-b - sq) / a, (-b + sq) / a};
+            for (int k = 0; k < 2; ++k) {
+                T t = ts[k];
+                if (t > T(0)) {
+                    T p[3] = {oc[0] + d[0] * t, oc[1] + d[1] * t, oc[2] + d[2] * t};
+                    T z = dot3(p, ax);
+                    if (-hl <= z && z <= hl && t < best) best = t;
+                    break;
+                }
+            }
+        }
+    }
+    return best;
+}
+
+template <class T> __device__ inline T ray_box(const T* c, const T* R, const T* size, const T* o, const T* d) {
+    T oc[3] = {o[0] - c[0], o[1] - c[1], o[2] - c[2]};
+    T tmin = T(-INFINITY), tmax = T(INFINITY);
+    for (int k = 0; k < 3; ++k) {
+        T ol = R[k] * oc[0] + R[3 + k] * oc[1] + R[6 + k] * oc[2];
+        T dl = R[k] * d[0] + R[3 + k] * d[1] + R[6 + k] * d[2];
+        if (fabs(dl) < T(1e-12)) {
+            if (ol < -size[k] || ol > size[k]) return T(INFINITY);
+            continue;
+        }
+        T t1 = (-size[k] - ol) / dl, t2 = (size[k] - ol) / dl;
+        if (t1 > t2) { T x = t1; t1 = t2; t2 = x; }
+        tmin = fmax(tmin, t1);
+        tmax = fmin(tmax, t2);
+    }
+    if (tmax < tmin || tmax <= T(0)) return T(INFINITY);
+    return tmin > T(0) ? tmin : tmax;
+}
+
+template <class T> __device__ inline T hf_f(const s3_model& m, const T* p) {
+    T dd, n[3];
+    if (!hfield_point(m, p, T(0), dd, n)) return T(1);
+    return dd;
+}
+
+template <class T> __device__ T ray_hfield(const s3_model& m, const T* o, const T* d, T tmax) {
+    T step = T(kHfMarch) * T(m.hf_spacing);
+    T t0 = T(0);
+    if (hf_f(m, o) < T(0)) return T(INFINITY);
+    int nstep = (int)ceil(tmax / step);
+    for (int i = 1; i <= nstep; ++i) {
+        T t1 = fmin(T(i) * step, tmax);
+        T p[3] = {o[0] + d[0] * t1, o[1] + d[1] * t1, o[2] + d[2] * t1};
+        if (hf_f(m, p) < T(0)) {
+            T a = t0, b = t1;
+            for (int k = 0; k < kHfBisect; ++k) {
+                T mid = T(0.5) * (a + b);
+                T q[3] = {o[0] + d[0] * mid, o[1] + d[1] * mid, o[2] + d[2] * mid};
+                if (hf_f(m, q) < T(0)) b = mid;
+                else a = mid;
+            }
+            return b;
+        }
+        t0 = t1;
+    }
+    return T(INFINITY);
+}
+
+template <class T>
+__device__ void raycast1(const s3_model& m, const T* gpos, const T* gmat, const T* o, const T* d, T maxd, int excl,
+                         T& dist, int& gid) {
+    const T* sz = F<T>(m.geom_size);
+    T best = T(INFINITY);
+    int bg = -1;
+    for (int g = 0; g < m.ngeom; ++g) {
+        if (m.geom_bodyid[g] == excl) continue;
+        int t = m.geom_type[g];
+        const T* c = gpos + 3 * g;
+        const T* R = gmat + 9 * g;
+        T tt;
+        if (t == kGeomPlane) {
+            T n[3] = {R[2], R[5], R[8]};
+            tt = ray_plane(n, c, o, d);
+        } else if (t == kGeomHfield) {
+            tt = ray_hfield(m, o, d, maxd);
+        } else if (t == kGeomSphere) {
+            tt = ray_sphere(c, sz[3 * g], o, d);
+        } else if (t == kGeomCapsule) {
+            T ax[3] = {R[2], R[5], R[8]};
+            tt = ray_capsule(c, ax, sz[3 * g + 1], sz[3 * g], o, d);
+        } else {
+            tt = ray_box(c, R, sz + 3 * g, o, d);
+        }
+        if (tt < best) { best = tt; bg = g; }
+    }
+    if (!(best <= maxd)) { dist = T(-1); gid = -1; }
+    else { dist = best; gid = bg; }
+}
+
+template <class T>
+__global__ void raycast_kernel(const __grid_constant__ s3_model m, const T* __restrict__ gpos, const T* __restrict__ gmat,
+                               int64_t nworld, int nray, const T* __restrict__ origin, const T* __restrict__ dir,
+                               T maxd, int excl, T* __restrict__ out, int* __restrict__ gout) {
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nworld * nray) return;
+    int64_t w = t / nray;
+    T o[3] = {origin[3 * t], origin[3 * t + 1], origin[3 * t + 2]};
+    T d[3] = {dir[3 * t], dir[3 * t + 1], dir[3 * t + 2]};
+    T dist;
+    int g;
+    raycast1(m, gpos + w * m.ngeom * 3, gmat + w * m.ngeom * 9, o, d, maxd, excl, dist, g);
+    out[t] = dist;
+    if (gout) gout[t] = g;
+}
+
+template <class T>
+__global__ void depth_kernel(const __grid_constant__ s3_model m, const T* __restrict__ gpos, const T* __restrict__ gmat,
+                             int64_t nworld, int cam, T ox, T oy, T oz, int W, int H, T tx, T ty, T maxd, int excl,
+                             T* __restrict__ out, int* __restrict__ gout) {
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int64_t npix = (int64_t)W * H;
+    if (t >= nworld * npix) return;
+    int64_t w = t / npix;
+    int pix = (int)(t - w * npix);
+    int i = pix / W, j = pix % W;
+    const T* gp = gpos + w * m.ngeom * 3;
+    const T* gm = gmat + w * m.ngeom * 9;
+    const T* R = gm + 9 * cam;
+    T off[3] = {ox, oy, oz}, v[3];
+    mv3(R, off, v);
+    T o[3] = {gp[3 * cam] + v[0], gp[3 * cam + 1] + v[1], gp[3 * cam + 2] + v[2]};
+    T a = (T(2) * (T(j) + T(0.5)) / T(W) - T(1)) * tx;
+    T b = (T(1) - T(2) * (T(i) + T(0.5)) / T(H)) * ty;
+    T dl[3] = {T(1), -a, b};
+    T rn = rsqrt_t(dot3(dl, dl));
+    dl[0] *= rn; dl[1] *= rn; dl[2] *= rn;
+    T d[3];
+    mv3(R, dl, d);
+    T dist;
+    int g;
+    raycast1(m, gp, gm, o, d, maxd, excl, dist, g);
+    out[t] = dist;
+    if (gout) gout[t] = g;
 }
 
 }  // namespace s3
@@ -1608,6 +1791,54 @@ int s3_step(const s3_model* m, const s3_data* d, const s3_layout* l, int32_t nsu
         if (e == cudaSuccess) step_kernel<float><<<grid, 32 * wpb, smem, st>>>(*m, *d, *l, nsub);
     }
     if (e == cudaSuccess) e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(S3_ERR_CUDA, cudaGetErrorString(e));
+    return S3_OK;
+}
+
+int s3_raycast(const s3_model* m, const void* geom_xpos, const void* geom_xmat, int64_t nworld, int32_t nray,
+               const void* origin, const void* dir, double max_dist, int32_t exclude_body, void* dist, int32_t* geom,
+               void* stream) {
+    using namespace s3;
+    if (!m || !geom_xpos || !geom_xmat || !origin || !dir || !dist || nray < 0) return fail(S3_ERR_ARG, "null argument");
+    int64_t n = nworld * nray;
+    if (n == 0) return S3_OK;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    unsigned grid = (unsigned)((n + 127) / 128);
+    if (m->dtype == S3_F64)
+        raycast_kernel<double><<<grid, 128, 0, st>>>(*m, (const double*)geom_xpos, (const double*)geom_xmat, nworld, nray,
+                                                     (const double*)origin, (const double*)dir, max_dist, exclude_body,
+                                                     (double*)dist, geom);
+    else
+        raycast_kernel<float><<<grid, 128, 0, st>>>(*m, (const float*)geom_xpos, (const float*)geom_xmat, nworld, nray,
+                                                    (const float*)origin, (const float*)dir, (float)max_dist,
+                                                    exclude_body, (float*)dist, geom);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(S3_ERR_CUDA, cudaGetErrorString(e));
+    return S3_OK;
+}
+
+int s3_depth(const s3_model* m, const void* geom_xpos, const void* geom_xmat, int64_t nworld, int32_t cam_geom,
+             const double* offset, int32_t width, int32_t height, double fovy, double max_dist, int32_t exclude_body,
+             void* dist, int32_t* geom, void* stream) {
+    using namespace s3;
+    if (!m || !geom_xpos || !geom_xmat || !offset || !dist || width <= 0 || height <= 0)
+        return fail(S3_ERR_ARG, "null argument");
+    if (cam_geom < 0 || cam_geom >= m->ngeom) return fail(S3_ERR_ARG, "camera geom out of range");
+    int64_t n = nworld * (int64_t)width * height;
+    if (n == 0) return S3_OK;
+    double ty = tan(0.5 * fovy), tx = ty * width / height;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    unsigned grid = (unsigned)((n + 127) / 128);
+    if (m->dtype == S3_F64)
+        depth_kernel<double><<<grid, 128, 0, st>>>(*m, (const double*)geom_xpos, (const double*)geom_xmat, nworld,
+                                                   cam_geom, offset[0], offset[1], offset[2], width, height, tx, ty,
+                                                   max_dist, exclude_body, (double*)dist, geom);
+    else
+        depth_kernel<float><<<grid, 128, 0, st>>>(*m, (const float*)geom_xpos, (const float*)geom_xmat, nworld,
+                                                  cam_geom, (float)offset[0], (float)offset[1], (float)offset[2], width,
+                                                  height, (float)tx, (float)ty, (float)max_dist, exclude_body,
+                                                  (float*)dist, geom);
+    cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(S3_ERR_CUDA, cudaGetErrorString(e));
     return S3_OK;
 }
