@@ -271,6 +271,66 @@ def at_scale(args, flush, stream) -> dict:
     return out
 
 
+def sim3d_leg(args, flush, stream) -> dict:
+    """The 3-D path: G1-like humanoid (29 dof, free base) velocity tracking on a rough
+    heightfield with the height scan, 4096 worlds, decimation 4, Newton contact solver; one fused launch
+    per control step (s3_env_step). Random actions are pre-drawn on the device (inputs resident in HBM).
+    Parity is against oracle/sim3d.py (unpinned w.r.t. the reference, which has no 3-D engine)."""
+    import torch
+
+    from paper_2601_22074_b200.sim3d import native as native3
+    from paper_2601_22074_b200.sim3d import robots
+    from paper_2601_22074_b200.sim3d.task import VelocityEnv3D, VelocityTaskCfg
+
+    n = args.envs
+    out = {"workload": f"G1-like 3-D humanoid velocity tracking, rough heightfield + height scan, {n} worlds/GPU, "
+                       "decimation 4 (planar-free 3-D path, SURVEY 8 f4)", "unit": UNIT}
+    for dtype in ("f32", "f64"):
+        m = robots.g1_like(rough=True, seed=args.seed)
+        cfg = VelocityTaskCfg(default_qpos=robots.default_qpos(m, robots.G1_DEFAULT_JOINTS), height_scan=True)
+        env = VelocityEnv3D(m, cfg, n, seed=args.seed, world_offset=int(os.environ.get("RANK", "0")) * n, dtype=dtype)
+        env.reset()
+        steps = 20
+        g = torch.Generator(device="cuda")
+        g.manual_seed(args.seed)
+        acts = torch.rand(steps + 5, n, m.nu, generator=g, device="cuda", dtype=env.dm.tdtype) * 2 - 1
+        for i in range(5):
+            env.step(acts[i])
+        l0 = native3.LAUNCHES["count"]
+        t = timed_steps(env, steps, flush, stream, lambda i: acts[5 + i])
+        launches = native3.LAUNCHES["count"] - l0
+        out[dtype] = {"value": n * steps / t, "ms_per_step": 1e3 * t / steps, "gpu_launches": launches,
+                      "warps_per_block": env.dm.layout.warps_per_block,
+                      "smem_bytes_per_world": env.dm.layout.elems_per_world * (4 if dtype == "f32" else 8),
+                      "terminated_frac_last": float(env.terminated.float().mean().item())}
+        del env
+    out["kernel"] = "s3::env_kernel (warp per world, shared-memory resident; one launch per control step)"
+    out["parity"] = "oracle/sim3d.py (tests/test_gpu_sim3d*.py); unpinned w.r.t. the reference (no 3-D engine)"
+    if not args.no_cpu:
+        out["cpu_baseline"] = sim3d_cpu(args.seed)
+    return out
+
+
+def sim3d_cpu(seed, worlds=4, steps=2) -> dict:
+    """The 3-D oracle (numpy, one core) on a bounded sample of the same task."""
+    from oracle import sim3d as O
+    from paper_2601_22074_b200.sim3d import robots
+    from paper_2601_22074_b200.sim3d.task import VelocityTaskCfg
+
+    m = robots.g1_like(rough=True, seed=seed)
+    O.set_const(m)
+    cfg = VelocityTaskCfg(default_qpos=robots.default_qpos(m, robots.G1_DEFAULT_JOINTS), height_scan=True)
+    ref = O.TaskOracle(m, cfg, worlds, seed=seed)
+    ref.reset()
+    rng = np.random.default_rng(seed)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        ref.step(rng.uniform(-1, 1, size=(worlds, m.nu)))
+    el = time.perf_counter() - t0
+    return {"value": worlds * steps / el, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"{worlds} worlds x {steps} control steps of the 3-D oracle (numpy float64, 1 process)"}
+
+
 def run_ours(args):
     import torch
 
@@ -346,6 +406,11 @@ def run_ours(args):
                    "into pinned host memory) -> stream sync"}
 
     scale = at_scale(args, flush, stream) if (world == 1 and args.scale_envs > 0) else None
+    s3 = None if args.no_sim3d else sim3d_leg(args, flush, stream)
+    if s3 is not None:
+        for k in ("f32", "f64"):
+            s3[k]["value"] = s3[k]["value"] * world  # whole job: every rank steps its own shard (weak scaling)
+            s3[k]["ms_per_step"] = allmax(s3[k]["ms_per_step"], world)
 
     if rank == 0:
         cpu = None
@@ -376,6 +441,7 @@ def run_ours(args):
                          "kernel_ms": 1e3 * t_kernel / args.steps},
             "policy": "random_policy fused into the step kernel (policies.RandomActions: same stream and values)",
             "at_scale": scale,
+            "sim3d": s3,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
@@ -438,6 +504,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the end-to-end leg (profiling runs)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-sim3d", action="store_true", help="skip the 3-D (SURVEY 8 f4) leg")
     ap.add_argument("--scale-envs", type=int, default=262144,
                     help="also time the step at this many worlds (HBM-bound regime); 0 disables")
     args = ap.parse_args()

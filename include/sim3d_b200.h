@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define S3_ABI_VERSION 3
+#define S3_ABI_VERSION 5
 #define S3_F64 0
 #define S3_F32 1
 
@@ -57,6 +57,8 @@ typedef struct s3_model {
     int32_t hf_ncol;
     int32_t iterations;
     int32_t ls_iterations;
+    int32_t nldl_norm;
+    int32_t ntree;
     double timestep;
     double gravity[3];
     double tolerance;
@@ -128,6 +130,10 @@ typedef struct s3_model {
      * pair's J^T J keeps the tree sparsity pattern, and the (a, b) decode of packed-lower index t */
     const int32_t* ldl_ptr;
     const uint16_t* ldl_pair;
+    const uint16_t* ldl_norm;
+    const uint16_t* tree_ent;
+    const uint64_t* dof_chainmask;
+    const uint64_t* pair_dofmask;
     const int32_t* pair_class;
     const int32_t* pair_tree;
     const uint16_t* tri_tab;

@@ -33,7 +33,7 @@ constexpr int kConStride = 14;  // dist, pos[3], frame[9], mu
 
 // layout slots (s3_layout.off)
 enum {
-    O_XPOS, O_XQUAT, O_XIPOS, O_CINERT, O_CRB, O_CDOF, O_CDOFD, O_CVEL, O_CACC, O_JANC, O_JAX,
+    O_XPOS, O_XQUAT, O_XIPOS, O_CINERT, O_JANC, O_JAX, O_CRB, O_CDOF, O_CDOFD, O_CVEL, O_CACC,
     O_M, O_LD, O_QPOS, O_QVEL, O_SMOOTH, O_A0, O_A, O_MA, O_GRAD, O_P, O_MP, O_KVD, O_GPOS, O_GMAT,
     O_CON, O_JC, O_RAREF, O_RD, O_RJAR, O_RJP, O_CDOT, O_BIAS, O_FCON, O_CTRL, O_COM, O_INT, O_END
 };
@@ -146,7 +146,7 @@ template <class T> __device__ inline T clampt(T x, T lo, T hi) { return x < lo ?
 template <class T> struct WS {
     T *xpos, *xquat, *xipos, *cinert, *crb, *cdof, *cdofd, *cvel, *cacc, *janc, *jax, *M, *LD, *qpos, *qvel,
         *smooth, *a0, *a, *Ma, *grad, *p, *Mp, *kvd, *gpos, *gmat, *con, *Jc, *raref, *rD, *rjar, *rJp, *cdot,
-        *bias, *fcon, *ctrl, *com, *tk, *u;
+        *bias, *fcon, *ctrl, *com, *tk, *u, *snap;
     int *con_pair, *lim_dof, *lim_sign, *misc;
 };
 
@@ -157,6 +157,9 @@ template <class T> __device__ inline WS<T> make_ws(T* base, const s3_layout& l) 
     s.cinert = base + o[O_CINERT]; s.crb = s.cinert; s.cdof = base + o[O_CDOF];
     s.tk = base + o[O_CRB]; s.u = s.tk + S3_MAX_NV;
     s.janc = base + o[O_JANC]; s.jax = base + o[O_JAX];
+    // factorization snapshot (rows touched by constraints, tree entries): xipos, cinert, janc, jax are
+    // contiguous and dead from the end of the mass-matrix build until the next substep's kinematics
+    s.snap = s.xipos;
     // RNE scratch lives in the contact-Jacobian region (dead until build_rows)
     s.cdofd = base + o[O_JC]; s.cvel = s.cdofd + o[O_CDOFD]; s.cacc = s.cvel + o[O_CVEL];
     s.M = base + o[O_M]; s.LD = base + o[O_LD]; s.qpos = base + o[O_QPOS]; s.qvel = base + o[O_QVEL];
@@ -179,7 +182,8 @@ template <class T> __device__ inline const T* F(const void* p) { return static_c
 // ---------------------------------------------------------------- stages
 
 // mj_kinematics: body frames level by level (oracle kinematics)
-template <class T> __device__ void kinematics(const s3_model& m, WS<T>& s, int lane) {
+template <class T> __device__ void __noinline__ kinematics(const s3_model& m, const s3_layout& L_, T* B_, int lane) {
+    WS<T> s = make_ws(B_, L_);
     const T* bpos = F<T>(m.body_pos);
     const T* bquat = F<T>(m.body_quat);
     const T* jpos = F<T>(m.jnt_pos);
@@ -242,7 +246,8 @@ template <class T> __device__ void kinematics(const s3_model& m, WS<T>& s, int l
 }
 
 // mj_comPos: xipos, subtree com (single tree), cinert, cdof; geom frames
-template <class T> __device__ void com_pos(const s3_model& m, WS<T>& s, int lane) {
+template <class T> __device__ void __noinline__ com_pos(const s3_model& m, const s3_layout& L_, T* B_, int lane) {
+    WS<T> s = make_ws(B_, L_);
     const T* ipos = F<T>(m.body_ipos);
     const T* ilmat = F<T>(m.body_ilmat);
     const T* mass = F<T>(m.body_mass);
@@ -315,7 +320,8 @@ template <class T> __device__ void com_pos(const s3_model& m, WS<T>& s, int lane
 }
 
 // geom frames from the body frames
-template <class T> __device__ void geom_frames(const s3_model& m, WS<T>& s, int lane) {
+template <class T> __device__ void __noinline__ geom_frames(const s3_model& m, const s3_layout& L_, T* B_, int lane) {
+    WS<T> s = make_ws(B_, L_);
     const T* gp = F<T>(m.geom_pos);
     const T* gl = F<T>(m.geom_lmat);
     for (int g = lane; g < m.ngeom; g += 32) {
@@ -334,7 +340,8 @@ template <class T> __device__ void geom_frames(const s3_model& m, WS<T>& s, int 
 
 // mj_crb: composite inertias (levels, deepest first, children in descending index) + packed M.
 // Accumulates in place over cinert (RNE, the only other reader of cinert, has already run).
-template <class T> __device__ void crb_mass(const s3_model& m, WS<T>& s, int lane) {
+template <class T> __device__ void __noinline__ crb_mass(const s3_model& m, const s3_layout& L_, T* B_, int lane) {
+    WS<T> s = make_ws(B_, L_);
     for (int L = m.nlevel - 2; L >= 1; --L) {
         int n0 = m.level_ptr[L], nl = m.level_ptr[L + 1] - n0;
         for (int t = lane; t < nl * 10; t += 32) {
@@ -365,50 +372,79 @@ template <class T> __device__ void crb_mass(const s3_model& m, WS<T>& s, int lan
     __syncwarp();
 }
 
-// mj_factorM: tree-sparse L^T D L in place on packed-lower A (oracle factor_ldl)
-// Row k is normalised first (tk[i] = L[k,i] / D[k], u keeps the unnormalised values), then the
-// (i, j) updates of step k run from the precomputed list, one pair per lane.
-template <class T> __device__ void factor_ldl(const s3_model& m, T* A, T* tk, T* u, int lane) {
+// mj_factorM: tree-sparse L^T D L in place on packed-lower A (oracle factor_ldl).
+// Step k applies the Schur updates A[i][j] -= (A[k][i] / D[k]) A[k][j] for the (i, j) pairs of its
+// precomputed list, one pair per lane, reading row k UNnormalised; row k is never read again by a later
+// step (those only touch rows of ancestors), so rows are normalised in one pass at the end: one barrier
+// per dof. `sel` restricts the elimination to the dofs outside (1) or inside (2) the ancestor-closed set
+// U (0: all): subtrees outside U eliminate identically for M and for H = M + J^T D J when every
+// constraint row lives on U, so Newton refactors only U (eliminations of disjoint subtrees commute).
+template <class T>
+__device__ __noinline__ void factor_ldl(const s3_model& m, T* A, int lane, uint64_t U = 0, int sel = 0) {
     for (int k = m.nv - 1; k >= 0; --k) {
-        int len = m.dof_chainlen[k] - 1;  // strict ancestors
-        if (len <= 0) continue;
-        const uint8_t* ch = m.dof_chain + k * S3_MAX_CHAIN;
-        T dk = A[tri(k, k)];
-        for (int a = lane; a < len; a += 32) {
-            int i = ch[a];
-            T v = A[tri(k, i)];
-            T t = v / dk;
-            u[i] = v;
-            tk[i] = t;
-            A[tri(k, i)] = t;
-        }
-        __syncwarp();
-        for (int t = m.ldl_ptr[k] + lane; t < m.ldl_ptr[k + 1]; t += 32) {
-            int pr = m.ldl_pair[t];
+        if (sel && (int)((U >> k) & 1ull) != (sel == 2)) continue;
+        int p0 = __ldg(m.ldl_ptr + k), p1 = __ldg(m.ldl_ptr + k + 1);
+        if (p0 == p1) continue;
+        T rk = T(1) / A[tri(k, k)];
+        int rkb = tri(k, 0);
+        for (int t = p0 + lane; t < p1; t += 32) {
+            int pr = __ldg(m.ldl_pair + t);
             int i = pr >> 8, j = pr & 255;
-            A[tri(i, j)] -= tk[i] * u[j];
+            A[tri(i, j)] -= (A[rkb + i] * rk) * A[rkb + j];
         }
         __syncwarp();
     }
+    for (int t = lane; t < m.nldl_norm; t += 32) {
+        int pr = __ldg(m.ldl_norm + t);
+        int k = pr >> 8, i = pr & 255;
+        if (sel && (int)((U >> k) & 1ull) != (sel == 2)) continue;
+        A[tri(k, i)] = A[tri(k, i)] / A[tri(k, k)];
+    }
+    __syncwarp();
+}
+
+// tree entries (i, j in chain(i)) of the rows in U: A -> snap (save) or snap -> A (restore); all rows if U = ~0
+template <class T>
+__device__ __noinline__ void tree_copy(const s3_model& m, T* A, T* snap, uint64_t U, bool save, int lane) {
+    for (int t = lane; t < m.ntree; t += 32) {
+        int pr = __ldg(m.tree_ent + t);
+        int i = pr >> 8, j = pr & 255;
+        if (!((U >> i) & 1ull)) continue;
+        if (save) snap[t] = A[tri(i, j)];
+        else A[tri(i, j)] = snap[t];
+    }
+    __syncwarp();
+}
+
+// copy the tree entries of M into A (everything a tree factorization / solve reads)
+template <class T> __device__ __noinline__ void tree_load(const s3_model& m, const T* M, T* A, int lane) {
+    for (int t = lane; t < m.ntree; t += 32) {
+        int pr = __ldg(m.tree_ent + t);
+        int k = tri(pr >> 8, pr & 255);
+        A[k] = M[k];
+    }
+    __syncwarp();
 }
 
 // x <- M^-1 x with the L^T D L factor (oracle solve_ldl; column-oriented forward pass)
-template <class T> __device__ void solve_ldl(const s3_model& m, const T* A, T* x, int lane) {
+template <class T> __device__ __noinline__ void solve_ldl(const s3_model& m, const T* A, T* x, int lane) {
     int nv = m.nv;
     for (int i = nv - 1; i >= 0; --i) {
-        int len = m.dof_chainlen[i] - 1;
+        int len = __ldg(m.dof_chainlen + i) - 1;
+        if (len <= 0) continue;
         const uint8_t* ch = m.dof_chain + i * S3_MAX_CHAIN;
         T xi = x[i];
+        int rb = tri(i, 0);
         for (int a = lane; a < len; a += 32) {
-            int j = ch[a];
-            x[j] -= A[tri(i, j)] * xi;
+            int j = __ldg(ch + a);
+            x[j] -= A[rb + j] * xi;
         }
         __syncwarp();
     }
     for (int i = lane; i < nv; i += 32) x[i] = x[i] / A[tri(i, i)];
     __syncwarp();
     for (int j = 0; j < nv; ++j) {
-        uint64_t dm = m.dof_descmask[j];
+        uint64_t dm = __ldg(reinterpret_cast<const unsigned long long*>(m.dof_descmask) + j);
         if (!dm) continue;
         T xj = x[j];
         for (int i = lane; i < nv; i += 32)
@@ -418,7 +454,7 @@ template <class T> __device__ void solve_ldl(const s3_model& m, const T* A, T* x
 }
 
 // dense Cholesky H = L L^T on packed lower (oracle cholesky), then x <- H^-1 x
-template <class T> __device__ void cholesky(int nv, T* H, int lane) {
+template <class T> __device__ __noinline__ void cholesky(int nv, T* H, int lane) {
     for (int k = 0; k < nv; ++k) {
         T d = sqrt(H[tri(k, k)]);
         for (int i = k + 1 + lane; i < nv; i += 32) H[tri(i, k)] = H[tri(i, k)] / d;
@@ -433,7 +469,7 @@ template <class T> __device__ void cholesky(int nv, T* H, int lane) {
     }
 }
 
-template <class T> __device__ void chol_solve(int nv, const T* L, T* x, int lane) {
+template <class T> __device__ __noinline__ void chol_solve(int nv, const T* L, T* x, int lane) {
     for (int i = 0; i < nv; ++i) {
         T xi = x[i] / L[tri(i, i)];
         __syncwarp();
@@ -451,7 +487,7 @@ template <class T> __device__ void chol_solve(int nv, const T* L, T* x, int lane
 }
 
 // y = M x with packed-lower symmetric M
-template <class T> __device__ void sym_mul(int nv, const T* M, const T* x, T* y, int lane) {
+template <class T> __device__ __noinline__ void sym_mul(int nv, const T* M, const T* x, T* y, int lane) {
     for (int i = lane; i < nv; i += 32) {
         T acc = T(0);
         for (int j = 0; j < nv; ++j) acc += (i >= j ? M[tri(i, j)] : M[tri(j, i)]) * x[j];
@@ -461,7 +497,8 @@ template <class T> __device__ void sym_mul(int nv, const T* M, const T* x, T* y,
 }
 
 // mj_comVel + mj_rne (qacc = 0): bias forces
-template <class T> __device__ void rne(const s3_model& m, WS<T>& s, int lane) {
+template <class T> __device__ void __noinline__ rne(const s3_model& m, const s3_layout& L_, T* B_, int lane) {
+    WS<T> s = make_ws(B_, L_);
     if (lane < 6) {
         s.cvel[lane] = T(0);
         s.cacc[lane] = lane < 3 ? T(0) : T(-m.gravity[lane - 3]);
@@ -524,7 +561,8 @@ template <class T> __device__ void rne(const s3_model& m, WS<T>& s, int lane) {
 }
 
 // actuation + passive + smooth force (oracle actuation / forward)
-template <class T> __device__ void smooth_force(const s3_model& m, WS<T>& s, const T* applied, int lane) {
+template <class T> __device__ void __noinline__ smooth_force(const s3_model& m, const s3_layout& L_, T* B_, const T* applied, int lane) {
+    WS<T> s = make_ws(B_, L_);
     for (int i = lane; i < m.nv; i += 32) { s.fcon[i] = T(0); s.kvd[i] = T(0); }
     __syncwarp();
     const T* gain = F<T>(m.act_gain);
@@ -651,8 +689,9 @@ template <class T> __device__ inline void point_of(const s3_model& m, const WS<T
     }
 }
 
-// Narrowphase of one pair; emits up to 4 contacts through `emit(hit)` in the oracle's order.
-template <class T, class Emit> __device__ int narrow(const s3_model& m, const WS<T>& s, int p, Emit emit) {
+// Narrowphase of one pair: up to 4 contacts into `hits`, in the oracle's order.
+template <class T> __device__ __noinline__ int narrow(const s3_model& m, const s3_layout& L_, T* B_, int p, Hit<T>* hits) {
+    WS<T> s = make_ws(B_, L_);
     int g1 = m.pair_geom[2 * p], g2 = m.pair_geom[2 * p + 1];
     int t1 = m.geom_type[g1], t2 = m.geom_type[g2];
     const T* c1 = s.gpos + 3 * g1;
@@ -673,7 +712,7 @@ template <class T, class Emit> __device__ int narrow(const s3_model& m, const WS
                 Hit<T> h;
                 h.d = d;
                 for (int i = 0; i < 3; ++i) { h.n[i] = n[i]; h.pos[i] = q[i] - n[i] * (r + T(0.5) * d); }
-                emit(h);
+                hits[cnt] = h;
                 ++cnt;
             }
         }
@@ -687,7 +726,7 @@ template <class T, class Emit> __device__ int narrow(const s3_model& m, const WS
                 Hit<T> h;
                 h.d = d;
                 for (int i = 0; i < 3; ++i) { h.n[i] = n[i]; h.pos[i] = q[i] - n[i] * (r + T(0.5) * d); }
-                emit(h);
+                hits[cnt] = h;
                 ++cnt;
             }
         }
@@ -724,7 +763,7 @@ template <class T, class Emit> __device__ int narrow(const s3_model& m, const WS
             Hit<T> h;
             h.d = d;
             for (int i = 0; i < 3; ++i) { h.n[i] = n[i]; h.pos[i] = A[i] + n[i] * (r1 + T(0.5) * d); }
-            emit(h);
+            hits[cnt] = h;
             ++cnt;
         }
     }
@@ -744,13 +783,15 @@ template <class T> __device__ inline void make_frame(const T* n, T* fr) {
 }
 
 // broadphase + narrowphase over all pairs, compacted in pair order; returns ncon (warp-uniform)
-template <class T> __device__ int collide(const s3_model& m, WS<T>& s, int lane, int& dropped) {
+template <class T> __device__ int __noinline__ collide(const s3_model& m, const s3_layout& L_, T* B_, int lane, int& dropped) {
+    WS<T> s = make_ws(B_, L_);
     int base = 0;
     dropped = 0;
     const T* fric = F<T>(m.geom_friction);
     for (int p0 = 0; p0 < m.npair; p0 += 32) {
         int p = p0 + lane;
-        int cnt = p < m.npair ? narrow(m, s, p, [](const Hit<T>&) {}) : 0;
+        Hit<T> hits[4];
+        int cnt = p < m.npair ? narrow(m, L_, B_, p, hits) : 0;
         int incl = cnt;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -762,9 +803,10 @@ template <class T> __device__ int collide(const s3_model& m, WS<T>& s, int lane,
         if (cnt) {
             int g1 = m.pair_geom[2 * p], g2 = m.pair_geom[2 * p + 1];
             T mu = fmax(fric[g1], fric[g2]);
-            int slot = off;
-            narrow(m, s, p, [&](const Hit<T>& h) {
+            for (int k = 0; k < cnt; ++k) {
+                int slot = off + k;
                 if (slot < S3_MAX_CON) {
+                    const Hit<T>& h = hits[k];
                     T* c = s.con + kConStride * slot;
                     c[0] = h.d;
                     c[1] = h.pos[0]; c[2] = h.pos[1]; c[3] = h.pos[2];
@@ -772,8 +814,7 @@ template <class T> __device__ int collide(const s3_model& m, WS<T>& s, int lane,
                     c[13] = mu;
                     s.con_pair[slot] = p;
                 }
-                ++slot;
-            });
+            }
         }
         base += total;
     }
@@ -786,6 +827,24 @@ template <class T> __device__ int collide(const s3_model& m, WS<T>& s, int lane,
 }
 
 // ---------------------------------------------------------------- constraints
+
+// U = union of the Jacobian column sets of every contact and every violated limit (warp-uniform)
+template <class T> __device__ __noinline__ uint64_t touched_mask(const s3_model& m, const s3_layout& L_, T* B_, int ncon,
+                                                                 int lane) {
+    WS<T> s = make_ws(B_, L_);
+    const unsigned long long* pm = reinterpret_cast<const unsigned long long*>(m.pair_dofmask);
+    const unsigned long long* cm = reinterpret_cast<const unsigned long long*>(m.dof_chainmask);
+    uint64_t u = 0;
+    for (int c = lane; c < ncon; c += 32) u |= __ldg(pm + s.con_pair[c]);
+    const T* rng = F<T>(m.lim_range);
+    for (int l = lane; l < m.nlimjnt; l += 32) {
+        T q = s.qpos[m.lim_qposadr[l]];
+        if (q - rng[2 * l] < T(0) || rng[2 * l + 1] - q < T(0)) u |= __ldg(cm + m.lim_dofadr[l]);
+    }
+    unsigned lo = __reduce_or_sync(FULL, (unsigned)(u & 0xffffffffu));
+    unsigned hi = __reduce_or_sync(FULL, (unsigned)(u >> 32));
+    return ((uint64_t)hi << 32) | lo;
+}
 
 template <class T> __device__ inline T impedance(const s3_model& m, T r) {
     T dmin = T(m.solimp[0]), dmax = T(m.solimp[1]), width = T(m.solimp[2]), mid = T(m.solimp[3]),
@@ -802,7 +861,8 @@ template <class T> __device__ inline T impedance(const s3_model& m, T r) {
 }
 
 // Contact Jacobians Jc[c][3][stride] (frame rows over the pair's chain), limit rows, aref, D.
-template <class T> __device__ int build_rows(const s3_model& m, WS<T>& s, int ncon, int& nlim, int lane) {
+template <class T> __device__ int __noinline__ build_rows(const s3_model& m, const s3_layout& L_, T* B_, int ncon, int& nlim, int lane) {
+    WS<T> s = make_ws(B_, L_);
     // limits: ballot-compact the violated sides
     const T* rng = F<T>(m.lim_range);
     nlim = 0;
@@ -900,8 +960,9 @@ template <class T> __device__ int build_rows(const s3_model& m, WS<T>& s, int nc
 }
 
 // out[r] = J_r x for all rows
-template <class T> __device__ void rows_mul(const s3_model& m, WS<T>& s, int ncon, int nlim, const T* x, T* out,
+template <class T> __device__ void __noinline__ rows_mul(const s3_model& m, const s3_layout& L_, T* B_, int ncon, int nlim, const T* x, T* out,
                                             int lane) {
+    WS<T> s = make_ws(B_, L_);
     int stride = m.chain_stride;
     for (int t = lane; t < 3 * ncon; t += 32) {
         int c = t / 3, r = t % 3;
@@ -929,8 +990,9 @@ template <class T> __device__ void rows_mul(const s3_model& m, WS<T>& s, int nco
 }
 
 // y += J^T (coef) where coef[r] is per row
-template <class T> __device__ void rows_tmul_add(const s3_model& m, WS<T>& s, int ncon, int nlim, const T* coef, T* y,
+template <class T> __device__ void __noinline__ rows_tmul_add(const s3_model& m, const s3_layout& L_, T* B_, int ncon, int nlim, const T* coef, T* y,
                                                  int lane) {
+    WS<T> s = make_ws(B_, L_);
     int stride = m.chain_stride;
     for (int r = lane; r < nlim; r += 32) y[s.lim_dof[r]] += T(s.lim_sign[r]) * coef[r];
     __syncwarp();
@@ -958,8 +1020,9 @@ template <class T> __device__ void rows_tmul_add(const s3_model& m, WS<T>& s, in
     }
 }
 
-template <class T> __device__ T total_cost(const s3_model& m, WS<T>& s, int nefc, const T* a, const T* Ma,
+template <class T> __device__ T __noinline__ total_cost(const s3_model& m, const s3_layout& L_, T* B_, int nefc, const T* a, const T* Ma,
                                            const T* jar, int lane) {
+    WS<T> s = make_ws(B_, L_);
     T g = T(0);
     for (int i = lane; i < m.nv; i += 32) g += (a[i] - s.a0[i]) * (Ma[i] - s.smooth[i]);
     T c = T(0);
@@ -969,7 +1032,8 @@ template <class T> __device__ T total_cost(const s3_model& m, WS<T>& s, int nefc
 }
 
 // mj_solNewton restated (oracle newton / line_search)
-template <class T> __device__ int newton(const s3_model& m, WS<T>& s, int ncon, int nlim, bool warm_ok, int lane) {
+template <class T> __device__ int __noinline__ newton(const s3_model& m, const s3_layout& L_, T* B_, int ncon, int nlim, bool warm_ok, uint64_t U, int lane) {
+    WS<T> s = make_ws(B_, L_);
     int nv = m.nv;
     int nefc = nlim + 4 * ncon;
     T scale = T(m.scale);
@@ -978,17 +1042,17 @@ template <class T> __device__ int newton(const s3_model& m, WS<T>& s, int ncon, 
     for (int i = lane; i < nv; i += 32) s.a[i] = s.a0[i];
     __syncwarp();
     sym_mul(nv, s.M, s.a, s.Ma, lane);
-    rows_mul(m, s, ncon, nlim, s.a, s.rjar, lane);
+    rows_mul(m, L_, B_, ncon, nlim, s.a, s.rjar, lane);
     for (int r = lane; r < nefc; r += 32) s.rjar[r] -= s.raref[r];
     __syncwarp();
-    T cost = total_cost(m, s, nefc, s.a, s.Ma, s.rjar, lane);
+    T cost = total_cost(m, L_, B_, nefc, s.a, s.Ma, s.rjar, lane);
     if (warm_ok) {
         // candidate: qacc_warmstart staged in s.p; Mw -> s.Mp, jw -> s.rJp
         sym_mul(nv, s.M, s.p, s.Mp, lane);
-        rows_mul(m, s, ncon, nlim, s.p, s.rJp, lane);
+        rows_mul(m, L_, B_, ncon, nlim, s.p, s.rJp, lane);
         for (int r = lane; r < nefc; r += 32) s.rJp[r] -= s.raref[r];
         __syncwarp();
-        T cw = total_cost(m, s, nefc, s.p, s.Mp, s.rJp, lane);
+        T cw = total_cost(m, L_, B_, nefc, s.p, s.Mp, s.rJp, lane);
         if (cw < cost) {
             for (int i = lane; i < nv; i += 32) { s.a[i] = s.p[i]; s.Ma[i] = s.Mp[i]; }
             for (int r = lane; r < nefc; r += 32) s.rjar[r] = s.rJp[r];
@@ -1005,16 +1069,21 @@ template <class T> __device__ int newton(const s3_model& m, WS<T>& s, int ncon, 
         for (int r = lane; r < nefc; r += 32) s.rJp[r] = s.rjar[r] < T(0) ? s.rD[r] * s.rjar[r] : T(0);
         for (int i = lane; i < nv; i += 32) s.grad[i] = s.Ma[i] - s.smooth[i];
         __syncwarp();
-        rows_tmul_add(m, s, ncon, nlim, s.rJp, s.grad, lane);
+        rows_tmul_add(m, L_, B_, ncon, nlim, s.rJp, s.grad, lane);
         T gn = T(0);
         for (int i = lane; i < nv; i += 32) gn += s.grad[i] * s.grad[i];
         gn = wsum(gn);
         if (scale * sqrt(gn) < tol) break;
         ++its;
-        // H = M + J^T diag(D act) J on the packed lower LD buffer
-        int np = nv * (nv + 1) / 2;
-        for (int t = lane; t < np; t += 32) s.LD[t] = s.M[t];
-        __syncwarp();
+        // H = M + J^T diag(D act) J on the packed lower LD buffer: in tree mode only the rows of U are
+        // rebuilt (from the snapshot of M partially eliminated by the untouched subtrees)
+        if (tree) {
+            tree_copy(m, s.LD, s.snap, U, false, lane);
+        } else {
+            int np = nv * (nv + 1) / 2;
+            for (int t = lane; t < np; t += 32) s.LD[t] = s.M[t];
+            __syncwarp();
+        }
         for (int r = lane; r < nlim; r += 32)
             if (s.rjar[r] < T(0)) s.LD[tri(s.lim_dof[r], s.lim_dof[r])] += s.rD[r];
         __syncwarp();
@@ -1055,14 +1124,14 @@ template <class T> __device__ int newton(const s3_model& m, WS<T>& s, int ncon, 
         for (int i = lane; i < nv; i += 32) s.p[i] = -s.grad[i];
         __syncwarp();
         if (tree) {
-            factor_ldl(m, s.LD, s.tk, s.u, lane);
+            factor_ldl(m, s.LD, lane, U, 2);
             solve_ldl(m, s.LD, s.p, lane);
         } else {
             cholesky(nv, s.LD, lane);
             chol_solve(nv, s.LD, s.p, lane);
         }
         sym_mul(nv, s.M, s.p, s.Mp, lane);
-        rows_mul(m, s, ncon, nlim, s.p, s.rJp, lane);
+        rows_mul(m, L_, B_, ncon, nlim, s.p, s.rJp, lane);
         // exact line search along p: bracketed Newton on phi'
         T g0 = T(0), h0 = T(0);
         for (int i = lane; i < nv; i += 32) {
@@ -1107,7 +1176,7 @@ template <class T> __device__ int newton(const s3_model& m, WS<T>& s, int ncon, 
         }
         for (int r = lane; r < nefc; r += 32) s.rjar[r] += alpha * s.rJp[r];
         __syncwarp();
-        T nc = total_cost(m, s, nefc, s.a, s.Ma, s.rjar, lane);
+        T nc = total_cost(m, L_, B_, nefc, s.a, s.Ma, s.rjar, lane);
         T impv = scale * (cost - nc);
         cost = nc;
         if (impv < tol) break;
@@ -1116,47 +1185,53 @@ template <class T> __device__ int newton(const s3_model& m, WS<T>& s, int ncon, 
     for (int r = lane; r < nefc; r += 32) s.rJp[r] = s.rjar[r] < T(0) ? -s.rD[r] * s.rjar[r] : T(0);
     for (int i = lane; i < nv; i += 32) s.fcon[i] = T(0);
     __syncwarp();
-    rows_tmul_add(m, s, ncon, nlim, s.rJp, s.fcon, lane);
+    rows_tmul_add(m, L_, B_, ncon, nlim, s.rJp, s.fcon, lane);
     return its;
 }
 
 // ---------------------------------------------------------------- one physics substep (mj_step)
 
 template <class T>
-__device__ void substep(const s3_model& m, const s3_data& d, WS<T>& s, int64_t w, T* gw, const T* gapp, bool last,
+__device__ __noinline__ void substep(const s3_model& m, const s3_data& d, const s3_layout& L_, T* B_, int64_t w, T* gw, const T* gapp, bool last,
                         int lane) {
+    WS<T> s = make_ws(B_, L_);
     const int nv = m.nv;
     const T dt = T(m.timestep);
     int ncon = 0, nlim = 0, dropped = 0, its = 0;
-    kinematics(m, s, lane);
-    com_pos(m, s, lane);
-    geom_frames(m, s, lane);
-    rne(m, s, lane);
-    crb_mass(m, s, lane);
+    kinematics(m, L_, B_, lane);
+    com_pos(m, L_, B_, lane);
+    geom_frames(m, L_, B_, lane);
+    rne(m, L_, B_, lane);
+    crb_mass(m, L_, B_, lane);
     int np = nv * (nv + 1) / 2;
-    for (int t = lane; t < np; t += 32) s.LD[t] = s.M[t];
-    __syncwarp();
-    factor_ldl(m, s.LD, s.tk, s.u, lane);
-    smooth_force(m, s, gapp, lane);
-    if (last && d.qM) {  // parity outputs of the factor before it is overwritten
+    ncon = collide(m, L_, B_, lane, dropped);
+    uint64_t U = touched_mask(m, L_, B_, ncon, lane);
+    tree_load(m, s.M, s.LD, lane);
+    factor_ldl(m, s.LD, lane, U, 1);          // subtrees no constraint touches: shared by M and H
+    tree_copy(m, s.LD, s.snap, U, true, lane);
+    factor_ldl(m, s.LD, lane, U, 2);
+    smooth_force(m, L_, B_, gapp, lane);
+    if (last && d.qM) {  // parity outputs of the factor before it is overwritten (tree entries; 0 elsewhere)
         T* o = static_cast<T*>(d.qLD) + w * np;
-        for (int t = lane; t < np; t += 32) o[t] = s.LD[t];
+        const unsigned long long* cm = reinterpret_cast<const unsigned long long*>(m.dof_chainmask);
+        for (int i = lane; i < nv; i += 32) {
+            uint64_t mk = __ldg(cm + i);
+            for (int j = 0; j <= i; ++j) o[tri(i, j)] = ((mk >> j) & 1ull) ? s.LD[tri(i, j)] : T(0);
+        }
     }
     solve_ldl(m, s.LD, s.a0, lane);
-    ncon = collide(m, s, lane, dropped);
-    build_rows(m, s, ncon, nlim, lane);
+    build_rows(m, L_, B_, ncon, nlim, lane);
     if (gw) {
         for (int i = lane; i < nv; i += 32) s.p[i] = gw[i];
         __syncwarp();
     }
-    its = newton(m, s, ncon, nlim, gw != nullptr, lane);
+    its = newton(m, L_, B_, ncon, nlim, gw != nullptr, U, lane);
     if (gw) {
         for (int i = lane; i < nv; i += 32) gw[i] = s.a[i];
     }
     // implicitfast: (M + dt diag(damping + kv)) acc = smooth + constraint
     const T* damp = F<T>(m.dof_damping);
-    for (int t = lane; t < np; t += 32) s.LD[t] = s.M[t];
-    __syncwarp();
+    tree_load(m, s.M, s.LD, lane);
     for (int i = lane; i < nv; i += 32) s.LD[tri(i, i)] += dt * (damp[i] + s.kvd[i]);
     for (int i = lane; i < nv; i += 32) s.grad[i] = s.smooth[i] + s.fcon[i];
     __syncwarp();
@@ -1191,7 +1266,8 @@ __device__ void substep(const s3_model& m, const s3_data& d, WS<T>& s, int64_t w
             d.solver_niter[w] = its;
         }
     }
-    factor_ldl(m, s.LD, s.tk, s.u, lane);
+    __syncwarp();
+    factor_ldl(m, s.LD, lane);
     solve_ldl(m, s.LD, s.grad, lane);
     for (int i = lane; i < nv; i += 32) s.qvel[i] += dt * s.grad[i];
     __syncwarp();
@@ -1222,11 +1298,12 @@ __device__ void substep(const s3_model& m, const s3_data& d, WS<T>& s, int64_t w
     if (d.time && lane == 0) static_cast<T*>(d.time)[w] += dt;
 }
 
-template <class T> __device__ void store_geom_frames(const s3_model& m, const s3_data& d, WS<T>& s, int64_t w,
+template <class T> __device__ __noinline__ void store_geom_frames(const s3_model& m, const s3_data& d, const s3_layout& L_, T* B_, int64_t w,
                                                      int lane) {
+    WS<T> s = make_ws(B_, L_);
     // frames at the FINAL state of the launch (what sensors see)
-    kinematics(m, s, lane);
-    geom_frames(m, s, lane);
+    kinematics(m, L_, B_, lane);
+    geom_frames(m, L_, B_, lane);
     for (int g = lane; g < m.ngeom; g += 32) {
         for (int k = 0; k < 3; ++k) static_cast<T*>(d.geom_xpos)[(w * m.ngeom + g) * 3 + k] = s.gpos[3 * g + k];
         for (int k = 0; k < 9; ++k) static_cast<T*>(d.geom_xmat)[(w * m.ngeom + g) * 9 + k] = s.gmat[9 * g + k];
@@ -1245,6 +1322,8 @@ __global__ void __launch_bounds__(32 * 16) step_kernel(const __grid_constant__ s
     if (w >= d.nworld) return;
     T* base = reinterpret_cast<T*>(smem_raw) + (size_t)wib * l.elems_per_world;
     WS<T> s = make_ws(base, l);
+    const s3_layout& L_ = l;
+    T* B_ = base;
     const int nq = m.nq, nv = m.nv, nu = m.nu;
     T* gq = static_cast<T*>(d.qpos) + w * nq;
     T* gv = static_cast<T*>(d.qvel) + w * nv;
@@ -1254,8 +1333,8 @@ __global__ void __launch_bounds__(32 * 16) step_kernel(const __grid_constant__ s
     for (int i = lane; i < nv; i += 32) s.qvel[i] = gv[i];
     for (int i = lane; i < nu; i += 32) s.ctrl[i] = static_cast<const T*>(d.ctrl)[w * nu + i];
     __syncwarp();
-    for (int sub = 0; sub < nsub; ++sub) substep(m, d, s, w, gw, gapp, sub == nsub - 1, lane);
-    if (d.geom_xpos) store_geom_frames(m, d, s, w, lane);
+    for (int sub = 0; sub < nsub; ++sub) substep(m, d, L_, B_, w, gw, gapp, sub == nsub - 1, lane);
+    if (d.geom_xpos) store_geom_frames(m, d, L_, B_, w, lane);
     for (int i = lane; i < nq; i += 32) gq[i] = s.qpos[i];
     for (int i = lane; i < nv; i += 32) gv[i] = s.qvel[i];
 }
@@ -1300,7 +1379,8 @@ template <class T> __device__ inline void base_frame(const T* qpos, const T* qve
 }
 
 template <class T>
-__device__ void task_reset(const s3_model& m, const s3_task& tk, WS<T>& s, int64_t w, uint64_t ctr, int lane) {
+__device__ __noinline__ void task_reset(const s3_model& m, const s3_task& tk, const s3_layout& L_, T* B_, int64_t w, uint64_t ctr, int lane) {
+    WS<T> s = make_ws(B_, L_);
     const T* dq = static_cast<const T*>(tk.default_qpos);
     uint64_t kr = stream_key(tk.seed, tk.world_offset + w, 1);
     for (int i = lane; i < m.nq; i += 32) s.qpos[i] = dq[i];
@@ -1334,8 +1414,9 @@ __device__ void task_resample(const s3_task& tk, T* cmd, int64_t w, uint64_t ctr
 }
 
 template <class T>
-__device__ void task_observe(const s3_model& m, const s3_task& tk, WS<T>& s, int64_t w, uint64_t ctr, const T* cmd,
+__device__ __noinline__ void task_observe(const s3_model& m, const s3_task& tk, const s3_layout& L_, T* B_, int64_t w, uint64_t ctr, const T* cmd,
                              const T* action, int lane) {
+    WS<T> s = make_ws(B_, L_);
     T vb[3], om[3], g[3];
     base_frame(s.qpos, s.qvel, vb, om, g);
     const T* dq = static_cast<const T*>(tk.default_qpos);
@@ -1391,6 +1472,8 @@ __global__ void __launch_bounds__(32 * 16) env_kernel(const __grid_constant__ s3
     if (w >= d.nworld) return;
     T* base = reinterpret_cast<T*>(smem_raw) + (size_t)wib * l.elems_per_world;
     WS<T> s = make_ws(base, l);
+    const s3_layout& L_ = l;
+    T* B_ = base;
     const int nq = m.nq, nv = m.nv, nu = m.nu;
     T* gq = static_cast<T*>(d.qpos) + w * nq;
     T* gv = static_cast<T*>(d.qvel) + w * nv;
@@ -1401,7 +1484,7 @@ __global__ void __launch_bounds__(32 * 16) env_kernel(const __grid_constant__ s3
     const T* dq = static_cast<const T*>(tk.default_qpos);
     uint64_t ctr = (uint64_t)global_step;
     if (mode == 1) {  // reset every world, counter 0
-        task_reset(m, tk, s, w, 0, lane);
+        task_reset(m, tk, L_, B_, w, 0, lane);
         for (int i = lane; i < nv; i += 32) gw[i] = T(0);
         for (int i = lane; i < nu; i += 32) { act[i] = T(0); prev[i] = T(0); }
         task_resample(tk, cmd, w, 0, lane);
@@ -1411,8 +1494,8 @@ __global__ void __launch_bounds__(32 * 16) env_kernel(const __grid_constant__ s3
             static_cast<T*>(tk.episode_return)[w] = T(0);
         }
         __syncwarp();
-        task_observe(m, tk, s, w, 0, cmd, act, lane);
-        if (d.geom_xpos) store_geom_frames(m, d, s, w, lane);
+        task_observe(m, tk, L_, B_, w, 0, cmd, act, lane);
+        if (d.geom_xpos) store_geom_frames(m, d, L_, B_, w, lane);
         for (int i = lane; i < nq; i += 32) gq[i] = s.qpos[i];
         for (int i = lane; i < nv; i += 32) gv[i] = s.qvel[i];
         return;
@@ -1431,7 +1514,7 @@ __global__ void __launch_bounds__(32 * 16) env_kernel(const __grid_constant__ s3
     }
     rate = wsum(rate);
     __syncwarp();
-    for (int sub = 0; sub < tk.decimation; ++sub) substep(m, d, s, w, gw, (const T*)nullptr, false, lane);
+    for (int sub = 0; sub < tk.decimation; ++sub) substep(m, d, L_, B_, w, gw, (const T*)nullptr, false, lane);
     // rewards, terminations (pre-reset state)
     T vb[3], om[3], g[3];
     base_frame(s.qpos, s.qvel, vb, om, g);
@@ -1460,7 +1543,7 @@ __global__ void __launch_bounds__(32 * 16) env_kernel(const __grid_constant__ s3
         tk.episode_step[w] = es;
     }
     if (term || trunc) {  // masked reset (warp-uniform)
-        task_reset(m, tk, s, w, ctr, lane);
+        task_reset(m, tk, L_, B_, w, ctr, lane);
         for (int i = lane; i < nv; i += 32) gw[i] = T(0);
         for (int i = lane; i < nu; i += 32) { act[i] = T(0); prev[i] = T(0); }
         task_resample(tk, cmd, w, ctr, lane);
@@ -1479,8 +1562,8 @@ __global__ void __launch_bounds__(32 * 16) env_kernel(const __grid_constant__ s3
         if (lane == 0) tk.cmd_timer[w] = tm;
     }
     __syncwarp();
-    task_observe(m, tk, s, w, ctr, cmd, act, lane);
-    if (d.geom_xpos) store_geom_frames(m, d, s, w, lane);  // sensors see the post-reset state, like obs
+    task_observe(m, tk, L_, B_, w, ctr, cmd, act, lane);
+    if (d.geom_xpos) store_geom_frames(m, d, L_, B_, w, lane);  // sensors see the post-reset state, like obs
     for (int i = lane; i < nq; i += 32) gq[i] = s.qpos[i];
     for (int i = lane; i < nv; i += 32) gv[i] = s.qvel[i];
 }
@@ -1711,6 +1794,8 @@ int s3_plan(const s3_model* m, int32_t warps_per_block, s3_layout* out) {
     sizes[O_JC] = jc > rne ? jc : rne; sizes[O_RAREF] = S3_MAX_ROWS; sizes[O_RD] = S3_MAX_ROWS;
     sizes[O_RJAR] = S3_MAX_ROWS; sizes[O_RJP] = S3_MAX_ROWS; sizes[O_CDOT] = 3 * S3_MAX_CON; sizes[O_BIAS] = nv;
     sizes[O_FCON] = nv; sizes[O_CTRL] = nu; sizes[O_COM] = 4;
+    int region = sizes[O_XIPOS] + sizes[O_CINERT] + sizes[O_JANC] + sizes[O_JAX];
+    if (region < m->ntree) sizes[O_JAX] += m->ntree - region;  // room for the factorization snapshot
     int esz = m->dtype == S3_F64 ? 8 : 4;
     int ints = S3_MAX_CON + 2 * S3_MAX_LIM + 8;
     sizes[O_INT] = (ints * 4 + esz - 1) / esz;

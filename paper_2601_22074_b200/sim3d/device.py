@@ -81,6 +81,16 @@ class DeviceModel:
                 for j in m.dof_chain[i]:
                     ldl_pair.append((i << 8) | j)
             ldl_ptr.append(len(ldl_pair))
+        ldl_norm = [(k << 8) | i for k in range(m.nv) for i in m.dof_chain[k][:-1]]
+        tree_ent = [(i << 8) | j for i in range(m.nv) for j in m.dof_chain[i]]
+        dof_chainmask = np.zeros(m.nv, dtype=np.uint64)
+        for d in range(m.nv):
+            for a in m.dof_chain[d]:
+                dof_chainmask[d] |= np.uint64(1) << np.uint64(a)
+        pair_dofmask = np.zeros(max(m.npair, 1), dtype=np.uint64)
+        for p, c in enumerate(m.pair_chain):
+            for a in c:
+                pair_dofmask[p] |= np.uint64(1) << np.uint64(a)
         classes, pair_class, pair_tree = {}, [], []
         for p, (g1, g2) in enumerate(m.pair_geom):
             key = tuple(m.pair_chain[p])
@@ -109,6 +119,8 @@ class DeviceModel:
             act_qposadr=np.append(m.actuator_qposadr, 0).astype(np.int32),
             act_kind=np.append(m.actuator_kind, 0).astype(np.int32),
             ldl_ptr=np.array(ldl_ptr, dtype=np.int32), ldl_pair=np.array(ldl_pair + [0], dtype=np.uint16),
+            ldl_norm=np.array(ldl_norm + [0], dtype=np.uint16),
+            tree_ent=np.array(tree_ent, dtype=np.uint16), dof_chainmask=dof_chainmask, pair_dofmask=pair_dofmask,
             pair_class=np.array(pair_class + [0], dtype=np.int32), pair_tree=np.array(pair_tree + [1], dtype=np.int32),
             tri_tab=tri_tab)
         floats = dict(
@@ -146,6 +158,8 @@ class DeviceModel:
         s.nlevel, s.chain_stride, s.terrain_hfield = nlevel, self.chain_stride, m.terrain_is_hfield
         s.hf_nrow, s.hf_ncol = m.hfield_data.shape
         s.iterations, s.ls_iterations = m.opt.iterations, m.opt.ls_iterations
+        s.nldl_norm = len(ldl_norm)
+        s.ntree = len(tree_ent)
         s.timestep = m.opt.timestep
         s.gravity[:] = m.opt.gravity
         s.tolerance, s.ls_tolerance = m.opt.tolerance, m.opt.ls_tolerance

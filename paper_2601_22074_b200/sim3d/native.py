@@ -14,7 +14,7 @@ from .. import native as _n
 
 _HERE = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "sim3d_b200.h")
-LIBRARY = os.path.join(_HERE, "_sim3d_b200.so")
+LIBRARY = os.environ.get("S3_LIBRARY") or os.path.join(_HERE, "_sim3d_b200.so")  # override: A/B of kernel builds
 
 MACROS, _STRUCTS, _ORDER = _n._parse_header(HEADER)
 globals().update({k: v for k, v in MACROS.items() if k.startswith("S3_")})
