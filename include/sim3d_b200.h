@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define S3_ABI_VERSION 5
+#define S3_ABI_VERSION 6
 #define S3_F64 0
 #define S3_F32 1
 
@@ -59,6 +59,8 @@ typedef struct s3_model {
     int32_t ls_iterations;
     int32_t nldl_norm;
     int32_t ntree;
+    int32_t flags; /* bit 0: refactor every dof in each Newton iteration (A/B of the partial refactorization) */
+    int32_t pad1;
     double timestep;
     double gravity[3];
     double tolerance;

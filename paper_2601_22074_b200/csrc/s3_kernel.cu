@@ -1070,10 +1070,15 @@ template <class T> __device__ int __noinline__ newton(const s3_model& m, const s
         for (int i = lane; i < nv; i += 32) s.grad[i] = s.Ma[i] - s.smooth[i];
         __syncwarp();
         rows_tmul_add(m, L_, B_, ncon, nlim, s.rJp, s.grad, lane);
-        T gn = T(0);
-        for (int i = lane; i < nv; i += 32) gn += s.grad[i] * s.grad[i];
+        T gn = T(0), mag = T(0);
+        for (int i = lane; i < nv; i += 32) {
+            gn += s.grad[i] * s.grad[i];
+            if (sizeof(T) == 4) mag += s.Ma[i] * s.Ma[i] + s.smooth[i] * s.smooth[i];
+        }
         gn = wsum(gn);
-        if (scale * sqrt(gn) < tol) break;
+        if (sizeof(T) == 4) mag = wsum(mag);
+        T gfloor = sizeof(T) == 4 ? T(8) * T(1.1920929e-7) * scale * sqrt(mag) : T(0);
+        if (scale * sqrt(gn) < tol + gfloor) break;
         ++its;
         // H = M + J^T diag(D act) J on the packed lower LD buffer: in tree mode only the rows of U are
         // rebuilt (from the snapshot of M partially eliminated by the untouched subtrees)
@@ -1179,7 +1184,10 @@ template <class T> __device__ int __noinline__ newton(const s3_model& m, const s
         T nc = total_cost(m, L_, B_, nefc, s.a, s.Ma, s.rjar, lane);
         T impv = scale * (cost - nc);
         cost = nc;
-        if (impv < tol) break;
+        // float32 build: an improvement below the rounding floor of the cost itself is noise, not
+        // progress (the float64 build keeps the oracle's exact criterion)
+        T floor_ = sizeof(T) == 4 ? T(8) * T(1.1920929e-7) * scale * fabs(nc) : T(0);
+        if (impv < tol + floor_) break;
     }
     // forces and qfrc_constraint
     for (int r = lane; r < nefc; r += 32) s.rJp[r] = s.rjar[r] < T(0) ? -s.rD[r] * s.rjar[r] : T(0);
@@ -1205,7 +1213,7 @@ __device__ __noinline__ void substep(const s3_model& m, const s3_data& d, const 
     crb_mass(m, L_, B_, lane);
     int np = nv * (nv + 1) / 2;
     ncon = collide(m, L_, B_, lane, dropped);
-    uint64_t U = touched_mask(m, L_, B_, ncon, lane);
+    uint64_t U = (m.flags & 1) ? (nv == 64 ? ~0ull : ((1ull << nv) - 1)) : touched_mask(m, L_, B_, ncon, lane);
     tree_load(m, s.M, s.LD, lane);
     factor_ldl(m, s.LD, lane, U, 1);          // subtrees no constraint touches: shared by M and H
     tree_copy(m, s.LD, s.snap, U, true, lane);

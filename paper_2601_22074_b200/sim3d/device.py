@@ -14,6 +14,7 @@ built extension nothing runs.
 from __future__ import annotations
 
 import ctypes
+import os
 
 import numpy as np
 import torch
@@ -160,6 +161,9 @@ class DeviceModel:
         s.iterations, s.ls_iterations = m.opt.iterations, m.opt.ls_iterations
         s.nldl_norm = len(ldl_norm)
         s.ntree = len(tree_ent)
+        # partial Newton refactorization: a measured win in float64 (latency-bound, 5-6 warps/SM) and a
+        # measured loss in float32 (12 warps/SM, issue-bound) -- tools/ab_sim3d.sh; S3_FLAGS overrides
+        s.flags = int(os.environ.get("S3_FLAGS", "1" if dtype == "f32" else "0"))
         s.timestep = m.opt.timestep
         s.gravity[:] = m.opt.gravity
         s.tolerance, s.ls_tolerance = m.opt.tolerance, m.opt.ls_tolerance
