@@ -661,6 +661,20 @@ int ss_env_step_jit_packed(void* handle, const ss_env_desc* desc, const void* pa
 int ss_rt_launch(const ss_env_desc* desc, ss_rt_state* st, const ss_launch* l, void* jit, void* stream);
 int ss_rt_poll(ss_rt_state* st, int32_t keep, int32_t* out_slots, int32_t max_out);
 int ss_rt_release(ss_rt_state* st);
+
+/* Pipelined host I/O for env.step_async / env.step_wait (gym VectorEnv style), nslot in [2, 4] slots:
+ * ss_pipe_pre copies a step's actions from pinned host memory into the slot's device buffer on a
+ * copy stream (the launching stream waits for it) and returns the slot; ss_pipe_post snapshots the
+ * output arena into the slot's staging buffer (SM copy kernel) and copies it to the slot's pinned
+ * host block on a second copy stream, so the PCIe transfers of one step overlap the kernel of the
+ * next; ss_pipe_wait blocks until the oldest pending step's results are in host memory and returns
+ * its slot. Buffers are owned by the caller (16-byte aligned). */
+int ss_pipe_create(int32_t nslot, void* const* dev_actions, void* const* stage, void* const* host,
+                   int64_t action_bytes, int64_t arena_bytes, void** out);
+int ss_pipe_destroy(void* pipe);
+int ss_pipe_pre(void* pipe, const void* host_actions, void* main_stream);
+int ss_pipe_post(void* pipe, const void* arena, void* main_stream);
+int ss_pipe_wait(void* pipe);
 int ss_actuator_eval(int32_t kind, const double* kp, const double* kd, double effort,
                      double saturation, double vel_limit, const double* q_des,
                      const double* q, const double* qd, double* out, int64_t n,

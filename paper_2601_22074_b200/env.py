@@ -45,6 +45,8 @@ from .terrain import generate_grid
 
 __all__ = ["EnvCfg", "SceneCfg", "InitStateCfg", "ManagerBasedRlEnv", "load_capture"]
 
+# steps that may be in flight between step_async and step_wait (ss_pipe, 2..4; SS_PIPE_SLOTS overrides for A/B)
+PIPE_SLOTS = int(os.environ.get("SS_PIPE_SLOTS", "4"))
 NF_LAG = 4  # control steps the host may run ahead before it must look at nonfinite flags
 
 _SIM = native.SS_ST_APPLY | native.SS_ST_PUSH | native.SS_ST_PHYS | native.SS_ST_SENSOR
@@ -249,6 +251,8 @@ class ManagerBasedRlEnv:
     def __del__(self):
         try:
             self._lib.ss_rt_release(self._rt_ref)
+            if getattr(self, "_pipe", None) is not None:
+                self._lib.ss_pipe_destroy(self._pipe["h"])
         except Exception:
             pass
 
@@ -497,7 +501,13 @@ class ManagerBasedRlEnv:
 
         Returns (obs groups, reward, terminated, truncated, extras); all device
         tensors, valid until the next step."""
-        a = self.action_manager.check_actions(actions)
+        self._step_checked(self.action_manager.check_actions(actions))
+        tm = self.termination_manager
+        return (self.observation_manager.outputs(), self.reward_manager.reward, tm.terminated, tm.truncated,
+                _Extras(self, self.global_step))
+
+    def _step_checked(self, a) -> None:
+        """The control step on already-validated actions (step / step_async)."""
         if not self._startup_done:
             self.event_manager.prepare_fields()
         self.global_step += 1
@@ -510,8 +520,69 @@ class ManagerBasedRlEnv:
         else:
             self._step_staged(a)
         self.ray_scanner._cached_step = -1
-        tm = self.termination_manager
-        return om.outputs(), self.reward_manager.reward, tm.terminated, tm.truncated, _Extras(self, self.global_step)
+
+    # -- pipelined host I/O (gym VectorEnv step_async / step_wait) -------------------------------
+
+    def step_async(self, actions) -> None:
+        """Enqueue one control step fed from, and delivered to, pinned host memory.
+
+        gym VectorEnv-style ``step_async`` / ``step_wait``. The native pipe
+        (``ss_pipe_*``, csrc/ss_runtime.cu) copies the step's actions
+        host->device on one copy-engine stream, runs the step exactly like
+        ``step`` on the device copy, snapshots the output arena with an SM copy
+        kernel into one of two staging buffers, and copies it to one of two
+        pinned host blocks on a second copy-engine stream -- so the PCIe
+        traffic of step i overlaps the kernels of the steps after it.
+        ``step_wait()`` blocks until the oldest pending step's results are in
+        host memory and returns its host views (obs groups, reward,
+        terminated, truncated), valid until ``step_async`` has been called
+        ``PIPE_SLOTS`` more times. At most ``PIPE_SLOTS`` steps may be pending;
+        with three, the host enqueues step i+1 while steps i-1 and i are in
+        flight, hiding its own per-step cost."""
+        import torch
+
+        if getattr(self, "_host_mirror", None) is not None:
+            raise RuntimeError("step_async uses device outputs + copy-engine transfers; do not enable_host_outputs")
+        P = getattr(self, "_pipe", None)
+        if P is None:
+            A = self.action_manager.total_dim
+            nb = self.step_outputs.numel()
+            S = PIPE_SLOTS
+            dev_actions = [torch.empty((self.num_envs, A), dtype=torch.float64, device=self.device) for _ in range(S)]
+            stage = [torch.empty(nb, dtype=torch.uint8, device=self.device) for _ in range(S)]
+            host = [torch.empty(nb, dtype=torch.uint8).pin_memory() for _ in range(S)]
+            arr = lambda ts: (ctypes.c_void_p * S)(*[t.data_ptr() for t in ts])  # noqa: E731
+            h = ctypes.c_void_p()
+            rc = self._lib.ss_pipe_create(S, arr(dev_actions), arr(stage), arr(host), self.num_envs * A * 8, nb,
+                                          ctypes.byref(h))
+            if rc != 0:
+                raise native.NativeError(f"ss_pipe_create failed: {self._lib.ss_last_error().decode()}")
+            P = self._pipe = dict(h=h, dev_actions=dev_actions, stage=stage, host=host, pinned=set(),
+                                  views=[self.unpack_outputs(x) for x in host])
+        if (actions.__class__ is not torch.Tensor or actions.dtype is not torch.float64 or actions.is_cuda
+                or not actions.is_contiguous() or actions.shape != P["dev_actions"][0].shape):
+            raise ValueError(f"step_async takes a contiguous pinned float64 host tensor of shape "
+                             f"{tuple(P['dev_actions'][0].shape)}")
+        sp = actions.untyped_storage().data_ptr()
+        if sp not in P["pinned"]:  # pinnedness is a property of the storage: check each storage once
+            if not actions.is_pinned():
+                raise ValueError("step_async takes PINNED host actions (tensor.pin_memory())")
+            P["pinned"].add(sp)
+        stream = native.current_stream(self._dev_index)
+        k = self._lib.ss_pipe_pre(P["h"], actions.data_ptr(), stream)
+        if k < 0:
+            raise RuntimeError(self._lib.ss_last_error().decode())
+        self._step_checked(P["dev_actions"][k])
+        if self._lib.ss_pipe_post(P["h"], self.step_outputs.data_ptr(), stream) < 0:
+            raise native.NativeError(self._lib.ss_last_error().decode())
+
+    def step_wait(self) -> dict:
+        """Host views (obs groups, reward, terminated, truncated) of the oldest step_async step."""
+        P = getattr(self, "_pipe", None)
+        k = -1 if P is None else self._lib.ss_pipe_wait(P["h"])
+        if k < 0:
+            raise RuntimeError("no pending step_async step")
+        return P["views"][k]
 
     def _step_staged(self, a) -> None:
         import torch

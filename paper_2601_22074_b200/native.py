@@ -184,6 +184,12 @@ _SIGNATURES = {
     "ss_rt_launch": ([ctypes.c_void_p] * 5, ctypes.c_int),
     "ss_rt_poll": ([ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_int32], ctypes.c_int),
     "ss_rt_release": ([ctypes.c_void_p], ctypes.c_int),
+    "ss_pipe_create": ([ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                        ctypes.c_int64, ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
+    "ss_pipe_destroy": ([ctypes.c_void_p], ctypes.c_int),
+    "ss_pipe_pre": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
+    "ss_pipe_post": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
+    "ss_pipe_wait": ([ctypes.c_void_p], ctypes.c_int),
     "ss_actuator_eval": (
         [ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double, ctypes.c_double, ctypes.c_double,
          ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p],

@@ -789,3 +789,35 @@ def test_host_io_zero_copy_equals_device_path(generic):
         assert torch.equal(xa.cpu(), host["truncated"])
     assert torch.equal(a.state.q, b.state.q)
     assert torch.equal(a.step_outputs, b.step_outputs)
+
+
+@pytest.mark.gpu
+def test_step_async_delivers_each_steps_results_to_host():
+    """Pipelined host I/O (step_async / step_wait: D2D snapshot + copy-engine D2H overlapping the
+    next step) returns, for every step, the same bits as a synchronous step."""
+    from paper_2601_22074_b200.env import ManagerBasedRlEnv
+    from paper_2601_22074_b200.tasks import make_env_cfg
+
+    a = ManagerBasedRlEnv(make_env_cfg("Velocity-Rough", num_envs=300, seed=6))
+    b = ManagerBasedRlEnv(make_env_cfg("Velocity-Rough", num_envs=300, seed=6))
+    a.reset()
+    b.reset()
+    rng = np.random.default_rng(4)
+    acts = [torch.from_numpy(rng.uniform(-1, 1, size=(300, a.action_manager.total_dim))).pin_memory()
+            for _ in range(12)]
+    expected = []
+    for i, x in enumerate(acts):
+        oa, ra, ta, xa, _ = a.step(x.cuda())
+        expected.append(({g: oa[g].cpu().clone() for g in oa}, ra.cpu().clone(), ta.cpu().clone(), xa.cpu().clone()))
+        b.step_async(x)
+        if i >= 2:  # up to three steps in flight
+            got = b.step_wait()
+            eo, er, et, ex = expected[i - 2]
+            for g in eo:
+                assert torch.equal(eo[g], got[f"obs/{g}"]), (i, g)
+            assert torch.equal(er, got["reward"]) and torch.equal(et, got["terminated"])
+            assert torch.equal(ex, got["truncated"])
+    assert torch.equal(expected[-2][1], b.step_wait()["reward"])
+    assert torch.equal(expected[-1][1], b.step_wait()["reward"])
+    with pytest.raises(RuntimeError):
+        b.step_wait()
