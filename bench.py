@@ -404,10 +404,11 @@ def run_ours(args):
         env.step_async(host_actions[i])
         if i >= PIPE_SLOTS - 1:
             checksum += float(env.step_wait()["reward"][0])
+    host_views = None
     for _ in range(min(PIPE_SLOTS - 1, e2e_steps)):
         host_views = env.step_wait()
     e2e_t = allmax(time.perf_counter() - t0, world)
-    assert host_views["reward"].shape == (n,) and host_views["reward"].device.type == "cpu"
+    assert host_views is None or (host_views["reward"].shape == (n,) and host_views["reward"].device.type == "cpu")
     e2e = None if not e2e_steps else {"value": n * world * e2e_steps / e2e_t, "unit": UNIT, "steps": e2e_steps, "h2d_bytes_per_step": n * A * 8,
            "d2h_bytes_per_step": int(env.step_outputs.numel()),
            "path": "pinned host actions -> env.step_async (kernel reads them over PCIe; output arena snapshotted "

@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define S3_ABI_VERSION 6
+#define S3_ABI_VERSION 7
 #define S3_F64 0
 #define S3_F32 1
 
@@ -59,7 +59,11 @@ typedef struct s3_model {
     int32_t ls_iterations;
     int32_t nldl_norm;
     int32_t ntree;
-    int32_t flags; /* bit 0: refactor every dof in each Newton iteration (A/B of the partial refactorization) */
+    int32_t flags; /* bit 0: refactor every dof in each Newton iteration (A/B of the partial refactorization);
+                      bit 1: tree-level schedule of the factorization / solves instead of one dof per step
+                      (measured slower; kept for A/B) */
+    int32_t nhlev;
+    int32_t ndlev;
     int32_t pad1;
     double timestep;
     double gravity[3];
@@ -136,6 +140,20 @@ typedef struct s3_model {
     const uint16_t* tree_ent;
     const uint64_t* dof_chainmask;
     const uint64_t* pair_dofmask;
+    /* level schedules: per height level the factorization's (i, j) entries (fl_ent = i << 8 | j) with
+     * the eliminated dofs k contributing to each (fl_k, CSR by fl_kptr), and the leaf-to-root solve's
+     * target ancestors (bl_ent) with their contributing dofs (bl_i, CSR by bl_iptr); per depth level
+     * the dofs of the root-to-leaf solve (fw_dof, CSR by fw_ptr) */
+    const int32_t* fl_ptr;
+    const uint16_t* fl_ent;
+    const int32_t* fl_kptr;
+    const uint8_t* fl_k;
+    const int32_t* bl_ptr;
+    const uint8_t* bl_ent;
+    const int32_t* bl_iptr;
+    const uint8_t* bl_i;
+    const int32_t* fw_ptr;
+    const uint8_t* fw_dof;
     const int32_t* pair_class;
     const int32_t* pair_tree;
     const uint16_t* tri_tab;

@@ -380,7 +380,45 @@ template <class T> __device__ void __noinline__ crb_mass(const s3_model& m, cons
 // U (0: all): subtrees outside U eliminate identically for M and for H = M + J^T D J when every
 // constraint row lives on U, so Newton refactors only U (eliminations of disjoint subtrees commute).
 template <class T>
-__device__ __noinline__ void factor_ldl(const s3_model& m, T* A, int lane, uint64_t U = 0, int sel = 0) {
+__device__ __noinline__ void factor_ldl(const s3_model& m, T* A, T* rk, int lane, uint64_t U = 0, int sel = 0) {
+    if (m.flags & 2) {
+        // level schedule (opt-in, flags bit 1; measured SLOWER than the sequential sweep below -- 6.6 vs
+        // 5.2 ms f32, 11.1 vs 8.0 ms f64 per G1 control step -- because each entry chains three dependent
+        // table loads that miss the small L1 left beside 224 KB of shared memory): every dof of one height
+        // level eliminates in the same step (none is an ancestor of another, and their Schur updates to
+        // shared ancestor entries add); one barrier per level.
+        // rk[k] = 1 / D[k]: set for every dof up front (final for leaves) and refreshed by the lane that
+        // applies the last update of A[k][k] (level height(k) - 1), so no division per contribution.
+        for (int k = lane; k < m.nv; k += 32) rk[k] = T(1) / A[tri(k, k)];
+        __syncwarp();
+        for (int L = 0; L < m.nhlev; ++L) {
+            const int e0 = __ldg(m.fl_ptr + L), e1 = __ldg(m.fl_ptr + L + 1);
+            for (int e = e0 + lane; e < e1; e += 32) {
+                const int pr = __ldg(m.fl_ent + e);
+                const int i = pr >> 8, j = pr & 255;
+                const int c0 = __ldg(m.fl_kptr + e), c1 = __ldg(m.fl_kptr + e + 1);
+                T acc = T(0);
+                for (int c = c0; c < c1; ++c) {
+                    const int k = __ldg(m.fl_k + c);
+                    if (sel && (int)((U >> k) & 1ull) != (sel == 2)) continue;
+                    const int rkb = tri(k, 0);
+                    acc += (A[rkb + i] * rk[k]) * A[rkb + j];
+                }
+                const T v = A[tri(i, j)] - acc;
+                A[tri(i, j)] = v;
+                if (i == j) rk[i] = T(1) / v;
+            }
+            __syncwarp();
+        }
+        for (int t = lane; t < m.nldl_norm; t += 32) {
+            int pr = __ldg(m.ldl_norm + t);
+            int k = pr >> 8, i = pr & 255;
+            if (sel && (int)((U >> k) & 1ull) != (sel == 2)) continue;
+            A[tri(k, i)] = A[tri(k, i)] / A[tri(k, k)];
+        }
+        __syncwarp();
+        return;
+    }
     for (int k = m.nv - 1; k >= 0; --k) {
         if (sel && (int)((U >> k) & 1ull) != (sel == 2)) continue;
         int p0 = __ldg(m.ldl_ptr + k), p1 = __ldg(m.ldl_ptr + k + 1);
@@ -429,6 +467,41 @@ template <class T> __device__ __noinline__ void tree_load(const s3_model& m, con
 // x <- M^-1 x with the L^T D L factor (oracle solve_ldl; column-oriented forward pass)
 template <class T> __device__ __noinline__ void solve_ldl(const s3_model& m, const T* A, T* x, int lane) {
     int nv = m.nv;
+    if (m.flags & 2) {
+        // leaf-to-root sweep by height levels: each target ancestor gathers the contributions of the
+        // level's dofs (their values are final: all their descendants sit in lower levels)
+        for (int L = 0; L < m.nhlev; ++L) {
+            const int e0 = __ldg(m.bl_ptr + L), e1 = __ldg(m.bl_ptr + L + 1);
+            for (int e = e0 + lane; e < e1; e += 32) {
+                const int j = __ldg(m.bl_ent + e);
+                const int c0 = __ldg(m.bl_iptr + e), c1 = __ldg(m.bl_iptr + e + 1);
+                T acc = T(0);
+                for (int c = c0; c < c1; ++c) {
+                    const int i = __ldg(m.bl_i + c);
+                    acc += A[tri(i, j)] * x[i];
+                }
+                x[j] -= acc;
+            }
+            __syncwarp();
+        }
+        for (int i = lane; i < nv; i += 32) x[i] = x[i] / A[tri(i, i)];
+        __syncwarp();
+        // root-to-leaf sweep by depth levels: each dof gathers over its (final) ancestors
+        for (int L = 1; L < m.ndlev; ++L) {
+            const int d0 = __ldg(m.fw_ptr + L), d1 = __ldg(m.fw_ptr + L + 1);
+            for (int t = d0 + lane; t < d1; t += 32) {
+                const int i = __ldg(m.fw_dof + t);
+                const int len = __ldg(m.dof_chainlen + i) - 1;
+                const uint8_t* ch = m.dof_chain + i * S3_MAX_CHAIN;
+                const int rb = tri(i, 0);
+                T acc = T(0);
+                for (int a = 0; a < len; ++a) acc += A[rb + __ldg(ch + a)] * x[__ldg(ch + a)];
+                x[i] -= acc;
+            }
+            __syncwarp();
+        }
+        return;
+    }
     for (int i = nv - 1; i >= 0; --i) {
         int len = __ldg(m.dof_chainlen + i) - 1;
         if (len <= 0) continue;
@@ -1129,7 +1202,7 @@ template <class T> __device__ int __noinline__ newton(const s3_model& m, const s
         for (int i = lane; i < nv; i += 32) s.p[i] = -s.grad[i];
         __syncwarp();
         if (tree) {
-            factor_ldl(m, s.LD, lane, U, 2);
+            factor_ldl(m, s.LD, s.tk, lane, U, 2);
             solve_ldl(m, s.LD, s.p, lane);
         } else {
             cholesky(nv, s.LD, lane);
@@ -1215,9 +1288,9 @@ __device__ __noinline__ void substep(const s3_model& m, const s3_data& d, const 
     ncon = collide(m, L_, B_, lane, dropped);
     uint64_t U = (m.flags & 1) ? (nv == 64 ? ~0ull : ((1ull << nv) - 1)) : touched_mask(m, L_, B_, ncon, lane);
     tree_load(m, s.M, s.LD, lane);
-    factor_ldl(m, s.LD, lane, U, 1);          // subtrees no constraint touches: shared by M and H
+    factor_ldl(m, s.LD, s.tk, lane, U, 1);          // subtrees no constraint touches: shared by M and H
     tree_copy(m, s.LD, s.snap, U, true, lane);
-    factor_ldl(m, s.LD, lane, U, 2);
+    factor_ldl(m, s.LD, s.tk, lane, U, 2);
     smooth_force(m, L_, B_, gapp, lane);
     if (last && d.qM) {  // parity outputs of the factor before it is overwritten (tree entries; 0 elsewhere)
         T* o = static_cast<T*>(d.qLD) + w * np;
@@ -1275,7 +1348,7 @@ __device__ __noinline__ void substep(const s3_model& m, const s3_data& d, const 
         }
     }
     __syncwarp();
-    factor_ldl(m, s.LD, lane);
+    factor_ldl(m, s.LD, s.tk, lane);
     solve_ldl(m, s.LD, s.grad, lane);
     for (int i = lane; i < nv; i += 32) s.qvel[i] += dt * s.grad[i];
     __syncwarp();

@@ -84,6 +84,42 @@ class DeviceModel:
             ldl_ptr.append(len(ldl_pair))
         ldl_norm = [(k << 8) | i for k in range(m.nv) for i in m.dof_chain[k][:-1]]
         tree_ent = [(i << 8) | j for i in range(m.nv) for j in m.dof_chain[i]]
+        # level schedules of the tree factorization / solves: dofs of equal height (distance to the
+        # deepest leaf below) eliminate together; equal depth for the root-to-leaf sweep
+        kids = [[] for _ in range(m.nv)]
+        for d in range(m.nv):
+            if m.dof_parentid[d] >= 0:
+                kids[m.dof_parentid[d]].append(d)
+        height = [0] * m.nv
+        for d in range(m.nv - 1, -1, -1):
+            height[d] = 1 + max(height[c] for c in kids[d]) if kids[d] else 0
+        nh = max(height) + 1 if m.nv else 0
+        hlev = [[d for d in range(m.nv) if height[d] == L] for L in range(nh)]
+        dlev = [[d for d in range(m.nv) if len(m.dof_chain[d]) - 1 == L]
+                for L in range(max(len(c) for c in m.dof_chain))]
+        fl_ptr, fl_ent, fl_kptr, fl_k = [0], [], [0], []
+        bl_ptr, bl_ent, bl_iptr, bl_i = [0], [], [0], []
+        for lev in hlev:
+            ent, tgt = {}, {}
+            for k in lev:
+                for i in m.dof_chain[k][:-1]:
+                    tgt.setdefault(i, []).append(k)
+                    for j in m.dof_chain[i]:
+                        ent.setdefault((i, j), []).append(k)
+            for (i, j), ks in sorted(ent.items()):
+                fl_ent.append((i << 8) | j)
+                fl_k += ks
+                fl_kptr.append(len(fl_k))
+            fl_ptr.append(len(fl_ent))
+            for j, srcs in sorted(tgt.items()):
+                bl_ent.append(j)
+                bl_i += srcs
+                bl_iptr.append(len(bl_i))
+            bl_ptr.append(len(bl_ent))
+        fw_ptr, fw_dof = [0], []
+        for lev in dlev:
+            fw_dof += lev
+            fw_ptr.append(len(fw_dof))
         dof_chainmask = np.zeros(m.nv, dtype=np.uint64)
         for d in range(m.nv):
             for a in m.dof_chain[d]:
@@ -122,6 +158,11 @@ class DeviceModel:
             ldl_ptr=np.array(ldl_ptr, dtype=np.int32), ldl_pair=np.array(ldl_pair + [0], dtype=np.uint16),
             ldl_norm=np.array(ldl_norm + [0], dtype=np.uint16),
             tree_ent=np.array(tree_ent, dtype=np.uint16), dof_chainmask=dof_chainmask, pair_dofmask=pair_dofmask,
+            fl_ptr=np.array(fl_ptr, dtype=np.int32), fl_ent=np.array(fl_ent + [0], dtype=np.uint16),
+            fl_kptr=np.array(fl_kptr, dtype=np.int32), fl_k=np.array(fl_k + [0], dtype=np.uint8),
+            bl_ptr=np.array(bl_ptr, dtype=np.int32), bl_ent=np.array(bl_ent + [0], dtype=np.uint8),
+            bl_iptr=np.array(bl_iptr, dtype=np.int32), bl_i=np.array(bl_i + [0], dtype=np.uint8),
+            fw_ptr=np.array(fw_ptr, dtype=np.int32), fw_dof=np.array(fw_dof + [0], dtype=np.uint8),
             pair_class=np.array(pair_class + [0], dtype=np.int32), pair_tree=np.array(pair_tree + [1], dtype=np.int32),
             tri_tab=tri_tab)
         floats = dict(
@@ -161,6 +202,7 @@ class DeviceModel:
         s.iterations, s.ls_iterations = m.opt.iterations, m.opt.ls_iterations
         s.nldl_norm = len(ldl_norm)
         s.ntree = len(tree_ent)
+        s.nhlev, s.ndlev = len(hlev), len(dlev)
         # partial Newton refactorization: a measured win in float64 (latency-bound, 5-6 warps/SM) and a
         # measured loss in float32 (12 warps/SM, issue-bound) -- tools/ab_sim3d.sh; S3_FLAGS overrides
         s.flags = int(os.environ.get("S3_FLAGS", "1" if dtype == "f32" else "0"))
