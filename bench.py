@@ -304,6 +304,30 @@ def sim3d_leg(args, flush, stream) -> dict:
                       "smem_bytes_per_world": env.dm.layout.elems_per_world * (4 if dtype == "f32" else 8),
                       "terminated_frac_last": float(env.terminated.float().mean().item())}
         del env
+    # BASELINE configs[2]: BeyondMimic-style motion imitation (reference-motion command), 8192 worlds/GPU
+    from paper_2601_22074_b200.sim3d.motion import synthetic_walk_clip
+    from paper_2601_22074_b200.sim3d.task import MotionTrackingCfg
+
+    nm = 2 * n
+    out["motion"] = {"workload": f"G1-like 3-D motion imitation (BeyondMimic-style reference-motion command, synthetic "
+                                 f"10 s walking clip, RSI), flat, {nm} worlds/GPU, decimation 4"}
+    for dtype in ("f32", "f64"):
+        m = robots.g1_like(seed=args.seed)
+        dq = robots.default_qpos(m, robots.G1_DEFAULT_JOINTS)
+        Q, V, fdt = synthetic_walk_clip(m, dq)
+        cfg = MotionTrackingCfg(default_qpos=dq, motion_qpos=Q, motion_qvel=V, motion_dt=fdt)
+        env = VelocityEnv3D(m, cfg, nm, seed=args.seed, world_offset=int(os.environ.get("RANK", "0")) * nm,
+                            dtype=dtype)
+        env.reset()
+        steps = 10
+        g = torch.Generator(device="cuda")
+        g.manual_seed(args.seed + 1)
+        acts = torch.rand(steps + 3, nm, m.nu, generator=g, device="cuda", dtype=env.dm.tdtype) * 2 - 1
+        for i in range(3):
+            env.step(acts[i])
+        t = timed_steps(env, steps, flush, stream, lambda i: acts[3 + i])
+        out["motion"][dtype] = {"value": nm * steps / t, "ms_per_step": 1e3 * t / steps}
+        del env
     out["kernel"] = "s3::env_kernel (warp per world, shared-memory resident; one launch per control step)"
     out["parity"] = "oracle/sim3d.py (tests/test_gpu_sim3d*.py); unpinned w.r.t. the reference (no 3-D engine)"
     if not args.no_cpu:
@@ -418,9 +442,10 @@ def run_ours(args):
     scale = at_scale(args, flush, stream) if (world == 1 and args.scale_envs > 0) else None
     s3 = None if args.no_sim3d else sim3d_leg(args, flush, stream)
     if s3 is not None:
-        for k in ("f32", "f64"):
-            s3[k]["value"] = s3[k]["value"] * world  # whole job: every rank steps its own shard (weak scaling)
-            s3[k]["ms_per_step"] = allmax(s3[k]["ms_per_step"], world)
+        for blk in (s3, s3["motion"]):
+            for k in ("f32", "f64"):
+                blk[k]["value"] = blk[k]["value"] * world  # whole job: every rank steps its shard (weak scaling)
+                blk[k]["ms_per_step"] = allmax(blk[k]["ms_per_step"], world)
 
     if rank == 0:
         cpu = None

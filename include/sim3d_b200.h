@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define S3_ABI_VERSION 7
+#define S3_ABI_VERSION 8
 #define S3_F64 0
 #define S3_F32 1
 
@@ -206,11 +206,13 @@ typedef struct s3_layout {
 /* Fused velocity-tracking task (paper_2601_22074_b200/sim3d/task.py): configuration + per-world
  * task state (device pointers, `dtype` elements unless noted). */
 typedef struct s3_task {
+    int32_t kind; /* 0 velocity tracking, 1 motion imitation (reference-motion command) */
     int32_t decimation;
     int32_t episode_steps;
     int32_t cmd_resample_steps;
     int32_t obs_dim;
     int32_t nscan;
+    int32_t nframes;
     int32_t pad0;
     uint64_t seed;
     int64_t world_offset;
@@ -228,6 +230,13 @@ typedef struct s3_task {
     double scan_xy[256];
     double scan_offset;
     double scan_noise;
+    double frame_dt;
+    double motion_sigmas[4];
+    double max_height_error;
+    double max_ori_error;
+    double motion_start_frac;
+    const void* motion_qpos; /* (nframes, nq) */
+    const void* motion_qvel; /* (nframes, nv) */
     const void* default_qpos;
     void* action;
     void* prev_action;
@@ -255,7 +264,7 @@ int s3_plan(const s3_model* m, int32_t warps_per_block, s3_layout* out);
  * env.py:228-233 of the reference; mjwarp.step in mjlab). */
 int s3_step(const s3_model* m, const s3_data* d, const s3_layout* l, int32_t nsub, void* stream);
 
-/* One control step of the fused velocity task (mode 0): ActionManager.process -> decimation x
+/* One control step of the fused task (mode 0; kind velocity or motion): ActionManager.process -> decimation x
  * substep -> terminations -> rewards -> masked reset + command resample -> command countdown ->
  * observations, every world in ONE launch (env.py:219-259 of the reference, on the 3-D model).
  * mode 1 resets every world (counter 0 draws) and writes the first observation; actions unused. */

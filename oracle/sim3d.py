@@ -968,3 +968,144 @@ def camera_rays(K, cam_geom, width, height, fovy, offset=np.zeros(3)):
             dl = dl / np.sqrt(dl @ dl)
             dirs[i, j] = R @ dl
     return o, dirs
+
+
+# ----------------------------------------------------------------------------- motion imitation task (3-D)
+# The fused task of paper_2601_22074_b200/sim3d/task.py with kind = motion (BeyondMimic-style): a
+# reference-motion command (per-world motion time + spawn anchor), reference state initialisation,
+# exp-kernel tracking rewards, deviation terminations, end-of-clip truncation.
+
+
+def qconj(q):
+    return np.array([q[0], -q[1], -q[2], -q[3]])
+
+
+def quat_rotvec(q):
+    """Rotation vector of a unit quaternion (shortest arc)."""
+    if q[0] < 0.0:
+        q = -q
+    s = np.sqrt(q[1] * q[1] + q[2] * q[2] + q[3] * q[3])
+    if s < 1e-12:
+        return 2.0 * q[1:4]
+    ang = 2.0 * np.arctan2(s, q[0])
+    return q[1:4] * (ang / s)
+
+
+def motion_ref(cfg, t):
+    """Reference qpos / qvel at motion time t (linear; quaternion nlerp with sign alignment)."""
+    Q, V, fdt = cfg.motion_qpos, cfg.motion_qvel, cfg.motion_dt
+    F = Q.shape[0]
+    f = t / fdt
+    i0 = int(np.floor(f))
+    i0 = min(max(i0, 0), F - 2)
+    a = f - i0
+    q = (1.0 - a) * Q[i0] + a * Q[i0 + 1]
+    q0, q1 = Q[i0, 3:7], Q[i0 + 1, 3:7]
+    if q0 @ q1 < 0.0:
+        q1 = -q1
+    qq = (1.0 - a) * q0 + a * q1
+    q[3:7] = qq / np.sqrt(qq @ qq)
+    v = (1.0 - a) * V[i0] + a * V[i0 + 1]
+    return q, v
+
+
+class MotionTaskOracle(TaskOracle):
+    """Per-world numpy restatement of the motion-imitation kind of the fused 3-D task.
+    cmd[w] = (motion time, anchor x, anchor y)."""
+
+    def clip_end(self):
+        return (self.cfg.motion_qpos.shape[0] - 1) * self.cfg.motion_dt
+
+    def reset_world(self, w, ctr):
+        m, cfg = self.m, self.cfg
+        kr = self.key(w, 1)
+        t0 = cfg.motion_start_frac * self.clip_end() * uniform(kr, ctr * 256 + 203)
+        ax = cfg.spawn_half_extent * (2.0 * uniform(kr, ctr * 256 + 200) - 1.0)
+        ay = cfg.spawn_half_extent * (2.0 * uniform(kr, ctr * 256 + 201) - 1.0)
+        q, v = motion_ref(cfg, t0)
+        q = q.copy()
+        q[0] += ax
+        q[1] += ay
+        q[2] += terrain_height(m, q[0], q[1])
+        self.qpos[w] = q
+        self.qvel[w] = v
+        self.warm[w] = 0.0
+        self.action[w] = 0.0
+        self.prev_action[w] = 0.0
+        self.episode_step[w] = 0
+        self.ep_return[w] = 0.0
+        self.cmd[w] = (t0, ax, ay)
+        self.cmd_timer[w] = 0
+
+    def resample(self, w, ctr):
+        pass
+
+    def _errors(self, w):
+        m, cfg = self.m, self.cfg
+        q, v = self.qpos[w], self.qvel[w]
+        qr, vr = motion_ref(cfg, self.cmd[w, 0])
+        pr = qr[0:3] + np.array([self.cmd[w, 1], self.cmd[w, 2], terrain_height(m, qr[0] + self.cmd[w, 1],
+                                                                               qr[1] + self.cmd[w, 2])])
+        quat = qnormalize(q[3:7])
+        R = qmat(quat)
+        pos_err_b = R.T @ (pr - q[0:3])
+        rot_err = quat_rotvec(qmul(qconj(quat), qnormalize(qr[3:7])))
+        return qr, vr, pos_err_b, rot_err
+
+    def observe(self, ctr):
+        m, cfg = self.m, self.cfg
+        act, dofs = m.actuator_qposadr, m.actuator_dofadr
+        out = np.zeros((self.n, cfg.obs_dim(m)))
+        for w in range(self.n):
+            vb, om, g, _ = base_frame(m, self.qpos[w], self.qvel[w])
+            qr, vr, pe, re = self._errors(w)
+            o = np.concatenate([qr[act] - self.act_default, vr[dofs], vb, om, g, pe, re,
+                                self.qpos[w][act] - self.act_default, self.qvel[w][dofs], self.action[w]])
+            ko = self.key(w, 3)
+            scales = cfg.noise_vector(m)
+            for i in range(o.size):
+                if scales[i] > 0.0:
+                    o[i] += scales[i] * (2.0 * uniform(ko, ctr * 1024 + i) - 1.0)
+            out[w] = o
+        return out
+
+    def step(self, actions):
+        m, cfg = self.m, self.cfg
+        self.global_step += 1
+        ctr = self.global_step
+        dtc = m.opt.timestep * cfg.decimation
+        rew = np.zeros(self.n)
+        term = np.zeros(self.n, dtype=bool)
+        trunc = np.zeros(self.n, dtype=bool)
+        act, dofs = m.actuator_qposadr, m.actuator_dofadr
+        for w in range(self.n):
+            a = np.clip(actions[w], -cfg.action_clip, cfg.action_clip)
+            self.prev_action[w] = self.action[w]
+            self.action[w] = a
+            ctrl = self.act_default + cfg.action_scale * a
+            q, v, warm = self.qpos[w], self.qvel[w], self.warm[w]
+            for _ in range(cfg.decimation):
+                q, v, warm, _ = step(m, q, v, ctrl, warm=warm)
+            self.qpos[w], self.qvel[w], self.warm[w] = q, v, warm
+            self.cmd[w, 0] += dtc
+            qr, vr, pe, re = self._errors(w)
+            s = cfg.motion_sigmas
+            ej = float(np.sum((q[act] - qr[act]) ** 2))
+            ev = float(np.sum((v[dofs] - vr[dofs]) ** 2))
+            terms = (np.exp(-ej / s[0]), np.exp(-ev / s[1]), np.exp(-float(pe @ pe) / s[2]),
+                     np.exp(-float(re @ re) / s[3]), float(np.sum((self.action[w] - self.prev_action[w]) ** 2)),
+                     0.0)
+            r = 0.0
+            for wt, t in zip(cfg.reward_weights, terms):
+                r += wt * t * dtc
+            rew[w] = r
+            self.ep_return[w] += r
+            nonfinite = not (np.all(np.isfinite(q)) and np.all(np.isfinite(v)))
+            term[w] = bool(abs(pe[2]) > cfg.max_height_error or float(np.sqrt(re @ re)) > cfg.max_ori_error
+                           or nonfinite)
+            self.episode_step[w] += 1
+            trunc[w] = bool(self.episode_step[w] >= cfg.episode_steps or self.cmd[w, 0] >= self.clip_end() - 1e-9)
+        for w in range(self.n):
+            if term[w] or trunc[w]:
+                self.reset_world(w, ctr)
+        return self.observe(ctr), rew, term, trunc

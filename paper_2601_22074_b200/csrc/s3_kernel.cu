@@ -1541,6 +1541,180 @@ __device__ __noinline__ void task_observe(const s3_model& m, const s3_task& tk, 
     }
 }
 
+// ---- motion imitation (kind 1): reference-motion command, cmd = (motion time, anchor x, anchor y)
+
+// reference qpos -> qr[nq], qvel -> vr[nv] at motion time t (oracle motion_ref)
+template <class T>
+__device__ __noinline__ void motion_ref(const s3_model& m, const s3_task& tk, T t, T* qr, T* vr, int lane) {
+    const T* Q = static_cast<const T*>(tk.motion_qpos);
+    const T* V = static_cast<const T*>(tk.motion_qvel);
+    const int F = tk.nframes;
+    T f = t / T(tk.frame_dt);
+    int i0 = (int)floor(f);
+    i0 = i0 < 0 ? 0 : (i0 > F - 2 ? F - 2 : i0);
+    T a = f - T(i0);
+    const T* q0 = Q + (size_t)i0 * m.nq;
+    const T* q1 = q0 + m.nq;
+    for (int i = lane; i < m.nq; i += 32) qr[i] = (T(1) - a) * q0[i] + a * q1[i];
+    for (int i = lane; i < m.nv; i += 32) vr[i] = (T(1) - a) * V[(size_t)i0 * m.nv + i] + a * V[(size_t)(i0 + 1) * m.nv + i];
+    __syncwarp();
+    if (lane == 0) {
+        T u[4] = {q0[3], q0[4], q0[5], q0[6]}, w[4] = {q1[3], q1[4], q1[5], q1[6]};
+        T d = u[0] * w[0] + u[1] * w[1] + u[2] * w[2] + u[3] * w[3];
+        if (d < T(0)) { w[0] = -w[0]; w[1] = -w[1]; w[2] = -w[2]; w[3] = -w[3]; }
+        T qq[4];
+        for (int k = 0; k < 4; ++k) qq[k] = (T(1) - a) * u[k] + a * w[k];
+        T r = rsqrt_t(qq[0] * qq[0] + qq[1] * qq[1] + qq[2] * qq[2] + qq[3] * qq[3]);
+        for (int k = 0; k < 4; ++k) qr[3 + k] = qq[k] * r;
+    }
+    __syncwarp();
+}
+
+// root position error in the base frame and orientation error (rotation vector of conj(q) q_ref)
+template <class T>
+__device__ inline void motion_errors(const s3_model& m, const T* qpos, const T* qr, const T* cmd, T* pe, T* re) {
+    T px = qr[0] + cmd[1], py = qr[1] + cmd[2];
+    T pz = qr[2] + terrain_height(m, px, py);
+    T q[4] = {qpos[3], qpos[4], qpos[5], qpos[6]};
+    qnormalize(q);
+    T R[9];
+    qmat(q, R);
+    T d[3] = {px - qpos[0], py - qpos[1], pz - qpos[2]};
+    for (int k = 0; k < 3; ++k) pe[k] = R[k] * d[0] + R[3 + k] * d[1] + R[6 + k] * d[2];
+    T qc[4] = {q[0], -q[1], -q[2], -q[3]};
+    T qf[4] = {qr[3], qr[4], qr[5], qr[6]};
+    qnormalize(qf);
+    T e[4];
+    qmul(qc, qf, e);
+    if (e[0] < T(0)) { e[0] = -e[0]; e[1] = -e[1]; e[2] = -e[2]; e[3] = -e[3]; }
+    T sn = sqrt(e[1] * e[1] + e[2] * e[2] + e[3] * e[3]);
+    T sc = sn < T(1e-12) ? T(2) : T(2) * atan2(sn, e[0]) / sn;
+    re[0] = e[1] * sc; re[1] = e[2] * sc; re[2] = e[3] * sc;
+}
+
+template <class T>
+__device__ __noinline__ void motion_reset(const s3_model& m, const s3_task& tk, const s3_layout& L_, T* B_, int64_t w,
+                                          uint64_t ctr, T* cmd, int lane) {
+    WS<T> s = make_ws(B_, L_);
+    uint64_t kr = stream_key(tk.seed, tk.world_offset + w, 1);
+    const T clip_end = T(tk.nframes - 1) * T(tk.frame_dt);
+    T t0 = T(tk.motion_start_frac) * clip_end * uniform01<T>(kr, ctr * 256 + 203);
+    T ax = T(tk.spawn_half_extent) * (T(2) * uniform01<T>(kr, ctr * 256 + 200) - T(1));
+    T ay = T(tk.spawn_half_extent) * (T(2) * uniform01<T>(kr, ctr * 256 + 201) - T(1));
+    motion_ref(m, tk, t0, s.qpos, s.qvel, lane);
+    if (lane == 0) {
+        s.qpos[0] += ax;
+        s.qpos[1] += ay;
+        s.qpos[2] += terrain_height(m, s.qpos[0], s.qpos[1]);
+        cmd[0] = t0; cmd[1] = ax; cmd[2] = ay;
+    }
+    __syncwarp();
+}
+
+template <class T>
+__device__ __noinline__ void motion_observe(const s3_model& m, const s3_task& tk, const s3_layout& L_, T* B_, int64_t w,
+                                            uint64_t ctr, const T* cmd, const T* action, int lane) {
+    WS<T> s = make_ws(B_, L_);
+    T* qr = s.LD;
+    T* vr = s.LD + m.nq;
+    motion_ref(m, tk, cmd[0], qr, vr, lane);
+    T vb[3], om[3], g[3], pe[3], re[3];
+    base_frame(s.qpos, s.qvel, vb, om, g);
+    motion_errors(m, s.qpos, qr, cmd, pe, re);
+    const T* dq = static_cast<const T*>(tk.default_qpos);
+    uint64_t ko = stream_key(tk.seed, tk.world_offset + w, 3);
+    T* out = static_cast<T*>(tk.obs) + w * tk.obs_dim;
+    const int nu = m.nu;
+    // [ref joint pos - default, ref joint vel, v_b, w_b, g_b, pos err_b, rot err, joint pos - default, joint vel, action]
+    for (int i = lane; i < tk.obs_dim; i += 32) {
+        T v, ns = T(0);
+        if (i < nu) {
+            int a = m.act_qposadr[i];
+            v = qr[a] - dq[a];
+        } else if (i < 2 * nu) {
+            v = vr[m.act_dofadr[i - nu]];
+        } else if (i < 2 * nu + 15) {
+            int r = i - 2 * nu, g3 = r / 3, k = r % 3;
+            v = g3 == 0 ? vb[k] : (g3 == 1 ? om[k] : (g3 == 2 ? g[k] : (g3 == 3 ? pe[k] : re[k])));
+            ns = g3 < 3 ? T(tk.noise[g3]) : T(0);
+        } else if (i < 3 * nu + 15) {
+            int a = m.act_qposadr[i - 2 * nu - 15];
+            v = s.qpos[a] - dq[a];
+            ns = T(tk.noise[4]);
+        } else if (i < 4 * nu + 15) {
+            v = s.qvel[m.act_dofadr[i - 3 * nu - 15]];
+            ns = T(tk.noise[5]);
+        } else {
+            v = action[i - 4 * nu - 15];
+            ns = T(tk.noise[6]);
+        }
+        if (ns > T(0)) v += ns * (T(2) * uniform01<T>(ko, ctr * 1024 + i) - T(1));
+        out[i] = v;
+    }
+}
+
+template <class T>
+__device__ __noinline__ void motion_post(const s3_model& m, const s3_task& tk, const s3_layout& L_, T* B_, int64_t w,
+                                         uint64_t ctr, T* cmd, T* act, T rate, T* gq, T* gv, T* gw, T* prev, int lane) {
+    WS<T> s = make_ws(B_, L_);
+    const int nu = m.nu, nq = m.nq, nv = m.nv;
+    const T dtc = T(m.timestep) * T(tk.decimation);
+    T tnow = cmd[0] + dtc;
+    __syncwarp();
+    if (lane == 0) cmd[0] = tnow;
+    __syncwarp();
+    T* qr = s.LD;
+    T* vr = s.LD + nq;
+    motion_ref(m, tk, tnow, qr, vr, lane);
+    T pe[3], re[3];
+    T c3[3] = {tnow, cmd[1], cmd[2]};
+    motion_errors(m, s.qpos, qr, c3, pe, re);
+    T ej = T(0), ev = T(0);
+    for (int i = lane; i < nu; i += 32) {
+        int a = m.act_qposadr[i], d = m.act_dofadr[i];
+        T dq = s.qpos[a] - qr[a], dv = s.qvel[d] - vr[d];
+        ej += dq * dq;
+        ev += dv * dv;
+    }
+    ej = wsum(ej);
+    ev = wsum(ev);
+    T terms[6] = {exp(-ej / T(tk.motion_sigmas[0])), exp(-ev / T(tk.motion_sigmas[1])),
+                  exp(-(pe[0] * pe[0] + pe[1] * pe[1] + pe[2] * pe[2]) / T(tk.motion_sigmas[2])),
+                  exp(-(re[0] * re[0] + re[1] * re[1] + re[2] * re[2]) / T(tk.motion_sigmas[3])), rate, T(0)};
+    T r = T(0);
+    for (int k = 0; k < 6; ++k) r += T(tk.reward_weights[k]) * terms[k] * dtc;
+    bool finite = true;
+    for (int i = lane; i < nq; i += 32) finite = finite && isfinite(s.qpos[i]);
+    for (int i = lane; i < nv; i += 32) finite = finite && isfinite(s.qvel[i]);
+    finite = __all_sync(FULL, finite);
+    T rot = sqrt(re[0] * re[0] + re[1] * re[1] + re[2] * re[2]);
+    bool term = fabs(pe[2]) > T(tk.max_height_error) || rot > T(tk.max_ori_error) || !finite;
+    int es = tk.episode_step[w] + 1;
+    const T clip_end = T(tk.nframes - 1) * T(tk.frame_dt);
+    bool trunc = es >= tk.episode_steps || tnow >= clip_end - T(1e-9);
+    __syncwarp();
+    if (lane == 0) {
+        static_cast<T*>(tk.reward)[w] = r;
+        static_cast<T*>(tk.episode_return)[w] += r;
+        tk.terminated[w] = term;
+        tk.truncated[w] = trunc;
+        tk.episode_step[w] = es;
+    }
+    if (term || trunc) {
+        motion_reset(m, tk, L_, B_, w, ctr, cmd, lane);
+        for (int i = lane; i < nv; i += 32) gw[i] = T(0);
+        for (int i = lane; i < nu; i += 32) { act[i] = T(0); prev[i] = T(0); }
+        if (lane == 0) {
+            tk.episode_step[w] = 0;
+            static_cast<T*>(tk.episode_return)[w] = T(0);
+        }
+    }
+    __syncwarp();
+    motion_observe(m, tk, L_, B_, w, ctr, cmd, act, lane);
+    for (int i = lane; i < nq; i += 32) gq[i] = s.qpos[i];
+    for (int i = lane; i < nv; i += 32) gv[i] = s.qvel[i];
+}
+
 template <class T>
 __global__ void __launch_bounds__(32 * 16) env_kernel(const __grid_constant__ s3_model m, const __grid_constant__ s3_data d,
                                                      const __grid_constant__ s3_layout l,
@@ -1565,17 +1739,22 @@ __global__ void __launch_bounds__(32 * 16) env_kernel(const __grid_constant__ s3
     const T* dq = static_cast<const T*>(tk.default_qpos);
     uint64_t ctr = (uint64_t)global_step;
     if (mode == 1) {  // reset every world, counter 0
-        task_reset(m, tk, L_, B_, w, 0, lane);
+        if (tk.kind == 1) {
+            motion_reset(m, tk, L_, B_, w, 0, cmd, lane);
+        } else {
+            task_reset(m, tk, L_, B_, w, 0, lane);
+            task_resample(tk, cmd, w, 0, lane);
+        }
         for (int i = lane; i < nv; i += 32) gw[i] = T(0);
         for (int i = lane; i < nu; i += 32) { act[i] = T(0); prev[i] = T(0); }
-        task_resample(tk, cmd, w, 0, lane);
         if (lane == 0) {
-            tk.cmd_timer[w] = tk.cmd_resample_steps;
+            tk.cmd_timer[w] = tk.kind == 1 ? 0 : tk.cmd_resample_steps;
             tk.episode_step[w] = 0;
             static_cast<T*>(tk.episode_return)[w] = T(0);
         }
         __syncwarp();
-        task_observe(m, tk, L_, B_, w, 0, cmd, act, lane);
+        if (tk.kind == 1) motion_observe(m, tk, L_, B_, w, 0, cmd, act, lane);
+        else task_observe(m, tk, L_, B_, w, 0, cmd, act, lane);
         if (d.geom_xpos) store_geom_frames(m, d, L_, B_, w, lane);
         for (int i = lane; i < nq; i += 32) gq[i] = s.qpos[i];
         for (int i = lane; i < nv; i += 32) gv[i] = s.qvel[i];
@@ -1596,6 +1775,10 @@ __global__ void __launch_bounds__(32 * 16) env_kernel(const __grid_constant__ s3
     rate = wsum(rate);
     __syncwarp();
     for (int sub = 0; sub < tk.decimation; ++sub) substep(m, d, L_, B_, w, gw, (const T*)nullptr, false, lane);
+    if (tk.kind == 1) {
+        motion_post(m, tk, L_, B_, w, ctr, cmd, act, rate, gq, gv, gw, prev, lane);
+        return;
+    }
     // rewards, terminations (pre-reset state)
     T vb[3], om[3], g[3];
     base_frame(s.qpos, s.qvel, vb, om, g);
@@ -1910,7 +2093,9 @@ int s3_env_step(const s3_model* m, const s3_data* d, const s3_layout* l, const s
     if (d->nworld == 0) return S3_OK;
     if (!d->qpos || !d->qvel || !d->qacc_warmstart) return fail(S3_ERR_ARG, "qpos/qvel/qacc_warmstart required");
     if (mode == 0 && !actions) return fail(S3_ERR_ARG, "actions required");
-    if (t->obs_dim != 12 + 3 * m->nu + t->nscan || t->nscan > S3_MAX_RAYS || t->decimation < 1)
+    const int want = t->kind == 1 ? 15 + 5 * m->nu : 12 + 3 * m->nu + t->nscan;
+    if (t->obs_dim != want || t->nscan > S3_MAX_RAYS || t->decimation < 1 ||
+        (t->kind == 1 && (t->nframes < 2 || !t->motion_qpos || !t->motion_qvel || m->nq + m->nv > m->nv * (m->nv + 1) / 2)))
         return fail(S3_ERR_ARG, "task layout does not match the model");
     if (d->qM) return fail(S3_ERR_ARG, "parity outputs are not written by s3_env_step");
     cudaStream_t st = static_cast<cudaStream_t>(stream);

@@ -73,8 +73,45 @@ class VelocityTaskCfg:
         return np.array(v)
 
 
+@dataclass
+class MotionTrackingCfg:
+    """BeyondMimic-style motion imitation (BASELINE configs[2]): a reference-motion command manager plays
+    a clip (motion.py); each world tracks it from a random phase (reference state initialisation) at a
+    random spawn anchor. Observations: [ref joint pos - default, ref joint vel, base lin vel, base ang vel,
+    projected gravity, root pos error (base frame), root orientation error (rotation vector), joint pos -
+    default, joint vel, last action]. Rewards: exp tracking kernels of joint pos / joint vel / root pos /
+    root orientation + action rate. Terminations: root height error, orientation error; truncation at the
+    clip end or after episode_steps. ``command`` holds (motion time, anchor x, anchor y) per world."""
+    default_qpos: np.ndarray
+    motion_qpos: np.ndarray
+    motion_qvel: np.ndarray
+    motion_dt: float
+    decimation: int = 4
+    action_scale: float = 0.25
+    action_clip: float = 2.0
+    episode_steps: int = 500
+    # track_joint_pos, track_joint_vel, track_root_pos, track_root_ori, action_rate_l2, (unused)
+    reward_weights: tuple = (0.5, 0.1, 0.5, 0.5, -0.01, 0.0)
+    motion_sigmas: tuple = (1.0, 50.0, 0.1, 0.5)
+    max_height_error: float = 0.25
+    max_ori_error: float = 0.8
+    spawn_half_extent: float = 0.5
+    motion_start_frac: float = 0.9
+    noise: tuple = (0.1, 0.2, 0.05, 0.0, 0.01, 1.5, 0.0)
+    kind: int = 1
+
+    def obs_dim(self, m: Model) -> int:
+        return 15 + 5 * m.nu
+
+    def noise_vector(self, m: Model) -> np.ndarray:
+        n = self.noise
+        return np.array([0.0] * (2 * m.nu) + [n[0]] * 3 + [n[1]] * 3 + [n[2]] * 3 + [0.0] * 6 +
+                        [n[4]] * m.nu + [n[5]] * m.nu + [n[6]] * m.nu)
+
+
 class VelocityEnv3D:
-    """Batched 3-D velocity-tracking env on the GPU (world index outermost)."""
+    """Batched fused 3-D env on the GPU (world index outermost): velocity tracking
+    (``VelocityTaskCfg``) or motion imitation (``MotionTrackingCfg``)."""
 
     def __init__(self, model: Model, cfg: VelocityTaskCfg, num_envs: int, seed: int = 0, world_offset: int = 0,
                  dtype: str = "f64", device="cuda"):
@@ -99,25 +136,39 @@ class VelocityEnv3D:
         self.truncated = torch.zeros(n, dtype=torch.uint8, device=dev)
         self.global_step = 0
         t = N.TaskT()
-        t.decimation, t.episode_steps, t.cmd_resample_steps = cfg.decimation, cfg.episode_steps, \
-            cfg.command_resample_steps
+        motion = isinstance(cfg, MotionTrackingCfg)
+        t.kind = 1 if motion else 0
+        t.decimation, t.episode_steps = cfg.decimation, cfg.episode_steps
         t.obs_dim = self.obs_dim
         t.seed = self.seed
         t.world_offset = self.world_offset
-        t.action_scale, t.action_clip, t.track_sigma = cfg.action_scale, cfg.action_clip, cfg.track_sigma
-        t.min_height, t.max_tilt_cos, t.reset_joint_jitter = cfg.min_height, cfg.max_tilt_cos, cfg.reset_joint_jitter
+        t.action_scale, t.action_clip = cfg.action_scale, cfg.action_clip
         t.spawn_half_extent = cfg.spawn_half_extent
-        for i, (lo, hi) in enumerate(cfg.command_ranges):
-            t.cmd_lo[i], t.cmd_hi[i] = lo, hi
         t.reward_weights[:] = cfg.reward_weights
         t.noise[:] = cfg.noise
-        pts = cfg.scan_points() if cfg.height_scan else []
+        if motion:
+            self._motion_q = torch.as_tensor(cfg.motion_qpos, dtype=dt, device=dev).contiguous()
+            self._motion_v = torch.as_tensor(cfg.motion_qvel, dtype=dt, device=dev).contiguous()
+            t.nframes, t.frame_dt = cfg.motion_qpos.shape[0], cfg.motion_dt
+            t.motion_qpos, t.motion_qvel = self._motion_q.data_ptr(), self._motion_v.data_ptr()
+            t.motion_sigmas[:] = cfg.motion_sigmas
+            t.max_height_error, t.max_ori_error = cfg.max_height_error, cfg.max_ori_error
+            t.motion_start_frac = cfg.motion_start_frac
+        else:
+            t.cmd_resample_steps = cfg.command_resample_steps
+            t.track_sigma = cfg.track_sigma
+            t.min_height, t.max_tilt_cos, t.reset_joint_jitter = cfg.min_height, cfg.max_tilt_cos, \
+                cfg.reset_joint_jitter
+            for i, (lo, hi) in enumerate(cfg.command_ranges):
+                t.cmd_lo[i], t.cmd_hi[i] = lo, hi
+        pts = cfg.scan_points() if getattr(cfg, "height_scan", False) else []
         if len(pts) > N.S3_MAX_RAYS:
             raise ValueError("height scan larger than S3_MAX_RAYS")
         t.nscan = len(pts)
         for i, (x, y) in enumerate(pts):
             t.scan_xy[2 * i], t.scan_xy[2 * i + 1] = x, y
-        t.scan_offset, t.scan_noise = cfg.scan_offset, cfg.scan_noise
+        if pts:
+            t.scan_offset, t.scan_noise = cfg.scan_offset, cfg.scan_noise
         self._default = torch.as_tensor(cfg.default_qpos, dtype=dt, device=dev).contiguous()
         t.default_qpos = self._default.data_ptr()
         for name in ("action", "prev_action", "command", "cmd_timer", "episode_step", "episode_return", "obs",

@@ -138,3 +138,65 @@ def test_world_offset_partition_independence():
         o0, r0, _, _ = a0.step(act[:4].contiguous())
         o1, r1, _, _ = a1.step(act[4:].contiguous())
     assert torch.equal(of, torch.cat([o0, o1])) and torch.equal(rf, torch.cat([r0, r1]))
+
+
+def _motion_pair(n, dtype="f64", **over):
+    from paper_2601_22074_b200.sim3d.motion import synthetic_walk_clip
+    from paper_2601_22074_b200.sim3d.task import MotionTrackingCfg, VelocityEnv3D
+
+    mg, mo = robots.g1_like(rough=True, seed=4), robots.g1_like(rough=True, seed=4)
+    dq = robots.default_qpos(mg, robots.G1_DEFAULT_JOINTS)
+    Q, V, fdt = synthetic_walk_clip(mg, dq, seconds=4.0)
+    cfg = MotionTrackingCfg(default_qpos=dq, motion_qpos=Q, motion_qvel=V, motion_dt=fdt, **over)
+    env = VelocityEnv3D(mg, cfg, n, seed=11, dtype=dtype)
+    O.set_const(mo)
+    return env, O.MotionTaskOracle(mo, cfg, n, seed=11)
+
+
+@pytest.mark.gpu
+def test_motion_imitation_free_running_f64():
+    """BeyondMimic-style task (BASELINE configs[2]): reference state initialisation, tracking rewards,
+    reference-aware observations match the oracle."""
+    import torch
+
+    n = 8
+    env, ref = _motion_pair(n)
+    np.testing.assert_allclose(env.reset().cpu().numpy(), ref.reset(), atol=1e-12)
+    np.testing.assert_allclose(env.command.cpu().numpy(), ref.cmd, atol=1e-12)
+    rng = np.random.default_rng(5)
+    for k in range(4):
+        a = rng.uniform(-1, 1, size=(n, env.model.nu))
+        o, r, te, tr = env.step(torch.as_tensor(a, device="cuda"))
+        o_ref, r_ref, te_ref, tr_ref = ref.step(a)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(te.cpu().numpy().astype(bool), te_ref)
+        np.testing.assert_array_equal(tr.cpu().numpy().astype(bool), tr_ref)
+        np.testing.assert_allclose(r.cpu().numpy(), r_ref, rtol=1e-8, atol=1e-10)
+        np.testing.assert_allclose(o.cpu().numpy(), o_ref, rtol=1e-7, atol=1e-7)
+
+
+@pytest.mark.gpu
+def test_motion_imitation_teacher_forced_terminations_and_clip_end():
+    import torch
+
+    n = 8
+    env, ref = _motion_pair(n, max_height_error=0.02, motion_start_frac=1.0)
+    env.reset()
+    ref.reset()
+    ref.cmd[:4, 0] = ref.clip_end() - 0.01  # four worlds run off the end of the clip in one step
+    rng = np.random.default_rng(6)
+    saw_term = saw_trunc = 0
+    for k in range(5):
+        _load(env, ref)
+        a = rng.uniform(-1, 1, size=(n, env.model.nu))
+        o, r, te, tr = env.step(torch.as_tensor(a, device="cuda"))
+        o_ref, r_ref, te_ref, tr_ref = ref.step(a)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(te.cpu().numpy().astype(bool), te_ref)
+        np.testing.assert_array_equal(tr.cpu().numpy().astype(bool), tr_ref)
+        np.testing.assert_allclose(r.cpu().numpy(), r_ref, rtol=1e-8, atol=1e-10)
+        np.testing.assert_allclose(o.cpu().numpy(), o_ref, rtol=1e-7, atol=1e-7)
+        np.testing.assert_allclose(env.command.cpu().numpy(), ref.cmd, atol=1e-12)
+        saw_term += int(te_ref.sum())
+        saw_trunc += int(tr_ref.sum())
+    assert saw_term > 0 and saw_trunc > 0
