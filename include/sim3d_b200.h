@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define S3_ABI_VERSION 8
+#define S3_ABI_VERSION 9
 #define S3_F64 0
 #define S3_F32 1
 
@@ -33,6 +33,7 @@ extern "C" {
 #define S3_MAX_LIM 32
 #define S3_MAX_ROWS 96
 #define S3_MAX_RAYS 128
+#define S3_MAX_TREE 4
 
 #define S3_OK 0
 #define S3_ERR_ARG 1
@@ -64,7 +65,7 @@ typedef struct s3_model {
                       (measured slower; kept for A/B) */
     int32_t nhlev;
     int32_t ndlev;
-    int32_t pad1;
+    int32_t nkintree; /* kinematic trees (robot, free objects) */
     double timestep;
     double gravity[3];
     double tolerance;
@@ -94,6 +95,8 @@ typedef struct s3_model {
     const void* body_mass;
     const void* body_inertia;
     const void* body_invweight0;
+    const int32_t* body_treeid; /* kinematic tree of each body (each tree's subtree com is its c-frame) */
+    const void* tree_mass;
     /* joints */
     const int32_t* jnt_type;
     const int32_t* jnt_qposadr;
@@ -173,7 +176,7 @@ typedef struct s3_data {
     /* outputs of the LAST substep of a launch (for parity tests / sensors) */
     void* xpos;
     void* xquat;
-    void* com;
+    void* com; /* (N, S3_MAX_TREE, 3) subtree com per kinematic tree */
     void* cdof;
     void* qM;
     void* qLD;

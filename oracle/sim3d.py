@@ -124,11 +124,14 @@ def kinematics(m, qpos):
 
 
 def com_pos(m, K):
-    """Subtree com of the (single) tree, cinert about it, cdof (mj_comPos)."""
-    mass = m.body_mass[1:]
-    com = (mass[:, None] * K["xipos"][1:]).sum(0) / mass.sum()
+    """Subtree com of every kinematic tree, cinert about its tree's com, cdof (mj_comPos)."""
+    coms = np.zeros((m.ntree, 3))
+    for t in range(m.ntree):
+        sel = [b for b in range(1, m.nbody) if m.body_treeid[b] == t]
+        coms[t] = (m.body_mass[sel][:, None] * K["xipos"][sel]).sum(0) / m.tree_mass[t]
     cinert = np.zeros((m.nbody, 10))
     for b in range(1, m.nbody):
+        com = coms[m.body_treeid[b]]
         R = K["ximat"][b]
         I = R @ np.diag(m.body_inertia[b]) @ R.T
         d = K["xipos"][b] - com
@@ -138,6 +141,7 @@ def com_pos(m, K):
     cdof = np.zeros((m.nv, 6))
     for j in range(m.njnt):
         b, da = m.jnt_bodyid[j], m.jnt_dofadr[j]
+        com = coms[m.body_treeid[b]]
         if m.jnt_type[j] == JNT_FREE:
             for i in range(3):
                 cdof[da + i, 3 + i] = 1.0
@@ -148,7 +152,7 @@ def com_pos(m, K):
         else:
             ax = K["xaxis"][j]
             cdof[da] = np.concatenate([ax, np.cross(ax, com - K["xanchor"][j])])
-    return dict(com=com, cinert=cinert, cdof=cdof)
+    return dict(com=coms, cinert=cinert, cdof=cdof)
 
 
 def crb(m, C):
@@ -341,6 +345,30 @@ def _sphere_sphere(c1, r1, c2, r2):
     return d, n, c1 + n * (r1 + 0.5 * d)
 
 
+def sphere_box(c, r, bc, R, size):
+    """Sphere (centre c, radius r) vs box (centre bc, rotation R, half sizes): (dist, normal sphere->box,
+    contact point). Centre outside: closest point on the box; inside: the face of least penetration."""
+    p = R.T @ (c - bc)
+    q = np.minimum(np.maximum(p, -size), size)
+    dq = p - q
+    L = np.sqrt(dq @ dq)
+    if L > 1e-12:
+        n_loc = -dq / L          # from the sphere centre towards the box
+        d = L - r
+        pos = bc + R @ q - (R @ n_loc) * (0.5 * d)  # midpoint of the two surface points
+        return d, R @ n_loc, pos
+    # inside: push out through the nearest face
+    gap = size - np.abs(p)
+    k = int(np.argmin(gap))
+    n_loc = np.zeros(3)
+    n_loc[k] = -1.0 if p[k] >= 0.0 else 1.0  # towards the box interior from that face
+    d = -gap[k] - r
+    face = p.copy()
+    face[k] = size[k] if p[k] >= 0.0 else -size[k]
+    pos = bc + R @ face - (R @ n_loc) * (0.5 * d)
+    return d, R @ n_loc, pos
+
+
 def _segment(m, K, g):
     a = K["geom_xmat"][g][:, 2] * m.geom_size[g][1]
     c = K["geom_xpos"][g]
@@ -390,6 +418,14 @@ def collide(m, K):
                 if h is not None and h[0] < 0.0:
                     d, n = h
                     found.append((d, n, q - n * (r + 0.5 * d)))
+        elif t2 == GEOM_BOX:  # sphere (g1) vs box (g2)
+            dv = c2 - c1
+            rb = m.geom_rbound[g1] + m.geom_rbound[g2]
+            if dv @ dv >= rb * rb:
+                continue
+            h = sphere_box(c1, m.geom_size[g1][0], c2, K["geom_xmat"][g2], m.geom_size[g2])
+            if h is not None and h[0] < 0.0:
+                found.append(h)
         else:
             dv = c2 - c1
             rb = m.geom_rbound[g1] + m.geom_rbound[g2]
@@ -427,8 +463,9 @@ def collide(m, K):
 def point_jac(m, C, b, p):
     """3 x nv translational Jacobian of world point p attached to body b (mj_jac)."""
     J = np.zeros((3, m.nv))
+    com = C["com"][m.body_treeid[b]]
     for d in m.body_chain[b]:
-        J[:, d] = C["cdof"][d][3:] + np.cross(C["cdof"][d][:3], p - C["com"])
+        J[:, d] = C["cdof"][d][3:] + np.cross(C["cdof"][d][:3], p - com)
     return J
 
 

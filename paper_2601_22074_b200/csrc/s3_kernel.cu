@@ -252,19 +252,29 @@ template <class T> __device__ void __noinline__ com_pos(const s3_model& m, const
     const T* ilmat = F<T>(m.body_ilmat);
     const T* mass = F<T>(m.body_mass);
     const T* inertia = F<T>(m.body_inertia);
-    T cx = T(0), cy = T(0), cz = T(0);
     for (int b = 1 + lane; b < m.nbody; b += 32) {
         T R[9], v[3];
         qmat(s.xquat + 4 * b, R);
         T ip[3] = {ipos[3 * b], ipos[3 * b + 1], ipos[3 * b + 2]};
         mv3(R, ip, v);
-        T x = s.xpos[3 * b] + v[0], y = s.xpos[3 * b + 1] + v[1], z = s.xpos[3 * b + 2] + v[2];
-        s.xipos[3 * b] = x; s.xipos[3 * b + 1] = y; s.xipos[3 * b + 2] = z;
-        cx += mass[b] * x; cy += mass[b] * y; cz += mass[b] * z;
+        s.xipos[3 * b] = s.xpos[3 * b] + v[0];
+        s.xipos[3 * b + 1] = s.xpos[3 * b + 1] + v[1];
+        s.xipos[3 * b + 2] = s.xpos[3 * b + 2] + v[2];
     }
-    T inv = T(1) / T(m.total_mass);
-    T com[3] = {wsum(cx) * inv, wsum(cy) * inv, wsum(cz) * inv};
-    if (lane == 0) { s.com[0] = com[0]; s.com[1] = com[1]; s.com[2] = com[2]; }
+    __syncwarp();
+    // subtree com of every kinematic tree (each tree's c-frame origin)
+    const T* tmass = F<T>(m.tree_mass);
+    for (int t = 0; t < m.nkintree; ++t) {
+        T cx = T(0), cy = T(0), cz = T(0);
+        for (int b = 1 + lane; b < m.nbody; b += 32) {
+            if (m.body_treeid[b] != t) continue;
+            cx += mass[b] * s.xipos[3 * b]; cy += mass[b] * s.xipos[3 * b + 1]; cz += mass[b] * s.xipos[3 * b + 2];
+        }
+        T inv = T(1) / tmass[t];
+        cx = wsum(cx) * inv; cy = wsum(cy) * inv; cz = wsum(cz) * inv;
+        if (lane == 0) { s.com[3 * t] = cx; s.com[3 * t + 1] = cy; s.com[3 * t + 2] = cz; }
+    }
+    __syncwarp();
     for (int b = 1 + lane; b < m.nbody; b += 32) {
         T R[9], Ri[9], IL[9];
         qmat(s.xquat + 4 * b, R);
@@ -278,6 +288,7 @@ template <class T> __device__ void __noinline__ com_pos(const s3_model& m, const
 #pragma unroll
             for (int c = 0; c < 3; ++c) I[3 * r + c] = Ri[3 * r] * i0 * Ri[3 * c] + Ri[3 * r + 1] * i1 * Ri[3 * c + 1] +
                                                      Ri[3 * r + 2] * i2 * Ri[3 * c + 2];
+        const T* com = s.com + 3 * m.body_treeid[b];
         T d[3] = {s.xipos[3 * b] - com[0], s.xipos[3 * b + 1] - com[1], s.xipos[3 * b + 2] - com[2]};
         T mb = mass[b];
         T dd = dot3(d, d);
@@ -293,6 +304,7 @@ template <class T> __device__ void __noinline__ com_pos(const s3_model& m, const
     // cdof, per joint
     for (int j = lane; j < m.njnt; j += 32) {
         int da = m.jnt_dofadr[j];
+        const T* com = s.com + 3 * m.body_treeid[m.dof_bodyid[da]];
         T off[3] = {com[0] - s.janc[3 * j], com[1] - s.janc[3 * j + 1], com[2] - s.janc[3 * j + 2]};
         if (m.jnt_type[j] == kJntFree) {
             int b = m.dof_bodyid[da];
@@ -803,6 +815,48 @@ template <class T> __device__ __noinline__ int narrow(const s3_model& m, const s
                 ++cnt;
             }
         }
+    } else if (t2 == kGeomBox) {  // sphere (g1) vs box (g2): oracle sphere_box
+        T dv[3] = {c2[0] - c1[0], c2[1] - c1[1], c2[2] - c1[2]};
+        T rr = rb[g1] + rb[g2];
+        if (!(dot3(dv, dv) < rr * rr)) return 0;
+        const T* sz = F<T>(m.geom_size);
+        const T* R = s.gmat + 9 * g2;
+        const T* hs = sz + 3 * g2;
+        T r = sz[3 * g1];
+        T dl[3] = {c1[0] - c2[0], c1[1] - c2[1], c1[2] - c2[2]};
+        T p[3], q[3], dq[3];
+        for (int k = 0; k < 3; ++k) {
+            p[k] = R[k] * dl[0] + R[3 + k] * dl[1] + R[6 + k] * dl[2];
+            q[k] = fmin(fmax(p[k], -hs[k]), hs[k]);
+            dq[k] = p[k] - q[k];
+        }
+        T L = sqrt(dot3(dq, dq));
+        T nl[3], fp[3], d;
+        if (L > T(1e-12)) {
+            for (int k = 0; k < 3; ++k) { nl[k] = -dq[k] / L; fp[k] = q[k]; }
+            d = L - r;
+        } else {
+            int kk = 0;
+            T best = hs[0] - fabs(p[0]);
+            for (int k = 1; k < 3; ++k) {
+                T gk = hs[k] - fabs(p[k]);
+                if (gk < best) { best = gk; kk = k; }
+            }
+            for (int k = 0; k < 3; ++k) { nl[k] = T(0); fp[k] = p[k]; }
+            nl[kk] = p[kk] >= T(0) ? T(-1) : T(1);
+            fp[kk] = p[kk] >= T(0) ? hs[kk] : -hs[kk];
+            d = -best - r;
+        }
+        if (d < T(0)) {
+            Hit<T> h;
+            h.d = d;
+            T n[3], wp[3];
+            mv3(R, nl, n);
+            mv3(R, fp, wp);
+            for (int k = 0; k < 3; ++k) { h.n[k] = n[k]; h.pos[k] = c2[k] + wp[k] - n[k] * (T(0.5) * d); }
+            hits[cnt] = h;
+            ++cnt;
+        }
     } else {
         T dv[3] = {c2[0] - c1[0], c2[1] - c1[1], c2[2] - c1[2]};
         T rr = rb[g1] + rb[g2];
@@ -972,9 +1026,10 @@ template <class T> __device__ int __noinline__ build_rows(const s3_model& m, con
         int b1 = m.geom_bodyid[m.pair_geom[2 * p]], b2 = m.geom_bodyid[m.pair_geom[2 * p + 1]];
         uint64_t m1 = m.body_dofmask[b1], m2 = m.body_dofmask[b2];
         const T* cc = s.con + kConStride * c;
-        T dp[3] = {cc[1] - s.com[0], cc[2] - s.com[1], cc[3] - s.com[2]};
         {
             int d = m.pair_chain[p * S3_MAX_CHAIN + k];
+            const T* com = s.com + 3 * m.body_treeid[m.dof_bodyid[d]];
+            T dp[3] = {cc[1] - com[0], cc[2] - com[1], cc[3] - com[2]};
             const T* cd = s.cdof + 6 * d;
             T w[3];
             cross3(cd, dp, w);
@@ -1331,7 +1386,7 @@ __device__ __noinline__ void substep(const s3_model& m, const s3_data& d, const 
             for (int k = 0; k < 3; ++k) static_cast<T*>(d.xpos)[(w * m.nbody + b) * 3 + k] = s.xpos[3 * b + k];
             for (int k = 0; k < 4; ++k) static_cast<T*>(d.xquat)[(w * m.nbody + b) * 4 + k] = s.xquat[4 * b + k];
         }
-        if (lane < 3) static_cast<T*>(d.com)[w * 3 + lane] = s.com[lane];
+        for (int k = lane; k < 3 * m.nkintree; k += 32) static_cast<T*>(d.com)[w * 3 * S3_MAX_TREE + k] = s.com[k];
         for (int c = lane; c < ncon; c += 32) {
             const T* cc = s.con + kConStride * c;
             static_cast<T*>(d.con_dist)[w * S3_MAX_CON + c] = cc[0];
@@ -2057,7 +2112,7 @@ int s3_plan(const s3_model* m, int32_t warps_per_block, s3_layout* out) {
     int jc = 3 * S3_MAX_CON * m->chain_stride, rne = 6 * nv + 12 * nb;
     sizes[O_JC] = jc > rne ? jc : rne; sizes[O_RAREF] = S3_MAX_ROWS; sizes[O_RD] = S3_MAX_ROWS;
     sizes[O_RJAR] = S3_MAX_ROWS; sizes[O_RJP] = S3_MAX_ROWS; sizes[O_CDOT] = 3 * S3_MAX_CON; sizes[O_BIAS] = nv;
-    sizes[O_FCON] = nv; sizes[O_CTRL] = nu; sizes[O_COM] = 4;
+    sizes[O_FCON] = nv; sizes[O_CTRL] = nu; sizes[O_COM] = 3 * S3_MAX_TREE;
     int region = sizes[O_XIPOS] + sizes[O_CINERT] + sizes[O_JANC] + sizes[O_JAX];
     if (region < m->ntree) sizes[O_JAX] += m->ntree - region;  // room for the factorization snapshot
     int esz = m->dtype == S3_F64 ? 8 : 4;

@@ -142,6 +142,7 @@ class DeviceModel:
         act_gain = np.stack([m.actuator_kp, m.actuator_kv, m.actuator_effort, m.actuator_saturation,
                              m.actuator_vmax], axis=1) if m.nu else np.zeros((1, 5))
         ints = dict(
+            body_treeid=m.body_treeid,
             body_parentid=m.body_parentid, body_jntadr=np.maximum(m.body_jntadr, 0), body_jntnum=m.body_jntnum,
             body_dofadr=np.maximum(m.body_dofadr, 0), body_dofnum=m.body_dofnum, body_dofmask=body_dofmask,
             level_ptr=level_ptr, level_body=np.array(order, dtype=np.int32), child_ptr=child_ptr,
@@ -168,6 +169,7 @@ class DeviceModel:
         floats = dict(
             body_pos=m.body_pos, body_quat=m.body_quat, body_ipos=m.body_ipos, body_ilmat=body_ilmat,
             body_mass=m.body_mass, body_inertia=m.body_inertia, body_invweight0=m.body_invweight0,
+            tree_mass=m.tree_mass,
             jnt_pos=m.jnt_pos, jnt_axis=m.jnt_axis, qpos0=m.qpos0, dof_damping=m.dof_damping,
             dof_armature=m.dof_armature, dof_invweight0=m.dof_invweight0,
             lim_range=np.append(m.jnt_range[lim].reshape(-1), [0.0, 0.0]), geom_pos=m.geom_pos, geom_lmat=geom_lmat,
@@ -212,6 +214,7 @@ class DeviceModel:
         s.solref[:] = m.opt.solref
         s.solimp[:] = m.opt.solimp
         s.total_mass = float(m.body_mass[1:].sum())
+        s.nkintree = m.ntree
         s.hf_spacing = m.hfield_spacing
         s.hf_origin[:] = m.hfield_origin
         s.hf_max = float(m.hfield_data.max())
@@ -243,10 +246,11 @@ class DeviceModel:
         cdof = out["cdof"][0].double().cpu().numpy()
         xpos = out["xpos"][0].double().cpu().numpy()
         xquat = out["xquat"][0].double().cpu().numpy()
-        com = out["com"][0].double().cpu().numpy()
+        coms = out["com"][0].double().cpu().numpy()
         jac = [np.zeros((3, m.nv))]
         for b in range(1, m.nbody):
             p = xpos[b] + quat2mat(xquat[b]) @ m.body_ipos[b]
+            com = coms[m.body_treeid[b]]
             J = np.zeros((3, m.nv))
             for dd in m.body_chain[b]:
                 J[:, dd] = cdof[dd, 3:] + np.cross(cdof[dd, :3], p - com)
@@ -293,7 +297,8 @@ class Data:
             np_ = m.nv * (m.nv + 1) // 2
             z = lambda *s: torch.zeros(*s, dtype=dt, device=dev)  # noqa: E731
             zi = lambda *s: torch.zeros(*s, dtype=torch.int32, device=dev)  # noqa: E731
-            self._out = dict(xpos=z(n, m.nbody, 3), xquat=z(n, m.nbody, 4), com=z(n, 3), cdof=z(n, m.nv, 6),
+            self._out = dict(xpos=z(n, m.nbody, 3), xquat=z(n, m.nbody, 4), com=z(n, N.S3_MAX_TREE, 3),
+                             cdof=z(n, m.nv, 6),
                              qM=z(n, np_), qLD=z(n, np_), qfrc_bias=z(n, m.nv), qfrc_smooth=z(n, m.nv),
                              qacc_smooth=z(n, m.nv), qacc=z(n, m.nv), qfrc_constraint=z(n, m.nv),
                              ncon=zi(n), ndropped=zi(n), nefc=zi(n), con_pair=zi(n, MAX_CON),

@@ -35,6 +35,7 @@ MAX_NBODY = 64
 MAX_CHAIN = 32
 MAX_CON = 16
 MAX_LIM = 32
+MAX_TREE = 4
 
 
 class ModelError(ValueError):
@@ -231,8 +232,13 @@ class Model:
             depth[i] = depth[p] + 1
         self.body_rootid = root
         self.body_depth = depth
-        if len(set(root[1:].tolist())) > 1:
-            raise ModelError("one kinematic tree per model (a single robot)")
+        # kinematic trees (a robot, a free object, ...): each uses its own subtree com as c-frame origin
+        roots = sorted(set(root[1:].tolist()))
+        if len(roots) > MAX_TREE:
+            raise ModelError(f"{len(roots)} kinematic trees exceed MAX_TREE={MAX_TREE}")
+        self.ntree = len(roots)
+        self.body_treeid = np.array([roots.index(root[i]) if i > 0 else 0 for i in range(nb)], dtype=np.int32)
+        self.tree_mass = np.array([self.body_mass[1:][self.body_treeid[1:] == t].sum() for t in range(self.ntree)])
 
         # joints, qpos / dof addresses (body order)
         jorder = [j for bd in b.bodies for j in bd.joints]
@@ -362,8 +368,9 @@ class Model:
                 if t1 in (GEOM_PLANE, GEOM_HFIELD):
                     if t2 not in (GEOM_SPHERE, GEOM_CAPSULE, GEOM_BOX):
                         continue
-                elif not (t1 in (GEOM_SPHERE, GEOM_CAPSULE) and t2 in (GEOM_SPHERE, GEOM_CAPSULE)):
-                    continue  # supported self pairs: sphere/capsule x sphere/capsule
+                elif not ((t1 in (GEOM_SPHERE, GEOM_CAPSULE) and t2 in (GEOM_SPHERE, GEOM_CAPSULE)) or
+                          (t1 == GEOM_SPHERE and t2 == GEOM_BOX)):
+                    continue  # supported pairs: sphere/capsule x sphere/capsule, sphere x box
                 pairs.append((g1, g2))
         self.npair = len(pairs)
         self.pair_geom = np.array(pairs, dtype=np.int32).reshape(-1, 2)

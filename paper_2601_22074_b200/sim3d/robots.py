@@ -190,3 +190,64 @@ def default_qpos(model, table: dict) -> np.ndarray:
         if best is not None:
             q[model.jnt_qposadr[j]] = table[best]
     return q
+
+
+ARM_DEFAULT_JOINTS = {"shoulder_yaw": 0.0, "shoulder_pitch": -0.5, "elbow": 1.1, "wrist_pitch": 0.971,
+                      "wrist_roll": 0.0, "hand_yaw": 0.0, "finger_left": 0.3, "finger_right": -0.3}
+
+
+def arm_cube_like(opt: Opt | None = None, cube_size: float = 0.025):
+    """A fixed-base 6-dof arm with a two-finger claw (hinged fingers, sphere fingertips) on a table
+    (the plane) and a free cube (BASELINE configs[3], cube lift). Two kinematic trees: the arm and the
+    cube. Collision filter: arm links touch the table only; fingertip spheres touch the cube (sphere-box);
+    the cube touches the table (box corners)."""
+    b = ModelBuilder("arm_cube_like", opt)
+    b.plane(friction=1.0)
+    base = b.body("link0", 0, pos=(0, 0, 0), mass=2.0, inertia=(0.01, 0.01, 0.01))
+    b.geom(base, GEOM_CAPSULE, (0.06,), fromto=(0, 0, 0.0, 0, 0, 0.1), name="base")
+    l1 = b.body("link1", base, pos=(0, 0, 0.1), mass=2.0, inertia=(0.01, 0.01, 0.005), ipos=(0, 0, 0.12))
+    b.hinge(l1, (0, 0, 1), name="shoulder_yaw", range=(-2.9, 2.9), armature=0.05, damping=1.0)
+    b.geom(l1, GEOM_CAPSULE, (0.05,), fromto=(0, 0, 0.0, 0, 0, 0.25))
+    l2 = b.body("link2", l1, pos=(0, 0, 0.25), mass=2.0, inertia=(0.005, 0.03, 0.03), ipos=(0.2, 0, 0))
+    b.hinge(l2, (0, 1, 0), name="shoulder_pitch", range=(-1.8, 1.8), armature=0.05, damping=1.0)
+    b.geom(l2, GEOM_CAPSULE, (0.045,), fromto=(0.0, 0, 0, 0.4, 0, 0))
+    l3 = b.body("link3", l2, pos=(0.4, 0, 0), mass=1.5, inertia=(0.004, 0.02, 0.02), ipos=(0.17, 0, 0))
+    b.hinge(l3, (0, 1, 0), name="elbow", range=(-0.2, 2.8), armature=0.05, damping=1.0)
+    b.geom(l3, GEOM_CAPSULE, (0.04,), fromto=(0.0, 0, 0, 0.35, 0, 0))
+    l4 = b.body("link4", l3, pos=(0.35, 0, 0), mass=0.6, inertia=(0.001, 0.001, 0.001), ipos=(0.03, 0, 0))
+    b.hinge(l4, (0, 1, 0), name="wrist_pitch", range=(-2.0, 2.0), armature=0.02, damping=0.5)
+    l5 = b.body("link5", l4, pos=(0.05, 0, 0), mass=0.4, inertia=(0.0008, 0.0008, 0.0008), ipos=(0.03, 0, 0))
+    b.hinge(l5, (1, 0, 0), name="wrist_roll", range=(-2.9, 2.9), armature=0.02, damping=0.5)
+    b.geom(l5, GEOM_CAPSULE, (0.035,), fromto=(0.0, 0, 0, 0.05, 0, 0))
+    hand = b.body("hand", l5, pos=(0.05, 0, 0), mass=0.5, inertia=(0.001, 0.001, 0.001), ipos=(0.03, 0, 0))
+    b.hinge(hand, (1, 0, 0), name="hand_yaw", range=(-2.9, 2.9), armature=0.02, damping=0.5)
+    b.geom(hand, GEOM_CAPSULE, (0.03,), fromto=(0.0, -0.04, 0, 0.0, 0.04, 0), name="palm")
+    for side, sy in (("left", 1.0), ("right", -1.0)):
+        f = b.body(f"finger_{side}_link", hand, pos=(0.03, 0.03 * sy, 0), mass=0.05, inertia=(1e-5, 1e-5, 1e-5),
+                   ipos=(0.04, 0, 0))
+        b.hinge(f, (0, 0, 1), name=f"finger_{side}", range=(-0.6, 0.6), armature=0.005, damping=0.1)
+        b.geom(f, GEOM_CAPSULE, (0.008,), fromto=(0.0, 0, 0, 0.07, 0, 0), name=f"{side}_finger")
+        b.geom(f, GEOM_SPHERE, (0.012,), pos=(0.08, -0.005 * sy, 0), name=f"{side}_tip")
+    cube = b.body("cube", 0, pos=(0.55, 0.0, cube_size), mass=0.1,
+                  inertia=(0.1 * (2 * cube_size) ** 2 / 6,) * 3)
+    b.free_joint(cube)
+    b.geom(cube, GEOM_BOX, (cube_size, cube_size, cube_size), friction=1.0, name="cube")
+    # collision filter: table (1), arm (2), fingertips (2|8), cube (4, affinity 1|8)
+    for g in b.geoms:
+        if g["type"] == 0:
+            g["contype"], g["conaffinity"] = 1, 1
+        elif g.get("name") == "base":
+            g["contype"], g["conaffinity"] = 0, 0  # static: never collides
+        elif g.get("name") == "cube":
+            g["contype"], g["conaffinity"] = 4, 1 | 8
+        elif g.get("name", "") and g["name"].endswith("_tip"):
+            g["contype"], g["conaffinity"] = 2 | 8, 1
+        else:
+            g["contype"], g["conaffinity"] = 2, 1
+    gains = {"finger": dict(kp=40.0, kv=2.0, effort=20.0)}
+    for j in b.joints:
+        if j["type"] != 3:
+            continue
+        g = gains["finger"] if j["name"].startswith("finger") else dict(kp=300.0, kv=30.0, effort=150.0)
+        b.actuator(j["name"], kind=ACT_IMPLICIT, **g)
+    return b.compile()

@@ -26,13 +26,40 @@ ROBOTS = {
     "g1_flat": (lambda: robots.g1_like(), robots.G1_DEFAULT_JOINTS),
     "g1_rough": (lambda: robots.g1_like(rough=True, seed=3), robots.G1_DEFAULT_JOINTS),
     "go1_flat": (lambda: robots.go1_like(), robots.GO1_DEFAULT_JOINTS),
+    "arm_cube": (lambda: robots.arm_cube_like(), robots.ARM_DEFAULT_JOINTS),
 }
+
+
+def _arm_states(m, table, n, rng):
+    """Arm near its default pose; the cube on the table (pressed), between the fingertips, or lifted."""
+    q0 = robots.default_qpos(m, table)
+    Q, V = [], []
+    hinge = m.jnt_qposadr[m.jnt_type == 3]
+    K = O.kinematics(m, q0)
+    tips = [g for g in range(m.ngeom) if m.geom_type[g] == 2]
+    mid = K["geom_xpos"][tips].mean(0)
+    for w in range(n):
+        q = q0.copy()
+        q[hinge] += rng.uniform(-0.05, 0.05, size=hinge.size)
+        if w % 3 == 0:
+            q[-7:-4] = (0.55 + rng.uniform(-0.05, 0.05), rng.uniform(-0.05, 0.05), 0.025 - 0.003)
+        else:  # cube between / against the fingertips
+            q[-7:-4] = mid + rng.uniform(-0.01, 0.01, size=3)
+        if w % 4 == 3:  # a joint past its limit
+            j = np.nonzero(m.jnt_limited)[0][w % m.nlim]
+            q[m.jnt_qposadr[j]] = m.jnt_range[j][w % 2] + (0.05 if w % 2 else -0.05)
+        Q.append(q)
+        V.append(rng.normal(size=m.nv) * 0.2)
+    ctrl = np.array([q0[m.actuator_qposadr] + rng.uniform(-0.1, 0.1, size=m.nu) for _ in range(n)])
+    return np.array(Q), np.array(V), ctrl
 
 
 def _states(m, table, n, seed):
     """Standing poses pressed into the ground, jittered joints, random velocities; some worlds tilted
     and sunk deep so that limits, self contacts and many terrain contacts occur."""
     rng = np.random.default_rng(seed)
+    if m.name == "arm_cube_like":
+        return _arm_states(m, table, n, rng)
     q0 = robots.default_qpos(m, table)
     K = O.kinematics(m, q0)
     low = min(K["geom_xpos"][g][2] - m.geom_rbound[g] for g in range(1, m.ngeom))
@@ -115,7 +142,7 @@ def test_single_substep_f64_all_stages(name):
         K, Cc = F["K"], F["C"]
         np.testing.assert_allclose(out["xpos"][w], K["xpos"], atol=1e-12)
         np.testing.assert_allclose(out["xquat"][w], K["xquat"], atol=1e-12)
-        np.testing.assert_allclose(out["com"][w], Cc["com"], atol=1e-12)
+        np.testing.assert_allclose(out["com"][w][:m.ntree], Cc["com"], atol=1e-12)
         np.testing.assert_allclose(out["cdof"][w], Cc["cdof"], atol=1e-12)
         Mg = unpack_lower(out["qM"][w], m.nv)
         assert _rel(Mg, F["M"]) < 1e-12
@@ -148,7 +175,7 @@ def test_single_substep_f64_all_stages(name):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["g1_rough", "go1_flat"])
+@pytest.mark.parametrize("name", ["g1_rough", "go1_flat", "arm_cube"])
 def test_rollout_f64(name):
     import torch
 

@@ -43,7 +43,7 @@ def _random_state(m, rng, scale=0.5):
     return q, v
 
 
-MODELS = {"g1": robots.g1_like, "go1": robots.go1_like, "arm": _arm}
+MODELS = {"g1": robots.g1_like, "go1": robots.go1_like, "arm": _arm, "arm_cube": robots.arm_cube_like}
 
 
 @pytest.fixture(params=list(MODELS))
@@ -250,9 +250,13 @@ def test_ball_comes_to_rest_on_plane_and_forces_in_cone():
 
 def test_newton_optimality(model, rng):
     m = model
-    q = robots.default_qpos(m, robots.G1_DEFAULT_JOINTS if m.name == "g1_like" else robots.GO1_DEFAULT_JOINTS) \
-        if m.name != "arm" else m.qpos0.copy()
-    if m.name != "arm":  # press the lowest geom 5 mm into the ground
+    if m.name == "arm_cube_like":  # cube pressed 3 mm into the table right under the open claw
+        q = robots.default_qpos(m, robots.ARM_DEFAULT_JOINTS)
+        q[-5] -= 0.003
+    else:
+        q = robots.default_qpos(m, robots.G1_DEFAULT_JOINTS if m.name == "g1_like" else robots.GO1_DEFAULT_JOINTS) \
+            if m.name != "arm" else m.qpos0.copy()
+    if m.name not in ("arm", "arm_cube_like"):  # press the lowest geom 5 mm into the ground
         K = O.kinematics(m, q)
         low = min(K["geom_xpos"][g][2] - m.geom_rbound[g] for g in range(1, m.ngeom))
         q[2] -= low + 0.005
@@ -337,3 +341,45 @@ def test_self_collision_pairs_generate_contacts():
     assert self_pairs, "crossed legs must touch"
     for c in self_pairs:
         assert m.geom_type[c["geom1"]] == GEOM_CAPSULE and c["dist"] < 0
+
+
+def test_sphere_box_contact_brute_force(rng):
+    """Sphere-box distance equals the brute-force distance from the sphere centre to the box minus r
+    (outside), and the normal points from the sphere into the box."""
+    R = O.qmat(O.qnormalize(rng.normal(size=4)))
+    size = np.array([0.05, 0.03, 0.02])
+    bc = rng.normal(size=3)
+    for _ in range(40):
+        c = bc + rng.normal(size=3) * 0.06
+        d, n, pos = O.sphere_box(c, 0.01, bc, R, size)
+        g = np.stack(np.meshgrid(*[np.linspace(-s, s, 41) for s in size], indexing="ij"), -1).reshape(-1, 3)
+        pts = bc + g @ R.T
+        p = R.T @ (c - bc)
+        if np.all(np.abs(p) <= size):
+            assert d < -0.01 + 1e-12
+        else:
+            brute = np.min(np.linalg.norm(pts - c, axis=1)) - 0.01
+            assert abs(d - brute) < 2e-3
+            assert np.dot(n, bc - c) > 0
+        assert abs(np.linalg.norm(n) - 1) < 1e-12
+
+
+def test_two_trees_arm_and_cube():
+    """Fixed-base arm + free cube: per-tree com, block-diagonal M across trees, and the cube resting
+    on the table with its weight carried by the contacts."""
+    m = robots.arm_cube_like()
+    O.set_const(m)
+    assert m.ntree == 2
+    q = robots.default_qpos(m, robots.ARM_DEFAULT_JOINTS)
+    v = np.zeros(m.nv)
+    F = O.forward(m, q, v, q[m.actuator_qposadr])
+    arm = [d for d in range(m.nv) if m.body_treeid[m.dof_bodyid[d]] == 0]
+    cube = [d for d in range(m.nv) if m.body_treeid[m.dof_bodyid[d]] == 1]
+    assert np.all(F["M"][np.ix_(arm, cube)] == 0)
+    np.testing.assert_allclose(F["C"]["com"][1], q[-7:-4], atol=1e-12)  # the cube's com is its centre
+    warm = None
+    for _ in range(100):
+        q, v, warm, F = O.step(m, q, v, q[m.actuator_qposadr] * 0 + F["qfrc_actuator"][m.actuator_dofadr] * 0
+                               + robots.default_qpos(m, robots.ARM_DEFAULT_JOINTS)[m.actuator_qposadr], warm=warm)
+    cube_contacts = [c for c in F["contacts"] if m.geom_bodyid[c["geom2"]] == m.body_names.index("cube")]
+    assert len(cube_contacts) == 4 and abs(q[-5] - 0.025) < 1e-3
