@@ -328,6 +328,37 @@ def sim3d_leg(args, flush, stream) -> dict:
         t = timed_steps(env, steps, flush, stream, lambda i: acts[3 + i])
         out["motion"][dtype] = {"value": nm * steps / t, "ms_per_step": 1e3 * t / steps}
         del env
+    # BASELINE configs[3]: arm cube lift with dense contacts + a palm depth camera rendered every step
+    from paper_2601_22074_b200.sim3d.sensors import DepthCamera
+    from paper_2601_22074_b200.sim3d.task import LiftTaskCfg
+
+    out["lift"] = {"workload": f"fixed-base 6-dof arm + claw, free cube (2 kinematic trees), cube lift, {n} worlds/GPU, "
+                               "decimation 4, + 32x24 palm depth camera rendered every control step"}
+    for dtype in ("f32", "f64"):
+        m = robots.arm_cube_like()
+        cfg = LiftTaskCfg.for_model(m, robots.default_qpos(m, robots.ARM_DEFAULT_JOINTS))
+        env = VelocityEnv3D(m, cfg, n, seed=args.seed, world_offset=int(os.environ.get("RANK", "0")) * n, dtype=dtype)
+        env.data.enable_geom_frames()
+        palm = [g for g in range(m.ngeom) if m.geom_bodyid[g] == m.body_names.index("hand")][0]
+        cam = DepthCamera(env.dm, palm, width=32, height=24, fovy=1.2, max_dist=1.0)
+        env.reset()
+
+        class _WithDepth:
+            def step(self, a, env=env, cam=cam):
+                env.step(a)
+                cam.render(env.data)
+
+        steps = 10
+        g = torch.Generator(device="cuda")
+        g.manual_seed(args.seed + 2)
+        acts = torch.rand(steps + 3, n, m.nu, generator=g, device="cuda", dtype=env.dm.tdtype) * 2 - 1
+        for i in range(3):
+            _WithDepth().step(acts[i])
+        t = timed_steps(_WithDepth(), steps, flush, stream, lambda i: acts[3 + i])
+        t_env = timed_steps(env, steps, flush, stream, lambda i: acts[3 + i])
+        out["lift"][dtype] = {"value": n * steps / t, "ms_per_step": 1e3 * t / steps,
+                              "env_only_ms_per_step": 1e3 * t_env / steps}
+        del env, cam
     out["kernel"] = "s3::env_kernel (warp per world, shared-memory resident; one launch per control step)"
     out["parity"] = "oracle/sim3d.py (tests/test_gpu_sim3d*.py); unpinned w.r.t. the reference (no 3-D engine)"
     if not args.no_cpu:
@@ -442,7 +473,7 @@ def run_ours(args):
     scale = at_scale(args, flush, stream) if (world == 1 and args.scale_envs > 0) else None
     s3 = None if args.no_sim3d else sim3d_leg(args, flush, stream)
     if s3 is not None:
-        for blk in (s3, s3["motion"]):
+        for blk in (s3, s3["motion"], s3["lift"]):
             for k in ("f32", "f64"):
                 blk[k]["value"] = blk[k]["value"] * world  # whole job: every rank steps its shard (weak scaling)
                 blk[k]["ms_per_step"] = allmax(blk[k]["ms_per_step"], world)

@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define S3_ABI_VERSION 9
+#define S3_ABI_VERSION 10
 #define S3_F64 0
 #define S3_F32 1
 
@@ -209,7 +209,7 @@ typedef struct s3_layout {
 /* Fused velocity-tracking task (paper_2601_22074_b200/sim3d/task.py): configuration + per-world
  * task state (device pointers, `dtype` elements unless noted). */
 typedef struct s3_task {
-    int32_t kind; /* 0 velocity tracking, 1 motion imitation (reference-motion command) */
+    int32_t kind; /* 0 velocity tracking, 1 motion imitation (reference-motion command), 2 cube lift */
     int32_t decimation;
     int32_t episode_steps;
     int32_t cmd_resample_steps;
@@ -238,6 +238,16 @@ typedef struct s3_task {
     double max_height_error;
     double max_ori_error;
     double motion_start_frac;
+    int32_t cube_qposadr;
+    int32_t tip_geom[2];
+    int32_t pad2;
+    double cube_half;
+    double reach_std;
+    double goal_std;
+    double lift_height;
+    double min_cube_z;
+    double cube_x[2];
+    double cube_y[2];
     const void* motion_qpos; /* (nframes, nq) */
     const void* motion_qvel; /* (nframes, nv) */
     const void* default_qpos;

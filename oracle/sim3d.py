@@ -1146,3 +1146,98 @@ class MotionTaskOracle(TaskOracle):
             if term[w] or trunc[w]:
                 self.reset_world(w, ctr)
         return self.observe(ctr), rew, term, trunc
+
+
+# ----------------------------------------------------------------------------- cube lift task (3-D)
+# kind = lift (BASELINE configs[3], mjlab's manipulation example): reach the cube with the claw, lift it
+# above lift_height, carry it to a goal; cmd[w] = goal position.
+
+
+class LiftTaskOracle(TaskOracle):
+    def _ee(self, q):
+        K = kinematics(self.m, q)
+        return K["geom_xpos"][list(self.cfg.tip_geoms)].mean(0)
+
+    def reset_world(self, w, ctr):
+        m, cfg = self.m, self.cfg
+        kr = self.key(w, 1)
+        q = self.default.copy()
+        ca = cfg.cube_qposadr
+        hinge = [a for a in m.jnt_qposadr[m.jnt_type == 3]]
+        for i, a in enumerate(hinge):
+            q[a] += cfg.reset_joint_jitter * (2.0 * uniform(kr, ctr * 256 + i) - 1.0)
+        q[ca] = cfg.cube_x[0] + (cfg.cube_x[1] - cfg.cube_x[0]) * uniform(kr, ctr * 256 + 200)
+        q[ca + 1] = cfg.cube_y[0] + (cfg.cube_y[1] - cfg.cube_y[0]) * uniform(kr, ctr * 256 + 201)
+        q[ca + 2] = cfg.cube_half
+        yaw = np.pi * (2.0 * uniform(kr, ctr * 256 + 202) - 1.0)
+        q[ca + 3:ca + 7] = (np.cos(0.5 * yaw), 0.0, 0.0, np.sin(0.5 * yaw))
+        self.qpos[w] = q
+        self.qvel[w] = 0.0
+        self.warm[w] = 0.0
+        self.action[w] = 0.0
+        self.prev_action[w] = 0.0
+        self.episode_step[w] = 0
+        self.ep_return[w] = 0.0
+        kc = self.key(w, 2)
+        for i, (lo, hi) in enumerate(cfg.goal_ranges):
+            self.cmd[w, i] = lo + (hi - lo) * uniform(kc, ctr * 4 + i)
+        self.cmd_timer[w] = 0
+
+    def resample(self, w, ctr):
+        pass
+
+    def observe(self, ctr):
+        m, cfg = self.m, self.cfg
+        act, dofs = m.actuator_qposadr, m.actuator_dofadr
+        ca = cfg.cube_qposadr
+        out = np.zeros((self.n, cfg.obs_dim(m)))
+        for w in range(self.n):
+            q = self.qpos[w]
+            o = np.concatenate([q[act] - self.act_default, self.qvel[w][dofs], q[ca:ca + 3], q[ca + 3:ca + 7],
+                                self._ee(q), self.cmd[w], self.action[w]])
+            ko = self.key(w, 3)
+            scales = cfg.noise_vector(m)
+            for i in range(o.size):
+                if scales[i] > 0.0:
+                    o[i] += scales[i] * (2.0 * uniform(ko, ctr * 1024 + i) - 1.0)
+            out[w] = o
+        return out
+
+    def step(self, actions):
+        m, cfg = self.m, self.cfg
+        self.global_step += 1
+        ctr = self.global_step
+        dtc = m.opt.timestep * cfg.decimation
+        rew = np.zeros(self.n)
+        term = np.zeros(self.n, dtype=bool)
+        trunc = np.zeros(self.n, dtype=bool)
+        ca, dofs = cfg.cube_qposadr, m.actuator_dofadr
+        for w in range(self.n):
+            a = np.clip(actions[w], -cfg.action_clip, cfg.action_clip)
+            self.prev_action[w] = self.action[w]
+            self.action[w] = a
+            ctrl = self.act_default + cfg.action_scale * a
+            q, v, warm = self.qpos[w], self.qvel[w], self.warm[w]
+            for _ in range(cfg.decimation):
+                q, v, warm, _ = step(m, q, v, ctrl, warm=warm)
+            self.qpos[w], self.qvel[w], self.warm[w] = q, v, warm
+            ee = self._ee(q)
+            cube = q[ca:ca + 3]
+            d_ee = np.sqrt(np.sum((ee - cube) ** 2))
+            lifted = 1.0 if cube[2] > cfg.lift_height else 0.0
+            d_goal = np.sqrt(np.sum((cube - self.cmd[w]) ** 2))
+            terms = (1.0 - np.tanh(d_ee / cfg.reach_std), lifted, lifted * (1.0 - np.tanh(d_goal / cfg.goal_std)),
+                     float(np.sum((self.action[w] - self.prev_action[w]) ** 2)), float(np.sum(v[dofs] ** 2)), 0.0)
+            r = 0.0
+            for wt, t in zip(cfg.reward_weights, terms):
+                r += wt * t * dtc
+            rew[w] = r
+            self.ep_return[w] += r
+            nonfinite = not (np.all(np.isfinite(q)) and np.all(np.isfinite(v)))
+            term[w] = bool(cube[2] < cfg.min_cube_z or nonfinite)
+            self.episode_step[w] += 1
+            trunc[w] = bool(self.episode_step[w] >= cfg.episode_steps)
+        for w in range(self.n):
+            if term[w] or trunc[w]:
+                self.reset_world(w, ctr)
+        return self.observe(ctr), rew, term, trunc

@@ -1770,6 +1770,137 @@ __device__ __noinline__ void motion_post(const s3_model& m, const s3_task& tk, c
     for (int i = lane; i < nv; i += 32) gv[i] = s.qvel[i];
 }
 
+// ---- cube lift (kind 2): cmd = goal position; claw position = mean of the two fingertip spheres
+
+template <class T>
+__device__ __noinline__ void lift_ee(const s3_model& m, const s3_task& tk, const s3_layout& L_, T* B_, T* ee, int lane) {
+    WS<T> s = make_ws(B_, L_);
+    kinematics(m, L_, B_, lane);
+    geom_frames(m, L_, B_, lane);
+    const int g0 = tk.tip_geom[0], g1 = tk.tip_geom[1];
+    for (int k = 0; k < 3; ++k) ee[k] = T(0.5) * (s.gpos[3 * g0 + k] + s.gpos[3 * g1 + k]);
+}
+
+template <class T>
+__device__ __noinline__ void lift_reset(const s3_model& m, const s3_task& tk, const s3_layout& L_, T* B_, int64_t w,
+                                        uint64_t ctr, T* cmd, int lane) {
+    WS<T> s = make_ws(B_, L_);
+    const T* dq = static_cast<const T*>(tk.default_qpos);
+    uint64_t kr = stream_key(tk.seed, tk.world_offset + w, 1);
+    for (int i = lane; i < m.nq; i += 32) s.qpos[i] = dq[i];
+    __syncwarp();
+    int nh = 0;  // hinge index among hinge joints, in joint order (the oracle's enumeration)
+    for (int j = 0; j < m.njnt; ++j) {
+        if (m.jnt_type[j] == kJntFree) continue;
+        if ((nh & 31) == lane) {
+            int a = m.jnt_qposadr[j];
+            s.qpos[a] = dq[a] + T(tk.reset_joint_jitter) * (T(2) * uniform01<T>(kr, ctr * 256 + nh) - T(1));
+        }
+        ++nh;
+    }
+    if (lane == 0) {
+        const int ca = tk.cube_qposadr;
+        s.qpos[ca] = T(tk.cube_x[0]) + T(tk.cube_x[1] - tk.cube_x[0]) * uniform01<T>(kr, ctr * 256 + 200);
+        s.qpos[ca + 1] = T(tk.cube_y[0]) + T(tk.cube_y[1] - tk.cube_y[0]) * uniform01<T>(kr, ctr * 256 + 201);
+        s.qpos[ca + 2] = T(tk.cube_half);
+        T yaw = T(3.141592653589793) * (T(2) * uniform01<T>(kr, ctr * 256 + 202) - T(1));
+        T sn, cs;
+        sincos_t(T(0.5) * yaw, &sn, &cs);
+        s.qpos[ca + 3] = cs; s.qpos[ca + 4] = T(0); s.qpos[ca + 5] = T(0); s.qpos[ca + 6] = sn;
+    }
+    for (int i = lane; i < m.nv; i += 32) s.qvel[i] = T(0);
+    task_resample(tk, cmd, w, ctr, lane);  // goal ~ U(cmd_lo, cmd_hi), purpose 2
+    __syncwarp();
+}
+
+template <class T>
+__device__ __noinline__ void lift_observe(const s3_model& m, const s3_task& tk, const s3_layout& L_, T* B_, int64_t w,
+                                          uint64_t ctr, const T* cmd, const T* action, int lane) {
+    WS<T> s = make_ws(B_, L_);
+    T ee[3];
+    lift_ee(m, tk, L_, B_, ee, lane);
+    const T* dq = static_cast<const T*>(tk.default_qpos);
+    uint64_t ko = stream_key(tk.seed, tk.world_offset + w, 3);
+    T* out = static_cast<T*>(tk.obs) + w * tk.obs_dim;
+    const int nu = m.nu, ca = tk.cube_qposadr;
+    // [joint pos - default, joint vel, cube pos, cube quat, claw pos, goal, action]
+    for (int i = lane; i < tk.obs_dim; i += 32) {
+        T v, ns = T(0);
+        if (i < nu) {
+            int a = m.act_qposadr[i];
+            v = s.qpos[a] - dq[a];
+            ns = T(tk.noise[4]);
+        } else if (i < 2 * nu) {
+            v = s.qvel[m.act_dofadr[i - nu]];
+            ns = T(tk.noise[5]);
+        } else if (i < 2 * nu + 7) {
+            v = s.qpos[ca + i - 2 * nu];
+        } else if (i < 2 * nu + 10) {
+            v = ee[i - 2 * nu - 7];
+        } else if (i < 2 * nu + 13) {
+            v = cmd[i - 2 * nu - 10];
+        } else {
+            v = action[i - 2 * nu - 13];
+            ns = T(tk.noise[6]);
+        }
+        if (ns > T(0)) v += ns * (T(2) * uniform01<T>(ko, ctr * 1024 + i) - T(1));
+        out[i] = v;
+    }
+}
+
+template <class T>
+__device__ __noinline__ void lift_post(const s3_model& m, const s3_task& tk, const s3_layout& L_, T* B_, int64_t w,
+                                       uint64_t ctr, T* cmd, T* act, T rate, T* gq, T* gv, T* gw, T* prev, int lane) {
+    WS<T> s = make_ws(B_, L_);
+    const int nu = m.nu, nq = m.nq, nv = m.nv, ca = tk.cube_qposadr;
+    const T dtc = T(m.timestep) * T(tk.decimation);
+    T ee[3];
+    lift_ee(m, tk, L_, B_, ee, lane);
+    T cube[3] = {s.qpos[ca], s.qpos[ca + 1], s.qpos[ca + 2]};
+    T de[3] = {ee[0] - cube[0], ee[1] - cube[1], ee[2] - cube[2]};
+    T dg[3] = {cube[0] - cmd[0], cube[1] - cmd[1], cube[2] - cmd[2]};
+    T d_ee = sqrt(dot3(de, de)), d_goal = sqrt(dot3(dg, dg));
+    T lifted = cube[2] > T(tk.lift_height) ? T(1) : T(0);
+    T jv = T(0);
+    for (int i = lane; i < nu; i += 32) {
+        T v = s.qvel[m.act_dofadr[i]];
+        jv += v * v;
+    }
+    jv = wsum(jv);
+    T terms[6] = {T(1) - tanh(d_ee / T(tk.reach_std)), lifted, lifted * (T(1) - tanh(d_goal / T(tk.goal_std))), rate, jv,
+                  T(0)};
+    T r = T(0);
+    for (int k = 0; k < 6; ++k) r += T(tk.reward_weights[k]) * terms[k] * dtc;
+    bool finite = true;
+    for (int i = lane; i < nq; i += 32) finite = finite && isfinite(s.qpos[i]);
+    for (int i = lane; i < nv; i += 32) finite = finite && isfinite(s.qvel[i]);
+    finite = __all_sync(FULL, finite);
+    bool term = cube[2] < T(tk.min_cube_z) || !finite;
+    int es = tk.episode_step[w] + 1;
+    bool trunc = es >= tk.episode_steps;
+    __syncwarp();
+    if (lane == 0) {
+        static_cast<T*>(tk.reward)[w] = r;
+        static_cast<T*>(tk.episode_return)[w] += r;
+        tk.terminated[w] = term;
+        tk.truncated[w] = trunc;
+        tk.episode_step[w] = es;
+    }
+    if (term || trunc) {
+        lift_reset(m, tk, L_, B_, w, ctr, cmd, lane);
+        for (int i = lane; i < nv; i += 32) gw[i] = T(0);
+        for (int i = lane; i < nu; i += 32) { act[i] = T(0); prev[i] = T(0); }
+        if (lane == 0) {
+            tk.episode_step[w] = 0;
+            static_cast<T*>(tk.episode_return)[w] = T(0);
+        }
+    }
+    __syncwarp();
+    lift_observe(m, tk, L_, B_, w, ctr, cmd, act, lane);
+    for (int i = lane; i < nq; i += 32) gq[i] = s.qpos[i];
+    for (int i = lane; i < nv; i += 32) gv[i] = s.qvel[i];
+}
+
 template <class T>
 __global__ void __launch_bounds__(32 * 16) env_kernel(const __grid_constant__ s3_model m, const __grid_constant__ s3_data d,
                                                      const __grid_constant__ s3_layout l,
@@ -1796,6 +1927,8 @@ __global__ void __launch_bounds__(32 * 16) env_kernel(const __grid_constant__ s3
     if (mode == 1) {  // reset every world, counter 0
         if (tk.kind == 1) {
             motion_reset(m, tk, L_, B_, w, 0, cmd, lane);
+        } else if (tk.kind == 2) {
+            lift_reset(m, tk, L_, B_, w, 0, cmd, lane);
         } else {
             task_reset(m, tk, L_, B_, w, 0, lane);
             task_resample(tk, cmd, w, 0, lane);
@@ -1803,12 +1936,13 @@ __global__ void __launch_bounds__(32 * 16) env_kernel(const __grid_constant__ s3
         for (int i = lane; i < nv; i += 32) gw[i] = T(0);
         for (int i = lane; i < nu; i += 32) { act[i] = T(0); prev[i] = T(0); }
         if (lane == 0) {
-            tk.cmd_timer[w] = tk.kind == 1 ? 0 : tk.cmd_resample_steps;
+            tk.cmd_timer[w] = tk.kind == 0 ? tk.cmd_resample_steps : 0;
             tk.episode_step[w] = 0;
             static_cast<T*>(tk.episode_return)[w] = T(0);
         }
         __syncwarp();
         if (tk.kind == 1) motion_observe(m, tk, L_, B_, w, 0, cmd, act, lane);
+        else if (tk.kind == 2) lift_observe(m, tk, L_, B_, w, 0, cmd, act, lane);
         else task_observe(m, tk, L_, B_, w, 0, cmd, act, lane);
         if (d.geom_xpos) store_geom_frames(m, d, L_, B_, w, lane);
         for (int i = lane; i < nq; i += 32) gq[i] = s.qpos[i];
@@ -1832,6 +1966,11 @@ __global__ void __launch_bounds__(32 * 16) env_kernel(const __grid_constant__ s3
     for (int sub = 0; sub < tk.decimation; ++sub) substep(m, d, L_, B_, w, gw, (const T*)nullptr, false, lane);
     if (tk.kind == 1) {
         motion_post(m, tk, L_, B_, w, ctr, cmd, act, rate, gq, gv, gw, prev, lane);
+        return;
+    }
+    if (tk.kind == 2) {
+        lift_post(m, tk, L_, B_, w, ctr, cmd, act, rate, gq, gv, gw, prev, lane);
+        if (d.geom_xpos) store_geom_frames(m, d, L_, B_, w, lane);
         return;
     }
     // rewards, terminations (pre-reset state)
@@ -2148,7 +2287,7 @@ int s3_env_step(const s3_model* m, const s3_data* d, const s3_layout* l, const s
     if (d->nworld == 0) return S3_OK;
     if (!d->qpos || !d->qvel || !d->qacc_warmstart) return fail(S3_ERR_ARG, "qpos/qvel/qacc_warmstart required");
     if (mode == 0 && !actions) return fail(S3_ERR_ARG, "actions required");
-    const int want = t->kind == 1 ? 15 + 5 * m->nu : 12 + 3 * m->nu + t->nscan;
+    const int want = t->kind == 1 ? 15 + 5 * m->nu : (t->kind == 2 ? 13 + 3 * m->nu : 12 + 3 * m->nu + t->nscan);
     if (t->obs_dim != want || t->nscan > S3_MAX_RAYS || t->decimation < 1 ||
         (t->kind == 1 && (t->nframes < 2 || !t->motion_qpos || !t->motion_qvel || m->nq + m->nv > m->nv * (m->nv + 1) / 2)))
         return fail(S3_ERR_ARG, "task layout does not match the model");

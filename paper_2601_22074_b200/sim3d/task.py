@@ -109,6 +109,50 @@ class MotionTrackingCfg:
                         [n[4]] * m.nu + [n[5]] * m.nu + [n[6]] * m.nu)
 
 
+@dataclass
+class LiftTaskCfg:
+    """Cube lift (BASELINE configs[3], mjlab's manipulation example) on ``robots.arm_cube_like``: reach the
+    cube with the claw (tanh kernel), lift it above ``lift_height``, carry it to a per-episode goal
+    (tanh kernel gated by the lift); action-rate and joint-velocity penalties; termination when the cube
+    falls off the table, truncation after ``episode_steps``. ``command`` holds the goal position.
+    Observations: [joint pos - default, joint vel, cube pos, cube quat, claw (mean fingertip) pos, goal,
+    last action]. Pair with sensors.DepthCamera on the palm for the depth stream."""
+    default_qpos: np.ndarray
+    cube_qposadr: int
+    tip_geoms: tuple
+    cube_half: float = 0.025
+    decimation: int = 4
+    action_scale: float = 0.5
+    action_clip: float = 2.0
+    episode_steps: int = 250
+    # reach, lifted, goal tracking, action_rate_l2, joint_vel_l2, (unused)
+    reward_weights: tuple = (1.0, 15.0, 16.0, -1e-4, -1e-4, 0.0)
+    reach_std: float = 0.1
+    goal_std: float = 0.3
+    lift_height: float = 0.04
+    min_cube_z: float = -0.05
+    reset_joint_jitter: float = 0.1
+    cube_x: tuple = (0.45, 0.65)
+    cube_y: tuple = (-0.15, 0.15)
+    goal_ranges: tuple = ((0.45, 0.65), (-0.2, 0.2), (0.2, 0.4))
+    noise: tuple = (0.0, 0.0, 0.0, 0.0, 0.01, 0.05, 0.0)
+    kind: int = 2
+
+    @classmethod
+    def for_model(cls, m: Model, default_qpos: np.ndarray, **kw) -> "LiftTaskCfg":
+        cube = m.body_names.index("cube")
+        j = [k for k in range(m.njnt) if m.jnt_bodyid[k] == cube][0]
+        tips = tuple(g for g in range(m.ngeom) if m.geom_type[g] == 2 and m.geom_bodyid[g] != cube)
+        return cls(default_qpos=default_qpos, cube_qposadr=int(m.jnt_qposadr[j]), tip_geoms=tips, **kw)
+
+    def obs_dim(self, m: Model) -> int:
+        return 13 + 3 * m.nu
+
+    def noise_vector(self, m: Model) -> np.ndarray:
+        n = self.noise
+        return np.array([n[4]] * m.nu + [n[5]] * m.nu + [0.0] * 13 + [n[6]] * m.nu)
+
+
 class VelocityEnv3D:
     """Batched fused 3-D env on the GPU (world index outermost): velocity tracking
     (``VelocityTaskCfg``) or motion imitation (``MotionTrackingCfg``)."""
@@ -137,13 +181,14 @@ class VelocityEnv3D:
         self.global_step = 0
         t = N.TaskT()
         motion = isinstance(cfg, MotionTrackingCfg)
-        t.kind = 1 if motion else 0
+        lift = isinstance(cfg, LiftTaskCfg)
+        t.kind = cfg.kind if (motion or lift) else 0
         t.decimation, t.episode_steps = cfg.decimation, cfg.episode_steps
         t.obs_dim = self.obs_dim
         t.seed = self.seed
         t.world_offset = self.world_offset
         t.action_scale, t.action_clip = cfg.action_scale, cfg.action_clip
-        t.spawn_half_extent = cfg.spawn_half_extent
+        t.spawn_half_extent = getattr(cfg, "spawn_half_extent", 0.0)
         t.reward_weights[:] = cfg.reward_weights
         t.noise[:] = cfg.noise
         if motion:
@@ -154,6 +199,14 @@ class VelocityEnv3D:
             t.motion_sigmas[:] = cfg.motion_sigmas
             t.max_height_error, t.max_ori_error = cfg.max_height_error, cfg.max_ori_error
             t.motion_start_frac = cfg.motion_start_frac
+        elif lift:
+            t.cube_qposadr = cfg.cube_qposadr
+            t.tip_geom[0], t.tip_geom[1] = cfg.tip_geoms
+            t.cube_half, t.reach_std, t.goal_std = cfg.cube_half, cfg.reach_std, cfg.goal_std
+            t.lift_height, t.min_cube_z, t.reset_joint_jitter = cfg.lift_height, cfg.min_cube_z, cfg.reset_joint_jitter
+            t.cube_x[:], t.cube_y[:] = cfg.cube_x, cfg.cube_y
+            for i, (lo, hi) in enumerate(cfg.goal_ranges):
+                t.cmd_lo[i], t.cmd_hi[i] = lo, hi
         else:
             t.cmd_resample_steps = cfg.command_resample_steps
             t.track_sigma = cfg.track_sigma

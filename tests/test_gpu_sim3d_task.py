@@ -200,3 +200,62 @@ def test_motion_imitation_teacher_forced_terminations_and_clip_end():
         saw_term += int(te_ref.sum())
         saw_trunc += int(tr_ref.sum())
     assert saw_term > 0 and saw_trunc > 0
+
+
+def _lift_pair(n, dtype="f64", **over):
+    from paper_2601_22074_b200.sim3d.task import LiftTaskCfg, VelocityEnv3D
+
+    mg, mo = robots.arm_cube_like(), robots.arm_cube_like()
+    cfg = LiftTaskCfg.for_model(mg, robots.default_qpos(mg, robots.ARM_DEFAULT_JOINTS), **over)
+    env = VelocityEnv3D(mg, cfg, n, seed=13, dtype=dtype)
+    O.set_const(mo)
+    return env, O.LiftTaskOracle(mo, cfg, n, seed=13)
+
+
+@pytest.mark.gpu
+def test_cube_lift_free_running_f64():
+    """Cube lift (BASELINE configs[3]): reset, claw/cube/goal observations, reach/lift/goal rewards."""
+    import torch
+
+    n = 8
+    env, ref = _lift_pair(n)
+    np.testing.assert_allclose(env.reset().cpu().numpy(), ref.reset(), atol=1e-12)
+    rng = np.random.default_rng(8)
+    for k in range(4):
+        a = rng.uniform(-1, 1, size=(n, env.model.nu))
+        o, r, te, tr = env.step(torch.as_tensor(a, device="cuda"))
+        o_ref, r_ref, te_ref, tr_ref = ref.step(a)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(te.cpu().numpy().astype(bool), te_ref)
+        np.testing.assert_array_equal(tr.cpu().numpy().astype(bool), tr_ref)
+        np.testing.assert_allclose(r.cpu().numpy(), r_ref, rtol=1e-8, atol=1e-10)
+        np.testing.assert_allclose(o.cpu().numpy(), o_ref, rtol=1e-7, atol=1e-7)
+
+
+@pytest.mark.gpu
+def test_cube_lift_teacher_forced_lift_termination_and_truncation():
+    import torch
+
+    n = 8
+    env, ref = _lift_pair(n, episode_steps=3)
+    env.reset()
+    ref.reset()
+    ca = ref.cfg.cube_qposadr
+    ref.qpos[0, ca + 2] = 0.2     # lifted cube (pays the lift and goal terms while it falls)
+    ref.qpos[1, ca + 2] = -0.2    # cube below the table: terminates
+    rng = np.random.default_rng(9)
+    saw_term = saw_trunc = 0
+    for k in range(5):
+        _load(env, ref)
+        a = rng.uniform(-1, 1, size=(n, env.model.nu))
+        o, r, te, tr = env.step(torch.as_tensor(a, device="cuda"))
+        o_ref, r_ref, te_ref, tr_ref = ref.step(a)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(te.cpu().numpy().astype(bool), te_ref)
+        np.testing.assert_array_equal(tr.cpu().numpy().astype(bool), tr_ref)
+        np.testing.assert_allclose(r.cpu().numpy(), r_ref, rtol=1e-8, atol=1e-10)
+        np.testing.assert_allclose(o.cpu().numpy(), o_ref, rtol=1e-7, atol=1e-7)
+        np.testing.assert_allclose(env.command.cpu().numpy(), ref.cmd, atol=1e-15)
+        saw_term += int(te_ref.sum())
+        saw_trunc += int(tr_ref.sum())
+    assert saw_term > 0 and saw_trunc > 0
