@@ -543,27 +543,24 @@ def chol_solve(L, b):
 
 
 def _cost(E, qfrc_smooth, a, Ma, jar):
+    """1/2 a^T M a - a^T f + sum_i 1/2 D_i min(J_i a - aref_i, 0)^2: the Gauss term
+    1/2 (a-a0)^T M (a-a0) up to the constant 1/2 a0^T f (a0 = M^-1 f), so differences are exact
+    and qacc_smooth is not needed by the solver."""
     act = jar < 0.0
-    gauss = 0.5 * ((a - E["a0"]) @ (Ma - qfrc_smooth))
+    gauss = 0.5 * (a @ (Ma - 2.0 * qfrc_smooth))
     return gauss + 0.5 * np.sum(E["D"][act] * jar[act] ** 2)
 
 
 def newton(m, M, E, qfrc_smooth, a0, warm):
-    """Primal Newton on 1/2 (a-a0)^T M (a-a0) + sum_i 1/2 D_i min(J_i a - aref_i, 0)^2
-    with an exact (bracketed 1-D Newton) line search (mj_solNewton restated)."""
-    E = dict(E, a0=a0)
+    """Primal Newton on 1/2 (a-a0)^T M (a-a0) + sum_i 1/2 D_i min(J_i a - aref_i, 0)^2, started
+    from the warm start (zeros when there is none), with an exact (bracketed 1-D Newton) line search
+    (mj_solNewton restated). ``a0`` is unused by the iteration (see _cost)."""
     J, D, aref = E["J"], E["D"], E["aref"]
     scale = 1.0 / (m.meaninertia * max(1, m.nv))
-    a = a0.copy()
+    a = np.zeros(m.nv) if warm is None else warm.copy()
     Ma = M @ a
     jar = J @ a - aref
     cost = _cost(E, qfrc_smooth, a, Ma, jar)
-    if warm is not None:
-        Mw = M @ warm
-        jw = J @ warm - aref
-        cw = _cost(E, qfrc_smooth, warm, Mw, jw)
-        if cw < cost:
-            a, Ma, jar, cost = warm.copy(), Mw, jw, cw
     its = 0
     for it in range(m.opt.iterations):
         act = jar < 0.0

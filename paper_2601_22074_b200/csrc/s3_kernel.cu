@@ -1151,8 +1151,9 @@ template <class T> __device__ void __noinline__ rows_tmul_add(const s3_model& m,
 template <class T> __device__ T __noinline__ total_cost(const s3_model& m, const s3_layout& L_, T* B_, int nefc, const T* a, const T* Ma,
                                            const T* jar, int lane) {
     WS<T> s = make_ws(B_, L_);
+    // 1/2 a^T M a - a^T f + constraint term: the Gauss term up to a constant (oracle _cost)
     T g = T(0);
-    for (int i = lane; i < m.nv; i += 32) g += (a[i] - s.a0[i]) * (Ma[i] - s.smooth[i]);
+    for (int i = lane; i < m.nv; i += 32) g += a[i] * (Ma[i] - T(2) * s.smooth[i]);
     T c = T(0);
     for (int r = lane; r < nefc; r += 32)
         if (jar[r] < T(0)) c += s.rD[r] * jar[r] * jar[r];
@@ -1166,28 +1167,14 @@ template <class T> __device__ int __noinline__ newton(const s3_model& m, const s
     int nefc = nlim + 4 * ncon;
     T scale = T(m.scale);
     T tol = T(m.tolerance);
-    // a = a0 (a0 currently holds qacc_smooth)
-    for (int i = lane; i < nv; i += 32) s.a[i] = s.a0[i];
+    // start from the warm start (staged in s.p by the caller), zeros without one (oracle newton)
+    for (int i = lane; i < nv; i += 32) s.a[i] = warm_ok ? s.p[i] : T(0);
     __syncwarp();
     sym_mul(nv, s.M, s.a, s.Ma, lane);
     rows_mul(m, L_, B_, ncon, nlim, s.a, s.rjar, lane);
     for (int r = lane; r < nefc; r += 32) s.rjar[r] -= s.raref[r];
     __syncwarp();
     T cost = total_cost(m, L_, B_, nefc, s.a, s.Ma, s.rjar, lane);
-    if (warm_ok) {
-        // candidate: qacc_warmstart staged in s.p; Mw -> s.Mp, jw -> s.rJp
-        sym_mul(nv, s.M, s.p, s.Mp, lane);
-        rows_mul(m, L_, B_, ncon, nlim, s.p, s.rJp, lane);
-        for (int r = lane; r < nefc; r += 32) s.rJp[r] -= s.raref[r];
-        __syncwarp();
-        T cw = total_cost(m, L_, B_, nefc, s.p, s.Mp, s.rJp, lane);
-        if (cw < cost) {
-            for (int i = lane; i < nv; i += 32) { s.a[i] = s.p[i]; s.Ma[i] = s.Mp[i]; }
-            for (int r = lane; r < nefc; r += 32) s.rjar[r] = s.rJp[r];
-            cost = cw;
-            __syncwarp();
-        }
-    }
     // H = M + J^T D J keeps the tree pattern unless a contact couples two branches
     bool tree = true;
     for (int c = 0; c < ncon; ++c) tree = tree && m.pair_tree[s.con_pair[c]] != 0;
@@ -1303,18 +1290,34 @@ template <class T> __device__ int __noinline__ newton(const s3_model& m, const s
             alpha = al;
         }
         if (alpha == T(0)) break;
+        T impv, floor_ = T(0);
+        if (sizeof(T) == 4) {
+            // float32 build: the improvement from its own small terms -- Gauss part alpha g0 + alpha^2 h0 / 2
+            // and the per-row change of the constraint cost -- instead of a difference of two large costs,
+            // and the rounding floor of those terms (the float64 build keeps the oracle's cost difference)
+            T dc = T(0), mg = T(0);
+            for (int r = lane; r < nefc; r += 32) {
+                T x0 = fmin(s.rjar[r], T(0)), x1 = fmin(s.rjar[r] + alpha * s.rJp[r], T(0));
+                dc += s.rD[r] * (x1 * x1 - x0 * x0);
+                mg += s.rD[r] * (x1 * x1 + x0 * x0);
+            }
+            dc = T(0.5) * wsum(dc);
+            mg = T(0.5) * wsum(mg);
+            T dg1 = alpha * g0, dg2 = T(0.5) * alpha * alpha * h0;
+            impv = -scale * ((dg1 + dg2) + dc);
+            floor_ = T(8) * T(1.1920929e-7) * scale * (fabs(dg1) + fabs(dg2) + mg);
+        }
         for (int i = lane; i < nv; i += 32) {
             s.a[i] += alpha * s.p[i];
             s.Ma[i] += alpha * s.Mp[i];
         }
         for (int r = lane; r < nefc; r += 32) s.rjar[r] += alpha * s.rJp[r];
         __syncwarp();
-        T nc = total_cost(m, L_, B_, nefc, s.a, s.Ma, s.rjar, lane);
-        T impv = scale * (cost - nc);
-        cost = nc;
-        // float32 build: an improvement below the rounding floor of the cost itself is noise, not
-        // progress (the float64 build keeps the oracle's exact criterion)
-        T floor_ = sizeof(T) == 4 ? T(8) * T(1.1920929e-7) * scale * fabs(nc) : T(0);
+        if (sizeof(T) != 4) {
+            T nc = total_cost(m, L_, B_, nefc, s.a, s.Ma, s.rjar, lane);
+            impv = scale * (cost - nc);
+            cost = nc;
+        }
         if (impv < tol + floor_) break;
     }
     // forces and qfrc_constraint
@@ -1345,17 +1348,19 @@ __device__ __noinline__ void substep(const s3_model& m, const s3_data& d, const 
     tree_load(m, s.M, s.LD, lane);
     factor_ldl(m, s.LD, s.tk, lane, U, 1);          // subtrees no constraint touches: shared by M and H
     tree_copy(m, s.LD, s.snap, U, true, lane);
-    factor_ldl(m, s.LD, s.tk, lane, U, 2);
     smooth_force(m, L_, B_, gapp, lane);
-    if (last && d.qM) {  // parity outputs of the factor before it is overwritten (tree entries; 0 elsewhere)
+    if (last && d.qM) {
+        // parity outputs only: finish M's factor and qacc_smooth = M^-1 f (the solver does not need them:
+        // Newton starts from the warm start and its first iteration factors H over the touched rows)
+        factor_ldl(m, s.LD, s.tk, lane, U, 2);
         T* o = static_cast<T*>(d.qLD) + w * np;
         const unsigned long long* cm = reinterpret_cast<const unsigned long long*>(m.dof_chainmask);
         for (int i = lane; i < nv; i += 32) {
             uint64_t mk = __ldg(cm + i);
             for (int j = 0; j <= i; ++j) o[tri(i, j)] = ((mk >> j) & 1ull) ? s.LD[tri(i, j)] : T(0);
         }
+        solve_ldl(m, s.LD, s.a0, lane);
     }
-    solve_ldl(m, s.LD, s.a0, lane);
     build_rows(m, L_, B_, ncon, nlim, lane);
     if (gw) {
         for (int i = lane; i < nv; i += 32) s.p[i] = gw[i];
