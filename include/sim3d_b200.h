@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define S3_ABI_VERSION 10
+#define S3_ABI_VERSION 11
 #define S3_F64 0
 #define S3_F32 1
 
@@ -173,6 +173,7 @@ typedef struct s3_data {
     void* qacc_warmstart;
     void* qfrc_applied;
     void* time;
+    void* friction_scale; /* (N,) per-world friction multiplier (domain randomisation), NULL = 1 */
     /* outputs of the LAST substep of a launch (for parity tests / sensors) */
     void* xpos;
     void* xquat;
@@ -248,6 +249,12 @@ typedef struct s3_task {
     double min_cube_z;
     double cube_x[2];
     double cube_y[2];
+    int32_t events; /* velocity kind: 1 = startup friction randomisation + interval pushes */
+    int32_t pad3;
+    double friction_range[2];
+    double push_interval[2];
+    double push_velocity;
+    void* event_timer; /* (N,) time to the next push */
     const void* motion_qpos; /* (nframes, nq) */
     const void* motion_qvel; /* (nframes, nv) */
     const void* default_qpos;

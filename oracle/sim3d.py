@@ -392,15 +392,16 @@ def _point_set(m, K, g):
     return out
 
 
-def collide(m, K):
+def collide(m, K, fscale=1.0):
     """Broadphase (bounding spheres) + narrowphase over the compiled candidate pairs, in pair order;
-    at most MAX_CON contacts (later ones dropped and counted)."""
+    at most MAX_CON contacts (later ones dropped and counted). ``fscale``: the world's friction
+    scale (domain randomisation), multiplying every pair's friction."""
     cons, dropped = [], 0
     hmax = float(m.hfield_data.max())
     for p, (g1, g2) in enumerate(m.pair_geom):
         t1, t2 = m.geom_type[g1], m.geom_type[g2]
         c1, c2 = K["geom_xpos"][g1], K["geom_xpos"][g2]
-        mu = max(m.geom_friction[g1], m.geom_friction[g2])
+        mu = max(m.geom_friction[g1], m.geom_friction[g2]) * fscale
         found = []
         if t1 == GEOM_PLANE:
             n = K["geom_xmat"][g1][:, 2]
@@ -638,7 +639,7 @@ def integrate_pos(m, qpos, qvel, dt):
     return q
 
 
-def forward(m, qpos, qvel, ctrl, qfrc_applied=None, warm=None):
+def forward(m, qpos, qvel, ctrl, qfrc_applied=None, warm=None, fscale=1.0):
     """Everything of one substep up to (and including) the constraint solve."""
     K = kinematics(m, qpos)
     C = com_pos(m, K)
@@ -651,7 +652,7 @@ def forward(m, qpos, qvel, ctrl, qfrc_applied=None, warm=None):
     if qfrc_applied is not None:
         smooth = smooth + qfrc_applied
     a0 = solve_ldl(m, L, smooth)
-    cons, dropped = collide(m, K)
+    cons, dropped = collide(m, K, fscale)
     E = constraints(m, C, cons, qpos, qvel)
     qacc, force, qfrc_con, its = newton(m, M, E, smooth, a0, warm)
     return dict(K=K, C=C, M=M, qLD=L, crb=crbs, cvel=cvel, cdofd=cdofd, bias=bias, qfrc_actuator=fact, kvd=kvd,
@@ -659,11 +660,11 @@ def forward(m, qpos, qvel, ctrl, qfrc_applied=None, warm=None):
                 efc_force=force, qfrc_constraint=qfrc_con, iterations=its)
 
 
-def step(m, qpos, qvel, ctrl, qfrc_applied=None, warm=None):
+def step(m, qpos, qvel, ctrl, qfrc_applied=None, warm=None, fscale=1.0):
     """One substep: forward, implicitfast velocity update, position integration.
     Returns (qpos, qvel, qacc_warmstart, forward-dict)."""
     dt = m.opt.timestep
-    F = forward(m, qpos, qvel, ctrl, qfrc_applied, warm)
+    F = forward(m, qpos, qvel, ctrl, qfrc_applied, warm, fscale)
     Mt = F["M"].copy()
     Mt[np.diag_indices(m.nv)] += dt * (m.dof_damping + F["kvd"])
     Lt = factor_ldl(m, Mt)
@@ -747,6 +748,11 @@ class TaskOracle:
         self.ep_return = np.zeros(nworld)
         self.global_step = 0
         self.act_default = self.default[act]
+        self.fscale = np.ones(nworld)          # startup event: per-world friction scale
+        self.ev_timer = np.zeros(nworld)       # interval event: time to the next push
+
+    def _events_on(self):
+        return getattr(self.cfg, "push_interval", None) is not None
 
     def key(self, w, purpose):
         return stream_key(self.seed, self.off + w, purpose)
@@ -771,6 +777,8 @@ class TaskOracle:
         self.episode_step[w] = 0
         self.ep_return[w] = 0.0
         self.resample(w, ctr)
+        if self._events_on():
+            self.draw_push_timer(w, ctr, 1)
 
     def resample(self, w, ctr):
         kc = self.key(w, 2)
@@ -779,9 +787,17 @@ class TaskOracle:
         self.cmd_timer[w] = self.cfg.command_resample_steps
 
     def reset(self):
+        if self._events_on():  # startup randomisation (purpose 5, counter 0, slot 0)
+            lo, hi = self.cfg.friction_range
+            for w in range(self.n):
+                self.fscale[w] = lo + (hi - lo) * uniform(self.key(w, 5), 0)
         for w in range(self.n):
             self.reset_world(w, 0)
         return self.observe(0)
+
+    def draw_push_timer(self, w, ctr, slot):
+        lo, hi = self.cfg.push_interval
+        self.ev_timer[w] = lo + (hi - lo) * uniform(self.key(w, 5), ctr * 8 + slot)
 
     def observe(self, ctr):
         m, cfg = self.m, self.cfg
@@ -833,7 +849,7 @@ class TaskOracle:
             ctrl = self.act_default + cfg.action_scale * a
             q, v, warm = self.qpos[w], self.qvel[w], self.warm[w]
             for _ in range(cfg.decimation):
-                q, v, warm, _ = step(m, q, v, ctrl, warm=warm)
+                q, v, warm, _ = step(m, q, v, ctrl, warm=warm, fscale=self.fscale[w])
             self.qpos[w], self.qvel[w], self.warm[w] = q, v, warm
             vb, om, g, _ = base_frame(m, q, v)
             e_xy = (self.cmd[w, 0] - vb[0]) ** 2 + (self.cmd[w, 1] - vb[1]) ** 2
@@ -857,6 +873,13 @@ class TaskOracle:
                 self.cmd_timer[w] -= 1
                 if self.cmd_timer[w] <= 0:
                     self.resample(w, ctr)
+            if self._events_on():  # interval push (every world, after resets/commands)
+                self.ev_timer[w] -= dtc
+                if self.ev_timer[w] <= 0.0:
+                    k5, pv = self.key(w, 5), cfg.push_velocity
+                    self.qvel[w, 0] += pv * (2.0 * uniform(k5, ctr * 8 + 2) - 1.0)
+                    self.qvel[w, 1] += pv * (2.0 * uniform(k5, ctr * 8 + 3) - 1.0)
+                    self.draw_push_timer(w, ctr, 4)
         return self.observe(ctr), rew, term, trunc
 
 

@@ -910,7 +910,7 @@ template <class T> __device__ inline void make_frame(const T* n, T* fr) {
 }
 
 // broadphase + narrowphase over all pairs, compacted in pair order; returns ncon (warp-uniform)
-template <class T> __device__ int __noinline__ collide(const s3_model& m, const s3_layout& L_, T* B_, int lane, int& dropped) {
+template <class T> __device__ int __noinline__ collide(const s3_model& m, const s3_layout& L_, T* B_, int lane, int& dropped, T fscale) {
     WS<T> s = make_ws(B_, L_);
     int base = 0;
     dropped = 0;
@@ -929,7 +929,7 @@ template <class T> __device__ int __noinline__ collide(const s3_model& m, const 
         int off = base + incl - cnt;
         if (cnt) {
             int g1 = m.pair_geom[2 * p], g2 = m.pair_geom[2 * p + 1];
-            T mu = fmax(fric[g1], fric[g2]);
+            T mu = fmax(fric[g1], fric[g2]) * fscale;
             for (int k = 0; k < cnt; ++k) {
                 int slot = off + k;
                 if (slot < S3_MAX_CON) {
@@ -1343,7 +1343,8 @@ __device__ __noinline__ void substep(const s3_model& m, const s3_data& d, const 
     rne(m, L_, B_, lane);
     crb_mass(m, L_, B_, lane);
     int np = nv * (nv + 1) / 2;
-    ncon = collide(m, L_, B_, lane, dropped);
+    const T fscale = d.friction_scale ? static_cast<const T*>(d.friction_scale)[w] : T(1);
+    ncon = collide(m, L_, B_, lane, dropped, fscale);
     uint64_t U = (m.flags & 1) ? (nv == 64 ? ~0ull : ((1ull << nv) - 1)) : touched_mask(m, L_, B_, ncon, lane);
     tree_load(m, s.M, s.LD, lane);
     factor_ldl(m, s.LD, s.tk, lane, U, 1);          // subtrees no constraint touches: shared by M and H
@@ -1937,6 +1938,13 @@ __global__ void __launch_bounds__(32 * 16) env_kernel(const __grid_constant__ s3
         } else {
             task_reset(m, tk, L_, B_, w, 0, lane);
             task_resample(tk, cmd, w, 0, lane);
+            if (tk.events && lane == 0) {  // startup friction randomisation + first push timer (purpose 5)
+                uint64_t k5 = stream_key(tk.seed, tk.world_offset + w, 5);
+                static_cast<T*>(d.friction_scale)[w] =
+                    T(tk.friction_range[0]) + T(tk.friction_range[1] - tk.friction_range[0]) * uniform01<T>(k5, 0);
+                static_cast<T*>(tk.event_timer)[w] =
+                    T(tk.push_interval[0]) + T(tk.push_interval[1] - tk.push_interval[0]) * uniform01<T>(k5, 1);
+            }
         }
         for (int i = lane; i < nv; i += 32) gw[i] = T(0);
         for (int i = lane; i < nu; i += 32) { act[i] = T(0); prev[i] = T(0); }
@@ -2007,6 +2015,11 @@ __global__ void __launch_bounds__(32 * 16) env_kernel(const __grid_constant__ s3
     }
     if (term || trunc) {  // masked reset (warp-uniform)
         task_reset(m, tk, L_, B_, w, ctr, lane);
+        if (tk.events && lane == 0) {
+            uint64_t k5 = stream_key(tk.seed, tk.world_offset + w, 5);
+            static_cast<T*>(tk.event_timer)[w] =
+                T(tk.push_interval[0]) + T(tk.push_interval[1] - tk.push_interval[0]) * uniform01<T>(k5, ctr * 8 + 1);
+        }
         for (int i = lane; i < nv; i += 32) gw[i] = T(0);
         for (int i = lane; i < nu; i += 32) { act[i] = T(0); prev[i] = T(0); }
         task_resample(tk, cmd, w, ctr, lane);
@@ -2025,6 +2038,21 @@ __global__ void __launch_bounds__(32 * 16) env_kernel(const __grid_constant__ s3
         if (lane == 0) tk.cmd_timer[w] = tm;
     }
     __syncwarp();
+    if (tk.events) {  // interval push: every world, after resets and commands (EventManager.apply_interval)
+        T tmr = static_cast<T*>(tk.event_timer)[w] - T(m.timestep) * T(tk.decimation);
+        __syncwarp();
+        if (lane == 0) {
+            uint64_t k5 = stream_key(tk.seed, tk.world_offset + w, 5);
+            if (tmr <= T(0)) {
+                T pv = T(tk.push_velocity);
+                s.qvel[0] += pv * (T(2) * uniform01<T>(k5, ctr * 8 + 2) - T(1));
+                s.qvel[1] += pv * (T(2) * uniform01<T>(k5, ctr * 8 + 3) - T(1));
+                tmr = T(tk.push_interval[0]) + T(tk.push_interval[1] - tk.push_interval[0]) * uniform01<T>(k5, ctr * 8 + 4);
+            }
+            static_cast<T*>(tk.event_timer)[w] = tmr;
+        }
+        __syncwarp();
+    }
     task_observe(m, tk, L_, B_, w, ctr, cmd, act, lane);
     if (d.geom_xpos) store_geom_frames(m, d, L_, B_, w, lane);  // sensors see the post-reset state, like obs
     for (int i = lane; i < nq; i += 32) gq[i] = s.qpos[i];
@@ -2292,6 +2320,8 @@ int s3_env_step(const s3_model* m, const s3_data* d, const s3_layout* l, const s
     if (d->nworld == 0) return S3_OK;
     if (!d->qpos || !d->qvel || !d->qacc_warmstart) return fail(S3_ERR_ARG, "qpos/qvel/qacc_warmstart required");
     if (mode == 0 && !actions) return fail(S3_ERR_ARG, "actions required");
+    if (t->kind == 0 && t->events && (!d->friction_scale || !t->event_timer))
+        return fail(S3_ERR_ARG, "events need friction_scale and event_timer");
     const int want = t->kind == 1 ? 15 + 5 * m->nu : (t->kind == 2 ? 13 + 3 * m->nu : 12 + 3 * m->nu + t->nscan);
     if (t->obs_dim != want || t->nscan > S3_MAX_RAYS || t->decimation < 1 ||
         (t->kind == 1 && (t->nframes < 2 || !t->motion_qpos || !t->motion_qvel || m->nq + m->nv > m->nv * (m->nv + 1) / 2)))

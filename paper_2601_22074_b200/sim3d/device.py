@@ -282,6 +282,7 @@ class Data:
         self.qacc_warmstart = torch.zeros(nworld, m.nv, dtype=dt, device=dev)
         self.qfrc_applied = None
         self.time = torch.zeros(nworld, dtype=dt, device=dev)
+        self.friction_scale = None  # (N,) per-world friction multiplier (domain randomisation)
         self.geom_xpos = None
         self.geom_xmat = None
         self._out = None
@@ -309,7 +310,8 @@ class Data:
     def struct(self, outputs: bool):
         s = N.DataT()
         s.nworld = self.nworld
-        for name in ("qpos", "qvel", "ctrl", "qacc_warmstart", "qfrc_applied", "time", "geom_xpos", "geom_xmat"):
+        for name in ("qpos", "qvel", "ctrl", "qacc_warmstart", "qfrc_applied", "time", "geom_xpos", "geom_xmat",
+                     "friction_scale"):
             t = getattr(self, name)
             setattr(s, name, None if t is None else t.data_ptr())
         if outputs:

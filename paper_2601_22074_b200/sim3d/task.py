@@ -54,6 +54,11 @@ class VelocityTaskCfg:
     scan_resolution: float = 0.2
     scan_offset: float = 0.5
     scan_noise: float = 0.02
+    # domain randomisation (EventManager analog): startup per-world friction scale; interval pushes that
+    # add U(-v, v) to the base's planar velocity every U(push_interval) seconds. None disables pushes.
+    friction_range: tuple = (0.6, 1.2)
+    push_interval: tuple | None = (10.0, 15.0)
+    push_velocity: float = 0.5
 
     def scan_points(self):
         nx = int(round(self.scan_size[0] / self.scan_resolution)) + 1
@@ -208,6 +213,14 @@ class VelocityEnv3D:
             for i, (lo, hi) in enumerate(cfg.goal_ranges):
                 t.cmd_lo[i], t.cmd_hi[i] = lo, hi
         else:
+            if cfg.push_interval is not None:
+                t.events = 1
+                self.data.friction_scale = torch.ones(n, dtype=dt, device=dev)
+                self.event_timer = z(n)
+                t.event_timer = self.event_timer.data_ptr()
+                t.friction_range[:] = cfg.friction_range
+                t.push_interval[:] = cfg.push_interval
+                t.push_velocity = cfg.push_velocity
             t.cmd_resample_steps = cfg.command_resample_steps
             t.track_sigma = cfg.track_sigma
             t.min_height, t.max_tilt_cos, t.reset_joint_jitter = cfg.min_height, cfg.max_tilt_cos, \

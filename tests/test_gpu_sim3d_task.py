@@ -68,6 +68,9 @@ def _load(env, ref):
     env.command.copy_(t(ref.cmd))
     env.cmd_timer.copy_(t(ref.cmd_timer.astype(np.int32)))
     env.episode_step.copy_(t(ref.episode_step.astype(np.int32)))
+    if getattr(env, "event_timer", None) is not None:
+        env.event_timer.copy_(t(ref.ev_timer))
+        env.data.friction_scale.copy_(t(ref.fscale))
     env.global_step = ref.global_step
 
 
@@ -280,3 +283,32 @@ def test_ppo_trains_on_the_3d_env():
     torch.cuda.synchronize()
     assert all(torch.isfinite(torch.as_tensor(float(v))) for v in stats.values())
     assert all(torch.isfinite(p).all() for p in tr.model.parameters())
+
+
+@pytest.mark.gpu
+def test_domain_randomisation_events_match_oracle():
+    """Startup friction randomisation (per world) and interval pushes: pushes every 1-3 control steps
+    here, so the kicked base velocities, timers and friction scales are all compared."""
+    import torch
+
+    n = 8
+    env, ref = _pair("g1_flat", n, push_interval=(0.02, 0.06), push_velocity=0.8)
+    np.testing.assert_allclose(env.reset().cpu().numpy(), ref.reset(), atol=1e-12)
+    np.testing.assert_allclose(env.data.friction_scale.cpu().numpy(), ref.fscale, atol=1e-15)
+    assert ref.fscale.std() > 0.01
+    rng = np.random.default_rng(12)
+    pushes = 0
+    for k in range(5):
+        _load(env, ref)
+        before = ref.ev_timer.copy()
+        a = rng.uniform(-1, 1, size=(n, env.model.nu))
+        o, r, te, tr = env.step(torch.as_tensor(a, device="cuda"))
+        o_ref, r_ref, te_ref, tr_ref = ref.step(a)
+        torch.cuda.synchronize()
+        pushes += int((ref.ev_timer > before).sum())
+        np.testing.assert_array_equal(te.cpu().numpy().astype(bool), te_ref)
+        np.testing.assert_allclose(r.cpu().numpy(), r_ref, rtol=1e-8, atol=1e-10)
+        np.testing.assert_allclose(o.cpu().numpy(), o_ref, rtol=1e-7, atol=1e-7)
+        np.testing.assert_allclose(env.event_timer.cpu().numpy(), ref.ev_timer, atol=1e-12)
+        np.testing.assert_allclose(env.data.qvel.cpu().numpy(), ref.qvel, rtol=1e-8, atol=1e-8)
+    assert pushes > 0
