@@ -369,6 +369,26 @@ def sphere_box(c, r, bc, R, size):
     return d, R @ n_loc, pos
 
 
+CAPSULE_BOX_ITERS = 8
+
+
+def capsule_box(p0, p1, r, bc, R, size):
+    """Capsule (segment p0-p1, radius r) vs box: the segment point closest to the box by alternating
+    projections (box clamp <-> segment projection, CAPSULE_BOX_ITERS rounds from the midpoint), then the
+    sphere-box contact at that point."""
+    a = R.T @ (p0 - bc)
+    b = R.T @ (p1 - bc)
+    d = b - a
+    dd = d @ d
+    t = 0.5
+    for _ in range(CAPSULE_BOX_ITERS):
+        p = a + d * t
+        q = np.minimum(np.maximum(p, -size), size)
+        t = min(max(((q - a) @ d) / dd, 0.0), 1.0) if dd > 1e-12 else 0.0
+    c = bc + R @ (a + d * t)
+    return sphere_box(c, r, bc, R, size)
+
+
 def _segment(m, K, g):
     a = K["geom_xmat"][g][:, 2] * m.geom_size[g][1]
     c = K["geom_xpos"][g]
@@ -419,12 +439,16 @@ def collide(m, K, fscale=1.0):
                 if h is not None and h[0] < 0.0:
                     d, n = h
                     found.append((d, n, q - n * (r + 0.5 * d)))
-        elif t2 == GEOM_BOX:  # sphere (g1) vs box (g2)
+        elif t2 == GEOM_BOX:  # sphere or capsule (g1) vs box (g2)
             dv = c2 - c1
             rb = m.geom_rbound[g1] + m.geom_rbound[g2]
             if dv @ dv >= rb * rb:
                 continue
-            h = sphere_box(c1, m.geom_size[g1][0], c2, K["geom_xmat"][g2], m.geom_size[g2])
+            if t1 == GEOM_CAPSULE:
+                p0, p1 = _segment(m, K, g1)
+                h = capsule_box(p0, p1, m.geom_size[g1][0], c2, K["geom_xmat"][g2], m.geom_size[g2])
+            else:
+                h = sphere_box(c1, m.geom_size[g1][0], c2, K["geom_xmat"][g2], m.geom_size[g2])
             if h is not None and h[0] < 0.0:
                 found.append(h)
         else:

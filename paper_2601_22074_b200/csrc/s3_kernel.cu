@@ -815,7 +815,7 @@ template <class T> __device__ __noinline__ int narrow(const s3_model& m, const s
                 ++cnt;
             }
         }
-    } else if (t2 == kGeomBox) {  // sphere (g1) vs box (g2): oracle sphere_box
+    } else if (t2 == kGeomBox) {  // sphere or capsule (g1) vs box (g2): oracle sphere_box / capsule_box
         T dv[3] = {c2[0] - c1[0], c2[1] - c1[1], c2[2] - c1[2]};
         T rr = rb[g1] + rb[g2];
         if (!(dot3(dv, dv) < rr * rr)) return 0;
@@ -823,10 +823,32 @@ template <class T> __device__ __noinline__ int narrow(const s3_model& m, const s
         const T* R = s.gmat + 9 * g2;
         const T* hs = sz + 3 * g2;
         T r = sz[3 * g1];
-        T dl[3] = {c1[0] - c2[0], c1[1] - c2[1], c1[2] - c2[2]};
         T p[3], q[3], dq[3];
+        if (t1 == kGeomCapsule) {
+            // segment point closest to the box: alternating projections from the midpoint (box frame)
+            T e0[3], e1[3], a[3], b[3], dd3[3];
+            segment(m, s, g1, e0, e1);
+            for (int k = 0; k < 3; ++k) {
+                a[k] = R[k] * (e0[0] - c2[0]) + R[3 + k] * (e0[1] - c2[1]) + R[6 + k] * (e0[2] - c2[2]);
+                b[k] = R[k] * (e1[0] - c2[0]) + R[3 + k] * (e1[1] - c2[1]) + R[6 + k] * (e1[2] - c2[2]);
+                dd3[k] = b[k] - a[k];
+            }
+            T dd = dot3(dd3, dd3), t = T(0.5);
+            for (int it = 0; it < 8; ++it) {
+                T qq[3];
+                for (int k = 0; k < 3; ++k) qq[k] = fmin(fmax(a[k] + dd3[k] * t, -hs[k]), hs[k]) - a[k];
+                t = dd > T(1e-12) ? clampt(dot3(qq, dd3) / dd, T(0), T(1)) : T(0);
+            }
+            T cl[3] = {a[0] + dd3[0] * t, a[1] + dd3[1] * t, a[2] + dd3[2] * t}, cw[3];
+            mv3(R, cl, cw);
+            T cc[3] = {c2[0] + cw[0], c2[1] + cw[1], c2[2] + cw[2]};
+            T dl[3] = {cc[0] - c2[0], cc[1] - c2[1], cc[2] - c2[2]};
+            for (int k = 0; k < 3; ++k) p[k] = R[k] * dl[0] + R[3 + k] * dl[1] + R[6 + k] * dl[2];
+        } else {
+            T dl[3] = {c1[0] - c2[0], c1[1] - c2[1], c1[2] - c2[2]};
+            for (int k = 0; k < 3; ++k) p[k] = R[k] * dl[0] + R[3 + k] * dl[1] + R[6 + k] * dl[2];
+        }
         for (int k = 0; k < 3; ++k) {
-            p[k] = R[k] * dl[0] + R[3 + k] * dl[1] + R[6 + k] * dl[2];
             q[k] = fmin(fmax(p[k], -hs[k]), hs[k]);
             dq[k] = p[k] - q[k];
         }

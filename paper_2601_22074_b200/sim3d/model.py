@@ -368,9 +368,8 @@ class Model:
                 if t1 in (GEOM_PLANE, GEOM_HFIELD):
                     if t2 not in (GEOM_SPHERE, GEOM_CAPSULE, GEOM_BOX):
                         continue
-                elif not ((t1 in (GEOM_SPHERE, GEOM_CAPSULE) and t2 in (GEOM_SPHERE, GEOM_CAPSULE)) or
-                          (t1 == GEOM_SPHERE and t2 == GEOM_BOX)):
-                    continue  # supported pairs: sphere/capsule x sphere/capsule, sphere x box
+                elif not ((t1 in (GEOM_SPHERE, GEOM_CAPSULE) and t2 in (GEOM_SPHERE, GEOM_CAPSULE, GEOM_BOX))):
+                    continue  # supported pairs: sphere/capsule x sphere/capsule/box (box second)
                 pairs.append((g1, g2))
         self.npair = len(pairs)
         self.pair_geom = np.array(pairs, dtype=np.int32).reshape(-1, 2)

@@ -199,8 +199,8 @@ ARM_DEFAULT_JOINTS = {"shoulder_yaw": 0.0, "shoulder_pitch": -0.5, "elbow": 1.1,
 def arm_cube_like(opt: Opt | None = None, cube_size: float = 0.025):
     """A fixed-base 6-dof arm with a two-finger claw (hinged fingers, sphere fingertips) on a table
     (the plane) and a free cube (BASELINE configs[3], cube lift). Two kinematic trees: the arm and the
-    cube. Collision filter: arm links touch the table only; fingertip spheres touch the cube (sphere-box);
-    the cube touches the table (box corners)."""
+    cube. Collision filter: arm links touch the table only; fingertip spheres and finger capsules touch
+    the cube (sphere-box, capsule-box); the cube touches the table (box corners)."""
     b = ModelBuilder("arm_cube_like", opt)
     b.plane(friction=1.0)
     base = b.body("link0", 0, pos=(0, 0, 0), mass=2.0, inertia=(0.01, 0.01, 0.01))
@@ -240,8 +240,8 @@ def arm_cube_like(opt: Opt | None = None, cube_size: float = 0.025):
             g["contype"], g["conaffinity"] = 0, 0  # static: never collides
         elif g.get("name") == "cube":
             g["contype"], g["conaffinity"] = 4, 1 | 8
-        elif g.get("name", "") and g["name"].endswith("_tip"):
-            g["contype"], g["conaffinity"] = 2 | 8, 1
+        elif g.get("name", "") and (g["name"].endswith("_tip") or g["name"].endswith("_finger")):
+            g["contype"], g["conaffinity"] = 2 | 8, 1  # fingertip spheres and finger capsules touch the cube
         else:
             g["contype"], g["conaffinity"] = 2, 1
     gains = {"finger": dict(kp=40.0, kv=2.0, effort=20.0)}

@@ -383,3 +383,23 @@ def test_two_trees_arm_and_cube():
                                + robots.default_qpos(m, robots.ARM_DEFAULT_JOINTS)[m.actuator_qposadr], warm=warm)
     cube_contacts = [c for c in F["contacts"] if m.geom_bodyid[c["geom2"]] == m.body_names.index("cube")]
     assert len(cube_contacts) == 4 and abs(q[-5] - 0.025) < 1e-3
+
+
+def test_capsule_box_contact_brute_force(rng):
+    """Capsule-box distance (alternating projections, then sphere-box) vs brute force over the segment
+    and the box volume, for capsules outside the box."""
+    size = np.array([0.05, 0.04, 0.03])
+    for _ in range(30):
+        R = O.qmat(O.qnormalize(rng.normal(size=4)))
+        bc = rng.normal(size=3) * 0.1
+        p0, p1 = bc + rng.normal(size=3) * 0.12, bc + rng.normal(size=3) * 0.12
+        d, n, pos = O.capsule_box(p0, p1, 0.01, bc, R, size)
+        seg = p0 + (p1 - p0) * np.linspace(0, 1, 201)[:, None]
+        loc = (seg - bc) @ R
+        if np.any(np.all(np.abs(loc) <= size, axis=1)):
+            continue  # segment passes through the box: penetration branch, no brute-force distance
+        g = np.stack(np.meshgrid(*[np.linspace(-s, s, 21) for s in size], indexing="ij"), -1).reshape(-1, 3)
+        pts = bc + g @ R.T
+        brute = np.min(np.linalg.norm(seg[:, None] - pts[None], axis=-1)) - 0.01
+        assert abs(d - brute) < 6e-3, (d, brute)
+        assert abs(np.linalg.norm(n) - 1) < 1e-12
