@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define S3_ABI_VERSION 11
+#define S3_ABI_VERSION 12
 #define S3_F64 0
 #define S3_F32 1
 
@@ -61,8 +61,8 @@ typedef struct s3_model {
     int32_t nldl_norm;
     int32_t ntree;
     int32_t flags; /* bit 0: refactor every dof in each Newton iteration (A/B of the partial refactorization);
-                      bit 1: tree-level schedule of the factorization / solves instead of one dof per step
-                      (measured slower; kept for A/B) */
+                      bit 1: tree-level schedule of the factorization / solves from CSR tables (measured
+                      slower; kept for A/B); bit 2: tree-level schedule driven by per-lane dof bit masks */
     int32_t nhlev;
     int32_t ndlev;
     int32_t nkintree; /* kinematic trees (robot, free objects) */
@@ -157,6 +157,8 @@ typedef struct s3_model {
     const uint8_t* bl_i;
     const int32_t* fw_ptr;
     const uint8_t* fw_dof;
+    const uint64_t* hlev_mask; /* dof bit mask of each height level */
+    const uint64_t* dlev_mask; /* dof bit mask of each depth level */
     const int32_t* pair_class;
     const int32_t* pair_tree;
     const uint16_t* tri_tab;

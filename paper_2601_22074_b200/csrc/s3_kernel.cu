@@ -393,6 +393,59 @@ template <class T> __device__ void __noinline__ crb_mass(const s3_model& m, cons
 // constraint row lives on U, so Newton refactors only U (eliminations of disjoint subtrees commute).
 template <class T>
 __device__ __noinline__ void factor_ldl(const s3_model& m, T* A, T* rk, int lane, uint64_t U = 0, int sel = 0) {
+    if (m.flags & 4) {
+        // mask-level schedule: lane owns dof rows i in {lane, lane + 32}; at height level h it applies
+        // the Schur updates of the level's dofs k that descend from i to its row (j in chain(i)). Rows of
+        // level-h dofs are final (their descendants sit lower) and are only read; no table loads.
+        const uint64_t all = m.nv == 64 ? ~0ull : ((1ull << m.nv) - 1);
+        const uint64_t selm = sel == 0 ? all : (sel == 1 ? (~U & all) : (U & all));
+        const unsigned long long* cm = reinterpret_cast<const unsigned long long*>(m.dof_chainmask);
+        const unsigned long long* dmk = reinterpret_cast<const unsigned long long*>(m.dof_descmask);
+        const unsigned long long* hm = reinterpret_cast<const unsigned long long*>(m.hlev_mask);
+        const int i0 = lane, i1 = lane + 32;
+        const uint64_t am0 = i0 < m.nv ? __ldg(cm + i0) : 0, am1 = i1 < m.nv ? __ldg(cm + i1) : 0;
+        const uint64_t dm0 = i0 < m.nv ? __ldg(dmk + i0) : 0, dm1 = i1 < m.nv ? __ldg(dmk + i1) : 0;
+        for (int h = 0; h < m.nhlev; ++h) {
+            const uint64_t lm = __ldg(hm + h) & selm;
+            if (!lm) continue;
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+                const int i = half ? i1 : i0;
+                uint64_t ks = (half ? dm1 : dm0) & lm;
+                const uint64_t am = half ? am1 : am0;
+                while (ks) {
+                    const int k = __ffsll((long long)ks) - 1;
+                    ks &= ks - 1;
+                    const int rkb = tri(k, 0);
+                    const T t = A[rkb + i] / A[rkb + k];
+                    const int rib = tri(i, 0);
+                    uint64_t js = am;
+                    while (js) {
+                        const int j = __ffsll((long long)js) - 1;
+                        js &= js - 1;
+                        A[rib + j] -= t * A[rkb + j];
+                    }
+                }
+            }
+            __syncwarp();
+        }
+        // normalise the selected rows: L[k][i] = A[k][i] / D[k] for strict ancestors i
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+            const int k = half ? i1 : i0;
+            if (k >= m.nv || !((selm >> k) & 1ull)) continue;
+            const int rkb = tri(k, 0);
+            const T dk = A[rkb + k];
+            uint64_t is = (half ? am1 : am0) & ~(1ull << k);
+            while (is) {
+                const int i = __ffsll((long long)is) - 1;
+                is &= is - 1;
+                A[rkb + i] = A[rkb + i] / dk;
+            }
+        }
+        __syncwarp();
+        return;
+    }
     if (m.flags & 2) {
         // level schedule (opt-in, flags bit 1; measured SLOWER than the sequential sweep below -- 6.6 vs
         // 5.2 ms f32, 11.1 vs 8.0 ms f64 per G1 control step -- because each entry chains three dependent
@@ -479,6 +532,56 @@ template <class T> __device__ __noinline__ void tree_load(const s3_model& m, con
 // x <- M^-1 x with the L^T D L factor (oracle solve_ldl; column-oriented forward pass)
 template <class T> __device__ __noinline__ void solve_ldl(const s3_model& m, const T* A, T* x, int lane) {
     int nv = m.nv;
+    if (m.flags & 4) {
+        // mask-level sweeps (see factor_ldl): leaf-to-root by height, each lane's dofs j gather the level's
+        // descendants; root-to-leaf by depth, each lane's dof gathers its (final) ancestors
+        const unsigned long long* cm = reinterpret_cast<const unsigned long long*>(m.dof_chainmask);
+        const unsigned long long* dmk = reinterpret_cast<const unsigned long long*>(m.dof_descmask);
+        const unsigned long long* hm = reinterpret_cast<const unsigned long long*>(m.hlev_mask);
+        const unsigned long long* dlm = reinterpret_cast<const unsigned long long*>(m.dlev_mask);
+        const int i0 = lane, i1 = lane + 32;
+        const uint64_t am0 = i0 < nv ? __ldg(cm + i0) : 0, am1 = i1 < nv ? __ldg(cm + i1) : 0;
+        const uint64_t dm0 = i0 < nv ? __ldg(dmk + i0) : 0, dm1 = i1 < nv ? __ldg(dmk + i1) : 0;
+        for (int h = 0; h < m.nhlev; ++h) {
+            const uint64_t lm = __ldg(hm + h);
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+                const int j = half ? i1 : i0;
+                uint64_t src = (half ? dm1 : dm0) & lm;
+                if (!src) continue;
+                T acc = T(0);
+                while (src) {
+                    const int i = __ffsll((long long)src) - 1;
+                    src &= src - 1;
+                    acc += A[tri(i, j)] * x[i];
+                }
+                x[j] -= acc;
+            }
+            __syncwarp();
+        }
+        if (i0 < nv) x[i0] = x[i0] / A[tri(i0, i0)];
+        if (i1 < nv) x[i1] = x[i1] / A[tri(i1, i1)];
+        __syncwarp();
+        for (int dl = 1; dl < m.ndlev; ++dl) {
+            const uint64_t lm = __ldg(dlm + dl);
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+                const int i = half ? i1 : i0;
+                if (i >= nv || !((lm >> i) & 1ull)) continue;
+                uint64_t anc = (half ? am1 : am0) & ~(1ull << i);
+                const int rb = tri(i, 0);
+                T acc = T(0);
+                while (anc) {
+                    const int j = __ffsll((long long)anc) - 1;
+                    anc &= anc - 1;
+                    acc += A[rb + j] * x[j];
+                }
+                x[i] -= acc;
+            }
+            __syncwarp();
+        }
+        return;
+    }
     if (m.flags & 2) {
         // leaf-to-root sweep by height levels: each target ancestor gathers the contributions of the
         // level's dofs (their values are final: all their descendants sit in lower levels)

@@ -120,6 +120,8 @@ class DeviceModel:
         for lev in dlev:
             fw_dof += lev
             fw_ptr.append(len(fw_dof))
+        hmask = np.array([sum(1 << d for d in lev) for lev in hlev] + [0], dtype=np.uint64)
+        dmask_lv = np.array([sum(1 << d for d in lev) for lev in dlev] + [0], dtype=np.uint64)
         dof_chainmask = np.zeros(m.nv, dtype=np.uint64)
         for d in range(m.nv):
             for a in m.dof_chain[d]:
@@ -164,6 +166,7 @@ class DeviceModel:
             bl_ptr=np.array(bl_ptr, dtype=np.int32), bl_ent=np.array(bl_ent + [0], dtype=np.uint8),
             bl_iptr=np.array(bl_iptr, dtype=np.int32), bl_i=np.array(bl_i + [0], dtype=np.uint8),
             fw_ptr=np.array(fw_ptr, dtype=np.int32), fw_dof=np.array(fw_dof + [0], dtype=np.uint8),
+            hlev_mask=hmask, dlev_mask=dmask_lv,
             pair_class=np.array(pair_class + [0], dtype=np.int32), pair_tree=np.array(pair_tree + [1], dtype=np.int32),
             tri_tab=tri_tab)
         floats = dict(

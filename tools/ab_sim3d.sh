@@ -1,6 +1,6 @@
 #!/bin/bash
 # A/B of 3-D kernel variants selected by S3_FLAGS (bit 0: full Newton refactorization instead of the
-# touched subtrees; bit 1: tree-level schedule of the factorization/solves instead of one dof per step).
+# touched subtrees; bit 1: tree-level schedule (CSR tables); bit 2: tree-level schedule (register bit masks)).
 FLAGS=${FLAGS:-"0 1 2 3"}
 for rep in 1 2; do
   for f in $FLAGS; do
