@@ -360,6 +360,19 @@ def sim3d_leg(args, flush, stream) -> dict:
                               "env_only_ms_per_step": 1e3 * t_env / steps}
         del env, cam
     out["kernel"] = "s3::env_kernel (warp per world, shared-memory resident; one launch per control step)"
+    # the kernel is latency/issue bound with ~0 DRAM traffic (per-world data lives in shared memory), so its
+    # evidence is the committed ncu capture, not an HBM roofline
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_sim3d_env_kernel.json")) as fh:
+            prof = json.load(fh)
+        out["roofline"] = {"bound": "latency (serial per-world factorization/solves in shared memory)",
+                           "dram_throughput_frac": prof["f32"]["dram_throughput_frac"],
+                           "issue_slots_busy_frac": prof["f32"]["issue_slots_busy_frac"],
+                           "executed_ipc_active": prof["f32"]["executed_ipc_active"],
+                           "achieved_occupancy_frac": prof["f32"]["achieved_occupancy_frac"],
+                           "source": "profiles/ncu_sim3d_env_kernel.json (f32, 4096 worlds)"}
+    except (OSError, KeyError, ValueError):
+        out["roofline"] = None
     out["parity"] = "oracle/sim3d.py (tests/test_gpu_sim3d*.py); unpinned w.r.t. the reference (no 3-D engine)"
     if not args.no_cpu:
         out["cpu_baseline"] = sim3d_cpu(args.seed)
