@@ -18,15 +18,26 @@ from paper_2601_22074_b200.tasks import make_env_cfg  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--envs", type=int, default=4096)
 ap.add_argument("--iters", type=int, default=10)
-ap.add_argument("--task", default="Velocity-Rough")
+ap.add_argument("--task", default="Velocity-Rough",
+                help="planar task id, or G1-3D / G1-3D-Rough for the fused 3-D G1 velocity task (float32)")
 args = ap.parse_args()
 rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
 torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
 if world > 1:
     dist.init_process_group("nccl", device_id=torch.device("cuda", torch.cuda.current_device()))
-cfg = make_env_cfg(args.task, num_envs=args.envs)
-cfg.scene.world_id_offset = rank * args.envs
-env = ManagerBasedRlEnv(cfg, args.task)
+if args.task.startswith("G1-3D"):
+    from paper_2601_22074_b200.sim3d import robots
+    from paper_2601_22074_b200.sim3d.rl import ManagerView
+    from paper_2601_22074_b200.sim3d.task import VelocityEnv3D, VelocityTaskCfg
+
+    rough = args.task.endswith("Rough")
+    m = robots.g1_like(rough=rough)
+    tcfg = VelocityTaskCfg(default_qpos=robots.default_qpos(m, robots.G1_DEFAULT_JOINTS), height_scan=rough)
+    env = ManagerView(VelocityEnv3D(m, tcfg, args.envs, world_offset=rank * args.envs, dtype="f32"))
+else:
+    cfg = make_env_cfg(args.task, num_envs=args.envs)
+    cfg.scene.world_id_offset = rank * args.envs
+    env = ManagerBasedRlEnv(cfg, args.task)
 tr = PpoTrainer(env, PpoCfg())
 tr.collect()
 tr.update()
