@@ -283,11 +283,13 @@ def sim3d_leg(args, flush, stream) -> dict:
     from paper_2601_22074_b200.sim3d.task import VelocityEnv3D, VelocityTaskCfg
 
     n = args.envs
-    out = {"workload": f"G1-like 3-D humanoid velocity tracking, rough heightfield + height scan, {n} worlds/GPU, "
-                       "decimation 4 (planar-free 3-D path, SURVEY 8 f4)", "unit": UNIT}
+    out = {"workload": f"G1-like 3-D humanoid velocity tracking on the 5x6 terrain-curriculum heightfield (levels, "
+                       f"height scan, friction randomisation, pushes), {n} worlds/GPU, decimation 4 (SURVEY 8 f4)",
+           "unit": UNIT}
     for dtype in ("f32", "f64"):
-        m = robots.g1_like(rough=True, seed=args.seed)
-        cfg = VelocityTaskCfg(default_qpos=robots.default_qpos(m, robots.G1_DEFAULT_JOINTS), height_scan=True)
+        m = robots.g1_like(rough="curriculum", seed=args.seed)
+        cfg = VelocityTaskCfg(default_qpos=robots.default_qpos(m, robots.G1_DEFAULT_JOINTS), height_scan=True,
+                              curriculum=(5, 6, 8.0))
         env = VelocityEnv3D(m, cfg, n, seed=args.seed, world_offset=int(os.environ.get("RANK", "0")) * n, dtype=dtype)
         env.reset()
         steps = 20

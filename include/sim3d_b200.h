@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define S3_ABI_VERSION 12
+#define S3_ABI_VERSION 13
 #define S3_F64 0
 #define S3_F32 1
 
@@ -257,6 +257,16 @@ typedef struct s3_task {
     double push_interval[2];
     double push_velocity;
     void* event_timer; /* (N,) time to the next push */
+    int32_t curriculum; /* velocity kind: 1 = terrain levels on a rows x cols patch grid */
+    int32_t terrain_rows;
+    int32_t terrain_cols;
+    int32_t curriculum_max_init_level;
+    double patch_size;
+    double curriculum_promote;
+    double curriculum_demote;
+    int32_t* terrain_level; /* (N,) */
+    void* spawn_xy;         /* (N, 2) */
+    void* cmd_dist;         /* (N,) commanded distance of the running episode */
     const void* motion_qpos; /* (nframes, nq) */
     const void* motion_qvel; /* (nframes, nv) */
     const void* default_qpos;

@@ -774,6 +774,12 @@ class TaskOracle:
         self.act_default = self.default[act]
         self.fscale = np.ones(nworld)          # startup event: per-world friction scale
         self.ev_timer = np.zeros(nworld)       # interval event: time to the next push
+        self.level = np.zeros(nworld, dtype=np.int64)   # terrain curriculum row
+        self.spawn = np.zeros((nworld, 2))
+        self.cmd_dist = np.zeros(nworld)
+
+    def _curriculum_on(self):
+        return getattr(self.cfg, "curriculum", None) is not None
 
     def _events_on(self):
         return getattr(self.cfg, "push_interval", None) is not None
@@ -790,6 +796,12 @@ class TaskOracle:
             q[a] += cfg.reset_joint_jitter * (2.0 * uniform(kr, ctr * 256 + i) - 1.0)
         q[0] = cfg.spawn_half_extent * (2.0 * uniform(kr, ctr * 256 + 200) - 1.0)
         q[1] = cfg.spawn_half_extent * (2.0 * uniform(kr, ctr * 256 + 201) - 1.0)
+        if self._curriculum_on():  # centre of the world's (level, column) patch
+            rows, cols, patch = cfg.curriculum
+            q[0] += ((self.off + w) % cols + 0.5) * patch
+            q[1] += (self.level[w] + 0.5) * patch
+            self.spawn[w] = q[0:2]
+            self.cmd_dist[w] = 0.0
         yaw = np.pi * (2.0 * uniform(kr, ctr * 256 + 202) - 1.0)
         q[2] = self.default[2] + terrain_height(m, q[0], q[1])
         q[3:7] = (np.cos(0.5 * yaw), 0.0, 0.0, np.sin(0.5 * yaw))
@@ -811,6 +823,10 @@ class TaskOracle:
         self.cmd_timer[w] = self.cfg.command_resample_steps
 
     def reset(self):
+        if self._curriculum_on():  # initial levels (purpose 6, counter 0)
+            for w in range(self.n):
+                u = uniform(self.key(w, 6), 0)
+                self.level[w] = min(int(u * (self.cfg.curriculum_max_init_level + 1)), self.cfg.curriculum[0] - 1)
         if self._events_on():  # startup randomisation (purpose 5, counter 0, slot 0)
             lo, hi = self.cfg.friction_range
             for w in range(self.n):
@@ -890,7 +906,15 @@ class TaskOracle:
             term[w] = bool(h < cfg.min_height or g[2] > cfg.max_tilt_cos or nonfinite)
             self.episode_step[w] += 1
             trunc[w] = bool(self.episode_step[w] >= cfg.episode_steps)
+            if self._curriculum_on():
+                self.cmd_dist[w] += np.sqrt(self.cmd[w, 0] ** 2 + self.cmd[w, 1] ** 2) * dtc
         for w in range(self.n):
+            if (term[w] or trunc[w]) and self._curriculum_on():  # on the finished episode, before the reset
+                walked = np.sqrt(np.sum((self.qpos[w, 0:2] - self.spawn[w]) ** 2))
+                if walked > cfg.curriculum_promote * self.cmd_dist[w]:
+                    self.level[w] = min(self.level[w] + 1, cfg.curriculum[0] - 1)
+                elif walked < cfg.curriculum_demote * self.cmd_dist[w]:
+                    self.level[w] = max(self.level[w] - 1, 0)
             if term[w] or trunc[w]:
                 self.reset_world(w, ctr)
             else:

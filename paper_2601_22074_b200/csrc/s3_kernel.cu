@@ -1663,6 +1663,13 @@ __device__ __noinline__ void task_reset(const s3_model& m, const s3_task& tk, co
         T x = T(tk.spawn_half_extent) * (T(2) * uniform01<T>(kr, ctr * 256 + 200) - T(1));
         T y = T(tk.spawn_half_extent) * (T(2) * uniform01<T>(kr, ctr * 256 + 201) - T(1));
         T yaw = T(3.141592653589793) * (T(2) * uniform01<T>(kr, ctr * 256 + 202) - T(1));
+        if (tk.curriculum) {  // centre of the world's (level row, world_id % cols) patch
+            x += (T((tk.world_offset + w) % tk.terrain_cols) + T(0.5)) * T(tk.patch_size);
+            y += (T(tk.terrain_level[w]) + T(0.5)) * T(tk.patch_size);
+            static_cast<T*>(tk.spawn_xy)[2 * w] = x;
+            static_cast<T*>(tk.spawn_xy)[2 * w + 1] = y;
+            static_cast<T*>(tk.cmd_dist)[w] = T(0);
+        }
         s.qpos[0] = x;
         s.qpos[1] = y;
         s.qpos[2] = dq[2] + terrain_height(m, x, y);
@@ -2061,6 +2068,12 @@ __global__ void __launch_bounds__(32 * 16) env_kernel(const __grid_constant__ s3
         } else if (tk.kind == 2) {
             lift_reset(m, tk, L_, B_, w, 0, cmd, lane);
         } else {
+            if (tk.curriculum && lane == 0) {  // initial terrain level (purpose 6, counter 0)
+                int lv = (int)(uniform01<T>(stream_key(tk.seed, tk.world_offset + w, 6), 0) *
+                               T(tk.curriculum_max_init_level + 1));
+                tk.terrain_level[w] = lv < tk.terrain_rows - 1 ? lv : tk.terrain_rows - 1;
+            }
+            __syncwarp();
             task_reset(m, tk, L_, B_, w, 0, lane);
             task_resample(tk, cmd, w, 0, lane);
             if (tk.events && lane == 0) {  // startup friction randomisation + first push timer (purpose 5)
@@ -2137,7 +2150,21 @@ __global__ void __launch_bounds__(32 * 16) env_kernel(const __grid_constant__ s3
         tk.terminated[w] = term;
         tk.truncated[w] = trunc;
         tk.episode_step[w] = es;
+        if (tk.curriculum) {
+            T cd = static_cast<T*>(tk.cmd_dist)[w] + sqrt(c0 * c0 + c1 * c1) * dtc;
+            static_cast<T*>(tk.cmd_dist)[w] = cd;
+            if (term || trunc) {  // terrain levels on the finished episode, before the reset
+                T dx = s.qpos[0] - static_cast<T*>(tk.spawn_xy)[2 * w];
+                T dy = s.qpos[1] - static_cast<T*>(tk.spawn_xy)[2 * w + 1];
+                T walked = sqrt(dx * dx + dy * dy);
+                int lv = tk.terrain_level[w];
+                if (walked > T(tk.curriculum_promote) * cd) lv = lv + 1 < tk.terrain_rows ? lv + 1 : tk.terrain_rows - 1;
+                else if (walked < T(tk.curriculum_demote) * cd) lv = lv > 0 ? lv - 1 : 0;
+                tk.terrain_level[w] = lv;
+            }
+        }
     }
+    __syncwarp();
     if (term || trunc) {  // masked reset (warp-uniform)
         task_reset(m, tk, L_, B_, w, ctr, lane);
         if (tk.events && lane == 0) {

@@ -33,16 +33,41 @@ def rough_heightfield(seed: int, size_m: float = 16.0, spacing: float = 0.1, amp
     return h, spacing, (-(n - 1) / 2 * spacing, -(n - 1) / 2 * spacing)
 
 
-def _terrain(b: ModelBuilder, rough: bool, seed: int):
-    if rough:
+def curriculum_heightfield(seed: int, rows: int = 5, cols: int = 6, patch: float = 8.0, spacing: float = 0.1,
+                           amplitude: tuple = (0.0, 0.12)):
+    """Terrain-curriculum grid (mjlab's rough-terrain generator analog, planar reference terrain.py:293-328
+    restated in 3-D): rows x cols patches of ``patch`` metres; row r carries smoothed uniform noise of
+    amplitude lerp(amplitude, r / (rows - 1)); each patch has a flat 1 m spawn pad at its centre.
+    Patch (row r, col c) spans x in [c P, (c+1) P), y in [r P, (r+1) P); origin (0, 0)."""
+    nx, ny = int(round(cols * patch / spacing)) + 1, int(round(rows * patch / spacing)) + 1
+    rng = np.random.default_rng(seed)
+    h = rng.uniform(-1.0, 1.0, size=(ny + 2, nx + 2))
+    h = sum(h[i:i + ny, j:j + nx] for i in range(3) for j in range(3)) / 9.0
+    x = np.arange(nx) * spacing
+    y = np.arange(ny) * spacing
+    row = np.minimum((y / patch).astype(int), rows - 1)
+    amp = amplitude[0] + (amplitude[1] - amplitude[0]) * row / max(rows - 1, 1)
+    h = h * amp[:, None]
+    px = np.abs((x % patch) - 0.5 * patch)
+    py = np.abs((y % patch) - 0.5 * patch)
+    pad = (py[:, None] < 0.5) & (px[None, :] < 0.5)
+    return np.where(pad, 0.0, h), spacing, (0.0, 0.0)
+
+
+def _terrain(b: ModelBuilder, rough, seed: int):
+    if rough == "curriculum":
+        data, sp, origin = curriculum_heightfield(seed)
+        b.heightfield(data, sp, origin, friction=1.0)
+    elif rough:
         data, sp, origin = rough_heightfield(seed)
         b.heightfield(data, sp, origin, friction=1.0)
     else:
         b.plane(friction=1.0)
 
 
-def g1_like(rough: bool = False, seed: int = 0, actuator_kind: int = ACT_IMPLICIT, self_collision: bool = True,
+def g1_like(rough: bool | str = False, seed: int = 0, actuator_kind: int = ACT_IMPLICIT, self_collision: bool = True,
             opt: Opt | None = None):
+    """rough: False (plane), True (16 m seeded rough patch), "curriculum" (5 x 6 graded patches)."""
     b = ModelBuilder("g1_like", opt)
     _terrain(b, rough, seed)
     pelvis = b.body("pelvis", 0, pos=(0, 0, 0.793), mass=3.81, inertia=(0.010, 0.009, 0.008))

@@ -59,6 +59,13 @@ class VelocityTaskCfg:
     friction_range: tuple = (0.6, 1.2)
     push_interval: tuple | None = (10.0, 15.0)
     push_velocity: float = 0.5
+    # terrain curriculum (robots.curriculum_heightfield): None disables. Worlds spawn at the centre of their
+    # (level row, world_id % cols) patch; at episode end a world walked farther than promote x its commanded
+    # distance moves one row up, less than demote x down (the planar reference's terrain_levels rule).
+    curriculum: tuple | None = None    # (rows, cols, patch metres)
+    curriculum_max_init_level: int = 1
+    curriculum_promote: float = 0.8
+    curriculum_demote: float = 0.4
 
     def scan_points(self):
         nx = int(round(self.scan_size[0] / self.scan_resolution)) + 1
@@ -221,6 +228,16 @@ class VelocityEnv3D:
                 t.friction_range[:] = cfg.friction_range
                 t.push_interval[:] = cfg.push_interval
                 t.push_velocity = cfg.push_velocity
+            if cfg.curriculum is not None:
+                rows, cols, patch = cfg.curriculum
+                t.curriculum, t.terrain_rows, t.terrain_cols, t.patch_size = 1, rows, cols, patch
+                t.curriculum_max_init_level = cfg.curriculum_max_init_level
+                t.curriculum_promote, t.curriculum_demote = cfg.curriculum_promote, cfg.curriculum_demote
+                self.terrain_level = torch.zeros(n, dtype=torch.int32, device=dev)
+                self.spawn_xy = z(n, 2)
+                self.cmd_dist = z(n)
+                t.terrain_level = self.terrain_level.data_ptr()
+                t.spawn_xy, t.cmd_dist = self.spawn_xy.data_ptr(), self.cmd_dist.data_ptr()
             t.cmd_resample_steps = cfg.command_resample_steps
             t.track_sigma = cfg.track_sigma
             t.min_height, t.max_tilt_cos, t.reset_joint_jitter = cfg.min_height, cfg.max_tilt_cos, \

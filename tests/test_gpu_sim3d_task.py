@@ -16,6 +16,8 @@ from paper_2601_22074_b200.sim3d.task import VelocityTaskCfg
 
 CASES = {
     "g1_flat": (lambda: robots.g1_like(), robots.G1_DEFAULT_JOINTS, dict()),
+    "g1_curriculum": (lambda: robots.g1_like(rough="curriculum", seed=2), robots.G1_DEFAULT_JOINTS,
+                      dict(height_scan=True, curriculum=(5, 6, 8.0), curriculum_max_init_level=3)),
     "g1_rough_scan": (lambda: robots.g1_like(rough=True, seed=1), robots.G1_DEFAULT_JOINTS, dict(height_scan=True)),
     "go1_flat": (lambda: robots.go1_like(), robots.GO1_DEFAULT_JOINTS, dict(min_height=0.15)),
 }
@@ -71,6 +73,10 @@ def _load(env, ref):
     if getattr(env, "event_timer", None) is not None:
         env.event_timer.copy_(t(ref.ev_timer))
         env.data.friction_scale.copy_(t(ref.fscale))
+    if getattr(env, "terrain_level", None) is not None:
+        env.terrain_level.copy_(t(ref.level.astype(np.int32)))
+        env.spawn_xy.copy_(t(ref.spawn))
+        env.cmd_dist.copy_(t(ref.cmd_dist))
     env.global_step = ref.global_step
 
 
@@ -312,3 +318,34 @@ def test_domain_randomisation_events_match_oracle():
         np.testing.assert_allclose(env.event_timer.cpu().numpy(), ref.ev_timer, atol=1e-12)
         np.testing.assert_allclose(env.data.qvel.cpu().numpy(), ref.qvel, rtol=1e-8, atol=1e-8)
     assert pushes > 0
+
+
+@pytest.mark.gpu
+def test_terrain_curriculum_levels_match_oracle():
+    """Terrain curriculum: spawn on the world's (level, column) patch, commanded-distance bookkeeping,
+    promotion/demotion on finished episodes (short episodes and commands force both directions)."""
+    import torch
+
+    n = 12
+    env, ref = _pair("g1_curriculum", n, episode_steps=2, command_ranges=((-0.05, 0.05), (-0.05, 0.05), (0, 0)),
+                     curriculum_promote=0.5, curriculum_demote=0.2)
+    np.testing.assert_allclose(env.reset().cpu().numpy(), ref.reset(), atol=1e-12)
+    np.testing.assert_array_equal(env.terrain_level.cpu().numpy(), ref.level)
+    np.testing.assert_allclose(env.spawn_xy.cpu().numpy(), ref.spawn, atol=1e-12)
+    rng = np.random.default_rng(21)
+    moved = 0
+    for k in range(6):
+        _load(env, ref)
+        lv0 = ref.level.copy()
+        a = rng.uniform(-1, 1, size=(n, env.model.nu))
+        o, r, te, tr = env.step(torch.as_tensor(a, device="cuda"))
+        o_ref, r_ref, te_ref, tr_ref = ref.step(a)
+        torch.cuda.synchronize()
+        moved += int((ref.level != lv0).sum())
+        np.testing.assert_array_equal(env.terrain_level.cpu().numpy(), ref.level)
+        np.testing.assert_allclose(env.spawn_xy.cpu().numpy(), ref.spawn, atol=1e-12)
+        np.testing.assert_allclose(env.cmd_dist.cpu().numpy(), ref.cmd_dist, atol=1e-12)
+        np.testing.assert_array_equal(te.cpu().numpy().astype(bool), te_ref)
+        np.testing.assert_allclose(r.cpu().numpy(), r_ref, rtol=1e-8, atol=1e-10)
+        np.testing.assert_allclose(o.cpu().numpy(), o_ref, rtol=1e-7, atol=1e-7)
+    assert moved > 0
