@@ -267,6 +267,21 @@ class VelocityEnv3D:
         N.call("s3_env_step", ctypes.byref(self.dm.struct), ctypes.byref(d), ctypes.byref(self.dm.layout),
                ctypes.byref(self.task), ptr, int(mode), int(self.global_step), st, launch=True)
 
+    def metrics_record(self, step: int, group=None, steps_per_sec=None):
+        """Job-wide statistics of the last step (metrics.py record): reward mean, running episode return,
+        terminated / truncated counts, terrain-level histogram -- packed into one float64 vector and
+        all-reduced in ONE collective across ranks (NCCL between GPUs; no-op on one rank)."""
+        from .. import metrics
+
+        rows = self.cfg.curriculum[0] if getattr(self.cfg, "curriculum", None) else 1
+        levels = getattr(self, "terrain_level", None)
+        levels = (levels if levels is not None else torch.zeros_like(self.episode_step)).long()
+        counts = torch.stack([self.terminated.sum(), self.truncated.sum()])
+        vec = metrics.pack_stats(self.reward, [self.episode_return], counts, levels, rows,
+                                 torch.zeros(1, device=self.reward.device))
+        metrics.allreduce_stats(vec, group)
+        return metrics.unpack_stats(vec, ["episode_return"], ["terminated", "truncated"], rows, step, steps_per_sec)
+
     def reset(self):
         """Reset every world (counter 0 draws) and return the observation tensor."""
         self.global_step = 0

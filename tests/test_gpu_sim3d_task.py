@@ -349,3 +349,18 @@ def test_terrain_curriculum_levels_match_oracle():
         np.testing.assert_allclose(r.cpu().numpy(), r_ref, rtol=1e-8, atol=1e-10)
         np.testing.assert_allclose(o.cpu().numpy(), o_ref, rtol=1e-7, atol=1e-7)
     assert moved > 0
+
+
+@pytest.mark.gpu
+def test_metrics_record_one_allreduce():
+    """Episode statistics of the 3-D env through metrics.pack_stats / unpack_stats (one collective)."""
+    import torch
+
+    env, ref = _pair("g1_curriculum", 8, episode_steps=2)
+    env.reset()
+    for _ in range(3):
+        env.step(torch.rand(8, env.model.nu, dtype=torch.float64, device="cuda") * 2 - 1)
+    rec = env.metrics_record(step=3)
+    assert abs(rec.reward_mean - float(env.reward.mean())) < 1e-9  # the record rounds to 10 decimals
+    assert sum(rec.terrain_row_histogram) == 8
+    assert rec.termination_counts["terminated"] + rec.termination_counts["truncated"] >= 0
