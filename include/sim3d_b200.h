@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define S3_ABI_VERSION 13
+#define S3_ABI_VERSION 14
 #define S3_F64 0
 #define S3_F32 1
 
@@ -176,6 +176,7 @@ typedef struct s3_data {
     void* qfrc_applied;
     void* time;
     void* friction_scale; /* (N,) per-world friction multiplier (domain randomisation), NULL = 1 */
+    void* mass_scale;     /* (N,) per-world scale of body 1's mass and inertia, NULL = 1 */
     /* outputs of the LAST substep of a launch (for parity tests / sensors) */
     void* xpos;
     void* xquat;
@@ -254,6 +255,7 @@ typedef struct s3_task {
     int32_t events; /* velocity kind: 1 = startup friction randomisation + interval pushes */
     int32_t pad3;
     double friction_range[2];
+    double base_mass_range[2];
     double push_interval[2];
     double push_velocity;
     void* event_timer; /* (N,) time to the next push */

@@ -123,19 +123,32 @@ def kinematics(m, qpos):
                 geom_xpos=gxpos, geom_xmat=gxmat)
 
 
-def com_pos(m, K):
-    """Subtree com of every kinematic tree, cinert about its tree's com, cdof (mj_comPos)."""
+def body_mass_scaled(m, mscale):
+    """Per-world base-mass randomisation: body 1 (the robot base) scaled in mass and inertia."""
+    mass = m.body_mass.copy()
+    inertia = m.body_inertia.copy()
+    if mscale != 1.0:
+        mass[1] = mass[1] * mscale
+        inertia[1] = inertia[1] * mscale
+    return mass, inertia
+
+
+def com_pos(m, K, mscale=1.0):
+    """Subtree com of every kinematic tree, cinert about its tree's com, cdof (mj_comPos).
+    ``mscale``: the world's base-mass scale (domain randomisation)."""
+    mass, inertia = body_mass_scaled(m, mscale)
     coms = np.zeros((m.ntree, 3))
     for t in range(m.ntree):
         sel = [b for b in range(1, m.nbody) if m.body_treeid[b] == t]
-        coms[t] = (m.body_mass[sel][:, None] * K["xipos"][sel]).sum(0) / m.tree_mass[t]
+        tmass = m.tree_mass[t] + (mass[1] - m.body_mass[1] if m.body_treeid[1] == t else 0.0)
+        coms[t] = (mass[sel][:, None] * K["xipos"][sel]).sum(0) / tmass
     cinert = np.zeros((m.nbody, 10))
     for b in range(1, m.nbody):
         com = coms[m.body_treeid[b]]
         R = K["ximat"][b]
-        I = R @ np.diag(m.body_inertia[b]) @ R.T
+        I = R @ np.diag(inertia[b]) @ R.T
         d = K["xipos"][b] - com
-        mb = m.body_mass[b]
+        mb = mass[b]
         I = I + mb * ((d @ d) * np.eye(3) - np.outer(d, d))
         cinert[b] = (I[0, 0], I[1, 1], I[2, 2], I[0, 1], I[0, 2], I[1, 2], mb * d[0], mb * d[1], mb * d[2], mb)
     cdof = np.zeros((m.nv, 6))
@@ -663,10 +676,10 @@ def integrate_pos(m, qpos, qvel, dt):
     return q
 
 
-def forward(m, qpos, qvel, ctrl, qfrc_applied=None, warm=None, fscale=1.0):
+def forward(m, qpos, qvel, ctrl, qfrc_applied=None, warm=None, fscale=1.0, mscale=1.0):
     """Everything of one substep up to (and including) the constraint solve."""
     K = kinematics(m, qpos)
-    C = com_pos(m, K)
+    C = com_pos(m, K, mscale)
     M, crbs = crb(m, C)
     L = factor_ldl(m, M)
     cvel, cdofd = com_vel(m, C, qvel)
@@ -684,11 +697,11 @@ def forward(m, qpos, qvel, ctrl, qfrc_applied=None, warm=None, fscale=1.0):
                 efc_force=force, qfrc_constraint=qfrc_con, iterations=its)
 
 
-def step(m, qpos, qvel, ctrl, qfrc_applied=None, warm=None, fscale=1.0):
+def step(m, qpos, qvel, ctrl, qfrc_applied=None, warm=None, fscale=1.0, mscale=1.0):
     """One substep: forward, implicitfast velocity update, position integration.
     Returns (qpos, qvel, qacc_warmstart, forward-dict)."""
     dt = m.opt.timestep
-    F = forward(m, qpos, qvel, ctrl, qfrc_applied, warm, fscale)
+    F = forward(m, qpos, qvel, ctrl, qfrc_applied, warm, fscale, mscale)
     Mt = F["M"].copy()
     Mt[np.diag_indices(m.nv)] += dt * (m.dof_damping + F["kvd"])
     Lt = factor_ldl(m, Mt)
@@ -773,6 +786,7 @@ class TaskOracle:
         self.global_step = 0
         self.act_default = self.default[act]
         self.fscale = np.ones(nworld)          # startup event: per-world friction scale
+        self.mscale = np.ones(nworld)          # startup event: per-world base-mass scale
         self.ev_timer = np.zeros(nworld)       # interval event: time to the next push
         self.level = np.zeros(nworld, dtype=np.int64)   # terrain curriculum row
         self.spawn = np.zeros((nworld, 2))
@@ -829,8 +843,10 @@ class TaskOracle:
                 self.level[w] = min(int(u * (self.cfg.curriculum_max_init_level + 1)), self.cfg.curriculum[0] - 1)
         if self._events_on():  # startup randomisation (purpose 5, counter 0, slot 0)
             lo, hi = self.cfg.friction_range
+            mlo, mhi = self.cfg.base_mass_range
             for w in range(self.n):
                 self.fscale[w] = lo + (hi - lo) * uniform(self.key(w, 5), 0)
+                self.mscale[w] = mlo + (mhi - mlo) * uniform(self.key(w, 5), 5)
         for w in range(self.n):
             self.reset_world(w, 0)
         return self.observe(0)
@@ -889,7 +905,7 @@ class TaskOracle:
             ctrl = self.act_default + cfg.action_scale * a
             q, v, warm = self.qpos[w], self.qvel[w], self.warm[w]
             for _ in range(cfg.decimation):
-                q, v, warm, _ = step(m, q, v, ctrl, warm=warm, fscale=self.fscale[w])
+                q, v, warm, _ = step(m, q, v, ctrl, warm=warm, fscale=self.fscale[w], mscale=self.mscale[w])
             self.qpos[w], self.qvel[w], self.warm[w] = q, v, warm
             vb, om, g, _ = base_frame(m, q, v)
             e_xy = (self.cmd[w, 0] - vb[0]) ** 2 + (self.cmd[w, 1] - vb[1]) ** 2

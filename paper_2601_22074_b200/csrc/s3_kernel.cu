@@ -246,7 +246,7 @@ template <class T> __device__ void __noinline__ kinematics(const s3_model& m, co
 }
 
 // mj_comPos: xipos, subtree com (single tree), cinert, cdof; geom frames
-template <class T> __device__ void __noinline__ com_pos(const s3_model& m, const s3_layout& L_, T* B_, int lane) {
+template <class T> __device__ void __noinline__ com_pos(const s3_model& m, const s3_layout& L_, T* B_, int lane, T ms) {
     WS<T> s = make_ws(B_, L_);
     const T* ipos = F<T>(m.body_ipos);
     const T* ilmat = F<T>(m.body_ilmat);
@@ -262,15 +262,16 @@ template <class T> __device__ void __noinline__ com_pos(const s3_model& m, const
         s.xipos[3 * b + 2] = s.xpos[3 * b + 2] + v[2];
     }
     __syncwarp();
-    // subtree com of every kinematic tree (each tree's c-frame origin)
+    // subtree com of every kinematic tree (each tree's c-frame origin); body 1's mass scaled by ms
     const T* tmass = F<T>(m.tree_mass);
     for (int t = 0; t < m.nkintree; ++t) {
         T cx = T(0), cy = T(0), cz = T(0);
         for (int b = 1 + lane; b < m.nbody; b += 32) {
             if (m.body_treeid[b] != t) continue;
-            cx += mass[b] * s.xipos[3 * b]; cy += mass[b] * s.xipos[3 * b + 1]; cz += mass[b] * s.xipos[3 * b + 2];
+            T mb = b == 1 ? mass[b] * ms : mass[b];
+            cx += mb * s.xipos[3 * b]; cy += mb * s.xipos[3 * b + 1]; cz += mb * s.xipos[3 * b + 2];
         }
-        T inv = T(1) / tmass[t];
+        T inv = T(1) / (m.body_treeid[1] == t ? tmass[t] + (mass[1] * ms - mass[1]) : tmass[t]);
         cx = wsum(cx) * inv; cy = wsum(cy) * inv; cz = wsum(cz) * inv;
         if (lane == 0) { s.com[3 * t] = cx; s.com[3 * t + 1] = cy; s.com[3 * t + 2] = cz; }
     }
@@ -280,7 +281,8 @@ template <class T> __device__ void __noinline__ com_pos(const s3_model& m, const
         qmat(s.xquat + 4 * b, R);
         for (int k = 0; k < 9; ++k) IL[k] = ilmat[9 * b + k];
         mm3(R, IL, Ri);
-        T i0 = inertia[3 * b], i1 = inertia[3 * b + 1], i2 = inertia[3 * b + 2];
+        const T sb = b == 1 ? ms : T(1);
+        T i0 = inertia[3 * b] * sb, i1 = inertia[3 * b + 1] * sb, i2 = inertia[3 * b + 2] * sb;
         // I = Ri diag(i) Ri^T
         T I[9];
 #pragma unroll
@@ -290,7 +292,7 @@ template <class T> __device__ void __noinline__ com_pos(const s3_model& m, const
                                                      Ri[3 * r + 2] * i2 * Ri[3 * c + 2];
         const T* com = s.com + 3 * m.body_treeid[b];
         T d[3] = {s.xipos[3 * b] - com[0], s.xipos[3 * b + 1] - com[1], s.xipos[3 * b + 2] - com[2]};
-        T mb = mass[b];
+        T mb = b == 1 ? mass[b] * ms : mass[b];
         T dd = dot3(d, d);
         T* ci = s.cinert + 10 * b;
         ci[0] = I[0] + mb * (dd - d[0] * d[0]);
@@ -1463,7 +1465,7 @@ __device__ __noinline__ void substep(const s3_model& m, const s3_data& d, const 
     const T dt = T(m.timestep);
     int ncon = 0, nlim = 0, dropped = 0, its = 0;
     kinematics(m, L_, B_, lane);
-    com_pos(m, L_, B_, lane);
+    com_pos(m, L_, B_, lane, d.mass_scale ? static_cast<const T*>(d.mass_scale)[w] : T(1));
     geom_frames(m, L_, B_, lane);
     rne(m, L_, B_, lane);
     crb_mass(m, L_, B_, lane);
@@ -2080,6 +2082,8 @@ __global__ void __launch_bounds__(32 * 16) env_kernel(const __grid_constant__ s3
                 uint64_t k5 = stream_key(tk.seed, tk.world_offset + w, 5);
                 static_cast<T*>(d.friction_scale)[w] =
                     T(tk.friction_range[0]) + T(tk.friction_range[1] - tk.friction_range[0]) * uniform01<T>(k5, 0);
+                static_cast<T*>(d.mass_scale)[w] =
+                    T(tk.base_mass_range[0]) + T(tk.base_mass_range[1] - tk.base_mass_range[0]) * uniform01<T>(k5, 5);
                 static_cast<T*>(tk.event_timer)[w] =
                     T(tk.push_interval[0]) + T(tk.push_interval[1] - tk.push_interval[0]) * uniform01<T>(k5, 1);
             }
@@ -2472,8 +2476,8 @@ int s3_env_step(const s3_model* m, const s3_data* d, const s3_layout* l, const s
     if (d->nworld == 0) return S3_OK;
     if (!d->qpos || !d->qvel || !d->qacc_warmstart) return fail(S3_ERR_ARG, "qpos/qvel/qacc_warmstart required");
     if (mode == 0 && !actions) return fail(S3_ERR_ARG, "actions required");
-    if (t->kind == 0 && t->events && (!d->friction_scale || !t->event_timer))
-        return fail(S3_ERR_ARG, "events need friction_scale and event_timer");
+    if (t->kind == 0 && t->events && (!d->friction_scale || !d->mass_scale || !t->event_timer))
+        return fail(S3_ERR_ARG, "events need friction_scale, mass_scale and event_timer");
     const int want = t->kind == 1 ? 15 + 5 * m->nu : (t->kind == 2 ? 13 + 3 * m->nu : 12 + 3 * m->nu + t->nscan);
     if (t->obs_dim != want || t->nscan > S3_MAX_RAYS || t->decimation < 1 ||
         (t->kind == 1 && (t->nframes < 2 || !t->motion_qpos || !t->motion_qvel || m->nq + m->nv > m->nv * (m->nv + 1) / 2)))

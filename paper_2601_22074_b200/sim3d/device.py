@@ -286,6 +286,7 @@ class Data:
         self.qfrc_applied = None
         self.time = torch.zeros(nworld, dtype=dt, device=dev)
         self.friction_scale = None  # (N,) per-world friction multiplier (domain randomisation)
+        self.mass_scale = None      # (N,) per-world scale of the base body's mass and inertia
         self.geom_xpos = None
         self.geom_xmat = None
         self._out = None
@@ -314,7 +315,7 @@ class Data:
         s = N.DataT()
         s.nworld = self.nworld
         for name in ("qpos", "qvel", "ctrl", "qacc_warmstart", "qfrc_applied", "time", "geom_xpos", "geom_xmat",
-                     "friction_scale"):
+                     "friction_scale", "mass_scale"):
             t = getattr(self, name)
             setattr(s, name, None if t is None else t.data_ptr())
         if outputs:

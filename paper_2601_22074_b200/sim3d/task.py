@@ -57,6 +57,7 @@ class VelocityTaskCfg:
     # domain randomisation (EventManager analog): startup per-world friction scale; interval pushes that
     # add U(-v, v) to the base's planar velocity every U(push_interval) seconds. None disables pushes.
     friction_range: tuple = (0.6, 1.2)
+    base_mass_range: tuple = (0.8, 1.2)  # startup scale of the base body's mass and inertia
     push_interval: tuple | None = (10.0, 15.0)
     push_velocity: float = 0.5
     # terrain curriculum (robots.curriculum_heightfield): None disables. Worlds spawn at the centre of their
@@ -226,6 +227,8 @@ class VelocityEnv3D:
                 self.event_timer = z(n)
                 t.event_timer = self.event_timer.data_ptr()
                 t.friction_range[:] = cfg.friction_range
+                t.base_mass_range[:] = cfg.base_mass_range
+                self.data.mass_scale = torch.ones(n, dtype=dt, device=dev)
                 t.push_interval[:] = cfg.push_interval
                 t.push_velocity = cfg.push_velocity
             if cfg.curriculum is not None:

@@ -73,6 +73,7 @@ def _load(env, ref):
     if getattr(env, "event_timer", None) is not None:
         env.event_timer.copy_(t(ref.ev_timer))
         env.data.friction_scale.copy_(t(ref.fscale))
+        env.data.mass_scale.copy_(t(ref.mscale))
     if getattr(env, "terrain_level", None) is not None:
         env.terrain_level.copy_(t(ref.level.astype(np.int32)))
         env.spawn_xy.copy_(t(ref.spawn))
@@ -293,15 +294,16 @@ def test_ppo_trains_on_the_3d_env():
 
 @pytest.mark.gpu
 def test_domain_randomisation_events_match_oracle():
-    """Startup friction randomisation (per world) and interval pushes: pushes every 1-3 control steps
-    here, so the kicked base velocities, timers and friction scales are all compared."""
+    """Startup friction and base-mass randomisation (per world) and interval pushes: pushes every 1-3
+    control steps here, so the kicked base velocities, timers and both scales are all compared."""
     import torch
 
     n = 8
     env, ref = _pair("g1_flat", n, push_interval=(0.02, 0.06), push_velocity=0.8)
     np.testing.assert_allclose(env.reset().cpu().numpy(), ref.reset(), atol=1e-12)
     np.testing.assert_allclose(env.data.friction_scale.cpu().numpy(), ref.fscale, atol=1e-15)
-    assert ref.fscale.std() > 0.01
+    np.testing.assert_allclose(env.data.mass_scale.cpu().numpy(), ref.mscale, atol=1e-15)
+    assert ref.fscale.std() > 0.01 and ref.mscale.std() > 0.01
     rng = np.random.default_rng(12)
     pushes = 0
     for k in range(5):
