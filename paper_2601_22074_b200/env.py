@@ -538,7 +538,9 @@ class ManagerBasedRlEnv:
         terminated, truncated), valid until ``step_async`` has been called
         ``PIPE_SLOTS`` more times. At most ``PIPE_SLOTS`` steps may be pending;
         with three, the host enqueues step i+1 while steps i-1 and i are in
-        flight, hiding its own per-step cost."""
+        flight, hiding its own per-step cost. The action tensor is read
+        asynchronously: do not overwrite it before that step's step_wait()
+        returns."""
         import torch
 
         if getattr(self, "_host_mirror", None) is not None:
