@@ -279,3 +279,42 @@ def test_sim3d_library_exports_and_plans_on_cpu():
     bad.nv = 65
     with pytest.raises(N.NativeError):
         N.call("s3_plan", ctypes.byref(bad), 0, ctypes.byref(N.LayoutT()))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_self_contacts_take_the_dense_newton_path(dtype):
+    """Crossed shins (a self pair coupling both legs) break the tree pattern of H = M + J^T D J; the
+    kernel falls back to the dense Cholesky for that Newton solve -- still equal to the oracle."""
+    import torch
+
+    from paper_2601_22074_b200.sim3d.device import Data, DeviceModel
+
+    mg, m = robots.g1_like(), robots.g1_like()
+    dm = DeviceModel(mg, dtype)
+    dm.set_const()
+    O.set_const(m)
+    q = robots.default_qpos(m, robots.G1_DEFAULT_JOINTS)
+    q[m.jnt_qposadr[m.jnt_names.index("left_hip_roll_joint")]] = -0.45
+    q[m.jnt_qposadr[m.jnt_names.index("right_hip_roll_joint")]] = 0.45
+    K = O.kinematics(m, q)
+    low = min(K["geom_xpos"][g][2] - m.geom_rbound[g] for g in range(1, m.ngeom))
+    q[2] -= low + 0.004
+    n = 4
+    rng = np.random.default_rng(3)
+    V = rng.normal(size=(n, m.nv)) * 0.2
+    d = Data(dm, n)
+    d.qpos.copy_(torch.as_tensor(np.tile(q, (n, 1))))
+    d.qvel.copy_(torch.as_tensor(V))
+    ctrl = np.tile(q[m.actuator_qposadr], (n, 1))
+    d.ctrl.copy_(torch.as_tensor(ctrl))
+    out = d.step(1, outputs=True)
+    torch.cuda.synchronize()
+    tol = 1e-8 if dtype == "f64" else 3e-3
+    for w in range(n):
+        _, v1, _, F = O.step(m, q, V[w], ctrl[w], warm=np.zeros(m.nv))
+        cons = F["contacts"]
+        assert any(c["geom1"] != 0 for c in cons)  # a robot-robot (self) contact is present
+        assert int(out["ncon"][w]) == len(cons)
+        qa = out["qacc"][w].double().cpu().numpy()
+        assert np.max(np.abs(qa - F["qacc"])) < tol * max(1.0, np.max(np.abs(F["qacc"])))
