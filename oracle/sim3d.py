@@ -427,7 +427,7 @@ def _point_set(m, K, g):
 
 def collide(m, K, fscale=1.0):
     """Broadphase (bounding spheres) + narrowphase over the compiled candidate pairs, in pair order;
-    at most MAX_CON contacts (later ones dropped and counted). ``fscale``: the world's friction
+    at most m.ncon_max contacts (later ones dropped and counted). ``fscale``: the world's friction
     scale (domain randomisation), multiplying every pair's friction."""
     cons, dropped = [], 0
     hmax = float(m.hfield_data.max())
@@ -488,7 +488,7 @@ def collide(m, K, fscale=1.0):
         if t2 == GEOM_BOX:
             found = found[:4]
         for d, n, pos in found:
-            if len(cons) >= MAX_CON:
+            if len(cons) >= m.ncon_max:
                 dropped += 1
                 continue
             cons.append(dict(dist=d, pos=pos, frame=make_frame(n), mu=mu, pair=p, geom1=g1, geom2=g2))

@@ -145,7 +145,7 @@ template <class T> __device__ inline T clampt(T x, T lo, T hi) { return x < lo ?
 
 template <class T> struct WS {
     T *xpos, *xquat, *xipos, *cinert, *crb, *cdof, *cdofd, *cvel, *cacc, *janc, *jax, *M, *LD, *qpos, *qvel,
-        *smooth, *a0, *a, *Ma, *grad, *p, *Mp, *kvd, *gpos, *gmat, *con, *Jc, *raref, *rD, *rjar, *rJp, *cdot,
+        *smooth, *a0, *a, *Ma, *grad, *p, *Mp, *kvd, *con, *Jc, *raref, *rD, *rjar, *rJp, *cdot,
         *bias, *fcon, *ctrl, *com, *tk, *u, *snap;
     int *con_pair, *lim_dof, *lim_sign, *misc;
 };
@@ -155,7 +155,7 @@ template <class T> __device__ inline WS<T> make_ws(T* base, const s3_layout& l) 
     const int* o = l.off;
     s.xpos = base + o[O_XPOS]; s.xquat = base + o[O_XQUAT]; s.xipos = base + o[O_XIPOS];
     s.cinert = base + o[O_CINERT]; s.crb = s.cinert; s.cdof = base + o[O_CDOF];
-    s.tk = base + o[O_CRB]; s.u = s.tk + S3_MAX_NV;
+    s.tk = base + o[O_CRB]; s.u = s.tk;
     s.janc = base + o[O_JANC]; s.jax = base + o[O_JAX];
     // factorization snapshot (rows touched by constraints, tree entries): xipos, cinert, janc, jax are
     // contiguous and dead from the end of the mass-matrix build until the next substep's kinematics
@@ -163,11 +163,13 @@ template <class T> __device__ inline WS<T> make_ws(T* base, const s3_layout& l) 
     // RNE scratch lives in the contact-Jacobian region (dead until build_rows)
     s.cdofd = base + o[O_JC]; s.cvel = s.cdofd + o[O_CDOFD]; s.cacc = s.cvel + o[O_CVEL];
     s.M = base + o[O_M]; s.LD = base + o[O_LD]; s.qpos = base + o[O_QPOS]; s.qvel = base + o[O_QVEL];
-    s.smooth = base + o[O_SMOOTH]; s.a0 = base + o[O_A0]; s.a = base + o[O_A]; s.Ma = base + o[O_MA];
+    s.smooth = base + o[O_SMOOTH]; s.a = base + o[O_A]; s.Ma = base + o[O_MA];
     s.grad = base + o[O_GRAD]; s.p = base + o[O_P]; s.Mp = base + o[O_MP]; s.kvd = base + o[O_KVD];
-    s.gpos = base + o[O_GPOS]; s.gmat = base + o[O_GMAT]; s.con = base + o[O_CON]; s.Jc = base + o[O_JC];
+    s.a0 = s.Mp;  // qacc_smooth: parity outputs only, written before Newton (which reuses Mp as scratch)
+    s.con = base + o[O_CON]; s.Jc = base + o[O_JC];
     s.raref = base + o[O_RAREF]; s.rD = base + o[O_RD]; s.rjar = base + o[O_RJAR]; s.rJp = base + o[O_RJP];
-    s.cdot = base + o[O_CDOT]; s.bias = base + o[O_BIAS]; s.fcon = base + o[O_FCON]; s.ctrl = base + o[O_CTRL];
+    s.cdot = base + o[O_CDOT]; s.bias = s.Ma;  // bias: RNE -> smooth_force, dead before Newton writes Ma
+    s.fcon = base + o[O_FCON]; s.ctrl = base + o[O_CTRL];
     s.com = base + o[O_COM];
     int* ib = reinterpret_cast<int*>(base + o[O_INT]);
     s.con_pair = ib;
@@ -329,25 +331,6 @@ template <class T> __device__ void __noinline__ com_pos(const s3_model& m, const
             T* r = s.cdof + 6 * da;
             r[0] = ax[0]; r[1] = ax[1]; r[2] = ax[2]; r[3] = lin[0]; r[4] = lin[1]; r[5] = lin[2];
         }
-    }
-    __syncwarp();
-}
-
-// geom frames from the body frames
-template <class T> __device__ void __noinline__ geom_frames(const s3_model& m, const s3_layout& L_, T* B_, int lane) {
-    WS<T> s = make_ws(B_, L_);
-    const T* gp = F<T>(m.geom_pos);
-    const T* gl = F<T>(m.geom_lmat);
-    for (int g = lane; g < m.ngeom; g += 32) {
-        int b = m.geom_bodyid[g];
-        T R[9], v[3], L[9];
-        qmat(s.xquat + 4 * b, R);
-        T p[3] = {gp[3 * g], gp[3 * g + 1], gp[3 * g + 2]};
-        mv3(R, p, v);
-        s.gpos[3 * g] = s.xpos[3 * b] + v[0]; s.gpos[3 * g + 1] = s.xpos[3 * b + 1] + v[1];
-        s.gpos[3 * g + 2] = s.xpos[3 * b + 2] + v[2];
-        for (int k = 0; k < 9; ++k) L[k] = gl[9 * g + k];
-        mm3(R, L, s.gmat + 9 * g);
     }
     __syncwarp();
 }
@@ -779,7 +762,6 @@ template <class T> __device__ void __noinline__ smooth_force(const s3_model& m, 
         T f = s.fcon[i] - damp[i] * s.qvel[i] - s.bias[i];
         if (applied) f += applied[i];
         s.smooth[i] = f;
-        s.a0[i] = f;
     }
     __syncwarp();
 }
@@ -841,10 +823,23 @@ template <class T> __device__ void seg_closest(const T* p1, const T* q1, const T
     for (int k = 0; k < 3; ++k) { A[k] = p1[k] + d1[k] * sN; B[k] = p2[k] + d2[k] * tN; }
 }
 
-template <class T> __device__ inline void segment(const s3_model& m, const WS<T>& s, int g, T* p, T* q) {
+// world frame of geom g from its body's frame (oracle kinematics: xpos + xmat @ geom_pos, xmat @ lmat);
+// computed where needed instead of stored per world (saves 12 ngeom shared-memory elements)
+template <class T> __device__ inline void geom_xform(const s3_model& m, const WS<T>& s, int g, T* c, T* R) {
+    const int b = m.geom_bodyid[g];
+    T Rb[9], v[3], L[9];
+    qmat(s.xquat + 4 * b, Rb);
+    const T* gp = F<T>(m.geom_pos) + 3 * g;
+    const T* gl = F<T>(m.geom_lmat) + 9 * g;
+    T pl[3] = {gp[0], gp[1], gp[2]};
+    mv3(Rb, pl, v);
+    c[0] = s.xpos[3 * b] + v[0]; c[1] = s.xpos[3 * b + 1] + v[1]; c[2] = s.xpos[3 * b + 2] + v[2];
+    for (int k = 0; k < 9; ++k) L[k] = gl[k];
+    mm3(Rb, L, R);
+}
+
+template <class T> __device__ inline void segment(const s3_model& m, int g, const T* c, const T* R, T* p, T* q) {
     T hl = F<T>(m.geom_size)[3 * g + 1];
-    const T* R = s.gmat + 9 * g;
-    const T* c = s.gpos + 3 * g;
     for (int k = 0; k < 3; ++k) {
         T a = R[3 * k + 2] * hl;
         p[k] = c[k] - a;
@@ -857,23 +852,22 @@ template <class T> __device__ inline int point_count(int type) {
     return type == kGeomSphere ? 1 : (type == kGeomCapsule ? 2 : 8);
 }
 
-template <class T> __device__ inline void point_of(const s3_model& m, const WS<T>& s, int g, int type, int k, T* q,
-                                                   T& r) {
+template <class T> __device__ inline void point_of(const s3_model& m, int g, const T* c, const T* R, int type, int k,
+                                                   T* q, T& r) {
     const T* sz = F<T>(m.geom_size) + 3 * g;
-    const T* c = s.gpos + 3 * g;
     if (type == kGeomSphere) {
         q[0] = c[0]; q[1] = c[1]; q[2] = c[2];
         r = sz[0];
     } else if (type == kGeomCapsule) {
         T p0[3], p1[3];
-        segment(m, s, g, p0, p1);
+        segment(m, g, c, R, p0, p1);
         const T* pp = k == 0 ? p0 : p1;
         q[0] = pp[0]; q[1] = pp[1]; q[2] = pp[2];
         r = sz[0];
     } else {
         T loc[3] = {(k & 1) ? sz[0] : -sz[0], (k & 2) ? sz[1] : -sz[1], (k & 4) ? sz[2] : -sz[2]};
         T v[3];
-        mv3(s.gmat + 9 * g, loc, v);
+        mv3(R, loc, v);
         q[0] = c[0] + v[0]; q[1] = c[1] + v[1]; q[2] = c[2] + v[2];
         r = T(0);
     }
@@ -884,18 +878,19 @@ template <class T> __device__ __noinline__ int narrow(const s3_model& m, const s
     WS<T> s = make_ws(B_, L_);
     int g1 = m.pair_geom[2 * p], g2 = m.pair_geom[2 * p + 1];
     int t1 = m.geom_type[g1], t2 = m.geom_type[g2];
-    const T* c1 = s.gpos + 3 * g1;
-    const T* c2 = s.gpos + 3 * g2;
+    T c1[3], R1[9], c2[3], R2[9];
+    geom_xform(m, s, g1, c1, R1);
+    geom_xform(m, s, g2, c2, R2);
     const T* rb = F<T>(m.geom_rbound);
     int cnt = 0, cap = t2 == kGeomBox ? 4 : 8;
     if (t1 == kGeomPlane) {
-        T n[3] = {s.gmat[9 * g1 + 2], s.gmat[9 * g1 + 5], s.gmat[9 * g1 + 8]};
+        T n[3] = {R1[2], R1[5], R1[8]};
         T dc[3] = {c2[0] - c1[0], c2[1] - c1[1], c2[2] - c1[2]};
         if (!(dot3(n, dc) - rb[g2] < T(0))) return 0;
         int np = point_count<T>(t2);
         for (int k = 0; k < np && cnt < cap; ++k) {
             T q[3], r;
-            point_of(m, s, g2, t2, k, q, r);
+            point_of(m, g2, c2, R2, t2, k, q, r);
             T dq[3] = {q[0] - c1[0], q[1] - c1[1], q[2] - c1[2]};
             T d = dot3(n, dq) - r;
             if (d < T(0)) {
@@ -911,7 +906,7 @@ template <class T> __device__ __noinline__ int narrow(const s3_model& m, const s
         int np = point_count<T>(t2);
         for (int k = 0; k < np && cnt < cap; ++k) {
             T q[3], r, d, n[3];
-            point_of(m, s, g2, t2, k, q, r);
+            point_of(m, g2, c2, R2, t2, k, q, r);
             if (hfield_point(m, q, r, d, n) && d < T(0)) {
                 Hit<T> h;
                 h.d = d;
@@ -925,14 +920,14 @@ template <class T> __device__ __noinline__ int narrow(const s3_model& m, const s
         T rr = rb[g1] + rb[g2];
         if (!(dot3(dv, dv) < rr * rr)) return 0;
         const T* sz = F<T>(m.geom_size);
-        const T* R = s.gmat + 9 * g2;
+        const T* R = R2;
         const T* hs = sz + 3 * g2;
         T r = sz[3 * g1];
         T p[3], q[3], dq[3];
         if (t1 == kGeomCapsule) {
             // segment point closest to the box: alternating projections from the midpoint (box frame)
             T e0[3], e1[3], a[3], b[3], dd3[3];
-            segment(m, s, g1, e0, e1);
+            segment(m, g1, c1, R1, e0, e1);
             for (int k = 0; k < 3; ++k) {
                 a[k] = R[k] * (e0[0] - c2[0]) + R[3 + k] * (e0[1] - c2[1]) + R[6 + k] * (e0[2] - c2[2]);
                 b[k] = R[k] * (e1[0] - c2[0]) + R[3 + k] * (e1[1] - c2[1]) + R[6 + k] * (e1[2] - c2[2]);
@@ -995,16 +990,16 @@ template <class T> __device__ __noinline__ int narrow(const s3_model& m, const s
             for (int k = 0; k < 3; ++k) { A[k] = c1[k]; B[k] = c2[k]; }
         } else if (t1 == kGeomSphere) {
             T p2[3], q2[3];
-            segment(m, s, g2, p2, q2);
+            segment(m, g2, c2, R2, p2, q2);
             seg_closest(p2, q2, c1, c1, B, A);
         } else if (t2 == kGeomSphere) {
             T p1[3], q1[3];
-            segment(m, s, g1, p1, q1);
+            segment(m, g1, c1, R1, p1, q1);
             seg_closest(p1, q1, c2, c2, A, B);
         } else {
             T p1[3], q1[3], p2[3], q2[3];
-            segment(m, s, g1, p1, q1);
-            segment(m, s, g2, p2, q2);
+            segment(m, g1, c1, R1, p1, q1);
+            segment(m, g2, c2, R2, p2, q2);
             seg_closest(p1, q1, p2, q2, A, B);
         }
         T e[3] = {B[0] - A[0], B[1] - A[1], B[2] - A[2]};
@@ -1059,7 +1054,7 @@ template <class T> __device__ int __noinline__ collide(const s3_model& m, const 
             T mu = fmax(fric[g1], fric[g2]) * fscale;
             for (int k = 0; k < cnt; ++k) {
                 int slot = off + k;
-                if (slot < S3_MAX_CON) {
+                if (slot < m.ncon_max) {
                     const Hit<T>& h = hits[k];
                     T* c = s.con + kConStride * slot;
                     c[0] = h.d;
@@ -1073,9 +1068,9 @@ template <class T> __device__ int __noinline__ collide(const s3_model& m, const 
         base += total;
     }
     __syncwarp();
-    if (base > S3_MAX_CON) {
-        dropped = base - S3_MAX_CON;
-        base = S3_MAX_CON;
+    if (base > m.ncon_max) {
+        dropped = base - m.ncon_max;
+        base = m.ncon_max;
     }
     return base;
 }
@@ -1466,7 +1461,6 @@ __device__ __noinline__ void substep(const s3_model& m, const s3_data& d, const 
     int ncon = 0, nlim = 0, dropped = 0, its = 0;
     kinematics(m, L_, B_, lane);
     com_pos(m, L_, B_, lane, d.mass_scale ? static_cast<const T*>(d.mass_scale)[w] : T(1));
-    geom_frames(m, L_, B_, lane);
     rne(m, L_, B_, lane);
     crb_mass(m, L_, B_, lane);
     int np = nv * (nv + 1) / 2;
@@ -1487,7 +1481,14 @@ __device__ __noinline__ void substep(const s3_model& m, const s3_data& d, const 
             uint64_t mk = __ldg(cm + i);
             for (int j = 0; j <= i; ++j) o[tri(i, j)] = ((mk >> j) & 1ull) ? s.LD[tri(i, j)] : T(0);
         }
+        for (int i = lane; i < nv; i += 32) s.a0[i] = s.smooth[i];
+        __syncwarp();
         solve_ldl(m, s.LD, s.a0, lane);
+        // bias and qacc_smooth alias Newton scratch: emit them now
+        for (int i = lane; i < nv; i += 32) {
+            static_cast<T*>(d.qfrc_bias)[w * nv + i] = s.bias[i];
+            static_cast<T*>(d.qacc_smooth)[w * nv + i] = s.a0[i];
+        }
     }
     build_rows(m, L_, B_, ncon, nlim, lane);
     if (gw) {
@@ -1508,9 +1509,7 @@ __device__ __noinline__ void substep(const s3_model& m, const s3_data& d, const 
         T* oM = static_cast<T*>(d.qM) + w * np;
         for (int t = lane; t < np; t += 32) oM[t] = s.M[t];
         for (int i = lane; i < nv; i += 32) {
-            static_cast<T*>(d.qfrc_bias)[w * nv + i] = s.bias[i];
             static_cast<T*>(d.qfrc_smooth)[w * nv + i] = s.smooth[i];
-            static_cast<T*>(d.qacc_smooth)[w * nv + i] = s.a0[i];
             static_cast<T*>(d.qacc)[w * nv + i] = s.a[i];
             static_cast<T*>(d.qfrc_constraint)[w * nv + i] = s.fcon[i];
             for (int k = 0; k < 6; ++k) static_cast<T*>(d.cdof)[(w * nv + i) * 6 + k] = s.cdof[6 * i + k];
@@ -1572,10 +1571,11 @@ template <class T> __device__ __noinline__ void store_geom_frames(const s3_model
     WS<T> s = make_ws(B_, L_);
     // frames at the FINAL state of the launch (what sensors see)
     kinematics(m, L_, B_, lane);
-    geom_frames(m, L_, B_, lane);
     for (int g = lane; g < m.ngeom; g += 32) {
-        for (int k = 0; k < 3; ++k) static_cast<T*>(d.geom_xpos)[(w * m.ngeom + g) * 3 + k] = s.gpos[3 * g + k];
-        for (int k = 0; k < 9; ++k) static_cast<T*>(d.geom_xmat)[(w * m.ngeom + g) * 9 + k] = s.gmat[9 * g + k];
+        T c[3], R[9];
+        geom_xform(m, s, g, c, R);
+        for (int k = 0; k < 3; ++k) static_cast<T*>(d.geom_xpos)[(w * m.ngeom + g) * 3 + k] = c[k];
+        for (int k = 0; k < 9; ++k) static_cast<T*>(d.geom_xmat)[(w * m.ngeom + g) * 9 + k] = R[k];
     }
 }
 
@@ -1916,9 +1916,10 @@ template <class T>
 __device__ __noinline__ void lift_ee(const s3_model& m, const s3_task& tk, const s3_layout& L_, T* B_, T* ee, int lane) {
     WS<T> s = make_ws(B_, L_);
     kinematics(m, L_, B_, lane);
-    geom_frames(m, L_, B_, lane);
-    const int g0 = tk.tip_geom[0], g1 = tk.tip_geom[1];
-    for (int k = 0; k < 3; ++k) ee[k] = T(0.5) * (s.gpos[3 * g0 + k] + s.gpos[3 * g1 + k]);
+    T c0[3], c1[3], R[9];
+    geom_xform(m, s, tk.tip_geom[0], c0, R);
+    geom_xform(m, s, tk.tip_geom[1], c1, R);
+    for (int k = 0; k < 3; ++k) ee[k] = T(0.5) * (c0[k] + c1[k]);
 }
 
 template <class T>
@@ -2427,19 +2428,22 @@ const char* s3_last_error(void) { return g_err; }
 int s3_plan(const s3_model* m, int32_t warps_per_block, s3_layout* out) {
     using namespace s3;
     if (!m || !out) return fail(S3_ERR_ARG, "null argument");
-    if (m->nv > S3_MAX_NV || m->nbody > S3_MAX_NBODY || m->chain_stride > S3_MAX_CHAIN || m->nlimjnt > 64)
+    if (m->nv > S3_MAX_NV || m->nbody > S3_MAX_NBODY || m->chain_stride > S3_MAX_CHAIN || m->nlimjnt > 64 ||
+        m->ncon_max < 1 || m->ncon_max > S3_MAX_CON)
         return fail(S3_ERR_BOUNDS, "model exceeds kernel bounds");
     int nb = m->nbody, nv = m->nv, nj = m->njnt, ng = m->ngeom, nq = m->nq, nu = m->nu;
     int np = nv * (nv + 1) / 2;
     int sizes[O_END] = {};
     sizes[O_XPOS] = 3 * nb; sizes[O_XQUAT] = 4 * nb; sizes[O_XIPOS] = 3 * nb; sizes[O_CINERT] = 10 * nb;
-    sizes[O_CRB] = 2 * S3_MAX_NV; sizes[O_CDOF] = 6 * nv; sizes[O_JANC] = 3 * nj; sizes[O_JAX] = 3 * nj; sizes[O_M] = np; sizes[O_LD] = np;
-    sizes[O_QPOS] = nq; sizes[O_QVEL] = nv; sizes[O_SMOOTH] = nv; sizes[O_A0] = nv; sizes[O_A] = nv;
+    sizes[O_CRB] = S3_MAX_NV; sizes[O_CDOF] = 6 * nv; sizes[O_JANC] = 3 * nj; sizes[O_JAX] = 3 * nj; sizes[O_M] = np; sizes[O_LD] = np;
+    sizes[O_QPOS] = nq; sizes[O_QVEL] = nv; sizes[O_SMOOTH] = nv; sizes[O_A0] = 0; sizes[O_A] = nv;
     sizes[O_MA] = nv; sizes[O_GRAD] = nv; sizes[O_P] = nv; sizes[O_MP] = nv; sizes[O_KVD] = nv;
-    sizes[O_GPOS] = 3 * ng; sizes[O_GMAT] = 9 * ng; sizes[O_CON] = kConStride * S3_MAX_CON;
-    int jc = 3 * S3_MAX_CON * m->chain_stride, rne = 6 * nv + 12 * nb;
-    sizes[O_JC] = jc > rne ? jc : rne; sizes[O_RAREF] = S3_MAX_ROWS; sizes[O_RD] = S3_MAX_ROWS;
-    sizes[O_RJAR] = S3_MAX_ROWS; sizes[O_RJP] = S3_MAX_ROWS; sizes[O_CDOT] = 3 * S3_MAX_CON; sizes[O_BIAS] = nv;
+    const int nc = m->ncon_max;  // per-model contact capacity (<= S3_MAX_CON)
+    const int nrow = (m->nlimjnt < S3_MAX_LIM ? m->nlimjnt : S3_MAX_LIM) + 4 * nc;
+    sizes[O_GPOS] = 0; sizes[O_GMAT] = 0; sizes[O_CON] = kConStride * nc;  // geom frames: computed on the fly
+    int jc = 3 * nc * m->chain_stride, rne = 6 * nv + 12 * nb;
+    sizes[O_JC] = jc > rne ? jc : rne; sizes[O_RAREF] = nrow; sizes[O_RD] = nrow;
+    sizes[O_RJAR] = nrow; sizes[O_RJP] = nrow; sizes[O_CDOT] = 3 * nc; sizes[O_BIAS] = 0;  // bias aliases Ma
     sizes[O_FCON] = nv; sizes[O_CTRL] = nu; sizes[O_COM] = 3 * S3_MAX_TREE;
     int region = sizes[O_XIPOS] + sizes[O_CINERT] + sizes[O_JANC] + sizes[O_JAX];
     if (region < m->ntree) sizes[O_JAX] += m->ntree - region;  // room for the factorization snapshot

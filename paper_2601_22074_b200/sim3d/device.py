@@ -218,6 +218,7 @@ class DeviceModel:
         s.solimp[:] = m.opt.solimp
         s.total_mass = float(m.body_mass[1:].sum())
         s.nkintree = m.ntree
+        s.ncon_max = m.ncon_max
         s.hf_spacing = m.hfield_spacing
         s.hf_origin[:] = m.hfield_origin
         s.hf_max = float(m.hfield_data.max())

@@ -93,9 +93,12 @@ class _Body:
 class ModelBuilder:
     """Tree builder: bodies must be added parent-first (topological order)."""
 
-    def __init__(self, name: str = "model", opt: Opt | None = None):
+    def __init__(self, name: str = "model", opt: Opt | None = None, ncon_max: int = MAX_CON):
         self.name = name
         self.opt = opt or Opt()
+        if not 1 <= ncon_max <= MAX_CON:
+            raise ModelError(f"ncon_max must be in [1, {MAX_CON}]")
+        self.ncon_max = int(ncon_max)  # contact capacity per world (MJWarp's nconmax analog)
         self.bodies: list[_Body] = [_Body("world", -1, np.zeros(3), np.array([1.0, 0, 0, 0]), 0.0, np.zeros(3),
                                           np.zeros(3), np.array([1.0, 0, 0, 0]))]
         self.joints: list[dict] = []
@@ -212,6 +215,7 @@ class Model:
     def __init__(self, b: ModelBuilder):
         self.name = b.name
         self.opt = b.opt
+        self.ncon_max = b.ncon_max
         nb = len(b.bodies)
         self.nbody = nb
         self.body_names = [x.name for x in b.bodies]
@@ -398,7 +402,7 @@ class Model:
         self.nlim = int(self.jnt_limited.sum())
         if self.nlim > MAX_LIM:
             raise ModelError(f"{self.nlim} limited joints exceed MAX_LIM={MAX_LIM}")
-        self.nefc_max = self.nlim + 4 * MAX_CON  # a limited hinge violates at most one side
+        self.nefc_max = self.nlim + 4 * self.ncon_max  # a limited hinge violates at most one side
         # set by set_const (inverse weights at qpos0; computed from M(qpos0) by whoever owns a dynamics engine)
         self.dof_invweight0 = np.ones(nv)
         self.body_invweight0 = np.zeros(nb)

@@ -68,7 +68,9 @@ def _terrain(b: ModelBuilder, rough, seed: int):
 def g1_like(rough: bool | str = False, seed: int = 0, actuator_kind: int = ACT_IMPLICIT, self_collision: bool = True,
             opt: Opt | None = None):
     """rough: False (plane), True (16 m seeded rough patch), "curriculum" (5 x 6 graded patches)."""
-    b = ModelBuilder("g1_like", opt)
+    # 12 contacts: 8 foot spheres standing plus knees/hands; a fallen humanoid (which terminates) may
+    # exceed it, later contacts are dropped in pair order and counted (ndropped)
+    b = ModelBuilder("g1_like", opt, ncon_max=12)
     _terrain(b, rough, seed)
     pelvis = b.body("pelvis", 0, pos=(0, 0, 0.793), mass=3.81, inertia=(0.010, 0.009, 0.008))
     b.free_joint(pelvis)

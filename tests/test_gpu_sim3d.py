@@ -219,8 +219,8 @@ def test_single_substep_f32(name):
 
 @pytest.mark.gpu
 def test_contact_capacity_drops_in_pair_order():
-    """A humanoid lying flat touches with more than MAX_CON points: the kernel keeps the first
-    MAX_CON in pair order and counts the rest, exactly like the oracle."""
+    """A humanoid lying flat touches with more than ncon_max points: the kernel keeps the first
+    ncon_max in pair order and counts the rest, exactly like the oracle."""
     import torch
 
     n = 2
@@ -236,7 +236,7 @@ def test_contact_capacity_drops_in_pair_order():
     torch.cuda.synchronize()
     for w in range(n):
         _, _, _, F = O.step(m, q[w], V[w], C[w], warm=np.zeros(m.nv))
-        assert int(out["ncon"][w]) == len(F["contacts"]) == MAX_CON
+        assert int(out["ncon"][w]) == len(F["contacts"]) == m.ncon_max
         assert int(out["ndropped"][w]) == F["dropped"] > 0
 
 
