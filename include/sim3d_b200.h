@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define S3_ABI_VERSION 15
+#define S3_ABI_VERSION 16
 #define S3_F64 0
 #define S3_F32 1
 
@@ -68,6 +68,8 @@ typedef struct s3_model {
     int32_t nkintree; /* kinematic trees (robot, free objects) */
     int32_t ncon_max; /* contact capacity per world (<= S3_MAX_CON); later contacts are dropped and counted */
     int32_t pad4;
+    uint64_t nonroot_mask; /* dofs with a parent dof */
+    uint64_t nonleaf_mask; /* dofs with a child dof */
     double timestep;
     double gravity[3];
     double tolerance;

@@ -469,10 +469,14 @@ __device__ __noinline__ void factor_ldl(const s3_model& m, T* A, T* rk, int lane
         __syncwarp();
         return;
     }
-    for (int k = m.nv - 1; k >= 0; --k) {
-        if (sel && (int)((U >> k) & 1ull) != (sel == 2)) continue;
-        int p0 = __ldg(m.ldl_ptr + k), p1 = __ldg(m.ldl_ptr + k + 1);
-        if (p0 == p1) continue;
+    // dofs with ancestors (dof_parentid >= 0 <=> nonempty update list), restricted to the selection,
+    // visited from the highest index down through the bit mask
+    const uint64_t all = m.nv == 64 ? ~0ull : ((1ull << m.nv) - 1);
+    uint64_t todo = (sel == 0 ? all : (sel == 1 ? (~U & all) : (U & all))) & m.nonroot_mask;
+    while (todo) {
+        const int k = 63 - __clzll((long long)todo);
+        todo &= ~(1ull << k);
+        const int p0 = __ldg(m.ldl_ptr + k), p1 = __ldg(m.ldl_ptr + k + 1);
         T rk = T(1) / A[tri(k, k)];
         int rkb = tri(k, 0);
         for (int t = p0 + lane; t < p1; t += 32) {
@@ -602,9 +606,11 @@ template <class T> __device__ __noinline__ void solve_ldl(const s3_model& m, con
         }
         return;
     }
-    for (int i = nv - 1; i >= 0; --i) {
-        int len = __ldg(m.dof_chainlen + i) - 1;
-        if (len <= 0) continue;
+    uint64_t todo = m.nonroot_mask;  // leaf-to-root: every dof with ancestors, highest index first
+    while (todo) {
+        const int i = 63 - __clzll((long long)todo);
+        todo &= ~(1ull << i);
+        const int len = __ldg(m.dof_chainlen + i) - 1;
         const uint8_t* ch = m.dof_chain + i * S3_MAX_CHAIN;
         T xi = x[i];
         int rb = tri(i, 0);
@@ -616,9 +622,11 @@ template <class T> __device__ __noinline__ void solve_ldl(const s3_model& m, con
     }
     for (int i = lane; i < nv; i += 32) x[i] = x[i] / A[tri(i, i)];
     __syncwarp();
-    for (int j = 0; j < nv; ++j) {
-        uint64_t dm = __ldg(reinterpret_cast<const unsigned long long*>(m.dof_descmask) + j);
-        if (!dm) continue;
+    uint64_t inner = m.nonleaf_mask;  // root-to-leaf: every dof with descendants, lowest index first
+    while (inner) {
+        const int j = __ffsll((long long)inner) - 1;
+        inner &= inner - 1;
+        const uint64_t dm = __ldg(reinterpret_cast<const unsigned long long*>(m.dof_descmask) + j);
         T xj = x[j];
         for (int i = lane; i < nv; i += 32)
             if ((dm >> i) & 1ull) x[i] -= A[tri(i, j)] * xj;

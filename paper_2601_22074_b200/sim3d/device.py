@@ -219,6 +219,8 @@ class DeviceModel:
         s.total_mass = float(m.body_mass[1:].sum())
         s.nkintree = m.ntree
         s.ncon_max = m.ncon_max
+        s.nonroot_mask = sum(1 << d for d in range(m.nv) if m.dof_parentid[d] >= 0)
+        s.nonleaf_mask = sum(1 << int(d) for d in set(m.dof_parentid.tolist()) if d >= 0)
         s.hf_spacing = m.hfield_spacing
         s.hf_origin[:] = m.hfield_origin
         s.hf_max = float(m.hfield_data.max())
