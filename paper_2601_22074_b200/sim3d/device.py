@@ -208,9 +208,10 @@ class DeviceModel:
         s.nldl_norm = len(ldl_norm)
         s.ntree = len(tree_ent)
         s.nhlev, s.ndlev = len(hlev), len(dlev)
-        # partial Newton refactorization: a measured win in float64 (latency-bound, 5-6 warps/SM) and a
-        # measured loss in float32 (12 warps/SM, issue-bound) -- tools/ab_sim3d.sh; S3_FLAGS overrides
-        s.flags = int(os.environ.get("S3_FLAGS", "1" if dtype == "f32" else "0"))
+        # bit 0 off: partial Newton refactorization (only the subtrees a constraint touches); bits 3 + 4: block
+        # phase sync at each substep and around the Newton solve -- measured defaults for both dtypes
+        # (tools/ab_sim3d.sh); S3_FLAGS overrides
+        s.flags = int(os.environ.get("S3_FLAGS", "24"))
         s.timestep = m.opt.timestep
         s.gravity[:] = m.opt.gravity
         s.tolerance, s.ls_tolerance = m.opt.tolerance, m.opt.ls_tolerance
@@ -229,7 +230,7 @@ class DeviceModel:
         self.struct = s
         self.set_scale()
         self.layout = N.LayoutT()
-        N.call("s3_plan", ctypes.byref(self.struct), 0, ctypes.byref(self.layout))
+        N.call("s3_plan", ctypes.byref(self.struct), int(os.environ.get("S3_WPB", "0")), ctypes.byref(self.layout))
 
     def set_scale(self):
         self.struct.scale = 1.0 / (self.model.meaninertia * max(1, self.model.nv))

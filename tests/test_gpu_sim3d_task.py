@@ -150,6 +150,32 @@ def test_world_offset_partition_independence():
     assert torch.equal(of, torch.cat([o0, o1])) and torch.equal(rf, torch.cat([r0, r1]))
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_block_phase_sync_is_bit_identical(dtype):
+    """The block barriers (flags bits 3, 4) only change when warps run: results are bit-identical with
+    and without them, including the partial last block (5000 worlds)."""
+    import torch
+
+    from paper_2601_22074_b200.sim3d.task import VelocityEnv3D
+
+    m = robots.g1_like(rough=True, seed=2)
+    cfg = VelocityTaskCfg(default_qpos=robots.default_qpos(m, robots.G1_DEFAULT_JOINTS), height_scan=True)
+    n = 5000
+    a = VelocityEnv3D(m, cfg, n, seed=5, dtype=dtype)
+    b = VelocityEnv3D(robots.g1_like(rough=True, seed=2), cfg, n, seed=5, dtype=dtype)
+    assert a.dm.struct.flags & 24 == 24
+    b.dm.struct.flags = a.dm.struct.flags & ~24
+    assert torch.equal(a.reset(), b.reset())
+    g = torch.Generator(device="cuda").manual_seed(0)
+    for _ in range(3):
+        act = (torch.rand(n, m.nu, device="cuda", generator=g) * 2 - 1).to(a.data.qpos.dtype)
+        oa, ra, ta, _ = a.step(act)
+        ob, rb, tb, _ = b.step(act)
+        assert torch.equal(oa, ob) and torch.equal(ra, rb) and torch.equal(ta, tb)
+    assert torch.equal(a.data.qpos, b.data.qpos) and torch.equal(a.data.qvel, b.data.qvel)
+
+
 def _motion_pair(n, dtype="f64", **over):
     from paper_2601_22074_b200.sim3d.motion import synthetic_walk_clip
     from paper_2601_22074_b200.sim3d.task import MotionTrackingCfg, VelocityEnv3D
