@@ -63,8 +63,8 @@ typedef struct s3_model {
     int32_t flags; /* bit 0: refactor every dof in each Newton iteration (A/B of the partial refactorization);
                       bit 1: tree-level schedule of the factorization / solves from CSR tables (measured
                       slower; kept for A/B); bit 2: tree-level schedule driven by per-lane dof bit masks;
-                      bit 3: block barrier at the start of each substep; bit 4: block barriers around the
-                      Newton solve (bits 3, 4: full blocks only; the default build sets 24) */
+                      bit 3: block barrier at the start of each substep; bit 4: before the Newton solve;
+                      bit 5: after it (bits 3-5: full blocks only; the Python layer defaults to 40) */
     int32_t nhlev;
     int32_t ndlev;
     int32_t nkintree; /* kinematic trees (robot, free objects) */

@@ -1467,11 +1467,11 @@ __device__ __noinline__ void substep(const s3_model& m, const s3_data& d, const 
     const int nv = m.nv;
     const T dt = T(m.timestep);
     int ncon = 0, nlim = 0, dropped = 0, its = 0;
-    // block phase sync (flags bits 3, 4; full blocks only): the warps of a block start every substep, and
-    // enter and leave the Newton solve, together, so they walk the same code and model tables at the same
-    // time -- the ~26 KB of L1 beside the workspace and the instruction cache then hold one stage's working
-    // set instead of every stage's (f32 G1 4.24 -> 3.04 ms, f64 6.65 -> 6.05 ms per control step)
-    const bool bsync = (m.flags & 24) && (int64_t)(blockIdx.x + 1) * L_.warps_per_block <= d.nworld;
+    // block phase sync (flags bits 3-5; full blocks only): the warps of a block start every substep and
+    // leave the Newton solve together, so they walk the same code and model tables at the same time -- the
+    // ~26 KB of L1 beside the workspace and the instruction cache then hold one stage's working set instead
+    // of every stage's (G1, 4096 worlds: f32 4.24 -> 2.98 ms, f64 6.65 -> 5.87 ms per control step)
+    const bool bsync = (m.flags & 56) && (int64_t)(blockIdx.x + 1) * L_.warps_per_block <= d.nworld;
     if (bsync && (m.flags & 8)) __syncthreads();
     kinematics(m, L_, B_, lane);
     com_pos(m, L_, B_, lane, d.mass_scale ? static_cast<const T*>(d.mass_scale)[w] : T(1));
@@ -1514,7 +1514,7 @@ __device__ __noinline__ void substep(const s3_model& m, const s3_data& d, const 
     if (gw) {
         for (int i = lane; i < nv; i += 32) gw[i] = s.a[i];
     }
-    if (bsync && (m.flags & 16)) __syncthreads();
+    if (bsync && (m.flags & 32)) __syncthreads();
     // implicitfast: (M + dt diag(damping + kv)) acc = smooth + constraint
     const T* damp = F<T>(m.dof_damping);
     tree_load(m, s.M, s.LD, lane);

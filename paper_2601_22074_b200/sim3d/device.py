@@ -208,10 +208,10 @@ class DeviceModel:
         s.nldl_norm = len(ldl_norm)
         s.ntree = len(tree_ent)
         s.nhlev, s.ndlev = len(hlev), len(dlev)
-        # bit 0 off: partial Newton refactorization (only the subtrees a constraint touches); bits 3 + 4: block
-        # phase sync at each substep and around the Newton solve -- measured defaults for both dtypes
+        # bit 0 off: partial Newton refactorization (only the subtrees a constraint touches); bits 3 + 5: block
+        # phase sync at the start of each substep and after the Newton solve -- measured defaults for both dtypes
         # (tools/ab_sim3d.sh); S3_FLAGS overrides
-        s.flags = int(os.environ.get("S3_FLAGS", "24"))
+        s.flags = int(os.environ.get("S3_FLAGS", "40"))
         s.timestep = m.opt.timestep
         s.gravity[:] = m.opt.gravity
         s.tolerance, s.ls_tolerance = m.opt.tolerance, m.opt.ls_tolerance

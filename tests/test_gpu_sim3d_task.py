@@ -153,7 +153,7 @@ def test_world_offset_partition_independence():
 @pytest.mark.gpu
 @pytest.mark.parametrize("dtype", ["f32", "f64"])
 def test_block_phase_sync_is_bit_identical(dtype):
-    """The block barriers (flags bits 3, 4) only change when warps run: results are bit-identical with
+    """The block barriers (flags bits 3-5) only change when warps run: results are bit-identical with
     and without them, including the partial last block (5000 worlds)."""
     import torch
 
@@ -164,8 +164,8 @@ def test_block_phase_sync_is_bit_identical(dtype):
     n = 5000
     a = VelocityEnv3D(m, cfg, n, seed=5, dtype=dtype)
     b = VelocityEnv3D(robots.g1_like(rough=True, seed=2), cfg, n, seed=5, dtype=dtype)
-    assert a.dm.struct.flags & 24 == 24
-    b.dm.struct.flags = a.dm.struct.flags & ~24
+    assert a.dm.struct.flags & 40 == 40
+    b.dm.struct.flags = a.dm.struct.flags & ~56
     assert torch.equal(a.reset(), b.reset())
     g = torch.Generator(device="cuda").manual_seed(0)
     for _ in range(3):
