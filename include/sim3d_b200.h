@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define S3_ABI_VERSION 16
+#define S3_ABI_VERSION 17
 #define S3_F64 0
 #define S3_F32 1
 
@@ -288,6 +288,12 @@ typedef struct s3_task {
     void* reward;
     uint8_t* terminated;
     uint8_t* truncated;
+    /* optional cost-ordered scheduling (both or neither): the step writes each world's solver cost (Newton
+     * iterations summed over its substeps) to cost[N]; the next step first sorts the worlds by it (heaviest
+     * first) into order[N] and block b's warps take worlds order[b * warps_per_block + i], so each block's
+     * worlds need similar solver work and the block's barriers wait less. Results do not depend on it. */
+    int32_t* cost;
+    int32_t* order;
 } s3_task;
 
 int s3_abi_version(void);

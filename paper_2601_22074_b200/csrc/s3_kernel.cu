@@ -1461,7 +1461,7 @@ template <class T> __device__ int __noinline__ newton(const s3_model& m, const s
 // ---------------------------------------------------------------- one physics substep (mj_step)
 
 template <class T>
-__device__ __noinline__ void substep(const s3_model& m, const s3_data& d, const s3_layout& L_, T* B_, int64_t w, T* gw, const T* gapp, bool last,
+__device__ __noinline__ int substep(const s3_model& m, const s3_data& d, const s3_layout& L_, T* B_, int64_t w, T* gw, const T* gapp, bool last,
                         int lane) {
     WS<T> s = make_ws(B_, L_);
     const int nv = m.nv;
@@ -1580,6 +1580,7 @@ __device__ __noinline__ void substep(const s3_model& m, const s3_data& d, const 
     }
     __syncwarp();
     if (d.time && lane == 0) static_cast<T*>(d.time)[w] += dt;
+    return its;
 }
 
 template <class T> __device__ __noinline__ void store_geom_frames(const s3_model& m, const s3_data& d, const s3_layout& L_, T* B_, int64_t w,
@@ -2068,6 +2069,7 @@ __global__ void __launch_bounds__(32 * 16) env_kernel(const __grid_constant__ s3
     int wib = threadIdx.x >> 5;
     int64_t w = (int64_t)blockIdx.x * l.warps_per_block + wib;
     if (w >= d.nworld) return;
+    if (tk.order && mode == 0) w = tk.order[w];  // cost-ordered schedule (s3_task.order; sorted before each step)
     T* base = reinterpret_cast<T*>(smem_raw) + (size_t)wib * l.elems_per_world;
     WS<T> s = make_ws(base, l);
     const s3_layout& L_ = l;
@@ -2135,7 +2137,9 @@ __global__ void __launch_bounds__(32 * 16) env_kernel(const __grid_constant__ s3
     }
     rate = wsum(rate);
     __syncwarp();
-    for (int sub = 0; sub < tk.decimation; ++sub) substep(m, d, L_, B_, w, gw, (const T*)nullptr, false, lane);
+    int cost = 0;
+    for (int sub = 0; sub < tk.decimation; ++sub) cost += substep(m, d, L_, B_, w, gw, (const T*)nullptr, false, lane);
+    if (tk.cost && lane == 0) tk.cost[w] = cost;
     if (tk.kind == 1) {
         motion_post(m, tk, L_, B_, w, ctr, cmd, act, rate, gq, gv, gw, prev, lane);
         return;
@@ -2230,6 +2234,35 @@ __global__ void __launch_bounds__(32 * 16) env_kernel(const __grid_constant__ s3
     if (d.geom_xpos) store_geom_frames(m, d, L_, B_, w, lane);  // sensors see the post-reset state, like obs
     for (int i = lane; i < nq; i += 32) gq[i] = s.qpos[i];
     for (int i = lane; i < nv; i += 32) gv[i] = s.qvel[i];
+}
+
+// cost-ordered schedule: counting sort of the worlds by their last solver cost, heaviest first, so the
+// warps of one block get worlds of similar Newton work (one block; order within a cost bucket is arbitrary
+// and does not affect results -- every world is computed independently)
+constexpr int kCostBuckets = 64;
+__global__ void __launch_bounds__(1024) order_kernel(const int32_t* __restrict__ cost, int32_t* __restrict__ order,
+                                                      int64_t n) {
+    __shared__ int hist[kCostBuckets];
+    for (int b = threadIdx.x; b < kCostBuckets; b += blockDim.x) hist[b] = 0;
+    __syncthreads();
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const int c = cost[i];
+        atomicAdd(&hist[c < 0 ? 0 : (c >= kCostBuckets ? kCostBuckets - 1 : c)], 1);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int acc = 0;
+        for (int b = kCostBuckets - 1; b >= 0; --b) {
+            const int h = hist[b];
+            hist[b] = acc;
+            acc += h;
+        }
+    }
+    __syncthreads();
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const int c = cost[i];
+        order[atomicAdd(&hist[c < 0 ? 0 : (c >= kCostBuckets ? kCostBuckets - 1 : c)], 1)] = (int32_t)i;
+    }
 }
 
 // ---------------------------------------------------------------- ray casting (oracle raycast)
@@ -2503,11 +2536,16 @@ int s3_env_step(const s3_model* m, const s3_data* d, const s3_layout* l, const s
         (t->kind == 1 && (t->nframes < 2 || !t->motion_qpos || !t->motion_qvel || m->nq + m->nv > m->nv * (m->nv + 1) / 2)))
         return fail(S3_ERR_ARG, "task layout does not match the model");
     if (d->qM) return fail(S3_ERR_ARG, "parity outputs are not written by s3_env_step");
+    if ((t->cost == nullptr) != (t->order == nullptr)) return fail(S3_ERR_ARG, "cost and order go together");
+    if (t->order && d->nworld > INT32_MAX) return fail(S3_ERR_BOUNDS, "cost-ordered schedule needs < 2^31 worlds");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     int wpb = l->warps_per_block;
     unsigned grid = (unsigned)((d->nworld + wpb - 1) / wpb);
     size_t smem = (size_t)l->bytes_per_block;
     cudaError_t e;
+    if (t->order && mode == 0) {  // sort by the previous step's solver cost (reset launches keep the order)
+        order_kernel<<<1, 1024, 0, st>>>(t->cost, t->order, d->nworld);
+    }
     if (m->dtype == S3_F64) {
         e = cudaFuncSetAttribute(env_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e == cudaSuccess)

@@ -20,6 +20,7 @@ return device tensors (obs (N, D), reward (N,), terminated (N,), truncated
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -260,6 +261,12 @@ class VelocityEnv3D:
         for name in ("action", "prev_action", "command", "cmd_timer", "episode_step", "episode_return", "obs",
                      "reward", "terminated", "truncated"):
             setattr(t, name, getattr(self, name).data_ptr())
+        # cost-ordered schedule (s3_task.cost / order): worlds sorted by their last solver cost before each step
+        self.solver_cost = self.world_order = None
+        if os.environ.get("S3_ORDER", "1") != "0":
+            self.solver_cost = torch.zeros(n, dtype=torch.int32, device=dev)
+            self.world_order = torch.zeros(n, dtype=torch.int32, device=dev)
+            t.cost, t.order = self.solver_cost.data_ptr(), self.world_order.data_ptr()
         self.task = t
         self._actions_in = z(n, nu)
 
@@ -269,6 +276,8 @@ class VelocityEnv3D:
         st = torch.cuda.current_stream(self.dm.device).cuda_stream
         N.call("s3_env_step", ctypes.byref(self.dm.struct), ctypes.byref(d), ctypes.byref(self.dm.layout),
                ctypes.byref(self.task), ptr, int(mode), int(self.global_step), st, launch=True)
+        if mode == 0 and self.world_order is not None:
+            N.LAUNCHES["count"] += 1  # the cost sort (order_kernel) launched ahead of the step kernel
 
     def metrics_record(self, step: int, group=None, steps_per_sec=None):
         """Job-wide statistics of the last step (metrics.py record): reward mean, running episode return,

@@ -176,6 +176,43 @@ def test_block_phase_sync_is_bit_identical(dtype):
     assert torch.equal(a.data.qpos, b.data.qpos) and torch.equal(a.data.qvel, b.data.qvel)
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_cost_ordered_schedule_is_bit_identical(dtype, monkeypatch):
+    """Sorting the worlds by their last solver cost before each step (s3_task.cost / order) only changes
+    which warp steps which world: results are bit-identical to the identity schedule, and the order is a
+    permutation sorted by cost (heaviest first)."""
+    import torch
+
+    from paper_2601_22074_b200.sim3d.task import VelocityEnv3D
+
+    m = robots.g1_like(rough=True, seed=2)
+    cfg = VelocityTaskCfg(default_qpos=robots.default_qpos(m, robots.G1_DEFAULT_JOINTS), height_scan=True)
+    n = 5000
+    a = VelocityEnv3D(m, cfg, n, seed=5, dtype=dtype)
+    monkeypatch.setenv("S3_ORDER", "0")
+    b = VelocityEnv3D(robots.g1_like(rough=True, seed=2), cfg, n, seed=5, dtype=dtype)
+    assert a.world_order is not None and b.world_order is None
+    assert torch.equal(a.reset(), b.reset())
+    g = torch.Generator(device="cuda").manual_seed(0)
+    for _ in range(4):
+        act = (torch.rand(n, m.nu, device="cuda", generator=g) * 2 - 1).to(a.data.qpos.dtype)
+        oa, ra, ta, _ = a.step(act)
+        ob, rb, tb, _ = b.step(act)
+        assert torch.equal(oa, ob) and torch.equal(ra, rb) and torch.equal(ta, tb)
+    assert torch.equal(a.data.qpos, b.data.qpos) and torch.equal(a.data.qvel, b.data.qvel)
+    order = a.world_order.long()
+    assert torch.equal(order.sort().values, torch.arange(n, device="cuda"))
+    assert int(a.solver_cost.min()) >= 0 and int(a.solver_cost.max()) > 0
+    # the order the last step used was sorted by the costs of the step before it: re-sorting the current
+    # costs must give non-increasing costs along the order the NEXT step will use
+    a.step(act)
+    prev = a.solver_cost.long().clamp(max=63)  # the sort's buckets
+    a._launch(0, act)  # one more step: its order kernel sorted by `prev`
+    used = a.world_order.long()
+    assert bool((prev[used][1:] <= prev[used][:-1]).all())
+
+
 def _motion_pair(n, dtype="f64", **over):
     from paper_2601_22074_b200.sim3d.motion import synthetic_walk_clip
     from paper_2601_22074_b200.sim3d.task import MotionTrackingCfg, VelocityEnv3D
