@@ -302,7 +302,7 @@ def sim3d_leg(args, flush, stream) -> dict:
         t = timed_steps(env, steps, flush, stream, lambda i: acts[5 + i])
         launches = native3.LAUNCHES["count"] - l0
         out[dtype] = {"value": n * steps / t, "ms_per_step": 1e3 * t / steps, "gpu_launches": launches,
-                      "warps_per_block": env.dm.layout.warps_per_block,
+                      "warps_per_block_max": env.dm.layout.warps_per_block,
                       "smem_bytes_per_world": env.dm.layout.elems_per_world * (4 if dtype == "f32" else 8),
                       "terminated_frac_last": float(env.terminated.float().mean().item())}
         del env

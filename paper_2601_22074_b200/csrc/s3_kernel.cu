@@ -35,7 +35,8 @@ constexpr int kConStride = 14;  // dist, pos[3], frame[9], mu
 enum {
     O_XPOS, O_XQUAT, O_XIPOS, O_CINERT, O_JANC, O_JAX, O_CRB, O_CDOF, O_CDOFD, O_CVEL, O_CACC,
     O_M, O_LD, O_QPOS, O_QVEL, O_SMOOTH, O_A0, O_A, O_MA, O_GRAD, O_P, O_MP, O_KVD, O_GPOS, O_GMAT,
-    O_CON, O_JC, O_RAREF, O_RD, O_RJAR, O_RJP, O_CDOT, O_BIAS, O_FCON, O_CTRL, O_COM, O_INT, O_END
+    O_CON, O_JC, O_RAREF, O_RD, O_RJAR, O_RJP, O_CDOT, O_BIAS, O_FCON, O_CTRL, O_COM, O_INT, O_END,
+    O_INT_LIMDOF = O_END, O_INT_LIMSIGN  // int offsets inside O_INT (not element offsets)
 };
 
 __host__ __device__ inline int tri(int i, int j) { return ((i * (i + 1)) >> 1) + j; }  // packed lower, i >= j
@@ -147,7 +148,7 @@ template <class T> struct WS {
     T *xpos, *xquat, *xipos, *cinert, *crb, *cdof, *cdofd, *cvel, *cacc, *janc, *jax, *M, *LD, *qpos, *qvel,
         *smooth, *a0, *a, *Ma, *grad, *p, *Mp, *kvd, *con, *Jc, *raref, *rD, *rjar, *rJp, *cdot,
         *bias, *fcon, *ctrl, *com, *tk, *u, *snap;
-    int *con_pair, *lim_dof, *lim_sign, *misc;
+    int *con_pair, *lim_dof, *lim_sign;
 };
 
 template <class T> __device__ inline WS<T> make_ws(T* base, const s3_layout& l) {
@@ -173,9 +174,8 @@ template <class T> __device__ inline WS<T> make_ws(T* base, const s3_layout& l) 
     s.com = base + o[O_COM];
     int* ib = reinterpret_cast<int*>(base + o[O_INT]);
     s.con_pair = ib;
-    s.lim_dof = ib + S3_MAX_CON;
-    s.lim_sign = ib + S3_MAX_CON + S3_MAX_LIM;
-    s.misc = ib + S3_MAX_CON + 2 * S3_MAX_LIM;
+    s.lim_dof = ib + o[O_INT_LIMDOF];  // int offsets inside the int region, sized by ncon_max / nlimjnt
+    s.lim_sign = ib + o[O_INT_LIMSIGN];
     return s;
 }
 
@@ -1504,6 +1504,11 @@ __device__ __noinline__ int substep(const s3_model& m, const s3_data& d, const s
             static_cast<T*>(d.qacc_smooth)[w * nv + i] = s.a0[i];
         }
     }
+    if (last && d.qM) {  // parity output; the constraint-force row buffer may reuse cdof's slot from here on
+        for (int i = lane; i < nv; i += 32)
+            for (int k = 0; k < 6; ++k) static_cast<T*>(d.cdof)[(w * nv + i) * 6 + k] = s.cdof[6 * i + k];
+        __syncwarp();
+    }
     build_rows(m, L_, B_, ncon, nlim, lane);
     if (bsync && (m.flags & 16)) __syncthreads();
     if (gw) {
@@ -1528,7 +1533,6 @@ __device__ __noinline__ int substep(const s3_model& m, const s3_data& d, const s
             static_cast<T*>(d.qfrc_smooth)[w * nv + i] = s.smooth[i];
             static_cast<T*>(d.qacc)[w * nv + i] = s.a[i];
             static_cast<T*>(d.qfrc_constraint)[w * nv + i] = s.fcon[i];
-            for (int k = 0; k < 6; ++k) static_cast<T*>(d.cdof)[(w * nv + i) * 6 + k] = s.cdof[6 * i + k];
         }
         for (int b = lane; b < m.nbody; b += 32) {
             for (int k = 0; k < 3; ++k) static_cast<T*>(d.xpos)[(w * m.nbody + b) * 3 + k] = s.xpos[3 * b + k];
@@ -2493,17 +2497,39 @@ int s3_plan(const s3_model* m, int32_t warps_per_block, s3_layout* out) {
     int jc = 3 * nc * m->chain_stride, rne = 6 * nv + 12 * nb;
     sizes[O_JC] = jc > rne ? jc : rne; sizes[O_RAREF] = nrow; sizes[O_RD] = nrow;
     sizes[O_RJAR] = nrow; sizes[O_RJP] = nrow; sizes[O_CDOT] = 3 * nc; sizes[O_BIAS] = 0;  // bias aliases Ma
-    sizes[O_FCON] = nv; sizes[O_CTRL] = nu; sizes[O_COM] = 3 * S3_MAX_TREE;
+    sizes[O_FCON] = nv; sizes[O_CTRL] = nu; sizes[O_COM] = 3 * (m->nkintree > 0 ? m->nkintree : 1);
+    // the per-dof reciprocal scratch (tk, in the O_CRB slot) is used by the level-schedule variants only
+    if (!(m->flags & 6)) sizes[O_CRB] = 0;
     int region = sizes[O_XIPOS] + sizes[O_CINERT] + sizes[O_JANC] + sizes[O_JAX];
     if (region < m->ntree) sizes[O_JAX] += m->ntree - region;  // room for the factorization snapshot
+    // row buffers are live from build_rows to the end of Newton only: aref / D / J·a go after the factorization
+    // snapshot in the xipos .. jax region and the force / J·p buffer into cdof's slot (cdof is last read by
+    // build_rows; its parity copy is written before) -- each when the host slot is large enough
+    auto ev = [](int x) { return (x + 1) & ~1; };
+    const int nre = ev(nrow);
+    const int snap_region = ev(sizes[O_XIPOS]) + ev(sizes[O_CINERT]) + ev(sizes[O_JANC]) + ev(sizes[O_JAX]);
+    const bool rows_in_snap = ev(m->ntree) + 3 * nre <= snap_region;
+    const bool jp_in_cdof = 6 * nv >= nrow;
+    if (rows_in_snap) sizes[O_RAREF] = sizes[O_RD] = sizes[O_RJAR] = 0;
+    if (jp_in_cdof) sizes[O_RJP] = 0;
     int esz = m->dtype == S3_F64 ? 8 : 4;
-    int ints = S3_MAX_CON + 2 * S3_MAX_LIM + 8;
+    const int nlim_cap = m->nlimjnt < S3_MAX_LIM ? m->nlimjnt : S3_MAX_LIM;
+    int ints = nc + 2 * nlim_cap;  // con_pair, lim_dof, lim_sign
     sizes[O_INT] = (ints * 4 + esz - 1) / esz;
     int off = 0;
     for (int k = 0; k < O_END; ++k) {
         out->off[k] = off;
         off += (sizes[k] + 1) & ~1;  // keep 8-byte alignment for the float build's int region
     }
+    if (rows_in_snap) {
+        const int t = out->off[O_XIPOS] + ev(m->ntree);
+        out->off[O_RAREF] = t;
+        out->off[O_RD] = t + nre;
+        out->off[O_RJAR] = t + 2 * nre;
+    }
+    if (jp_in_cdof) out->off[O_RJP] = out->off[O_CDOF];
+    out->off[O_INT_LIMDOF] = nc;
+    out->off[O_INT_LIMSIGN] = nc + nlim_cap;
     out->off[O_CDOFD] = 6 * nv;  // RNE scratch offsets relative to the Jacobian region
     out->off[O_CVEL] = 6 * nb;
     out->off[O_CACC] = 0;
@@ -2522,6 +2548,40 @@ int s3_plan(const s3_model* m, int32_t warps_per_block, s3_layout* out) {
     return S3_OK;
 }
 
+// Launch layout: the planned (maximal) warps per block packs the most worlds per SM; when all worlds fit
+// in one partial wave, smaller blocks spread them over every SM instead (G1 f32, 1024 worlds: 147 blocks of
+// 7 warps instead of 64 blocks of 16, 1.62 -> 1.50 ms). Over several waves, flags bit 6 also balances the
+// waves (same wave count, fewer warps per block): a win for latency-bound models (G1 f32 at 4096 worlds:
+// 2 waves of 14 instead of 16, 3.03 -> 2.98 ms) and a loss for light ones (arm: +6 %), so the Python layer
+// sets it by model size.
+extern "C++" s3_layout balanced_layout(const s3_layout& l, int64_t nworld, int flags) {
+    static int dev_c = -1, nsm = 0, smem_sm = 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev != dev_c) {
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+        dev_c = dev;
+    }
+    s3_layout o = l;
+    const int wmax = l.warps_per_block;
+    if (nsm <= 0 || wmax <= 1 || nworld <= 0) return o;
+    const int per_world = l.bytes_per_block / wmax;
+    int per_sm = 16 / wmax;  // 128 registers per thread: at most 16 resident warps per SM
+    const int by_smem = smem_sm > 0 ? smem_sm / l.bytes_per_block : 1;
+    if (by_smem < per_sm) per_sm = by_smem;
+    if (per_sm < 1) per_sm = 1;
+    const int64_t slots = (int64_t)nsm * per_sm;  // resident blocks
+    if (nworld > slots * wmax && !(flags & 64)) return o;  // several waves: keep the maximal block
+    const int64_t waves = (nworld + slots * wmax - 1) / (slots * wmax);
+    int64_t w = (nworld + slots * waves - 1) / (slots * waves);
+    if (w < 1) w = 1;
+    if (w > wmax) w = wmax;
+    o.warps_per_block = (int32_t)w;
+    o.bytes_per_block = (int32_t)(w * per_world);
+    return o;
+}
+
 int s3_env_step(const s3_model* m, const s3_data* d, const s3_layout* l, const s3_task* t, const void* actions,
                 int32_t mode, int64_t global_step, void* stream) {
     using namespace s3;
@@ -2537,11 +2597,14 @@ int s3_env_step(const s3_model* m, const s3_data* d, const s3_layout* l, const s
         return fail(S3_ERR_ARG, "task layout does not match the model");
     if (d->qM) return fail(S3_ERR_ARG, "parity outputs are not written by s3_env_step");
     if ((t->cost == nullptr) != (t->order == nullptr)) return fail(S3_ERR_ARG, "cost and order go together");
+    if ((m->flags & 6) && l->off[O_CDOF] - l->off[O_CRB] < m->nv)
+        return fail(S3_ERR_ARG, "layout planned without the level-schedule scratch (flags bits 1-2): re-plan");
     if (t->order && d->nworld > INT32_MAX) return fail(S3_ERR_BOUNDS, "cost-ordered schedule needs < 2^31 worlds");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    int wpb = l->warps_per_block;
+    const s3_layout ll = balanced_layout(*l, d->nworld, m->flags);
+    int wpb = ll.warps_per_block;
     unsigned grid = (unsigned)((d->nworld + wpb - 1) / wpb);
-    size_t smem = (size_t)l->bytes_per_block;
+    size_t smem = (size_t)ll.bytes_per_block;
     cudaError_t e;
     if (t->order && mode == 0) {  // sort by the previous step's solver cost (reset launches keep the order)
         order_kernel<<<1, 1024, 0, st>>>(t->cost, t->order, d->nworld);
@@ -2549,12 +2612,12 @@ int s3_env_step(const s3_model* m, const s3_data* d, const s3_layout* l, const s
     if (m->dtype == S3_F64) {
         e = cudaFuncSetAttribute(env_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e == cudaSuccess)
-            env_kernel<double><<<grid, 32 * wpb, smem, st>>>(*m, *d, *l, *t, static_cast<const double*>(actions), mode,
+            env_kernel<double><<<grid, 32 * wpb, smem, st>>>(*m, *d, ll, *t, static_cast<const double*>(actions), mode,
                                                               global_step);
     } else {
         e = cudaFuncSetAttribute(env_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e == cudaSuccess)
-            env_kernel<float><<<grid, 32 * wpb, smem, st>>>(*m, *d, *l, *t, static_cast<const float*>(actions), mode,
+            env_kernel<float><<<grid, 32 * wpb, smem, st>>>(*m, *d, ll, *t, static_cast<const float*>(actions), mode,
                                                              global_step);
     }
     if (e == cudaSuccess) e = cudaGetLastError();
@@ -2572,17 +2635,20 @@ int s3_step(const s3_model* m, const s3_data* d, const s3_layout* l, int32_t nsu
                   !d->con_pair || !d->con_dist || !d->con_pos || !d->con_frame || !d->efc_force || !d->solver_niter))
         return fail(S3_ERR_ARG, "qM set: every parity output is required");
     if (d->geom_xpos && !d->geom_xmat) return fail(S3_ERR_ARG, "geom_xmat required with geom_xpos");
+    if ((m->flags & 6) && l->off[O_CDOF] - l->off[O_CRB] < m->nv)
+        return fail(S3_ERR_ARG, "layout planned without the level-schedule scratch (flags bits 1-2): re-plan");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    int wpb = l->warps_per_block;
+    const s3_layout ll = balanced_layout(*l, d->nworld, m->flags);
+    int wpb = ll.warps_per_block;
     unsigned grid = (unsigned)((d->nworld + wpb - 1) / wpb);
-    size_t smem = (size_t)l->bytes_per_block;
+    size_t smem = (size_t)ll.bytes_per_block;
     cudaError_t e;
     if (m->dtype == S3_F64) {
         e = cudaFuncSetAttribute(step_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e == cudaSuccess) step_kernel<double><<<grid, 32 * wpb, smem, st>>>(*m, *d, *l, nsub);
+        if (e == cudaSuccess) step_kernel<double><<<grid, 32 * wpb, smem, st>>>(*m, *d, ll, nsub);
     } else {
         e = cudaFuncSetAttribute(step_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e == cudaSuccess) step_kernel<float><<<grid, 32 * wpb, smem, st>>>(*m, *d, *l, nsub);
+        if (e == cudaSuccess) step_kernel<float><<<grid, 32 * wpb, smem, st>>>(*m, *d, ll, nsub);
     }
     if (e == cudaSuccess) e = cudaGetLastError();
     if (e != cudaSuccess) return fail(S3_ERR_CUDA, cudaGetErrorString(e));

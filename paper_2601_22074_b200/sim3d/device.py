@@ -209,9 +209,10 @@ class DeviceModel:
         s.ntree = len(tree_ent)
         s.nhlev, s.ndlev = len(hlev), len(dlev)
         # bit 0 off: partial Newton refactorization (only the subtrees a constraint touches); bits 3 + 5: block
-        # phase sync at the start of each substep and after the Newton solve -- measured defaults for both dtypes
+        # phase sync at the start of each substep and after the Newton solve; bit 6 (latency-bound, large models):
+        # balance warps per block over the waves of a launch -- measured defaults for both dtypes
         # (tools/ab_sim3d.sh); S3_FLAGS overrides
-        s.flags = int(os.environ.get("S3_FLAGS", "40"))
+        s.flags = int(os.environ.get("S3_FLAGS", "40" if m.nv < 24 else "104"))  # bit 6: balanced waves
         s.timestep = m.opt.timestep
         s.gravity[:] = m.opt.gravity
         s.tolerance, s.ls_tolerance = m.opt.tolerance, m.opt.ls_tolerance

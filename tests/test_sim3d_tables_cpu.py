@@ -151,7 +151,20 @@ def test_layout_fits_and_struct_sizes():
             dm = DeviceModel(make(), dtype, device="cpu")
             lay = dm.layout
             assert lay.bytes_per_block == lay.elems_per_world * esz * lay.warps_per_block <= 227 * 1024
-            # O_XPOS .. O_INT: the per-world regions, in order (8-10 hold RNE offsets inside the Jacobian region)
-            offs = [lay.off[k] for k in range(37) if k not in (8, 9, 10)]
+            # O_XPOS .. O_INT: the per-world regions, in order (8-10 hold RNE offsets inside the Jacobian region;
+            # the row buffers 27-30 may reuse dead slots: aref / D / J·a after the factorization snapshot in the
+            # xipos .. jax region, the force buffer in cdof's slot)
+            offs = [lay.off[k] for k in range(37) if k not in (8, 9, 10, 27, 28, 29, 30)]
             assert offs == sorted(offs) and offs[-1] < lay.elems_per_world
+            dm_s = dm.struct
+            nrow = min(dm_s.nlimjnt, 32) + 4 * dm_s.ncon_max
+            nre = (nrow + 1) & ~1
+            raref, rd, rjar, rjp = (lay.off[k] for k in (27, 28, 29, 30))
+            assert rd - raref >= nrow and rjar - rd >= nrow
+            if raref < lay.off[6]:  # in the snapshot region, after the ntree snapshot entries
+                assert raref >= lay.off[2] + dm_s.ntree and rjar + nre <= lay.off[6]
+            if rjp == lay.off[7]:  # in cdof's slot
+                assert 6 * dm_s.nv >= nrow
+            # int region: con_pair, lim_dof, lim_sign (int offsets)
+            assert lay.off[37] == dm_s.ncon_max and lay.off[38] == dm_s.ncon_max + min(dm_s.nlimjnt, 32)
     assert N.lib().s3_sizeof(3) == ctypes.sizeof(N.TaskT)
