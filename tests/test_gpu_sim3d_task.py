@@ -306,6 +306,28 @@ def test_cube_lift_free_running_f64():
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("task", ["motion", "lift"])
+def test_f32_motion_and_lift_close_to_oracle(task):
+    """float32 builds of BASELINE configs[2] / [3] (partial Newton refactorization, phase sync, cost order):
+    one control step from the oracle's reset within float32 tolerances; flags exact."""
+    import torch
+
+    n = 8
+    env, ref = (_motion_pair if task == "motion" else _lift_pair)(n, dtype="f32")
+    o = env.reset().double().cpu().numpy()
+    o_ref = ref.reset()
+    np.testing.assert_allclose(o, o_ref, atol=1e-5 * max(1.0, np.abs(o_ref).max()))
+    a = np.random.default_rng(3).uniform(-1, 1, size=(n, env.model.nu)).astype(np.float32)
+    o, r, te, tr = env.step(torch.as_tensor(a, device="cuda"))
+    o_ref, r_ref, te_ref, tr_ref = ref.step(a.astype(np.float64))
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(te.cpu().numpy().astype(bool), te_ref)
+    np.testing.assert_array_equal(tr.cpu().numpy().astype(bool), tr_ref)
+    np.testing.assert_allclose(r.double().cpu().numpy(), r_ref, atol=1e-4 * max(1.0, np.abs(r_ref).max()))
+    np.testing.assert_allclose(o.double().cpu().numpy(), o_ref, atol=5e-3 * max(1.0, np.abs(o_ref).max()))
+
+
+@pytest.mark.gpu
 def test_cube_lift_teacher_forced_lift_termination_and_truncation():
     import torch
 
