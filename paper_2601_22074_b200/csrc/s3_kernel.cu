@@ -606,32 +606,48 @@ template <class T> __device__ __noinline__ void solve_ldl(const s3_model& m, con
         }
         return;
     }
-    uint64_t todo = m.nonroot_mask;  // leaf-to-root: every dof with ancestors, highest index first
-    while (todo) {
-        const int i = 63 - __clzll((long long)todo);
-        todo &= ~(1ull << i);
-        const int len = __ldg(m.dof_chainlen + i) - 1;
-        const uint8_t* ch = m.dof_chain + i * S3_MAX_CHAIN;
-        T xi = x[i];
-        int rb = tri(i, 0);
-        for (int a = lane; a < len; a += 32) {
-            int j = __ldg(ch + a);
-            x[j] -= A[rb + j] * xi;
-        }
-        __syncwarp();
+    // register sweeps: lane l holds x[l] and x[l + 32]; step k broadcasts the (final) x[k] with a shuffle and
+    // every lane applies its own update, so the serial chain per dof is shuffle -> FMA instead of a shared
+    // memory store / barrier / load round trip; the factor entries and masks do not depend on x and are
+    // loaded ahead. Same operations in the same order per entry as the reference sweeps (bit-identical).
+    const unsigned long long* cm = reinterpret_cast<const unsigned long long*>(m.dof_chainmask);
+    const unsigned long long* dmk = reinterpret_cast<const unsigned long long*>(m.dof_descmask);
+    const int i0 = lane, i1 = lane + 32;
+    const bool two = nv > 32;
+    T x0 = i0 < nv ? x[i0] : T(0);
+    T x1 = (two && i1 < nv) ? x[i1] : T(0);
+    // leaf-to-root: x[j] -= L[i][j] x[i] over the ancestors j of i, i from the highest index down
+#pragma unroll 4
+    for (int i = nv - 1; i >= 1; --i) {
+        const uint64_t anc = __ldg(cm + i) & ~(1ull << i);
+        const int rb = tri(i, 0);
+        const bool u0 = (anc >> i0) & 1ull, u1 = two && ((anc >> i1) & 1ull);
+        const T a0 = u0 ? A[rb + i0] : T(0);
+        const T a1 = u1 ? A[rb + i1] : T(0);
+        const T s0 = __shfl_sync(FULL, x0, i & 31);
+        const T s1 = two ? __shfl_sync(FULL, x1, i & 31) : T(0);
+        const T xi = i < 32 ? s0 : s1;
+        if (u0) x0 -= a0 * xi;
+        if (u1) x1 -= a1 * xi;
     }
-    for (int i = lane; i < nv; i += 32) x[i] = x[i] / A[tri(i, i)];
+    if (i0 < nv) x0 = x0 / A[tri(i0, i0)];
+    if (two && i1 < nv) x1 = x1 / A[tri(i1, i1)];
+    // root-to-leaf: x[i] -= L[i][j] x[j] over the descendants i of j, j from the lowest index up
+#pragma unroll 4
+    for (int j = 0; j < nv - 1; ++j) {
+        const uint64_t dm = __ldg(dmk + j);
+        const bool u0 = (dm >> i0) & 1ull, u1 = two && ((dm >> i1) & 1ull);
+        const T a0 = u0 ? A[tri(i0, j)] : T(0);
+        const T a1 = u1 ? A[tri(i1, j)] : T(0);
+        const T s0 = __shfl_sync(FULL, x0, j & 31);
+        const T s1 = two ? __shfl_sync(FULL, x1, j & 31) : T(0);
+        const T xj = j < 32 ? s0 : s1;
+        if (u0) x0 -= a0 * xj;
+        if (u1) x1 -= a1 * xj;
+    }
+    if (i0 < nv) x[i0] = x0;
+    if (two && i1 < nv) x[i1] = x1;
     __syncwarp();
-    uint64_t inner = m.nonleaf_mask;  // root-to-leaf: every dof with descendants, lowest index first
-    while (inner) {
-        const int j = __ffsll((long long)inner) - 1;
-        inner &= inner - 1;
-        const uint64_t dm = __ldg(reinterpret_cast<const unsigned long long*>(m.dof_descmask) + j);
-        T xj = x[j];
-        for (int i = lane; i < nv; i += 32)
-            if ((dm >> i) & 1ull) x[i] -= A[tri(i, j)] * xj;
-        __syncwarp();
-    }
 }
 
 // dense Cholesky H = L L^T on packed lower (oracle cholesky), then x <- H^-1 x
