@@ -36,7 +36,7 @@ def metrics(rep):
 here = os.path.dirname(os.path.abspath(__file__))
 doc = {"f32": metrics(sys.argv[1]), "f64": metrics(sys.argv[2]),
        "source": "ncu --set full --import-source on --clock-control none of tools/sim3d_env_profile.py <dtype> 4096 "
-                 "(one fused control step, block phase sync on); summaries in profiles/r1_sim3d_env_kernel_<dtype>.md"}
+                 "(one fused control step, current defaults); summaries in profiles/r1_sim3d_env_kernel_<dtype>.md"}
 with open(os.path.join(here, "ncu_sim3d_env_kernel.json"), "w") as fh:
     json.dump(doc, fh, indent=1)
 print(json.dumps(doc, indent=1))
