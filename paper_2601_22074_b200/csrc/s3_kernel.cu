@@ -147,7 +147,7 @@ template <class T> __device__ inline T clampt(T x, T lo, T hi) { return x < lo ?
 template <class T> struct WS {
     T *xpos, *xquat, *xipos, *cinert, *crb, *cdof, *cdofd, *cvel, *cacc, *janc, *jax, *M, *LD, *qpos, *qvel,
         *smooth, *a0, *a, *Ma, *grad, *p, *Mp, *kvd, *con, *Jc, *raref, *rD, *rjar, *rJp, *cdot,
-        *bias, *fcon, *ctrl, *com, *tk, *u, *snap;
+        *bias, *fcon, *ctrl, *com, *tk, *snap;
     int *con_pair, *lim_dof, *lim_sign;
 };
 
@@ -156,7 +156,7 @@ template <class T> __device__ inline WS<T> make_ws(T* base, const s3_layout& l) 
     const int* o = l.off;
     s.xpos = base + o[O_XPOS]; s.xquat = base + o[O_XQUAT]; s.xipos = base + o[O_XIPOS];
     s.cinert = base + o[O_CINERT]; s.crb = s.cinert; s.cdof = base + o[O_CDOF];
-    s.tk = base + o[O_CRB]; s.u = s.tk;
+    s.tk = base + o[O_CRB];  // per-dof scratch of the level-schedule factorization (flags bit 1) only
     s.janc = base + o[O_JANC]; s.jax = base + o[O_JAX];
     // factorization snapshot (rows touched by constraints, tree entries): xipos, cinert, janc, jax are
     // contiguous and dead from the end of the mass-matrix build until the next substep's kinematics
