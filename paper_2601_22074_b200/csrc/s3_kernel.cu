@@ -473,21 +473,27 @@ __device__ __noinline__ void factor_ldl(const s3_model& m, T* A, T* rk, int lane
     // visited from the highest index down through the bit mask
     const uint64_t all = m.nv == 64 ? ~0ull : ((1ull << m.nv) - 1);
     uint64_t todo = (sel == 0 ? all : (sel == 1 ? (~U & all) : (U & all))) & m.nonroot_mask;
+    // table pointers in registers: through `m` (a generic reference to the grid-constant block) every
+    // use is a reload the compiler cannot hoist past the shared-memory stores
+    const int32_t* __restrict__ lptr = m.ldl_ptr;
+    const uint16_t* __restrict__ lpair = m.ldl_pair;
+    const uint16_t* __restrict__ lnorm = m.ldl_norm;
+    const int nnorm = m.nldl_norm;
     while (todo) {
         const int k = 63 - __clzll((long long)todo);
         todo &= ~(1ull << k);
-        const int p0 = __ldg(m.ldl_ptr + k), p1 = __ldg(m.ldl_ptr + k + 1);
+        const int p0 = __ldg(lptr + k), p1 = __ldg(lptr + k + 1);
         T rk = T(1) / A[tri(k, k)];
         int rkb = tri(k, 0);
         for (int t = p0 + lane; t < p1; t += 32) {
-            int pr = __ldg(m.ldl_pair + t);
+            int pr = __ldg(lpair + t);
             int i = pr >> 8, j = pr & 255;
             A[tri(i, j)] -= (A[rkb + i] * rk) * A[rkb + j];
         }
         __syncwarp();
     }
-    for (int t = lane; t < m.nldl_norm; t += 32) {
-        int pr = __ldg(m.ldl_norm + t);
+    for (int t = lane; t < nnorm; t += 32) {
+        int pr = __ldg(lnorm + t);
         int k = pr >> 8, i = pr & 255;
         if (sel && (int)((U >> k) & 1ull) != (sel == 2)) continue;
         A[tri(k, i)] = A[tri(k, i)] / A[tri(k, k)];
@@ -498,8 +504,10 @@ __device__ __noinline__ void factor_ldl(const s3_model& m, T* A, T* rk, int lane
 // tree entries (i, j in chain(i)) of the rows in U: A -> snap (save) or snap -> A (restore); all rows if U = ~0
 template <class T>
 __device__ __noinline__ void tree_copy(const s3_model& m, T* A, T* snap, uint64_t U, bool save, int lane) {
-    for (int t = lane; t < m.ntree; t += 32) {
-        int pr = __ldg(m.tree_ent + t);
+    const uint16_t* __restrict__ ent = m.tree_ent;
+    const int n = m.ntree;
+    for (int t = lane; t < n; t += 32) {
+        int pr = __ldg(ent + t);
         int i = pr >> 8, j = pr & 255;
         if (!((U >> i) & 1ull)) continue;
         if (save) snap[t] = A[tri(i, j)];
@@ -510,8 +518,10 @@ __device__ __noinline__ void tree_copy(const s3_model& m, T* A, T* snap, uint64_
 
 // copy the tree entries of M into A (everything a tree factorization / solve reads)
 template <class T> __device__ __noinline__ void tree_load(const s3_model& m, const T* M, T* A, int lane) {
-    for (int t = lane; t < m.ntree; t += 32) {
-        int pr = __ldg(m.tree_ent + t);
+    const uint16_t* __restrict__ ent = m.tree_ent;
+    const int n = m.ntree;
+    for (int t = lane; t < n; t += 32) {
+        int pr = __ldg(ent + t);
         int k = tri(pr >> 8, pr & 255);
         A[k] = M[k];
     }
