@@ -181,10 +181,24 @@ template <class T> __device__ inline WS<T> make_ws(T* base, const s3_layout& l) 
 
 template <class T> __device__ inline const T* F(const void* p) { return static_cast<const T*>(p); }
 
+// The model of the launch, copied into constant memory ahead of each step kernel on the launching stream.
+// The physics stages read it from here instead of through a reference to the kernel's grid-constant
+// parameter: that reference is a generic pointer, so every table pointer read inside a loop that stores to
+// shared memory was reloaded each iteration; constant-bank reads are cached and may be hoisted.
+__constant__ s3_model c_s3m;
+// float64 stages read the constant-bank copy (-5.5 % per G1 control step, -7 % motion imitation); float32
+// stages keep the parameter reference (the constant-bank reads, hoisted, raised float32 register pressure
+// and spills: +7.5 %)
+template <class T> __device__ __forceinline__ const s3_model& model_ref(const s3_model& param) {
+    if constexpr (sizeof(T) == 8) return c_s3m;
+    else return param;
+}
+
 // ---------------------------------------------------------------- stages
 
 // mj_kinematics: body frames level by level (oracle kinematics)
-template <class T> __device__ void __noinline__ kinematics(const s3_model& m, const s3_layout& L_, T* B_, int lane) {
+template <class T> __device__ void __noinline__ kinematics(const s3_model& m_, const s3_layout& L_, T* B_, int lane) {
+    const s3_model& m = model_ref<T>(m_);  // float64: the constant-bank copy (see c_s3m)
     WS<T> s = make_ws(B_, L_);
     const T* bpos = F<T>(m.body_pos);
     const T* bquat = F<T>(m.body_quat);
@@ -248,7 +262,8 @@ template <class T> __device__ void __noinline__ kinematics(const s3_model& m, co
 }
 
 // mj_comPos: xipos, subtree com (single tree), cinert, cdof; geom frames
-template <class T> __device__ void __noinline__ com_pos(const s3_model& m, const s3_layout& L_, T* B_, int lane, T ms) {
+template <class T> __device__ void __noinline__ com_pos(const s3_model& m_, const s3_layout& L_, T* B_, int lane, T ms) {
+    const s3_model& m = model_ref<T>(m_);  // float64: the constant-bank copy (see c_s3m)
     WS<T> s = make_ws(B_, L_);
     const T* ipos = F<T>(m.body_ipos);
     const T* ilmat = F<T>(m.body_ilmat);
@@ -337,7 +352,8 @@ template <class T> __device__ void __noinline__ com_pos(const s3_model& m, const
 
 // mj_crb: composite inertias (levels, deepest first, children in descending index) + packed M.
 // Accumulates in place over cinert (RNE, the only other reader of cinert, has already run).
-template <class T> __device__ void __noinline__ crb_mass(const s3_model& m, const s3_layout& L_, T* B_, int lane) {
+template <class T> __device__ void __noinline__ crb_mass(const s3_model& m_, const s3_layout& L_, T* B_, int lane) {
+    const s3_model& m = model_ref<T>(m_);  // float64: the constant-bank copy (see c_s3m)
     WS<T> s = make_ws(B_, L_);
     for (int L = m.nlevel - 2; L >= 1; --L) {
         int n0 = m.level_ptr[L], nl = m.level_ptr[L + 1] - n0;
@@ -377,7 +393,8 @@ template <class T> __device__ void __noinline__ crb_mass(const s3_model& m, cons
 // U (0: all): subtrees outside U eliminate identically for M and for H = M + J^T D J when every
 // constraint row lives on U, so Newton refactors only U (eliminations of disjoint subtrees commute).
 template <class T>
-__device__ __noinline__ void factor_ldl(const s3_model& m, T* A, T* rk, int lane, uint64_t U = 0, int sel = 0) {
+__device__ __noinline__ void factor_ldl(const s3_model& m_, T* A, T* rk, int lane, uint64_t U = 0, int sel = 0) {
+    const s3_model& m = model_ref<T>(m_);  // float64: the constant-bank copy (see c_s3m)
     if (m.flags & 4) {
         // mask-level schedule: lane owns dof rows i in {lane, lane + 32}; at height level h it applies
         // the Schur updates of the level's dofs k that descend from i to its row (j in chain(i)). Rows of
@@ -503,7 +520,8 @@ __device__ __noinline__ void factor_ldl(const s3_model& m, T* A, T* rk, int lane
 
 // tree entries (i, j in chain(i)) of the rows in U: A -> snap (save) or snap -> A (restore); all rows if U = ~0
 template <class T>
-__device__ __noinline__ void tree_copy(const s3_model& m, T* A, T* snap, uint64_t U, bool save, int lane) {
+__device__ __noinline__ void tree_copy(const s3_model& m_, T* A, T* snap, uint64_t U, bool save, int lane) {
+    const s3_model& m = model_ref<T>(m_);  // float64: the constant-bank copy (see c_s3m)
     const uint16_t* __restrict__ ent = m.tree_ent;
     const int n = m.ntree;
     for (int t = lane; t < n; t += 32) {
@@ -517,7 +535,8 @@ __device__ __noinline__ void tree_copy(const s3_model& m, T* A, T* snap, uint64_
 }
 
 // copy the tree entries of M into A (everything a tree factorization / solve reads)
-template <class T> __device__ __noinline__ void tree_load(const s3_model& m, const T* M, T* A, int lane) {
+template <class T> __device__ __noinline__ void tree_load(const s3_model& m_, const T* M, T* A, int lane) {
+    const s3_model& m = model_ref<T>(m_);  // float64: the constant-bank copy (see c_s3m)
     const uint16_t* __restrict__ ent = m.tree_ent;
     const int n = m.ntree;
     for (int t = lane; t < n; t += 32) {
@@ -529,7 +548,8 @@ template <class T> __device__ __noinline__ void tree_load(const s3_model& m, con
 }
 
 // x <- M^-1 x with the L^T D L factor (oracle solve_ldl; column-oriented forward pass)
-template <class T> __device__ __noinline__ void solve_ldl(const s3_model& m, const T* A, T* x, int lane) {
+template <class T> __device__ __noinline__ void solve_ldl(const s3_model& m_, const T* A, T* x, int lane) {
+    const s3_model& m = model_ref<T>(m_);  // float64: the constant-bank copy (see c_s3m)
     int nv = m.nv;
     if (m.flags & 4) {
         // mask-level sweeps (see factor_ldl): leaf-to-root by height, each lane's dofs j gather the level's
@@ -704,7 +724,8 @@ template <class T> __device__ __noinline__ void sym_mul(int nv, const T* M, cons
 }
 
 // mj_comVel + mj_rne (qacc = 0): bias forces
-template <class T> __device__ void __noinline__ rne(const s3_model& m, const s3_layout& L_, T* B_, int lane) {
+template <class T> __device__ void __noinline__ rne(const s3_model& m_, const s3_layout& L_, T* B_, int lane) {
+    const s3_model& m = model_ref<T>(m_);  // float64: the constant-bank copy (see c_s3m)
     WS<T> s = make_ws(B_, L_);
     if (lane < 6) {
         s.cvel[lane] = T(0);
@@ -768,7 +789,8 @@ template <class T> __device__ void __noinline__ rne(const s3_model& m, const s3_
 }
 
 // actuation + passive + smooth force (oracle actuation / forward)
-template <class T> __device__ void __noinline__ smooth_force(const s3_model& m, const s3_layout& L_, T* B_, const T* applied, int lane) {
+template <class T> __device__ void __noinline__ smooth_force(const s3_model& m_, const s3_layout& L_, T* B_, const T* applied, int lane) {
+    const s3_model& m = model_ref<T>(m_);  // float64: the constant-bank copy (see c_s3m)
     WS<T> s = make_ws(B_, L_);
     for (int i = lane; i < m.nv; i += 32) { s.fcon[i] = T(0); s.kvd[i] = T(0); }
     __syncwarp();
@@ -908,7 +930,8 @@ template <class T> __device__ inline void point_of(const s3_model& m, int g, con
 }
 
 // Narrowphase of one pair: up to 4 contacts into `hits`, in the oracle's order.
-template <class T> __device__ __noinline__ int narrow(const s3_model& m, const s3_layout& L_, T* B_, int p, Hit<T>* hits) {
+template <class T> __device__ __noinline__ int narrow(const s3_model& m_, const s3_layout& L_, T* B_, int p, Hit<T>* hits) {
+    const s3_model& m = model_ref<T>(m_);  // float64: the constant-bank copy (see c_s3m)
     WS<T> s = make_ws(B_, L_);
     int g1 = m.pair_geom[2 * p], g2 = m.pair_geom[2 * p + 1];
     int t1 = m.geom_type[g1], t2 = m.geom_type[g2];
@@ -1066,7 +1089,8 @@ template <class T> __device__ inline void make_frame(const T* n, T* fr) {
 }
 
 // broadphase + narrowphase over all pairs, compacted in pair order; returns ncon (warp-uniform)
-template <class T> __device__ int __noinline__ collide(const s3_model& m, const s3_layout& L_, T* B_, int lane, int& dropped, T fscale) {
+template <class T> __device__ int __noinline__ collide(const s3_model& m_, const s3_layout& L_, T* B_, int lane, int& dropped, T fscale) {
+    const s3_model& m = model_ref<T>(m_);  // float64: the constant-bank copy (see c_s3m)
     WS<T> s = make_ws(B_, L_);
     int base = 0;
     dropped = 0;
@@ -1112,8 +1136,9 @@ template <class T> __device__ int __noinline__ collide(const s3_model& m, const 
 // ---------------------------------------------------------------- constraints
 
 // U = union of the Jacobian column sets of every contact and every violated limit (warp-uniform)
-template <class T> __device__ __noinline__ uint64_t touched_mask(const s3_model& m, const s3_layout& L_, T* B_, int ncon,
+template <class T> __device__ __noinline__ uint64_t touched_mask(const s3_model& m_, const s3_layout& L_, T* B_, int ncon,
                                                                  int lane) {
+    const s3_model& m = model_ref<T>(m_);  // float64: the constant-bank copy (see c_s3m)
     WS<T> s = make_ws(B_, L_);
     const unsigned long long* pm = reinterpret_cast<const unsigned long long*>(m.pair_dofmask);
     const unsigned long long* cm = reinterpret_cast<const unsigned long long*>(m.dof_chainmask);
@@ -1144,7 +1169,8 @@ template <class T> __device__ inline T impedance(const s3_model& m, T r) {
 }
 
 // Contact Jacobians Jc[c][3][stride] (frame rows over the pair's chain), limit rows, aref, D.
-template <class T> __device__ int __noinline__ build_rows(const s3_model& m, const s3_layout& L_, T* B_, int ncon, int& nlim, int lane) {
+template <class T> __device__ int __noinline__ build_rows(const s3_model& m_, const s3_layout& L_, T* B_, int ncon, int& nlim, int lane) {
+    const s3_model& m = model_ref<T>(m_);  // float64: the constant-bank copy (see c_s3m)
     WS<T> s = make_ws(B_, L_);
     // limits: ballot-compact the violated sides
     const T* rng = F<T>(m.lim_range);
@@ -1244,8 +1270,9 @@ template <class T> __device__ int __noinline__ build_rows(const s3_model& m, con
 }
 
 // out[r] = J_r x for all rows
-template <class T> __device__ void __noinline__ rows_mul(const s3_model& m, const s3_layout& L_, T* B_, int ncon, int nlim, const T* x, T* out,
+template <class T> __device__ void __noinline__ rows_mul(const s3_model& m_, const s3_layout& L_, T* B_, int ncon, int nlim, const T* x, T* out,
                                             int lane) {
+    const s3_model& m = model_ref<T>(m_);  // float64: the constant-bank copy (see c_s3m)
     WS<T> s = make_ws(B_, L_);
     int stride = m.chain_stride;
     for (int t = lane; t < 3 * ncon; t += 32) {
@@ -1274,8 +1301,9 @@ template <class T> __device__ void __noinline__ rows_mul(const s3_model& m, cons
 }
 
 // y += J^T (coef) where coef[r] is per row
-template <class T> __device__ void __noinline__ rows_tmul_add(const s3_model& m, const s3_layout& L_, T* B_, int ncon, int nlim, const T* coef, T* y,
+template <class T> __device__ void __noinline__ rows_tmul_add(const s3_model& m_, const s3_layout& L_, T* B_, int ncon, int nlim, const T* coef, T* y,
                                                  int lane) {
+    const s3_model& m = model_ref<T>(m_);  // float64: the constant-bank copy (see c_s3m)
     WS<T> s = make_ws(B_, L_);
     int stride = m.chain_stride;
     for (int r = lane; r < nlim; r += 32) y[s.lim_dof[r]] += T(s.lim_sign[r]) * coef[r];
@@ -1304,8 +1332,9 @@ template <class T> __device__ void __noinline__ rows_tmul_add(const s3_model& m,
     }
 }
 
-template <class T> __device__ T __noinline__ total_cost(const s3_model& m, const s3_layout& L_, T* B_, int nefc, const T* a, const T* Ma,
+template <class T> __device__ T __noinline__ total_cost(const s3_model& m_, const s3_layout& L_, T* B_, int nefc, const T* a, const T* Ma,
                                            const T* jar, int lane) {
+    const s3_model& m = model_ref<T>(m_);  // float64: the constant-bank copy (see c_s3m)
     WS<T> s = make_ws(B_, L_);
     // 1/2 a^T M a - a^T f + constraint term: the Gauss term up to a constant (oracle _cost)
     T g = T(0);
@@ -1317,7 +1346,8 @@ template <class T> __device__ T __noinline__ total_cost(const s3_model& m, const
 }
 
 // mj_solNewton restated (oracle newton / line_search)
-template <class T> __device__ int __noinline__ newton(const s3_model& m, const s3_layout& L_, T* B_, int ncon, int nlim, bool warm_ok, uint64_t U, int lane) {
+template <class T> __device__ int __noinline__ newton(const s3_model& m_, const s3_layout& L_, T* B_, int ncon, int nlim, bool warm_ok, uint64_t U, int lane) {
+    const s3_model& m = model_ref<T>(m_);  // float64: the constant-bank copy (see c_s3m)
     WS<T> s = make_ws(B_, L_);
     int nv = m.nv;
     int nefc = nlim + 4 * ncon;
@@ -1487,8 +1517,9 @@ template <class T> __device__ int __noinline__ newton(const s3_model& m, const s
 // ---------------------------------------------------------------- one physics substep (mj_step)
 
 template <class T>
-__device__ __noinline__ int substep(const s3_model& m, const s3_data& d, const s3_layout& L_, T* B_, int64_t w, T* gw, const T* gapp, bool last,
+__device__ __noinline__ int substep(const s3_model& m_, const s3_data& d, const s3_layout& L_, T* B_, int64_t w, T* gw, const T* gapp, bool last,
                         int lane) {
+    const s3_model& m = model_ref<T>(m_);  // float64: the constant-bank copy (see c_s3m)
     WS<T> s = make_ws(B_, L_);
     const int nv = m.nv;
     const T dt = T(m.timestep);
@@ -2627,6 +2658,10 @@ int s3_env_step(const s3_model* m, const s3_data* d, const s3_layout* l, const s
         return fail(S3_ERR_ARG, "layout planned without the level-schedule scratch (flags bits 1-2): re-plan");
     if (t->order && d->nworld > INT32_MAX) return fail(S3_ERR_BOUNDS, "cost-ordered schedule needs < 2^31 worlds");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    // the physics stages read the model from constant memory (s3::c_s3m): upload it on this stream
+    if (cudaMemcpyToSymbolAsync(c_s3m, m, sizeof(s3_model), 0, cudaMemcpyHostToDevice,
+                                static_cast<cudaStream_t>(stream)) != cudaSuccess)
+        return fail(S3_ERR_CUDA, cudaGetErrorString(cudaGetLastError()));
     const s3_layout ll = balanced_layout(*l, d->nworld, m->flags);
     int wpb = ll.warps_per_block;
     unsigned grid = (unsigned)((d->nworld + wpb - 1) / wpb);
@@ -2664,6 +2699,10 @@ int s3_step(const s3_model* m, const s3_data* d, const s3_layout* l, int32_t nsu
     if ((m->flags & 6) && l->off[O_CDOF] - l->off[O_CRB] < m->nv)
         return fail(S3_ERR_ARG, "layout planned without the level-schedule scratch (flags bits 1-2): re-plan");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    // the physics stages read the model from constant memory (s3::c_s3m): upload it on this stream
+    if (cudaMemcpyToSymbolAsync(c_s3m, m, sizeof(s3_model), 0, cudaMemcpyHostToDevice,
+                                static_cast<cudaStream_t>(stream)) != cudaSuccess)
+        return fail(S3_ERR_CUDA, cudaGetErrorString(cudaGetLastError()));
     const s3_layout ll = balanced_layout(*l, d->nworld, m->flags);
     int wpb = ll.warps_per_block;
     unsigned grid = (unsigned)((d->nworld + wpb - 1) / wpb);
