@@ -186,9 +186,10 @@ template <class T> __device__ inline const T* F(const void* p) { return static_c
 // parameter: that reference is a generic pointer, so every table pointer read inside a loop that stores to
 // shared memory was reloaded each iteration; constant-bank reads are cached and may be hoisted.
 __constant__ s3_model c_s3m;
-// float64 stages read the constant-bank copy (-5.5 % per G1 control step, -7 % motion imitation); float32
-// stages keep the parameter reference (the constant-bank reads, hoisted, raised float32 register pressure
-// and spills: +7.5 %)
+// The kinematics / dynamics / collision / row-building stages read the constant-bank copy in both builds;
+// the factorization, solves, row products and Newton read it in float64 only (-5.5 % per G1 control step,
+// -7 % motion imitation) -- in float32 the hoisted constant-bank reads there raised register pressure and
+// spills (+7.5 %), while the first group alone is -2.2 %.
 template <class T> __device__ __forceinline__ const s3_model& model_ref(const s3_model& param) {
     if constexpr (sizeof(T) == 8) return c_s3m;
     else return param;
@@ -198,7 +199,7 @@ template <class T> __device__ __forceinline__ const s3_model& model_ref(const s3
 
 // mj_kinematics: body frames level by level (oracle kinematics)
 template <class T> __device__ void __noinline__ kinematics(const s3_model& m_, const s3_layout& L_, T* B_, int lane) {
-    const s3_model& m = model_ref<T>(m_);  // float64: the constant-bank copy (see c_s3m)
+    const s3_model& m = c_s3m;  // constant-bank model (both dtypes; see c_s3m)
     WS<T> s = make_ws(B_, L_);
     const T* bpos = F<T>(m.body_pos);
     const T* bquat = F<T>(m.body_quat);
@@ -263,7 +264,7 @@ template <class T> __device__ void __noinline__ kinematics(const s3_model& m_, c
 
 // mj_comPos: xipos, subtree com (single tree), cinert, cdof; geom frames
 template <class T> __device__ void __noinline__ com_pos(const s3_model& m_, const s3_layout& L_, T* B_, int lane, T ms) {
-    const s3_model& m = model_ref<T>(m_);  // float64: the constant-bank copy (see c_s3m)
+    const s3_model& m = c_s3m;  // constant-bank model (both dtypes; see c_s3m)
     WS<T> s = make_ws(B_, L_);
     const T* ipos = F<T>(m.body_ipos);
     const T* ilmat = F<T>(m.body_ilmat);
@@ -353,7 +354,7 @@ template <class T> __device__ void __noinline__ com_pos(const s3_model& m_, cons
 // mj_crb: composite inertias (levels, deepest first, children in descending index) + packed M.
 // Accumulates in place over cinert (RNE, the only other reader of cinert, has already run).
 template <class T> __device__ void __noinline__ crb_mass(const s3_model& m_, const s3_layout& L_, T* B_, int lane) {
-    const s3_model& m = model_ref<T>(m_);  // float64: the constant-bank copy (see c_s3m)
+    const s3_model& m = c_s3m;  // constant-bank model (both dtypes; see c_s3m)
     WS<T> s = make_ws(B_, L_);
     for (int L = m.nlevel - 2; L >= 1; --L) {
         int n0 = m.level_ptr[L], nl = m.level_ptr[L + 1] - n0;
@@ -725,7 +726,7 @@ template <class T> __device__ __noinline__ void sym_mul(int nv, const T* M, cons
 
 // mj_comVel + mj_rne (qacc = 0): bias forces
 template <class T> __device__ void __noinline__ rne(const s3_model& m_, const s3_layout& L_, T* B_, int lane) {
-    const s3_model& m = model_ref<T>(m_);  // float64: the constant-bank copy (see c_s3m)
+    const s3_model& m = c_s3m;  // constant-bank model (both dtypes; see c_s3m)
     WS<T> s = make_ws(B_, L_);
     if (lane < 6) {
         s.cvel[lane] = T(0);
@@ -790,7 +791,7 @@ template <class T> __device__ void __noinline__ rne(const s3_model& m_, const s3
 
 // actuation + passive + smooth force (oracle actuation / forward)
 template <class T> __device__ void __noinline__ smooth_force(const s3_model& m_, const s3_layout& L_, T* B_, const T* applied, int lane) {
-    const s3_model& m = model_ref<T>(m_);  // float64: the constant-bank copy (see c_s3m)
+    const s3_model& m = c_s3m;  // constant-bank model (both dtypes; see c_s3m)
     WS<T> s = make_ws(B_, L_);
     for (int i = lane; i < m.nv; i += 32) { s.fcon[i] = T(0); s.kvd[i] = T(0); }
     __syncwarp();
@@ -931,7 +932,7 @@ template <class T> __device__ inline void point_of(const s3_model& m, int g, con
 
 // Narrowphase of one pair: up to 4 contacts into `hits`, in the oracle's order.
 template <class T> __device__ __noinline__ int narrow(const s3_model& m_, const s3_layout& L_, T* B_, int p, Hit<T>* hits) {
-    const s3_model& m = model_ref<T>(m_);  // float64: the constant-bank copy (see c_s3m)
+    const s3_model& m = c_s3m;  // constant-bank model (both dtypes; see c_s3m)
     WS<T> s = make_ws(B_, L_);
     int g1 = m.pair_geom[2 * p], g2 = m.pair_geom[2 * p + 1];
     int t1 = m.geom_type[g1], t2 = m.geom_type[g2];
@@ -1090,7 +1091,7 @@ template <class T> __device__ inline void make_frame(const T* n, T* fr) {
 
 // broadphase + narrowphase over all pairs, compacted in pair order; returns ncon (warp-uniform)
 template <class T> __device__ int __noinline__ collide(const s3_model& m_, const s3_layout& L_, T* B_, int lane, int& dropped, T fscale) {
-    const s3_model& m = model_ref<T>(m_);  // float64: the constant-bank copy (see c_s3m)
+    const s3_model& m = c_s3m;  // constant-bank model (both dtypes; see c_s3m)
     WS<T> s = make_ws(B_, L_);
     int base = 0;
     dropped = 0;
@@ -1138,7 +1139,7 @@ template <class T> __device__ int __noinline__ collide(const s3_model& m_, const
 // U = union of the Jacobian column sets of every contact and every violated limit (warp-uniform)
 template <class T> __device__ __noinline__ uint64_t touched_mask(const s3_model& m_, const s3_layout& L_, T* B_, int ncon,
                                                                  int lane) {
-    const s3_model& m = model_ref<T>(m_);  // float64: the constant-bank copy (see c_s3m)
+    const s3_model& m = c_s3m;  // constant-bank model (both dtypes; see c_s3m)
     WS<T> s = make_ws(B_, L_);
     const unsigned long long* pm = reinterpret_cast<const unsigned long long*>(m.pair_dofmask);
     const unsigned long long* cm = reinterpret_cast<const unsigned long long*>(m.dof_chainmask);
@@ -1170,7 +1171,7 @@ template <class T> __device__ inline T impedance(const s3_model& m, T r) {
 
 // Contact Jacobians Jc[c][3][stride] (frame rows over the pair's chain), limit rows, aref, D.
 template <class T> __device__ int __noinline__ build_rows(const s3_model& m_, const s3_layout& L_, T* B_, int ncon, int& nlim, int lane) {
-    const s3_model& m = model_ref<T>(m_);  // float64: the constant-bank copy (see c_s3m)
+    const s3_model& m = c_s3m;  // constant-bank model (both dtypes; see c_s3m)
     WS<T> s = make_ws(B_, L_);
     // limits: ballot-compact the violated sides
     const T* rng = F<T>(m.lim_range);
