@@ -186,10 +186,10 @@ template <class T> __device__ inline const T* F(const void* p) { return static_c
 // parameter: that reference is a generic pointer, so every table pointer read inside a loop that stores to
 // shared memory was reloaded each iteration; constant-bank reads are cached and may be hoisted.
 __constant__ s3_model c_s3m;
-// The kinematics / dynamics / collision / row-building stages read the constant-bank copy in both builds;
-// the factorization, solves, row products and Newton read it in float64 only (-5.5 % per G1 control step,
-// -7 % motion imitation) -- in float32 the hoisted constant-bank reads there raised register pressure and
-// spills (+7.5 %), while the first group alone is -2.2 %.
+// The kinematics / dynamics / collision / row-building stages and Newton read the constant-bank copy in
+// both builds; the factorization, solves, row products, cost and substep driver read it in float64 only
+// (-5.5 % per G1 control step, -7 % motion imitation) -- in float32 the hoisted constant-bank reads there
+// raised register pressure and spills (+7.5 %), while the first group alone is -3.5 %.
 template <class T> __device__ __forceinline__ const s3_model& model_ref(const s3_model& param) {
     if constexpr (sizeof(T) == 8) return c_s3m;
     else return param;
@@ -1348,7 +1348,7 @@ template <class T> __device__ T __noinline__ total_cost(const s3_model& m_, cons
 
 // mj_solNewton restated (oracle newton / line_search)
 template <class T> __device__ int __noinline__ newton(const s3_model& m_, const s3_layout& L_, T* B_, int ncon, int nlim, bool warm_ok, uint64_t U, int lane) {
-    const s3_model& m = model_ref<T>(m_);  // float64: the constant-bank copy (see c_s3m)
+    const s3_model& m = c_s3m;  // constant-bank model (both dtypes; see c_s3m)
     WS<T> s = make_ws(B_, L_);
     int nv = m.nv;
     int nefc = nlim + 4 * ncon;
