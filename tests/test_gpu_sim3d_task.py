@@ -177,6 +177,34 @@ def test_block_phase_sync_is_bit_identical(dtype):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("n", [700, 5000])
+def test_launch_shape_is_bit_identical(n):
+    """Warps per block only decide where a world runs: the wave-balanced launch (flags bit 6, the G1
+    default), the maximal block and a fixed small block give bit-identical steps, for one partial wave
+    (700 worlds) and several waves (5000)."""
+    import torch
+
+    from paper_2601_22074_b200.sim3d.task import VelocityEnv3D
+
+    m = robots.g1_like(rough=True, seed=2)
+    cfg = VelocityTaskCfg(default_qpos=robots.default_qpos(m, robots.G1_DEFAULT_JOINTS), height_scan=True)
+    envs = [VelocityEnv3D(robots.g1_like(rough=True, seed=2), cfg, n, seed=5, dtype="f32") for _ in range(3)]
+    assert envs[0].dm.struct.flags & 64
+    envs[1].dm.struct.flags &= ~64
+    envs[2].dm.layout.warps_per_block = 3
+    envs[2].dm.layout.bytes_per_block = 3 * envs[2].dm.layout.elems_per_world * 4
+    outs = [e.reset() for e in envs]
+    assert all(torch.equal(outs[0], o) for o in outs[1:])
+    g = torch.Generator(device="cuda").manual_seed(0)
+    for _ in range(3):
+        act = torch.rand(n, m.nu, device="cuda", generator=g) * 2 - 1
+        res = [e.step(act) for e in envs]
+        for r in res[1:]:
+            assert all(torch.equal(a, b) for a, b in zip(res[0], r))
+    assert all(torch.equal(envs[0].data.qpos, e.data.qpos) for e in envs[1:])
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("dtype", ["f32", "f64"])
 def test_cost_ordered_schedule_is_bit_identical(dtype, monkeypatch):
     """Sorting the worlds by their last solver cost before each step (s3_task.cost / order) only changes
