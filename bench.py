@@ -63,21 +63,46 @@ def _ncu_traffic():
 
 
 # ---------------------------------------------------------------------------
-# CPU side: the oracle port partitioned over host processes (world_id_offset)
+# CPU side: the reference's own implementation on the host cores, partitioned
+# over processes through world_id_offset (partition-independent per world,
+# reference tests/test_env.py:256-270)
+
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")  # the unmodified reference, pip-installed
 
 
-def _cpu_worker(conn, task, n_total, n_local, offset, seed):
+def reference_available() -> bool:
+    return os.path.isfile(os.path.join(REF_DIR, "stridesim", "env.py"))
+
+
+def _cpu_worker(conn, kind, task, n_local, offset, seed):
     os.environ.setdefault("OMP_NUM_THREADS", "1")
-    sys.path.insert(0, ROOT)
-    from oracle import OracleEnv
-    from paper_2601_22074_b200.tasks import make_env_cfg
-    from paper_2601_22074_b200.terrain import generate_grid
+    if kind == "reference":
+        # the unmodified reference through its own public API: make_env_cfg ->
+        # ManagerBasedRlEnv -> reset -> step(random_policy(env, i)) (cli.py:155-164)
+        sys.path.insert(0, REF_DIR)
+        from stridesim.env import ManagerBasedRlEnv
+        from stridesim.policies import random_policy
+        from stridesim.tasks import make_env_cfg
 
-    cfg = make_env_cfg(task, num_envs=n_local, seed=seed)
-    cfg.scene.world_id_offset = offset
-    env = OracleEnv(cfg, generate_grid(cfg.scene.terrain, cfg.seed).samples)
-    env.reset()
+        cfg = make_env_cfg(task, num_envs=n_local, seed=seed)
+        cfg.scene.world_id_offset = offset
+        env = ManagerBasedRlEnv(cfg, task)
+        env.reset()
+        step = lambda i: env.step(random_policy(env, i))  # noqa: E731
+    else:
+        # the numpy restatement (oracle/, bit-identical to the reference, tests/test_oracle_golden.py)
+        sys.path.insert(0, ROOT)
+        from oracle import OracleEnv
+        from paper_2601_22074_b200.tasks import make_env_cfg
+        from paper_2601_22074_b200.terrain import generate_grid
+
+        cfg = make_env_cfg(task, num_envs=n_local, seed=seed)
+        cfg.scene.world_id_offset = offset
+        env = OracleEnv(cfg, generate_grid(cfg.scene.terrain, cfg.seed).samples)
+        env.reset()
+        step = lambda i: env.step(env.random_actions())  # noqa: E731
     conn.send("ready")
+    i = 0
     while True:
         msg = conn.recv()
         if msg == "stop":
@@ -85,14 +110,19 @@ def _cpu_worker(conn, task, n_total, n_local, offset, seed):
         n_steps = int(msg)
         t0 = time.perf_counter()
         for _ in range(n_steps):
-            env.step(env.random_actions())
+            step(i)
+            i += 1
         conn.send(time.perf_counter() - t0)
 
 
 class CpuBaseline:
-    """Persistent worker pool; each step() runs one control step of all worlds."""
+    """Persistent worker pool; each run(k) runs k control steps of all worlds.
 
-    def __init__(self, task, n_total, seed=0, procs=None):
+    kind "reference": the unmodified reference package (baseline/_ref);
+    kind "port": the oracle restatement."""
+
+    def __init__(self, task, n_total, seed=0, procs=None, kind=None):
+        self.kind = kind or ("reference" if reference_available() else "port")
         procs = procs or min(os.cpu_count() or 1, n_total)
         self.procs = procs
         ctx = mp.get_context("spawn")
@@ -100,7 +130,7 @@ class CpuBaseline:
         split = np.array_split(np.arange(n_total), procs)
         for part in split:
             a, b = ctx.Pipe()
-            w = ctx.Process(target=_cpu_worker, args=(b, task, n_total, len(part), int(part[0]), seed), daemon=True)
+            w = ctx.Process(target=_cpu_worker, args=(b, self.kind, task, len(part), int(part[0]), seed), daemon=True)
             w.start()
             self.conns.append(a)
             self.workers.append(w)
@@ -108,7 +138,7 @@ class CpuBaseline:
             assert c.recv() == "ready"
 
     def run(self, n_steps: int) -> float:
-        """Wall seconds for n_steps control steps of all worlds (max over workers)."""
+        """Wall seconds for n_steps control steps of all worlds (the slowest worker)."""
         t0 = time.perf_counter()
         for c in self.conns:
             c.send(n_steps)
@@ -133,8 +163,14 @@ def cpu_model_name() -> str:
     return "unknown"
 
 
-def measure_cpu(task, n, seconds=10.0, procs=None):
-    pool = CpuBaseline(task, n, procs=procs)
+def _describe(kind: str) -> str:
+    return ("the unmodified reference (stridesim 0.1.0 from baseline/_ref, its own make_env_cfg / "
+            "ManagerBasedRlEnv / random_policy)" if kind == "reference"
+            else "the numpy oracle port of the reference (oracle/, bit-identical to it)")
+
+
+def measure_cpu(task, n, seconds=10.0, procs=None, kind=None):
+    pool = CpuBaseline(task, n, procs=procs, kind=kind)
     try:
         pool.run(3)
         steps, el = 0, 0.0
@@ -143,9 +179,22 @@ def measure_cpu(task, n, seconds=10.0, procs=None):
             steps += 5
     finally:
         pool.close()
-    return {"value": n * steps / el, "unit": UNIT, "cores": pool.procs, "kind": "port",
+    return {"value": n * steps / el, "unit": UNIT, "cores": pool.procs, "kind": pool.kind,
             "sample": f"{task} N={n} split over {pool.procs} processes (world_id_offset), {steps} control steps "
-                      f"({el:.1f} s wall), random actions, numpy oracle, CPU {cpu_model_name()}"}
+                      f"({el:.1f} s wall), random actions, {_describe(pool.kind)}, CPU {cpu_model_name()}"}
+
+
+def bench_config(task: str, n: int, world: int) -> dict:
+    """The workload record, key- and value-identical in both arms."""
+    sys.path.insert(0, ROOT)
+    from paper_2601_22074_b200.tasks import make_env_cfg
+
+    cfg = make_env_cfg(task, num_envs=n)
+    dec = cfg.decimation if cfg.decimation is not None else cfg.scene.model.decimation
+    return {"workload": f"{task} (planar biped restatement of BASELINE configs[1], SURVEY 0.1)",
+            "task": task, "envs_per_gpu": n, "total_envs": n * world, "decimation": int(dec),
+            "parallelism": f"dp{world} (world shards, world_id_offset = rank * envs_per_gpu)",
+            "l2": "flushed between timed iterations (GPU arm: 512 MiB device write before each step)"}
 
 
 # ---------------------------------------------------------------------------
@@ -206,18 +255,23 @@ class Clocks:
 # ---------------------------------------------------------------------------
 
 
-def dist_setup(gpus):
-    import torch
-
+def dist_setup(gpus, backend="nccl"):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
+    if backend == "nccl":
+        import torch
+
+        torch.cuda.set_device(local)
     if world > 1:
+        import torch
         import torch.distributed as dist
 
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     return rank, world, local
 
 
@@ -239,9 +293,10 @@ def allmax(x: float, world: int) -> float:
     return float(t.item())
 
 
-def timed_steps(env, steps: int, flush, stream, policy) -> float:
+def timed_steps(env, steps: int, flush, stream, policy, after=None) -> float:
     """Seconds of GPU time for `steps` env steps, each preceded by an L2 flush
-    (untimed) and bracketed by CUDA events on the launching stream."""
+    (untimed) and bracketed by CUDA events on the launching stream. `after(i)`
+    runs inside step i's bracket (the per-log-interval stats all-reduce)."""
     import torch
 
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
@@ -251,6 +306,8 @@ def timed_steps(env, steps: int, flush, stream, policy) -> float:
         e0, e1 = evs[i]
         e0.record(stream)
         env.step(policy(i))
+        if after is not None:
+            after(i)
         e1.record(stream)
         if i >= 2:
             # bound the host's lead to two iterations: the flush of the next
@@ -421,18 +478,21 @@ def run_ours(args):
     import __graft_entry__
 
     rank, world, local = dist_setup(args.gpus)
+    if world == 1 and args.gpus > 1:
+        raise SystemExit("--gpus N > 1 needs one process per GPU (bench.py self-launches them when WORLD_SIZE is unset)")
     if rank == 0:
         __graft_entry__.build()
     barrier(world)
     from paper_2601_22074_b200 import native
     from paper_2601_22074_b200.env import ManagerBasedRlEnv
+    from paper_2601_22074_b200.metrics import allreduce_stats, build_record, unpack_stats
     from paper_2601_22074_b200.policies import random_policy
     from paper_2601_22074_b200.tasks import make_env_cfg
     from paper_2601_22074_b200.traffic import step_bytes_per_world
 
     n = args.envs
     cfg = make_env_cfg(args.task, num_envs=n, seed=args.seed)
-    cfg.scene.world_id_offset = rank * n
+    cfg.scene.world_id_offset = rank * n  # rank r owns worlds [r*N, (r+1)*N) (env.py:67-69, :114)
     env = ManagerBasedRlEnv(cfg, args.task)
     env.reset()
     stream = torch.cuda.current_stream()
@@ -442,19 +502,37 @@ def run_ours(args):
     # fused=True draws the same actions (stream policy.random) inside the step kernel
     for i in range(args.warmup):
         env.step(random_policy(env, i, fused=True))
+    build_record(env, 0, env.reward_manager.reward, None)  # warm the stats kernel and the collective
     torch.cuda.synchronize()
+
+    # every log interval (cli.py:118, --log-every 10) the job's statistics are
+    # reduced across ranks inside the timed step: one ss_stats_pack launch packs
+    # this rank's reward / episodic sums / trigger counts / terrain-row
+    # histogram / nonfinite count, one all_reduce (NCCL) sums them over ranks;
+    # the records are unpacked on the host after the timed region
+    vecs = []
+
+    def log_interval(i):
+        if args.log_every > 0 and (i + 1) % args.log_every == 0:
+            vecs.append((i + 1, allreduce_stats(env._stats_packer.pack().clone())))
 
     clocks = Clocks(local)
     barrier(world)
     launches0 = native.LAUNCHES["count"]
-    t_step = timed_steps(env, args.steps, flush, stream, lambda i: random_policy(env, args.warmup + i, fused=True))
+    t_step = timed_steps(env, args.steps, flush, stream, lambda i: random_policy(env, args.warmup + i, fused=True),
+                         after=log_interval)
     barrier(world)
     launches = native.LAUNCHES["count"] - launches0
-    t_kernel = t_step  # one launch per step: the fused step kernel is the whole step
     t_max = allmax(t_step, world)
     value = n * world * args.steps / t_max
+    rm, tm = env.reward_manager, env.termination_manager
+    records = [unpack_stats(v, list(rm.terms), list(tm.trigger_counts), env.terrain.rows, st).__dict__
+               for st, v in vecs]
 
-    # roofline of the dominant kernel (the fused step)
+    # roofline of the dominant kernel (the fused step), timed on its own
+    # (the log-interval reduction excluded) with the same flush protocol
+    t_kernel = timed_steps(env, args.steps, flush, stream,
+                           lambda i: random_policy(env, args.warmup + args.steps + i, fused=True))
     per_world = step_bytes_per_world(env, fused_policy=True)
     peak, peak_kind = _peaks()
     achieved = per_world["total"] * n / (t_kernel / args.steps) / 1e9
@@ -463,13 +541,14 @@ def run_ours(args):
         traffic = None
 
     # end-to-end through the public API with host buffers (gym VectorEnv-style
-    # step_async / step_wait): each step's actions are read from pinned host
-    # memory by the step kernel itself; its results (obs groups, reward,
-    # terminated, truncated: the whole output arena) are snapshotted on the
-    # device and copied into pinned host memory by a copy engine, overlapping
-    # the next step's kernel; step_wait() blocks until a step's results are in
-    # host memory. Every step's inputs and outputs cross PCIe inside the timed
-    # region; the last step is waited for before the clock stops.
+    # step_async / step_wait): each step's actions are copied from pinned host
+    # memory to the device by a copy engine ahead of the step kernel; its
+    # results (obs groups, reward, terminated, truncated: the whole output
+    # arena) are snapshotted on the device and copied into pinned host memory
+    # by a second copy engine, overlapping the next step's kernel; step_wait()
+    # blocks until a step's results are in host memory. Every step's inputs
+    # and outputs cross PCIe inside the timed region; the last step is waited
+    # for before the clock stops.
     A = env.action_manager.total_dim
     rng = np.random.default_rng(rank)
     e2e_steps = 0 if args.no_e2e else max(args.steps, 200)  # tens of us each: a longer sample smooths jitter
@@ -492,11 +571,12 @@ def run_ours(args):
         host_views = env.step_wait()
     e2e_t = allmax(time.perf_counter() - t0, world)
     assert host_views is None or (host_views["reward"].shape == (n,) and host_views["reward"].device.type == "cpu")
-    e2e = None if not e2e_steps else {"value": n * world * e2e_steps / e2e_t, "unit": UNIT, "steps": e2e_steps, "h2d_bytes_per_step": n * A * 8,
-           "d2h_bytes_per_step": int(env.step_outputs.numel()),
-           "path": "pinned host actions -> env.step_async (kernel reads them over PCIe; output arena snapshotted "
-                   "D2D and copied to pinned host memory on a copy-engine stream, overlapping the next step) "
-                   "-> env.step_wait (results in host memory)"}
+    e2e = None if not e2e_steps else {
+        "value": n * world * e2e_steps / e2e_t, "unit": UNIT, "steps": e2e_steps, "h2d_bytes_per_step": n * A * 8,
+        "d2h_bytes_per_step": int(env.step_outputs.numel()),
+        "path": "pinned host actions -> env.step_async (H2D cudaMemcpyAsync on a copy-engine stream, the step "
+                "kernel waits on it; the output arena is snapshotted D2D and copied to pinned host memory on a "
+                "second copy-engine stream, overlapping the next step) -> env.step_wait (results in host memory)"}
 
     scale = at_scale(args, flush, stream) if (world == 1 and args.scale_envs > 0) else None
     s3 = None if args.no_sim3d else sim3d_leg(args, flush, stream)
@@ -510,6 +590,13 @@ def run_ours(args):
                 blk[k]["value"] = blk[k]["value"] * world  # whole job: every rank steps its shard (weak scaling)
                 blk[k]["ms_per_step"] = allmax(blk[k]["ms_per_step"], world)
 
+    offsets = [rank * n]
+    if world > 1:
+        import torch.distributed as dist
+
+        got = [None] * world
+        dist.all_gather_object(got, rank * n)
+        offsets = got
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu:
@@ -527,10 +614,7 @@ def run_ours(args):
             "vs_baseline": None,
             "dtype": "f64",
             "data": "synthetic (random actions from the per-world device streams; random-init env, no checkpoint)",
-            "config": {"workload": f"{args.task} (planar biped restatement of BASELINE configs[1], SURVEY 0.1)",
-                       "task": args.task, "envs_per_gpu": n, "decimation": env.decimation,
-                       "substeps_per_step": env.decimation, "parallelism": f"dp{world} (world shards)",
-                       "l2": "flushed (512 MiB write) between timed iterations"},
+            "config": bench_config(args.task, n, world),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_kind": peak_kind, "traffic": traffic,
                          "algorithmic_bytes_per_env_step": per_world["total"],
@@ -538,6 +622,11 @@ def run_ours(args):
                          if env.use_jit else "step_kernel<4,2> (fused control step, generic)",
                          "kernel_ms": 1e3 * t_kernel / args.steps},
             "policy": "random_policy fused into the step kernel (policies.RandomActions: same stream and values)",
+            "stats_allreduce": {"every_steps": args.log_every, "per_interval": "1 ss_stats_pack launch + 1 all_reduce "
+                                f"({'NCCL' if world > 1 else 'no-op at 1 rank'}) of {int(env._stats_packer.out.numel())} "
+                                "float64, inside the timed step", "records": len(records),
+                                "last": records[-1] if records else None},
+            "shards": {"world_id_offsets": offsets, "envs_per_rank": n},
             "at_scale": scale,
             "sim3d": s3,
             "cpu_baseline": cpu,
@@ -559,13 +648,21 @@ def run_reference(args):
     # the whole job of our arm: envs per GPU x GPUs (weak scaling), on the host cores
     world = int(os.environ.get("WORLD_SIZE", str(max(1, args.gpus))))
     n = args.envs * world
-    pool = CpuBaseline(args.task, n)
-    try:
-        pool.run(max(1, args.warmup))
-        el = pool.run(args.steps)
-    finally:
-        pool.close()
-    v = n * args.steps / el
+    runs = {}
+    for kind in (["reference", "port"] if reference_available() else ["port"]):
+        pool = CpuBaseline(args.task, n, kind=kind)
+        try:
+            pool.run(max(1, args.warmup))
+            el = pool.run(args.steps)
+        finally:
+            pool.close()
+        runs[kind] = {"value": n * args.steps / el, "unit": UNIT, "cores": pool.procs, "kind": kind,
+                      "ms_per_step": 1e3 * el / args.steps,
+                      "sample": f"{args.task} N={n} over {pool.procs} host processes (world_id_offset shards), "
+                                f"{args.steps} control steps after {max(1, args.warmup)} warm-up steps, random "
+                                f"actions, {_describe(kind)}, CPU {cpu_model_name()}"}
+    head = runs.get("reference") or runs["port"]
+    v = head["value"]
     line = {
         "metric": METRIC,
         "value": v,
@@ -573,21 +670,85 @@ def run_reference(args):
         "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
-        "ms_per_step": 1e3 * el / args.steps,
+        "ms_per_step": head["ms_per_step"],
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (random actions from the per-world streams)",
-        "config": {"workload": f"{args.task} (planar biped restatement of BASELINE configs[1], SURVEY 0.1)",
-                   "task": args.task, "envs_per_gpu": args.envs, "total_envs": n, "decimation": 4},
+        "config": bench_config(args.task, args.envs, world),
         "impl": "reference",
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": pool.procs, "kind": "port",
-                         "sample": f"{args.task} N={n} over {pool.procs} host processes, {args.steps} control steps, "
-                                   f"numpy oracle port of the reference, CPU {cpu_model_name()}"},
+        "cpu_baseline": {k: head[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "beside": {k: r for k, r in runs.items() if r is not head},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def run_dry(args):
+    """--dry-cpu: the multi-rank plumbing of run_ours on CPU (gloo), for tests:
+    each rank steps its world shard (oracle env, world_id_offset = rank * N)
+    and the job's stats are reduced with the same pack / all_reduce / unpack
+    path; rank 0 prints the shard offsets and the reduced record."""
+    rank, world, _ = dist_setup(args.gpus, backend="gloo")
+    import torch
+
+    from oracle import OracleEnv
+    from paper_2601_22074_b200.metrics import allreduce_stats, pack_stats, unpack_stats
+    from paper_2601_22074_b200.tasks import make_env_cfg
+    from paper_2601_22074_b200.terrain import generate_grid
+
+    n = args.envs
+    cfg = make_env_cfg(args.task, num_envs=n, seed=args.seed)
+    cfg.scene.world_id_offset = rank * n
+    env = OracleEnv(cfg, generate_grid(cfg.scene.terrain, cfg.seed).samples)
+    env.reset()
+    steps = args.warmup + args.steps
+    for _ in range(steps):
+        _, rew, *_ = env.step(env.random_actions())
+    vec = pack_stats(torch.from_numpy(rew), [torch.from_numpy(env.ep_sums[k]) for k in env.rw],
+                     torch.tensor(list(env.trigger_counts.values())), torch.from_numpy(env.terrain_rows),
+                     env.t_rows, torch.from_numpy(env.last_nonfinite))
+    vec = allreduce_stats(vec)
+    rec = unpack_stats(vec, list(env.rw), list(env.trigger_counts), env.t_rows, steps)
+    offsets = [rank * n]
+    if world > 1:
+        import torch.distributed as dist
+
+        offsets = [None] * world
+        dist.all_gather_object(offsets, rank * n)
+    if rank == 0:
+        print(json.dumps({"dry": True, "n_gpus": world, "config": bench_config(args.task, n, world),
+                          "shards": {"world_id_offsets": offsets, "envs_per_rank": n}, "steps": steps,
+                          "record": rec.__dict__}), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+def self_launch(argv) -> int:
+    """bench.py --gpus N with no WORLD_SIZE in the environment: start N ranks
+    (one process per GPU) through torch.distributed.run on this node and
+    relay their output (rank 0 prints the JSON line)."""
+    import socket
+
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    gpus = None
+    for i, a in enumerate(argv):
+        if a == "--gpus":
+            gpus = int(argv[i + 1])
+        elif a.startswith("--gpus="):
+            gpus = int(a.split("=", 1)[1])
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # communicator setup on stderr (rank count, NVLS / NVLink transport)
+    env.setdefault("OMP_NUM_THREADS", "1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *argv]
+    return subprocess.call(cmd, env=env)
 
 
 def main():
@@ -599,17 +760,29 @@ def main():
     ap.add_argument("--task", default="Velocity-Rough")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--log-every", type=int, default=10,
+                    help="steps between stats all-reduces inside the timed loop (cli.py --log-every; 0 disables)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the end-to-end leg (profiling runs)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-sim3d", action="store_true", help="skip the 3-D (SURVEY 8 f4) leg")
+    ap.add_argument("--dry-cpu", action="store_true", help="multi-rank plumbing on CPU (gloo + oracle), for tests")
     ap.add_argument("--scale-envs", type=int, default=262144,
                     help="also time the step at this many worlds (HBM-bound regime); 0 disables")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.impl == "ours" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        if not args.dry_cpu:
+            import torch
+
+            if torch.cuda.device_count() < args.gpus:
+                raise SystemExit(f"--gpus {args.gpus}: only {torch.cuda.device_count()} CUDA devices visible")
+        raise SystemExit(self_launch(sys.argv[1:]))
     if args.impl == "reference":
         run_reference(args)
+    elif args.dry_cpu:
+        run_dry(args)
     else:
         run_ours(args)
 

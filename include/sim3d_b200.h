@@ -309,8 +309,11 @@ int s3_plan(const s3_model* m, int32_t warps_per_block, s3_layout* out);
  * RNE, actuation, collision, constraints, Newton, implicitfast), ctrl held fixed.
  * Replaces, for the 3-D path, StepPipeline.substep x decimation (sim/physics.py:239-249,
  * env.py:228-233 of the reference; mjwarp.step in mjlab).
- * s3_step and s3_env_step upload *m to the library's constant-memory model slot on `stream` before their
- * kernel (the float64 stages read it there): launches for different models must be stream-ordered. */
+ * s3_step and s3_env_step upload *m to the library's constant-memory model slot (one per device) on
+ * `stream` before their kernel. The library serializes the slot itself: a launch from another stream than
+ * the previous launch waits on the GPU for that launch's kernels before the slot changes, an identical
+ * model on the same stream skips the upload, and concurrent host threads take a per-device lock, so
+ * different models / dtypes / streams may be mixed freely (at the price of serializing their kernels). */
 int s3_step(const s3_model* m, const s3_data* d, const s3_layout* l, int32_t nsub, void* stream);
 
 /* One control step of the fused task (mode 0; kind velocity or motion): ActionManager.process -> decimation x

@@ -27,6 +27,7 @@
  *   ss_heights       Heightfield.heights                terrain.py:159-169
  *   ss_randomize     randomize_field (startup/explicit) managers/event.py:19-52
  *   ss_actuator_eval pd_torque / dc_motor_torque        actuators.py:104-117
+ *   ss_stats_pack    metrics.build_record reductions    metrics.py:31-45
  *   ss_rt_*          ManagerBasedRlEnv.step bookkeeping (env.py:219-259)
  *   ss_jit_*         StepPipeline._rebuild (re-specialize to the layout) sim/physics.py:158-237
  *
@@ -624,9 +625,35 @@ typedef struct ss_rng_draw_args {
     double* out;
 } ss_rng_draw_args;
 
+/* One log interval's statistics of this rank packed into ONE float64 vector
+ * (metrics.build_record, metrics.py:31-45), ready for a single all-reduce:
+ *   out = [n_worlds, sum(reward), sum(ep_sums[t]) for t < n_rewards,
+ *          trigger_counts[c] for c < n_counts, histogram(terrain_rows)[r] for r < n_rows,
+ *          sum(nonfinite)]            (length 3 + n_rewards + n_counts + n_rows)
+ * One launch: every block reduces a fixed stride of worlds in a fixed order
+ * into `partials` (grid x SS_STATS_MAXV doubles), the last block to finish
+ * (ticket) sums the partials in block order -- deterministic for a given N.
+ * `ticket` is one zero-initialised uint32 the kernel resets itself. */
+#define SS_STATS_MAXV 64
+#define SS_STATS_GRID 148
+typedef struct ss_stats_args {
+    int32_t n_worlds;
+    int32_t n_rewards;
+    int32_t n_counts;
+    int32_t n_rows;
+    const double* reward;
+    const double* ep_sums;
+    const int64_t* trigger_counts;
+    const int64_t* terrain_rows;
+    const uint8_t* nonfinite;
+    double* partials;
+    uint32_t* ticket;
+    double* out;
+} ss_stats_args;
+
 #ifndef __CUDACC_RTC__ /* host entry points (not part of the JIT translation unit) */
 int ss_abi_version(void);
-size_t ss_sizeof(int which); /* 0 env_desc, 1 uniforms, 2 rng_draw_args, 3 rt_state, 4 launch */
+size_t ss_sizeof(int which); /* 0 env_desc, 1 uniforms, 2 rng_draw_args, 3 rt_state, 4 launch, 5 stats_args */
 const char* ss_last_error(void);
 
 int ss_env_step(const ss_env_desc* desc, const ss_uniforms* u, void* stream);
@@ -675,6 +702,7 @@ int ss_pipe_destroy(void* pipe);
 int ss_pipe_pre(void* pipe, const void* host_actions, void* main_stream);
 int ss_pipe_post(void* pipe, const void* arena, void* main_stream);
 int ss_pipe_wait(void* pipe);
+int ss_stats_pack(const ss_stats_args* args, void* stream);
 int ss_actuator_eval(int32_t kind, const double* kp, const double* kd, double effort,
                      double saturation, double vel_limit, const double* q_des,
                      const double* q, const double* qd, double* out, int64_t n,

@@ -21,6 +21,8 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <mutex>
+
 #include "../../include/sim3d_b200.h"
 
 namespace s3 {
@@ -2606,21 +2608,91 @@ int s3_plan(const s3_model* m, int32_t warps_per_block, s3_layout* out) {
     return S3_OK;
 }
 
+// The constant-memory model slot (s3::c_s3m) is one per device and shared by every model and stream.
+// ModelSlot serializes its use: it holds a per-device lock from the upload through the kernel launch;
+// a launch from a different stream than the previous one first waits (on the GPU) for the previous
+// launch's kernels, so no running kernel ever sees the slot change under it; an identical model on the
+// same stream skips the upload; uploads go through a small pinned staging ring (a pageable source could
+// make the async copy synchronous), each slot reused only after its previous copy has completed.
+namespace {
+constexpr int kStageSlots = 8;
+struct DeviceSlot {
+    std::mutex mu;
+    bool init = false, valid = false;
+    cudaStream_t stream = nullptr;  // stream of the last launch that used the slot
+    cudaEvent_t last = nullptr;     // recorded after that launch's kernels
+    s3_model model;                 // contents of c_s3m as of the last upload
+    s3_model* stage = nullptr;      // pinned staging ring
+    cudaEvent_t stage_done[kStageSlots] = {};
+    int next = 0;
+};
+DeviceSlot g_slots[64];
+
+class ModelSlot {
+  public:
+    ModelSlot(const s3_model* m, cudaStream_t st) : st_(st) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        s_ = &g_slots[dev & 63];
+        lk_ = std::unique_lock<std::mutex>(s_->mu);
+        if (!s_->init) {
+            if ((err_ = cudaEventCreateWithFlags(&s_->last, cudaEventDisableTiming)) != cudaSuccess) return;
+            if ((err_ = cudaMallocHost(&s_->stage, kStageSlots * sizeof(s3_model))) != cudaSuccess) return;
+            for (int i = 0; i < kStageSlots; ++i)
+                if ((err_ = cudaEventCreateWithFlags(&s_->stage_done[i], cudaEventDisableTiming)) != cudaSuccess) return;
+            s_->init = true;
+        }
+        if (s_->valid && s_->stream != st && (err_ = cudaStreamWaitEvent(st, s_->last, 0)) != cudaSuccess) return;
+        if (s_->valid && s_->stream == st && memcmp(&s_->model, m, sizeof(s3_model)) == 0) return;
+        s_->stream = st;  // from here on the slot's latest work is on st (even if the launch fails later)
+        const int k = s_->next;
+        s_->next = (k + 1) % kStageSlots;
+        if ((err_ = cudaEventSynchronize(s_->stage_done[k])) != cudaSuccess) return;
+        s_->stage[k] = *m;
+        if ((err_ = cudaMemcpyToSymbolAsync(s3::c_s3m, &s_->stage[k], sizeof(s3_model), 0, cudaMemcpyHostToDevice,
+                                            st)) != cudaSuccess)
+            return;
+        if ((err_ = cudaEventRecord(s_->stage_done[k], st)) != cudaSuccess) return;
+        s_->model = *m;
+        s_->valid = true;
+        err_ = cudaEventRecord(s_->last, st);
+    }
+    cudaError_t error() const { return err_; }
+    // after the launch's kernels are enqueued: later launches from other streams wait for them
+    cudaError_t done() {
+        s_->stream = st_;
+        return cudaEventRecord(s_->last, st_);
+    }
+
+  private:
+    cudaStream_t st_;
+    DeviceSlot* s_ = nullptr;
+    std::unique_lock<std::mutex> lk_;
+    cudaError_t err_ = cudaSuccess;
+};
+}  // namespace
+
 // Launch layout: the planned (maximal) warps per block packs the most worlds per SM; when all worlds fit
 // in one partial wave, smaller blocks spread them over every SM instead (G1 f32, 1024 worlds: 147 blocks of
 // 7 warps instead of 64 blocks of 16, 1.62 -> 1.50 ms). Over several waves, flags bit 6 also balances the
 // waves (same wave count, fewer warps per block): a win for latency-bound models (G1 f32 at 4096 worlds:
 // 2 waves of 14 instead of 16, 3.03 -> 2.98 ms) and a loss for light ones (arm: +6 %), so the Python layer
 // sets it by model size.
+struct DeviceAttrs {
+    std::once_flag once;
+    int nsm = 0, smem_sm = 0;
+};
+static DeviceAttrs g_attrs[64];
+
 extern "C++" s3_layout balanced_layout(const s3_layout& l, int64_t nworld, int flags) {
-    static int dev_c = -1, nsm = 0, smem_sm = 0;
     int dev = 0;
     cudaGetDevice(&dev);
-    if (dev != dev_c) {
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
-        dev_c = dev;
-    }
+    DeviceAttrs& a = g_attrs[dev & 63];
+    std::call_once(a.once, [&] {
+        cudaDeviceGetAttribute(&a.nsm, cudaDevAttrMultiProcessorCount, dev);
+        cudaDeviceGetAttribute(&a.smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    });
+    const int nsm = a.nsm, smem_sm = a.smem_sm;
     s3_layout o = l;
     const int wmax = l.warps_per_block;
     if (nsm <= 0 || wmax <= 1 || nworld <= 0) return o;
@@ -2659,10 +2731,9 @@ int s3_env_step(const s3_model* m, const s3_data* d, const s3_layout* l, const s
         return fail(S3_ERR_ARG, "layout planned without the level-schedule scratch (flags bits 1-2): re-plan");
     if (t->order && d->nworld > INT32_MAX) return fail(S3_ERR_BOUNDS, "cost-ordered schedule needs < 2^31 worlds");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    // the physics stages read the model from constant memory (s3::c_s3m): upload it on this stream
-    if (cudaMemcpyToSymbolAsync(c_s3m, m, sizeof(s3_model), 0, cudaMemcpyHostToDevice,
-                                static_cast<cudaStream_t>(stream)) != cudaSuccess)
-        return fail(S3_ERR_CUDA, cudaGetErrorString(cudaGetLastError()));
+    // the physics stages read the model from constant memory (s3::c_s3m): take the slot on this stream
+    ModelSlot slot(m, st);
+    if (slot.error() != cudaSuccess) return fail(S3_ERR_CUDA, cudaGetErrorString(slot.error()));
     const s3_layout ll = balanced_layout(*l, d->nworld, m->flags);
     int wpb = ll.warps_per_block;
     unsigned grid = (unsigned)((d->nworld + wpb - 1) / wpb);
@@ -2683,6 +2754,7 @@ int s3_env_step(const s3_model* m, const s3_data* d, const s3_layout* l, const s
                                                              global_step);
     }
     if (e == cudaSuccess) e = cudaGetLastError();
+    if (e == cudaSuccess) e = slot.done();
     if (e != cudaSuccess) return fail(S3_ERR_CUDA, cudaGetErrorString(e));
     return S3_OK;
 }
@@ -2700,10 +2772,9 @@ int s3_step(const s3_model* m, const s3_data* d, const s3_layout* l, int32_t nsu
     if ((m->flags & 6) && l->off[O_CDOF] - l->off[O_CRB] < m->nv)
         return fail(S3_ERR_ARG, "layout planned without the level-schedule scratch (flags bits 1-2): re-plan");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    // the physics stages read the model from constant memory (s3::c_s3m): upload it on this stream
-    if (cudaMemcpyToSymbolAsync(c_s3m, m, sizeof(s3_model), 0, cudaMemcpyHostToDevice,
-                                static_cast<cudaStream_t>(stream)) != cudaSuccess)
-        return fail(S3_ERR_CUDA, cudaGetErrorString(cudaGetLastError()));
+    // the physics stages read the model from constant memory (s3::c_s3m): take the slot on this stream
+    ModelSlot slot(m, st);
+    if (slot.error() != cudaSuccess) return fail(S3_ERR_CUDA, cudaGetErrorString(slot.error()));
     const s3_layout ll = balanced_layout(*l, d->nworld, m->flags);
     int wpb = ll.warps_per_block;
     unsigned grid = (unsigned)((d->nworld + wpb - 1) / wpb);
@@ -2717,6 +2788,7 @@ int s3_step(const s3_model* m, const s3_data* d, const s3_layout* l, int32_t nsu
         if (e == cudaSuccess) step_kernel<float><<<grid, 32 * wpb, smem, st>>>(*m, *d, ll, nsub);
     }
     if (e == cudaSuccess) e = cudaGetLastError();
+    if (e == cudaSuccess) e = slot.done();
     if (e != cudaSuccess) return fail(S3_ERR_CUDA, cudaGetErrorString(e));
     return S3_OK;
 }

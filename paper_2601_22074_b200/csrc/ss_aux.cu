@@ -196,3 +196,76 @@ extern "C" int ss_actuator_eval(int32_t kind, const double* kp, const double* kd
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? 0 : aux_fail("ss_actuator_eval", e);
 }
+
+// ---------------------------------------------------------------------------
+// metrics.build_record's reductions (metrics.py:31-45) for one rank, packed
+// into one vector for the single per-log-interval all-reduce.
+// Value layout inside a block: [reward, ep_sums[0..T), nonfinite, hist[0..R)];
+// the integer trigger counts are copied by the last block.
+
+constexpr int kStatsBlock = 256;
+
+__global__ void __launch_bounds__(kStatsBlock) stats_pack_kernel(const __grid_constant__ ss_stats_args a) {
+    const int N = a.n_worlds, T = a.n_rewards, R = a.n_rows;
+    const int V = 2 + T + R;  // float-summed values per block
+    __shared__ double red[kStatsBlock / 32][SS_STATS_MAXV];
+    __shared__ bool last;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int v = 0; v < V; ++v) {
+        // each thread sums its strided worlds in index order, then a fixed
+        // shuffle tree per warp and a fixed warp order per block
+        double acc = 0.0;
+        for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < N; w += gridDim.x * blockDim.x) {
+            double x;
+            if (v == 0) x = a.reward[w];
+            else if (v <= T) x = a.ep_sums[(int64_t)(v - 1) * N + w];
+            else if (v == T + 1) x = a.nonfinite[w] ? 1.0 : 0.0;
+            else x = (a.terrain_rows[w] == (int64_t)(v - T - 2)) ? 1.0 : 0.0;
+            acc += x;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+        if (lane == 0) red[warp][v] = acc;
+    }
+    __syncthreads();
+    for (int v = threadIdx.x; v < V; v += blockDim.x) {
+        double acc = 0.0;
+        for (int k = 0; k < kStatsBlock / 32; ++k) acc += red[k][v];
+        a.partials[(int64_t)blockIdx.x * SS_STATS_MAXV + v] = acc;
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(a.ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    const int C = a.n_counts;
+    for (int v = threadIdx.x; v < V; v += blockDim.x) {
+        double acc = 0.0;
+        for (int b = 0; b < (int)gridDim.x; ++b) acc += ((volatile double*)a.partials)[(int64_t)b * SS_STATS_MAXV + v];
+        int o;
+        if (v == 0) o = 1;                    // sum(reward)
+        else if (v <= T) o = 1 + v;           // sum(ep_sums[v-1])
+        else if (v == T + 1) o = 2 + T + C + R;  // sum(nonfinite)
+        else o = 2 + T + C + (v - T - 2);     // histogram bin
+        a.out[o] = acc;
+    }
+    for (int c = threadIdx.x; c < C; c += blockDim.x) a.out[2 + T + c] = (double)a.trigger_counts[c];
+    if (threadIdx.x == 0) {
+        a.out[0] = (double)N;
+        *a.ticket = 0u;  // ready for the next launch on this stream
+    }
+}
+
+extern "C" int ss_stats_pack(const ss_stats_args* a, void* stream) {
+    if (!a || a->n_worlds <= 0) return 0;
+    if (2 + a->n_rewards + a->n_rows > SS_STATS_MAXV) {
+        ss_set_error("ss_stats_pack", "too many statistics for SS_STATS_MAXV");
+        return -5;
+    }
+    int grid = (a->n_worlds + kStatsBlock - 1) / kStatsBlock;
+    if (grid > SS_STATS_GRID) grid = SS_STATS_GRID;
+    stats_pack_kernel<<<grid, kStatsBlock, 0, (cudaStream_t)stream>>>(*a);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? 0 : aux_fail("ss_stats_pack", e);
+}

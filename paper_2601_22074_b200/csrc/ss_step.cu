@@ -57,6 +57,7 @@ extern "C" size_t ss_sizeof(int which) {
         case 2: return sizeof(ss_rng_draw_args);
         case 3: return sizeof(ss_rt_state);
         case 4: return sizeof(ss_launch);
+        case 5: return sizeof(ss_stats_args);
         default: return 0;
     }
 }

@@ -69,10 +69,68 @@ def unpack_stats(vec, term_names, count_names, n_rows: int, step: int, steps_per
                          nonfinite_worlds=int(round(v[2 + t + c + n_rows])))
 
 
+class StatsPacker:
+    """The CUDA env's per-rank statistics in ONE kernel launch (``ss_stats_pack``,
+    csrc/ss_aux.cu): reads the step's reward, the episodic sums, trigger
+    counts, terrain rows and the nonfinite mask straight from the env's device
+    buffers and writes the packed vector ``pack_stats`` would build (same
+    layout), deterministically. Buffers are allocated once per env."""
+
+    def __init__(self, env):
+        import torch
+
+        from . import native
+
+        self.env = env
+        rm, tm = env.reward_manager, env.termination_manager
+        self.n_rewards = len(rm.terms)
+        self.n_counts = int(tm._counts.numel())
+        self.n_rows = int(env.terrain.rows)
+        dev = env.device
+        self.out = torch.zeros(3 + self.n_rewards + self.n_counts + self.n_rows, dtype=torch.float64, device=dev)
+        self.partials = torch.zeros(native.SS_STATS_GRID * native.SS_STATS_MAXV, dtype=torch.float64, device=dev)
+        self.ticket = torch.zeros(1, dtype=torch.int32, device=dev)
+        self._args = native.StatsArgs()
+        self._lib = native.lib()
+
+    def pack(self, reward=None):
+        """Launch the reduction on the current stream; returns the (device) vector."""
+        import ctypes
+
+        from . import native
+
+        env = self.env
+        rm, tm = env.reward_manager, env.termination_manager
+        reward = rm.reward if reward is None else reward
+        a = self._args
+        a.n_worlds, a.n_rewards, a.n_counts, a.n_rows = env.num_envs, self.n_rewards, self.n_counts, self.n_rows
+        a.reward = reward.data_ptr()
+        a.ep_sums = rm._sums.data_ptr() if self.n_rewards else None  # one SoA block (T, N)
+        a.trigger_counts = tm._counts.data_ptr()
+        a.terrain_rows = env.terrain_rows.data_ptr()
+        a.nonfinite = tm.last_nonfinite.data_ptr()
+        a.partials = self.partials.data_ptr()
+        a.ticket = self.ticket.data_ptr()
+        a.out = self.out.data_ptr()
+        native.LAUNCHES["count"] += 1
+        rc = self._lib.ss_stats_pack(ctypes.byref(a), native.current_stream(env._dev_index))
+        if rc != 0:
+            raise native.NativeError(f"ss_stats_pack failed ({rc}): {self._lib.ss_last_error().decode()}")
+        return self.out
+
+
 def build_record(env, step: int, reward, steps_per_sec: float | None, group=None) -> MetricsRecord:
+    """One JSONL record of the job (metrics.py:31-45): this rank's statistics
+    packed on the device, ONE all-reduce across ranks, unpacked on the host."""
     rm, tm = env.reward_manager, env.termination_manager
-    vec = pack_stats(reward, [rm.episodic_sums[k] for k in rm.terms], tm._counts, env.terrain_rows,
-                     env.terrain.rows, tm.last_nonfinite)
+    if getattr(env, "_lib", None) is not None and reward.is_cuda:
+        packer = getattr(env, "_stats_packer", None)
+        if packer is None:
+            packer = env._stats_packer = StatsPacker(env)
+        vec = packer.pack(reward)
+    else:
+        vec = pack_stats(reward, [rm.episodic_sums[k] for k in rm.terms], tm._counts, env.terrain_rows,
+                         env.terrain.rows, tm.last_nonfinite)
     vec = allreduce_stats(vec, group)
     return unpack_stats(vec, list(rm.terms), list(tm.trigger_counts), env.terrain.rows, step, steps_per_sec)
 
@@ -90,5 +148,6 @@ class MetricsWriter:
         self._fh.close()
 
 
-__all__ = ["MetricsRecord", "MetricsWriter", "allreduce_stats", "build_record", "pack_stats", "unpack_stats"]
+__all__ = ["MetricsRecord", "MetricsWriter", "StatsPacker", "allreduce_stats", "build_record", "pack_stats",
+           "unpack_stats"]
 _ = np

@@ -102,6 +102,7 @@ RngDrawArgs = _TYPES["ss_rng_draw_args"]
 Terrain = _TYPES["ss_terrain"]
 RtState = _TYPES["ss_rt_state"]
 Launch = _TYPES["ss_launch"]
+StatsArgs = _TYPES["ss_stats_args"]
 
 DCAPS = ("JOINTS", "FEET", "ACTION_TERMS", "ACTUATORS", "CMD", "RAYS", "GROUPS", "OBS_TERMS", "REWARDS",
          "TERMINATIONS", "EVENTS", "CURRICULUM", "FIELDS", "SLOTS", "MLP_LAYERS")
@@ -190,6 +191,7 @@ _SIGNATURES = {
     "ss_pipe_pre": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
     "ss_pipe_post": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
     "ss_pipe_wait": ([ctypes.c_void_p], ctypes.c_int),
+    "ss_stats_pack": ([ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
     "ss_actuator_eval": (
         [ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double, ctypes.c_double, ctypes.c_double,
          ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p],
@@ -215,7 +217,7 @@ def lib():
             fn.restype = res
         if so.ss_abi_version() != SS_ABI_VERSION:  # noqa: F821
             raise NativeError("stale extension: ABI version mismatch, rebuild it")
-        for which, cls in ((0, EnvDesc), (1, Uniforms), (2, RngDrawArgs), (3, RtState), (4, Launch)):
+        for which, cls in ((0, EnvDesc), (1, Uniforms), (2, RngDrawArgs), (3, RtState), (4, Launch), (5, StatsArgs)):
             if so.ss_sizeof(which) != ctypes.sizeof(cls):
                 raise NativeError(
                     f"struct layout mismatch for {cls.__name__}: C {so.ss_sizeof(which)} vs "

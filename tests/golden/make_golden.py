@@ -212,7 +212,42 @@ def rng_cases():
     return out
 
 
+def capture_cases():
+    """SSCAPT v1 dumps written by the reference itself (capture.py:81-104):
+    the replay case of tests/test_env.py:182-213 (Velocity-Flat, 2 worlds,
+    seed 5, six zero-action steps, env.dump_capture) and an automatic
+    nonfinite dump (env.py:240-241, :276-298) of a Velocity-Rough run whose
+    world 1 gets an infinite velocity after three random-policy steps."""
+    import shutil
+    import tempfile
+
+    cfg = make_env_cfg("Velocity-Flat", num_envs=2, seed=5)
+    env = ManagerBasedRlEnv(cfg, "Velocity-Flat")
+    env.reset()
+    for _ in range(6):
+        env.step(np.zeros((2, 4)))
+    env.dump_capture(os.path.join(OUT, "capture_flat.bin"))
+
+    tmp = tempfile.mkdtemp()
+    cfg = make_env_cfg("Velocity-Rough", num_envs=3, seed=9)
+    cfg.capture_len = 10
+    cfg.capture_dir = tmp
+    env = ManagerBasedRlEnv(cfg, "Velocity-Rough")
+    env.reset()
+    for i in range(3):
+        env.step(random_policy(env, i))
+    env.state.qd[1, 0] = np.inf
+    env.step(random_policy(env, 3))
+    assert len(env.dump_paths) == 1
+    shutil.copy(env.dump_paths[0], os.path.join(OUT, "capture_nan.bin"))
+    shutil.rmtree(tmp)
+
+
 def main():
+    if "--only-capture" in sys.argv:
+        capture_cases()
+        return
+    capture_cases()
     t = generate_grid(make_env_cfg("Velocity-Rough").scene.terrain, 0)
     np.savez_compressed(os.path.join(OUT, "terrain_rough_seed0.npz"), samples=t.samples,
                         difficulty=t.difficulty, type_index=t.type_index)

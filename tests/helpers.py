@@ -45,16 +45,26 @@ def two_leg_spec() -> C.ModelSpec:
     return C.ModelSpec(name="biped", joints=joints, feet=[1, 3])
 
 
-def sync_from_oracle(env, ref):
+def sync_from_oracle(env, ref, world_start=None):
     """Teacher forcing: copy every floating-point state array of the oracle env
     into the GPU env (discrete state -- counters, RNG counters, flags -- evolves
     identically on both sides as long as the flags match, which the tests
-    assert). After this the next step starts from bit-identical state."""
+    assert). After this the next step starts from bit-identical state.
+
+    With ``world_start`` the oracle holds only worlds [world_start,
+    world_start + ref.n) of the GPU env (built with world_id_offset =
+    world_start, partition-independent per SPEC.md:113): every array is
+    written into that slice of its world axis."""
     import torch
 
     dev = env.device
+    N = env.num_envs
 
     def put(dst, src):
+        if world_start is not None:
+            axes = [i for i, s in enumerate(dst.shape) if s == N]
+            assert len(axes) == 1, (tuple(dst.shape), N)
+            dst = dst.narrow(axes[0], world_start, ref.n)
         dst.copy_(torch.as_tensor(np.array(src, copy=True), device=dev).to(dst.dtype).reshape(dst.shape))
 
     S = ref.S
@@ -96,7 +106,10 @@ def sync_from_oracle(env, ref):
         f = env.model.field(name)
         v = ref.m.fields[name][0]
         if f.expanded:
-            put(f.value, np.broadcast_to(v, tuple(f.value.shape)))
+            shape = tuple(f.value.shape)
+            if world_start is not None:
+                shape = tuple(ref.n if s == N else s for s in shape)
+            put(f.value, np.broadcast_to(v, shape))
     for k, el in ref.ev_elapsed.items():
         put(env.event_manager._elapsed[k], el)
         put(env.event_manager._target[k], ref.ev_target[k])

@@ -479,3 +479,47 @@ def test_metrics_record_one_allreduce():
     assert abs(rec.reward_mean - float(env.reward.mean())) < 1e-9  # the record rounds to 10 decimals
     assert sum(rec.terrain_row_histogram) == 8
     assert rec.termination_counts["terminated"] + rec.termination_counts["truncated"] >= 0
+
+
+@pytest.mark.gpu
+def test_models_on_two_streams_match_sequential():
+    """Two different models (G1 float64, Go1 float32) stepped from two CUDA streams, interleaved without
+    any user synchronization, give bit-identical results to stepping each alone on the default stream:
+    the library serializes its constant-memory model slot across streams (s3_kernel.cu ModelSlot)."""
+    import torch
+
+    from paper_2601_22074_b200.sim3d.task import VelocityEnv3D
+
+    def make(name, dtype):
+        mk, table, kw = CASES[name]
+        m = mk()
+        return VelocityEnv3D(m, VelocityTaskCfg(default_qpos=robots.default_qpos(m, table), **kw), 256, seed=3,
+                             dtype=dtype)
+
+    steps = 6
+    rng = np.random.default_rng(1)
+    acts = {k: [torch.as_tensor(rng.uniform(-1, 1, size=(256, nu)), device="cuda") for _ in range(steps)]
+            for k, nu in (("g1", make("g1_flat", "f64").model.nu), ("go1", make("go1_flat", "f32").model.nu))}
+    solo = {}
+    for key, name, dtype in (("g1", "g1_flat", "f64"), ("go1", "go1_flat", "f32")):
+        env = make(name, dtype)
+        env.reset()
+        for a in acts[key]:
+            env.step(a.to(env.dm.tdtype))
+        torch.cuda.synchronize()
+        solo[key] = (env.data.qpos.clone(), env.data.qvel.clone())
+    e1, e2 = make("g1_flat", "f64"), make("go1_flat", "f32")
+    torch.cuda.synchronize()  # construction ran on the default stream
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    with torch.cuda.stream(s1):
+        e1.reset()
+    with torch.cuda.stream(s2):
+        e2.reset()
+    for i in range(steps):
+        with torch.cuda.stream(s1):
+            e1.step(acts["g1"][i].to(e1.dm.tdtype))
+        with torch.cuda.stream(s2):
+            e2.step(acts["go1"][i].to(e2.dm.tdtype))
+    torch.cuda.synchronize()
+    assert torch.equal(e1.data.qpos, solo["g1"][0]) and torch.equal(e1.data.qvel, solo["g1"][1])
+    assert torch.equal(e2.data.qpos, solo["go1"][0]) and torch.equal(e2.data.qvel, solo["go1"][1])

@@ -82,3 +82,47 @@ def test_two_rank_shards_equal_single_process(tmp_path):
     assert multi["reward_mean"] == pytest.approx(single.reward_mean, abs=1e-9)
     for k, v in single.reward_terms.items():
         assert multi["reward_terms"][k] == pytest.approx(v, abs=1e-9)
+
+
+def test_bench_self_launch_two_ranks_dry(tmp_path):
+    """`bench.py --gpus 2` with no WORLD_SIZE starts 2 ranks itself (torch.distributed.run on 127.0.0.1);
+    --dry-cpu runs the same shard / reduce plumbing on gloo + the oracle. The line must report 2 ranks,
+    disjoint contiguous shards, and the reduced record of a single 2N-world run."""
+    import json
+    import subprocess
+    import sys
+
+    from oracle import OracleEnv
+    from paper_2601_22074_b200.metrics import pack_stats, unpack_stats
+    from paper_2601_22074_b200.tasks import make_env_cfg
+    from paper_2601_22074_b200.terrain import generate_grid
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env_vars = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    n, steps, warmup = 20, 5, 3
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--dry-cpu", "--envs", str(n),
+                          "--steps", str(steps), "--warmup", str(warmup)], capture_output=True, text=True,
+                         timeout=600, env=env_vars, cwd=str(tmp_path))
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout  # rank 0 alone prints
+    got = json.loads(lines[0])
+    assert got["n_gpus"] == 2
+    assert got["shards"]["world_id_offsets"] == [0, n]
+    assert got["config"]["total_envs"] == 2 * n
+    cfg = make_env_cfg("Velocity-Rough", num_envs=2 * n, seed=0)
+    env = OracleEnv(cfg, generate_grid(cfg.scene.terrain, cfg.seed).samples)
+    env.reset()
+    for _ in range(steps + warmup):
+        _, rew, *_ = env.step(env.random_actions())
+    vec = pack_stats(torch.from_numpy(rew), [torch.from_numpy(env.ep_sums[k]) for k in env.rw],
+                     torch.tensor(list(env.trigger_counts.values())), torch.from_numpy(env.terrain_rows),
+                     env.t_rows, torch.from_numpy(env.last_nonfinite))
+    single = unpack_stats(vec, list(env.rw), list(env.trigger_counts), env.t_rows, steps + warmup)
+    rec = got["record"]
+    assert rec["termination_counts"] == single.termination_counts
+    assert rec["terrain_row_histogram"] == single.terrain_row_histogram
+    assert rec["nonfinite_worlds"] == single.nonfinite_worlds
+    assert rec["reward_mean"] == pytest.approx(single.reward_mean, abs=1e-9)
+    for k, v in single.reward_terms.items():
+        assert rec["reward_terms"][k] == pytest.approx(v, abs=1e-9)
