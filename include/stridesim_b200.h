@@ -692,10 +692,12 @@ int ss_rt_release(ss_rt_state* st);
 /* Pipelined host I/O for env.step_async / env.step_wait (gym VectorEnv style), nslot in [2, 4] slots:
  * ss_pipe_pre copies a step's actions from pinned host memory into the slot's device buffer on a
  * copy stream (the launching stream waits for it) and returns the slot; ss_pipe_post snapshots the
- * output arena into the slot's staging buffer (SM copy kernel) and copies it to the slot's pinned
- * host block on a second copy stream, so the PCIe transfers of one step overlap the kernel of the
- * next; ss_pipe_wait blocks until the oldest pending step's results are in host memory and returns
- * its slot. Buffers are owned by the caller (16-byte aligned). */
+ * output arena into the slot's staging buffer (SM copy kernel) and copies it to a pinned host block
+ * on a second copy stream, so the PCIe transfers of one step overlap the kernel of the next;
+ * ss_pipe_wait blocks until the oldest pending step's results are in host memory and returns the
+ * index of its host block. `host` holds nslot + 1 blocks used round-robin: the block step_wait
+ * returned is not written again before the following ss_pipe_wait call. Buffers are owned by the
+ * caller (16-byte aligned). */
 int ss_pipe_create(int32_t nslot, void* const* dev_actions, void* const* stage, void* const* host,
                    int64_t action_bytes, int64_t arena_bytes, void** out);
 int ss_pipe_destroy(void* pipe);

@@ -177,7 +177,7 @@ struct Pipe {
     int64_t submitted = 0, waited = 0;
     void* dev_actions[4] = {};
     void* stage[4] = {};
-    void* host[4] = {};
+    void* host[5] = {};  // nslot + 1 pinned blocks: a view step_wait returned survives the next step_async
     int64_t action_bytes = 0, arena_bytes = 0;
 };
 
@@ -204,8 +204,8 @@ extern "C" int ss_pipe_create(int32_t nslot, void* const* dev_actions, void* con
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->out_done[k], cudaEventDisableTiming);
         p->dev_actions[k] = dev_actions[k];
         p->stage[k] = stage[k];
-        p->host[k] = host[k];
     }
+    for (int k = 0; k <= nslot; ++k) p->host[k] = host[k];
     if (e != cudaSuccess) {
         delete p;
         return pipe_err(e, "ss_pipe_create");
@@ -278,8 +278,11 @@ extern "C" int ss_pipe_post(void* h, const void* arena, void* main_stream) {
     if (e == cudaSuccess) e = cudaEventRecord(p->snap[k], main);
     // (one stream: splitting the D2H over two copy-engine streams measured no faster, 36.4 vs 34.0 us/step)
     if (e == cudaSuccess) e = cudaStreamWaitEvent(p->out, p->snap[k], 0);
+    // host blocks rotate over nslot + 1: the block of step i is rewritten by step i + nslot + 1, which
+    // cannot be submitted before step i + 1 has been waited for
+    const int hk = (int)(p->submitted % (p->nslot + 1));
     if (e == cudaSuccess)
-        e = cudaMemcpyAsync(p->host[k], p->stage[k], (size_t)p->arena_bytes, cudaMemcpyDeviceToHost, p->out);
+        e = cudaMemcpyAsync(p->host[hk], p->stage[k], (size_t)p->arena_bytes, cudaMemcpyDeviceToHost, p->out);
     if (e == cudaSuccess) e = cudaEventRecord(p->out_done[k], p->out);
     if (e != cudaSuccess) return pipe_err(e, "ss_pipe_post");
     p->used[k] = true;
@@ -287,7 +290,8 @@ extern "C" int ss_pipe_post(void* h, const void* arena, void* main_stream) {
     return k;
 }
 
-// Block until the oldest pending step's results are in host memory; returns its slot.
+// Block until the oldest pending step's results are in host memory; returns its host block index
+// (0..nslot; the block stays untouched until step_wait is called again).
 extern "C" int ss_pipe_wait(void* h) {
     Pipe* p = static_cast<Pipe*>(h);
     if (p->waited >= p->submitted) {
@@ -295,8 +299,9 @@ extern "C" int ss_pipe_wait(void* h) {
         return -1;
     }
     const int k = (int)(p->waited % p->nslot);
+    const int hk = (int)(p->waited % (p->nslot + 1));
     cudaError_t e = cudaEventSynchronize(p->out_done[k]);
     if (e != cudaSuccess) return pipe_err(e, "ss_pipe_wait");
     p->waited += 1;
-    return k;
+    return hk;
 }

@@ -94,10 +94,14 @@ class _Extras(Mapping):
 
 
 class ManagerBasedRlEnv:
-    def __init__(self, cfg: EnvCfg, task_id: str = "", device=None):
+    def __init__(self, cfg: EnvCfg, task_id: str = "", device=None, copy_outputs: bool = False):
+        """``copy_outputs=True`` makes ``step``/``reset`` return FRESH tensors every call, like the
+        reference's fresh numpy arrays (one device copy of the output arena per step); by default they
+        are views of persistent device buffers that the next step overwrites (mjlab's convention)."""
         import torch
 
         self.cfg = cfg
+        self.copy_outputs = bool(copy_outputs)
         self.task_id = task_id
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
         spec = cfg.scene.model
@@ -492,6 +496,8 @@ class ManagerBasedRlEnv:
             mask = om.begin(list(om.groups))
             self._launch(native.SS_ST_RESET_ALL | native.SS_ST_PREV_BEFORE | native.SS_ST_OBS, groups_mask=mask)
         self.ray_scanner._cached_step = -1
+        if self.copy_outputs:
+            return {g: t.clone() for g, t in om.outputs().items()}
         return om.outputs()
 
     # -- step -------------------------------------------------------------------------------
@@ -503,6 +509,10 @@ class ManagerBasedRlEnv:
         tensors, valid until the next step."""
         self._step_checked(self.action_manager.check_actions(actions))
         tm = self.termination_manager
+        if self.copy_outputs:
+            v = self.unpack_outputs(self.step_outputs.clone())  # one D2D copy of the whole arena
+            obs = {g: v[f"obs/{g}"] for g in self.observation_manager.outputs()}
+            return obs, v["reward"], v["terminated"], v["truncated"], _Extras(self, self.global_step)
         return (self.observation_manager.outputs(), self.reward_manager.reward, tm.terminated, tm.truncated,
                 _Extras(self, self.global_step))
 
@@ -552,10 +562,11 @@ class ManagerBasedRlEnv:
             S = PIPE_SLOTS
             dev_actions = [torch.empty((self.num_envs, A), dtype=torch.float64, device=self.device) for _ in range(S)]
             stage = [torch.empty(nb, dtype=torch.uint8, device=self.device) for _ in range(S)]
-            host = [torch.empty(nb, dtype=torch.uint8).pin_memory() for _ in range(S)]
+            host = [torch.empty(nb, dtype=torch.uint8).pin_memory() for _ in range(S + 1)]
             arr = lambda ts: (ctypes.c_void_p * S)(*[t.data_ptr() for t in ts])  # noqa: E731
             h = ctypes.c_void_p()
-            rc = self._lib.ss_pipe_create(S, arr(dev_actions), arr(stage), arr(host), self.num_envs * A * 8, nb,
+            hosts = (ctypes.c_void_p * (S + 1))(*[t.data_ptr() for t in host])
+            rc = self._lib.ss_pipe_create(S, arr(dev_actions), arr(stage), hosts, self.num_envs * A * 8, nb,
                                           ctypes.byref(h))
             if rc != 0:
                 raise native.NativeError(f"ss_pipe_create failed: {self._lib.ss_last_error().decode()}")

@@ -242,34 +242,58 @@ _MODULES: dict[str, int] = {}
 STATS = {"compiled": 0, "disk_hits": 0, "memory_hits": 0}
 
 
+def _store_cubin(path: str, cubin: bytes) -> None:
+    """Atomically publish a cubin: a private temp file (mkstemp), fsync, rename (ranks of one node may
+    share the cache directory; a reader sees the old file or the complete new one)."""
+    import tempfile
+
+    try:
+        os.makedirs(os.path.dirname(path), exist_ok=True)
+        fd, tmp = tempfile.mkstemp(dir=os.path.dirname(path), prefix=".cubin.")
+        try:
+            with os.fdopen(fd, "wb") as fh:
+                fh.write(cubin)
+                fh.flush()
+                os.fsync(fh.fileno())
+            os.replace(tmp, path)
+        except BaseException:
+            os.unlink(tmp)
+            raise
+    except OSError:
+        pass
+
+
+def _load(cubin: bytes, d) -> int:
+    handle = ctypes.c_void_p()
+    native.call("ss_jit_load", cubin, len(cubin), KERNEL.encode(), block_size(), ctypes.byref(handle))
+    native.call("ss_jit_set_desc_bytes", handle, ctypes.sizeof(native.packed_desc_type(desc_caps(d))))
+    return handle.value
+
+
 def module_for(d) -> int:
-    """Loaded kernel handle specialized for descriptor ``d`` (compiled on first use)."""
+    """Loaded kernel handle specialized for descriptor ``d`` on the current device (compiled on first use)."""
+    import torch
+
     src = kernel_source(d)
     key = hashlib.sha256((src + "|".join(options()) + "".join(open(p).read() for p in _HEADERS.values())).encode()).hexdigest()
-    h = _MODULES.get(key)
+    mkey = f"{key}@{torch.cuda.current_device()}"  # a module is loaded into one device's context
+    h = _MODULES.get(mkey)
     if h is not None:
         STATS["memory_hits"] += 1
         return h
     path = os.path.join(_cache_dir(), key + ".cubin")
-    cubin = None
+    handle = None
     try:
         with open(path, "rb") as fh:
             cubin = fh.read()
+        handle = _load(cubin, d)
         STATS["disk_hits"] += 1
-    except OSError:
-        pass
-    if cubin is None:
+    except (OSError, native.NativeError):
+        handle = None  # absent or unloadable (e.g. truncated by a crashed writer): recompile
+    if handle is None:
         cubin = compile_cubin(src)
         STATS["compiled"] += 1
-        try:
-            os.makedirs(os.path.dirname(path), exist_ok=True)
-            with open(path + ".tmp", "wb") as fh:
-                fh.write(cubin)
-            os.replace(path + ".tmp", path)
-        except OSError:
-            pass
-    handle = ctypes.c_void_p()
-    native.call("ss_jit_load", cubin, len(cubin), KERNEL.encode(), block_size(), ctypes.byref(handle))
-    native.call("ss_jit_set_desc_bytes", handle, ctypes.sizeof(native.packed_desc_type(desc_caps(d))))
-    _MODULES[key] = handle.value
-    return handle.value
+        _store_cubin(path, cubin)
+        handle = _load(cubin, d)
+    _MODULES[mkey] = handle
+    return handle

@@ -119,6 +119,19 @@ def gae(rewards, values, dones, last_value, gamma: float, lam: float):
     return adv, adv + values
 
 
+def normalize_advantages(adv, group=None):
+    """(adv - mean) / std with the mean and variance of the WHOLE job: data-parallel ranks all-reduce
+    [sum, sum of squares, count] (one 3-float collective) so every rank normalizes identically."""
+    st = torch.stack([adv.sum(), (adv * adv).sum(), torch.tensor(float(adv.numel()), device=adv.device)])
+    st = st.double()
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(st, op=dist.ReduceOp.SUM, group=group)
+    n = st[2]
+    mean = st[0] / n
+    var = (st[1] - n * mean * mean) / (n - 1).clamp(min=1.0)  # unbiased, like torch.std
+    return ((adv.double() - mean) / (var.clamp(min=0.0).sqrt() + 1e-8)).to(adv.dtype)
+
+
 def ppo_loss(model: ActorCritic, cfg: PpoCfg, obs_p, obs_c, actions, old_logp, adv, ret):
     d = model.dist(obs_p)
     logp = d.log_prob(actions).sum(-1)
@@ -175,7 +188,10 @@ class PpoTrainer:
             b["logp"][t] = d.log_prob(a).sum(-1)
             b["val"][t] = self.model.value(c)
             self.obs, rew, term, trunc, _ = env.step(a.double())
-            b["rew"][t] = rew.float()
+            # episode boundary for GAE; a time-limit truncation is not a terminal state, so its reward
+            # bootstraps gamma * V (the value of the state the last action was taken in, the pre-reset
+            # estimate available once the env has auto-reset; rsl_rl's time_outs treatment)
+            b["rew"][t] = rew.float() + self.cfg.gamma * b["val"][t] * (trunc & ~term).float()
             b["done"][t] = (term | trunc).float()
 
     def update(self) -> dict:
@@ -183,7 +199,7 @@ class PpoTrainer:
         with torch.no_grad():
             _, c = self._split(self.obs)
             adv, ret = gae(b["rew"], b["val"], b["done"], self.model.value(c), cfg.gamma, cfg.lam)
-            adv = (adv - adv.mean()) / (adv.std() + 1e-8)
+            adv = normalize_advantages(adv, self.reducer.group)
         T, n = b["rew"].shape
         flat = {k: v.reshape(T * n, *v.shape[2:]) for k, v in b.items()}
         adv, ret = adv.reshape(-1), ret.reshape(-1)

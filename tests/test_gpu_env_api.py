@@ -821,3 +821,60 @@ def test_step_async_delivers_each_steps_results_to_host():
     assert torch.equal(expected[-1][1], b.step_wait()["reward"])
     with pytest.raises(RuntimeError):
         b.step_wait()
+
+
+@pytest.mark.gpu
+def test_step_wait_view_survives_the_next_step_async():
+    """With the pipeline full (PIPE_SLOTS steps pending), the host view step_wait returned is not
+    overwritten by the following step_async (nslot + 1 host blocks, ss_pipe_*)."""
+    from paper_2601_22074_b200.env import PIPE_SLOTS, ManagerBasedRlEnv
+    from paper_2601_22074_b200.tasks import make_env_cfg
+
+    a = ManagerBasedRlEnv(make_env_cfg("Velocity-Rough", num_envs=256, seed=2))
+    b = ManagerBasedRlEnv(make_env_cfg("Velocity-Rough", num_envs=256, seed=2))
+    a.reset()
+    b.reset()
+    rng = np.random.default_rng(8)
+    acts = [torch.from_numpy(rng.uniform(-1, 1, size=(256, a.action_manager.total_dim))).pin_memory()
+            for _ in range(PIPE_SLOTS + 6)]
+    want = []
+    for x in acts:
+        _, r, _, _, _ = a.step(x.cuda())
+        want.append(r.cpu().clone())
+    for i in range(PIPE_SLOTS):
+        b.step_async(acts[i])
+    for i in range(PIPE_SLOTS, len(acts)):
+        view = b.step_wait()  # step i - PIPE_SLOTS
+        b.step_async(acts[i])  # the pipeline is full again
+        torch.cuda.synchronize()  # every copy issued so far has landed
+        assert torch.equal(view["reward"], want[i - PIPE_SLOTS]), i
+    for i in range(len(acts) - PIPE_SLOTS, len(acts)):
+        assert torch.equal(b.step_wait()["reward"], want[i])
+
+
+@pytest.mark.gpu
+def test_copy_outputs_returns_fresh_tensors():
+    """copy_outputs=True: every step returns new tensors (the reference returns fresh arrays), equal to
+    the persistent buffers of that step; the default mode returns views the next step overwrites."""
+    from paper_2601_22074_b200.env import ManagerBasedRlEnv
+    from paper_2601_22074_b200.policies import random_policy
+    from paper_2601_22074_b200.tasks import make_env_cfg
+
+    fresh = ManagerBasedRlEnv(make_env_cfg("Velocity-Rough", num_envs=128, seed=4), copy_outputs=True)
+    views = ManagerBasedRlEnv(make_env_cfg("Velocity-Rough", num_envs=128, seed=4))
+    o0 = fresh.reset()
+    views.reset()
+    kept, first = [], None
+    for i in range(5):
+        o, r, te, tr, _ = fresh.step(random_policy(fresh, i))
+        ov, rv, tev, trv, _ = views.step(random_policy(views, i))
+        assert torch.equal(r, rv) and torch.equal(te, tev) and torch.equal(tr, trv)
+        for g in o:
+            assert torch.equal(o[g], ov[g])
+        kept.append((o["policy"].clone(), r.clone(), o, r))
+        if first is None:
+            first = rv
+    for snap_o, snap_r, o, r in kept:  # earlier steps' tensors were not overwritten
+        assert torch.equal(o["policy"], snap_o) and torch.equal(r, snap_r)
+    assert first.data_ptr() == views.reward_manager.reward.data_ptr()  # default: persistent buffer
+    assert o0["policy"].data_ptr() != fresh.observation_manager.outputs()["policy"].data_ptr()

@@ -78,3 +78,33 @@ def test_gae_matches_scalar_recurrence():
             last = delta + 0.99 * 0.95 * (1 - d[t, j]) * last
             assert abs(float(adv[t, j]) - float(last)) < 1e-5
     assert torch.allclose(ret, adv + v)
+
+
+def test_advantage_normalization_single_rank_matches_torch():
+    from paper_2601_22074_b200.ppo import normalize_advantages
+
+    a = torch.randn(64, 8, generator=torch.Generator().manual_seed(2))
+    want = (a - a.mean()) / (a.std() + 1e-8)
+    assert torch.allclose(normalize_advantages(a), want, atol=1e-6)
+
+
+def _norm_worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2601_22074_b200.ppo import normalize_advantages
+
+    full = torch.randn(32, 6, generator=torch.Generator().manual_seed(5))
+    mine = full[rank * 16 : (rank + 1) * 16]
+    torch.save(normalize_advantages(mine), os.path.join(out, f"n{rank}.pt"))
+    dist.destroy_process_group()
+
+
+def test_advantage_normalization_uses_job_statistics(tmp_path):
+    """Two ranks normalize their halves with the job-wide mean/std: identical to normalizing the whole batch."""
+    from paper_2601_22074_b200.ppo import normalize_advantages
+
+    tmp.spawn(_norm_worker, args=(2, _port(), str(tmp_path)), nprocs=2, join=True)
+    full = torch.randn(32, 6, generator=torch.Generator().manual_seed(5))
+    got = torch.cat([torch.load(tmp_path / "n0.pt"), torch.load(tmp_path / "n1.pt")])
+    assert torch.allclose(got, normalize_advantages(full), atol=1e-6)
