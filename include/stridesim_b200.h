@@ -678,6 +678,8 @@ int ss_env_step_jit(void* handle, const ss_env_desc* desc, const ss_uniforms* u,
  * declare its size once, then launch with the full descriptor (validated)
  * plus the packed copy that becomes the kernel parameter block. */
 int ss_jit_set_desc_bytes(void* handle, int64_t bytes);
+/* Dynamic shared memory per block of a module whose staging buffers exceed the static 48 KB. */
+int ss_jit_set_smem(void* handle, int32_t bytes);
 int ss_env_step_jit_packed(void* handle, const ss_env_desc* desc, const void* packed, int64_t packed_bytes,
                            const ss_uniforms* u, void* stream);
 /* Runtime: derive the uniforms from *st, launch (JIT module when jit != NULL,

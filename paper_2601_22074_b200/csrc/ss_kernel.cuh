@@ -29,6 +29,9 @@
 #ifndef SS_MIRROR_TMA
 #define SS_MIRROR_TMA 1
 #endif
+#ifndef SS_DCAP_ACTION_COLS
+#define SS_DCAP_ACTION_COLS 1  /* action columns in shared memory (JIT: the env's action dim) */
+#endif
 #ifndef SS_PEEL_LAST_SUBSTEP
 #define SS_PEEL_LAST_SUBSTEP 0
 #endif
@@ -50,6 +53,20 @@ __device__ __forceinline__ T* mirror_of(const ss_env_desc& d, T* p) {
 // between steps, so every first touch of a per-world array is a DRAM trip;
 // prefetching at kernel entry turns the later dependent loads into L2 hits).
 __device__ __forceinline__ void l2_prefetch(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+// The arrays read after the substeps and on the reset path: pulled into L1
+// (SS_PF_L1=1) so their loads -- which sit behind the step's stores and its
+// branches, so the compiler cannot issue them early -- cost an L1 hit instead
+// of an L2 round trip each; SS_PF_L1=0 stops at L2.
+#ifndef SS_PF_L1
+#define SS_PF_L1 1
+#endif
+__device__ __forceinline__ void late_prefetch_line(const void* p) {
+#if SS_PF_L1
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+#else
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+#endif
+}
 
 template <int M>
 __device__ __forceinline__ double sel(const double (&a)[M], int j) {
@@ -163,7 +180,30 @@ __device__ __forceinline__ void height_raw_n(const ss_env_desc& d, const double 
     for (int r = 0; r < NR; ++r) out[r] = a[r] * (1.0 - frac[r]) + b[r] * frac[r];
 }
 
-template <int KM, int FM>
+// The action / previous-action vectors of a world: registers (S == 0), or
+// columns of stride S in shared memory (value k at p[k * S]; large models,
+// where the 2 x A doubles would otherwise stay live in registers all step).
+template <int S>
+struct ActArr {
+    double r[S ? 1 : SS_MAX_ACTION];
+    double* p;
+    __device__ __forceinline__ double& operator[](int k) {
+        if constexpr (S > 0) return p[k * S];
+        else return r[k];
+    }
+    __device__ __forceinline__ double operator[](int k) const {
+        if constexpr (S > 0) return p[k * S];
+        else return r[k];
+    }
+};
+
+template <int S>
+__device__ __forceinline__ double sel(const ActArr<S>& a, int j) {
+    if constexpr (S > 0) return a[j];
+    else return sel(a.r, j);
+}
+
+template <int KM, int FM, int AS = 0>
 struct World {
     double q[3 + KM], qd[3 + KM], ctrl[KM];
     double ext0, ext1, time;
@@ -176,7 +216,7 @@ struct World {
     double sp, cp;
     bool trig_ok;
     double targets[KM];
-    double action[SS_MAX_ACTION], prev_action[SS_MAX_ACTION];
+    ActArr<AS> action, prev_action;
     bool have_action;
     double cmd[SS_MAX_CMD];
     bool s_in[FM];
@@ -196,14 +236,47 @@ struct World {
     double plv0, plv1;
 };
 
-// model fields hoisted out of the substep loop (they cannot change within a launch)
-template <int KM>
+// model fields hoisted out of the substep loop (they cannot change within a launch).
+// S == 0: registers (generic build); S > 0: a shared-memory column per thread
+// (value v at p[v * S], the block's threads side by side, bank-conflict free)
+// -- the specialized kernel keeps these ~30 doubles out of its register file
+// (236 -> 208 registers for the rough biped), where they would otherwise stay
+// live through the whole substep loop.
+template <int KM, int NA, int S>
 struct Params {
-    double base_mass, base_inertia, friction;
-    double lm[KM], rot[KM], dmp[KM];
-    // stage_integrate's divisors (sim/physics.py:216-224), formed once per launch
-    double m_total, inv_m, inv_inertia, inv_rot[KM];
-    double kp[SS_MAX_ACTUATORS][KM], kd[SS_MAX_ACTUATORS][KM];
+    static constexpr int BM = 0, BI = 1, FR = 2, MT = 3, IM = 4, II = 5, LM = 6, ROT = 6 + KM, DMP = 6 + 2 * KM,
+                         IROT = 6 + 3 * KM, KP = 6 + 4 * KM, KD = KP + NA * KM, NV = KD + NA * KM;
+    double r[S ? 1 : NV];
+    double* p;
+    __device__ __forceinline__ double& v(int i) {
+        if constexpr (S > 0) return p[i * S];
+        else return r[i];
+    }
+    __device__ __forceinline__ double v(int i) const {
+        if constexpr (S > 0) return p[i * S];
+        else return r[i];
+    }
+    __device__ __forceinline__ double& base_mass() { return v(BM); }
+    __device__ __forceinline__ double& base_inertia() { return v(BI); }
+    __device__ __forceinline__ double& friction() { return v(FR); }
+    __device__ __forceinline__ double& m_total() { return v(MT); }
+    __device__ __forceinline__ double& inv_m() { return v(IM); }
+    __device__ __forceinline__ double& inv_inertia() { return v(II); }
+    __device__ __forceinline__ double& lm(int j) { return v(LM + j); }
+    __device__ __forceinline__ double& rot(int j) { return v(ROT + j); }
+    __device__ __forceinline__ double& dmp(int j) { return v(DMP + j); }
+    __device__ __forceinline__ double& inv_rot(int j) { return v(IROT + j); }
+    __device__ __forceinline__ double& kp(int a, int i) { return v(KP + a * KM + i); }
+    __device__ __forceinline__ double& kd(int a, int i) { return v(KD + a * KM + i); }
+    __device__ __forceinline__ double friction() const { return v(FR); }
+    __device__ __forceinline__ double m_total() const { return v(MT); }
+    __device__ __forceinline__ double inv_m() const { return v(IM); }
+    __device__ __forceinline__ double inv_inertia() const { return v(II); }
+    __device__ __forceinline__ double lm(int j) const { return v(LM + j); }
+    __device__ __forceinline__ double dmp(int j) const { return v(DMP + j); }
+    __device__ __forceinline__ double inv_rot(int j) const { return v(IROT + j); }
+    __device__ __forceinline__ double kp(int a, int i) const { return v(KP + a * KM + i); }
+    __device__ __forceinline__ double kd(int a, int i) const { return v(KD + a * KM + i); }
 };
 
 __device__ __forceinline__ uint64_t rng_begin(const ss_env_desc& d, int slot, int w, uint64_t& key) {
@@ -217,8 +290,8 @@ __device__ __forceinline__ void rng_end(const ss_env_desc& d, int slot, int w, u
 // ---------------------------------------------------------------------------
 // state load / store, entity refresh
 
-template <class C, int KM, int FM>
-__device__ __forceinline__ void load_phys(const ss_env_desc& d, int w, World<KM, FM>& s, bool load_cache) {
+template <class C, int KM, int FM, int AS>
+__device__ __forceinline__ void load_phys(const ss_env_desc& d, int w, World<KM, FM, AS>& s, bool load_cache) {
     const int N = C::NW(d), K = C::K(d), F = C::F(d);
 #pragma unroll
     for (int i = 0; i < 3 + KM; ++i) {
@@ -244,8 +317,8 @@ __device__ __forceinline__ void load_phys(const ss_env_desc& d, int w, World<KM,
     s.trig_ok = false;
 }
 
-template <class C, int KM, int FM>
-__device__ __forceinline__ void store_phys(const ss_env_desc& d, int w, const World<KM, FM>& s, bool store_cache) {
+template <class C, int KM, int FM, int AS>
+__device__ __forceinline__ void store_phys(const ss_env_desc& d, int w, const World<KM, FM, AS>& s, bool store_cache) {
     const int N = C::NW(d), K = C::K(d), F = C::F(d);
 #pragma unroll
     for (int i = 0; i < 3 + KM; ++i) {
@@ -276,9 +349,14 @@ __device__ __forceinline__ void store_phys(const ss_env_desc& d, int w, const Wo
     }
 }
 
+__device__ __forceinline__ double* dyn_smem() {
+    extern __shared__ __align__(16) double ss_dyn_smem[];
+    return ss_dyn_smem;
+}
+
 // EntityData.refresh (entity.py:145-165): a register snapshot
-template <int KM, int FM>
-__device__ __forceinline__ void refresh(World<KM, FM>& s) {
+template <int KM, int FM, int AS>
+__device__ __forceinline__ void refresh(World<KM, FM, AS>& s) {
     double sn, c;
     ss_sincos(s.q[2], &sn, &c);
     s.sp = sn;
@@ -305,23 +383,27 @@ __device__ __forceinline__ void refresh(World<KM, FM>& s) {
 // ---------------------------------------------------------------------------
 // StepPipeline.substep (sim/physics.py:178-249)
 
-template <class C, int KM>
-__device__ __forceinline__ void load_params(const ss_env_desc& d, int w, Params<KM>& P, bool actuators) {
+template <class C, int KM, class PP>
+__device__ __forceinline__ void load_params(const ss_env_desc& d, int w, PP& P, bool actuators) {
     const int K = C::K(d);
-    P.base_mass = fld<C>(d, C::f_base_mass(d), 0, w);
-    P.base_inertia = fld<C>(d, C::f_base_inertia(d), 0, w);
-    P.friction = fld<C>(d, C::f_friction(d), 0, w);
+    P.base_mass() = fld<C>(d, C::f_base_mass(d), 0, w);
+    P.base_inertia() = fld<C>(d, C::f_base_inertia(d), 0, w);
+    P.friction() = fld<C>(d, C::f_friction(d), 0, w);
+    double lm[KM], rot[KM];
 #pragma unroll
     for (int j = 0; j < KM; ++j) {
-        P.lm[j] = (j < K) ? fld<C>(d, C::f_link_mass(d), j, w) : 0.0;
-        P.rot[j] = (j < K) ? fld<C>(d, C::f_rotor(d), j, w) : 1.0;
-        P.dmp[j] = (j < K) ? fld<C>(d, C::f_damping(d), j, w) : 0.0;
+        lm[j] = (j < K) ? fld<C>(d, C::f_link_mass(d), j, w) : 0.0;
+        rot[j] = (j < K) ? fld<C>(d, C::f_rotor(d), j, w) : 1.0;
+        P.lm(j) = lm[j];
+        P.rot(j) = rot[j];
+        P.dmp(j) = (j < K) ? fld<C>(d, C::f_damping(d), j, w) : 0.0;
     }
-    P.m_total = P.base_mass + np_sum<KM>(P.lm, K);
-    P.inv_m = 1.0 / P.m_total;
-    P.inv_inertia = 1.0 / P.base_inertia;
+    const double mt = P.base_mass() + np_sum<KM>(lm, K);
+    P.m_total() = mt;
+    P.inv_m() = 1.0 / mt;
+    P.inv_inertia() = 1.0 / P.base_inertia();
 #pragma unroll
-    for (int j = 0; j < KM; ++j) P.inv_rot[j] = 1.0 / P.rot[j];
+    for (int j = 0; j < KM; ++j) P.inv_rot(j) = 1.0 / rot[j];
     if (actuators) {
         for_terms<C, C::kCapAct>(0, C::n_act(d), [&](auto aa) {
             const int a = ival(aa);
@@ -329,8 +411,8 @@ __device__ __forceinline__ void load_params(const ss_env_desc& d, int w, Params<
 #pragma unroll
                 for (int i = 0; i < KM; ++i) {
                     if (i < C::act_dim(d, a)) {
-                        P.kp[a][i] = fld<C>(d, C::act_f_kp(d, a), i, w);
-                        P.kd[a][i] = fld<C>(d, C::act_f_kd(d, a), i, w);
+                        P.kp(a, i) = fld<C>(d, C::act_f_kp(d, a), i, w);
+                        P.kd(a, i) = fld<C>(d, C::act_f_kd(d, a), i, w);
                     }
                 }
             }
@@ -338,12 +420,10 @@ __device__ __forceinline__ void load_params(const ss_env_desc& d, int w, Params<
     }
 }
 
-template <class C, int KM, int FM>
-__device__ __forceinline__ void phys_substep(const ss_env_desc& d, int w, World<KM, FM>& s, const Params<KM>& P) {
+template <class C, int KM, int FM, class PP, int AS>
+__device__ __forceinline__ void phys_substep(const ss_env_desc& d, int w, World<KM, FM, AS>& s, const PP& P) {
     const int K = C::K(d), F = C::F(d);
-    const double friction = P.friction;
-    const double(&lm)[KM] = P.lm;
-    const double(&dmp)[KM] = P.dmp;
+    const double friction = P.friction();
 
     // forward kinematics (fk_batch_trig, sim/physics.py:22-57)
     double sp, cp;
@@ -435,10 +515,10 @@ __device__ __forceinline__ void phys_substep(const ss_env_desc& d, int w, World<
 #pragma unroll
     for (int j = 0; j < KM; ++j) tau[3 + j] = 0.0 + s.ctrl[j];
 #pragma unroll
-    for (int j = 0; j < KM; ++j) tau[3 + j] = tau[3 + j] - dmp[j] * s.qd[3 + j];
-    tau[1] = tau[1] - P.m_total * g;
+    for (int j = 0; j < KM; ++j) tau[3 + j] = tau[3 + j] - P.dmp(j) * s.qd[3 + j];
+    tau[1] = tau[1] - P.m_total() * g;
 #pragma unroll
-    for (int j = 0; j < KM; ++j) tau[3 + j] = tau[3 + j] - lm[j] * g * C::half_len(d, j) * st[j];
+    for (int j = 0; j < KM; ++j) tau[3 + j] = tau[3 + j] - P.lm(j) * g * C::half_len(d, j) * st[j];
     tau[0] = tau[0] + s.ext0;
     tau[1] = tau[1] + s.ext1;
 #pragma unroll
@@ -459,11 +539,11 @@ __device__ __forceinline__ void phys_substep(const ss_env_desc& d, int w, World<
     s.ext1 = 0.0;
 
     // semi-implicit Euler (stage_integrate, sim/physics.py:216-224)
-    tau[0] = tau[0] * P.inv_m;
-    tau[1] = tau[1] * P.inv_m;
-    tau[2] = tau[2] * P.inv_inertia;
+    tau[0] = tau[0] * P.inv_m();
+    tau[1] = tau[1] * P.inv_m();
+    tau[2] = tau[2] * P.inv_inertia();
 #pragma unroll
-    for (int j = 0; j < KM; ++j) tau[3 + j] = tau[3 + j] * P.inv_rot[j];
+    for (int j = 0; j < KM; ++j) tau[3 + j] = tau[3 + j] * P.inv_rot(j);
     const double dt = C::dt(d);
 #pragma unroll
     for (int i = 0; i < 3 + KM; ++i)
@@ -532,9 +612,9 @@ __device__ __noinline__ double mlp_torque(const ss_env_desc& d, int a, int i, in
     return np_clip(cur[0], -A.effort, A.effort);
 }
 
-template <class C, int KM, int FM>
+template <class C, int KM, int FM, class PP, int AS>
 __device__ __forceinline__ void apply_actuators(const ss_env_desc& d, const ss_uniforms& u, int w, int sub,
-                                                World<KM, FM>& s, const Params<KM>& P) {
+                                                World<KM, FM, AS>& s, const PP& P) {
     const int N = C::NW(d);
     for_terms<C, C::kCapAct>(0, C::n_act(d), [&](auto aa) {
         const int a = ival(aa);
@@ -566,7 +646,7 @@ __device__ __forceinline__ void apply_actuators(const ss_env_desc& d, const ss_u
             if (kind == SS_ACT_MLP) {
                 tau = mlp_torque<KM, FM>(d, a, i, w, qdes, qj, qdj);
             } else {
-                const double kp = P.kp[a][i], kd = P.kd[a][i];
+                const double kp = P.kp(a, i), kd = P.kd(a, i);
                 tau = kp * (qdes - qj) + kd * (0.0 - qdj);
                 if (kind == SS_ACT_PD) {
                     tau = np_clip(tau, -eff, eff);
@@ -656,8 +736,8 @@ __device__ __forceinline__ double draw_interval_target(const ss_env_desc& d, int
     return np_clip(quantized, C::ev_iv_lo_q(d, e), C::ev_iv_hi_q(d, e));
 }
 
-template <class C, int KM, int FM>
-__device__ __forceinline__ void apply_event(const ss_env_desc& d, int e, int w, World<KM, FM>& s) {
+template <class C, int KM, int FM, int AS>
+__device__ __forceinline__ void apply_event(const ss_env_desc& d, int e, int w, World<KM, FM, AS>& s) {
     const int K = C::K(d);
     const int func = C::ev_func(d, e);
     if (func == SS_EVT_RANDOMIZE_FIELD) {
@@ -687,8 +767,8 @@ __device__ __forceinline__ void apply_event(const ss_env_desc& d, int e, int w, 
 }
 
 // CommandManager.resample for one world (managers/command.py:33-39)
-template <class C, int KM, int FM>
-__device__ __forceinline__ void resample_command(const ss_env_desc& d, int w, World<KM, FM>& s) {
+template <class C, int KM, int FM, int AS>
+__device__ __forceinline__ void resample_command(const ss_env_desc& d, int w, World<KM, FM, AS>& s) {
     const int N = C::NW(d);
     uint64_t key;
     const int slot = C::cmd_slot(d);
@@ -711,8 +791,8 @@ __device__ __forceinline__ void resample_command(const ss_env_desc& d, int w, Wo
 
 constexpr int kObsMax = SS_MAX_JOINTS > 2 * SS_MAX_FEET ? SS_MAX_JOINTS : 2 * SS_MAX_FEET;
 
-template <class C, int KM, int FM>
-__device__ __forceinline__ void obs_raw(const ss_env_desc& d, int t, int w, const World<KM, FM>& s,
+template <class C, int KM, int FM, int AS>
+__device__ __forceinline__ void obs_raw(const ss_env_desc& d, int t, int w, const World<KM, FM, AS>& s,
                                         double (&v)[kObsMax]) {
     const int N = C::NW(d), K = C::K(d), F = C::F(d);
     switch (C::obs_func(d, t)) {
@@ -786,9 +866,9 @@ __device__ __forceinline__ void obs_raw(const ss_env_desc& d, int t, int w, cons
 }
 
 // ObservationManager.compute, one term of one world (managers/observation.py:99-137)
-template <class C, int KM, int FM>
+template <class C, int KM, int FM, int AS>
 __device__ __forceinline__ void obs_term(const ss_env_desc& d, const ss_uniforms& u, int t, int w,
-                                         World<KM, FM>& s, bool pending, double* out, unsigned& bad_bits) {
+                                         World<KM, FM, AS>& s, bool pending, double* out, unsigned& bad_bits) {
     const int N = C::NW(d);
     double v[kObsMax];
     obs_raw<C>(d, t, w, s, v);
@@ -891,8 +971,8 @@ __device__ __forceinline__ void obs_term(const ss_env_desc& d, const ss_uniforms
 // ---------------------------------------------------------------------------
 // reward terms (mdp.py:96-160)
 
-template <class C, int KM, int FM>
-__device__ __forceinline__ double reward_value(const ss_env_desc& d, int r, int w, const World<KM, FM>& s,
+template <class C, int KM, int FM, int AS>
+__device__ __forceinline__ double reward_value(const ss_env_desc& d, int r, int w, const World<KM, FM, AS>& s,
                                                long long sim_step_now) {
     const int K = C::K(d), F = C::F(d);
     switch (C::rew_func(d, r)) {
@@ -915,7 +995,7 @@ __device__ __forceinline__ double reward_value(const ss_env_desc& d, int r, int 
             double sq[SS_MAX_ACTION];
 #pragma unroll
             for (int k = 0; k < SS_MAX_ACTION; ++k) {
-                const double dl = s.action[k] - s.prev_action[k];
+                const double dl = k < C::A(d) ? s.action[k] - s.prev_action[k] : 0.0;
                 sq[k] = dl * dl;
             }
             return np_sum<SS_MAX_ACTION>(sq, C::A(d));
@@ -994,11 +1074,22 @@ __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniform
     // Observation rows are staged in shared memory and leave the block as one
     // contiguous bulk copy per group (TMA, cp.async.bulk) instead of 32-way
     // scattered row stores (specialized builds whose groups fit 48 KB).
-    __shared__ __align__(16) double obs_stage[C::kStageObs ? C::kBlock * C::kObsTotal : 2];
+    // staging buffers: static shared memory, or one dynamic block (C::kDynSmem bytes, the layout
+    // C::kDynObs / kDynParam / kDynAct in doubles) when together they exceed the 48 KB static limit
+    __shared__ __align__(16) double obs_stage_s[(C::kStageObs && !C::kDynSmem) ? C::kBlock * C::kObsTotal : 2];
+    double* const obs_stage = C::kDynSmem ? dyn_smem() + C::kDynObs : obs_stage_s;
     SS_PROBE_SPAN(1);
-    World<KM, FM> s;
+    // JIT builds of large models keep the action vectors in shared-memory columns (ActArr)
+    constexpr int AS = C::kActSmem ? C::kBlock : 0;
+    __shared__ double act_cols_s[(AS && !C::kDynSmem) ? 2 * SS_DCAP_ACTION_COLS * AS : 1];
+    double* const act_cols = C::kDynSmem ? dyn_smem() + C::kDynAct : act_cols_s;
+    World<KM, FM, AS> s;
+    s.action.p = act_cols + threadIdx.x;
+    s.prev_action.p = act_cols + SS_DCAP_ACTION_COLS * AS + threadIdx.x;
 #pragma unroll
-    for (int k = 0; k < SS_MAX_ACTION; ++k) s.action[k] = s.prev_action[k] = 0.0;
+    for (int k = 0; k < SS_MAX_ACTION; ++k) {
+        if (!AS || k < SS_DCAP_ACTION_COLS) s.action[k] = s.prev_action[k] = 0.0;
+    }
     s.trig_bits = 0;
     s.terminated = s.truncated = s.nonfinite = s.was_reset = false;
 
@@ -1061,44 +1152,46 @@ __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniform
         }
         // L2 prefetch of everything read after the substeps or on the reset path
         if (st & (SS_ST_TERM | SS_ST_CURRICULUM)) {
-            l2_prefetch(d.episode_steps + w);
-            l2_prefetch(d.commanded_distance + w);
+            late_prefetch_line(d.episode_steps + w);
+            late_prefetch_line(d.commanded_distance + w);
         }
+        if (st & SS_ST_CURRICULUM) late_prefetch_line(d.episode_start_x + w);
         if (st & (SS_ST_REWARD | SS_ST_CURRICULUM | SS_ST_RESET | SS_ST_RESET_ALL)) {
             for_terms<C, C::kCapRewards>(0, C::n_rewards(d), [&](auto rr) {
-                l2_prefetch(d.ep_sums + (int64_t)ival(rr) * N + w);
-                l2_prefetch(d.ep_raw + (int64_t)ival(rr) * N + w);
+                late_prefetch_line(d.ep_sums + (int64_t)ival(rr) * N + w);
+                late_prefetch_line(d.ep_raw + (int64_t)ival(rr) * N + w);
             });
         }
-        if ((st & SS_ST_COMMAND) && C::n_cmd(d) > 0) {
-            l2_prefetch(d.countdown + w);
-            l2_prefetch(d.rng.counter[C::cmd_slot(d)] + w);
+        if ((st & (SS_ST_COMMAND | SS_ST_RESET | SS_ST_RESET_ALL)) && C::n_cmd(d) > 0) {
+            late_prefetch_line(d.countdown + w);
+            late_prefetch_line(d.rng.counter[C::cmd_slot(d)] + w);
+            for (int c = 0; c < 2 * C::n_cmd(d); ++c) late_prefetch_line(d.ranges + (int64_t)c * N + w);
         }
         if (st & (SS_ST_EVENTS | SS_ST_RESET | SS_ST_RESET_ALL)) {
             for_terms<C, C::kCapEvents>(0, C::n_events(d), [&](auto ee) {
                 const int e = ival(ee);
                 if (C::ev_mode(d, e) == SS_MODE_INTERVAL) {
-                    l2_prefetch(d.event[e].elapsed + w);
-                    l2_prefetch(d.event[e].target + w);
-                    l2_prefetch(d.rng.counter[C::ev_iv_slot(d, e)] + w);
+                    late_prefetch_line(d.event[e].elapsed + w);
+                    late_prefetch_line(d.event[e].target + w);
+                    late_prefetch_line(d.rng.counter[C::ev_iv_slot(d, e)] + w);
                 }
                 if (C::ev_mode(d, e) != SS_MODE_STARTUP && C::ev_func(d, e) != SS_EVT_EXTERNAL) {
-                    l2_prefetch(d.rng.counter[C::ev_slot_a(d, e)] + w);
-                    if (C::ev_func(d, e) == SS_EVT_PUSH_BASE) l2_prefetch(d.rng.counter[C::ev_slot_b(d, e)] + w);
+                    late_prefetch_line(d.rng.counter[C::ev_slot_a(d, e)] + w);
+                    if (C::ev_func(d, e) == SS_EVT_PUSH_BASE) late_prefetch_line(d.rng.counter[C::ev_slot_b(d, e)] + w);
                 }
             });
         }
         if (st & SS_ST_OBS) {
             for_terms<C, C::kCapObs>(0, C::n_obs(d), [&](auto tt) {
                 const int t = ival(tt);
-                if (C::obs_noise(d, t) != SS_NOISE_NONE) l2_prefetch(d.rng.counter[C::obs_noise_slot(d, t)] + w);
+                if (C::obs_noise(d, t) != SS_NOISE_NONE) late_prefetch_line(d.rng.counter[C::obs_noise_slot(d, t)] + w);
             });
-            l2_prefetch(d.prev_lin_vel_b + w);
-            l2_prefetch(d.prev_lin_vel_b + N + w);
+            late_prefetch_line(d.prev_lin_vel_b + w);
+            late_prefetch_line(d.prev_lin_vel_b + N + w);
         }
         if (resets) {
-            l2_prefetch(d.terrain_rows + w);
-            l2_prefetch(d.terrain_cols + w);
+            late_prefetch_line(d.terrain_rows + w);
+            late_prefetch_line(d.terrain_cols + w);
         }
         // action inputs and contact-sensor state: loaded here, ahead of the
         // ACTION stage's stores (which would otherwise order them behind)
@@ -1136,8 +1229,14 @@ __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniform
                 for (int i = 0; i < FM; ++i)
                     s.s_hist[h][i] = (need_hist && h < H && i < F) ? d.s_force_hist[((int64_t)h * F + i) * N + w] : 0.0;
         }
-        Params<KM> P;
-        if (sim && (st & (SS_ST_PHYS | SS_ST_APPLY))) load_params<C>(d, w, P, st & SS_ST_APPLY);
+        // JIT: the hoisted model fields live in a shared-memory column (Params, S = kBlock)
+        constexpr int PS = C::kParamSmem ? C::kBlock : 0;
+        using PT = Params<KM, C::kCapAct, PS>;
+        __shared__ double param_cols_s[(PS && !C::kDynSmem) ? PT::NV * PS : 1];
+        double* const param_cols = C::kDynSmem ? dyn_smem() + C::kDynParam : param_cols_s;
+        PT P;
+        P.p = param_cols + threadIdx.x;
+        if (sim && (st & (SS_ST_PHYS | SS_ST_APPLY))) load_params<C, KM>(d, w, P, st & SS_ST_APPLY);
         if (!phys) refresh(s);  // staged launch: entity data from the stored state
         SS_PROBE(1);
 
@@ -1315,8 +1414,10 @@ __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniform
             if (!s.have_action) {
 #pragma unroll
                 for (int k = 0; k < SS_MAX_ACTION; ++k) {
-                    s.action[k] = (k < A) ? d.action[(int64_t)k * N + w] : 0.0;
-                    s.prev_action[k] = (k < A) ? d.prev_action[(int64_t)k * N + w] : 0.0;
+                    if (k < A) {
+                        s.action[k] = d.action[(int64_t)k * N + w];
+                        s.prev_action[k] = d.prev_action[(int64_t)k * N + w];
+                    }
                 }
                 s.have_action = true;
             }

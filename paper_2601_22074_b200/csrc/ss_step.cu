@@ -110,6 +110,7 @@ struct JitModule {
     int block;
     int min_grid;  // experiment knob (SS_MIN_GRID): pad the grid with empty blocks
     int64_t desc_bytes;  // size of the kernel's descriptor parameter (packed when < sizeof(ss_env_desc))
+    int smem = 0;        // dynamic shared memory per block (staging buffers beyond the 48 KB static limit)
 };
 
 // Compile `src` (with named headers) for sm_100a. Returns the cubin through
@@ -180,7 +181,8 @@ static int jit_launch(JitModule* m, const ss_env_desc* desc, const void* param, 
     int blocks = (desc->n_worlds + m->block - 1) / m->block;
     if (blocks < m->min_grid) blocks = m->min_grid;
     const dim3 grid(blocks);
-    cudaError_t e = cudaLaunchKernel((const void*)m->kernel, grid, dim3(m->block), args, 0, (cudaStream_t)stream);
+    cudaError_t e = cudaLaunchKernel((const void*)m->kernel, grid, dim3(m->block), args, (size_t)m->smem,
+                                     (cudaStream_t)stream);
     if (e != cudaSuccess) return ss_fail("ss_env_step_jit launch", e);
     return 0;
 }
@@ -203,6 +205,20 @@ extern "C" int ss_jit_set_desc_bytes(void* handle, int64_t bytes) {
         return -14;
     }
     m->desc_bytes = bytes;
+    return 0;
+}
+
+extern "C" int ss_jit_set_smem(void* handle, int32_t bytes) {
+    JitModule* m = (JitModule*)handle;
+    if (!m || bytes < 0) {
+        ss_set_error("ss_jit_set_smem", "bad handle or size");
+        return -14;
+    }
+    if (bytes > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute((const void*)m->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+        if (e != cudaSuccess) return ss_fail("ss_jit_set_smem", e);
+    }
+    m->smem = bytes;
     return 0;
 }
 

@@ -95,12 +95,13 @@ def config_source(d) -> str:
     # shared-memory staging of the observation rows (one bulk copy per group)
     dims = [int(d.group[g].dim) for g in range(int(d.n_groups))]
     soff = [sum(dims[:g]) for g in range(len(dims))] + [0] * (native.SS_MAX_GROUPS - len(dims))
-    block = block_size()
-    stage = int(sum(dims) > 0 and block * sum(dims) * 8 <= 48 * 1024 and os.environ.get("SS_STAGE_OBS", "1") != "0")
+    block = block_size(d)
+    stage = obs_staged(d, block)
     lines += [f"  static constexpr int kBlock = {block}, kStageObs = {stage}, kObsTotal = {max(sum(dims), 1)}, "
               f"kRays = {max(int(d.n_rays), 1)};",
               f"  static __device__ __forceinline__ int g_soff(const ss_env_desc&, int g) {{ constexpr int a[{native.SS_MAX_GROUPS}] = "
               f"{{{', '.join(str(x) for x in soff)}}}; return a[g]; }}"]
+    lines += [staging_config(d, block, stage, sum(dims))]
     head = "  static __device__ __forceinline__"
     # Integers (counts, ids, flags, indices) become immediates: they drive the
     # unrolling and fold the term tables. Doubles stay kernel-parameter loads:
@@ -139,14 +140,64 @@ def config_source(d) -> str:
     return "\n".join(lines)
 
 
+def obs_staged(d, block: int) -> int:
+    """Observation rows staged in shared memory (one TMA bulk copy per group) while they fit 48 KB."""
+    total = sum(int(d.group[g].dim) for g in range(int(d.n_groups)))
+    return int(total > 0 and block * total * 8 <= 48 * 1024 and os.environ.get("SS_STAGE_OBS", "1") != "0")
+
+
+def dyn_smem_bytes(d) -> int:
+    block = block_size(d)
+    total = sum(int(d.group[g].dim) for g in range(int(d.n_groups)))
+    return staging_layout(d, block, obs_staged(d, block), total)["dyn"]
+
+
+def staging_layout(d, block: int, stage: int, obs_total: int) -> dict:
+    """Shared-memory staging of the specialized kernel (ss_kernel.cuh): the observation rows (one TMA
+    bulk copy per group), the hoisted model fields (Params columns) and, for large action vectors, the
+    action / previous-action columns (ActArr). The three sit in static shared memory while they fit its
+    48 KB; beyond that, in one dynamic block (up to SS_DYN_SMEM_MAX bytes) -- the large surrogates,
+    whose register-resident copies spill."""
+    km, na = max(int(d.model.n_joints), 1), max(int(d.n_actuators), 1)
+    a = max(int(d.action_dim), 1)
+    nv = 6 + 4 * km + 2 * na * km
+    obs = stage * block * obs_total
+    param = nv * block if os.environ.get("SS_PARAM_SMEM", "1") != "0" else 0
+    act = 2 * a * block if (a >= 8 and os.environ.get("SS_ACT_SMEM", "1") != "0") else 0
+    static_max = 48 * 1024 - 64
+    dyn_max = int(os.environ.get("SS_DYN_SMEM_MAX", str(100 * 1024)))
+    if (obs + param + act) * 8 <= static_max:
+        return {"param": int(param > 0), "act": int(act > 0), "dyn": 0, "obs_off": 0, "param_off": 0, "act_off": 0,
+                "act_cols": a}
+    if act and (obs + param + act) * 8 <= dyn_max:
+        return {"param": int(param > 0), "act": 1, "dyn": (obs + param + act) * 8, "obs_off": 0, "param_off": obs,
+                "act_off": obs + param, "act_cols": a}
+    # the biped's layout: params only while they fit the static budget
+    param_fits = param and (obs + param) * 8 <= static_max
+    return {"param": int(bool(param_fits)), "act": 0, "dyn": 0, "obs_off": 0, "param_off": 0, "act_off": 0,
+            "act_cols": a}
+
+
+def staging_config(d, block: int, stage: int, obs_total: int) -> str:
+    L = staging_layout(d, block, stage, obs_total)
+    return (f"  static constexpr int kParamSmem = {L['param']}, kActSmem = {L['act']}, kDynSmem = {L['dyn']}, "
+            f"kDynObs = {L['obs_off']}, kDynParam = {L['param_off']}, kDynAct = {L['act_off']};")
+
+
 def const_worlds_min() -> int:
     """World count from which N is compiled in as a constant (SS_CONST_N_MIN)."""
     return int(os.environ.get("SS_CONST_N_MIN", "1024"))
 
 
-def block_size() -> int:
-    """Threads per block of the specialized kernel (one world per thread)."""
-    return int(os.environ.get("SS_BLOCK", "64"))
+def block_size(d=None) -> int:
+    """Threads per block of the specialized kernel (one world per thread). 64 spreads a partial wave over
+    the most SMs (4096 worlds: 64 blocks); from 65,536 worlds, where the grid is many waves deep, 128 is
+    faster (fewer, larger TMA row copies of the observation blocks; Velocity-Rough 262,144 worlds 162 ->
+    156 us, 1,048,576 worlds 628 -> 583 us, tools/kab.py on one B200). SS_BLOCK overrides."""
+    env = os.environ.get("SS_BLOCK")
+    if env:
+        return int(env)
+    return 128 if d is not None and int(d.n_worlds) >= 65536 else 64
 
 
 def min_blocks() -> int:
@@ -178,11 +229,12 @@ def kernel_source(d) -> str:
     packed = ctypes.sizeof(native.packed_desc_type(caps))
     return "\n".join([
         *[f"#define SS_DCAP_{c} {v}" for c, v in caps.items()],
+        f"#define SS_DCAP_ACTION_COLS {max(int(d.action_dim), 1)}",
         '#include "stridesim_b200.h"',
         f'static_assert(sizeof(ss_env_desc) == {packed}, "packed descriptor layout differs from the host packing");',
         '#include "ss_kernel.cuh"',
         config_source(d),
-        f"extern \"C\" __global__ void __launch_bounds__({block_size()}"
+        f"extern \"C\" __global__ void __launch_bounds__({block_size(d)}"
         f"{', ' + str(min_blocks()) if min_blocks() else ''}) {KERNEL}(",
         "    const __grid_constant__ ss_env_desc d, const __grid_constant__ ss_uniforms u) {",
         f"  ss::step_body<JitCfg, {max(k, 1)}, {max(f, 1)}>(d, u);",
@@ -265,8 +317,11 @@ def _store_cubin(path: str, cubin: bytes) -> None:
 
 def _load(cubin: bytes, d) -> int:
     handle = ctypes.c_void_p()
-    native.call("ss_jit_load", cubin, len(cubin), KERNEL.encode(), block_size(), ctypes.byref(handle))
+    native.call("ss_jit_load", cubin, len(cubin), KERNEL.encode(), block_size(d), ctypes.byref(handle))
     native.call("ss_jit_set_desc_bytes", handle, ctypes.sizeof(native.packed_desc_type(desc_caps(d))))
+    dyn = dyn_smem_bytes(d)
+    if dyn:
+        native.call("ss_jit_set_smem", handle, dyn)
     return handle.value
 
 

@@ -180,6 +180,7 @@ _SIGNATURES = {
     "ss_jit_unload": ([ctypes.c_void_p], ctypes.c_int),
     "ss_env_step_jit": ([ctypes.c_void_p] * 4, ctypes.c_int),
     "ss_jit_set_desc_bytes": ([ctypes.c_void_p, ctypes.c_int64], ctypes.c_int),
+    "ss_jit_set_smem": ([ctypes.c_void_p, ctypes.c_int32], ctypes.c_int),
     "ss_env_step_jit_packed": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
                                 ctypes.c_void_p], ctypes.c_int),
     "ss_rt_launch": ([ctypes.c_void_p] * 5, ctypes.c_int),

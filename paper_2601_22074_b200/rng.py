@@ -92,9 +92,19 @@ class StreamPack:
     ``integers`` return CUDA float64 tensors, exactly the draws of
     StreamPack in the reference (rng.py:86-131)."""
 
-    def __init__(self, seed: int, world_id_offset: int, n: int, device, on_new_slot=None):
+    def __init__(self, seed: int, world_id_offset, n: int | None = None, device=None, on_new_slot=None):
+        """``StreamPack(seed, world_id_offset, n, device)``, or the reference's ``StreamPack(seed, ids)``
+        (rng.py:53) with ``ids`` a contiguous run of global ids (``offset + arange(n)``, the only form the
+        reference creates: env.py:114-115) on the current CUDA device."""
         import torch
 
+        if n is None:
+            ids = np.asarray(world_id_offset, dtype=np.int64).reshape(-1)
+            if ids.size == 0 or not np.array_equal(ids, ids[0] + np.arange(ids.size)):
+                raise ValueError("StreamPack ids must be a contiguous run offset + arange(n)")
+            world_id_offset, n = int(ids[0]), int(ids.size)
+        if device is None:
+            device = torch.device("cuda", torch.cuda.current_device())
         self.seed = int(seed)
         self.world_id_offset = int(world_id_offset)
         self.n = int(n)

@@ -375,9 +375,12 @@ def test_action_dim_mismatch_reports_expected():
         env.step(torch.zeros((4, 5), dtype=torch.float64, device="cuda"))
 
 
-def test_action_clip_history_and_pd_apply():
-    from paper_2601_22074_b200.actuators import pd_torque
+def pd_torque(kp, kd, effort_limit, q_des, qd_des, q, qd):
+    """numpy restatement of actuators.py:104-107 (the expected values)."""
+    return np.clip(kp * (q_des - q) + kd * (qd_des - qd), -effort_limit, effort_limit)
 
+
+def test_action_clip_history_and_pd_apply():
     env = quiet_env()
     am = env.action_manager
     am.process(np.full((4, 4), 0.1))
@@ -394,7 +397,6 @@ def test_action_clip_history_and_pd_apply():
 
 
 def test_delayed_actuator_first_substep_uses_reset_fill():
-    from paper_2601_22074_b200.actuators import pd_torque
     from paper_2601_22074_b200.config import DelayedCfg, IdealPdCfg
     from paper_2601_22074_b200.env import ManagerBasedRlEnv
 
@@ -658,7 +660,11 @@ def test_dc_motor_envelope_on_device(rng):
 
     kp, kd, eff, sat, vl = 40.0, 1.0, 30.0, 45.0, 20.0
     q_des, q, qd = rng.uniform(-2, 2, 50), rng.uniform(-2, 2, 50), rng.uniform(-30, 30, 50)
-    host = dc_motor_torque(kp, kd, eff, sat, vl, q_des, 0.0, q, qd)
+    tau = kp * (q_des - q) + kd * (0.0 - qd)  # numpy restatement of actuators.py:110-117
+    hi = np.clip(sat * (1.0 - qd / vl), 0.0, eff)
+    lo = np.clip(sat * (-1.0 - qd / vl), -eff, 0.0)
+    host = np.clip(tau, lo, hi)
+    assert np.array_equal(host, _np(dc_motor_torque(kp, kd, eff, sat, vl, q_des, 0.0, q, qd)))  # host inputs
     dev = dc_motor_torque(torch.full((50,), kp, device="cuda", dtype=torch.float64), kd, eff, sat, vl,
                           torch.as_tensor(q_des, device="cuda"), 0.0, torch.as_tensor(q, device="cuda"),
                           torch.as_tensor(qd, device="cuda"))

@@ -83,3 +83,22 @@ for i in range(100):
     env.step_wait()
 pr.disable()
 pstats.Stats(pr).sort_stats("tottime").print_stats(12)
+
+# floors: back-to-back D2H of the arena (pinned), H2D of the actions, and both at once
+nb = env.step_outputs.numel()
+hb = torch.empty(nb, dtype=torch.uint8).pin_memory()
+ha = acts[0]
+da = torch.empty_like(ha, device="cuda")
+s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+run("D2H arena only", lambda i: hb.copy_(env.step_outputs, non_blocking=True))
+run("H2D actions only", lambda i: da.copy_(ha, non_blocking=True))
+
+
+def both(i):
+    with torch.cuda.stream(s1):
+        hb.copy_(env.step_outputs, non_blocking=True)
+    with torch.cuda.stream(s2):
+        da.copy_(ha, non_blocking=True)
+
+
+run("D2H + H2D on two streams", both)

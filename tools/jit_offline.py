@@ -18,6 +18,7 @@ from paper_2601_22074_b200 import jit, native  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("tu")
 ap.add_argument("--sass", default=None)
+ap.add_argument("--cubin", default=None, help="also write the cubin (nvdisasm -g for line info)")
 args = ap.parse_args()
 src = open(args.tu).read()
 opts = [o.encode() for o in jit.options() + ["--ptxas-options=-v"]]
@@ -35,6 +36,8 @@ for line in log.value.decode().splitlines():
         print(line.strip())
 with tempfile.NamedTemporaryFile(suffix=".cubin", delete=False) as fh:
     fh.write(buf.raw[: size.value])
+if args.cubin:
+    open(args.cubin, "wb").write(buf.raw[: size.value])
 sass = subprocess.run(["cuobjdump", "-sass", fh.name], capture_output=True, text=True).stdout
 os.unlink(fh.name)
 ins = [l for l in sass.splitlines() if re.match(r"\s+/\*[0-9a-f]{4,}\*/", l)]
