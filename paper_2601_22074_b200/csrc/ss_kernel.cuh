@@ -32,6 +32,9 @@
 #ifndef SS_DCAP_ACTION_COLS
 #define SS_DCAP_ACTION_COLS 1  /* action columns in shared memory (JIT: the env's action dim) */
 #endif
+#ifndef SS_DCAP_REWARDS
+#define SS_DCAP_REWARDS 1
+#endif
 #ifndef SS_PEEL_LAST_SUBSTEP
 #define SS_PEEL_LAST_SUBSTEP 0
 #endif
@@ -180,12 +183,14 @@ __device__ __forceinline__ void height_raw_n(const ss_env_desc& d, const double 
     for (int r = 0; r < NR; ++r) out[r] = a[r] * (1.0 - frac[r]) + b[r] * frac[r];
 }
 
-// The action / previous-action vectors of a world: registers (S == 0), or
-// columns of stride S in shared memory (value k at p[k * S]; large models,
-// where the 2 x A doubles would otherwise stay live in registers all step).
-template <int S>
-struct ActArr {
-    double r[S ? 1 : SS_MAX_ACTION];
+// Per-world vectors of M doubles: registers (S == 0), or a column of stride S
+// in shared memory (value k at p[k * S], the block's threads side by side) --
+// large models keep their action / previous-action / target vectors and the
+// episodic reward sums there, which would otherwise stay live in registers all
+// step and spill.
+template <int S, int M>
+struct Col {
+    double r[S ? 1 : M];
     double* p;
     __device__ __forceinline__ double& operator[](int k) {
         if constexpr (S > 0) return p[k * S];
@@ -197,10 +202,16 @@ struct ActArr {
     }
 };
 
-template <int S>
-__device__ __forceinline__ double sel(const ActArr<S>& a, int j) {
+template <int S, int M>
+__device__ __forceinline__ double sel(const Col<S, M>& a, int j) {
     if constexpr (S > 0) return a[j];
     else return sel(a.r, j);
+}
+
+template <int S, int M>
+__device__ __forceinline__ void sel_store(Col<S, M>& a, int j, double v) {
+    if constexpr (S > 0) a[j] = v;
+    else sel_store(a.r, j, v);
 }
 
 template <int KM, int FM, int AS = 0>
@@ -215,8 +226,8 @@ struct World {
     bool efin[FM];
     double sp, cp;
     bool trig_ok;
-    double targets[KM];
-    ActArr<AS> action, prev_action;
+    Col<AS, KM> targets;
+    Col<AS, SS_MAX_ACTION> action, prev_action;
     bool have_action;
     double cmd[SS_MAX_CMD];
     bool s_in[FM];
@@ -229,7 +240,7 @@ struct World {
     bool terminated, truncated, nonfinite, was_reset;
     unsigned trig_bits;
     // per-step state prefetched at kernel entry (one round trip, see step_body)
-    double ep_sum[SS_MAX_REWARDS], ep_rw[SS_MAX_REWARDS];
+    Col<AS, SS_MAX_REWARDS> ep_sum, ep_rw;
     long long countdown;
     double ev_el[SS_MAX_EVENTS], ev_tg[SS_MAX_EVENTS];
     uint64_t nctr[SS_MAX_OBS_TERMS];
@@ -664,8 +675,8 @@ __device__ __forceinline__ void apply_actuators(const ss_env_desc& d, const ss_u
 }
 
 // Actuator.reset (actuators.py:269-277) for one world
-template <class C, int KM>
-__device__ __forceinline__ void reset_actuators(const ss_env_desc& d, int w, const double (&targets)[KM]) {
+template <class C, int KM, class T>
+__device__ __forceinline__ void reset_actuators(const ss_env_desc& d, int w, const T& targets) {
     const int N = C::NW(d);
     for (int a = 0; a < C::n_act(d); ++a) {
         const ss_actuator& A = d.actuator[a];
@@ -1079,13 +1090,18 @@ __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniform
     __shared__ __align__(16) double obs_stage_s[(C::kStageObs && !C::kDynSmem) ? C::kBlock * C::kObsTotal : 2];
     double* const obs_stage = C::kDynSmem ? dyn_smem() + C::kDynObs : obs_stage_s;
     SS_PROBE_SPAN(1);
-    // JIT builds of large models keep the action vectors in shared-memory columns (ActArr)
+    // JIT builds of large models keep the action / target vectors and the episodic sums in
+    // shared-memory columns (Col): [action A][prev action A][targets K][ep_sum R][ep_raw R]
     constexpr int AS = C::kActSmem ? C::kBlock : 0;
-    __shared__ double act_cols_s[(AS && !C::kDynSmem) ? 2 * SS_DCAP_ACTION_COLS * AS : 1];
+    constexpr int NCOL = 2 * SS_DCAP_ACTION_COLS + KM + 2 * SS_DCAP_REWARDS;
+    __shared__ double act_cols_s[(AS && !C::kDynSmem) ? NCOL * AS : 1];
     double* const act_cols = C::kDynSmem ? dyn_smem() + C::kDynAct : act_cols_s;
     World<KM, FM, AS> s;
     s.action.p = act_cols + threadIdx.x;
     s.prev_action.p = act_cols + SS_DCAP_ACTION_COLS * AS + threadIdx.x;
+    s.targets.p = act_cols + 2 * SS_DCAP_ACTION_COLS * AS + threadIdx.x;
+    s.ep_sum.p = act_cols + (2 * SS_DCAP_ACTION_COLS + KM) * AS + threadIdx.x;
+    s.ep_rw.p = act_cols + (2 * SS_DCAP_ACTION_COLS + KM + SS_DCAP_REWARDS) * AS + threadIdx.x;
 #pragma unroll
     for (int k = 0; k < SS_MAX_ACTION; ++k) {
         if (!AS || k < SS_DCAP_ACTION_COLS) s.action[k] = s.prev_action[k] = 0.0;
@@ -1558,7 +1574,7 @@ __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniform
 #pragma unroll
             for (int j = 0; j < KM; ++j)
                 if (j < K) d.targets[(int64_t)j * N + w] = s.targets[j];
-            reset_actuators<C>(d, w, s.targets);
+            reset_actuators<C, KM>(d, w, s.targets);
             // ContactSensor.reset (sensors.py:81-89)
 #pragma unroll
             for (int i = 0; i < FM; ++i) {
