@@ -164,7 +164,8 @@ def staging_layout(d, block: int, stage: int, obs_total: int) -> dict:
     obs = stage * block * obs_total
     param = nv * block if os.environ.get("SS_PARAM_SMEM", "1") != "0" else 0
     ncol = 2 * a + km + 2 * max(int(d.n_rewards), 1)  # ss_kernel.cuh step_world: action, prev, targets, ep sums
-    act = ncol * block if (a >= 8 and os.environ.get("SS_ACT_SMEM", "1") != "0") else 0
+    act_mode = os.environ.get("SS_ACT_SMEM", "1")  # "0" never, "1" from 8 actions, "all" always
+    act = ncol * block if ((a >= 8 and act_mode != "0") or act_mode == "all") else 0
     static_max = 48 * 1024 - 64
     dyn_max = int(os.environ.get("SS_DYN_SMEM_MAX", str(112 * 1024)))  # 2 blocks per SM
     if (obs + param + act) * 8 <= static_max:
