@@ -293,10 +293,11 @@ def allmax(x: float, world: int) -> float:
     return float(t.item())
 
 
-def timed_steps(env, steps: int, flush, stream, policy, after=None) -> float:
+def timed_steps(env, steps: int, flush, stream, policy, after=None, before=None) -> float:
     """Seconds of GPU time for `steps` env steps, each preceded by an L2 flush
-    (untimed) and bracketed by CUDA events on the launching stream. `after(i)`
-    runs inside step i's bracket (the per-log-interval stats all-reduce)."""
+    (untimed) and bracketed by CUDA events on the launching stream. `before(i)`
+    / `after(i)` run inside step i's bracket (the per-log-interval statistics:
+    fused into the step, then the all-reduce)."""
     import torch
 
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
@@ -305,6 +306,8 @@ def timed_steps(env, steps: int, flush, stream, policy, after=None) -> float:
         flush.fill_(float(i))  # evict L2 (126 MB) between timed iterations (untimed)
         e0, e1 = evs[i]
         e0.record(stream)
+        if before is not None:
+            before(i)
         env.step(policy(i))
         if after is not None:
             after(i)
@@ -503,24 +506,33 @@ def run_ours(args):
     for i in range(args.warmup):
         env.step(random_policy(env, i, fused=True))
     build_record(env, 0, env.reward_manager.reward, None)  # warm the stats kernel and the collective
+    env._stats_packer.request()  # and the fused statistics tail of the step kernel
+    env.step(random_policy(env, args.warmup, fused=True))
     torch.cuda.synchronize()
 
     # every log interval (cli.py:118, --log-every 10) the job's statistics are
-    # reduced across ranks inside the timed step: one ss_stats_pack launch packs
+    # reduced across ranks inside the timed step: the step kernel itself reduces
     # this rank's reward / episodic sums / trigger counts / terrain-row
-    # histogram / nonfinite count, one all_reduce (NCCL) sums them over ranks;
-    # the records are unpacked on the host after the timed region
+    # histogram / nonfinite count into one vector in its tail (StatsPacker.request,
+    # no extra launch), one all_reduce (NCCL) sums it over ranks; the records are
+    # unpacked on the host after the timed region
     vecs = []
+    n_rec = args.steps // args.log_every if args.log_every > 0 else 0
+    rec_bufs = [torch.zeros_like(env._stats_packer.out) for _ in range(n_rec)]
+
+    def log_request(i):
+        if args.log_every > 0 and (i + 1) % args.log_every == 0:
+            env._stats_packer.request(rec_bufs[len(vecs)])
 
     def log_interval(i):
         if args.log_every > 0 and (i + 1) % args.log_every == 0:
-            vecs.append((i + 1, allreduce_stats(env._stats_packer.pack().clone())))
+            vecs.append((i + 1, allreduce_stats(rec_bufs[len(vecs)])))
 
     clocks = Clocks(local)
     barrier(world)
     launches0 = native.LAUNCHES["count"]
     t_step = timed_steps(env, args.steps, flush, stream, lambda i: random_policy(env, args.warmup + i, fused=True),
-                         after=log_interval)
+                         after=log_interval, before=log_request)
     barrier(world)
     launches = native.LAUNCHES["count"] - launches0
     t_max = allmax(t_step, world)
@@ -622,7 +634,8 @@ def run_ours(args):
                          if env.use_jit else "step_kernel<4,2> (fused control step, generic)",
                          "kernel_ms": 1e3 * t_kernel / args.steps},
             "policy": "random_policy fused into the step kernel (policies.RandomActions: same stream and values)",
-            "stats_allreduce": {"every_steps": args.log_every, "per_interval": "1 ss_stats_pack launch + 1 all_reduce "
+            "stats_allreduce": {"every_steps": args.log_every, "per_interval": "the job statistics reduced in the step "
+                                "kernel's tail (fused, no extra launch) + 1 all_reduce "
                                 f"({'NCCL' if world > 1 else 'no-op at 1 rank'}) of {int(env._stats_packer.out.numel())} "
                                 "float64, inside the timed step", "records": len(records),
                                 "last": records[-1] if records else None},

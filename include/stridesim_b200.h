@@ -539,6 +539,15 @@ typedef struct ss_uniforms {
     int32_t policy_pad;
     double policy_lo;
     double policy_hi;
+    /* non-NULL: this launch also reduces the job statistics of metrics.build_record
+     * (metrics.py:31-45) over its worlds, fused into the step's tail, into stats_out
+     * (the ss_stats_pack layout); stats_partials holds gridDim x SS_STATS_MAXV doubles,
+     * stats_ticket one zeroed uint32 the kernel resets */
+    double* stats_out;
+    double* stats_partials;
+    uint32_t* stats_ticket;
+    int32_t stats_rows;
+    int32_t stats_pad;
 } ss_uniforms;
 
 /* Host-side runtime state of one env: every per-launch uniform (step
@@ -603,6 +612,12 @@ typedef struct ss_launch {
      * (NULL: the kernel takes the full ss_env_desc); its size in bytes */
     const void* jit_desc;
     int64_t jit_desc_bytes;
+    /* fused statistics of this step (see ss_uniforms.stats_out); NULL: none */
+    double* stats_out;
+    double* stats_partials;
+    uint32_t* stats_ticket;
+    int32_t stats_rows;
+    int32_t stats_pad;
 } ss_launch;
 
 /* One draw call of StreamPack.uniform/normal (rng.py:69-119). sel == NULL

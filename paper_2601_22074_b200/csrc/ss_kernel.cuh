@@ -1081,6 +1081,7 @@ __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniform
     const int w = blockIdx.x * blockDim.x + threadIdx.x;
     const bool active = w < N;
     const unsigned st = u.stages;
+    double stat_reward = 0.0;  // this step's reward of world w (the fused statistics, stats_tail)
     const int K = C::K(d), F = C::F(d), A = C::A(d);
     // Observation rows are staged in shared memory and leave the block as one
     // contiguous bulk copy per group (TMA, cp.async.bulk) instead of 32-way
@@ -1464,6 +1465,7 @@ __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniform
                 d.last_values[(int64_t)r * N + w] = v;
             });
             d.reward_out[w] = total;
+            stat_reward = total;
             if (C::mirror_on(d)) *mirror_of(d, d.reward_out + w) = total;
         }
 
@@ -1760,6 +1762,63 @@ __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniform
             // zero-copy flag in mapped pinned host memory: the host notices a
             // nonfinite step without a per-step device->host copy (env.py:240-241)
             if (d.nf_flags) *((volatile uint32_t*)&d.nf_flags[u.nf_slot]) = 1u;
+        }
+    }
+
+    // ---- the job statistics of metrics.build_record (metrics.py:31-45), fused into the step's tail
+    // on log-interval steps: [n, sum reward, sum ep_sums[t], trigger counts, terrain-row histogram,
+    // sum nonfinite] (the ss_stats_pack layout) reduced in a fixed order -- lanes by shuffle tree,
+    // warps in order, blocks in order by the last block to arrive -- so the vector is deterministic,
+    // ready for the single all_reduce; one launch fewer per log interval than a separate pack
+    if (u.stats_out && (int)gridDim.x * (int)blockDim.x >= N && (int)blockDim.x <= C::kBlock) {
+        // the warp partials reuse the observation staging buffer when there is one (its bulk copies
+        // have been read: thread 0 waited on them before this barrier), keeping builds within 48 KB
+        constexpr bool kReuse = C::kStageObs && C::kObsTotal * 32 >= SS_STATS_MAXV;
+        __shared__ double red_s[kReuse ? 1 : (C::kBlock / 32) * SS_STATS_MAXV];
+        double* const red = kReuse ? obs_stage : red_s;
+        __shared__ bool last;
+        __syncthreads();
+        const int T = C::n_rewards(d), R = u.stats_rows, V = 2 + T + R;
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (int)blockDim.x >> 5;
+        const long long row = active ? d.terrain_rows[w] : -1;
+        auto reduce_to = [&](int v, double x) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+            if (lane == 0) red[warp * SS_STATS_MAXV + v] = x;
+        };
+        reduce_to(0, active ? stat_reward : 0.0);
+        for_terms<C, C::kCapRewards>(0, C::n_rewards(d), [&](auto rr) {
+            const int r = ival(rr);
+            reduce_to(1 + r, active ? s.ep_sum[r] : 0.0);
+        });
+        reduce_to(T + 1, (active && s.nonfinite) ? 1.0 : 0.0);
+        for (int k = 0; k < R; ++k) reduce_to(T + 2 + k, (row == (long long)k) ? 1.0 : 0.0);
+        __syncthreads();
+        for (int v = threadIdx.x; v < V; v += blockDim.x) {
+            double acc = 0.0;
+            for (int k = 0; k < nw; ++k) acc += red[k * SS_STATS_MAXV + v];
+            u.stats_partials[(int64_t)blockIdx.x * SS_STATS_MAXV + v] = acc;
+        }
+        __threadfence();  // partials and this block's trigger-count atomics before the ticket
+        __syncthreads();
+        if (threadIdx.x == 0) last = atomicAdd(u.stats_ticket, 1u) == gridDim.x - 1;
+        __syncthreads();
+        if (last) {
+            __threadfence();
+            const int Cn = C::n_terms(d) + 1;
+            for (int v = threadIdx.x; v < V; v += blockDim.x) {
+                double acc = 0.0;
+                for (int b = 0; b < (int)gridDim.x; ++b)
+                    acc += ((volatile double*)u.stats_partials)[(int64_t)b * SS_STATS_MAXV + v];
+                const int o = v == 0 ? 1 : (v <= T ? 1 + v : (v == T + 1 ? 2 + T + Cn + R : 2 + T + Cn + (v - T - 2)));
+                u.stats_out[o] = acc;
+            }
+            for (int c = threadIdx.x; c < Cn; c += blockDim.x)
+                u.stats_out[2 + T + c] = (double)((volatile unsigned long long*)d.trigger_counts)[c];
+            if (threadIdx.x == 0) {
+                u.stats_out[0] = (double)N;
+                *u.stats_ticket = 0u;
+            }
         }
     }
     SS_PROBE_SPAN(0);

@@ -81,6 +81,11 @@ extern "C" int ss_rt_launch(const ss_env_desc* d, ss_rt_state* st, const ss_laun
     u.policy_pad = 0;
     u.policy_lo = l->policy_lo;
     u.policy_hi = l->policy_hi;
+    u.stats_out = l->stats_out;
+    u.stats_partials = l->stats_partials;
+    u.stats_ticket = l->stats_ticket;
+    u.stats_rows = l->stats_rows;
+    u.stats_pad = 0;
     int slot = -1;
     if (stages & SS_ST_TERM) {
         if (st->nf_pending >= st->nf_slots) {

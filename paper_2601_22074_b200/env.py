@@ -164,6 +164,7 @@ class ManagerBasedRlEnv:
         self._la = native.Launch()
         self._la_ref = ctypes.byref(self._la)
         self._la_key = None  # (stages, nsub, flags, groups_mask) last written into _la
+        self._stats_req = None  # pending fused-statistics request (metrics.StatsPacker.request)
         self._rt.global_step = 0
         self._rt.sensor_last_update = -1
         # nonfinite bookkeeping: zero-copy flags (mapped pinned memory) + a ring of
@@ -389,6 +390,13 @@ class ManagerBasedRlEnv:
             la.actions = None if actions is None else actions.data_ptr()
             la.policy_slot = -1
         la.reset_mask = None if reset_mask is None else reset_mask.data_ptr()
+        req = self._stats_req
+        if req is not None and stages == native.SS_ST_STEP_ALL:
+            # metrics.StatsPacker.request: this step also reduces the job statistics (fused tail)
+            la.stats_out, la.stats_partials, la.stats_ticket, la.stats_rows = req
+            self._stats_req = None
+        elif la.stats_out:
+            la.stats_out = None
         rt.sim_step = self.state.sim_step
         native.LAUNCHES["count"] += 1
         rc = self._lib.ss_rt_launch(self._desc_ref, self._rt_ref, self._la_ref,

@@ -88,10 +88,26 @@ class StatsPacker:
         self.n_rows = int(env.terrain.rows)
         dev = env.device
         self.out = torch.zeros(3 + self.n_rewards + self.n_counts + self.n_rows, dtype=torch.float64, device=dev)
+        self._maxv = native.SS_STATS_MAXV
         self.partials = torch.zeros(native.SS_STATS_GRID * native.SS_STATS_MAXV, dtype=torch.float64, device=dev)
         self.ticket = torch.zeros(1, dtype=torch.int32, device=dev)
         self._args = native.StatsArgs()
         self._lib = native.lib()
+
+    def request(self, out=None):
+        """Have the env's NEXT full control step reduce the statistics itself, fused into the step
+        kernel's tail (no extra launch), into ``out`` (default ``self.out``; same layout as ``pack``).
+        The vector holds the statistics of that step once it has run."""
+        import torch
+
+        env = self.env
+        if getattr(self, "_fpartials", None) is None:
+            grid = -(-env.num_envs // 32)  # >= the step kernel's grid at any block size
+            self._fpartials = torch.zeros(grid * self._maxv, dtype=torch.float64, device=env.device)
+            self._fticket = torch.zeros(1, dtype=torch.int32, device=env.device)
+        out = self.out if out is None else out
+        env._stats_req = (out.data_ptr(), self._fpartials.data_ptr(), self._fticket.data_ptr(), self.n_rows)
+        return out
 
     def pack(self, reward=None):
         """Launch the reduction on the current stream; returns the (device) vector."""

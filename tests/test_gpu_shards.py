@@ -96,3 +96,34 @@ def test_stats_pack_deterministic_and_reusable():
     rec = build_record(env, 3, env.reward_manager.reward, None)
     assert sum(rec.terrain_row_histogram) == 65536
     assert rec.reward_mean == pytest.approx(float(env.reward_manager.reward.mean()), abs=1e-9)
+
+
+@pytest.mark.parametrize("n", [4096, 262144])
+def test_fused_step_statistics_equal_the_pack(n):
+    """StatsPacker.request: the step kernel reduces the statistics in its tail (bench.py's log-interval
+    path); the vector equals a separate ss_stats_pack of the same step's outputs, and the next step
+    (no request) leaves it alone."""
+    from paper_2601_22074_b200.metrics import StatsPacker
+    from paper_2601_22074_b200.policies import random_policy
+
+    env = _env(n, 0, seed=4)
+    for i in range(30):
+        env.step(random_policy(env, i, fused=True))
+    p = StatsPacker(env)
+    out = torch.full_like(p.out, -1.0)
+    p.request(out)
+    env.step(random_policy(env, 30, fused=True))
+    want = p.pack().clone()
+    torch.cuda.synchronize()
+    np.testing.assert_allclose(out.cpu().numpy(), want.cpu().numpy(), rtol=1e-12, atol=1e-9)
+    assert float(out[0]) == n and float(out[1:].abs().sum()) > 0
+    keep = out.clone()
+    env.step(random_policy(env, 31, fused=True))
+    torch.cuda.synchronize()
+    assert torch.equal(out, keep)
+    # and again (the ticket was reset by the kernel)
+    p.request(out)
+    env.step(random_policy(env, 32, fused=True))
+    want = p.pack().clone()
+    torch.cuda.synchronize()
+    np.testing.assert_allclose(out.cpu().numpy(), want.cpu().numpy(), rtol=1e-12, atol=1e-9)

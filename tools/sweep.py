@@ -14,42 +14,48 @@ from paper_2601_22074_b200.tasks import make_env_cfg  # noqa: E402
 from paper_2601_22074_b200.traffic import step_bytes_per_world  # noqa: E402
 
 tasks = sys.argv[1].split(",") if len(sys.argv) > 1 else ["Velocity-Rough"]
-sizes = [int(x) for x in (sys.argv[2].split(",") if len(sys.argv) > 2 else ["1024", "4096", "16384", "65536"])]
+sizes = [int(x) for x in (sys.argv[2].split(",") if len(sys.argv) > 2 else ["1024", "4096", "16384", "65536", "262144"])]
 flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
-print("| task | N | step us (warm) | env-steps/s (warm) | step us (L2 flushed) | kernel us (flushed) | B/env-step | kernel GB/s (flushed) | frac of 6544 GB/s |")
+try:
+    import json
+
+    PEAK = float(json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                             "MEASURED_PEAKS.json")))["hbm_gbs"])
+except (OSError, KeyError, ValueError):
+    PEAK = 6650.0
+print("Fused random policy (one launch per control step, `random_policy(env, i, fused=True)`).")
+print()
+print(f"| task | N | step us (warm) | env-steps/s (warm) | step us (L2 flushed) | env-steps/s (flushed) | B/env-step | "
+      f"GB/s (flushed) | frac of {PEAK:.0f} GB/s |")
 print("|---|---|---|---|---|---|---|---|---|")
 for task in tasks:
     for n in sizes:
         env = ManagerBasedRlEnv(make_env_cfg(task, num_envs=n))
         env.reset()
         for i in range(60):
-            env.step(random_policy(env, i))
+            env.step(random_policy(env, i, fused=True))
         torch.cuda.synchronize()
         K = 50
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for i in range(K):
-            env.step(random_policy(env, i))
+            env.step(random_policy(env, i, fused=True))
         e1.record()
         torch.cuda.synchronize()
         warm = e0.elapsed_time(e1) * 1e3 / K
-        tot = ker = 0.0
+        tot = 0.0
         for i in range(20):
             flush.fill_(float(i))
-            a0, a1, a2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a0.record()
-            a = random_policy(env, i)
+            env.step(random_policy(env, 60 + K + i, fused=True))
             a1.record()
-            env.step(a)
-            a2.record()
-            a2.synchronize()
-            tot += a0.elapsed_time(a2) * 1e3
-            ker += a1.elapsed_time(a2) * 1e3
+            a1.synchronize()
+            tot += a0.elapsed_time(a1) * 1e3
         tot /= 20
-        ker /= 20
-        b = step_bytes_per_world(env)["total"]
-        gbs = b * n / (ker * 1e-6) / 1e9
-        print(f"| {task} | {n} | {warm:.1f} | {n / warm * 1e6:,.0f} | {tot:.1f} | {ker:.1f} | {b} | {gbs:,.0f} | {gbs / 6543.7:.3f} |",
-              flush=True)
+        b = step_bytes_per_world(env, fused_policy=True)["total"]
+        gbs = b * n / (tot * 1e-6) / 1e9
+        print(f"| {task} | {n} | {warm:.1f} | {n / warm * 1e6:,.0f} | {tot:.1f} | {n / tot * 1e6:,.0f} | {b} | {gbs:,.0f} | "
+              f"{gbs / PEAK:.3f} |", flush=True)
         del env
         torch.cuda.empty_cache()
