@@ -156,6 +156,7 @@ struct RuntimeCfg {
     static constexpr int kCapTerms = SS_MAX_TERMINATIONS, kCapRewards = SS_MAX_REWARDS;
     static constexpr int kCapEvents = SS_MAX_EVENTS, kCapGroups = SS_MAX_GROUPS, kCapObs = SS_MAX_OBS_TERMS;
     static constexpr int kBlock = 128, kStageObs = 0, kObsTotal = 0, kRays = SS_MAX_RAYS;
+    static constexpr int kParamSmemAlone = 0;
     static constexpr int kParamSmem = 0, kActSmem = 0, kDynSmem = 0, kDynObs = 0, kDynParam = 0, kDynAct = 0;
     static __device__ __forceinline__ int g_soff(const ss_env_desc&, int) { return 0; }
 #define SS_RT_X(T, name, expr) \

@@ -1074,13 +1074,16 @@ __device__ __forceinline__ long long gtimer() {
     } while (0)
 #endif
 
-template <class C, int KM, int FM>
+// FS != 0 compiles the body for exactly that stage set (the split launch of large
+// envs: physics | terms + observations, each kernel with ~40 registers fewer
+// than the whole body); FS == 0 takes the set from u.stages.
+template <class C, int KM, int FM, unsigned FS = 0>
 __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniforms& u) {
     const int N = C::NW(d);
     if ((int)(blockIdx.x * blockDim.x) >= N) return;  // padding block (grid rounded up to fill the SMs)
     const int w = blockIdx.x * blockDim.x + threadIdx.x;
     const bool active = w < N;
-    const unsigned st = u.stages;
+    const unsigned st = FS ? FS : u.stages;  // FS: a kernel compiled for one fixed stage set
     double stat_reward = 0.0;  // this step's reward of world w (the fused statistics, stats_tail)
     const int K = C::K(d), F = C::F(d), A = C::A(d);
     // Observation rows are staged in shared memory and leave the block as one
@@ -1088,7 +1091,10 @@ __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniform
     // scattered row stores (specialized builds whose groups fit 48 KB).
     // staging buffers: static shared memory, or one dynamic block (C::kDynSmem bytes, the layout
     // C::kDynObs / kDynParam / kDynAct in doubles) when together they exceed the 48 KB static limit
-    __shared__ __align__(16) double obs_stage_s[(C::kStageObs && !C::kDynSmem) ? C::kBlock * C::kObsTotal : 2];
+    // a fixed-stage kernel allocates only the staging its stages use (FS: step_body)
+    constexpr bool kObsUsed = FS == 0 || (FS & SS_ST_OBS);
+    __shared__ __align__(16) double
+        obs_stage_s[(C::kStageObs && !C::kDynSmem && kObsUsed) ? C::kBlock * C::kObsTotal : 2];
     double* const obs_stage = C::kDynSmem ? dyn_smem() + C::kDynObs : obs_stage_s;
     SS_PROBE_SPAN(1);
     // JIT builds of large models keep the action / target vectors and the episodic sums in
@@ -1247,10 +1253,13 @@ __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniform
                     s.s_hist[h][i] = (need_hist && h < H && i < F) ? d.s_force_hist[((int64_t)h * F + i) * N + w] : 0.0;
         }
         // JIT: the hoisted model fields live in a shared-memory column (Params, S = kBlock)
-        constexpr int PS = C::kParamSmem ? C::kBlock : 0;
+        // (the physics-only kernel of a split env has no observation staging beside them: kParamSmemAlone)
+        constexpr bool kParUsed = FS == 0 || (FS & (SS_ST_PHYS | SS_ST_APPLY));
+        constexpr bool kParSmem = C::kParamSmem || (FS != 0 && !(FS & SS_ST_OBS) && C::kParamSmemAlone);
+        constexpr int PS = (kParSmem && kParUsed) ? C::kBlock : 0;
         using PT = Params<KM, C::kCapAct, PS>;
-        __shared__ double param_cols_s[(PS && !C::kDynSmem) ? PT::NV * PS : 1];
-        double* const param_cols = C::kDynSmem ? dyn_smem() + C::kDynParam : param_cols_s;
+        __shared__ double param_cols_s[(PS && !(C::kDynSmem && C::kParamSmem)) ? PT::NV * PS : 1];
+        double* const param_cols = (C::kDynSmem && C::kParamSmem) ? dyn_smem() + C::kDynParam : param_cols_s;
         PT P;
         P.p = param_cols + threadIdx.x;
         if (sim && (st & (SS_ST_PHYS | SS_ST_APPLY))) load_params<C, KM>(d, w, P, st & SS_ST_APPLY);
@@ -1770,6 +1779,7 @@ __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniform
     // sum nonfinite] (the ss_stats_pack layout) reduced in a fixed order -- lanes by shuffle tree,
     // warps in order, blocks in order by the last block to arrive -- so the vector is deterministic,
     // ready for the single all_reduce; one launch fewer per log interval than a separate pack
+    if constexpr (FS == 0 || (FS & SS_ST_REWARD))
     if (u.stats_out && (int)gridDim.x * (int)blockDim.x >= N && (int)blockDim.x <= C::kBlock) {
         // the warp partials reuse the observation staging buffer when there is one (its bulk copies
         // have been read: thread 0 waited on them before this barrier), keeping builds within 48 KB

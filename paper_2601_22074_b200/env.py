@@ -155,6 +155,7 @@ class ManagerBasedRlEnv:
         self._desc = None
         self._desc_ref = None
         self._jit_handle = None
+        self._jit_split = None  # (physics kernel, terms + observations kernel) of a split env
         self.use_jit = jit.enabled()
         self._lib = native.lib()
 
@@ -348,7 +349,9 @@ class ManagerBasedRlEnv:
         la = self._la
         if self.use_jit and self._jit_handle is None:
             try:
-                self._jit_handle = jit.module_for(d)
+                hs = jit.modules_for(d)
+                self._jit_handle = hs["main"]
+                self._jit_split = (hs["phys"], hs["post"]) if "phys" in hs else None
                 # the specialized kernel's parameter block: the descriptor
                 # packed to this env's counts (4 KB instead of 13 KB)
                 self._jit_packed = native.pack_desc(d, jit.desc_caps(d))
@@ -363,7 +366,7 @@ class ManagerBasedRlEnv:
             la.jit_desc_bytes = 0
 
     def _launch(self, stages: int, nsub: int = 0, actions=None, reset_mask=None, groups_mask: int = 0,
-                flags: int = 0) -> None:
+                flags: int = 0, handle=None) -> None:
         """One launch through the native runtime (ss_rt_launch): it derives the
         per-step uniforms from the shared ss_rt_state, launches the
         specialized (or generic) kernel and advances the counters."""
@@ -391,7 +394,7 @@ class ManagerBasedRlEnv:
             la.policy_slot = -1
         la.reset_mask = None if reset_mask is None else reset_mask.data_ptr()
         req = self._stats_req
-        if req is not None and stages == native.SS_ST_STEP_ALL:
+        if req is not None and stages in (native.SS_ST_STEP_ALL, jit.SPLIT_POST):
             # metrics.StatsPacker.request: this step also reduces the job statistics (fused tail)
             la.stats_out, la.stats_partials, la.stats_ticket, la.stats_rows = req
             self._stats_req = None
@@ -400,7 +403,7 @@ class ManagerBasedRlEnv:
         rt.sim_step = self.state.sim_step
         native.LAUNCHES["count"] += 1
         rc = self._lib.ss_rt_launch(self._desc_ref, self._rt_ref, self._la_ref,
-                                    self._jit_handle if self.use_jit else None,
+                                    (handle or self._jit_handle) if self.use_jit else None,
                                     native.current_stream(self._dev_index))
         if rc != 0:
             raise native.NativeError(f"ss_rt_launch failed ({rc}): {self._lib.ss_last_error().decode()}")
@@ -533,7 +536,18 @@ class ManagerBasedRlEnv:
         om._cache.clear()
         if not self.staged:
             mask = om.begin_all()
-            self._launch(native.SS_ST_STEP_ALL, nsub=self.decimation, actions=a, groups_mask=mask)
+            if a.__class__ is RandomActions:
+                self.streams.slot("policy.random")  # allocate before the handles are chosen
+            if self._desc is None or (self.use_jit and self._jit_handle is None):
+                self._prepare_launch()
+            if self.use_jit and self._jit_split is not None:
+                # split env (jit.split_enabled): physics, then terms + observations, two kernels each
+                # compiled for its stage set (fewer registers, more warps per SM at large N)
+                phys, post = self._jit_split
+                self._launch(jit.SPLIT_PHYS, nsub=self.decimation, actions=a, handle=phys)
+                self._launch(jit.SPLIT_POST, groups_mask=mask, handle=post)
+            else:
+                self._launch(native.SS_ST_STEP_ALL, nsub=self.decimation, actions=a, groups_mask=mask)
             self.curriculum_manager.run_host(None)
         else:
             self._step_staged(a)

@@ -182,7 +182,10 @@ def staging_layout(d, block: int, stage: int, obs_total: int) -> dict:
 
 def staging_config(d, block: int, stage: int, obs_total: int) -> str:
     L = staging_layout(d, block, stage, obs_total)
-    return (f"  static constexpr int kParamSmem = {L['param']}, kActSmem = {L['act']}, kDynSmem = {L['dyn']}, "
+    km, na = max(int(d.model.n_joints), 1), max(int(d.n_actuators), 1)
+    alone = int(os.environ.get("SS_PARAM_SMEM", "1") != "0" and (6 + 4 * km + 2 * na * km) * block * 8 + 64 <= 48 * 1024)
+    return (f"  static constexpr int kParamSmemAlone = {alone};\n"
+            f"  static constexpr int kParamSmem = {L['param']}, kActSmem = {L['act']}, kDynSmem = {L['dyn']}, "
             f"kDynObs = {L['obs_off']}, kDynParam = {L['param_off']}, kDynAct = {L['act_off']};")
 
 
@@ -225,23 +228,47 @@ def desc_caps(d) -> dict:
             "SLOTS": slots, "MLP_LAYERS": layers}
 
 
+SPLIT_PHYS = native.SS_ST_ACTION | native.SS_ST_APPLY | native.SS_ST_PUSH | native.SS_ST_PHYS | native.SS_ST_SENSOR
+SPLIT_POST = (native.SS_ST_TERM | native.SS_ST_REWARD | native.SS_ST_CURRICULUM | native.SS_ST_RESET
+              | native.SS_ST_COMMAND | native.SS_ST_EVENTS | native.SS_ST_OBS | native.SS_ST_PREV_AFTER)
+KERNELS = {"main": (KERNEL, 0), "phys": (KERNEL + "_phys", SPLIT_PHYS), "post": (KERNEL + "_post", SPLIT_POST)}
+
+
+def split_enabled(d) -> bool:
+    """Step in two launches of kernels compiled for fixed stage sets (physics | terms + observations):
+    each needs ~40 registers fewer than the whole body (244 -> 168 at block 128), 12 warps per SM
+    instead of 8 -- and the second re-reads ~400 B per world the first wrote. Measured slower at every
+    size (262,144 worlds 156 -> 162 us, 1,048,576 583 -> 622 us), so off unless SS_SPLIT=1
+    (or SS_SPLIT=auto: from SS_SPLIT_MIN worlds). Bit-identical to the fused launch (tested)."""
+    mode = os.environ.get("SS_SPLIT", "0")
+    if mode in ("0", "1"):
+        return mode == "1"
+    return int(d.n_worlds) >= int(os.environ.get("SS_SPLIT_MIN", "65536"))
+
+
 def kernel_source(d) -> str:
     k, f = int(d.model.n_joints), int(d.model.n_feet)
     caps = desc_caps(d)
     packed = ctypes.sizeof(native.packed_desc_type(caps))
-    return "\n".join([
+    lines = [
         *[f"#define SS_DCAP_{c} {v}" for c, v in caps.items()],
         f"#define SS_DCAP_ACTION_COLS {max(int(d.action_dim), 1)}",
         '#include "stridesim_b200.h"',
         f'static_assert(sizeof(ss_env_desc) == {packed}, "packed descriptor layout differs from the host packing");',
         '#include "ss_kernel.cuh"',
         config_source(d),
-        f"extern \"C\" __global__ void __launch_bounds__({block_size(d)}"
-        f"{', ' + str(min_blocks()) if min_blocks() else ''}) {KERNEL}(",
-        "    const __grid_constant__ ss_env_desc d, const __grid_constant__ ss_uniforms u) {",
-        f"  ss::step_body<JitCfg, {max(k, 1)}, {max(f, 1)}>(d, u);",
-        "}",
-    ]) + "\n"
+    ]
+    names = ["main"] + (["phys", "post"] if split_enabled(d) else [])
+    for which in names:
+        name, fs = KERNELS[which]
+        lines += [
+            f"extern \"C\" __global__ void __launch_bounds__({block_size(d)}"
+            f"{', ' + str(min_blocks()) if min_blocks() else ''}) {name}(",
+            "    const __grid_constant__ ss_env_desc d, const __grid_constant__ ss_uniforms u) {",
+            f"  ss::step_body<JitCfg, {max(k, 1)}, {max(f, 1)}, {fs}u>(d, u);",
+            "}",
+        ]
+    return "\n".join(lines) + "\n"
 
 
 def _headers():
@@ -317,9 +344,9 @@ def _store_cubin(path: str, cubin: bytes) -> None:
         pass
 
 
-def _load(cubin: bytes, d) -> int:
+def _load(cubin: bytes, d, name: str = KERNEL) -> int:
     handle = ctypes.c_void_p()
-    native.call("ss_jit_load", cubin, len(cubin), KERNEL.encode(), block_size(d), ctypes.byref(handle))
+    native.call("ss_jit_load", cubin, len(cubin), name.encode(), block_size(d), ctypes.byref(handle))
     native.call("ss_jit_set_desc_bytes", handle, ctypes.sizeof(native.packed_desc_type(desc_caps(d))))
     dyn = dyn_smem_bytes(d)
     if dyn:
@@ -327,30 +354,37 @@ def _load(cubin: bytes, d) -> int:
     return handle.value
 
 
-def module_for(d) -> int:
-    """Loaded kernel handle specialized for descriptor ``d`` on the current device (compiled on first use)."""
+def modules_for(d) -> dict:
+    """Loaded kernel handles specialized for descriptor ``d`` on the current device (compiled on first
+    use): {"main": whole step} and, for split envs, {"phys": ..., "post": ...}."""
     import torch
 
     src = kernel_source(d)
     key = hashlib.sha256((src + "|".join(options()) + "".join(open(p).read() for p in _HEADERS.values())).encode()).hexdigest()
     mkey = f"{key}@{torch.cuda.current_device()}"  # a module is loaded into one device's context
-    h = _MODULES.get(mkey)
-    if h is not None:
+    hs = _MODULES.get(mkey)
+    if hs is not None:
         STATS["memory_hits"] += 1
-        return h
+        return hs
+    names = ["main"] + (["phys", "post"] if split_enabled(d) else [])
     path = os.path.join(_cache_dir(), key + ".cubin")
-    handle = None
+    hs = None
     try:
         with open(path, "rb") as fh:
             cubin = fh.read()
-        handle = _load(cubin, d)
+        hs = {w: _load(cubin, d, KERNELS[w][0]) for w in names}
         STATS["disk_hits"] += 1
     except (OSError, native.NativeError):
-        handle = None  # absent or unloadable (e.g. truncated by a crashed writer): recompile
-    if handle is None:
+        hs = None  # absent or unloadable (e.g. truncated by a crashed writer): recompile
+    if hs is None:
         cubin = compile_cubin(src)
         STATS["compiled"] += 1
         _store_cubin(path, cubin)
-        handle = _load(cubin, d)
-    _MODULES[mkey] = handle
-    return handle
+        hs = {w: _load(cubin, d, KERNELS[w][0]) for w in names}
+    _MODULES[mkey] = hs
+    return hs
+
+
+def module_for(d) -> int:
+    """Loaded kernel handle of the whole step specialized for descriptor ``d``."""
+    return modules_for(d)["main"]

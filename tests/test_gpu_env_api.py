@@ -884,3 +884,32 @@ def test_copy_outputs_returns_fresh_tensors():
         assert torch.equal(o["policy"], snap_o) and torch.equal(r, snap_r)
     assert first.data_ptr() == views.reward_manager.reward.data_ptr()  # default: persistent buffer
     assert o0["policy"].data_ptr() != fresh.observation_manager.outputs()["policy"].data_ptr()
+
+
+@pytest.mark.gpu
+def test_split_launch_bitwise_equals_fused(monkeypatch):
+    """Large envs step as two kernels compiled for fixed stage sets (physics | terms + observations,
+    jit.split_enabled): bit-identical to the single fused launch, outputs and state."""
+    from paper_2601_22074_b200.env import ManagerBasedRlEnv
+    from paper_2601_22074_b200.policies import random_policy
+    from paper_2601_22074_b200.tasks import make_env_cfg
+
+    envs = []
+    for mode in ("0", "1"):
+        monkeypatch.setenv("SS_SPLIT", mode)
+        e = ManagerBasedRlEnv(make_env_cfg("Velocity-Rough", num_envs=4096, seed=8), "Velocity-Rough")
+        e.reset()
+        e.step(random_policy(e, 0, fused=True))
+        envs.append(e)
+    a, b = envs
+    assert a._jit_split is None and b._jit_split is not None
+    for i in range(1, 40):
+        for e in envs:
+            e.step(random_policy(e, i, fused=True))
+    torch.cuda.synchronize()
+    assert torch.equal(a.step_outputs, b.step_outputs)
+    for name in ("q", "qd", "ctrl", "ext_force", "time"):
+        assert torch.equal(getattr(a.state, name), getattr(b.state, name)), name
+    assert torch.equal(a.terrain_rows, b.terrain_rows)
+    assert np.array_equal(np.array(list(a.termination_manager.trigger_counts.values())),
+                          np.array(list(b.termination_manager.trigger_counts.values())))
