@@ -89,15 +89,18 @@ def test_headline_config_fused_policy_lockstep():
     assert resets > 0, "the window must exercise the masked reset path"
 
 
-@pytest.mark.parametrize("starts", [(0, 131072 - 1024, 262144 - 2048)])
-def test_at_scale_config_world_slices(starts):
-    """bench.py's at_scale launch: 262,144 worlds, fused random policy, world slices vs the oracle."""
+@pytest.mark.parametrize("n,m,starts", [(262144, 2048, (0, 131072 - 1024, 262144 - 2048)),
+                                         # block 128 with a partial last block (70001 = 546 x 128 + 113)
+                                         (70001, 1500, (0, 70001 - 1500))])
+def test_at_scale_config_world_slices(n, m, starts):
+    """bench.py's at_scale launch: 262,144 worlds, fused random policy, world slices vs the oracle
+    (and a large world count that is not a multiple of the block)."""
     from oracle import OracleEnv
     from paper_2601_22074_b200.env import ManagerBasedRlEnv
     from paper_2601_22074_b200.policies import random_policy
     from paper_2601_22074_b200.tasks import make_env_cfg
 
-    n, m, seed = 262144, 2048, 0
+    seed = 0
     env = ManagerBasedRlEnv(make_env_cfg(TASK, num_envs=n, seed=seed), TASK)
     assert env.use_jit
     refs = []
