@@ -322,14 +322,22 @@ def timed_steps(env, steps: int, flush, stream, policy, after=None, before=None)
 
 
 def at_scale(args, flush, stream) -> dict:
-    """The same step at a world count past the L2 (the roofline
-    fraction is quoted where the working set streams from HBM)."""
+    """The same step at world counts past the L2 (the roofline
+    fraction is quoted where the working set streams from HBM): --scale-envs
+    (262,144) and 4x that; the first is the line's `at_scale`, both are listed
+    in `at_scale.points`."""
+    pts = [_at_scale_point(args, flush, stream, n) for n in (args.scale_envs, 4 * args.scale_envs)]
+    out = dict(pts[0])
+    out["points"] = [{k: p[k] for k in ("envs", "value", "ms_per_step", "achieved_gbs", "frac")} for p in pts]
+    return out
+
+
+def _at_scale_point(args, flush, stream, n) -> dict:
     from paper_2601_22074_b200.env import ManagerBasedRlEnv
     from paper_2601_22074_b200.policies import random_policy
     from paper_2601_22074_b200.tasks import make_env_cfg
     from paper_2601_22074_b200.traffic import step_bytes_per_world
 
-    n = args.scale_envs
     env = ManagerBasedRlEnv(make_env_cfg(args.task, num_envs=n, seed=args.seed), args.task)
     env.reset()
     for i in range(5):
@@ -342,6 +350,9 @@ def at_scale(args, flush, stream) -> dict:
     out = {"envs": n, "value": n * steps / t, "unit": UNIT, "ms_per_step": 1e3 * t / steps,
            "achieved_gbs": gbs, "frac": gbs / peak, "bytes_per_env_step": per_world}
     del env
+    import torch
+
+    torch.cuda.empty_cache()
     return out
 
 

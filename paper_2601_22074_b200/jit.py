@@ -42,6 +42,8 @@ class JitUnsupported(RuntimeError):
 
 def options() -> list[str]:
     opts = list(OPTIONS)
+    if os.environ.get("SS_FMAD") == "1":  # experiment: let NVRTC contract a*b+c into FMA (not numpy's rounding)
+        opts = [o if o != "--fmad=false" else "--fmad=true" for o in opts]
     if os.environ.get("SS_PROBES") == "1":
         opts.append("-DSS_PROBES=1")
     # experiment switches, e.g. SS_JIT_DEFINES="-DSS_PEEL_LAST_SUBSTEP=0"

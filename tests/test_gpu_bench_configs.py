@@ -90,6 +90,7 @@ def test_headline_config_fused_policy_lockstep():
 
 
 @pytest.mark.parametrize("n,m,starts", [(262144, 2048, (0, 131072 - 1024, 262144 - 2048)),
+                                         (1048576, 1024, (0, 1048576 - 1024)),  # the at_scale leg's 4x point
                                          # block 128 with a partial last block (70001 = 546 x 128 + 113)
                                          (70001, 1500, (0, 70001 - 1500))])
 def test_at_scale_config_world_slices(n, m, starts):
