@@ -7,11 +7,13 @@ the tests check the distributed gradient algebra instead.
 
 Design: rollouts stay on the GPU (observations come straight from the env's
 output buffers, cast to float32 once); the actor-critic is two small MLPs
-(cuBLAS GEMMs -- library code, not the hot path of this repo); after each
-minibatch backward, all gradients are packed into ONE contiguous float32
-bucket and reduced with a single all_reduce (NCCL over NVLink between GPUs,
-gloo in CPU tests), i.e. one latency-bound collective of ~1.4 MB per
-minibatch instead of one per parameter tensor.
+(cuBLAS GEMMs -- library code, not the hot path of this repo -- in bf16 on the
+tensor cores during the update, distribution math in float32); parameters
+and gradients live in two flat float32 buffers, so after each minibatch
+backward the gradients already form ONE contiguous bucket, reduced in place
+with a single all_reduce (NCCL over NVLink between GPUs, gloo in CPU tests),
+i.e. one latency-bound collective of ~1.4 MB per minibatch instead of one per
+parameter tensor; fused Adam.
 """
 
 from __future__ import annotations
@@ -56,47 +58,58 @@ class ActorCritic(nn.Module):
         self.log_std = nn.Parameter(torch.full((n_actions,), float(torch.log(torch.tensor(cfg.init_std)))))
 
     def dist(self, obs_p):
-        mean = self.actor(obs_p)
+        mean = self.actor(obs_p).float()  # distribution math in float32 (the GEMMs may run in bf16)
         # validate_args=False: argument validation is a data-dependent check that
         # synchronizes the device on every call
         return torch.distributions.Normal(mean, self.log_std.exp().expand_as(mean), validate_args=False)
 
     def value(self, obs_c):
-        return self.critic(obs_c).squeeze(-1)
+        return self.critic(obs_c).squeeze(-1).float()
 
 
 class FlatGradReducer:
-    """All gradients of a module in one contiguous bucket, one collective."""
+    """All gradients of a module in one contiguous bucket, one collective.
+
+    At construction the module's parameters and gradients are re-pointed into
+    two flat float32 buffers (``flat_param`` / ``bucket``; each ``p.data`` /
+    ``p.grad`` becomes a view), so backward accumulates straight into the
+    bucket: ``reduce`` is a single in-place all_reduce (no gather / scatter
+    copies), ``zero_grad`` one fill, the gradient norm one reduction."""
 
     def __init__(self, module: nn.Module, group=None):
         self.params = [p for p in module.parameters() if p.requires_grad]
         self.numel = sum(p.numel() for p in self.params)
         self.group = group
-        self.bucket = torch.zeros(self.numel, dtype=torch.float32, device=self.params[0].device)
+        dev = self.params[0].device
+        self.flat_param = torch.empty(self.numel, dtype=torch.float32, device=dev)
+        self.bucket = torch.zeros(self.numel, dtype=torch.float32, device=dev)
+        off = 0
+        for p in self.params:
+            n = p.numel()
+            self.flat_param[off : off + n].copy_(p.data.reshape(-1))
+            p.data = self.flat_param[off : off + n].view_as(p)
+            g = self.bucket[off : off + n].view_as(p)
+            if p.grad is not None:
+                g.copy_(p.grad)
+            p.grad = g
+            off += n
 
     @property
     def world(self) -> int:
         return dist.get_world_size(self.group) if dist.is_available() and dist.is_initialized() else 1
 
+    def zero_grad(self) -> None:
+        self.bucket.zero_()
+
     def reduce(self) -> None:
-        off = 0
-        for p in self.params:
-            n = p.numel()
-            if p.grad is None:
-                self.bucket[off : off + n].zero_()
-            else:
-                self.bucket[off : off + n].copy_(p.grad.reshape(-1))
-            off += n
         if self.world > 1:
             dist.all_reduce(self.bucket, op=dist.ReduceOp.SUM, group=self.group)
             self.bucket.div_(self.world)
-        off = 0
-        for p in self.params:
-            n = p.numel()
-            if p.grad is None:
-                p.grad = torch.empty_like(p)
-            p.grad.copy_(self.bucket[off : off + n].view_as(p))
-            off += n
+
+    def clip_(self, max_norm: float) -> None:
+        """clip_grad_norm_ over the bucket: one norm, one scale, no host sync."""
+        norm = torch.linalg.vector_norm(self.bucket)
+        self.bucket.mul_(torch.clamp(max_norm / (norm + 1e-6), max=1.0))
 
 
 def broadcast_parameters(module: nn.Module, group=None) -> None:
@@ -155,8 +168,10 @@ class PpoTrainer:
         torch.manual_seed(seed)
         self.model = ActorCritic(self.n_p, self.n_c, self.n_a, self.cfg).to(env.device)
         broadcast_parameters(self.model, group)
-        self.opt = torch.optim.Adam(self.model.parameters(), lr=self.cfg.lr)
-        self.reducer = FlatGradReducer(self.model, group)
+        self.reducer = FlatGradReducer(self.model, group)  # parameters / gradients -> flat buffers
+        fused = env.device.type == "cuda"
+        self.opt = torch.optim.Adam(self.model.parameters(), lr=self.cfg.lr, fused=fused)
+        self.amp = fused  # bf16 GEMMs on the tensor cores in the update's forward / backward
         T, n = self.cfg.steps_per_env, env.num_envs
         dev = env.device
         self.buf = {
@@ -205,17 +220,20 @@ class PpoTrainer:
         adv, ret = adv.reshape(-1), ret.reshape(-1)
         mb = (T * n) // cfg.minibatches
         stats = {"loss": 0.0, "allreduces": 0}
+        last = None
         for _ in range(cfg.epochs):
             perm = torch.randperm(T * n, device=adv.device)
             for m in range(cfg.minibatches):
                 idx = perm[m * mb : (m + 1) * mb]
-                loss = ppo_loss(self.model, cfg, flat["obs_p"][idx], flat["obs_c"][idx], flat["act"][idx],
-                                flat["logp"][idx], adv[idx], ret[idx])
-                self.opt.zero_grad(set_to_none=False)
+                with torch.autocast("cuda", dtype=torch.bfloat16, enabled=self.amp):
+                    loss = ppo_loss(self.model, cfg, flat["obs_p"][idx], flat["obs_c"][idx], flat["act"][idx],
+                                    flat["logp"][idx], adv[idx], ret[idx])
+                self.reducer.zero_grad()
                 loss.backward()
                 self.reducer.reduce()
-                nn.utils.clip_grad_norm_(self.model.parameters(), cfg.max_grad_norm)
+                self.reducer.clip_(cfg.max_grad_norm)
                 self.opt.step()
                 stats["allreduces"] += 1
-                stats["loss"] = float(loss.detach()) if m == cfg.minibatches - 1 else stats["loss"]
+                last = loss.detach()
+        stats["loss"] = float(last) if last is not None else 0.0  # one host sync per update
         return stats
