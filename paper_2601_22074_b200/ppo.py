@@ -39,6 +39,7 @@ class PpoCfg:
     entropy_coef: float = 0.01
     max_grad_norm: float = 1.0
     init_std: float = 1.0
+    cuda_graph: bool = True  # capture the minibatch step (forward, backward, all-reduce, clip, Adam) once
 
 
 def _mlp(n_in: int, hidden, n_out: int) -> nn.Sequential:
@@ -170,8 +171,12 @@ class PpoTrainer:
         broadcast_parameters(self.model, group)
         self.reducer = FlatGradReducer(self.model, group)  # parameters / gradients -> flat buffers
         fused = env.device.type == "cuda"
-        self.opt = torch.optim.Adam(self.model.parameters(), lr=self.cfg.lr, fused=fused)
+        # one rank only: the multi-rank step keeps eager launches (collective capture not exercised here)
+        self.use_graph = fused and self.cfg.cuda_graph and self.reducer.world == 1
+        self.opt = torch.optim.Adam(self.model.parameters(), lr=self.cfg.lr, fused=fused,
+                                    capturable=self.use_graph)
         self.amp = fused  # bf16 GEMMs on the tensor cores in the update's forward / backward
+        self._graph = None
         T, n = self.cfg.steps_per_env, env.num_envs
         dev = env.device
         self.buf = {
@@ -209,31 +214,75 @@ class PpoTrainer:
             b["rew"][t] = rew.float() + self.cfg.gamma * b["val"][t] * (trunc & ~term).float()
             b["done"][t] = (term | trunc).float()
 
+    def _minibatch_step(self) -> None:
+        """One minibatch: forward (bf16 GEMMs), backward into the flat bucket, the bucket's single
+        all-reduce, clip, Adam -- on the static buffers (self._mb_idx selects the samples)."""
+        cfg, fl, idx = self.cfg, self._flat, self._mb_idx
+        with torch.autocast("cuda", dtype=torch.bfloat16, enabled=self.amp):
+            loss = ppo_loss(self.model, cfg, fl["obs_p"][idx], fl["obs_c"][idx], fl["act"][idx], fl["logp"][idx],
+                            self._adv[idx], self._ret[idx])
+        self.reducer.zero_grad()
+        loss.backward()
+        self.reducer.reduce()
+        self.reducer.clip_(cfg.max_grad_norm)
+        self.opt.step()
+        self._mb_loss.copy_(loss.detach())
+
+    def _ensure_static(self, T: int, n: int, mb: int) -> None:
+        if getattr(self, "_flat", None) is not None:
+            return
+        b = self.buf
+        self._flat = {k: v.reshape(T * n, *v.shape[2:]) for k, v in b.items()}  # views of the rollout buffers
+        dev = b["rew"].device
+        self._adv = torch.zeros(T * n, device=dev)
+        self._ret = torch.zeros(T * n, device=dev)
+        self._mb_idx = torch.zeros(mb, dtype=torch.int64, device=dev)
+        self._mb_loss = torch.zeros((), device=dev)
+
+    def _capture(self) -> None:
+        """Record the minibatch step as one CUDA graph (after warm-up iterations on a side stream, as
+        graph capture requires): a minibatch then costs one graph launch instead of ~100 kernel launches
+        from Python -- the update was launch-bound."""
+        saved = self.reducer.flat_param.clone()  # the warm-up steps must not train: restore after them
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            for _ in range(3):
+                self._minibatch_step()
+        torch.cuda.current_stream().wait_stream(s)
+        self._graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self._graph):
+            self._minibatch_step()
+        # back to the state before the warm-up: the parameters, and Adam's moments and step (created by
+        # the warm-up -- the graph is recorded at the first update -- so zero is their initial value)
+        self.reducer.flat_param.copy_(saved)
+        for p, st in self.opt.state.items():
+            for k, v in st.items():
+                if torch.is_tensor(v):
+                    v.zero_()
+
     def update(self) -> dict:
         cfg, b = self.cfg, self.buf
+        T, n = b["rew"].shape
+        mb = (T * n) // cfg.minibatches
+        self._ensure_static(T, n, mb)
         with torch.no_grad():
             _, c = self._split(self.obs)
             adv, ret = gae(b["rew"], b["val"], b["done"], self.model.value(c), cfg.gamma, cfg.lam)
             adv = normalize_advantages(adv, self.reducer.group)
-        T, n = b["rew"].shape
-        flat = {k: v.reshape(T * n, *v.shape[2:]) for k, v in b.items()}
-        adv, ret = adv.reshape(-1), ret.reshape(-1)
-        mb = (T * n) // cfg.minibatches
+            self._adv.copy_(adv.reshape(-1))
+            self._ret.copy_(ret.reshape(-1))
         stats = {"loss": 0.0, "allreduces": 0}
-        last = None
         for _ in range(cfg.epochs):
-            perm = torch.randperm(T * n, device=adv.device)
+            perm = torch.randperm(T * n, device=self._adv.device)
             for m in range(cfg.minibatches):
-                idx = perm[m * mb : (m + 1) * mb]
-                with torch.autocast("cuda", dtype=torch.bfloat16, enabled=self.amp):
-                    loss = ppo_loss(self.model, cfg, flat["obs_p"][idx], flat["obs_c"][idx], flat["act"][idx],
-                                    flat["logp"][idx], adv[idx], ret[idx])
-                self.reducer.zero_grad()
-                loss.backward()
-                self.reducer.reduce()
-                self.reducer.clip_(cfg.max_grad_norm)
-                self.opt.step()
+                self._mb_idx.copy_(perm[m * mb : (m + 1) * mb])
+                if self.use_graph:
+                    if self._graph is None:
+                        self._capture()
+                    self._graph.replay()
+                else:
+                    self._minibatch_step()
                 stats["allreduces"] += 1
-                last = loss.detach()
-        stats["loss"] = float(last) if last is not None else 0.0  # one host sync per update
+        stats["loss"] = float(self._mb_loss) if stats["allreduces"] else 0.0  # one host sync per update
         return stats

@@ -913,3 +913,30 @@ def test_split_launch_bitwise_equals_fused(monkeypatch):
     assert torch.equal(a.terrain_rows, b.terrain_rows)
     assert np.array_equal(np.array(list(a.termination_manager.trigger_counts.values())),
                           np.array(list(b.termination_manager.trigger_counts.values())))
+
+
+@pytest.mark.gpu
+def test_ppo_update_graph_equals_eager():
+    """The CUDA-graph minibatch step trains exactly like the eager one (same parameters after the
+    update, from the same rollout and the same random permutations)."""
+    from paper_2601_22074_b200.env import ManagerBasedRlEnv
+    from paper_2601_22074_b200.ppo import PpoCfg, PpoTrainer
+    from paper_2601_22074_b200.tasks import make_env_cfg
+
+    params = []
+    for graph in (False, True):
+        env = ManagerBasedRlEnv(make_env_cfg("Velocity-Flat", num_envs=256, seed=1))
+        tr = PpoTrainer(env, PpoCfg(hidden=(64, 64), steps_per_env=8, epochs=2, minibatches=2, cuda_graph=graph),
+                        seed=3)
+        torch.manual_seed(5)
+        tr.collect()
+        torch.manual_seed(6)
+        tr.update()
+        torch.manual_seed(7)
+        tr.collect()
+        torch.manual_seed(8)
+        st = tr.update()
+        torch.cuda.synchronize()
+        assert (tr._graph is not None) == graph and np.isfinite(st["loss"])
+        params.append(tr.reducer.flat_param.clone())
+    torch.testing.assert_close(params[0], params[1], rtol=1e-5, atol=1e-6)
