@@ -523,7 +523,10 @@ class ManagerBasedRlEnv:
         if self.copy_outputs:
             v = self.unpack_outputs(self.step_outputs.clone())  # one D2D copy of the whole arena
             obs = {g: v[f"obs/{g}"] for g in self.observation_manager.outputs()}
-            return obs, v["reward"], v["terminated"], v["truncated"], _Extras(self, self.global_step)
+            # extras too are fresh values of this step (built now, not lazily from live buffers)
+            x = _Extras(self, self.global_step)
+            x._data = {k: (t.clone() if hasattr(t, "clone") else t) for k, t in x._build().items()}
+            return obs, v["reward"], v["terminated"], v["truncated"], x
         return (self.observation_manager.outputs(), self.reward_manager.reward, tm.terminated, tm.truncated,
                 _Extras(self, self.global_step))
 

@@ -882,6 +882,11 @@ def test_copy_outputs_returns_fresh_tensors():
             first = rv
     for snap_o, snap_r, o, r in kept:  # earlier steps' tensors were not overwritten
         assert torch.equal(o["policy"], snap_o) and torch.equal(r, snap_r)
+    _, _, _, _, x1 = fresh.step(random_policy(fresh, 10))
+    rows = x1["curriculum/terrain_rows"].clone()
+    fresh.terrain_rows.add_(1)  # later changes to the env do not reach an earlier step's extras
+    assert torch.equal(x1["curriculum/terrain_rows"], rows)
+    fresh.terrain_rows.sub_(1)
     assert first.data_ptr() == views.reward_manager.reward.data_ptr()  # default: persistent buffer
     assert o0["policy"].data_ptr() != fresh.observation_manager.outputs()["policy"].data_ptr()
 
