@@ -235,7 +235,7 @@ __global__ void __launch_bounds__(kStatsBlock) stats_pack_kernel(const __grid_co
     }
     __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) last = atomicAdd(a.ticket, 1u) == gridDim.x - 1;
+    if (threadIdx.x == 0) last = atomicInc(a.ticket, gridDim.x - 1) == gridDim.x - 1;  // wraps to 0
     __syncthreads();
     if (!last) return;
     __threadfence();
@@ -251,10 +251,7 @@ __global__ void __launch_bounds__(kStatsBlock) stats_pack_kernel(const __grid_co
         a.out[o] = acc;
     }
     for (int c = threadIdx.x; c < C; c += blockDim.x) a.out[2 + T + c] = (double)a.trigger_counts[c];
-    if (threadIdx.x == 0) {
-        a.out[0] = (double)N;
-        *a.ticket = 0u;  // ready for the next launch on this stream
-    }
+    if (threadIdx.x == 0) a.out[0] = (double)N;
 }
 
 extern "C" int ss_stats_pack(const ss_stats_args* a, void* stream) {

@@ -1811,7 +1811,8 @@ __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniform
         }
         __threadfence();  // partials and this block's trigger-count atomics before the ticket
         __syncthreads();
-        if (threadIdx.x == 0) last = atomicAdd(u.stats_ticket, 1u) == gridDim.x - 1;
+        // atomicInc wraps the ticket back to 0 at the last arrival: ready for the next launch
+        if (threadIdx.x == 0) last = atomicInc(u.stats_ticket, gridDim.x - 1) == gridDim.x - 1;
         __syncthreads();
         if (last) {
             __threadfence();
@@ -1825,10 +1826,7 @@ __device__ __forceinline__ void step_body(const ss_env_desc& d, const ss_uniform
             }
             for (int c = threadIdx.x; c < Cn; c += blockDim.x)
                 u.stats_out[2 + T + c] = (double)((volatile unsigned long long*)d.trigger_counts)[c];
-            if (threadIdx.x == 0) {
-                u.stats_out[0] = (double)N;
-                *u.stats_ticket = 0u;
-            }
+            if (threadIdx.x == 0) u.stats_out[0] = (double)N;
         }
     }
     SS_PROBE_SPAN(0);

@@ -21,7 +21,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 @pytest.mark.skipif(not os.path.isfile(os.path.join(ROOT, "baseline", "_ref_tests", "test_env.py")),
                     reason="reference tests not copied (tools/reftests/run.sh prepare)")
 def test_reference_test_suite_passes_against_the_package():
-    out = subprocess.run([os.path.join(ROOT, "tools", "reftests", "run.sh"), "-q"], capture_output=True, text=True,
+    out = subprocess.run([os.path.join(ROOT, "tools", "reftests", "run.sh")], capture_output=True, text=True,
                          timeout=1200)
     tail = (out.stdout + out.stderr)[-3000:]
     m = re.search(r"(\d+) passed", tail)
