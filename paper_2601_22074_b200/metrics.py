@@ -107,6 +107,7 @@ class StatsPacker:
             self._fticket = torch.zeros(1, dtype=torch.int32, device=env.device)
         out = self.out if out is None else out
         env._stats_req = (out.data_ptr(), self._fpartials.data_ptr(), self._fticket.data_ptr(), self.n_rows)
+        env._stats_req_out = out  # keeps the destination alive until the launch has consumed the request
         return out
 
     def pack(self, reward=None):
