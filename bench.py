@@ -269,6 +269,10 @@ def dist_setup(gpus, backend="nccl"):
 
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         if backend == "nccl":
+            # communicator setup (rank count, NVLink / NVLS transport) logged -- to stderr, so stdout
+            # carries nothing but rank 0's JSON line
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
@@ -664,11 +668,13 @@ def run_ours(args):
             "gpu_launches": launches,
             "clocks": clk,
         }
-        print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
 
+        dist.barrier()
         dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(line), flush=True)  # last: after the communicator's teardown messages
 
 
 def run_reference(args):
@@ -774,7 +780,8 @@ def self_launch(argv) -> int:
         elif a.startswith("--gpus="):
             gpus = int(a.split("=", 1)[1])
     env = dict(os.environ)
-    env.setdefault("NCCL_DEBUG", "INFO")  # communicator setup on stderr (rank count, NVLS / NVLink transport)
+    env.setdefault("NCCL_DEBUG", "INFO")  # communicator setup (rank count, NVLS / NVLink transport) ...
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")  # ... on stderr: stdout is the JSON line
     env.setdefault("OMP_NUM_THREADS", "1")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
            "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *argv]
