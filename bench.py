@@ -1,7 +1,7 @@
 """Benchmark: env-steps/s of the batched ManagerBasedRlEnv.step on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--envs 4096] [--task Velocity-Rough]
-    python bench.py --impl reference ...      # the CPU implementation of the path (oracle port)
+    python bench.py --impl reference ...      # the unmodified reference on the host cores
 
 Workload (BASELINE.json configs[1] restated): Velocity-Rough,
 the planar biped on the 5x6 curriculum heightfield, 4096 worlds per GPU,
@@ -9,16 +9,19 @@ decimation 4, random actions from the per-world policy.random streams, drawn
 inside the timed region like cli.py:163 -- by the step kernel itself
 (policies.RandomActions; the same values as random_policy's separate draw,
 tests/test_gpu_env_api.py). One step = one control step of every world (4
-physics substeps each) = one kernel launch. --scale-envs adds the same step
-at 262144 worlds, where the working set streams from HBM. Multi-GPU: one
-process per GPU, world_id_offset = rank * N (weak scaling, no collective on
-the data path); time = max over ranks.
+physics substeps each) = one kernel launch; every --log-every steps that
+launch also reduces the job statistics, all-reduced across ranks. Multi-GPU:
+one process per GPU (self-launched with torch.distributed.run when WORLD_SIZE
+is unset), world_id_offset = rank * N (weak scaling, no collective on the
+data path); time = max over ranks.
 
 Timing: W untimed warm-up steps; then K steps, each preceded by an L2 flush
 (a 512 MiB write, untimed) and bracketed by CUDA events on the launching
 stream; barrier + synchronize around the whole region. The JSON line adds the
-roofline of the fused step kernel, the CPU baseline (oracle port on the host
-cores), and an end-to-end figure through the public API with host buffers.
+roofline of the fused step kernel (and the same step at 262,144 / 1,048,576
+worlds), the CPU baseline (the unmodified reference on the host cores), an
+end-to-end figure through the public API with host buffers, the 3-D path's
+legs and a PPO training leg with its gradient all-reduce (f2).
 """
 
 from __future__ import annotations
@@ -470,6 +473,45 @@ def sim3d_leg(args, flush, stream) -> dict:
     return out
 
 
+def ppo_leg(args, rank: int, world: int) -> dict:
+    """BASELINE configs[4]'s "incl. PPO gradient allreduce": the on-device PPO learner (ppo.py) on this
+    rank's Velocity-Rough shard -- every minibatch's gradients reduced across ranks as ONE flat bucket
+    (NCCL; the minibatch step is one CUDA graph at one rank). Whole-job training env-steps/s over a few
+    iterations (collect + update), time = max over ranks."""
+    import torch
+
+    from paper_2601_22074_b200.env import ManagerBasedRlEnv
+    from paper_2601_22074_b200.ppo import PpoCfg, PpoTrainer
+    from paper_2601_22074_b200.tasks import make_env_cfg
+
+    n = args.envs
+    cfg = make_env_cfg(args.task, num_envs=n, seed=args.seed)
+    cfg.scene.world_id_offset = rank * n
+    env = ManagerBasedRlEnv(cfg, args.task)
+    tr = PpoTrainer(env, PpoCfg(), seed=args.seed)
+    tr.collect()
+    tr.update()  # warm-up (graph capture at one rank)
+    torch.cuda.synchronize()
+    barrier(world)
+    iters = 3
+    t0 = time.perf_counter()
+    st = None
+    for _ in range(iters):
+        tr.collect()
+        st = tr.update()
+    torch.cuda.synchronize()
+    t = allmax(time.perf_counter() - t0, world)
+    steps = iters * tr.cfg.steps_per_env * n * world
+    out = {"workload": f"PPO on {args.task}, {n} worlds per GPU, {tr.cfg.steps_per_env} steps x {world} GPU(s) "
+                       f"per iteration, MLPs {'-'.join(str(h) for h in tr.cfg.hidden)}",
+           "unit": UNIT, "train_env_steps_per_s": steps / t, "iterations": iters,
+           "allreduces_per_iter": st["allreduces"], "grad_bucket_floats": tr.reducer.numel,
+           "cuda_graph": tr._graph is not None, "collective": "NCCL all_reduce" if world > 1 else "none (1 rank)",
+           "parity": "unpinned (the reference has no learner, SPEC.md:509)"}
+    del tr, env
+    return out
+
+
 def sim3d_cpu(seed, worlds=4, steps=2) -> dict:
     """The 3-D oracle (numpy, one core) on a bounded sample of the same task."""
     from oracle import sim3d as O
@@ -613,6 +655,7 @@ def run_ours(args):
 
     scale = at_scale(args, flush, stream) if (world == 1 and args.scale_envs > 0) else None
     s3 = None if args.no_sim3d else sim3d_leg(args, flush, stream)
+    ppo = None if args.no_ppo else ppo_leg(args, rank, world)
     # the headline region lasts ~1 ms (shorter than nvidia-smi's 100 ms period): the sampler runs from just
     # before it through the e2e, at-scale and 3-D legs, so its samples are of the GPU under this load
     clk = clocks.stop()
@@ -663,6 +706,7 @@ def run_ours(args):
             "shards": {"world_id_offsets": offsets, "envs_per_rank": n},
             "at_scale": scale,
             "sim3d": s3,
+            "ppo": ppo,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
@@ -803,6 +847,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true", help="skip the end-to-end leg (profiling runs)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-sim3d", action="store_true", help="skip the 3-D (SURVEY 8 f4) leg")
+    ap.add_argument("--no-ppo", action="store_true", help="skip the PPO training leg (SURVEY 8 f2)")
     ap.add_argument("--dry-cpu", action="store_true", help="multi-rank plumbing on CPU (gloo + oracle), for tests")
     ap.add_argument("--scale-envs", type=int, default=262144,
                     help="also time the step at this many worlds (HBM-bound regime); 0 disables")
