@@ -105,3 +105,34 @@ def test_traffic_model_constants():
 
 def test_pendulum_spec_valid():
     pendulum_spec().validate()
+
+
+def test_jit_staging_layout_decisions(monkeypatch):
+    """The specialized kernel's shared-memory staging (jit.staging_layout): the biped keeps the model
+    fields in static shared memory beside the observation rows; a 12-joint model also moves its action /
+    target vectors and episodic sums there and needs the dynamic block (> 48 KB); block 128 (large N)
+    drops the biped's field columns (they no longer fit beside 128 observation rows)."""
+    from paper_2601_22074_b200 import jit, native
+
+    def desc(k, a, rewards, groups):
+        d = native.EnvDesc()
+        d.model.n_joints, d.n_actuators, d.action_dim, d.n_rewards = k, 1, a, rewards
+        d.n_groups = len(groups)
+        for g, dim in enumerate(groups):
+            d.group[g].dim = dim
+        return d
+
+    for var in ("SS_PARAM_SMEM", "SS_ACT_SMEM", "SS_DYN_SMEM_MAX", "SS_STAGE_OBS"):
+        monkeypatch.delenv(var, raising=False)
+    biped = desc(4, 4, 7, (19, 28))
+    L = jit.staging_layout(biped, 64, jit.obs_staged(biped, 64), 47)
+    assert (L["param"], L["act"], L["dyn"]) == (1, 0, 0)
+    L = jit.staging_layout(biped, 128, jit.obs_staged(biped, 128), 47)
+    assert (L["param"], L["act"], L["dyn"]) == (0, 0, 0)
+    quad = desc(12, 12, 7, (43, 51))
+    L = jit.staging_layout(quad, 64, jit.obs_staged(quad, 64), 94)
+    assert L["param"] == 1 and L["act"] == 1 and 48 * 1024 < L["dyn"] <= 112 * 1024
+    assert L["obs_off"] == 0 < L["param_off"] < L["act_off"]
+    monkeypatch.setenv("SS_ACT_SMEM", "0")
+    L = jit.staging_layout(quad, 64, jit.obs_staged(quad, 64), 94)
+    assert (L["act"], L["dyn"]) == (0, 0)
