@@ -706,7 +706,7 @@ int ss_rt_launch(const ss_env_desc* desc, ss_rt_state* st, const ss_launch* l, v
 int ss_rt_poll(ss_rt_state* st, int32_t keep, int32_t* out_slots, int32_t max_out);
 int ss_rt_release(ss_rt_state* st);
 
-/* Pipelined host I/O for env.step_async / env.step_wait (gym VectorEnv style), nslot in [2, 4] slots:
+/* Pipelined host I/O for env.step_async / env.step_wait (gym VectorEnv style), nslot in [2, 8] slots:
  * ss_pipe_pre copies a step's actions from pinned host memory into the slot's device buffer on a
  * copy stream (the launching stream waits for it) and returns the slot; ss_pipe_post snapshots the
  * output arena into the slot's staging buffer (SM copy kernel) and copies it to a pinned host block

@@ -176,13 +176,13 @@ __global__ void arena_copy_kernel(const int4* __restrict__ src, int4* __restrict
 
 struct Pipe {
     cudaStream_t in = nullptr, out = nullptr;
-    cudaEvent_t in_done[4] = {}, snap[4] = {}, out_done[4] = {};
-    bool used[4] = {false, false, false, false};
+    cudaEvent_t in_done[8] = {}, snap[8] = {}, out_done[8] = {};
+    bool used[8] = {};
     int nslot = 2;
     int64_t submitted = 0, waited = 0;
-    void* dev_actions[4] = {};
-    void* stage[4] = {};
-    void* host[5] = {};  // nslot + 1 pinned blocks: a view step_wait returned survives the next step_async
+    void* dev_actions[8] = {};
+    void* stage[8] = {};
+    void* host[9] = {};  // nslot + 1 pinned blocks: a view step_wait returned survives the next step_async
     int64_t action_bytes = 0, arena_bytes = 0;
 };
 
@@ -195,8 +195,8 @@ int pipe_err(cudaError_t e, const char* what) {
 
 extern "C" int ss_pipe_create(int32_t nslot, void* const* dev_actions, void* const* stage, void* const* host,
                               int64_t action_bytes, int64_t arena_bytes, void** out) {
-    if (!dev_actions || !stage || !host || !out || arena_bytes <= 0 || action_bytes < 0 || nslot < 2 || nslot > 4) {
-        ss_set_error("ss_pipe_create", "null buffer, empty arena or nslot outside [2, 4]");
+    if (!dev_actions || !stage || !host || !out || arena_bytes <= 0 || action_bytes < 0 || nslot < 2 || nslot > 8) {
+        ss_set_error("ss_pipe_create", "null buffer, empty arena or nslot outside [2, 8]");
         return -1;
     }
     Pipe* p = new Pipe();
