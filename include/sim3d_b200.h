@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define S3_ABI_VERSION 17
+#define S3_ABI_VERSION 18
 #define S3_F64 0
 #define S3_F32 1
 
@@ -34,6 +34,9 @@ extern "C" {
 #define S3_MAX_ROWS 96
 #define S3_MAX_RAYS 128
 #define S3_MAX_TREE 4
+#define S3_MAX_TRACK 16 /* tracked bodies of the motion task (besides the anchor) */
+#define S3_MAX_SENSOR 4 /* contact sensors */
+#define S3_BODY_STATE 13 /* pos[3] quat[4] linvel[3] angvel[3] (world frame; linvel of the body origin) */
 
 #define S3_OK 0
 #define S3_ERR_ARG 1
@@ -239,16 +242,28 @@ typedef struct s3_task {
     double spawn_half_extent;
     double cmd_lo[3];
     double cmd_hi[3];
-    double reward_weights[6];
+    double reward_weights[10];
     double noise[7];
     double scan_xy[256];
     double scan_offset;
     double scan_noise;
     double frame_dt;
-    double motion_sigmas[4];
+    double motion_sigmas[8];
     double max_height_error;
     double max_ori_error;
     double motion_start_frac;
+    /* motion kind, BeyondMimic's relative body terms: the anchor body and the tracked bodies; the clip's
+     * body states (S3_BODY_STATE per body, anchor first) come from s3_motion_bodies */
+    int32_t anchor_body;
+    int32_t ntrack;
+    int32_t track_body[S3_MAX_TRACK];
+    /* contact sensors (every kind): bit s of pair_sensor[p] makes the contacts of collision pair p count
+     * toward sensor s; sensor[w * nsensor + s] = the most such contacts any substep of the control step saw */
+    int32_t nsensor;
+    int32_t pad5;
+    const uint8_t* pair_sensor; /* (npair,) */
+    void* sensor;               /* (N, nsensor) */
+    const void* motion_body;    /* (nframes, 1 + ntrack, S3_BODY_STATE) */
     int32_t cube_qposadr;
     int32_t tip_geom[2];
     int32_t pad2;
@@ -322,6 +337,14 @@ int s3_step(const s3_model* m, const s3_data* d, const s3_layout* l, int32_t nsu
  * mode 1 resets every world (counter 0 draws) and writes the first observation; actions unused. */
 int s3_env_step(const s3_model* m, const s3_data* d, const s3_layout* l, const s3_task* t, const void* actions,
                 int32_t mode, int64_t global_step, void* stream);
+
+/* Body states of a motion clip (the per-frame body_pos_w / body_quat_w / body_lin_vel_w / body_ang_vel_w a
+ * BeyondMimic motion file carries): for each of t->nframes frames of t->motion_qpos / t->motion_qvel, forward
+ * kinematics + the dof motion vectors of that frame, then for the anchor body and each tracked body its
+ * world position, orientation, origin linear velocity and angular velocity, written to
+ * out[(f * (1 + ntrack) + k) * S3_BODY_STATE ...] (k = 0 the anchor). One warp per frame. The motion kind
+ * of s3_env_step reads the table through t->motion_body. */
+int s3_motion_bodies(const s3_model* m, const s3_layout* l, const s3_task* t, void* out, void* stream);
 
 /* Ray casting against every geom of each world (frames from s3_step / s3_env_step geom outputs):
  * nearest hit distance along o + t d (|d| = 1, t <= max_dist), -1 and geom -1 on a miss; geoms on

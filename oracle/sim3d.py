@@ -791,6 +791,30 @@ class TaskOracle:
         self.level = np.zeros(nworld, dtype=np.int64)   # terrain curriculum row
         self.spawn = np.zeros((nworld, 2))
         self.cmd_dist = np.zeros(nworld)
+        self.sensors = tuple(cfg.sensors(m)) if hasattr(cfg, "sensors") else ()
+        self.sensor = np.zeros((nworld, len(self.sensors)))
+
+    def _contact_counts(self, contacts):
+        """Contacts of each sensor among one substep's (kept) contacts: one geom in the sensor's first set,
+        the other in its second (None: any)."""
+        out = np.zeros(len(self.sensors))
+        for c in contacts:
+            g1, g2 = c["geom1"], c["geom2"]
+            for k, (_, a, b) in enumerate(self.sensors):
+                if (g1 in a and (b is None or g2 in b)) or (g2 in a and (b is None or g1 in b)):
+                    out[k] += 1.0
+        return out
+
+    def _substeps(self, w, ctrl, fscale=1.0, mscale=1.0):
+        """decimation substeps of world w; sensor[w] = the most contacts of each sensor in one substep."""
+        q, v, warm = self.qpos[w], self.qvel[w], self.warm[w]
+        found = np.zeros(len(self.sensors))
+        for _ in range(self.cfg.decimation):
+            q, v, warm, F = step(self.m, q, v, ctrl, warm=warm, fscale=fscale, mscale=mscale)
+            found = np.maximum(found, self._contact_counts(F["contacts"]))
+        self.qpos[w], self.qvel[w], self.warm[w] = q, v, warm
+        self.sensor[w] = found
+        return q, v, found
 
     def _curriculum_on(self):
         return getattr(self.cfg, "curriculum", None) is not None
@@ -903,10 +927,7 @@ class TaskOracle:
             self.prev_action[w] = self.action[w]
             self.action[w] = a
             ctrl = self.act_default + cfg.action_scale * a
-            q, v, warm = self.qpos[w], self.qvel[w], self.warm[w]
-            for _ in range(cfg.decimation):
-                q, v, warm, _ = step(m, q, v, ctrl, warm=warm, fscale=self.fscale[w], mscale=self.mscale[w])
-            self.qpos[w], self.qvel[w], self.warm[w] = q, v, warm
+            q, v, _ = self._substeps(w, ctrl, self.fscale[w], self.mscale[w])
             vb, om, g, _ = base_frame(m, q, v)
             e_xy = (self.cmd[w, 0] - vb[0]) ** 2 + (self.cmd[w, 1] - vb[1]) ** 2
             terms = (np.exp(-e_xy / cfg.track_sigma), np.exp(-((self.cmd[w, 2] - om[2]) ** 2) / cfg.track_sigma),
@@ -1130,9 +1151,83 @@ def motion_ref(cfg, t):
     return q, v
 
 
+def body_state(m, K, C, qvel, b):
+    """World state of body b: position, orientation, linear velocity of its origin, angular velocity
+    (the sum of the motion vectors of the dofs on its chain, about the tree's com)."""
+    v = np.zeros(6)
+    for d in m.body_chain[b]:
+        v = v + C["cdof"][d] * qvel[d]
+    r = K["xpos"][b] - C["com"][m.body_treeid[b]]
+    return np.concatenate([K["xpos"][b], K["xquat"][b], v[3:6] + np.cross(v[0:3], r), v[0:3]])
+
+
+def motion_body_table(m, cfg):
+    """(F, 1 + ntrack, 13) clip body states, anchor first (s3_motion_bodies)."""
+    anchor, bodies = cfg.tracked(m)
+    Q, V = cfg.motion_qpos, cfg.motion_qvel
+    out = np.zeros((Q.shape[0], 1 + len(bodies), 13))
+    for f in range(Q.shape[0]):
+        K = kinematics(m, Q[f])
+        C = com_pos(m, K)
+        for k, b in enumerate((anchor,) + tuple(bodies)):
+            out[f, k] = body_state(m, K, C, V[f], b)
+    return out
+
+
+def motion_body_ref(cfg, table, t):
+    """Clip body states at motion time t (linear; quaternion nlerp with sign alignment)."""
+    F = table.shape[0]
+    f = t / cfg.motion_dt
+    i0 = min(max(int(np.floor(f)), 0), F - 2)
+    a = f - i0
+    b0, b1 = table[i0], table[i0 + 1]
+    o = (1.0 - a) * b0 + a * b1
+    for k in range(table.shape[1]):
+        if b0[k, 3:7] @ b1[k, 3:7] < 0.0:
+            o[k, 3:7] = (1.0 - a) * b0[k, 3:7] - a * b1[k, 3:7]
+        o[k, 3:7] /= np.sqrt(o[k, 3:7] @ o[k, 3:7])
+    return o
+
+
+def quat_err2(a, b):
+    """Squared angle of the rotation conj(a) b."""
+    e = qmul(qconj(a), b)
+    ang = 2.0 * np.arctan2(np.sqrt(e[1:4] @ e[1:4]), abs(e[0]))
+    return ang * ang
+
+
 class MotionTaskOracle(TaskOracle):
     """Per-world numpy restatement of the motion-imitation kind of the fused 3-D task.
     cmd[w] = (motion time, anchor x, anchor y)."""
+
+    def __init__(self, m, cfg, nworld, seed=0, world_offset=0):
+        super().__init__(m, cfg, nworld, seed, world_offset)
+        self.anchor, self.bodies = cfg.tracked(m)
+        self.body_table = motion_body_table(m, cfg)
+
+    def body_errors(self, w):
+        """BeyondMimic's body errors (means over the tracked bodies): position and orientation with the
+        clip's bodies re-expressed about the robot's anchor (its xy, the clip anchor's height over the terrain
+        under the spawn anchor, the yaw between the anchors), world linear and angular velocity."""
+        m = self.m
+        K = kinematics(m, self.qpos[w])
+        C = com_pos(m, K)
+        rb = [body_state(m, K, C, self.qvel[w], b) for b in (self.anchor,) + tuple(self.bodies)]
+        rf = motion_body_ref(self.cfg, self.body_table, self.cmd[w, 0])
+        pa, qa, pr, qr = rb[0][0:3], rb[0][3:7], rf[0, 0:3], rf[0, 3:7]
+        dq = qmul(qa, qconj(qr))
+        yaw = np.arctan2(2.0 * (dq[0] * dq[3] + dq[1] * dq[2]), 1.0 - 2.0 * (dq[2] * dq[2] + dq[3] * dq[3]))
+        dy = np.array([np.cos(0.5 * yaw), 0.0, 0.0, np.sin(0.5 * yaw)])
+        tz = pr[2] + terrain_height(m, pr[0] + self.cmd[w, 1], pr[1] + self.cmd[w, 2])
+        R = qmat(dy)
+        e = np.zeros(4)
+        for k in range(1, len(rb)):
+            p = np.array([pa[0], pa[1], tz]) + R @ (rf[k, 0:3] - pr)
+            e[0] += float((p - rb[k][0:3]) @ (p - rb[k][0:3]))
+            e[1] += quat_err2(qmul(dy, rf[k, 3:7]), rb[k][3:7])
+            e[2] += float((rf[k, 7:10] - rb[k][7:10]) @ (rf[k, 7:10] - rb[k][7:10]))
+            e[3] += float((rf[k, 10:13] - rb[k][10:13]) @ (rf[k, 10:13] - rb[k][10:13]))
+        return e / len(self.bodies)
 
     def clip_end(self):
         return (self.cfg.motion_qpos.shape[0] - 1) * self.cfg.motion_dt
@@ -1204,18 +1299,18 @@ class MotionTaskOracle(TaskOracle):
             self.prev_action[w] = self.action[w]
             self.action[w] = a
             ctrl = self.act_default + cfg.action_scale * a
-            q, v, warm = self.qpos[w], self.qvel[w], self.warm[w]
-            for _ in range(cfg.decimation):
-                q, v, warm, _ = step(m, q, v, ctrl, warm=warm)
-            self.qpos[w], self.qvel[w], self.warm[w] = q, v, warm
+            q, v, found = self._substeps(w, ctrl)
             self.cmd[w, 0] += dtc
             qr, vr, pe, re = self._errors(w)
             s = cfg.motion_sigmas
             ej = float(np.sum((q[act] - qr[act]) ** 2))
             ev = float(np.sum((v[dofs] - vr[dofs]) ** 2))
-            terms = (np.exp(-ej / s[0]), np.exp(-ev / s[1]), np.exp(-float(pe @ pe) / s[2]),
+            terms = [np.exp(-ej / s[0]), np.exp(-ev / s[1]), np.exp(-float(pe @ pe) / s[2]),
                      np.exp(-float(re @ re) / s[3]), float(np.sum((self.action[w] - self.prev_action[w]) ** 2)),
-                     0.0)
+                     0.0, 0.0, 0.0, 0.0, float(found[0]) if len(found) else 0.0]
+            be = self.body_errors(w)
+            for k in range(4):
+                terms[5 + k] = np.exp(-be[k] / s[4 + k])
             r = 0.0
             for wt, t in zip(cfg.reward_weights, terms):
                 r += wt * t * dtc
@@ -1301,17 +1396,15 @@ class LiftTaskOracle(TaskOracle):
             self.prev_action[w] = self.action[w]
             self.action[w] = a
             ctrl = self.act_default + cfg.action_scale * a
-            q, v, warm = self.qpos[w], self.qvel[w], self.warm[w]
-            for _ in range(cfg.decimation):
-                q, v, warm, _ = step(m, q, v, ctrl, warm=warm)
-            self.qpos[w], self.qvel[w], self.warm[w] = q, v, warm
+            q, v, found = self._substeps(w, ctrl)
             ee = self._ee(q)
             cube = q[ca:ca + 3]
             d_ee = np.sqrt(np.sum((ee - cube) ** 2))
             lifted = 1.0 if cube[2] > cfg.lift_height else 0.0
             d_goal = np.sqrt(np.sum((cube - self.cmd[w]) ** 2))
             terms = (1.0 - np.tanh(d_ee / cfg.reach_std), lifted, lifted * (1.0 - np.tanh(d_goal / cfg.goal_std)),
-                     float(np.sum((self.action[w] - self.prev_action[w]) ** 2)), float(np.sum(v[dofs] ** 2)), 0.0)
+                     float(np.sum((self.action[w] - self.prev_action[w]) ** 2)), float(np.sum(v[dofs] ** 2)),
+                     float(found[1]) if len(found) > 1 else 0.0)
             r = 0.0
             for wt, t in zip(cfg.reward_weights, terms):
                 r += wt * t * dtc

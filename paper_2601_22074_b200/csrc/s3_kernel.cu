@@ -1521,7 +1521,7 @@ template <class T> __device__ int __noinline__ newton(const s3_model& m_, const 
 
 template <class T>
 __device__ __noinline__ int substep(const s3_model& m_, const s3_data& d, const s3_layout& L_, T* B_, int64_t w, T* gw, const T* gapp, bool last,
-                        int lane) {
+                        int lane, const uint8_t* psens = nullptr, uint32_t* found = nullptr) {
     const s3_model& m = model_ref<T>(m_);  // float64: the constant-bank copy (see c_s3m)
     WS<T> s = make_ws(B_, L_);
     const int nv = m.nv;
@@ -1540,6 +1540,16 @@ __device__ __noinline__ int substep(const s3_model& m_, const s3_data& d, const 
     int np = nv * (nv + 1) / 2;
     const T fscale = d.friction_scale ? static_cast<const T*>(d.friction_scale)[w] : T(1);
     ncon = collide(m, L_, B_, lane, dropped, fscale);
+    if (psens) {
+        // contact sensors (s3_task.pair_sensor): per sensor, this substep's contacts on its pairs; byte k of
+        // *found keeps the most any substep of the control step saw (ncon <= S3_MAX_CON < 32: one per lane)
+        const unsigned bits = lane < ncon ? psens[s.con_pair[lane]] : 0u;
+#pragma unroll
+        for (int k = 0; k < S3_MAX_SENSOR; ++k) {
+            const uint32_t n = (uint32_t)__popc(__ballot_sync(FULL, (bits >> k) & 1u));
+            if (n > ((*found >> (8 * k)) & 255u)) *found = (*found & ~(255u << (8 * k))) | (n << (8 * k));
+        }
+    }
     uint64_t U = (m.flags & 1) ? (nv == 64 ? ~0ull : ((1ull << nv) - 1)) : touched_mask(m, L_, B_, ncon, lane);
     tree_load(m, s.M, s.LD, lane);
     factor_ldl(m, s.LD, s.tk, lane, U, 1);          // subtrees no constraint touches: shared by M and H
@@ -1868,6 +1878,112 @@ __device__ inline void motion_errors(const s3_model& m, const T* qpos, const T* 
     re[0] = e[1] * sc; re[1] = e[2] * sc; re[2] = e[3] * sc;
 }
 
+// ---- BeyondMimic's relative body terms
+
+// World state of body b (S3_BODY_STATE values: position, orientation, origin linear velocity, angular
+// velocity) from the workspace's kinematics + com_pos and s.qvel: the body's spatial velocity is the sum of
+// the motion vectors (cdof, about the tree's com) of the dofs on its chain (oracle body_state).
+template <class T> __device__ inline void body_state(const s3_model& m, const WS<T>& s, int b, T* o) {
+    for (int k = 0; k < 3; ++k) o[k] = s.xpos[3 * b + k];
+    for (int k = 0; k < 4; ++k) o[3 + k] = s.xquat[4 * b + k];
+    T v[6] = {T(0), T(0), T(0), T(0), T(0), T(0)};
+    uint64_t mk = m.body_dofmask[b];
+    while (mk) {
+        const int i = __ffsll((long long)mk) - 1;
+        mk &= mk - 1;
+        const T qd = s.qvel[i];
+        for (int k = 0; k < 6; ++k) v[k] += s.cdof[6 * i + k] * qd;
+    }
+    const T* com = s.com + 3 * m.body_treeid[b];
+    T r[3] = {o[0] - com[0], o[1] - com[1], o[2] - com[2]}, wr[3];
+    cross3(v, r, wr);
+    for (int k = 0; k < 3; ++k) {
+        o[7 + k] = v[3 + k] + wr[k];
+        o[10 + k] = v[k];
+    }
+}
+
+// body k's (0: the anchor) clip state at motion time t: the s3_motion_bodies table interpolated like
+// motion_ref (linear; quaternion nlerp with sign alignment)
+template <class T> __device__ inline void motion_body_ref(const s3_task& tk, T t, int k, T* o) {
+    const T* Bt = static_cast<const T*>(tk.motion_body);
+    const int F = tk.nframes, K1 = tk.ntrack + 1;
+    T f = t / T(tk.frame_dt);
+    int i0 = (int)floor(f);
+    i0 = i0 < 0 ? 0 : (i0 > F - 2 ? F - 2 : i0);
+    const T a = f - T(i0);
+    const T* b0 = Bt + ((size_t)i0 * K1 + k) * S3_BODY_STATE;
+    const T* b1 = b0 + (size_t)K1 * S3_BODY_STATE;
+    for (int c = 0; c < S3_BODY_STATE; ++c) o[c] = (T(1) - a) * b0[c] + a * b1[c];
+    T d = b0[3] * b1[3] + b0[4] * b1[4] + b0[5] * b1[5] + b0[6] * b1[6];
+    if (d < T(0))
+        for (int c = 3; c < 7; ++c) o[c] = (T(1) - a) * b0[c] - a * b1[c];
+    T r = rsqrt_t(o[3] * o[3] + o[4] * o[4] + o[5] * o[5] + o[6] * o[6]);
+    for (int c = 3; c < 7; ++c) o[c] *= r;
+}
+
+// squared angle of the rotation conj(a) b (quat_error_magnitude^2)
+template <class T> __device__ inline T quat_err2(const T* a, const T* b) {
+    T ac[4] = {a[0], -a[1], -a[2], -a[3]}, e[4];
+    qmul(ac, b, e);
+    T sn = sqrt(e[1] * e[1] + e[2] * e[2] + e[3] * e[3]);
+    T ang = T(2) * atan2(sn, fabs(e[0]));
+    return ang * ang;
+}
+
+// The four BeyondMimic body-tracking errors at the final state of the control step: the clip's tracked body
+// poses re-expressed about the robot's anchor (the robot anchor's xy, the clip anchor's height above the
+// terrain under the spawn anchor, the yaw between the two anchors), compared with the robot's body poses;
+// body velocities compared in the world frame. Means over the tracked bodies: out[0] position (squared
+// distance), out[1] orientation (squared angle), out[2] linear velocity, out[3] angular velocity.
+template <class T>
+__device__ __noinline__ void motion_body_errors(const s3_model& m, const s3_task& tk, const s3_layout& L_, T* B_, T tnow,
+                                                const T* cmd, T* out, int lane) {
+    WS<T> s = make_ws(B_, L_);
+    kinematics(m, L_, B_, lane);
+    com_pos(m, L_, B_, lane, T(1));
+    const int K1 = tk.ntrack + 1;
+    T rb[S3_BODY_STATE], rf[S3_BODY_STATE];
+    if (lane < K1) {
+        body_state(m, s, lane ? tk.track_body[lane - 1] : tk.anchor_body, rb);
+        motion_body_ref(tk, tnow, lane, rf);
+    }
+    T pa[3], qa[4], pr[3], qr[4];
+    for (int k = 0; k < 3; ++k) {
+        pa[k] = __shfl_sync(FULL, rb[k], 0);
+        pr[k] = __shfl_sync(FULL, rf[k], 0);
+    }
+    for (int k = 0; k < 4; ++k) {
+        qa[k] = __shfl_sync(FULL, rb[3 + k], 0);
+        qr[k] = __shfl_sync(FULL, rf[3 + k], 0);
+    }
+    // yaw of qa conj(qr)
+    T qrc[4] = {qr[0], -qr[1], -qr[2], -qr[3]}, dq[4];
+    qmul(qa, qrc, dq);
+    T yaw = atan2(T(2) * (dq[0] * dq[3] + dq[1] * dq[2]), T(1) - T(2) * (dq[2] * dq[2] + dq[3] * dq[3]));
+    T sy, cy;
+    sincos_t(T(0.5) * yaw, &sy, &cy);
+    const T dy[4] = {cy, T(0), T(0), sy};
+    const T tz = pr[2] + terrain_height(m, pr[0] + cmd[1], pr[1] + cmd[2]);
+    T e[4] = {T(0), T(0), T(0), T(0)};
+    if (lane >= 1 && lane < K1) {
+        T R[9], rel[3] = {rf[0] - pr[0], rf[1] - pr[1], rf[2] - pr[2]}, rot[3];
+        qmat(dy, R);
+        mv3(R, rel, rot);
+        T p[3] = {pa[0] + rot[0], pa[1] + rot[1], tz + rot[2]};
+        T qh[4];
+        qmul(dy, rf + 3, qh);
+        for (int k = 0; k < 3; ++k) {
+            e[0] += (p[k] - rb[k]) * (p[k] - rb[k]);
+            e[2] += (rf[7 + k] - rb[7 + k]) * (rf[7 + k] - rb[7 + k]);
+            e[3] += (rf[10 + k] - rb[10 + k]) * (rf[10 + k] - rb[10 + k]);
+        }
+        e[1] = quat_err2(qh, rb + 3);
+    }
+    const T inv = T(1) / T(tk.ntrack);
+    for (int k = 0; k < 4; ++k) out[k] = wsum(e[k]) * inv;
+}
+
 template <class T>
 __device__ __noinline__ void motion_reset(const s3_model& m, const s3_task& tk, const s3_layout& L_, T* B_, int64_t w,
                                           uint64_t ctr, T* cmd, int lane) {
@@ -1931,7 +2047,8 @@ __device__ __noinline__ void motion_observe(const s3_model& m, const s3_task& tk
 
 template <class T>
 __device__ __noinline__ void motion_post(const s3_model& m, const s3_task& tk, const s3_layout& L_, T* B_, int64_t w,
-                                         uint64_t ctr, T* cmd, T* act, T rate, T* gq, T* gv, T* gw, T* prev, int lane) {
+                                         uint64_t ctr, T* cmd, T* act, T rate, T* gq, T* gv, T* gw, T* prev,
+                                         uint32_t found, int lane) {
     WS<T> s = make_ws(B_, L_);
     const int nu = m.nu, nq = m.nq, nv = m.nv;
     const T dtc = T(m.timestep) * T(tk.decimation);
@@ -1954,11 +2071,17 @@ __device__ __noinline__ void motion_post(const s3_model& m, const s3_task& tk, c
     }
     ej = wsum(ej);
     ev = wsum(ev);
-    T terms[6] = {exp(-ej / T(tk.motion_sigmas[0])), exp(-ev / T(tk.motion_sigmas[1])),
-                  exp(-(pe[0] * pe[0] + pe[1] * pe[1] + pe[2] * pe[2]) / T(tk.motion_sigmas[2])),
-                  exp(-(re[0] * re[0] + re[1] * re[1] + re[2] * re[2]) / T(tk.motion_sigmas[3])), rate, T(0)};
+    T be[4] = {T(0), T(0), T(0), T(0)};
+    if (tk.ntrack) motion_body_errors(m, tk, L_, B_, tnow, cmd, be, lane);
+    // joint pos / vel, anchor pos / ori, action rate, body pos / ori / lin vel / ang vel, self contacts
+    T terms[10] = {exp(-ej / T(tk.motion_sigmas[0])), exp(-ev / T(tk.motion_sigmas[1])),
+                   exp(-(pe[0] * pe[0] + pe[1] * pe[1] + pe[2] * pe[2]) / T(tk.motion_sigmas[2])),
+                   exp(-(re[0] * re[0] + re[1] * re[1] + re[2] * re[2]) / T(tk.motion_sigmas[3])), rate,
+                   T(0), T(0), T(0), T(0), T(found & 255u)};
+    if (tk.ntrack)
+        for (int k = 0; k < 4; ++k) terms[5 + k] = exp(-be[k] / T(tk.motion_sigmas[4 + k]));
     T r = T(0);
-    for (int k = 0; k < 6; ++k) r += T(tk.reward_weights[k]) * terms[k] * dtc;
+    for (int k = 0; k < 10; ++k) r += T(tk.reward_weights[k]) * terms[k] * dtc;
     bool finite = true;
     for (int i = lane; i < nq; i += 32) finite = finite && isfinite(s.qpos[i]);
     for (int i = lane; i < nv; i += 32) finite = finite && isfinite(s.qvel[i]);
@@ -2072,7 +2195,8 @@ __device__ __noinline__ void lift_observe(const s3_model& m, const s3_task& tk, 
 
 template <class T>
 __device__ __noinline__ void lift_post(const s3_model& m, const s3_task& tk, const s3_layout& L_, T* B_, int64_t w,
-                                       uint64_t ctr, T* cmd, T* act, T rate, T* gq, T* gv, T* gw, T* prev, int lane) {
+                                       uint64_t ctr, T* cmd, T* act, T rate, T* gq, T* gv, T* gw, T* prev,
+                                       uint32_t found, int lane) {
     WS<T> s = make_ws(B_, L_);
     const int nu = m.nu, nq = m.nq, nv = m.nv, ca = tk.cube_qposadr;
     const T dtc = T(m.timestep) * T(tk.decimation);
@@ -2089,8 +2213,9 @@ __device__ __noinline__ void lift_post(const s3_model& m, const s3_task& tk, con
         jv += v * v;
     }
     jv = wsum(jv);
+    // reach, lifted, goal tracking, action rate, joint velocity, end-effector / ground contacts (sensor 1)
     T terms[6] = {T(1) - tanh(d_ee / T(tk.reach_std)), lifted, lifted * (T(1) - tanh(d_goal / T(tk.goal_std))), rate, jv,
-                  T(0)};
+                  T((found >> 8) & 255u)};
     T r = T(0);
     for (int k = 0; k < 6; ++k) r += T(tk.reward_weights[k]) * terms[k] * dtc;
     bool finite = true;
@@ -2202,14 +2327,18 @@ __global__ void __launch_bounds__(32 * 16) env_kernel(const __grid_constant__ s3
     rate = wsum(rate);
     __syncwarp();
     int cost = 0;
-    for (int sub = 0; sub < tk.decimation; ++sub) cost += substep(m, d, L_, B_, w, gw, (const T*)nullptr, false, lane);
+    uint32_t found = 0;  // contact sensors: byte k = sensor k's most contacts in one substep
+    const uint8_t* psens = tk.nsensor ? tk.pair_sensor : nullptr;
+    for (int sub = 0; sub < tk.decimation; ++sub)
+        cost += substep(m, d, L_, B_, w, gw, (const T*)nullptr, false, lane, psens, &found);
     if (tk.cost && lane == 0) tk.cost[w] = cost;
+    if (tk.nsensor && lane < tk.nsensor) static_cast<T*>(tk.sensor)[w * tk.nsensor + lane] = T((found >> (8 * lane)) & 255u);
     if (tk.kind == 1) {
-        motion_post(m, tk, L_, B_, w, ctr, cmd, act, rate, gq, gv, gw, prev, lane);
+        motion_post(m, tk, L_, B_, w, ctr, cmd, act, rate, gq, gv, gw, prev, found, lane);
         return;
     }
     if (tk.kind == 2) {
-        lift_post(m, tk, L_, B_, w, ctr, cmd, act, rate, gq, gv, gw, prev, lane);
+        lift_post(m, tk, L_, B_, w, ctr, cmd, act, rate, gq, gv, gw, prev, found, lane);
         if (d.geom_xpos) store_geom_frames(m, d, L_, B_, w, lane);
         return;
     }
@@ -2298,6 +2427,33 @@ __global__ void __launch_bounds__(32 * 16) env_kernel(const __grid_constant__ s3
     if (d.geom_xpos) store_geom_frames(m, d, L_, B_, w, lane);  // sensors see the post-reset state, like obs
     for (int i = lane; i < nq; i += 32) gq[i] = s.qpos[i];
     for (int i = lane; i < nv; i += 32) gv[i] = s.qvel[i];
+}
+
+// s3_motion_bodies: one warp per clip frame -- the frame's qpos / qvel into the workspace, kinematics +
+// com_pos, then the anchor's and each tracked body's state (lanes over bodies)
+template <class T>
+__global__ void __launch_bounds__(32 * 16) motion_table_kernel(const __grid_constant__ s3_model m, const __grid_constant__ s3_layout l,
+                                                              const __grid_constant__ s3_task tk, T* __restrict__ out) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31;
+    const int64_t f = (int64_t)blockIdx.x * l.warps_per_block + (threadIdx.x >> 5);
+    if (f >= tk.nframes) return;
+    T* B_ = reinterpret_cast<T*>(smem_raw) + (size_t)(threadIdx.x >> 5) * l.elems_per_world;
+    const s3_layout& L_ = l;
+    WS<T> s = make_ws(B_, L_);
+    const T* q = static_cast<const T*>(tk.motion_qpos) + f * m.nq;
+    const T* v = static_cast<const T*>(tk.motion_qvel) + f * m.nv;
+    for (int i = lane; i < m.nq; i += 32) s.qpos[i] = q[i];
+    for (int i = lane; i < m.nv; i += 32) s.qvel[i] = v[i];
+    __syncwarp();
+    kinematics(m, L_, B_, lane);
+    com_pos(m, L_, B_, lane, T(1));
+    const int K1 = tk.ntrack + 1;
+    if (lane < K1) {
+        T o[S3_BODY_STATE];
+        body_state(m, s, lane ? tk.track_body[lane - 1] : tk.anchor_body, o);
+        for (int c = 0; c < S3_BODY_STATE; ++c) out[(f * K1 + lane) * S3_BODY_STATE + c] = o[c];
+    }
 }
 
 // cost-ordered schedule: counting sort of the worlds by their last solver cost, heaviest first, so the
@@ -2726,6 +2882,10 @@ int s3_env_step(const s3_model* m, const s3_data* d, const s3_layout* l, const s
         (t->kind == 1 && (t->nframes < 2 || !t->motion_qpos || !t->motion_qvel || m->nq + m->nv > m->nv * (m->nv + 1) / 2)))
         return fail(S3_ERR_ARG, "task layout does not match the model");
     if (d->qM) return fail(S3_ERR_ARG, "parity outputs are not written by s3_env_step");
+    if (t->kind == 1 && t->ntrack && (t->ntrack > S3_MAX_TRACK || !t->motion_body))
+        return fail(S3_ERR_ARG, "tracked bodies need the s3_motion_bodies table");
+    if (t->nsensor < 0 || t->nsensor > S3_MAX_SENSOR || (t->nsensor && (!t->pair_sensor || !t->sensor)))
+        return fail(S3_ERR_ARG, "contact sensors need pair_sensor and sensor");
     if ((t->cost == nullptr) != (t->order == nullptr)) return fail(S3_ERR_ARG, "cost and order go together");
     if ((m->flags & 6) && l->off[O_CDOF] - l->off[O_CRB] < m->nv)
         return fail(S3_ERR_ARG, "layout planned without the level-schedule scratch (flags bits 1-2): re-plan");
@@ -2752,6 +2912,34 @@ int s3_env_step(const s3_model* m, const s3_data* d, const s3_layout* l, const s
         if (e == cudaSuccess)
             env_kernel<float><<<grid, 32 * wpb, smem, st>>>(*m, *d, ll, *t, static_cast<const float*>(actions), mode,
                                                              global_step);
+    }
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e == cudaSuccess) e = slot.done();
+    if (e != cudaSuccess) return fail(S3_ERR_CUDA, cudaGetErrorString(e));
+    return S3_OK;
+}
+
+int s3_motion_bodies(const s3_model* m, const s3_layout* l, const s3_task* t, void* out, void* stream) {
+    using namespace s3;
+    if (!m || !l || !t || !out || !t->motion_qpos || !t->motion_qvel) return fail(S3_ERR_ARG, "null argument");
+    if (t->nframes < 1 || t->ntrack < 1 || t->ntrack > S3_MAX_TRACK) return fail(S3_ERR_ARG, "bad frame / body count");
+    for (int k = -1; k < t->ntrack; ++k) {
+        const int b = k < 0 ? t->anchor_body : t->track_body[k];
+        if (b < 1 || b >= m->nbody) return fail(S3_ERR_ARG, "tracked body out of range");
+    }
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    ModelSlot slot(m, st);
+    if (slot.error() != cudaSuccess) return fail(S3_ERR_CUDA, cudaGetErrorString(slot.error()));
+    const int wpb = l->warps_per_block;
+    const unsigned grid = (unsigned)((t->nframes + wpb - 1) / wpb);
+    const size_t smem = (size_t)l->bytes_per_block;
+    cudaError_t e;
+    if (m->dtype == S3_F64) {
+        e = cudaFuncSetAttribute(motion_table_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e == cudaSuccess) motion_table_kernel<double><<<grid, 32 * wpb, smem, st>>>(*m, *l, *t, static_cast<double*>(out));
+    } else {
+        e = cudaFuncSetAttribute(motion_table_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e == cudaSuccess) motion_table_kernel<float><<<grid, 32 * wpb, smem, st>>>(*m, *l, *t, static_cast<float*>(out));
     }
     if (e == cudaSuccess) e = cudaGetLastError();
     if (e == cudaSuccess) e = slot.done();

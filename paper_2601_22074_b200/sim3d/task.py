@@ -32,6 +32,40 @@ from .model import Model
 
 PURPOSE_RESET, PURPOSE_COMMAND, PURPOSE_OBS = 1, 2, 3
 
+# BeyondMimic's tracked bodies on the G1 (the anchor is the torso); models without these names track every
+# body of the first kinematic tree (up to S3_MAX_TRACK) about its root
+BEYONDMIMIC_ANCHOR = "torso_link"
+BEYONDMIMIC_BODIES = ("pelvis", "left_hip_roll_link", "left_knee_link", "left_ankle_roll_link", "right_hip_roll_link",
+                      "right_knee_link", "right_ankle_roll_link", "torso_link", "left_shoulder_roll_link",
+                      "left_elbow_link", "left_wrist_yaw_link", "right_shoulder_roll_link", "right_elbow_link",
+                      "right_wrist_yaw_link")
+
+
+def robot_geoms(m: Model, tree: int = 0) -> tuple:
+    """Geoms on the bodies of kinematic tree ``tree`` (not the terrain)."""
+    return tuple(g for g in range(m.ngeom) if m.geom_bodyid[g] > 0 and m.body_treeid[m.geom_bodyid[g]] == tree)
+
+
+def pair_sensor_bits(m: Model, sensors) -> np.ndarray:
+    """s3_task.pair_sensor: bit s of entry p is set when collision pair p is a contact of sensor s, i.e. one
+    geom of the pair is in the sensor's first set and the other in its second set (None: any geom)."""
+    bits = np.zeros(max(m.npair, 1), dtype=np.uint8)
+    for s, (_, a, b) in enumerate(sensors):
+        a = set(a)
+        b = None if b is None else set(b)
+        for p, (g1, g2) in enumerate(m.pair_geom):
+            if (g1 in a and (b is None or g2 in b)) or (g2 in a and (b is None or g1 in b)):
+                bits[p] |= np.uint8(1 << s)
+    return bits
+
+
+def padded(v, n: int) -> tuple:
+    """A reward-weight / sigma tuple padded with zeros to the struct's length."""
+    v = tuple(v)
+    if len(v) > n:
+        raise ValueError(f"at most {n} values")
+    return v + (0.0,) * (n - len(v))
+
 
 @dataclass
 class VelocityTaskCfg:
@@ -68,6 +102,12 @@ class VelocityTaskCfg:
     curriculum_max_init_level: int = 1
     curriculum_promote: float = 0.8
     curriculum_demote: float = 0.4
+    # contact sensors (ContactSensor analog): (name, geoms, other geoms or None for any), at most
+    # S3_MAX_SENSOR; env.sensor[w, s] = the most contacts of sensor s in one substep of the control step
+    contact_sensors: tuple = ()
+
+    def sensors(self, m: Model) -> tuple:
+        return tuple(self.contact_sensors)
 
     def scan_points(self):
         nx = int(round(self.scan_size[0] / self.scan_resolution)) + 1
@@ -94,8 +134,12 @@ class MotionTrackingCfg:
     random spawn anchor. Observations: [ref joint pos - default, ref joint vel, base lin vel, base ang vel,
     projected gravity, root pos error (base frame), root orientation error (rotation vector), joint pos -
     default, joint vel, last action]. Rewards: exp tracking kernels of joint pos / joint vel / root pos /
-    root orientation + action rate. Terminations: root height error, orientation error; truncation at the
-    clip end or after episode_steps. ``command`` holds (motion time, anchor x, anchor y) per world."""
+    root orientation, action rate, and BeyondMimic's body terms -- exp kernels of the tracked bodies'
+    position / orientation error with the clip's body poses re-expressed about the robot's anchor body, and
+    of their world linear / angular velocity error (the clip's body states come from s3_motion_bodies) --
+    plus a self-collision cost (contact sensor 0: robot-robot contacts). Terminations: root height error,
+    orientation error; truncation at the clip end or after episode_steps. ``command`` holds (motion time,
+    anchor x, anchor y) per world."""
     default_qpos: np.ndarray
     motion_qpos: np.ndarray
     motion_qvel: np.ndarray
@@ -104,9 +148,15 @@ class MotionTrackingCfg:
     action_scale: float = 0.25
     action_clip: float = 2.0
     episode_steps: int = 500
-    # track_joint_pos, track_joint_vel, track_root_pos, track_root_ori, action_rate_l2, (unused)
-    reward_weights: tuple = (0.5, 0.1, 0.5, 0.5, -0.01, 0.0)
-    motion_sigmas: tuple = (1.0, 50.0, 0.1, 0.5)
+    # track_joint_pos, track_joint_vel, track_root_pos, track_root_ori, action_rate_l2, body_pos, body_ori,
+    # body_lin_vel, body_ang_vel, self_collisions
+    reward_weights: tuple = (0.5, 0.1, 0.5, 0.5, -0.01, 1.0, 1.0, 1.0, 1.0, -0.1)
+    # exp-kernel denominators of the same terms (BeyondMimic's std^2 for the body terms: 0.3, 0.4, 1, pi)
+    motion_sigmas: tuple = (1.0, 50.0, 0.1, 0.5, 0.09, 0.16, 1.0, 9.8696)
+    anchor_body: str | int | None = None      # None: BEYONDMIMIC_ANCHOR if the model has it, else body 1
+    track_bodies: tuple | None = None         # None: BEYONDMIMIC_BODIES present in the model, else tree 0
+    self_collision: bool = True
+    contact_sensors: tuple = ()               # extra sensors after the self-collision one
     max_height_error: float = 0.25
     max_ori_error: float = 0.8
     spawn_half_extent: float = 0.5
@@ -116,6 +166,27 @@ class MotionTrackingCfg:
 
     def obs_dim(self, m: Model) -> int:
         return 15 + 5 * m.nu
+
+    def tracked(self, m: Model) -> tuple[int, tuple]:
+        """(anchor body id, tracked body ids)."""
+        bid = lambda b: m.body_names.index(b) if isinstance(b, str) else int(b)  # noqa: E731
+        if self.anchor_body is not None:
+            anchor = bid(self.anchor_body)
+        else:
+            anchor = m.body_names.index(BEYONDMIMIC_ANCHOR) if BEYONDMIMIC_ANCHOR in m.body_names else 1
+        if self.track_bodies is not None:
+            bodies = tuple(bid(b) for b in self.track_bodies)
+        else:
+            bodies = tuple(m.body_names.index(b) for b in BEYONDMIMIC_BODIES if b in m.body_names)
+            if not bodies:
+                bodies = tuple(b for b in range(1, m.nbody) if m.body_treeid[b] == 0)[:N.S3_MAX_TRACK]
+        if not 1 <= len(bodies) <= N.S3_MAX_TRACK:
+            raise ValueError(f"1..{N.S3_MAX_TRACK} tracked bodies")
+        return anchor, bodies
+
+    def sensors(self, m: Model) -> tuple:
+        own = (("self_collision", robot_geoms(m), robot_geoms(m)),) if self.self_collision else ()
+        return own + tuple(self.contact_sensors)
 
     def noise_vector(self, m: Model) -> np.ndarray:
         n = self.noise
@@ -139,8 +210,8 @@ class LiftTaskCfg:
     action_scale: float = 0.5
     action_clip: float = 2.0
     episode_steps: int = 250
-    # reach, lifted, goal tracking, action_rate_l2, joint_vel_l2, (unused)
-    reward_weights: tuple = (1.0, 15.0, 16.0, -1e-4, -1e-4, 0.0)
+    # reach, lifted, goal tracking, action_rate_l2, joint_vel_l2, end-effector / ground contacts (sensor 1)
+    reward_weights: tuple = (1.0, 15.0, 16.0, -1e-4, -1e-4, -0.1)
     reach_std: float = 0.1
     goal_std: float = 0.3
     lift_height: float = 0.04
@@ -151,13 +222,24 @@ class LiftTaskCfg:
     goal_ranges: tuple = ((0.45, 0.65), (-0.2, 0.2), (0.2, 0.4))
     noise: tuple = (0.0, 0.0, 0.0, 0.0, 0.01, 0.05, 0.0)
     kind: int = 2
+    # contact sensors on the end effector (the claw: the hand and finger bodies) and the ground plane (PAPER.md
+    # §6.3): 0 claw-cube, 1 claw-ground (costed by reward term 5), 2 cube-ground; set by for_model
+    contact_sensors: tuple = ()
 
     @classmethod
     def for_model(cls, m: Model, default_qpos: np.ndarray, **kw) -> "LiftTaskCfg":
         cube = m.body_names.index("cube")
         j = [k for k in range(m.njnt) if m.jnt_bodyid[k] == cube][0]
         tips = tuple(g for g in range(m.ngeom) if m.geom_type[g] == 2 and m.geom_bodyid[g] != cube)
+        fingers = {int(m.geom_bodyid[g]) for g in tips}
+        claw = fingers | {int(m.body_parentid[b]) for b in fingers}
+        ee = tuple(g for g in range(m.ngeom) if int(m.geom_bodyid[g]) in claw)
+        cube_g = tuple(g for g in range(m.ngeom) if m.geom_bodyid[g] == cube)
+        kw.setdefault("contact_sensors", (("ee_cube", ee, cube_g), ("ee_ground", ee, (0,)), ("cube_ground", cube_g, (0,))))
         return cls(default_qpos=default_qpos, cube_qposadr=int(m.jnt_qposadr[j]), tip_geoms=tips, **kw)
+
+    def sensors(self, m: Model) -> tuple:
+        return tuple(self.contact_sensors)
 
     def obs_dim(self, m: Model) -> int:
         return 13 + 3 * m.nu
@@ -203,14 +285,33 @@ class VelocityEnv3D:
         t.world_offset = self.world_offset
         t.action_scale, t.action_clip = cfg.action_scale, cfg.action_clip
         t.spawn_half_extent = getattr(cfg, "spawn_half_extent", 0.0)
-        t.reward_weights[:] = cfg.reward_weights
+        t.reward_weights[:] = padded(cfg.reward_weights, len(t.reward_weights))
         t.noise[:] = cfg.noise
+        # contact sensors
+        self.sensor_names = tuple(name for name, _, _ in cfg.sensors(model))
+        if len(self.sensor_names) > N.S3_MAX_SENSOR:
+            raise ValueError(f"at most {N.S3_MAX_SENSOR} contact sensors")
+        self.sensor = z(n, len(self.sensor_names))
+        if self.sensor_names:
+            self._pair_sensor = torch.as_tensor(pair_sensor_bits(model, cfg.sensors(model)), device=dev)
+            t.nsensor, t.pair_sensor, t.sensor = len(self.sensor_names), self._pair_sensor.data_ptr(), \
+                self.sensor.data_ptr()
+        self.motion_body = None
         if motion:
             self._motion_q = torch.as_tensor(cfg.motion_qpos, dtype=dt, device=dev).contiguous()
             self._motion_v = torch.as_tensor(cfg.motion_qvel, dtype=dt, device=dev).contiguous()
             t.nframes, t.frame_dt = cfg.motion_qpos.shape[0], cfg.motion_dt
             t.motion_qpos, t.motion_qvel = self._motion_q.data_ptr(), self._motion_v.data_ptr()
-            t.motion_sigmas[:] = cfg.motion_sigmas
+            t.motion_sigmas[:] = padded(cfg.motion_sigmas, len(t.motion_sigmas))
+            anchor, bodies = cfg.tracked(model)
+            t.anchor_body, t.ntrack = anchor, len(bodies)
+            t.track_body[:len(bodies)] = bodies
+            # the clip's body states (BeyondMimic's body_pos_w / quat / lin_vel / ang_vel): one launch, here
+            self.motion_body = z(t.nframes, 1 + len(bodies), N.S3_BODY_STATE)
+            t.motion_body = self.motion_body.data_ptr()
+            st = torch.cuda.current_stream(dev).cuda_stream
+            N.call("s3_motion_bodies", ctypes.byref(self.dm.struct), ctypes.byref(self.dm.layout), ctypes.byref(t),
+                   self.motion_body.data_ptr(), st, launch=True)
             t.max_height_error, t.max_ori_error = cfg.max_height_error, cfg.max_ori_error
             t.motion_start_frac = cfg.motion_start_frac
         elif lift:

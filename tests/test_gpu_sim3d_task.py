@@ -264,6 +264,8 @@ def test_motion_imitation_free_running_f64():
     env, ref = _motion_pair(n)
     np.testing.assert_allclose(env.reset().cpu().numpy(), ref.reset(), atol=1e-12)
     np.testing.assert_allclose(env.command.cpu().numpy(), ref.cmd, atol=1e-12)
+    # the clip's body-state table (s3_motion_bodies) against the oracle's FK of every frame
+    np.testing.assert_allclose(env.motion_body.cpu().numpy(), ref.body_table, rtol=1e-12, atol=1e-12)
     rng = np.random.default_rng(5)
     for k in range(4):
         a = rng.uniform(-1, 1, size=(n, env.model.nu))
@@ -274,6 +276,42 @@ def test_motion_imitation_free_running_f64():
         np.testing.assert_array_equal(tr.cpu().numpy().astype(bool), tr_ref)
         np.testing.assert_allclose(r.cpu().numpy(), r_ref, rtol=1e-8, atol=1e-10)
         np.testing.assert_allclose(o.cpu().numpy(), o_ref, rtol=1e-7, atol=1e-7)
+        np.testing.assert_array_equal(env.sensor.cpu().numpy(), ref.sensor)
+
+
+@pytest.mark.gpu
+def test_motion_body_terms_and_self_collision_teacher_forced():
+    """BeyondMimic's relative body terms and the self-collision cost: worlds loaded with crossed legs
+    (self contacts), a yawed / shifted robot (relative frame), and off-clip joint states; each reward term
+    is isolated by its weight and compared with the oracle; the self-collision sensor fires."""
+    import torch
+
+    n = 8
+    for term in range(5, 10):
+        w = [0.0] * 10
+        w[term] = 1.0
+        env, ref = _motion_pair(n, reward_weights=tuple(w), max_height_error=10.0, max_ori_error=10.0)
+        env.reset()
+        ref.reset()
+        m = ref.m
+        for i in range(0, n, 2):  # crossed legs in half of the worlds
+            ref.qpos[i, m.jnt_qposadr[m.jnt_names.index("left_hip_roll_joint")]] = -0.45
+            ref.qpos[i, m.jnt_qposadr[m.jnt_names.index("right_hip_roll_joint")]] = 0.45
+        ref.qpos[1, 0:2] += (0.4, -0.3)
+        ref.qvel[3] += np.random.default_rng(1).normal(size=m.nv) * 0.5
+        rng = np.random.default_rng(7)
+        for k in range(2):
+            _load(env, ref)
+            a = rng.uniform(-1, 1, size=(n, env.model.nu))
+            o, r, te, tr = env.step(torch.as_tensor(a, device="cuda"))
+            o_ref, r_ref, te_ref, tr_ref = ref.step(a)
+            torch.cuda.synchronize()
+            np.testing.assert_array_equal(te.cpu().numpy().astype(bool), te_ref)
+            np.testing.assert_allclose(r.cpu().numpy(), r_ref, rtol=1e-8, atol=1e-12)
+            np.testing.assert_array_equal(env.sensor.cpu().numpy(), ref.sensor)
+            assert np.abs(r_ref).max() > 0
+        if term == 9:
+            assert ref.sensor[:, 0].max() > 0
 
 
 @pytest.mark.gpu
@@ -321,6 +359,7 @@ def test_cube_lift_free_running_f64():
     n = 8
     env, ref = _lift_pair(n)
     np.testing.assert_allclose(env.reset().cpu().numpy(), ref.reset(), atol=1e-12)
+    assert env.sensor_names == ("ee_cube", "ee_ground", "cube_ground")
     rng = np.random.default_rng(8)
     for k in range(4):
         a = rng.uniform(-1, 1, size=(n, env.model.nu))
@@ -331,6 +370,39 @@ def test_cube_lift_free_running_f64():
         np.testing.assert_array_equal(tr.cpu().numpy().astype(bool), tr_ref)
         np.testing.assert_allclose(r.cpu().numpy(), r_ref, rtol=1e-8, atol=1e-10)
         np.testing.assert_allclose(o.cpu().numpy(), o_ref, rtol=1e-7, atol=1e-7)
+        np.testing.assert_array_equal(env.sensor.cpu().numpy(), ref.sensor)
+    assert ref.sensor[:, 2].min() > 0  # the cube rests on the table
+
+
+@pytest.mark.gpu
+def test_cube_lift_claw_contact_sensors_teacher_forced():
+    """End-effector contact sensors: a claw pushed into the table (ee_ground, costed by reward term 5) and
+    a claw closed on the cube (ee_cube), compared with the oracle."""
+    import torch
+
+    n = 4
+    env, ref = _lift_pair(n)
+    env.reset()
+    ref.reset()
+    m, ca = ref.m, ref.cfg.cube_qposadr
+    K = O.kinematics(m, ref.qpos[1])
+    t0, t1 = K["geom_xpos"][list(ref.cfg.tip_geoms)]
+    ref.qpos[1, ca:ca + 3] = t0 + 0.03 * (t1 - t0) / np.linalg.norm(t1 - t0)  # cube against a fingertip
+    ref.qpos[2, m.jnt_qposadr[m.jnt_names.index("shoulder_pitch")]] += 0.6  # claw down into the table
+    ref.qpos[3, m.jnt_qposadr[m.jnt_names.index("shoulder_pitch")]] += 0.6
+    ref.qpos[3, ca:ca + 3] = (0.3, 0.4, ref.cfg.cube_half)
+    seen = np.zeros(3)
+    rng = np.random.default_rng(10)
+    for k in range(3):
+        _load(env, ref)
+        a = rng.uniform(-0.2, 0.2, size=(n, env.model.nu))
+        o, r, te, tr = env.step(torch.as_tensor(a, device="cuda"))
+        o_ref, r_ref, te_ref, tr_ref = ref.step(a)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(env.sensor.cpu().numpy(), ref.sensor)
+        np.testing.assert_allclose(r.cpu().numpy(), r_ref, rtol=1e-8, atol=1e-10)
+        seen = np.maximum(seen, ref.sensor.max(0))
+    assert seen[0] > 0 and seen[1] > 0
 
 
 @pytest.mark.gpu

@@ -403,3 +403,79 @@ def test_capsule_box_contact_brute_force(rng):
         brute = np.min(np.linalg.norm(seg[:, None] - pts[None], axis=-1)) - 0.01
         assert abs(d - brute) < 6e-3, (d, brute)
         assert abs(np.linalg.norm(n) - 1) < 1e-12
+
+
+def test_body_state_velocities_are_fd_of_fk(model, rng):
+    """BeyondMimic body states: origin linear velocity and angular velocity == finite differences of FK."""
+    m = model
+    q, v = _random_state(m, rng)
+    K = O.kinematics(m, q)
+    C = O.com_pos(m, K)
+    h = 1e-6
+    Kp = O.kinematics(m, O.integrate_pos(m, q, v, h))
+    Km = O.kinematics(m, O.integrate_pos(m, q, v, -h))
+    for b in range(1, m.nbody):
+        st = O.body_state(m, K, C, v, b)
+        np.testing.assert_array_equal(st[0:3], K["xpos"][b])
+        np.testing.assert_array_equal(st[3:7], K["xquat"][b])
+        np.testing.assert_allclose(st[7:10], (Kp["xpos"][b] - Km["xpos"][b]) / (2 * h), atol=1e-7)
+        # angular velocity: dR/dt R^T is its cross-product matrix
+        W = (Kp["xmat"][b] - Km["xmat"][b]) / (2 * h) @ K["xmat"][b].T
+        np.testing.assert_allclose(st[10:13], [W[2, 1], W[0, 2], W[1, 0]], atol=1e-7)
+
+
+def test_motion_body_table_and_relative_errors():
+    """The clip body table is FK of the clip frames; a robot exactly on the clip has zero body errors, and
+    the errors are invariant to the robot's yaw / planar offset about its anchor (BeyondMimic's relative
+    frame) but not to a joint deviation."""
+    from paper_2601_22074_b200.sim3d.motion import synthetic_walk_clip
+    from paper_2601_22074_b200.sim3d.task import MotionTrackingCfg
+
+    m = robots.g1_like()
+    O.set_const(m)
+    dq = robots.default_qpos(m, robots.G1_DEFAULT_JOINTS)
+    Q, V, fdt = synthetic_walk_clip(m, dq, seconds=1.0)
+    cfg = MotionTrackingCfg(default_qpos=dq, motion_qpos=Q, motion_qvel=V, motion_dt=fdt, spawn_half_extent=0.0)
+    ref = O.MotionTaskOracle(m, cfg, 1, seed=0)
+    anchor, bodies = cfg.tracked(m)
+    assert m.body_names[anchor] == "torso_link" and len(bodies) == 14
+    f = 7
+    K = O.kinematics(m, Q[f])
+    for k, b in enumerate((anchor,) + bodies):
+        np.testing.assert_array_equal(ref.body_table[f, k, 0:3], K["xpos"][b])
+    ref.cmd[0] = (f * fdt, 0.0, 0.0)
+    ref.qpos[0], ref.qvel[0] = Q[f], V[f]
+    np.testing.assert_allclose(ref.body_errors(0), 0.0, atol=1e-20)
+    # yaw the whole robot about the world z axis and shift it in the plane: positions / orientations unchanged
+    q = Q[f].copy()
+    yaw = 0.7
+    qz = np.array([np.cos(0.5 * yaw), 0, 0, np.sin(0.5 * yaw)])
+    q[0:3] = O.qmat(qz) @ q[0:3] + np.array([0.3, -0.2, 0.0])
+    q[3:7] = O.qmul(qz, q[3:7])
+    ref.qpos[0], ref.qvel[0] = q, np.zeros(m.nv)
+    e = ref.body_errors(0)
+    assert e[0] < 1e-20 and e[1] < 1e-20
+    q[m.jnt_qposadr[m.jnt_names.index("left_knee_joint")]] += 0.3
+    ref.qpos[0] = q
+    assert ref.body_errors(0)[0] > 1e-4
+
+
+def test_contact_sensor_counts_match_pair_bits():
+    """Sensor counts from geoms (oracle) == counts through the per-pair bit table the kernel reads."""
+    from paper_2601_22074_b200.sim3d.task import MotionTrackingCfg, pair_sensor_bits
+
+    m = robots.g1_like()
+    O.set_const(m)
+    q = robots.default_qpos(m, robots.G1_DEFAULT_JOINTS)
+    q[m.jnt_qposadr[m.jnt_names.index("left_hip_roll_joint")]] = -0.45
+    q[m.jnt_qposadr[m.jnt_names.index("right_hip_roll_joint")]] = 0.45
+    q[2] -= 0.1  # feet into the ground too
+    cfg = MotionTrackingCfg(default_qpos=q, motion_qpos=np.tile(q, (2, 1)), motion_qvel=np.zeros((2, m.nv)),
+                            motion_dt=0.02, contact_sensors=(("feet_ground", (4, 5, 6, 7, 10, 11, 12, 13), (0,)),))
+    ref = O.MotionTaskOracle(m, cfg, 1)
+    cons, _ = O.collide(m, O.kinematics(m, q))
+    counts = ref._contact_counts(cons)
+    bits = pair_sensor_bits(m, cfg.sensors(m))
+    via_bits = [sum(1 for c in cons if (bits[c["pair"]] >> s) & 1) for s in range(2)]
+    np.testing.assert_array_equal(counts, via_bits)
+    assert counts[0] > 0 and counts[1] > 0
