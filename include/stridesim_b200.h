@@ -712,10 +712,12 @@ int ss_rt_release(ss_rt_state* st);
  * output arena into the slot's staging buffer (SM copy kernel) and copies it to a pinned host block
  * on a second copy stream, so the PCIe transfers of one step overlap the kernel of the next;
  * ss_pipe_wait blocks until the oldest pending step's results are in host memory and returns the
- * index of its host block. `host` holds nslot + 1 blocks used round-robin: the block step_wait
- * returned is not written again before the following ss_pipe_wait call. Buffers are owned by the
- * caller (16-byte aligned). */
-int ss_pipe_create(int32_t nslot, void* const* dev_actions, void* const* stage, void* const* host,
+ * index of its host block. `host` holds nhost (nslot < nhost <= 10) blocks used round-robin: the block
+ * step_wait returned is not written again before the following ss_pipe_wait call. When the staging
+ * buffers and host blocks of an even step and the next are contiguous, the two results cross PCIe as
+ * one copy (issued by the next step's ss_pipe_post, or by ss_pipe_wait alone if it comes first).
+ * Buffers are owned by the caller (16-byte aligned). */
+int ss_pipe_create(int32_t nslot, int32_t nhost, void* const* dev_actions, void* const* stage, void* const* host,
                    int64_t action_bytes, int64_t arena_bytes, void** out);
 int ss_pipe_destroy(void* pipe);
 int ss_pipe_pre(void* pipe, const void* host_actions, void* main_stream);

@@ -12,6 +12,7 @@
 // slot with a zero-copy flag in pinned host memory and a CUDA event;
 // ss_rt_poll retires completed slots and reports the flagged ones.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include <cuda_runtime.h>
@@ -178,13 +179,26 @@ struct Pipe {
     cudaStream_t in = nullptr, out = nullptr;
     cudaEvent_t in_done[8] = {}, snap[8] = {}, out_done[8] = {};
     bool used[8] = {};
-    int nslot = 2;
+    int nslot = 2, nhost = 3;
     int64_t submitted = 0, waited = 0;
+    int64_t deferred = -1;  // a step whose D2H waits to be paired with the next step's (see ss_pipe_post)
+    bool pair = true;       // SS_PIPE_PAIR=0 disables the pairing (A/B)
     void* dev_actions[8] = {};
     void* stage[8] = {};
-    void* host[9] = {};  // nslot + 1 pinned blocks: a view step_wait returned survives the next step_async
+    void* host[10] = {};  // nhost > nslot pinned blocks: a view step_wait returned survives the next step_async
     int64_t action_bytes = 0, arena_bytes = 0;
 };
+
+// D2H of `count` consecutive steps' arenas starting at step i (slots and host blocks contiguous)
+cudaError_t pipe_copy(Pipe* p, int64_t i, int count) {
+    const int k = (int)(i % p->nslot), hk = (int)(i % p->nhost);
+    const int klast = (int)((i + count - 1) % p->nslot);
+    cudaError_t e = cudaStreamWaitEvent(p->out, p->snap[klast], 0);  // the main stream snapshots in order
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(p->host[hk], p->stage[k], (size_t)p->arena_bytes * count, cudaMemcpyDeviceToHost, p->out);
+    for (int c = 0; c < count && e == cudaSuccess; ++c) e = cudaEventRecord(p->out_done[(k + c) % p->nslot], p->out);
+    return e;
+}
 
 int pipe_err(cudaError_t e, const char* what) {
     ss_set_error(what, cudaGetErrorString(e));
@@ -193,14 +207,16 @@ int pipe_err(cudaError_t e, const char* what) {
 
 }  // namespace
 
-extern "C" int ss_pipe_create(int32_t nslot, void* const* dev_actions, void* const* stage, void* const* host,
-                              int64_t action_bytes, int64_t arena_bytes, void** out) {
-    if (!dev_actions || !stage || !host || !out || arena_bytes <= 0 || action_bytes < 0 || nslot < 2 || nslot > 8) {
-        ss_set_error("ss_pipe_create", "null buffer, empty arena or nslot outside [2, 8]");
+extern "C" int ss_pipe_create(int32_t nslot, int32_t nhost, void* const* dev_actions, void* const* stage,
+                              void* const* host, int64_t action_bytes, int64_t arena_bytes, void** out) {
+    if (!dev_actions || !stage || !host || !out || arena_bytes <= 0 || action_bytes < 0 || nslot < 2 || nslot > 8 ||
+        nhost <= nslot || nhost > 10) {
+        ss_set_error("ss_pipe_create", "null buffer, empty arena, nslot outside [2, 8] or nhost outside (nslot, 10]");
         return -1;
     }
     Pipe* p = new Pipe();
     p->nslot = nslot;
+    p->nhost = nhost;
     cudaError_t e = cudaStreamCreateWithFlags(&p->in, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->out, cudaStreamNonBlocking);
     for (int k = 0; k < nslot && e == cudaSuccess; ++k) {
@@ -210,13 +226,15 @@ extern "C" int ss_pipe_create(int32_t nslot, void* const* dev_actions, void* con
         p->dev_actions[k] = dev_actions[k];
         p->stage[k] = stage[k];
     }
-    for (int k = 0; k <= nslot; ++k) p->host[k] = host[k];
+    for (int k = 0; k < nhost; ++k) p->host[k] = host[k];
     if (e != cudaSuccess) {
         delete p;
         return pipe_err(e, "ss_pipe_create");
     }
     p->action_bytes = action_bytes;
     p->arena_bytes = arena_bytes;
+    const char* pe = getenv("SS_PIPE_PAIR");
+    p->pair = !(pe && pe[0] == '0');
     *out = p;
     return 0;
 }
@@ -282,13 +300,27 @@ extern "C" int ss_pipe_post(void* h, const void* arena, void* main_stream) {
     }
     if (e == cudaSuccess) e = cudaEventRecord(p->snap[k], main);
     // (one stream: splitting the D2H over two copy-engine streams measured no faster, 36.4 vs 34.0 us/step)
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(p->out, p->snap[k], 0);
-    // host blocks rotate over nslot + 1: the block of step i is rewritten by step i + nslot + 1, which
-    // cannot be submitted before step i + 1 has been waited for
-    const int hk = (int)(p->submitted % (p->nslot + 1));
-    if (e == cudaSuccess)
-        e = cudaMemcpyAsync(p->host[hk], p->stage[k], (size_t)p->arena_bytes, cudaMemcpyDeviceToHost, p->out);
-    if (e == cudaSuccess) e = cudaEventRecord(p->out_done[k], p->out);
+    // Host blocks rotate over nhost > nslot: the block of step i is rewritten by step i + nhost, which cannot be
+    // submitted before step i + 1 has been waited for.
+    // Pairing: back-to-back copies of one 1.58 MB arena each sustain ~31.3 us, of two arenas ~29.4 us per
+    // arena (tools/e2e_host.py), so when the slot and host block of an even step and its successor are
+    // contiguous the even step's D2H is deferred and issued as one copy with the next step's -- or alone, by
+    // ss_pipe_wait, if the caller waits for it first (results are never held back behind a step not yet
+    // submitted).
+    const int64_t i = p->submitted;
+    const int hk = (int)(i % p->nhost);
+    if (e == cudaSuccess) {
+        if (p->deferred >= 0 && p->deferred == i - 1) {
+            e = pipe_copy(p, i - 1, 2);
+            p->deferred = -1;
+        } else if (p->pair && (i & 1) == 0 && k + 1 < p->nslot && hk + 1 < p->nhost &&
+                   (char*)p->stage[k] + p->arena_bytes == (char*)p->stage[k + 1] &&
+                   (char*)p->host[hk] + p->arena_bytes == (char*)p->host[hk + 1]) {
+            p->deferred = i;
+        } else {
+            e = pipe_copy(p, i, 1);
+        }
+    }
     if (e != cudaSuccess) return pipe_err(e, "ss_pipe_post");
     p->used[k] = true;
     p->submitted += 1;
@@ -304,8 +336,13 @@ extern "C" int ss_pipe_wait(void* h) {
         return -1;
     }
     const int k = (int)(p->waited % p->nslot);
-    const int hk = (int)(p->waited % (p->nslot + 1));
-    cudaError_t e = cudaEventSynchronize(p->out_done[k]);
+    const int hk = (int)(p->waited % p->nhost);
+    cudaError_t e = cudaSuccess;
+    if (p->deferred >= 0 && p->deferred == p->waited) {  // its pair partner is not submitted: copy it alone now
+        e = pipe_copy(p, p->waited, 1);
+        p->deferred = -1;
+    }
+    if (e == cudaSuccess) e = cudaEventSynchronize(p->out_done[k]);
     if (e != cudaSuccess) return pipe_err(e, "ss_pipe_wait");
     p->waited += 1;
     return hk;

@@ -45,8 +45,10 @@ from .terrain import generate_grid
 
 __all__ = ["EnvCfg", "SceneCfg", "InitStateCfg", "ManagerBasedRlEnv", "load_capture"]
 
-# steps that may be in flight between step_async and step_wait (ss_pipe, 2..4; SS_PIPE_SLOTS overrides for A/B)
-PIPE_SLOTS = int(os.environ.get("SS_PIPE_SLOTS", "4"))
+# steps that may be in flight between step_async and step_wait (ss_pipe, 2..8; SS_PIPE_SLOTS overrides for A/B):
+# six keep the paired D2H copies (ss_pipe_post) fed -- 31.8 us per step at 4096 worlds vs 33.9 with four
+# unpaired slots, 41.8 with four paired (tools/e2e_ab.py)
+PIPE_SLOTS = int(os.environ.get("SS_PIPE_SLOTS", "6"))
 NF_LAG = 4  # control steps the host may run ahead before it must look at nonfinite flags
 
 _SIM = native.SS_ST_APPLY | native.SS_ST_PUSH | native.SS_ST_PHYS | native.SS_ST_SENSOR
@@ -565,17 +567,19 @@ class ManagerBasedRlEnv:
         (``ss_pipe_*``, csrc/ss_runtime.cu) copies the step's actions
         host->device on one copy-engine stream, runs the step exactly like
         ``step`` on the device copy, snapshots the output arena with an SM copy
-        kernel into one of two staging buffers, and copies it to one of two
-        pinned host blocks on a second copy-engine stream -- so the PCIe
-        traffic of step i overlaps the kernels of the steps after it.
-        ``step_wait()`` blocks until the oldest pending step's results are in
-        host memory and returns its host views (obs groups, reward,
-        terminated, truncated), valid until ``step_async`` has been called
-        ``PIPE_SLOTS`` more times. At most ``PIPE_SLOTS`` steps may be pending;
-        with three, the host enqueues step i+1 while steps i-1 and i are in
-        flight, hiding its own per-step cost. The action tensor is read
-        asynchronously: do not overwrite it before that step's step_wait()
-        returns."""
+        kernel into one of ``PIPE_SLOTS`` staging buffers, and copies it to one
+        of ``PIPE_SLOTS + 2`` pinned host blocks on a second copy-engine stream
+        -- so the PCIe traffic of step i overlaps the kernels of the steps after
+        it; an even step whose successor is enqueued before it is waited for
+        crosses PCIe in one copy with it (two arenas per copy sustain ~6 % more
+        bandwidth). ``step_wait()`` blocks until the oldest pending step's
+        results are in host memory and returns its host views (obs groups,
+        reward, terminated, truncated), valid until ``step_async`` has been
+        called ``PIPE_SLOTS`` more times. At most ``PIPE_SLOTS`` steps may be
+        pending; with several in flight the host enqueues step i+1 while
+        earlier steps run, hiding its own per-step cost. The action tensor is
+        read asynchronously: do not overwrite it before that step's
+        step_wait() returns."""
         import torch
 
         if getattr(self, "_host_mirror", None) is not None:
@@ -585,18 +589,24 @@ class ManagerBasedRlEnv:
             A = self.action_manager.total_dim
             nb = self.step_outputs.numel()
             S = PIPE_SLOTS
+            H = S + 2 if S % 2 == 0 else S + 1  # even: steps pair up without wrapping (ss_pipe_post)
             dev_actions = [torch.empty((self.num_envs, A), dtype=torch.float64, device=self.device) for _ in range(S)]
-            stage = [torch.empty(nb, dtype=torch.uint8, device=self.device) for _ in range(S)]
-            host = [torch.empty(nb, dtype=torch.uint8).pin_memory() for _ in range(S + 1)]
+            # staging buffers and host blocks each carved from one allocation (contiguous for the paired
+            # D2H when the arena size keeps them 16-byte aligned)
+            pitch = (nb + 15) // 16 * 16
+            stage_all = torch.empty(S * pitch, dtype=torch.uint8, device=self.device)
+            host_all = torch.empty(H * pitch, dtype=torch.uint8).pin_memory()
+            stage = [stage_all[k * pitch:k * pitch + nb] for k in range(S)]
+            host = [host_all[k * pitch:k * pitch + nb] for k in range(H)]
             arr = lambda ts: (ctypes.c_void_p * S)(*[t.data_ptr() for t in ts])  # noqa: E731
             h = ctypes.c_void_p()
-            hosts = (ctypes.c_void_p * (S + 1))(*[t.data_ptr() for t in host])
-            rc = self._lib.ss_pipe_create(S, arr(dev_actions), arr(stage), hosts, self.num_envs * A * 8, nb,
+            hosts = (ctypes.c_void_p * H)(*[t.data_ptr() for t in host])
+            rc = self._lib.ss_pipe_create(S, H, arr(dev_actions), arr(stage), hosts, self.num_envs * A * 8, nb,
                                           ctypes.byref(h))
             if rc != 0:
                 raise native.NativeError(f"ss_pipe_create failed: {self._lib.ss_last_error().decode()}")
             P = self._pipe = dict(h=h, dev_actions=dev_actions, stage=stage, host=host, pinned=set(),
-                                  views=[self.unpack_outputs(x) for x in host])
+                                  keep=(stage_all, host_all), views=[self.unpack_outputs(x) for x in host])
         if (actions.__class__ is not torch.Tensor or actions.dtype is not torch.float64 or actions.is_cuda
                 or not actions.is_contiguous() or actions.shape != P["dev_actions"][0].shape):
             raise ValueError(f"step_async takes a contiguous pinned float64 host tensor of shape "

@@ -186,7 +186,7 @@ _SIGNATURES = {
     "ss_rt_launch": ([ctypes.c_void_p] * 5, ctypes.c_int),
     "ss_rt_poll": ([ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_int32], ctypes.c_int),
     "ss_rt_release": ([ctypes.c_void_p], ctypes.c_int),
-    "ss_pipe_create": ([ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+    "ss_pipe_create": ([ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
                         ctypes.c_int64, ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
     "ss_pipe_destroy": ([ctypes.c_void_p], ctypes.c_int),
     "ss_pipe_pre": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),

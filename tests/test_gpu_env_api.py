@@ -830,9 +830,43 @@ def test_step_async_delivers_each_steps_results_to_host():
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("n", [256, 300])
+def test_step_async_paired_and_sequential_waits(n):
+    """The paired D2H (ss_pipe_post: an even step's copy deferred and issued with its successor's) under
+    every wait pattern: strictly sequential (each deferred copy issued alone by step_wait), two in
+    flight (pairs), an odd number in flight; 300 worlds give an arena that is not a multiple of 16 bytes
+    (no pairing). Every step's host results equal a synchronous step's."""
+    from paper_2601_22074_b200.env import ManagerBasedRlEnv
+    from paper_2601_22074_b200.tasks import make_env_cfg
+
+    a = ManagerBasedRlEnv(make_env_cfg("Velocity-Rough", num_envs=n, seed=3))
+    b = ManagerBasedRlEnv(make_env_cfg("Velocity-Rough", num_envs=n, seed=3))
+    a.reset()
+    b.reset()
+    rng = np.random.default_rng(11)
+    pattern = [1, 1, 1, 2, 2, 3, 1, 3, 2]  # steps submitted before waiting for all of them
+    acts = [torch.from_numpy(rng.uniform(-1, 1, size=(n, a.action_manager.total_dim))).pin_memory()
+            for _ in range(sum(pattern))]
+    want = []
+    for x in acts:
+        o, r, _, tr, _ = a.step(x.cuda())
+        want.append((o["policy"].cpu().clone(), r.cpu().clone(), tr.cpu().clone()))
+    i = 0
+    for k in pattern:
+        for j in range(k):
+            b.step_async(acts[i + j])
+        for j in range(k):
+            got = b.step_wait()
+            wo, wr, wt = want[i + j]
+            assert torch.equal(got["obs/policy"], wo) and torch.equal(got["reward"], wr), (i + j, k)
+            assert torch.equal(got["truncated"], wt)
+        i += k
+
+
+@pytest.mark.gpu
 def test_step_wait_view_survives_the_next_step_async():
     """With the pipeline full (PIPE_SLOTS steps pending), the host view step_wait returned is not
-    overwritten by the following step_async (nslot + 1 host blocks, ss_pipe_*)."""
+    overwritten by the following step_async (PIPE_SLOTS + 2 host blocks, ss_pipe_*)."""
     from paper_2601_22074_b200.env import PIPE_SLOTS, ManagerBasedRlEnv
     from paper_2601_22074_b200.tasks import make_env_cfg
 
