@@ -402,6 +402,114 @@ def capsule_box(p0, p1, r, bc, R, size):
     return sphere_box(c, r, bc, R, size)
 
 
+BOX_FACE_BIAS = 0.95  # an edge axis wins only below this fraction of the best face overlap (face contacts first)
+BOX_TIE = 1e-12  # a candidate axis / face / point replaces the current one only when better by this margin, so
+# symmetric configurations (equal overlaps, rectangle corners) pick the same one in every rounding
+
+
+def box_box(c1, R1, h1, c2, R2, h2):
+    """Box-box narrowphase: the separating-axis test over the 3 + 3 face normals and the 9 edge-edge cross
+    products (parallel pairs skipped), then for a face axis the incident face of the other box clipped
+    (Sutherland-Hodgman) against the reference face's four side planes -- the clipped points below the
+    reference face are the contacts, at most 4 (the deepest, then repeatedly the point farthest from those
+    chosen) -- and for an edge axis one contact at the closest points of the two support edges. Normal from
+    box 1 to box 2; each contact (dist = -depth, normal, midpoint)."""
+    dv = c2 - c1
+    A = [R1[:, i] for i in range(3)]
+    B = [R2[:, j] for j in range(3)]
+
+    def overlap(u):
+        r1 = h1[0] * abs(u @ A[0]) + h1[1] * abs(u @ A[1]) + h1[2] * abs(u @ A[2])
+        r2 = h2[0] * abs(u @ B[0]) + h2[1] * abs(u @ B[1]) + h2[2] * abs(u @ B[2])
+        sd = u @ dv
+        return r1 + r2 - abs(sd), sd
+
+    face = None
+    for k in range(6):
+        u = A[k] if k < 3 else B[k - 3]
+        ov, sd = overlap(u)
+        if ov < 0.0:
+            return []
+        if face is None or ov < face[0] - BOX_TIE:
+            face = (ov, k, u, sd)
+    edge = None
+    for i in range(3):
+        for j in range(3):
+            u = np.cross(A[i], B[j])
+            L = np.sqrt(u @ u)
+            if L < 1e-6:
+                continue
+            u = u / L
+            ov, sd = overlap(u)
+            if ov < 0.0:
+                return []
+            if edge is None or ov < edge[0] - BOX_TIE:
+                edge = (ov, 6 + 3 * i + j, u, sd)
+    best = edge if (edge is not None and edge[0] < BOX_FACE_BIAS * face[0]) else face
+    ov, k, u, sd = best
+    n = u if sd >= 0.0 else -u
+    if k >= 6:
+        i, j = (k - 6) // 3, (k - 6) % 3
+        e1 = c1.copy()
+        for q in range(3):
+            if q != i:
+                e1 = e1 + (1.0 if A[q] @ n >= 0.0 else -1.0) * h1[q] * A[q]
+        e2 = c2.copy()
+        for q in range(3):
+            if q != j:
+                e2 = e2 + (1.0 if B[q] @ n <= 0.0 else -1.0) * h2[q] * B[q]
+        P, Q = seg_closest(e1 - A[i] * h1[i], e1 + A[i] * h1[i], e2 - B[j] * h2[j], e2 + B[j] * h2[j])
+        return [(-ov, n, 0.5 * (P + Q))]
+    if k < 3:
+        cr, Ar, hr, ia, ci, Ai, hi, nref = c1, A, h1, k, c2, B, h2, n
+    else:
+        cr, Ar, hr, ia, ci, Ai, hi, nref = c2, B, h2, k - 3, c1, A, h1, -n
+    cf = cr + nref * hr[ia]
+    proj = [abs(Ai[q] @ nref) for q in range(3)]
+    jf = 0
+    for q in (1, 2):
+        if proj[q] > proj[jf] + BOX_TIE:
+            jf = q
+    ninc = -Ai[jf] if Ai[jf] @ nref >= 0.0 else Ai[jf]
+    fi = ci + ninc * hi[jf]
+    ua, va = [q for q in range(3) if q != jf]
+    poly = [fi + su * hi[ua] * Ai[ua] + sv * hi[va] * Ai[va] for su, sv in ((-1.0, -1.0), (1.0, -1.0), (1.0, 1.0),
+                                                                             (-1.0, 1.0))]
+    for t in [q for q in range(3) if q != ia]:
+        for sg in (1.0, -1.0):
+            out = []
+            for idx in range(len(poly)):
+                P, Q = poly[idx], poly[(idx + 1) % len(poly)]
+                dP = hr[t] - sg * ((P - cr) @ Ar[t])
+                dQ = hr[t] - sg * ((Q - cr) @ Ar[t])
+                if dP >= 0.0:
+                    out.append(P)
+                if (dP >= 0.0) != (dQ >= 0.0):
+                    out.append(P + (Q - P) * (dP / (dP - dQ)))
+            poly = out
+            if not poly:
+                return []
+    pts = [(nref @ (cf - x), x) for x in poly]
+    pts = [(dep, x) for dep, x in pts if dep > 0.0]
+    chosen = []
+    if pts:
+        b = 0
+        for q in range(1, len(pts)):
+            if pts[q][0] > pts[b][0] + BOX_TIE:
+                b = q
+        chosen.append(b)
+        while len(chosen) < min(4, len(pts)):
+            bq, bd = -1, -1.0
+            for q in range(len(pts)):
+                if q in chosen:
+                    continue
+                dm = min(float((pts[q][1] - pts[c][1]) @ (pts[q][1] - pts[c][1])) for c in chosen)
+                if dm > bd + BOX_TIE:
+                    bq, bd = q, dm
+            chosen.append(bq)
+    return [(-pts[q][0], n, pts[q][1] + nref * (0.5 * pts[q][0])) for q in chosen]
+
+
 def _segment(m, K, g):
     a = K["geom_xmat"][g][:, 2] * m.geom_size[g][1]
     c = K["geom_xpos"][g]
@@ -452,6 +560,12 @@ def collide(m, K, fscale=1.0):
                 if h is not None and h[0] < 0.0:
                     d, n = h
                     found.append((d, n, q - n * (r + 0.5 * d)))
+        elif t1 == GEOM_BOX:  # box-box (both boxes; pairs put a box first only against a box)
+            dv = c2 - c1
+            rb = m.geom_rbound[g1] + m.geom_rbound[g2]
+            if dv @ dv >= rb * rb:
+                continue
+            found += box_box(c1, K["geom_xmat"][g1], m.geom_size[g1], c2, K["geom_xmat"][g2], m.geom_size[g2])
         elif t2 == GEOM_BOX:  # sphere or capsule (g1) vs box (g2)
             dv = c2 - c1
             rb = m.geom_rbound[g1] + m.geom_rbound[g2]

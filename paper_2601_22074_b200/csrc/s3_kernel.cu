@@ -932,6 +932,171 @@ template <class T> __device__ inline void point_of(const s3_model& m, int g, con
     }
 }
 
+// Box-box (oracle box_box): separating axes (3 + 3 face normals, 9 edge-edge cross products, parallel pairs
+// skipped); a face axis clips the other box's incident face against the reference face's side planes and
+// keeps the points below the reference face (at most 4: the deepest, then farthest-point selection); an edge
+// axis gives one contact between the two support edges. Normal from box 1 to box 2.
+constexpr double kBoxFaceBias = 0.95;  // an edge axis wins only below this fraction of the best face overlap
+constexpr double kBoxTie = 1e-12;  // replace the current axis / face / point only when better by this margin
+
+template <class T>
+__device__ __noinline__ int box_box(const T* c1, const T* R1, const T* h1, const T* c2, const T* R2, const T* h2,
+                                    Hit<T>* hits) {
+    T dv[3] = {c2[0] - c1[0], c2[1] - c1[1], c2[2] - c1[2]};
+    T A[3][3], B[3][3];
+    for (int i = 0; i < 3; ++i)
+        for (int k = 0; k < 3; ++k) { A[i][k] = R1[3 * k + i]; B[i][k] = R2[3 * k + i]; }
+    auto overlap = [&](const T* u, T& sd) {
+        T r1 = h1[0] * fabs(dot3(u, A[0])) + h1[1] * fabs(dot3(u, A[1])) + h1[2] * fabs(dot3(u, A[2]));
+        T r2 = h2[0] * fabs(dot3(u, B[0])) + h2[1] * fabs(dot3(u, B[1])) + h2[2] * fabs(dot3(u, B[2]));
+        sd = dot3(u, dv);
+        return r1 + r2 - fabs(sd);
+    };
+    T fov = T(0), fsd = T(0), fu[3] = {T(0), T(0), T(0)};
+    int fk = -1;
+    for (int k = 0; k < 6; ++k) {
+        const T* u = k < 3 ? A[k] : B[k - 3];
+        T sd, ov = overlap(u, sd);
+        if (ov < T(0)) return 0;
+        if (fk < 0 || ov < fov - T(kBoxTie)) { fov = ov; fk = k; fsd = sd; fu[0] = u[0]; fu[1] = u[1]; fu[2] = u[2]; }
+    }
+    T eov = T(0), esd = T(0), eu[3] = {T(0), T(0), T(0)};
+    int ek = -1;
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) {
+            T u[3];
+            cross3(A[i], B[j], u);
+            T L = sqrt(dot3(u, u));
+            if (L < T(1e-6)) continue;
+            u[0] = u[0] / L; u[1] = u[1] / L; u[2] = u[2] / L;
+            T sd, ov = overlap(u, sd);
+            if (ov < T(0)) return 0;
+            if (ek < 0 || ov < eov - T(kBoxTie)) { eov = ov; ek = 6 + 3 * i + j; esd = sd; eu[0] = u[0]; eu[1] = u[1]; eu[2] = u[2]; }
+        }
+    const bool use_edge = ek >= 0 && eov < T(kBoxFaceBias) * fov;
+    const T ov = use_edge ? eov : fov, sd = use_edge ? esd : fsd;
+    const int kk = use_edge ? ek : fk;
+    const T* u = use_edge ? eu : fu;
+    T n[3];
+    for (int k = 0; k < 3; ++k) n[k] = sd >= T(0) ? u[k] : -u[k];
+    if (kk >= 6) {
+        const int i = (kk - 6) / 3, j = (kk - 6) % 3;
+        T e1[3] = {c1[0], c1[1], c1[2]}, e2[3] = {c2[0], c2[1], c2[2]};
+        for (int q = 0; q < 3; ++q) {
+            if (q != i) {
+                const T sg = dot3(A[q], n) >= T(0) ? T(1) : T(-1);
+                for (int k = 0; k < 3; ++k) e1[k] = e1[k] + (sg * h1[q]) * A[q][k];
+            }
+            if (q != j) {
+                const T sg = dot3(B[q], n) <= T(0) ? T(1) : T(-1);
+                for (int k = 0; k < 3; ++k) e2[k] = e2[k] + (sg * h2[q]) * B[q][k];
+            }
+        }
+        T p1[3], q1[3], p2[3], q2[3], P[3], Q[3];
+        for (int k = 0; k < 3; ++k) {
+            p1[k] = e1[k] - A[i][k] * h1[i]; q1[k] = e1[k] + A[i][k] * h1[i];
+            p2[k] = e2[k] - B[j][k] * h2[j]; q2[k] = e2[k] + B[j][k] * h2[j];
+        }
+        seg_closest(p1, q1, p2, q2, P, Q);
+        hits[0].d = -ov;
+        for (int k = 0; k < 3; ++k) { hits[0].n[k] = n[k]; hits[0].pos[k] = T(0.5) * (P[k] + Q[k]); }
+        return 1;
+    }
+    // face axis: reference box (its face along the axis) and incident box
+    const bool r1 = kk < 3;
+    const T* cr = r1 ? c1 : c2;
+    const T* ci = r1 ? c2 : c1;
+    const T* hr = r1 ? h1 : h2;
+    const T* hi = r1 ? h2 : h1;
+    const T(*Ar)[3] = r1 ? A : B;
+    const T(*Ai)[3] = r1 ? B : A;
+    const int ia = r1 ? kk : kk - 3;
+    T nref[3];
+    for (int k = 0; k < 3; ++k) nref[k] = r1 ? n[k] : -n[k];
+    T cf[3];
+    for (int k = 0; k < 3; ++k) cf[k] = cr[k] + nref[k] * hr[ia];
+    int jf = 0;
+    T pj = fabs(dot3(Ai[0], nref));
+    for (int q = 1; q < 3; ++q) {
+        const T pq = fabs(dot3(Ai[q], nref));
+        if (pq > pj + T(kBoxTie)) { pj = pq; jf = q; }
+    }
+    const T sgi = dot3(Ai[jf], nref) >= T(0) ? T(-1) : T(1);
+    T fi[3];
+    for (int k = 0; k < 3; ++k) fi[k] = ci[k] + (sgi * Ai[jf][k]) * hi[jf];
+    const int ua = jf == 0 ? 1 : 0, va = jf == 2 ? 1 : 2;
+    T poly[8][3], tmp[8][3];
+    int np = 4;
+    const T su[4] = {T(-1), T(1), T(1), T(-1)}, sv[4] = {T(-1), T(-1), T(1), T(1)};
+    for (int v = 0; v < 4; ++v)
+        for (int k = 0; k < 3; ++k) poly[v][k] = fi[k] + (su[v] * hi[ua]) * Ai[ua][k] + (sv[v] * hi[va]) * Ai[va][k];
+    for (int t = 0; t < 3; ++t) {
+        if (t == ia) continue;
+        for (int sgn = 0; sgn < 2; ++sgn) {
+            const T sg = sgn == 0 ? T(1) : T(-1);
+            int no = 0;
+            for (int idx = 0; idx < np; ++idx) {
+                const T* P = poly[idx];
+                const T* Q = poly[idx + 1 < np ? idx + 1 : 0];
+                T dpv[3] = {P[0] - cr[0], P[1] - cr[1], P[2] - cr[2]}, dqv[3] = {Q[0] - cr[0], Q[1] - cr[1], Q[2] - cr[2]};
+                const T dP = hr[t] - sg * dot3(dpv, Ar[t]);
+                const T dQ = hr[t] - sg * dot3(dqv, Ar[t]);
+                if (dP >= T(0) && no < 8) { tmp[no][0] = P[0]; tmp[no][1] = P[1]; tmp[no][2] = P[2]; ++no; }
+                if ((dP >= T(0)) != (dQ >= T(0)) && no < 8) {
+                    const T f = dP / (dP - dQ);
+                    for (int k = 0; k < 3; ++k) tmp[no][k] = P[k] + (Q[k] - P[k]) * f;
+                    ++no;
+                }
+            }
+            np = no;
+            for (int v = 0; v < np; ++v)
+                for (int k = 0; k < 3; ++k) poly[v][k] = tmp[v][k];
+            if (np == 0) return 0;
+        }
+    }
+    T dep[8];
+    int nk = 0;
+    for (int v = 0; v < np; ++v) {
+        T dc[3] = {cf[0] - poly[v][0], cf[1] - poly[v][1], cf[2] - poly[v][2]};
+        const T dd = dot3(nref, dc);
+        if (dd > T(0)) {
+            dep[nk] = dd;
+            for (int k = 0; k < 3; ++k) tmp[nk][k] = poly[v][k];
+            ++nk;
+        }
+    }
+    if (nk == 0) return 0;
+    int chosen[4], nc = 0;
+    int b = 0;
+    for (int q = 1; q < nk; ++q)
+        if (dep[q] > dep[b] + T(kBoxTie)) b = q;
+    chosen[nc++] = b;
+    const int want = nk < 4 ? nk : 4;
+    while (nc < want) {
+        int bq = -1;
+        T bd = T(-1);
+        for (int q = 0; q < nk; ++q) {
+            bool used = false;
+            for (int c = 0; c < nc; ++c) used = used || chosen[c] == q;
+            if (used) continue;
+            T dm = T(0);
+            for (int c = 0; c < nc; ++c) {
+                T e[3] = {tmp[q][0] - tmp[chosen[c]][0], tmp[q][1] - tmp[chosen[c]][1], tmp[q][2] - tmp[chosen[c]][2]};
+                const T d2 = dot3(e, e);
+                dm = c == 0 ? d2 : fmin(dm, d2);
+            }
+            if (dm > bd + T(kBoxTie)) { bq = q; bd = dm; }
+        }
+        chosen[nc++] = bq;
+    }
+    for (int c = 0; c < nc; ++c) {
+        const int q = chosen[c];
+        hits[c].d = -dep[q];
+        for (int k = 0; k < 3; ++k) { hits[c].n[k] = n[k]; hits[c].pos[k] = tmp[q][k] + nref[k] * (T(0.5) * dep[q]); }
+    }
+    return nc;
+}
+
 // Narrowphase of one pair: up to 4 contacts into `hits`, in the oracle's order.
 template <class T> __device__ __noinline__ int narrow(const s3_model& m_, const s3_layout& L_, T* B_, int p, Hit<T>* hits) {
     const s3_model& m = c_s3m;  // constant-bank model (both dtypes; see c_s3m)
@@ -975,6 +1140,13 @@ template <class T> __device__ __noinline__ int narrow(const s3_model& m_, const 
                 ++cnt;
             }
         }
+    } else if (t1 == kGeomBox) {  // box-box: oracle box_box
+        T dv[3] = {c2[0] - c1[0], c2[1] - c1[1], c2[2] - c1[2]};
+        T rr = rb[g1] + rb[g2];
+        if (!(dot3(dv, dv) < rr * rr)) return 0;
+        const T* sz = F<T>(m.geom_size);
+        T h1[3] = {sz[3 * g1], sz[3 * g1 + 1], sz[3 * g1 + 2]}, h2[3] = {sz[3 * g2], sz[3 * g2 + 1], sz[3 * g2 + 2]};
+        cnt = box_box(c1, R1, h1, c2, R2, h2, hits);
     } else if (t2 == kGeomBox) {  // sphere or capsule (g1) vs box (g2): oracle sphere_box / capsule_box
         T dv[3] = {c2[0] - c1[0], c2[1] - c1[1], c2[2] - c1[2]};
         T rr = rb[g1] + rb[g2];
@@ -2951,7 +3123,7 @@ int s3_step(const s3_model* m, const s3_data* d, const s3_layout* l, int32_t nsu
     using namespace s3;
     if (!m || !d || !l || nsub < 0) return fail(S3_ERR_ARG, "null argument");
     if (d->nworld == 0 || nsub == 0) return S3_OK;
-    if (!d->qpos || !d->qvel || !d->ctrl) return fail(S3_ERR_ARG, "qpos/qvel/ctrl required");
+    if (!d->qpos || !d->qvel || (!d->ctrl && m->nu > 0)) return fail(S3_ERR_ARG, "qpos/qvel/ctrl required");
     if (d->qM && (!d->qLD || !d->qfrc_bias || !d->qfrc_smooth || !d->qacc_smooth || !d->qacc || !d->qfrc_constraint ||
                   !d->cdof || !d->xpos || !d->xquat || !d->com || !d->ncon || !d->ndropped || !d->nefc ||
                   !d->con_pair || !d->con_dist || !d->con_pos || !d->con_frame || !d->efc_force || !d->solver_niter))

@@ -372,8 +372,12 @@ class Model:
                 if t1 in (GEOM_PLANE, GEOM_HFIELD):
                     if t2 not in (GEOM_SPHERE, GEOM_CAPSULE, GEOM_BOX):
                         continue
-                elif not ((t1 in (GEOM_SPHERE, GEOM_CAPSULE) and t2 in (GEOM_SPHERE, GEOM_CAPSULE, GEOM_BOX))):
-                    continue  # supported pairs: sphere/capsule x sphere/capsule/box (box second)
+                elif t1 == GEOM_BOX and t2 in (GEOM_SPHERE, GEOM_CAPSULE):
+                    pairs.append((g2, g1))  # the narrowphase takes the box second
+                    continue
+                elif not ((t1 in (GEOM_SPHERE, GEOM_CAPSULE) and t2 in (GEOM_SPHERE, GEOM_CAPSULE, GEOM_BOX)) or
+                          (t1 == GEOM_BOX and t2 == GEOM_BOX)):
+                    continue  # supported pairs: sphere/capsule x sphere/capsule/box (box second), box x box
                 pairs.append((g1, g2))
         self.npair = len(pairs)
         self.pair_geom = np.array(pairs, dtype=np.int32).reshape(-1, 2)

@@ -479,3 +479,126 @@ def test_contact_sensor_counts_match_pair_bits():
     via_bits = [sum(1 for c in cons if (bits[c["pair"]] >> s) & 1) for s in range(2)]
     np.testing.assert_array_equal(counts, via_bits)
     assert counts[0] > 0 and counts[1] > 0
+
+
+def _rotz(a):
+    c, s = np.cos(a), np.sin(a)
+    return np.array([[c, -s, 0.0], [s, c, 0.0], [0.0, 0.0, 1.0]])
+
+
+def _rotx(a):
+    c, s = np.cos(a), np.sin(a)
+    return np.array([[1.0, 0.0, 0.0], [0.0, c, -s], [0.0, s, c]])
+
+
+def _roty(a):
+    c, s = np.cos(a), np.sin(a)
+    return np.array([[c, 0.0, s], [0.0, 1.0, 0.0], [-s, 0.0, c]])
+
+
+def _inside(x, c, R, h, tol=1e-12):
+    return bool(np.all(np.abs(R.T @ (x - c)) <= h + tol))
+
+
+def test_box_box_face_contacts_analytic():
+    """A smaller box pressed 4 mm into a larger one's top face: four contacts at the small box's bottom
+    corners (midway into the overlap), depth 4 mm, normal +z; yawed 45 deg and larger than the face, the
+    overlap octagon is reduced to four of its corners, all at the same depth."""
+    h1, h2, dep = np.array([0.3, 0.2, 0.1]), np.array([0.1, 0.07, 0.05]), 0.004
+    c1, R1 = np.zeros(3), np.eye(3)
+    c2, R2 = np.array([0.05, -0.02, 0.1 + 0.05 - dep]), _rotz(0.3)
+    hits = O.box_box(c1, R1, h1, c2, R2, h2)
+    assert len(hits) == 4
+    corners = [c2 + R2 @ (np.array([sx, sy, -1.0]) * h2) for sx in (-1, 1) for sy in (-1, 1)]
+    for d, n, pos in hits:
+        assert abs(d + dep) < 1e-12
+        np.testing.assert_allclose(n, [0, 0, 1], atol=1e-12)
+        assert min(np.linalg.norm(pos - (cc + np.array([0, 0, dep / 2]))) for cc in corners) < 1e-12
+    # wider than box 1 and yawed 45 deg: the overlap is an octagon
+    h2 = np.array([0.28, 0.28, 0.05])
+    c2, R2 = np.array([0.0, 0.0, 0.1 + 0.05 - dep]), _rotz(np.pi / 4)
+    hits = O.box_box(c1, R1, h1, c2, R2, h2)
+    assert len(hits) == 4
+    for d, n, pos in hits:
+        assert abs(d + dep) < 1e-12
+        x = pos - np.array([0, 0, dep / 2])  # on box 2's bottom face, inside both footprints
+        assert abs(x[2] - (0.1 - dep)) < 1e-12 and np.all(np.abs(x[:2]) <= h1[:2] + 1e-12)
+        assert np.all(np.abs((R2.T @ (x - c2))[:2]) <= h2[:2] + 1e-12)
+
+
+def test_box_box_edge_edge_and_separated():
+    """Two edges crossing at right angles (box 1 rolled 45 deg about x, box 2 pitched 45 deg about y and
+    pushed down 3 mm): one contact midway between the edges, normal +z, depth 3 mm. Lifted apart: none."""
+    h = np.array([0.2, 0.2, 0.2])
+    R1, R2 = _rotx(np.pi / 4), _roty(np.pi / 4)
+    top = 0.2 * np.sqrt(2.0)
+    c1 = np.zeros(3)
+    c2 = np.array([0.01, -0.02, 2 * top - 0.003])
+    hits = O.box_box(c1, R1, h, c2, R2, h)
+    assert len(hits) == 1
+    d, n, pos = hits[0]
+    assert abs(d + 0.003) < 1e-12
+    np.testing.assert_allclose(n, [0, 0, 1], atol=1e-12)
+    np.testing.assert_allclose(pos, [0.01, 0.0, top - 0.0015], atol=1e-12)  # box 2 edge x, box 1 edge y
+    assert O.box_box(c1, R1, h, c2 + np.array([0, 0, 0.01]), R2, h) == []
+
+
+def test_box_box_random_poses_contacts_on_and_in_the_boxes(rng):
+    """Random overlapping poses: every contact's normal is a unit vector from box 1 towards box 2 with a
+    penetration no deeper than the overlap along any of the 15 axes, and the contact's incident point (half
+    its depth back along the normal towards the box it belongs to) lies inside the other box."""
+    def min_overlap(c1, R1, h1, c2, R2, h2):
+        axes = [R1[:, i] for i in range(3)] + [R2[:, j] for j in range(3)]
+        axes += [np.cross(R1[:, i], R2[:, j]) for i in range(3) for j in range(3)]
+        return min(h1 @ np.abs(R1.T @ u) + h2 @ np.abs(R2.T @ u) - abs(u @ (c2 - c1))
+                   for u in (a / np.linalg.norm(a) for a in axes if np.linalg.norm(a) > 1e-6))
+
+    seen = 0
+    for _ in range(300):
+        h1, h2 = rng.uniform(0.05, 0.3, size=3), rng.uniform(0.05, 0.3, size=3)
+        q1, q2 = rng.normal(size=4), rng.normal(size=4)
+        R1, R2 = O.qmat(q1 / np.linalg.norm(q1)), O.qmat(q2 / np.linalg.norm(q2))
+        c1 = np.zeros(3)
+        u = rng.normal(size=3)
+        u /= np.linalg.norm(u)
+        target, lo_t, hi_t = rng.uniform(0.001, 0.02), 0.0, 2.0  # a shallow overlap (bisection on the offset)
+        for _ in range(60):
+            mid = 0.5 * (lo_t + hi_t)
+            lo_t, hi_t = (mid, hi_t) if min_overlap(c1, R1, h1, mid * u, R2, h2) > target else (lo_t, mid)
+        c2 = lo_t * u
+        hits = O.box_box(c1, R1, h1, c2, R2, h2)
+        assert hits
+        for d, n, pos in hits:
+            seen += 1
+            assert d <= 0.0 and abs(np.linalg.norm(n) - 1.0) < 1e-12
+            lo, hi = pos - n * (-d / 2), pos + n * (-d / 2)  # the two surface points along the normal
+            # box 2's incident point inside box 1 (box 1 the reference), or box 1's inside box 2
+            assert _inside(lo, c1, R1, h1, 1e-9) or _inside(hi, c2, R2, h2, 1e-9)
+            axes = [R1[:, i] for i in range(3)] + [R2[:, j] for j in range(3)]
+            axes += [np.cross(R1[:, i], R2[:, j]) for i in range(3) for j in range(3)]
+            ovs = []
+            for u in axes:
+                if np.linalg.norm(u) < 1e-6:
+                    continue
+                u = u / np.linalg.norm(u)
+                ovs.append(h1 @ np.abs(R1.T @ u) + h2 @ np.abs(R2.T @ u) - abs(u @ (c2 - c1)))
+            assert -d <= min(ovs) / O.BOX_FACE_BIAS + 1e-12
+    assert seen > 100
+
+
+def test_box_stack_settles():
+    """Three free boxes stacked 2 mm into each other at different yaws (box-box + box-plane contacts)
+    push apart to the soft-contact equilibrium and stay stacked: no drift, no spin, velocities ~0."""
+    m = robots.box_stack()
+    O.set_const(m)
+    q, v, w = m.qpos0.copy(), np.zeros(m.nv), np.zeros(m.nv)
+    for _ in range(300):
+        q, v, w, F = O.step(m, q, v, np.zeros(0), warm=w)
+    dq = q - m.qpos0
+    for j in range(m.njnt):
+        a = m.jnt_qposadr[j]
+        assert np.abs(dq[a:a + 2]).max() < 1e-4           # no sliding
+        assert 0.0 < dq[a + 2] < 0.002 * (j + 1) + 1e-4    # rose out of the initial overlap, no more
+        assert np.abs(dq[a + 3:a + 7]).max() < 1e-4        # no spin / tilt
+    assert np.abs(v).max() < 1e-3
+    assert sum(1 for c in F["contacts"] if c["geom1"] != 0) == 8  # 4 per box-box face contact
