@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define S3_ABI_VERSION 18
+#define S3_ABI_VERSION 19
 #define S3_F64 0
 #define S3_F32 1
 
@@ -260,7 +260,8 @@ typedef struct s3_task {
     /* contact sensors (every kind): bit s of pair_sensor[p] makes the contacts of collision pair p count
      * toward sensor s; sensor[w * nsensor + s] = the most such contacts any substep of the control step saw */
     int32_t nsensor;
-    int32_t pad5;
+    int32_t nfeet; /* velocity kind: sensors 0..nfeet-1 are the feet's ground contacts (foot-slip term) */
+    int32_t foot_body[S3_MAX_SENSOR];
     const uint8_t* pair_sensor; /* (npair,) */
     void* sensor;               /* (N, nsensor) */
     const void* motion_body;    /* (nframes, 1 + ntrack, S3_BODY_STATE) */

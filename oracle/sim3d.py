@@ -1012,6 +1012,39 @@ class TaskOracle:
             out[w] = o
         return out
 
+    def velocity_extras(self, w, found):
+        """(|centroidal angular momentum of the robot|^2, joint-limit violation, foot slip) at the final state
+        (the velocity kind's mjlab penalties; each computed only when its weight is nonzero)."""
+        m, cfg = self.m, self.cfg
+        wts = tuple(cfg.reward_weights) + (0.0,) * 9
+        q, v = self.qpos[w], self.qvel[w]
+        lim = 0.0
+        if wts[7] != 0.0:
+            for j in range(m.njnt):
+                if m.jnt_limited[j]:
+                    lo, hi = m.jnt_range[j]
+                    x = q[m.jnt_qposadr[j]]
+                    lim += max(lo - x, 0.0) + max(x - hi, 0.0)
+        feet = cfg.foot_bodies(m)
+        h, slip = np.zeros(3), 0.0
+        if wts[6] != 0.0 or (wts[8] != 0.0 and feet):
+            K = kinematics(m, q)
+            C = com_pos(m, K, self.mscale[w])
+            if wts[6] != 0.0:
+                for b in range(1, m.nbody):
+                    if m.body_treeid[b] != 0:
+                        continue
+                    vb = np.zeros(6)
+                    for dd in m.body_chain[b]:
+                        vb = vb + C["cdof"][dd] * v[dd]
+                    h = h + inert_mul(C["cinert"][b], vb)[:3]
+            if wts[8] != 0.0:
+                for k, b in enumerate(feet):
+                    if found[k] > 0:
+                        st = body_state(m, K, C, v, b)
+                        slip += st[7] * st[7] + st[8] * st[8]
+        return float(h @ h), lim, slip
+
     def height_scan(self, w):
         m, cfg = self.m, self.cfg
         q = self.qpos[w]
@@ -1041,12 +1074,13 @@ class TaskOracle:
             self.prev_action[w] = self.action[w]
             self.action[w] = a
             ctrl = self.act_default + cfg.action_scale * a
-            q, v, _ = self._substeps(w, ctrl, self.fscale[w], self.mscale[w])
+            q, v, found = self._substeps(w, ctrl, self.fscale[w], self.mscale[w])
             vb, om, g, _ = base_frame(m, q, v)
             e_xy = (self.cmd[w, 0] - vb[0]) ** 2 + (self.cmd[w, 1] - vb[1]) ** 2
             terms = (np.exp(-e_xy / cfg.track_sigma), np.exp(-((self.cmd[w, 2] - om[2]) ** 2) / cfg.track_sigma),
                      vb[2] * vb[2], om[0] * om[0] + om[1] * om[1],
-                     float(np.sum((self.action[w] - self.prev_action[w]) ** 2)), g[0] * g[0] + g[1] * g[1])
+                     float(np.sum((self.action[w] - self.prev_action[w]) ** 2)), g[0] * g[0] + g[1] * g[1],
+                     *self.velocity_extras(w, found))
             r = 0.0
             for wt, t in zip(cfg.reward_weights, terms):
                 r += wt * t * dtc

@@ -2420,6 +2420,55 @@ __device__ __noinline__ void lift_post(const s3_model& m, const s3_task& tk, con
     for (int i = lane; i < nv; i += 32) gv[i] = s.qvel[i];
 }
 
+// mjlab's velocity-task penalties beyond the base-frame terms, at the final state of the control step:
+// out[0] |centroidal angular momentum|^2 of the robot (tree 0: sum over its bodies of the angular part of
+// cinert x cvel, about the tree's com), out[1] joint-limit violation (sum over limited joints of the distance
+// outside [lo, hi]), out[2] foot slip (sum over feet in contact -- contact sensors 0..nfeet-1 -- of the
+// foot body's squared horizontal velocity). Kinematics + com_pos run only when a weight needs them.
+template <class T>
+__device__ __noinline__ void velocity_extra_terms(const s3_model& m, const s3_data& d, const s3_task& tk, const s3_layout& L_,
+                                                  T* B_, int64_t w, uint32_t found, T* out, int lane) {
+    WS<T> s = make_ws(B_, L_);
+    T lim = T(0);
+    if (tk.reward_weights[7] != 0.0) {
+        const T* rg = F<T>(m.lim_range);
+        for (int l = lane; l < m.nlimjnt; l += 32) {
+            const T q = s.qpos[m.lim_qposadr[l]];
+            lim += fmax(rg[2 * l] - q, T(0)) + fmax(q - rg[2 * l + 1], T(0));
+        }
+        lim = wsum(lim);
+    }
+    T h[3] = {T(0), T(0), T(0)}, slip = T(0);
+    if (tk.reward_weights[6] != 0.0 || (tk.reward_weights[8] != 0.0 && tk.nfeet > 0)) {
+        kinematics(m, L_, B_, lane);
+        com_pos(m, L_, B_, lane, d.mass_scale ? static_cast<const T*>(d.mass_scale)[w] : T(1));
+        if (tk.reward_weights[6] != 0.0) {
+            for (int b = 1 + lane; b < m.nbody; b += 32) {
+                if (m.body_treeid[b] != 0) continue;
+                T v[6] = {T(0), T(0), T(0), T(0), T(0), T(0)}, f[6];
+                uint64_t mk = m.body_dofmask[b];
+                while (mk) {
+                    const int i = __ffsll((long long)mk) - 1;
+                    mk &= mk - 1;
+                    for (int k = 0; k < 6; ++k) v[k] += s.cdof[6 * i + k] * s.qvel[i];
+                }
+                inert_mul(s.cinert + 10 * b, v, f);
+                h[0] += f[0]; h[1] += f[1]; h[2] += f[2];
+            }
+            h[0] = wsum(h[0]); h[1] = wsum(h[1]); h[2] = wsum(h[2]);
+        }
+        if (tk.reward_weights[8] != 0.0 && lane < tk.nfeet && ((found >> (8 * lane)) & 255u)) {
+            T o[S3_BODY_STATE];
+            body_state(m, s, tk.foot_body[lane], o);
+            slip = o[7] * o[7] + o[8] * o[8];
+        }
+        slip = wsum(slip);
+    }
+    out[0] = h[0] * h[0] + h[1] * h[1] + h[2] * h[2];
+    out[1] = lim;
+    out[2] = slip;
+}
+
 template <class T>
 __global__ void __launch_bounds__(32 * 16) env_kernel(const __grid_constant__ s3_model m, const __grid_constant__ s3_data d,
                                                      const __grid_constant__ s3_layout l,
@@ -2521,10 +2570,14 @@ __global__ void __launch_bounds__(32 * 16) env_kernel(const __grid_constant__ s3
     T dtc = T(m.timestep) * T(tk.decimation);
     T e_xy = (c0 - vb[0]) * (c0 - vb[0]) + (c1 - vb[1]) * (c1 - vb[1]);
     T sig = T(tk.track_sigma);
-    T terms[6] = {exp(-e_xy / sig), exp(-((c2 - om[2]) * (c2 - om[2])) / sig), vb[2] * vb[2],
-                  om[0] * om[0] + om[1] * om[1], rate, g[0] * g[0] + g[1] * g[1]};
+    T extra[3];
+    velocity_extra_terms(m, d, tk, L_, B_, w, found, extra, lane);
+    // track lin vel xy, track ang vel z, lin vel z, ang vel xy, action rate, flat orientation, angular
+    // momentum, joint limits, foot slip
+    T terms[9] = {exp(-e_xy / sig), exp(-((c2 - om[2]) * (c2 - om[2])) / sig), vb[2] * vb[2],
+                  om[0] * om[0] + om[1] * om[1], rate, g[0] * g[0] + g[1] * g[1], extra[0], extra[1], extra[2]};
     T r = T(0);
-    for (int k = 0; k < 6; ++k) r += T(tk.reward_weights[k]) * terms[k] * dtc;
+    for (int k = 0; k < 9; ++k) r += T(tk.reward_weights[k]) * terms[k] * dtc;
     bool finite = true;
     for (int i = lane; i < nq; i += 32) finite = finite && isfinite(s.qpos[i]);
     for (int i = lane; i < nv; i += 32) finite = finite && isfinite(s.qvel[i]);

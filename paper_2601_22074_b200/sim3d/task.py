@@ -77,8 +77,10 @@ class VelocityTaskCfg:
     command_resample_steps: int = 500  # 10 s
     command_ranges: tuple = ((-1.0, 1.0), (-0.5, 0.5), (-1.0, 1.0))
     track_sigma: float = 0.25
-    # track_lin_vel_xy_exp, track_ang_vel_z_exp, lin_vel_z_l2, ang_vel_xy_l2, action_rate_l2, flat_orientation_l2
-    reward_weights: tuple = (1.0, 0.5, -2.0, -0.05, -0.01, -1.0)
+    # track_lin_vel_xy_exp, track_ang_vel_z_exp, lin_vel_z_l2, ang_vel_xy_l2, action_rate_l2, flat_orientation_l2,
+    # angular_momentum_l2 (robot's centroidal angular momentum), joint_pos_limits (distance outside the ranges),
+    # foot_slip (squared horizontal velocity of the feet in ground contact) -- PAPER.md §6.1's penalty set
+    reward_weights: tuple = (1.0, 0.5, -2.0, -0.05, -0.01, -1.0, -0.02, -1.0, -0.1)
     min_height: float = 0.3
     max_tilt_cos: float = -0.5         # terminate when projected gravity z > -cos(60 deg)
     reset_joint_jitter: float = 0.1
@@ -102,12 +104,23 @@ class VelocityTaskCfg:
     curriculum_max_init_level: int = 1
     curriculum_promote: float = 0.8
     curriculum_demote: float = 0.4
+    # feet (body names; None: the *ankle_roll_link / *_calf bodies): each gets a ground-contact sensor (the
+    # first sensors), read by the foot-slip term
+    feet: tuple | None = None
     # contact sensors (ContactSensor analog): (name, geoms, other geoms or None for any), at most
-    # S3_MAX_SENSOR; env.sensor[w, s] = the most contacts of sensor s in one substep of the control step
+    # S3_MAX_SENSOR with the feet's; env.sensor[w, s] = the most contacts of sensor s in one substep of the
+    # control step
     contact_sensors: tuple = ()
 
+    def foot_bodies(self, m: Model) -> tuple:
+        if self.feet is not None:
+            return tuple(m.body_names.index(b) if isinstance(b, str) else int(b) for b in self.feet)
+        return tuple(b for b, nm in enumerate(m.body_names) if nm.endswith("ankle_roll_link") or nm.endswith("_calf"))
+
     def sensors(self, m: Model) -> tuple:
-        return tuple(self.contact_sensors)
+        feet = tuple((f"{m.body_names[b]}_ground", tuple(g for g in range(m.ngeom) if m.geom_bodyid[g] == b), (0,))
+                     for b in self.foot_bodies(m))
+        return feet + tuple(self.contact_sensors)
 
     def scan_points(self):
         nx = int(round(self.scan_size[0] / self.scan_resolution)) + 1
@@ -323,6 +336,11 @@ class VelocityEnv3D:
             for i, (lo, hi) in enumerate(cfg.goal_ranges):
                 t.cmd_lo[i], t.cmd_hi[i] = lo, hi
         else:
+            feet = cfg.foot_bodies(model)
+            if len(feet) > N.S3_MAX_SENSOR:
+                raise ValueError(f"at most {N.S3_MAX_SENSOR} feet")
+            t.nfeet = len(feet)
+            t.foot_body[:len(feet)] = feet
             if cfg.push_interval is not None:
                 t.events = 1
                 self.data.friction_scale = torch.ones(n, dtype=dt, device=dev)

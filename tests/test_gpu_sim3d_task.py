@@ -112,6 +112,44 @@ def test_teacher_forced_resets_truncations_and_commands():
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("name", ["g1_rough_scan", "go1_flat"])
+def test_velocity_penalties_angular_momentum_limits_foot_slip(name):
+    """PAPER.md §6.1's velocity penalties, each isolated by its weight: the robot's centroidal angular
+    momentum, joint-limit violation (joints loaded past their ranges) and foot slip (feet in ground contact,
+    read from the per-foot contact sensors, with random base velocities): kernel vs oracle, every step;
+    the feet's sensors equal the oracle's."""
+    import torch
+
+    n = 8
+    for term in (6, 7, 8):
+        wts = [0.0] * 9
+        wts[term] = 1.0
+        env, ref = _pair(name, n, reward_weights=tuple(wts), min_height=0.0, max_tilt_cos=1.0, push_interval=None)
+        env.reset()
+        ref.reset()
+        m = ref.m
+        lim = np.nonzero(m.jnt_limited)[0]
+        for w in range(n):
+            j = lim[w % lim.size]
+            ref.qpos[w, m.jnt_qposadr[j]] = m.jnt_range[j][w % 2] + (0.5 if w % 2 else -0.5)
+            ref.qvel[w, m.jnt_dofadr[j]] = 5.0 if w % 2 else -5.0  # still moving outwards
+            ref.qvel[w, 0:6] += np.random.default_rng(w).normal(size=6) * 0.5
+        rng = np.random.default_rng(4)
+        seen = 0.0
+        for k in range(2):
+            _load(env, ref)
+            a = rng.uniform(-1, 1, size=(n, env.model.nu))
+            o, r, te, tr = env.step(torch.as_tensor(a, device="cuda"))
+            o_ref, r_ref, te_ref, tr_ref = ref.step(a)
+            torch.cuda.synchronize()
+            np.testing.assert_allclose(r.cpu().numpy(), r_ref, rtol=1e-8, atol=1e-12)
+            np.testing.assert_array_equal(env.sensor.cpu().numpy(), ref.sensor)
+            seen = max(seen, float(np.abs(r_ref).max()))
+        assert seen > 0, term  # (the limit constraint pushes the joints back in range within a step or two)
+        assert len(env.sensor_names) == len(ref.cfg.foot_bodies(m)) and ref.sensor.max() > 0
+
+
+@pytest.mark.gpu
 def test_f32_task_close_to_oracle():
     import torch
 

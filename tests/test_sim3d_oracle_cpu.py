@@ -602,3 +602,33 @@ def test_box_stack_settles():
         assert np.abs(dq[a + 3:a + 7]).max() < 1e-4        # no spin / tilt
     assert np.abs(v).max() < 1e-3
     assert sum(1 for c in F["contacts"] if c["geom1"] != 0) == 8  # 4 per box-box face contact
+
+
+def test_centroidal_angular_momentum_is_fd_of_fk(model, rng):
+    """The velocity task's angular momentum (sum over the robot's bodies of cinert x cvel, angular part about
+    the tree's com) equals sum_b I_b w_b + m_b (x_b - c) x v_b with every body's com velocity and angular
+    velocity from finite differences of FK."""
+    from paper_2601_22074_b200.sim3d.task import VelocityTaskCfg
+
+    m = model
+    q, v = _random_state(m, rng)
+    cfg = VelocityTaskCfg(default_qpos=m.qpos0.copy(), reward_weights=(0,) * 6 + (1.0, 0.0, 0.0), feet=())
+    ref = O.TaskOracle(m, cfg, 1)
+    ref.qpos[0], ref.qvel[0] = q, v
+    h2, _, _ = ref.velocity_extras(0, np.zeros(0))
+    K = O.kinematics(m, q)
+    C = O.com_pos(m, K)
+    dt = 1e-6
+    Kp, Km = O.kinematics(m, O.integrate_pos(m, q, v, dt)), O.kinematics(m, O.integrate_pos(m, q, v, -dt))
+    c = C["com"][0]
+    h = np.zeros(3)
+    for b in range(1, m.nbody):
+        if m.body_treeid[b] != 0:
+            continue
+        R = K["ximat"][b]
+        W = (Kp["ximat"][b] - Km["ximat"][b]) / (2 * dt) @ R.T
+        wb = np.array([W[2, 1], W[0, 2], W[1, 0]])
+        vb = (Kp["xipos"][b] - Km["xipos"][b]) / (2 * dt)
+        I = R @ np.diag(m.body_inertia[b]) @ R.T
+        h += I @ wb + m.body_mass[b] * np.cross(K["xipos"][b] - c, vb)
+    assert abs(h2 - h @ h) < 1e-6 * max(1.0, h @ h)
