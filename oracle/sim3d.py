@@ -1455,7 +1455,7 @@ class MotionTaskOracle(TaskOracle):
             ev = float(np.sum((v[dofs] - vr[dofs]) ** 2))
             terms = [np.exp(-ej / s[0]), np.exp(-ev / s[1]), np.exp(-float(pe @ pe) / s[2]),
                      np.exp(-float(re @ re) / s[3]), float(np.sum((self.action[w] - self.prev_action[w]) ** 2)),
-                     0.0, 0.0, 0.0, 0.0, float(found[0]) if len(found) else 0.0]
+                     0.0, 0.0, 0.0, 0.0, float(found[0]) if (cfg.self_collision and len(found)) else 0.0]
             be = self.body_errors(w)
             for k in range(4):
                 terms[5 + k] = np.exp(-be[k] / s[4 + k])

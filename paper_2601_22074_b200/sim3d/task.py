@@ -168,7 +168,7 @@ class MotionTrackingCfg:
     motion_sigmas: tuple = (1.0, 50.0, 0.1, 0.5, 0.09, 0.16, 1.0, 9.8696)
     anchor_body: str | int | None = None      # None: BEYONDMIMIC_ANCHOR if the model has it, else body 1
     track_bodies: tuple | None = None         # None: BEYONDMIMIC_BODIES present in the model, else tree 0
-    self_collision: bool = True
+    self_collision: bool = True               # contact sensor 0 = robot-robot contacts, costed by term 9
     contact_sensors: tuple = ()               # extra sensors after the self-collision one
     max_height_error: float = 0.25
     max_ori_error: float = 0.8
@@ -316,6 +316,8 @@ class VelocityEnv3D:
             t.nframes, t.frame_dt = cfg.motion_qpos.shape[0], cfg.motion_dt
             t.motion_qpos, t.motion_qvel = self._motion_q.data_ptr(), self._motion_v.data_ptr()
             t.motion_sigmas[:] = padded(cfg.motion_sigmas, len(t.motion_sigmas))
+            if not cfg.self_collision:  # term 9 costs sensor 0, the self-collision sensor when there is one
+                t.reward_weights[9] = 0.0
             anchor, bodies = cfg.tracked(model)
             t.anchor_body, t.ntrack = anchor, len(bodies)
             t.track_body[:len(bodies)] = bodies
