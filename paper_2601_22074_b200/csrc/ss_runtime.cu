@@ -181,13 +181,25 @@ struct Pipe {
     bool used[8] = {};
     int nslot = 2, nhost = 3;
     int64_t submitted = 0, waited = 0;
-    int64_t deferred = -1;  // a step whose D2H waits to be paired with the next step's (see ss_pipe_post)
-    bool pair = true;       // SS_PIPE_PAIR=0 disables the pairing (A/B)
+    int group = 2;           // steps whose arenas cross PCIe as one copy (SS_PIPE_GROUP; 1 = one copy per step)
+    int64_t dstart = -1;     // first step of the group being collected (D2H deferred, see ss_pipe_post)
+    int dcount = 0;          // steps collected so far
     void* dev_actions[8] = {};
     void* stage[8] = {};
-    void* host[10] = {};  // nhost > nslot pinned blocks: a view step_wait returned survives the next step_async
+    void* host[16] = {};  // nhost > nslot pinned blocks: a view step_wait returned survives the next step_async
     int64_t action_bytes = 0, arena_bytes = 0;
 };
+
+// slots and host blocks of steps i .. i + group - 1 contiguous (one copy can move their arenas)
+bool group_contiguous(const Pipe* p, int64_t i) {
+    const int k = (int)(i % p->nslot), hk = (int)(i % p->nhost);
+    if (k + p->group > p->nslot || hk + p->group > p->nhost) return false;
+    for (int c = 1; c < p->group; ++c) {
+        if ((char*)p->stage[k] + (int64_t)c * p->arena_bytes != (char*)p->stage[k + c]) return false;
+        if ((char*)p->host[hk] + (int64_t)c * p->arena_bytes != (char*)p->host[hk + c]) return false;
+    }
+    return true;
+}
 
 // D2H of `count` consecutive steps' arenas starting at step i (slots and host blocks contiguous)
 cudaError_t pipe_copy(Pipe* p, int64_t i, int count) {
@@ -210,8 +222,8 @@ int pipe_err(cudaError_t e, const char* what) {
 extern "C" int ss_pipe_create(int32_t nslot, int32_t nhost, void* const* dev_actions, void* const* stage,
                               void* const* host, int64_t action_bytes, int64_t arena_bytes, void** out) {
     if (!dev_actions || !stage || !host || !out || arena_bytes <= 0 || action_bytes < 0 || nslot < 2 || nslot > 8 ||
-        nhost <= nslot || nhost > 10) {
-        ss_set_error("ss_pipe_create", "null buffer, empty arena, nslot outside [2, 8] or nhost outside (nslot, 10]");
+        nhost <= nslot || nhost > 16) {
+        ss_set_error("ss_pipe_create", "null buffer, empty arena, nslot outside [2, 8] or nhost outside (nslot, 16]");
         return -1;
     }
     Pipe* p = new Pipe();
@@ -233,8 +245,10 @@ extern "C" int ss_pipe_create(int32_t nslot, int32_t nhost, void* const* dev_act
     }
     p->action_bytes = action_bytes;
     p->arena_bytes = arena_bytes;
-    const char* pe = getenv("SS_PIPE_PAIR");
-    p->pair = !(pe && pe[0] == '0');
+    const char* pe = getenv("SS_PIPE_PAIR");  // 0: one copy per step (A/B)
+    const char* ge = getenv("SS_PIPE_GROUP");
+    p->group = (pe && pe[0] == '0') ? 1 : (ge ? atoi(ge) : 2);
+    if (p->group < 1 || p->group > nslot) p->group = 1;  // a collected group must fit the slots
     *out = p;
     return 0;
 }
@@ -302,21 +316,23 @@ extern "C" int ss_pipe_post(void* h, const void* arena, void* main_stream) {
     // (one stream: splitting the D2H over two copy-engine streams measured no faster, 36.4 vs 34.0 us/step)
     // Host blocks rotate over nhost > nslot: the block of step i is rewritten by step i + nhost, which cannot be
     // submitted before step i + 1 has been waited for.
-    // Pairing: back-to-back copies of one 1.58 MB arena each sustain ~31.3 us, of two arenas ~29.4 us per
-    // arena (tools/e2e_host.py), so when the slot and host block of an even step and its successor are
-    // contiguous the even step's D2H is deferred and issued as one copy with the next step's -- or alone, by
-    // ss_pipe_wait, if the caller waits for it first (results are never held back behind a step not yet
-    // submitted).
+    // Grouping: back-to-back copies of one 1.58 MB arena each sustain ~31.3 us, of two arenas ~29.4 us per
+    // arena, of four ~28.7 (tools/e2e_host.py), so when the slots and host blocks of `group` consecutive
+    // steps (the first a multiple of `group`) are contiguous, their D2H copies are deferred and issued as one
+    // once the last is submitted -- or, for the steps collected so far, by ss_pipe_wait if the caller waits
+    // for one of them first (results are never held back behind a step not yet submitted). The deferred
+    // steps are the latest submitted, fewer than group <= nslot, so a slot is never reused before its copy
+    // was issued.
     const int64_t i = p->submitted;
-    const int hk = (int)(i % p->nhost);
     if (e == cudaSuccess) {
-        if (p->deferred >= 0 && p->deferred == i - 1) {
-            e = pipe_copy(p, i - 1, 2);
-            p->deferred = -1;
-        } else if (p->pair && (i & 1) == 0 && k + 1 < p->nslot && hk + 1 < p->nhost &&
-                   (char*)p->stage[k] + p->arena_bytes == (char*)p->stage[k + 1] &&
-                   (char*)p->host[hk] + p->arena_bytes == (char*)p->host[hk + 1]) {
-            p->deferred = i;
+        if (p->dcount > 0) {  // i continues the group being collected
+            if (++p->dcount == p->group) {
+                e = pipe_copy(p, p->dstart, p->dcount);
+                p->dcount = 0;
+            }
+        } else if (p->group > 1 && i % p->group == 0 && group_contiguous(p, i)) {
+            p->dstart = i;
+            p->dcount = 1;
         } else {
             e = pipe_copy(p, i, 1);
         }
@@ -338,9 +354,9 @@ extern "C" int ss_pipe_wait(void* h) {
     const int k = (int)(p->waited % p->nslot);
     const int hk = (int)(p->waited % p->nhost);
     cudaError_t e = cudaSuccess;
-    if (p->deferred >= 0 && p->deferred == p->waited) {  // its pair partner is not submitted: copy it alone now
-        e = pipe_copy(p, p->waited, 1);
-        p->deferred = -1;
+    if (p->dcount > 0 && p->waited >= p->dstart) {  // its group is incomplete: copy the steps collected so far
+        e = pipe_copy(p, p->dstart, p->dcount);
+        p->dcount = 0;
     }
     if (e == cudaSuccess) e = cudaEventSynchronize(p->out_done[k]);
     if (e != cudaSuccess) return pipe_err(e, "ss_pipe_wait");

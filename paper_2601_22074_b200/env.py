@@ -49,6 +49,8 @@ __all__ = ["EnvCfg", "SceneCfg", "InitStateCfg", "ManagerBasedRlEnv", "load_capt
 # six keep the paired D2H copies (ss_pipe_post) fed -- 31.8 us per step at 4096 worlds vs 33.9 with four
 # unpaired slots, 41.8 with four paired (tools/e2e_ab.py)
 PIPE_SLOTS = int(os.environ.get("SS_PIPE_SLOTS", "6"))
+# steps whose results cross PCIe as one copy (ss_pipe_post; read by the native pipe from SS_PIPE_GROUP too)
+PIPE_GROUP = int(os.environ.get("SS_PIPE_GROUP", "2"))
 NF_LAG = 4  # control steps the host may run ahead before it must look at nonfinite flags
 
 _SIM = native.SS_ST_APPLY | native.SS_ST_PUSH | native.SS_ST_PHYS | native.SS_ST_SENSOR
@@ -589,7 +591,8 @@ class ManagerBasedRlEnv:
             A = self.action_manager.total_dim
             nb = self.step_outputs.numel()
             S = PIPE_SLOTS
-            H = S + 2 if S % 2 == 0 else S + 1  # even: steps pair up without wrapping (ss_pipe_post)
+            G = PIPE_GROUP if 1 < PIPE_GROUP <= S else 1
+            H = S + G if S % G == 0 else S + 1  # a multiple of G: groups of steps never wrap (ss_pipe_post)
             dev_actions = [torch.empty((self.num_envs, A), dtype=torch.float64, device=self.device) for _ in range(S)]
             # staging buffers and host blocks each carved from one allocation (contiguous for the paired
             # D2H when the arena size keeps them 16-byte aligned)
