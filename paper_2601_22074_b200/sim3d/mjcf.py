@@ -11,12 +11,13 @@ support. This loader covers the subset the 3-D kernels simulate:
   ``pos`` ``range`` ``damping`` ``armature``), ``<freejoint/>`` /
   ``type="free"``, ``<geom type="plane|sphere|capsule|box">`` (``size``,
   ``pos``, ``quat``, ``fromto``, ``friction``, ``contype``, ``conaffinity``);
-* ``<actuator><position joint kp kv forcerange>``.
+* ``<actuator><position joint kp kv forcerange>``;
+* ``<contact><exclude body1 body2/>`` (body pairs that never collide).
 
 Unsupported elements (mesh geoms, sites, sensors, tendons, equality
-constraints, slide / ball joints, other actuator types) are skipped with a
-warning, except joints, which raise (the dynamics would be wrong without
-them). A terrain is taken from a world plane geom, or added with
+constraints, explicit contact pairs, geoms with ``condim`` other than 3,
+slide / ball joints, other actuator types) are skipped with a warning, except
+joints, which raise (the dynamics would be wrong without them). A terrain is taken from a world plane geom, or added with
 ``terrain=`` ("plane" or a ModelBuilder.heightfield argument tuple).
 """
 
@@ -138,6 +139,8 @@ def load_mjcf(xml: str, terrain=None, opt: Opt | None = None) -> Model:
         if t not in _GEOMS:
             warnings.warn(f"MJCF geom type {t!r} skipped (unsupported)")
             return
+        if a.get("condim", "3") != "3":
+            warnings.warn(f"MJCF geom condim={a['condim']} simulated as condim 3 (pyramidal, sliding friction only)")
         size = list(_vec(a.get("size", "0")))
         kw = dict(friction=float(a.get("friction", "1").split()[0]), contype=int(a.get("contype", "1")),
                   conaffinity=int(a.get("conaffinity", "1")), name=a.get("name"))
@@ -190,6 +193,17 @@ def load_mjcf(xml: str, terrain=None, opt: Opt | None = None) -> Model:
                 walk(child, bid, ccls)
 
     walk(wb, 0, "main")
+    for tag in ("equality", "tendon", "sensor"):
+        sec = root.find(tag)
+        if sec is not None and len(sec):
+            warnings.warn(f"MJCF <{tag}> section skipped (unsupported): {len(sec)} element(s)")
+    con = root.find("contact")
+    if con is not None:
+        for c_el in con:
+            if c_el.tag == "exclude":
+                b.exclude_pair(c_el.get("body1"), c_el.get("body2"))
+            else:
+                warnings.warn(f"MJCF contact <{c_el.tag}> skipped (excludes only)")
     act = root.find("actuator")
     if act is not None:
         for a_el in act:

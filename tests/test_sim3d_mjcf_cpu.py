@@ -90,3 +90,27 @@ def test_mjcf_frames_defaults_and_errors():
     assert m.jnt_limited.tolist() == [1, 0]
     with pytest.raises(ModelError):
         load_mjcf(xml.replace('<joint name="j2" axis="0 1 0"/>', '<joint name="j2" type="slide"/>'))
+
+
+def test_mjcf_contact_excludes_and_skipped_sections():
+    """<contact><exclude> removes a body pair's collision candidates (the G1 MJCF's shin / thigh excludes);
+    <equality>, <tendon>, <sensor>, explicit <pair>s and condim != 3 are reported, not silently dropped."""
+    base = """<mujoco>
+  <worldbody>
+    <geom type="plane" size="1 1 1"/>
+    <body name="a" pos="0 0 1"><freejoint/><geom type="sphere" size="0.1"/></body>
+    <body name="b" pos="0 0 1.15"><freejoint/><geom type="sphere" size="0.1" condim="%s"/></body>
+  </worldbody>
+  %s
+</mujoco>"""
+    m = load_mjcf(base % ("3", ""))
+    assert [1, 2] in m.pair_geom.tolist()
+    m = load_mjcf(base % ("3", '<contact><exclude body1="a" body2="b"/></contact>'))
+    assert [1, 2] not in m.pair_geom.tolist() and [0, 1] in m.pair_geom.tolist()
+    extra = ('<equality><weld body1="a" body2="b"/></equality><tendon><fixed name="t"/></tendon>'
+             '<sensor><accelerometer site="s"/></sensor><contact><pair geom1="x" geom2="y"/></contact>')
+    with pytest.warns(UserWarning) as rec:
+        load_mjcf(base % ("1", extra))
+    msgs = " ".join(str(r.message) for r in rec)
+    for word in ("equality", "tendon", "sensor", "pair", "condim=1"):
+        assert word in msgs, word
