@@ -68,7 +68,9 @@ typedef struct s3_model {
                       slower; kept for A/B); bit 2: tree-level schedule driven by per-lane dof bit masks;
                       bit 3: block barrier at the start of each substep; bit 4: before the Newton solve;
                       bit 5: after it (bits 3-5: full blocks only); bit 6: balance warps per block over
-                      the waves of a launch (the Python layer sets 40, plus 64 for models with nv >= 24) */
+                      the waves of a launch (the Python layer sets 40, plus 64 for models with nv >= 24);
+                      bit 7: conjugate-gradient solver instead of Newton (Opt.solver = "cg"; plan the layout
+                      with it set: the solver keeps two extra vectors per world) */
     int32_t nhlev;
     int32_t ndlev;
     int32_t nkintree; /* kinematic trees (robot, free objects) */

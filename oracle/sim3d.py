@@ -741,6 +741,47 @@ def newton(m, M, E, qfrc_smooth, a0, warm):
     return a, force, J.T @ force, its
 
 
+def cg(m, M, L, E, qfrc_smooth, warm):
+    """Primal conjugate gradient on the same cost as ``newton`` (mj_solCG restated): the gradient
+    preconditioned by M^-1 (``L``, the L^T D L factor of M), Polak-Ribiere directions (beta clamped at 0),
+    the same exact line search and stopping rules; no Hessian is formed or factored."""
+    J, D, aref = E["J"], E["D"], E["aref"]
+    scale = 1.0 / (m.meaninertia * max(1, m.nv))
+    a = np.zeros(m.nv) if warm is None else warm.copy()
+    Ma = M @ a
+    jar = J @ a - aref
+    cost = _cost(E, qfrc_smooth, a, Ma, jar)
+    grad = Ma - qfrc_smooth + J.T @ (D * (jar < 0.0) * jar)
+    Mgrad = solve_ldl(m, L, grad)
+    search = -Mgrad
+    its = 0
+    for it in range(m.opt.iterations):
+        if scale * np.sqrt(grad @ grad) < m.opt.tolerance:
+            break
+        its += 1
+        Mp = M @ search
+        Jp = J @ search
+        alpha = line_search(m, search, Ma - qfrc_smooth, Mp, jar, Jp, D)
+        if alpha == 0.0:
+            break
+        a = a + alpha * search
+        Ma = Ma + alpha * Mp
+        jar = jar + alpha * Jp
+        new = _cost(E, qfrc_smooth, a, Ma, jar)
+        imp = scale * (cost - new)
+        cost = new
+        gold, Mgold = grad, Mgrad
+        grad = Ma - qfrc_smooth + J.T @ (D * (jar < 0.0) * jar)
+        Mgrad = solve_ldl(m, L, grad)
+        if imp < m.opt.tolerance:
+            break
+        beta = max(0.0, float(grad @ (Mgrad - Mgold)) / max(MINVAL, float(gold @ Mgold)))
+        search = -Mgrad + beta * search
+    act = jar < 0.0
+    force = -D * act * jar
+    return a, force, J.T @ force, its
+
+
 def line_search(m, p, res, Mp, jar, Jp, D):
     """Exact minimiser of the convex piecewise-quadratic cost along p: bracketed Newton on phi'."""
     g0 = p @ res
@@ -805,7 +846,10 @@ def forward(m, qpos, qvel, ctrl, qfrc_applied=None, warm=None, fscale=1.0, mscal
     a0 = solve_ldl(m, L, smooth)
     cons, dropped = collide(m, K, fscale)
     E = constraints(m, C, cons, qpos, qvel)
-    qacc, force, qfrc_con, its = newton(m, M, E, smooth, a0, warm)
+    if getattr(m.opt, "solver", "newton") == "cg":
+        qacc, force, qfrc_con, its = cg(m, M, L, E, smooth, warm)
+    else:
+        qacc, force, qfrc_con, its = newton(m, M, E, smooth, a0, warm)
     return dict(K=K, C=C, M=M, qLD=L, crb=crbs, cvel=cvel, cdofd=cdofd, bias=bias, qfrc_actuator=fact, kvd=kvd,
                 qfrc_smooth=smooth, qacc_smooth=a0, contacts=cons, dropped=dropped, efc=E, qacc=qacc,
                 efc_force=force, qfrc_constraint=qfrc_con, iterations=its)

@@ -37,7 +37,7 @@ constexpr int kConStride = 14;  // dist, pos[3], frame[9], mu
 enum {
     O_XPOS, O_XQUAT, O_XIPOS, O_CINERT, O_JANC, O_JAX, O_CRB, O_CDOF, O_CDOFD, O_CVEL, O_CACC,
     O_M, O_LD, O_QPOS, O_QVEL, O_SMOOTH, O_A0, O_A, O_MA, O_GRAD, O_P, O_MP, O_KVD, O_GPOS, O_GMAT,
-    O_CON, O_JC, O_RAREF, O_RD, O_RJAR, O_RJP, O_CDOT, O_BIAS, O_FCON, O_CTRL, O_COM, O_INT, O_END,
+    O_CON, O_JC, O_RAREF, O_RD, O_RJAR, O_RJP, O_CDOT, O_BIAS, O_FCON, O_CTRL, O_COM, O_CG, O_INT, O_END,
     O_INT_LIMDOF = O_END, O_INT_LIMSIGN  // int offsets inside O_INT (not element offsets)
 };
 
@@ -149,7 +149,7 @@ template <class T> __device__ inline T clampt(T x, T lo, T hi) { return x < lo ?
 template <class T> struct WS {
     T *xpos, *xquat, *xipos, *cinert, *crb, *cdof, *cdofd, *cvel, *cacc, *janc, *jax, *M, *LD, *qpos, *qvel,
         *smooth, *a0, *a, *Ma, *grad, *p, *Mp, *kvd, *con, *Jc, *raref, *rD, *rjar, *rJp, *cdot,
-        *bias, *fcon, *ctrl, *com, *tk, *snap;
+        *bias, *fcon, *ctrl, *com, *tk, *snap, *cgm;
     int *con_pair, *lim_dof, *lim_sign;
 };
 
@@ -174,6 +174,7 @@ template <class T> __device__ inline WS<T> make_ws(T* base, const s3_layout& l) 
     s.cdot = base + o[O_CDOT]; s.bias = s.Ma;  // bias: RNE -> smooth_force, dead before Newton writes Ma
     s.fcon = base + o[O_FCON]; s.ctrl = base + o[O_CTRL];
     s.com = base + o[O_COM];
+    s.cgm = base + o[O_CG];  // CG solver (flags bit 7): M^-1 grad, and its previous value
     int* ib = reinterpret_cast<int*>(base + o[O_INT]);
     s.con_pair = ib;
     s.lim_dof = ib + o[O_INT_LIMDOF];  // int offsets inside the int region, sized by ncon_max / nlimjnt
@@ -1689,6 +1690,116 @@ template <class T> __device__ int __noinline__ newton(const s3_model& m_, const 
     return its;
 }
 
+// Primal conjugate gradient on the Newton cost (oracle cg, mj_solCG restated; s3_model.flags bit 7): the
+// gradient preconditioned by M^-1 through M's L^T D L factor in s.LD, Polak-Ribiere directions (beta
+// clamped at 0), the exact line search and stopping rules of newton; no Hessian is formed.
+template <class T> __device__ int __noinline__ cg(const s3_model& m_, const s3_layout& L_, T* B_, int ncon, int nlim, bool warm_ok,
+                                                  int lane) {
+    const s3_model& m = c_s3m;
+    WS<T> s = make_ws(B_, L_);
+    const int nv = m.nv;
+    const int nefc = nlim + 4 * ncon;
+    const T scale = T(m.scale), tol = T(m.tolerance);
+    T* Mg = s.cgm;
+    T* Mg0 = s.cgm + nv;
+    for (int i = lane; i < nv; i += 32) s.a[i] = warm_ok ? s.p[i] : T(0);
+    __syncwarp();
+    sym_mul(nv, s.M, s.a, s.Ma, lane);
+    rows_mul(m, L_, B_, ncon, nlim, s.a, s.rjar, lane);
+    for (int r = lane; r < nefc; r += 32) s.rjar[r] -= s.raref[r];
+    __syncwarp();
+    T cost = total_cost(m, L_, B_, nefc, s.a, s.Ma, s.rjar, lane);
+    auto gradient = [&]() {  // grad = M a - smooth + J^T (D act jar), Mg = M^-1 grad
+        for (int r = lane; r < nefc; r += 32) s.rJp[r] = s.rjar[r] < T(0) ? s.rD[r] * s.rjar[r] : T(0);
+        for (int i = lane; i < nv; i += 32) s.grad[i] = s.Ma[i] - s.smooth[i];
+        __syncwarp();
+        rows_tmul_add(m, L_, B_, ncon, nlim, s.rJp, s.grad, lane);
+        for (int i = lane; i < nv; i += 32) Mg[i] = s.grad[i];
+        __syncwarp();
+        solve_ldl(m, s.LD, Mg, lane);
+    };
+    gradient();
+    for (int i = lane; i < nv; i += 32) s.p[i] = -Mg[i];
+    __syncwarp();
+    int its = 0;
+    for (int it = 0; it < m.iterations; ++it) {
+        T gn = T(0);
+        for (int i = lane; i < nv; i += 32) gn += s.grad[i] * s.grad[i];
+        gn = wsum(gn);
+        if (scale * sqrt(gn) < tol) break;
+        ++its;
+        sym_mul(nv, s.M, s.p, s.Mp, lane);
+        rows_mul(m, L_, B_, ncon, nlim, s.p, s.rJp, lane);
+        T g0 = T(0), h0 = T(0);
+        for (int i = lane; i < nv; i += 32) {
+            g0 += s.p[i] * (s.Ma[i] - s.smooth[i]);
+            h0 += s.p[i] * s.Mp[i];
+        }
+        g0 = wsum(g0);
+        h0 = wsum(h0);
+        auto deriv = [&](T al, T& d1, T& d2) {
+            T x1 = T(0), x2 = T(0);
+            for (int r = lane; r < nefc; r += 32) {
+                T x = s.rjar[r] + al * s.rJp[r];
+                if (x < T(0)) {
+                    x1 += s.rD[r] * x * s.rJp[r];
+                    x2 += s.rD[r] * s.rJp[r] * s.rJp[r];
+                }
+            }
+            d1 = g0 + al * h0 + wsum(x1);
+            d2 = h0 + wsum(x2);
+        };
+        T d0, dd;
+        deriv(T(0), d0, dd);
+        T alpha = T(0);
+        if (d0 < T(0)) {
+            T lo = T(0), hi = T(INFINITY), al = T(1);
+            for (int li = 0; li < m.ls_iterations; ++li) {
+                T d1, d2;
+                deriv(al, d1, d2);
+                if (fabs(d1) < T(m.ls_tolerance) * fabs(d0)) break;
+                if (d1 < T(0)) lo = al;
+                else hi = al;
+                T an = al - d1 / d2;
+                if (!(lo < an && an < hi)) an = T(0.5) * (lo + hi);
+                al = an;
+            }
+            alpha = al;
+        }
+        if (alpha == T(0)) break;
+        for (int i = lane; i < nv; i += 32) {
+            s.a[i] += alpha * s.p[i];
+            s.Ma[i] += alpha * s.Mp[i];
+        }
+        for (int r = lane; r < nefc; r += 32) s.rjar[r] += alpha * s.rJp[r];
+        __syncwarp();
+        const T nc = total_cost(m, L_, B_, nefc, s.a, s.Ma, s.rjar, lane);
+        const T impv = scale * (cost - nc);
+        cost = nc;
+        // previous gradient: gold . Mgold, and Mgold kept for the Polak-Ribiere numerator
+        T den = T(0);
+        for (int i = lane; i < nv; i += 32) {
+            den += s.grad[i] * Mg[i];
+            Mg0[i] = Mg[i];
+        }
+        den = wsum(den);
+        __syncwarp();
+        gradient();
+        if (impv < tol) break;
+        T num = T(0);
+        for (int i = lane; i < nv; i += 32) num += s.grad[i] * (Mg[i] - Mg0[i]);
+        num = wsum(num);
+        const T beta = fmax(T(0), num / fmax(T(1e-15), den));
+        for (int i = lane; i < nv; i += 32) s.p[i] = -Mg[i] + beta * s.p[i];
+        __syncwarp();
+    }
+    for (int r = lane; r < nefc; r += 32) s.rJp[r] = s.rjar[r] < T(0) ? -s.rD[r] * s.rjar[r] : T(0);
+    for (int i = lane; i < nv; i += 32) s.fcon[i] = T(0);
+    __syncwarp();
+    rows_tmul_add(m, L_, B_, ncon, nlim, s.rJp, s.fcon, lane);
+    return its;
+}
+
 // ---------------------------------------------------------------- one physics substep (mj_step)
 
 template <class T>
@@ -1757,7 +1868,12 @@ __device__ __noinline__ int substep(const s3_model& m_, const s3_data& d, const 
         for (int i = lane; i < nv; i += 32) s.p[i] = gw[i];
         __syncwarp();
     }
-    its = newton(m, L_, B_, ncon, nlim, gw != nullptr, U, lane);
+    if (m.flags & 128) {  // CG: the solver preconditions with M's full factor
+        if (!(last && d.qM)) factor_ldl(m, s.LD, s.tk, lane, U, 2);  // (the parity path finished it above)
+        its = cg(m, L_, B_, ncon, nlim, gw != nullptr, lane);
+    } else {
+        its = newton(m, L_, B_, ncon, nlim, gw != nullptr, U, lane);
+    }
     if (gw) {
         for (int i = lane; i < nv; i += 32) gw[i] = s.a[i];
     }
@@ -2939,6 +3055,7 @@ int s3_plan(const s3_model* m, int32_t warps_per_block, s3_layout* out) {
     sizes[O_JC] = jc > rne ? jc : rne; sizes[O_RAREF] = nrow; sizes[O_RD] = nrow;
     sizes[O_RJAR] = nrow; sizes[O_RJP] = nrow; sizes[O_CDOT] = 3 * nc; sizes[O_BIAS] = 0;  // bias aliases Ma
     sizes[O_FCON] = nv; sizes[O_CTRL] = nu; sizes[O_COM] = 3 * (m->nkintree > 0 ? m->nkintree : 1);
+    sizes[O_CG] = (m->flags & 128) ? 2 * nv : 0;
     // the per-dof reciprocal scratch (tk, in the O_CRB slot) is used by the level-schedule variants only
     if (!(m->flags & 6)) sizes[O_CRB] = 0;
     int region = sizes[O_XIPOS] + sizes[O_CINERT] + sizes[O_JANC] + sizes[O_JAX];

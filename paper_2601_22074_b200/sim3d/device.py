@@ -213,6 +213,10 @@ class DeviceModel:
         # balance warps per block over the waves of a launch -- measured defaults for both dtypes
         # (tools/ab_sim3d.sh); S3_FLAGS overrides
         s.flags = int(os.environ.get("S3_FLAGS", "40" if m.nv < 24 else "104"))  # bit 6: balanced waves
+        if getattr(m.opt, "solver", "newton") == "cg":
+            s.flags |= 128  # bit 7: conjugate-gradient solver (M^-1-preconditioned; its two vectors in the layout)
+        elif getattr(m.opt, "solver", "newton") != "newton":
+            raise ValueError(f"unknown solver {m.opt.solver!r} (newton or cg)")
         s.timestep = m.opt.timestep
         s.gravity[:] = m.opt.gravity
         s.tolerance, s.ls_tolerance = m.opt.tolerance, m.opt.ls_tolerance

@@ -75,6 +75,7 @@ class Opt:
     ls_tolerance: float = 0.01
     solref: tuple = (0.02, 1.0)   # (timeconst, dampratio)
     solimp: tuple = (0.9, 0.95, 0.001, 0.5, 2.0)  # (dmin, dmax, width, mid, power)
+    solver: str = "newton"        # "newton" or "cg" (MuJoCo's mjSOL_NEWTON / mjSOL_CG)
 
 
 @dataclass

@@ -20,7 +20,7 @@ import pytest
 
 from oracle import sim3d as O
 from paper_2601_22074_b200.sim3d import robots
-from paper_2601_22074_b200.sim3d.model import MAX_CON
+from paper_2601_22074_b200.sim3d.model import MAX_CON, Opt
 
 ROBOTS = {
     "g1_flat": (lambda: robots.g1_like(), robots.G1_DEFAULT_JOINTS),
@@ -28,6 +28,9 @@ ROBOTS = {
     "go1_flat": (lambda: robots.go1_like(), robots.GO1_DEFAULT_JOINTS),
     "arm_cube": (lambda: robots.arm_cube_like(), robots.ARM_DEFAULT_JOINTS),
     "box_stack": (lambda: robots.box_stack(), {}),
+    # the conjugate-gradient solver (Opt.solver = "cg", s3_model.flags bit 7)
+    "g1_flat_cg": (lambda: robots.g1_like(opt=Opt(solver="cg")), robots.G1_DEFAULT_JOINTS),
+    "box_stack_cg": (lambda: robots.box_stack(opt=Opt(solver="cg")), {}),
 }
 
 
@@ -216,8 +219,8 @@ def test_rollout_f64(name):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", list(ROBOTS))
-def test_single_substep_f32(name):
+@pytest.mark.parametrize("name", [r for r in ROBOTS if not r.endswith("_cg")])  # CG stops at its iteration
+def test_single_substep_f32(name):  # cap short of the optimum: f32 rounding steers it elsewhere (f64 pinned above)
     import torch
 
     from paper_2601_22074_b200.sim3d.device import unpack_lower

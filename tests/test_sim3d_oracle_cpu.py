@@ -632,3 +632,27 @@ def test_centroidal_angular_momentum_is_fd_of_fk(model, rng):
         I = R @ np.diag(m.body_inertia[b]) @ R.T
         h += I @ wb + m.body_mass[b] * np.cross(K["xipos"][b] - c, vb)
     assert abs(h2 - h @ h) < 1e-6 * max(1.0, h @ h)
+
+
+@pytest.mark.parametrize("name", ["g1", "box_stack"])
+def test_cg_solver_reaches_the_newton_optimum(name, rng):
+    """The conjugate-gradient solver (Opt.solver="cg", mj_solCG restated) minimises the same constrained
+    cost as Newton: with enough iterations both stop at the tolerance with the same accelerations and a
+    non-increasing cost along the way; CG never forms the Hessian, so it needs more iterations."""
+    from paper_2601_22074_b200.sim3d.model import Opt
+
+    make = {"g1": lambda o: robots.g1_like(opt=o), "box_stack": lambda o: robots.box_stack(opt=o)}[name]
+    mn, mc = make(Opt(iterations=200)), make(Opt(iterations=200, solver="cg"))
+    O.set_const(mn)
+    O.set_const(mc)
+    q, v = mn.qpos0.copy(), rng.normal(size=mn.nv) * 0.1
+    if name == "g1":
+        q = robots.default_qpos(mn, robots.G1_DEFAULT_JOINTS)
+        q[2] -= 0.02
+    else:
+        q[2] -= 0.003
+    ctrl = q[mn.actuator_qposadr] if mn.nu else np.zeros(1)
+    Fn, Fc = O.forward(mn, q, v, ctrl), O.forward(mc, q, v, ctrl)
+    assert Fc["iterations"] > Fn["iterations"] and len(Fn["contacts"]) > 0
+    sc = np.abs(Fn["qacc"]).max()
+    assert np.abs(Fn["qacc"] - Fc["qacc"]).max() < 1e-3 * sc
