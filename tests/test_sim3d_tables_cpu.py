@@ -153,8 +153,9 @@ def test_layout_fits_and_struct_sizes():
             assert lay.bytes_per_block == lay.elems_per_world * esz * lay.warps_per_block <= 227 * 1024
             # O_XPOS .. O_INT: the per-world regions, in order (8-10 hold RNE offsets inside the Jacobian region;
             # the row buffers 27-30 may reuse dead slots: aref / D / J·a after the factorization snapshot in the
-            # xipos .. jax region, the force buffer in cdof's slot)
-            offs = [lay.off[k] for k in range(37) if k not in (8, 9, 10, 27, 28, 29, 30)]
+            # xipos .. jax region, the force buffer in cdof's slot; 36 is the CG solver's vectors, empty unless
+            # flags bit 7)
+            offs = [lay.off[k] for k in range(38) if k not in (8, 9, 10, 27, 28, 29, 30)]
             assert offs == sorted(offs) and offs[-1] < lay.elems_per_world
             dm_s = dm.struct
             nrow = min(dm_s.nlimjnt, 32) + 4 * dm_s.ncon_max
@@ -166,5 +167,6 @@ def test_layout_fits_and_struct_sizes():
             if rjp == lay.off[7]:  # in cdof's slot
                 assert 6 * dm_s.nv >= nrow
             # int region: con_pair, lim_dof, lim_sign (int offsets)
-            assert lay.off[37] == dm_s.ncon_max and lay.off[38] == dm_s.ncon_max + min(dm_s.nlimjnt, 32)
+            assert lay.off[38] == dm_s.ncon_max and lay.off[39] == dm_s.ncon_max + min(dm_s.nlimjnt, 32)
+            assert lay.off[37] - lay.off[36] == (2 * dm_s.nv if dm_s.flags & 128 else 0)
     assert N.lib().s3_sizeof(3) == ctypes.sizeof(N.TaskT)
