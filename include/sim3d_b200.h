@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define S3_ABI_VERSION 19
+#define S3_ABI_VERSION 20
 #define S3_F64 0
 #define S3_F32 1
 
@@ -141,6 +141,8 @@ typedef struct s3_model {
     const int32_t* pair_geom;
     const uint8_t* pair_chain;
     const int32_t* pair_chainlen;
+    const uint8_t* pair_condim; /* 1: frictionless (mu = 0, its 4 pyramid rows at 1/4 the normal stiffness each,
+                                   i.e. MuJoCo's single normal row), 3: pyramidal sliding friction */
     /* actuators */
     const int32_t* act_dofadr;
     const int32_t* act_qposadr;

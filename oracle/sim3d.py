@@ -542,7 +542,7 @@ def collide(m, K, fscale=1.0):
     for p, (g1, g2) in enumerate(m.pair_geom):
         t1, t2 = m.geom_type[g1], m.geom_type[g2]
         c1, c2 = K["geom_xpos"][g1], K["geom_xpos"][g2]
-        mu = max(m.geom_friction[g1], m.geom_friction[g2]) * fscale
+        mu = 0.0 if m.pair_condim[p] == 1 else max(m.geom_friction[g1], m.geom_friction[g2]) * fscale
         found = []
         if t1 == GEOM_PLANE:
             n = K["geom_xmat"][g1][:, 2]
@@ -652,7 +652,9 @@ def constraints(m, C, cons, qpos, qvel):
         Jp = point_jac(m, C, b2, c["pos"]) - point_jac(m, C, b1, c["pos"])
         Jc = c["frame"] @ Jp
         mu = c["mu"]
-        A = (1.0 + mu * mu) * (m.body_invweight0[b1] + m.body_invweight0[b2])
+        # condim 1 (frictionless): mu = 0 turns the 4 pyramid rows into the normal row; with 4x the normal
+        # row's R each, their sum is MuJoCo's single frictionless row (identical cost, Hessian, total force)
+        A = (4.0 if m.pair_condim[c["pair"]] == 1 else 1.0 + mu * mu) * (m.body_invweight0[b1] + m.body_invweight0[b2])
         for k in (1, 2):
             for s in (1.0, -1.0):
                 rows.append(dict(J=Jc[0] + (s * mu) * Jc[k], pos=c["dist"], A=A))

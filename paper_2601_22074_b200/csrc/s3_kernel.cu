@@ -1285,7 +1285,7 @@ template <class T> __device__ int __noinline__ collide(const s3_model& m_, const
         int off = base + incl - cnt;
         if (cnt) {
             int g1 = m.pair_geom[2 * p], g2 = m.pair_geom[2 * p + 1];
-            T mu = fmax(fric[g1], fric[g2]) * fscale;
+            T mu = m.pair_condim[p] == 1 ? T(0) : fmax(fric[g1], fric[g2]) * fscale;  // condim 1: frictionless
             for (int k = 0; k < cnt; ++k) {
                 int slot = off + k;
                 if (slot < m.ncon_max) {
@@ -1434,7 +1434,9 @@ template <class T> __device__ int __noinline__ build_rows(const s3_model& m_, co
             vel = s.cdot[3 * c] + sg * s.cdot[3 * c + 1 + (e >> 1)];
             int p = s.con_pair[c];
             int b1 = m.geom_bodyid[m.pair_geom[2 * p]], b2 = m.geom_bodyid[m.pair_geom[2 * p + 1]];
-            A = (T(1) + mu * mu) * (iw[b1] + iw[b2]);
+            // condim 1: mu = 0 makes the 4 pyramid rows the normal row; at 4x its R each they sum to MuJoCo's
+            // single frictionless row (same cost, Hessian and total force)
+            A = (m.pair_condim[p] == 1 ? T(4) : T(1) + mu * mu) * (iw[b1] + iw[b2]);
         }
         T imp = impedance(m, pos);
         T R = fmax((T(1) - imp) / imp * A, T(1e-15));

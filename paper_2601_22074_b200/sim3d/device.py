@@ -155,6 +155,7 @@ class DeviceModel:
             lim_dofadr=np.append(m.jnt_dofadr[lim], 0).astype(np.int32),
             geom_type=m.geom_type, geom_bodyid=m.geom_bodyid, pair_geom=np.append(m.pair_geom.reshape(-1), [0, 0]),
             pair_chain=pair_chain, pair_chainlen=pair_chainlen,
+            pair_condim=np.append(m.pair_condim, 3).astype(np.uint8),
             act_dofadr=np.append(m.actuator_dofadr, 0).astype(np.int32),
             act_qposadr=np.append(m.actuator_qposadr, 0).astype(np.int32),
             act_kind=np.append(m.actuator_kind, 0).astype(np.int32),

@@ -15,7 +15,7 @@ support. This loader covers the subset the 3-D kernels simulate:
 * ``<contact><exclude body1 body2/>`` (body pairs that never collide).
 
 Unsupported elements (mesh geoms, sites, sensors, tendons, equality
-constraints, explicit contact pairs, geoms with ``condim`` other than 3,
+constraints, explicit contact pairs, geoms with ``condim`` other than 1 / 3,
 slide / ball joints, other actuator types) are skipped with a warning, except
 joints, which raise (the dynamics would be wrong without them). A terrain is taken from a world plane geom, or added with
 ``terrain=`` ("plane" or a ModelBuilder.heightfield argument tuple).
@@ -139,11 +139,13 @@ def load_mjcf(xml: str, terrain=None, opt: Opt | None = None) -> Model:
         if t not in _GEOMS:
             warnings.warn(f"MJCF geom type {t!r} skipped (unsupported)")
             return
-        if a.get("condim", "3") != "3":
-            warnings.warn(f"MJCF geom condim={a['condim']} simulated as condim 3 (pyramidal, sliding friction only)")
+        condim = int(a.get("condim", "3"))
+        if condim not in (1, 3):
+            warnings.warn(f"MJCF geom condim={condim} simulated as condim 3 (pyramidal, sliding friction only)")
+            condim = 3
         size = list(_vec(a.get("size", "0")))
         kw = dict(friction=float(a.get("friction", "1").split()[0]), contype=int(a.get("contype", "1")),
-                  conaffinity=int(a.get("conaffinity", "1")), name=a.get("name"))
+                  conaffinity=int(a.get("conaffinity", "1")), name=a.get("name"), condim=condim)
         if "fromto" in a:
             b.geom(bid, _GEOMS[t], size[:1], fromto=_vec(a["fromto"], 6), **kw)
         else:

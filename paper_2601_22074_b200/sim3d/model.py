@@ -146,7 +146,10 @@ class ModelBuilder:
 
     # -- geometry -------------------------------------------------------------
     def geom(self, body, type, size, pos=(0, 0, 0), quat=(1, 0, 0, 0), friction=1.0, contype=1, conaffinity=1,
-             fromto=None, name=None):
+             fromto=None, name=None, condim=3):
+        """condim 3: pyramidal sliding friction; 1: frictionless (a pair takes the larger of its geoms')."""
+        if condim not in (1, 3):
+            raise ModelError(f"condim {condim} is not supported (1 or 3)")
         b = self.body_id(body) if isinstance(body, str) else body
         size = list(size) + [0.0] * (3 - len(size))
         pos = np.asarray(pos, dtype=np.float64)
@@ -166,11 +169,11 @@ class ModelBuilder:
                 q = axis_angle(v / s, np.arctan2(s, np.dot(z, d / L)))
         self.geoms.append(dict(name=name, type=int(type), body=b, size=np.asarray(size, dtype=np.float64), pos=pos,
                                quat=q / np.linalg.norm(q), friction=float(friction), contype=int(contype),
-                               conaffinity=int(conaffinity)))
+                               conaffinity=int(conaffinity), condim=int(condim)))
         return len(self.geoms) - 1
 
-    def plane(self, friction=1.0):
-        return self.geom(0, GEOM_PLANE, (0, 0, 0), friction=friction)
+    def plane(self, friction=1.0, condim=3):
+        return self.geom(0, GEOM_PLANE, (0, 0, 0), friction=friction, condim=condim)
 
     def heightfield(self, data, spacing, origin=(0.0, 0.0), friction=1.0):
         """Terrain as a (nrow, ncol) height grid (rows along y, cols along x), cell size ``spacing``,
@@ -338,6 +341,7 @@ class Model:
         self.geom_pos = np.array([g["pos"] for g in G]).reshape(-1, 3)
         self.geom_quat = np.array([g["quat"] for g in G]).reshape(-1, 4)
         self.geom_friction = np.array([g["friction"] for g in G])
+        self.geom_condim = np.array([g.get("condim", 3) for g in G], dtype=np.int32)
         self.geom_rbound = np.array([_rbound(g) for g in G])
         self.geom_contype = np.array([g["contype"] for g in G], dtype=np.int32)
         self.geom_conaffinity = np.array([g["conaffinity"] for g in G], dtype=np.int32)
@@ -382,6 +386,10 @@ class Model:
                 pairs.append((g1, g2))
         self.npair = len(pairs)
         self.pair_geom = np.array(pairs, dtype=np.int32).reshape(-1, 2)
+        # a pair's contact dimensionality is the larger of its geoms' (MuJoCo's rule at equal priority):
+        # 1 = frictionless normal contact, 3 = pyramidal sliding friction
+        self.pair_condim = np.array([max(self.geom_condim[g1], self.geom_condim[g2]) for g1, g2 in pairs],
+                                    dtype=np.uint8)
         self.pair_chain = []
         for g1, g2 in pairs:
             c = sorted(set(self.body_chain[self.geom_bodyid[g1]]) | set(self.body_chain[self.geom_bodyid[g2]]))

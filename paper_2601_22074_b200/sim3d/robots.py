@@ -281,19 +281,20 @@ def arm_cube_like(opt: Opt | None = None, cube_size: float = 0.025):
 
 
 def box_stack(opt: Opt | None = None, sizes=((0.25, 0.18, 0.08), (0.12, 0.09, 0.06), (0.07, 0.05, 0.04)),
-              yaws=(0.1, 0.5, -0.3)):
+              yaws=(0.1, 0.5, -0.3), condims=(3, 3, 3)):
     """Free boxes stacked on a plane (box-box and box-plane contacts; one kinematic tree per box), each
-    resting 2 mm into the one below at a different yaw: the narrowphase scene for box-box contacts."""
+    resting 2 mm into the one below at a different yaw: the narrowphase scene for box-box contacts.
+    ``condims``: each box's contact dimensionality (a pair of two condim-1 boxes is frictionless)."""
     b = ModelBuilder("box_stack", opt)
     b.plane(friction=1.0)
     z = 0.0
-    for k, (h, yaw) in enumerate(zip(sizes, yaws)):
+    for k, (h, yaw, cd) in enumerate(zip(sizes, yaws, condims)):
         z += h[2] - 0.002
         mass = 500.0 * 8 * h[0] * h[1] * h[2]
         inertia = tuple(mass / 3.0 * (h[(i + 1) % 3] ** 2 + h[(i + 2) % 3] ** 2) for i in range(3))
         body = b.body(f"box{k}", 0, pos=(0.02 * k, -0.01 * k, z), quat=(np.cos(0.5 * yaw), 0, 0, np.sin(0.5 * yaw)),
                       mass=mass, inertia=inertia)
         b.free_joint(body)
-        b.geom(body, GEOM_BOX, h, friction=0.8, name=f"box{k}")
+        b.geom(body, GEOM_BOX, h, friction=0.8, name=f"box{k}", condim=cd)
         z += h[2]
     return b.compile()

@@ -31,6 +31,8 @@ ROBOTS = {
     # the conjugate-gradient solver (Opt.solver = "cg", s3_model.flags bit 7)
     "g1_flat_cg": (lambda: robots.g1_like(opt=Opt(solver="cg")), robots.G1_DEFAULT_JOINTS),
     "box_stack_cg": (lambda: robots.box_stack(opt=Opt(solver="cg")), {}),
+    # frictionless (condim 1) contact between the upper two boxes
+    "box_stack_condim1": (lambda: robots.box_stack(condims=(3, 1, 1)), {}),
 }
 
 
@@ -196,6 +198,7 @@ def test_single_substep_f64_all_stages(name):
         assert _rel(qn[w], q1) < 1e-11
     assert saw_contacts >= n // 2 and (saw_limits > 0 or m.nlim == 0)
     if m.name == "box_stack":  # box-box contacts (geom pairs of two boxes) in every world
+        assert any(m.pair_condim[c["pair"]] == 1 for c in cons) or m.pair_condim.min() == 3
         assert saw_self == n
 
 

@@ -94,7 +94,8 @@ def test_mjcf_frames_defaults_and_errors():
 
 def test_mjcf_contact_excludes_and_skipped_sections():
     """<contact><exclude> removes a body pair's collision candidates (the G1 MJCF's shin / thigh excludes);
-    <equality>, <tendon>, <sensor>, explicit <pair>s and condim != 3 are reported, not silently dropped."""
+    <equality>, <tendon>, <sensor>, explicit <pair>s and condim other than 1 / 3 are reported, not silently
+    dropped; condim 1 makes a frictionless pair."""
     base = """<mujoco>
   <worldbody>
     <geom type="plane" size="1 1 1"/>
@@ -110,7 +111,10 @@ def test_mjcf_contact_excludes_and_skipped_sections():
     extra = ('<equality><weld body1="a" body2="b"/></equality><tendon><fixed name="t"/></tendon>'
              '<sensor><accelerometer site="s"/></sensor><contact><pair geom1="x" geom2="y"/></contact>')
     with pytest.warns(UserWarning) as rec:
-        load_mjcf(base % ("1", extra))
+        load_mjcf(base % ("6", extra))
     msgs = " ".join(str(r.message) for r in rec)
-    for word in ("equality", "tendon", "sensor", "pair", "condim=1"):
+    for word in ("equality", "tendon", "sensor", "pair", "condim=6"):
         assert word in msgs, word
+    m = load_mjcf((base % ("1", "")).replace('<geom type="sphere" size="0.1"/>', '<geom type="sphere" size="0.1" condim="1"/>'))
+    # a pair takes the larger condim of its geoms (MuJoCo): frictionless between the two spheres only
+    assert m.pair_condim[m.pair_geom.tolist().index([1, 2])] == 1 and m.pair_condim[0] == 3

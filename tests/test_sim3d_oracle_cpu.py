@@ -656,3 +656,36 @@ def test_cg_solver_reaches_the_newton_optimum(name, rng):
     assert Fc["iterations"] > Fn["iterations"] and len(Fn["contacts"]) > 0
     sc = np.abs(Fn["qacc"]).max()
     assert np.abs(Fn["qacc"] - Fc["qacc"]).max() < 1e-3 * sc
+
+
+def _ball_on_slope(condim, tilt=0.3):
+    """A ball resting 1 mm into a plane tilted by `tilt` about x (gravity rotated instead of the plane)."""
+    from paper_2601_22074_b200.sim3d.model import Opt
+
+    g = 9.81
+    b = ModelBuilder("ball", Opt(gravity=(0.0, g * np.sin(tilt), -g * np.cos(tilt)), iterations=50))
+    b.plane(friction=1.0, condim=condim)  # both geoms: a pair takes the larger condim
+    ball = b.body("ball", 0, pos=(0, 0, 0.099), mass=1.0, inertia=(0.004, 0.004, 0.004))
+    b.free_joint(ball)
+    b.geom(ball, GEOM_SPHERE, (0.1,), friction=1.0, condim=condim)
+    m = b.compile()
+    O.set_const(m)
+    return m
+
+
+def test_condim1_frictionless_contact_equals_one_normal_row():
+    """condim 1: the contact's 4 pyramid rows (mu = 0, 4x the normal row's R each) minimise exactly the cost
+    of MuJoCo's single frictionless row -- same accelerations as the one-row problem -- and the ball slides
+    down the slope without rolling (tangential acceleration g sin(tilt), no spin), while condim 3 rolls."""
+    m1, m3 = _ball_on_slope(1), _ball_on_slope(3)
+    q, v = m1.qpos0.copy(), np.zeros(m1.nv)
+    F1 = O.forward(m1, q, v, np.zeros(1))
+    E = F1["efc"]
+    assert E["nefc"] == 4 and np.allclose(E["J"], E["J"][0]) and np.allclose(E["D"], E["D"][0])
+    E1 = dict(E, J=E["J"][:1], D=4.0 * E["D"][:1], aref=E["aref"][:1], nefc=1)
+    a1, _, _, _ = O.newton(m1, F1["M"], E1, F1["qfrc_smooth"], None, None)
+    np.testing.assert_allclose(F1["qacc"], a1, rtol=1e-9, atol=1e-12)
+    tilt, g = 0.3, 9.81
+    assert abs(F1["qacc"][1] - g * np.sin(tilt)) < 1e-6 and np.abs(F1["qacc"][3:6]).max() < 1e-9
+    F3 = O.forward(m3, q, v, np.zeros(1))
+    assert F3["qacc"][1] < 0.8 * g * np.sin(tilt) and np.abs(F3["qacc"][3:6]).max() > 1.0  # rolls
