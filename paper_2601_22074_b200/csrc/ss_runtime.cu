@@ -161,10 +161,10 @@ extern "C" int ss_rt_release(ss_rt_state* st) {
 //   in stream : H2D actions(i) -> event in_done[k]
 //   main      : wait in_done[k]; step kernel(i); wait out_done[k] (slot k's previous D2H);
 //               snapshot kernel arena -> stage[k] (SM copy, not a copy engine); event snap[k]
-//   out stream: wait snap[k]; D2H stage[k] -> host[k]; event out_done[k]
-// S slots (k = i mod S, S <= 4; three let the host enqueue step i+1 while steps i-1 and i are still in
-// flight, which hides the host's per-step cost). The step kernel reads device actions, so no mapped
-// PCIe reads compete with the bulk D2H writes.
+//   out stream: wait snap[k]; D2H stage[k] -> host[i mod nhost]; event out_done[k]
+// S slots (k = i mod S, 2 <= S <= 8; several in flight let the host enqueue the next steps while earlier
+// ones run, which hides the host's per-step cost; consecutive steps' copies are grouped, ss_pipe_post).
+// The step kernel reads device actions, so no mapped PCIe reads compete with the bulk D2H writes.
 
 namespace {
 
