@@ -1,0 +1,54 @@
+"""Host-side task configuration of the 3-D path (no GPU): tracked bodies, contact-sensor tables, feet."""
+import numpy as np
+import pytest
+
+from paper_2601_22074_b200.sim3d import robots
+from paper_2601_22074_b200.sim3d.task import (BEYONDMIMIC_BODIES, LiftTaskCfg, MotionTrackingCfg, VelocityTaskCfg,
+                                              padded, pair_sensor_bits, robot_geoms)
+
+
+def _motion_cfg(m, **kw):
+    dq = robots.default_qpos(m, robots.G1_DEFAULT_JOINTS)
+    return MotionTrackingCfg(default_qpos=dq, motion_qpos=np.tile(dq, (2, 1)), motion_qvel=np.zeros((2, m.nv)),
+                             motion_dt=0.02, **kw)
+
+
+def test_tracked_bodies_defaults_and_overrides():
+    m = robots.g1_like()
+    anchor, bodies = _motion_cfg(m).tracked(m)
+    assert m.body_names[anchor] == "torso_link" and [m.body_names[b] for b in bodies] == list(BEYONDMIMIC_BODIES)
+    anchor, bodies = _motion_cfg(m, anchor_body="pelvis", track_bodies=("left_knee_link", 5)).tracked(m)
+    assert anchor == 1 and bodies == (m.body_names.index("left_knee_link"), 5)
+    with pytest.raises(ValueError):
+        _motion_cfg(m, track_bodies=tuple(range(1, 20))).tracked(m)  # more than S3_MAX_TRACK
+    go1 = robots.go1_like()  # no BeyondMimic names: every body of the robot's tree about its root
+    anchor, bodies = _motion_cfg(go1).tracked(go1)
+    assert anchor == 1 and bodies == tuple(range(1, go1.nbody))
+
+
+def test_contact_sensor_tables():
+    m = robots.g1_like()
+    sens = _motion_cfg(m).sensors(m)
+    assert sens[0][0] == "self_collision" and set(sens[0][1]) == set(robot_geoms(m))
+    bits = pair_sensor_bits(m, sens)
+    assert [bool(b & 1) for b in bits] == [g1 != 0 for g1, _ in m.pair_geom]  # robot-robot pairs only
+    # a sensor against any geom (None) and a second bit
+    any_bits = pair_sensor_bits(m, (("feet_any", (4, 5), None), ("torso_ground", (14,), (0,))))
+    for p, (g1, g2) in enumerate(m.pair_geom):
+        assert bool(any_bits[p] & 1) == (g1 in (4, 5) or g2 in (4, 5))
+        assert bool(any_bits[p] & 2) == ({g1, g2} == {0, 14})
+    assert _motion_cfg(m, self_collision=False).sensors(m) == ()
+
+
+def test_velocity_feet_and_lift_sensors():
+    g1, go1 = robots.g1_like(), robots.go1_like()
+    cfg = VelocityTaskCfg(default_qpos=g1.qpos0.copy())
+    assert [g1.body_names[b] for b in cfg.foot_bodies(g1)] == ["left_ankle_roll_link", "right_ankle_roll_link"]
+    assert [s[0] for s in cfg.sensors(g1)] == ["left_ankle_roll_link_ground", "right_ankle_roll_link_ground"]
+    assert len(VelocityTaskCfg(default_qpos=go1.qpos0.copy()).foot_bodies(go1)) == 4
+    arm = robots.arm_cube_like()
+    lift = LiftTaskCfg.for_model(arm, robots.default_qpos(arm, robots.ARM_DEFAULT_JOINTS))
+    assert [s[0] for s in lift.sensors(arm)] == ["ee_cube", "ee_ground", "cube_ground"]
+    assert padded((1.0, 2.0), 4) == (1.0, 2.0, 0.0, 0.0)
+    with pytest.raises(ValueError):
+        padded((1.0,) * 11, 10)
