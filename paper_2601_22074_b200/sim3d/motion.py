@@ -58,3 +58,48 @@ def synthetic_walk_clip(m: Model, default_qpos: np.ndarray, seconds: float = 10.
         else:
             V[:, d] = np.gradient(Q[:, a], dt)
     return Q, V, dt
+
+
+def _qconj_rotate(q, v):
+    """R(q)^T v for a unit quaternion q = (w, x, y, z) (world -> body frame)."""
+    w, x, y, z = q
+    R = np.array([[1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y)],
+                  [2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)],
+                  [2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)]])
+    return R.T @ v
+
+
+def load_motion_npz(path, m: Model, joint_names=None):
+    """A BeyondMimic / mjlab motion file (``.npz``: ``fps``, ``joint_pos`` / ``joint_vel`` (F, J) in the
+    robot's hinge-joint order or ``joint_names`` order, ``body_pos_w`` / ``body_quat_w`` (w, x, y, z) /
+    ``body_lin_vel_w`` / ``body_ang_vel_w`` (F, B, .) with the root body first) -> the task's clip
+    ``(qpos (F, nq), qvel (F, nv), frame_dt)``: the free joint from the root body's pose and velocity (its
+    angular velocity rotated into the body frame, MuJoCo's free-joint convention), the hinges from the
+    joint arrays. The clip's body states for the relative body terms are then rebuilt on the device from
+    this qpos / qvel (``s3_motion_bodies``), so every tracked body follows the model's own kinematics."""
+    data = np.load(path)
+    fps = float(np.asarray(data["fps"]).reshape(-1)[0])
+    jp, jv = np.asarray(data["joint_pos"], dtype=np.float64), np.asarray(data["joint_vel"], dtype=np.float64)
+    F = jp.shape[0]
+    hinges = [j for j in range(m.njnt) if m.jnt_type[j] != JNT_FREE]
+    if joint_names is not None:
+        order = [list(joint_names).index(m.jnt_names[j]) for j in hinges]
+    else:
+        if jp.shape[1] != len(hinges):
+            raise ValueError(f"joint_pos has {jp.shape[1]} joints, the model {len(hinges)} hinges")
+        order = list(range(len(hinges)))
+    Q = np.tile(m.qpos0, (F, 1))
+    V = np.zeros((F, m.nv))
+    for col, j in zip(order, hinges):
+        Q[:, m.jnt_qposadr[j]] = jp[:, col]
+        V[:, m.jnt_dofadr[j]] = jv[:, col]
+    free = [j for j in range(m.njnt) if m.jnt_type[j] == JNT_FREE]
+    if free:
+        a, d = m.jnt_qposadr[free[0]], m.jnt_dofadr[free[0]]
+        pos, quat = np.asarray(data["body_pos_w"])[:, 0], np.asarray(data["body_quat_w"])[:, 0]
+        quat = quat / np.linalg.norm(quat, axis=1, keepdims=True)
+        Q[:, a:a + 3], Q[:, a + 3:a + 7] = pos, quat
+        V[:, d:d + 3] = np.asarray(data["body_lin_vel_w"])[:, 0]
+        ang = np.asarray(data["body_ang_vel_w"])[:, 0]
+        V[:, d + 3:d + 6] = np.array([_qconj_rotate(quat[f], ang[f]) for f in range(F)])
+    return Q, V, 1.0 / fps

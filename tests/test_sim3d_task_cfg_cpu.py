@@ -52,3 +52,27 @@ def test_velocity_feet_and_lift_sensors():
     assert padded((1.0, 2.0), 4) == (1.0, 2.0, 0.0, 0.0)
     with pytest.raises(ValueError):
         padded((1.0,) * 11, 10)
+
+
+def test_beyondmimic_motion_file_round_trip(tmp_path):
+    """A clip written in the BeyondMimic / mjlab .npz layout (root body pose and world velocities, joint
+    arrays, fps) loads back to the same qpos / qvel (free joint in MuJoCo's convention: angular velocity in
+    the body frame), with the file's joints in a permuted, named order."""
+    from oracle import sim3d as O
+    from paper_2601_22074_b200.sim3d.motion import load_motion_npz, synthetic_walk_clip
+
+    m = robots.g1_like()
+    Q, V, dt = synthetic_walk_clip(m, robots.default_qpos(m, robots.G1_DEFAULT_JOINTS), seconds=0.5)
+    hinges = [j for j in range(m.njnt) if m.jnt_type[j] != 0]
+    perm = np.random.default_rng(0).permutation(len(hinges))
+    names = [m.jnt_names[hinges[k]] for k in perm]
+    jp = np.stack([Q[:, m.jnt_qposadr[hinges[k]]] for k in perm], 1)
+    jv = np.stack([V[:, m.jnt_dofadr[hinges[k]]] for k in perm], 1)
+    root_w = np.stack([O.qmat(Q[f, 3:7]) @ V[f, 3:6] for f in range(Q.shape[0])])  # body-frame -> world
+    path = tmp_path / "clip.npz"
+    np.savez(path, fps=np.array([1.0 / dt]), joint_pos=jp, joint_vel=jv, body_pos_w=Q[:, None, 0:3],
+             body_quat_w=Q[:, None, 3:7], body_lin_vel_w=V[:, None, 0:3], body_ang_vel_w=root_w[:, None])
+    Q2, V2, dt2 = load_motion_npz(path, m, joint_names=names)
+    np.testing.assert_allclose(Q2, Q, atol=1e-12)
+    np.testing.assert_allclose(V2, V, atol=1e-12)
+    assert abs(dt2 - dt) < 1e-15
