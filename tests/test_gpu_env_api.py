@@ -830,8 +830,9 @@ def test_step_async_delivers_each_steps_results_to_host():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("n,group", [(256, 2), (300, 2), (256, 4), (256, 1)])
-def test_step_async_paired_and_sequential_waits(monkeypatch, n, group):
+@pytest.mark.parametrize("n,group,slots", [(256, 2, 6), (300, 2, 6), (256, 4, 6), (256, 1, 6), (256, 2, 2),
+                                           (256, 2, 3)])
+def test_step_async_paired_and_sequential_waits(monkeypatch, n, group, slots):
     """The grouped D2H (ss_pipe_post: the copies of `group` consecutive steps deferred and issued as one)
     under every wait pattern: strictly sequential (each deferred copy issued alone by step_wait), 2 to 6
     in flight (whole and partial groups); 300 worlds give an arena that is not a multiple of 16 bytes (no
@@ -842,12 +843,13 @@ def test_step_async_paired_and_sequential_waits(monkeypatch, n, group):
 
     monkeypatch.setenv("SS_PIPE_GROUP", str(group))
     monkeypatch.setattr(envmod, "PIPE_GROUP", group)
+    monkeypatch.setattr(envmod, "PIPE_SLOTS", slots)
     a = ManagerBasedRlEnv(make_env_cfg("Velocity-Rough", num_envs=n, seed=3))
     b = ManagerBasedRlEnv(make_env_cfg("Velocity-Rough", num_envs=n, seed=3))
     a.reset()
     b.reset()
     rng = np.random.default_rng(11)
-    pattern = [1, 1, 1, 2, 2, 3, 1, 3, 2, 4, 5, 6, 4]  # steps submitted before waiting for all of them
+    pattern = [k for k in (1, 1, 1, 2, 2, 3, 1, 3, 2, 4, 5, 6, 4) if k <= slots]  # steps in flight per round
     acts = [torch.from_numpy(rng.uniform(-1, 1, size=(n, a.action_manager.total_dim))).pin_memory()
             for _ in range(sum(pattern))]
     want = []
