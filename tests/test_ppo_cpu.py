@@ -1,6 +1,7 @@
-"""Learner-side algebra on CPU (no oracle exists for PPO -- parity unpinned):
-the flat-bucket all-reduce across 2 gloo ranks equals the gradient of the
-concatenated batch on one process, and GAE matches a scalar recurrence."""
+"""Learner-side algebra on CPU (the reference has no learner -- parity unpinned): the flat-bucket
+all-reduce across 2 gloo ranks equals the gradient of the concatenated batch on one process, GAE matches a
+scalar recurrence, advantage normalization uses the job's statistics, and the PPO objective matches a
+float64 numpy restatement of the clipped surrogate."""
 
 import os
 import socket
@@ -108,3 +109,31 @@ def test_advantage_normalization_uses_job_statistics(tmp_path):
     full = torch.randn(32, 6, generator=torch.Generator().manual_seed(5))
     got = torch.cat([torch.load(tmp_path / "n0.pt"), torch.load(tmp_path / "n1.pt")])
     assert torch.allclose(got, normalize_advantages(full), atol=1e-6)
+
+
+def test_ppo_loss_matches_a_numpy_restatement():
+    """The clipped-surrogate objective (Schulman et al. 2017): -mean(min(r A, clip(r, 1-e, 1+e) A)) +
+    c_v mean((R - V)^2) - c_e mean(entropy), with a diagonal Gaussian policy -- restated in float64 numpy
+    from the network's own mean / log-std / value outputs, including ratios outside the clip range."""
+    import math
+
+    import numpy as np
+
+    from paper_2601_22074_b200.ppo import ppo_loss
+
+    model, cfg = _model()
+    obs_p, obs_c, act, old_logp, adv, ret = _data(7, 64)
+    old_logp = old_logp * 2.0  # ratios far from 1: both clip branches taken
+    loss = float(ppo_loss(model, cfg, obs_p, obs_c, act, old_logp, adv, ret))
+    with torch.no_grad():
+        mu = model.actor(obs_p).double().numpy()
+        ls = model.log_std.double().numpy()
+        v = model.critic(obs_c).squeeze(-1).double().numpy()
+    a, A, R, lp0 = (x.double().numpy() for x in (act, adv, ret, old_logp))
+    logp = np.sum(-((a - mu) ** 2) / (2.0 * np.exp(2.0 * ls)) - ls - 0.5 * math.log(2.0 * math.pi), axis=1)
+    ratio = np.exp(logp - lp0)
+    assert (ratio > 1 + cfg.clip).any() and (ratio < 1 - cfg.clip).any()
+    surr = np.minimum(ratio * A, np.clip(ratio, 1 - cfg.clip, 1 + cfg.clip) * A)
+    ent = np.sum(0.5 + 0.5 * math.log(2.0 * math.pi) + ls) * np.ones(len(a))
+    want = -surr.mean() + cfg.value_coef * np.mean((R - v) ** 2) - cfg.entropy_coef * ent.mean()
+    assert abs(loss - want) < 1e-5 * max(1.0, abs(want))
