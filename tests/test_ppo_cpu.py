@@ -124,7 +124,7 @@ def test_ppo_loss_matches_a_numpy_restatement():
     model, cfg = _model()
     obs_p, obs_c, act, old_logp, adv, ret = _data(7, 64)
     old_logp = old_logp * 2.0  # ratios far from 1: both clip branches taken
-    loss = float(ppo_loss(model, cfg, obs_p, obs_c, act, old_logp, adv, ret))
+    loss = float(ppo_loss(model, cfg, obs_p, obs_c, act, old_logp, adv, ret).detach())
     with torch.no_grad():
         mu = model.actor(obs_p).double().numpy()
         ls = model.log_std.double().numpy()
