@@ -381,7 +381,8 @@ def sim3d_leg(args, flush, stream) -> dict:
 
     n = args.envs
     out = {"workload": f"G1-like 3-D humanoid velocity tracking on the 5x6 terrain-curriculum heightfield (levels, "
-                       f"height scan, friction randomisation, pushes), {n} worlds/GPU, decimation 4 (SURVEY 8 f4)",
+                       f"height scan, friction randomisation, pushes; mjlab's penalties incl. angular momentum, joint "
+                       f"limits, foot slip over per-foot contact sensors), {n} worlds/GPU, decimation 4 (SURVEY 8 f4)",
            "unit": UNIT}
     for dtype in ("f32", "f64"):
         m = robots.g1_like(rough="curriculum", seed=args.seed)
