@@ -46,9 +46,9 @@ from .terrain import generate_grid
 __all__ = ["EnvCfg", "SceneCfg", "InitStateCfg", "ManagerBasedRlEnv", "load_capture"]
 
 # steps that may be in flight between step_async and step_wait (ss_pipe, 2..8; SS_PIPE_SLOTS overrides for A/B):
-# six keep the paired D2H copies (ss_pipe_post) fed -- 31.8 us per step at 4096 worlds vs 33.9 with four
-# unpaired slots, 41.8 with four paired (tools/e2e_ab.py)
-PIPE_SLOTS = int(os.environ.get("SS_PIPE_SLOTS", "6"))
+# eight keep the paired D2H copies (ss_pipe_post) fed with slack for host jitter -- 31.5-31.9 us per step at
+# 4096 worlds vs 32.0-33.0 with six, 33.9 with four unpaired slots, 41.8 with four paired (tools/e2e_ab.py)
+PIPE_SLOTS = int(os.environ.get("SS_PIPE_SLOTS", "8"))
 # steps whose results cross PCIe as one copy (ss_pipe_post; read by the native pipe from SS_PIPE_GROUP too)
 PIPE_GROUP = int(os.environ.get("SS_PIPE_GROUP", "2"))
 NF_LAG = 4  # control steps the host may run ahead before it must look at nonfinite flags
