@@ -1,3 +1,5 @@
+"""Back-to-back D2H copies of one output arena (1.58 MB) on a side stream: plain, with an event per copy,
+with host syncs lagging 3 / 8 copies, with a cross-stream wait -- all ~31.3 us per copy (the pipe's floor)."""
 import time, torch
 nb = 1581056
 K = 300
