@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define S3_ABI_VERSION 20
+#define S3_ABI_VERSION 21
 #define S3_F64 0
 #define S3_F32 1
 
@@ -36,6 +36,7 @@ extern "C" {
 #define S3_MAX_TREE 4
 #define S3_MAX_TRACK 16 /* tracked bodies of the motion task (besides the anchor) */
 #define S3_MAX_SENSOR 4 /* contact sensors */
+#define S3_MAX_KERNEL 8 /* adaptive-sampling smoothing kernel length */
 #define S3_BODY_STATE 13 /* pos[3] quat[4] linvel[3] angvel[3] (world frame; linvel of the body origin) */
 
 #define S3_OK 0
@@ -269,6 +270,21 @@ typedef struct s3_task {
     const uint8_t* pair_sensor; /* (npair,) */
     void* sensor;               /* (N, nsensor) */
     const void* motion_body;    /* (nframes, 1 + ntrack, S3_BODY_STATE) */
+    /* motion kind, BeyondMimic's adaptive sampling of the start time (nbins = 0: uniform over the first
+     * motion_start_frac of the clip): each termination counts in the clip bin of its motion time
+     * (bin_fail_now, uint32 atomics); the last block of the launch folds the counts into an exponential
+     * average bin_failed = alpha now + (1 - alpha) bin_failed, adds uniform_ratio / nbins, smooths
+     * forward with the kernel weights (q_b = sum_i w_i p_min(b + i, nbins - 1)) and writes the cumulative
+     * sums bin_cum that the NEXT launch's resets sample a bin from (a uniform time inside it) */
+    int32_t nbins;
+    int32_t nkernel;
+    double adaptive_alpha;
+    double adaptive_uniform;
+    double adaptive_kernel[S3_MAX_KERNEL];
+    void* bin_failed;       /* (nbins,) */
+    void* bin_cum;          /* (nbins,) */
+    uint32_t* bin_fail_now; /* (nbins,) */
+    uint32_t* bin_ticket;   /* (1,) */
     int32_t cube_qposadr;
     int32_t tip_geom[2];
     int32_t pad2;

@@ -1398,6 +1398,43 @@ class MotionTaskOracle(TaskOracle):
         super().__init__(m, cfg, nworld, seed, world_offset)
         self.anchor, self.bodies = cfg.tracked(m)
         self.body_table = motion_body_table(m, cfg)
+        # adaptive start-time sampling (BeyondMimic): failure average, cumulative weights, this step's counts
+        self.nbins = cfg.n_bins()
+        self.bin_failed = np.zeros(self.nbins)
+        self.bin_cum = np.zeros(self.nbins)
+        self.bin_now = np.zeros(self.nbins, dtype=np.int64)
+        if self.nbins:
+            self.fold_bins()  # zero counts: the uniform initial weights
+
+    def fold_bins(self):
+        """failed <- alpha now + (1 - alpha) failed; cumulative sums of q_b = sum_i w_i (failed_min(b+i, nb-1)
+        + uniform / nb), w_i = lambda^i normalised (BeyondMimic's adaptive sampling, bins in order)."""
+        cfg, nb = self.cfg, self.nbins
+        a = cfg.adaptive_alpha
+        for b in range(nb):
+            self.bin_failed[b] = a * float(self.bin_now[b]) + (1.0 - a) * self.bin_failed[b]
+        self.bin_now[:] = 0
+        lam = cfg.adaptive_lambda ** np.arange(cfg.adaptive_kernel_size, dtype=np.float64)
+        w = lam / lam.sum()
+        u = cfg.adaptive_uniform_ratio / nb
+        acc = 0.0
+        for b in range(nb):
+            q = 0.0
+            for i in range(len(w)):
+                q += w[i] * (self.bin_failed[min(b + i, nb - 1)] + u)
+            acc += q
+            self.bin_cum[b] = acc
+
+    def start_time(self, kr, ctr):
+        """Start time of a reset: a bin by the cumulative weights of the last fold and a uniform time inside
+        it (adaptive), or uniform over the first motion_start_frac of the clip."""
+        if not self.nbins:
+            return self.cfg.motion_start_frac * self.clip_end() * uniform(kr, ctr * 256 + 203)
+        target = uniform(kr, ctr * 256 + 203) * self.bin_cum[-1]
+        b = 0
+        while b < self.nbins - 1 and not target < self.bin_cum[b]:
+            b += 1
+        return (b + uniform(kr, ctr * 256 + 204)) / self.nbins * self.clip_end()
 
     def body_errors(self, w):
         """BeyondMimic's body errors (means over the tracked bodies): position and orientation with the
@@ -1429,7 +1466,7 @@ class MotionTaskOracle(TaskOracle):
     def reset_world(self, w, ctr):
         m, cfg = self.m, self.cfg
         kr = self.key(w, 1)
-        t0 = cfg.motion_start_frac * self.clip_end() * uniform(kr, ctr * 256 + 203)
+        t0 = self.start_time(kr, ctr)
         ax = cfg.spawn_half_extent * (2.0 * uniform(kr, ctr * 256 + 200) - 1.0)
         ay = cfg.spawn_half_extent * (2.0 * uniform(kr, ctr * 256 + 201) - 1.0)
         q, v = motion_ref(cfg, t0)
@@ -1513,11 +1550,16 @@ class MotionTaskOracle(TaskOracle):
             nonfinite = not (np.all(np.isfinite(q)) and np.all(np.isfinite(v)))
             term[w] = bool(abs(pe[2]) > cfg.max_height_error or float(np.sqrt(re @ re)) > cfg.max_ori_error
                            or nonfinite)
+            if term[w] and self.nbins:  # a failure in the bin of its motion time
+                b = int(np.floor(self.cmd[w, 0] / self.clip_end() * self.nbins))
+                self.bin_now[min(max(b, 0), self.nbins - 1)] += 1
             self.episode_step[w] += 1
             trunc[w] = bool(self.episode_step[w] >= cfg.episode_steps or self.cmd[w, 0] >= self.clip_end() - 1e-9)
         for w in range(self.n):
             if term[w] or trunc[w]:
-                self.reset_world(w, ctr)
+                self.reset_world(w, ctr)  # with the weights of the previous fold
+        if self.nbins:  # the launch's fold, after every world (the kernel's last-world ticket)
+            self.fold_bins()
         return self.observe(ctr), rew, term, trunc
 
 

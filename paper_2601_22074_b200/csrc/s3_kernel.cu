@@ -2280,7 +2280,16 @@ __device__ __noinline__ void motion_reset(const s3_model& m, const s3_task& tk, 
     WS<T> s = make_ws(B_, L_);
     uint64_t kr = stream_key(tk.seed, tk.world_offset + w, 1);
     const T clip_end = T(tk.nframes - 1) * T(tk.frame_dt);
-    T t0 = T(tk.motion_start_frac) * clip_end * uniform01<T>(kr, ctr * 256 + 203);
+    T t0;
+    if (tk.nbins > 0) {  // adaptive sampling: a bin by the cumulative weights of the last fold, a time inside it
+        const T* cum = static_cast<const T*>(tk.bin_cum);
+        const T target = uniform01<T>(kr, ctr * 256 + 203) * cum[tk.nbins - 1];
+        int b = 0;
+        while (b < tk.nbins - 1 && !(target < cum[b])) ++b;
+        t0 = (T(b) + uniform01<T>(kr, ctr * 256 + 204)) / T(tk.nbins) * clip_end;
+    } else {
+        t0 = T(tk.motion_start_frac) * clip_end * uniform01<T>(kr, ctr * 256 + 203);
+    }
     T ax = T(tk.spawn_half_extent) * (T(2) * uniform01<T>(kr, ctr * 256 + 200) - T(1));
     T ay = T(tk.spawn_half_extent) * (T(2) * uniform01<T>(kr, ctr * 256 + 201) - T(1));
     motion_ref(m, tk, t0, s.qpos, s.qvel, lane);
@@ -2380,6 +2389,11 @@ __device__ __noinline__ void motion_post(const s3_model& m, const s3_task& tk, c
     bool term = fabs(pe[2]) > T(tk.max_height_error) || rot > T(tk.max_ori_error) || !finite;
     int es = tk.episode_step[w] + 1;
     const T clip_end = T(tk.nframes - 1) * T(tk.frame_dt);
+    if (tk.nbins > 0 && term && lane == 0) {  // adaptive sampling: a failure in the bin of its motion time
+        int b = (int)floor(tnow / clip_end * T(tk.nbins));
+        b = b < 0 ? 0 : (b > tk.nbins - 1 ? tk.nbins - 1 : b);
+        atomicAdd(tk.bin_fail_now + b, 1u);
+    }
     bool trunc = es >= tk.episode_steps || tnow >= clip_end - T(1e-9);
     __syncwarp();
     if (lane == 0) {
@@ -2587,6 +2601,40 @@ __device__ __noinline__ void velocity_extra_terms(const s3_model& m, const s3_da
     out[2] = slip;
 }
 
+// Adaptive sampling (s3_task.nbins): the last world of the launch to finish (a per-warp ticket, so no block
+// barrier) folds the launch's failure counts into the exponential average and rebuilds the cumulative
+// sampling weights for the next launch -- one thread, bins in order (oracle MotionTaskOracle.fold_bins)
+template <class T> __device__ __noinline__ void adaptive_fold(const s3_task& tk, int64_t nworld, int lane) {
+    __syncwarp();
+    unsigned last = 0;
+    if (lane == 0) {
+        __threadfence();  // this world's failure count before its ticket
+        last = atomicInc(tk.bin_ticket, (unsigned)(nworld - 1)) == (unsigned)(nworld - 1);
+    }
+    last = __shfl_sync(FULL, last, 0);
+    if (!last || lane != 0) return;
+    __threadfence();
+    T* F = static_cast<T*>(tk.bin_failed);
+    T* C = static_cast<T*>(tk.bin_cum);
+    const int nb = tk.nbins;
+    const T a = T(tk.adaptive_alpha);
+    for (int b = 0; b < nb; ++b) {
+        const T now = T(atomicExch(tk.bin_fail_now + b, 0u));
+        F[b] = a * now + (T(1) - a) * F[b];
+    }
+    const T u = T(tk.adaptive_uniform) / T(nb);
+    T acc = T(0);
+    for (int b = 0; b < nb; ++b) {
+        T q = T(0);
+        for (int i = 0; i < tk.nkernel; ++i) {
+            const int j = b + i < nb - 1 ? b + i : nb - 1;
+            q += T(tk.adaptive_kernel[i]) * (F[j] + u);
+        }
+        acc += q;
+        C[b] = acc;
+    }
+}
+
 template <class T>
 __global__ void __launch_bounds__(32 * 16) env_kernel(const __grid_constant__ s3_model m, const __grid_constant__ s3_data d,
                                                      const __grid_constant__ s3_layout l,
@@ -2674,6 +2722,7 @@ __global__ void __launch_bounds__(32 * 16) env_kernel(const __grid_constant__ s3
     if (tk.nsensor && lane < tk.nsensor) static_cast<T*>(tk.sensor)[w * tk.nsensor + lane] = T((found >> (8 * lane)) & 255u);
     if (tk.kind == 1) {
         motion_post(m, tk, L_, B_, w, ctr, cmd, act, rate, gq, gv, gw, prev, found, lane);
+        if (tk.nbins > 0) adaptive_fold<T>(tk, d.nworld, lane);
         return;
     }
     if (tk.kind == 2) {
@@ -3230,6 +3279,9 @@ int s3_env_step(const s3_model* m, const s3_data* d, const s3_layout* l, const s
         return fail(S3_ERR_ARG, "tracked bodies need the s3_motion_bodies table");
     if (t->nsensor < 0 || t->nsensor > S3_MAX_SENSOR || (t->nsensor && (!t->pair_sensor || !t->sensor)))
         return fail(S3_ERR_ARG, "contact sensors need pair_sensor and sensor");
+    if (t->kind == 1 && t->nbins && (t->nbins < 0 || t->nkernel < 1 || t->nkernel > S3_MAX_KERNEL || !t->bin_failed ||
+                                     !t->bin_cum || !t->bin_fail_now || !t->bin_ticket))
+        return fail(S3_ERR_ARG, "adaptive sampling needs its bin buffers and 1..S3_MAX_KERNEL kernel weights");
     if ((t->cost == nullptr) != (t->order == nullptr)) return fail(S3_ERR_ARG, "cost and order go together");
     if ((m->flags & 6) && l->off[O_CDOF] - l->off[O_CRB] < m->nv)
         return fail(S3_ERR_ARG, "layout planned without the level-schedule scratch (flags bits 1-2): re-plan");

@@ -59,6 +59,24 @@ def pair_sensor_bits(m: Model, sensors) -> np.ndarray:
     return bits
 
 
+def fold_bins(failed: np.ndarray, now: np.ndarray, cfg) -> tuple:
+    """Adaptive sampling's fold (s3_kernel.cu adaptive_fold, in the same order): failed <- alpha now +
+    (1 - alpha) failed; cumulative sums of q_b = sum_i w_i (failed_min(b + i, nb - 1) + uniform / nb)."""
+    nb = len(failed)
+    a = cfg.adaptive_alpha
+    failed = np.array([a * float(now[b]) + (1.0 - a) * failed[b] for b in range(nb)])
+    u = cfg.adaptive_uniform_ratio / nb
+    w = cfg.kernel_weights()
+    cum, acc = np.zeros(nb), 0.0
+    for b in range(nb):
+        q = 0.0
+        for i in range(len(w)):
+            q += w[i] * (failed[min(b + i, nb - 1)] + u)
+        acc += q
+        cum[b] = acc
+    return failed, cum
+
+
 def padded(v, n: int) -> tuple:
     """A reward-weight / sigma tuple padded with zeros to the struct's length."""
     v = tuple(v)
@@ -170,6 +188,27 @@ class MotionTrackingCfg:
     track_bodies: tuple | None = None         # None: BEYONDMIMIC_BODIES present in the model, else tree 0
     self_collision: bool = True               # contact sensor 0 = robot-robot contacts, costed by term 9
     contact_sensors: tuple = ()               # extra sensors after the self-collision one
+    # BeyondMimic's adaptive sampling of the start time over clip bins (failures of the previous launches,
+    # exponentially averaged, plus a uniform share, smoothed forward with lambda^i weights); False: uniform
+    # over the first motion_start_frac of the clip
+    adaptive_sampling: bool = True
+    bin_seconds: float = 1.0
+    adaptive_kernel_size: int = 3
+    adaptive_lambda: float = 0.8
+    adaptive_uniform_ratio: float = 0.1
+    adaptive_alpha: float = 0.001
+
+    def n_bins(self) -> int:
+        clip = (self.motion_qpos.shape[0] - 1) * self.motion_dt
+        return int(clip / self.bin_seconds) + 1 if self.adaptive_sampling else 0
+
+    def kernel_weights(self) -> np.ndarray:
+        w = self.adaptive_lambda ** np.arange(self.adaptive_kernel_size, dtype=np.float64)
+        return w / w.sum()
+
+    def initial_bin_cum(self) -> np.ndarray:
+        """Cumulative sampling weights before any failure (the fold of zero counts): uniform."""
+        return fold_bins(np.zeros(self.n_bins()), np.zeros(self.n_bins()), self)[1]
     max_height_error: float = 0.25
     max_ori_error: float = 0.8
     spawn_half_extent: float = 0.5
@@ -318,6 +357,19 @@ class VelocityEnv3D:
             t.motion_sigmas[:] = padded(cfg.motion_sigmas, len(t.motion_sigmas))
             if not cfg.self_collision:  # term 9 costs sensor 0, the self-collision sensor when there is one
                 t.reward_weights[9] = 0.0
+            nb = cfg.n_bins()
+            if nb:
+                if not 1 <= cfg.adaptive_kernel_size <= N.S3_MAX_KERNEL:
+                    raise ValueError(f"adaptive_kernel_size in 1..{N.S3_MAX_KERNEL}")
+                t.nbins, t.nkernel = nb, cfg.adaptive_kernel_size
+                t.adaptive_alpha, t.adaptive_uniform = cfg.adaptive_alpha, cfg.adaptive_uniform_ratio
+                t.adaptive_kernel[:cfg.adaptive_kernel_size] = tuple(cfg.kernel_weights())
+                self.bin_failed = z(nb)
+                self.bin_cum = torch.as_tensor(cfg.initial_bin_cum(), dtype=dt, device=dev)
+                self._bin_now = torch.zeros(nb, dtype=torch.int32, device=dev)
+                self._bin_ticket = torch.zeros(1, dtype=torch.int32, device=dev)
+                t.bin_failed, t.bin_cum = self.bin_failed.data_ptr(), self.bin_cum.data_ptr()
+                t.bin_fail_now, t.bin_ticket = self._bin_now.data_ptr(), self._bin_ticket.data_ptr()
             anchor, bodies = cfg.tracked(model)
             t.anchor_body, t.ntrack = anchor, len(bodies)
             t.track_body[:len(bodies)] = bodies

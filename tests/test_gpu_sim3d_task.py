@@ -357,7 +357,7 @@ def test_motion_imitation_teacher_forced_terminations_and_clip_end():
     import torch
 
     n = 8
-    env, ref = _motion_pair(n, max_height_error=0.02, motion_start_frac=1.0)
+    env, ref = _motion_pair(n, max_height_error=0.02, motion_start_frac=1.0, adaptive_alpha=0.3)
     env.reset()
     ref.reset()
     ref.cmd[:4, 0] = ref.clip_end() - 0.01  # four worlds run off the end of the clip in one step
@@ -374,9 +374,12 @@ def test_motion_imitation_teacher_forced_terminations_and_clip_end():
         np.testing.assert_allclose(r.cpu().numpy(), r_ref, rtol=1e-8, atol=1e-10)
         np.testing.assert_allclose(o.cpu().numpy(), o_ref, rtol=1e-7, atol=1e-7)
         np.testing.assert_allclose(env.command.cpu().numpy(), ref.cmd, atol=1e-12)
+        # adaptive start-time sampling: the failure average and the cumulative weights of the fold
+        np.testing.assert_allclose(env.bin_failed.cpu().numpy(), ref.bin_failed, rtol=1e-14, atol=0)
+        np.testing.assert_allclose(env.bin_cum.cpu().numpy(), ref.bin_cum, rtol=1e-14, atol=0)
         saw_term += int(te_ref.sum())
         saw_trunc += int(tr_ref.sum())
-    assert saw_term > 0 and saw_trunc > 0
+    assert saw_term > 0 and saw_trunc > 0 and ref.bin_failed.max() > 0
 
 
 def _lift_pair(n, dtype="f64", **over):

@@ -76,3 +76,36 @@ def test_beyondmimic_motion_file_round_trip(tmp_path):
     np.testing.assert_allclose(Q2, Q, atol=1e-12)
     np.testing.assert_allclose(V2, V, atol=1e-12)
     assert abs(dt2 - dt) < 1e-15
+
+
+def test_adaptive_sampling_weights_follow_failures():
+    """BeyondMimic's adaptive sampling: uniform weights before any failure; failures in a bin raise that bin
+    and (through the forward kernel) the bins just before it; the host fold (task.fold_bins) and the oracle's
+    agree bit for bit; start times land inside the drawn bin."""
+    from oracle import sim3d as O
+    from paper_2601_22074_b200.sim3d.task import fold_bins
+
+    m = robots.g1_like()
+    dq = robots.default_qpos(m, robots.G1_DEFAULT_JOINTS)
+    from paper_2601_22074_b200.sim3d.motion import synthetic_walk_clip
+
+    Q, V, dt = synthetic_walk_clip(m, dq, seconds=6.0)
+    cfg = MotionTrackingCfg(default_qpos=dq, motion_qpos=Q, motion_qvel=V, motion_dt=dt, adaptive_alpha=0.5)
+    nb = cfg.n_bins()
+    assert nb == 7
+    cum0 = cfg.initial_bin_cum()
+    np.testing.assert_allclose(np.diff(np.concatenate([[0.0], cum0])), cum0[0], rtol=1e-12)  # uniform
+    ref = O.MotionTaskOracle(m, cfg, 1)
+    np.testing.assert_array_equal(ref.bin_cum, cum0)
+    now = np.zeros(nb)
+    now[4] = 10
+    ref.bin_now[:] = now.astype(np.int64)
+    ref.fold_bins()
+    failed, cum = fold_bins(np.zeros(nb), now, cfg)
+    np.testing.assert_array_equal(ref.bin_cum, cum)
+    q = np.diff(np.concatenate([[0.0], cum]))
+    assert q.argmax() == 4 and q[3] > q[2] > q[1] and q[5] < q[4]  # the failing bin and the lead-up to it
+    ref.cmd[:] = 0.0
+    for ctr in range(1, 50):
+        t0 = ref.start_time(ref.key(0, 1), ctr)
+        assert 0.0 <= t0 <= ref.clip_end()
