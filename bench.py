@@ -410,8 +410,9 @@ def sim3d_leg(args, flush, stream) -> dict:
 
     nm = 2 * n
     out["motion"] = {"workload": f"G1-like 3-D motion imitation (BeyondMimic-style reference-motion command, synthetic "
-                                 f"10 s walking clip, RSI, relative body pose / velocity rewards over 14 tracked "
-                                 f"bodies, self-collision sensor), flat, {nm} worlds/GPU, decimation 4"}
+                                 f"10 s walking clip, RSI with adaptive start-time sampling, relative body pose / "
+                                 f"velocity rewards over 14 tracked bodies, self-collision sensor), flat, {nm} "
+                                 f"worlds/GPU, decimation 4"}
     for dtype in ("f32", "f64"):
         m = robots.g1_like(seed=args.seed)
         dq = robots.default_qpos(m, robots.G1_DEFAULT_JOINTS)
