@@ -1035,6 +1035,18 @@ class TaskOracle:
             self.reset_world(w, 0)
         return self.observe(0)
 
+    def interval_push(self, w, ctr):
+        """EventManager.apply_interval: U(-v, v) on the base's planar velocity when the timer runs out."""
+        if not self._events_on():
+            return
+        cfg = self.cfg
+        self.ev_timer[w] -= self.m.opt.timestep * cfg.decimation
+        if self.ev_timer[w] <= 0.0:
+            k5, pv = self.key(w, 5), cfg.push_velocity
+            self.qvel[w, 0] += pv * (2.0 * uniform(k5, ctr * 8 + 2) - 1.0)
+            self.qvel[w, 1] += pv * (2.0 * uniform(k5, ctr * 8 + 3) - 1.0)
+            self.draw_push_timer(w, ctr, 4)
+
     def draw_push_timer(self, w, ctr, slot):
         lo, hi = self.cfg.push_interval
         self.ev_timer[w] = lo + (hi - lo) * uniform(self.key(w, 5), ctr * 8 + slot)
@@ -1152,13 +1164,7 @@ class TaskOracle:
                 self.cmd_timer[w] -= 1
                 if self.cmd_timer[w] <= 0:
                     self.resample(w, ctr)
-            if self._events_on():  # interval push (every world, after resets/commands)
-                self.ev_timer[w] -= dtc
-                if self.ev_timer[w] <= 0.0:
-                    k5, pv = self.key(w, 5), cfg.push_velocity
-                    self.qvel[w, 0] += pv * (2.0 * uniform(k5, ctr * 8 + 2) - 1.0)
-                    self.qvel[w, 1] += pv * (2.0 * uniform(k5, ctr * 8 + 3) - 1.0)
-                    self.draw_push_timer(w, ctr, 4)
+            self.interval_push(w, ctr)  # every world, after resets / commands
         return self.observe(ctr), rew, term, trunc
 
 
@@ -1483,6 +1489,8 @@ class MotionTaskOracle(TaskOracle):
         self.ep_return[w] = 0.0
         self.cmd[w] = (t0, ax, ay)
         self.cmd_timer[w] = 0
+        if self._events_on():
+            self.draw_push_timer(w, ctr, 1)
 
     def resample(self, w, ctr):
         pass
@@ -1530,7 +1538,7 @@ class MotionTaskOracle(TaskOracle):
             self.prev_action[w] = self.action[w]
             self.action[w] = a
             ctrl = self.act_default + cfg.action_scale * a
-            q, v, found = self._substeps(w, ctrl)
+            q, v, found = self._substeps(w, ctrl, self.fscale[w], self.mscale[w])
             self.cmd[w, 0] += dtc
             qr, vr, pe, re = self._errors(w)
             s = cfg.motion_sigmas
@@ -1558,6 +1566,7 @@ class MotionTaskOracle(TaskOracle):
         for w in range(self.n):
             if term[w] or trunc[w]:
                 self.reset_world(w, ctr)  # with the weights of the previous fold
+            self.interval_push(w, ctr)
         if self.nbins:  # the launch's fold, after every world (the kernel's last-world ticket)
             self.fold_bins()
         return self.observe(ctr), rew, term, trunc

@@ -2117,6 +2117,48 @@ __device__ __noinline__ void task_observe(const s3_model& m, const s3_task& tk, 
     }
 }
 
+// ---- domain-randomisation events (velocity and motion kinds; s3_task.events, purpose 5)
+
+// startup: per-world friction and base-mass scales, and the first push timer (reset-all launch, counter 0)
+template <class T> __device__ inline void events_startup(const s3_data& d, const s3_task& tk, int64_t w, int lane) {
+    if (!tk.events || lane != 0) return;
+    uint64_t k5 = stream_key(tk.seed, tk.world_offset + w, 5);
+    static_cast<T*>(d.friction_scale)[w] =
+        T(tk.friction_range[0]) + T(tk.friction_range[1] - tk.friction_range[0]) * uniform01<T>(k5, 0);
+    static_cast<T*>(d.mass_scale)[w] =
+        T(tk.base_mass_range[0]) + T(tk.base_mass_range[1] - tk.base_mass_range[0]) * uniform01<T>(k5, 5);
+    static_cast<T*>(tk.event_timer)[w] =
+        T(tk.push_interval[0]) + T(tk.push_interval[1] - tk.push_interval[0]) * uniform01<T>(k5, 1);
+}
+
+// masked reset: a fresh push timer (slot 1 of the step's counter)
+template <class T> __device__ inline void events_reset(const s3_task& tk, int64_t w, uint64_t ctr, int lane) {
+    if (!tk.events || lane != 0) return;
+    uint64_t k5 = stream_key(tk.seed, tk.world_offset + w, 5);
+    static_cast<T*>(tk.event_timer)[w] =
+        T(tk.push_interval[0]) + T(tk.push_interval[1] - tk.push_interval[0]) * uniform01<T>(k5, ctr * 8 + 1);
+}
+
+// interval push (EventManager.apply_interval): every world after resets -- U(-v, v) on the base's planar
+// velocity when its timer runs out, then a new timer
+template <class T>
+__device__ inline void events_interval(const s3_model& m, const s3_task& tk, T* qvel, int64_t w, uint64_t ctr, int lane) {
+    if (!tk.events) return;
+    T tmr = static_cast<T*>(tk.event_timer)[w] - T(m.timestep) * T(tk.decimation);
+    __syncwarp();
+    if (lane == 0) {
+        uint64_t k5 = stream_key(tk.seed, tk.world_offset + w, 5);
+        if (tmr <= T(0)) {
+            T pv = T(tk.push_velocity);
+            qvel[0] += pv * (T(2) * uniform01<T>(k5, ctr * 8 + 2) - T(1));
+            qvel[1] += pv * (T(2) * uniform01<T>(k5, ctr * 8 + 3) - T(1));
+            tmr = T(tk.push_interval[0]) + T(tk.push_interval[1] - tk.push_interval[0]) * uniform01<T>(k5, ctr * 8 + 4);
+        }
+        static_cast<T*>(tk.event_timer)[w] = tmr;
+    }
+    __syncwarp();
+}
+
 // ---- motion imitation (kind 1): reference-motion command, cmd = (motion time, anchor x, anchor y)
 
 // reference qpos -> qr[nq], qvel -> vr[nv] at motion time t (oracle motion_ref)
@@ -2405,6 +2447,7 @@ __device__ __noinline__ void motion_post(const s3_model& m, const s3_task& tk, c
     }
     if (term || trunc) {
         motion_reset(m, tk, L_, B_, w, ctr, cmd, lane);
+        events_reset<T>(tk, w, ctr, lane);
         for (int i = lane; i < nv; i += 32) gw[i] = T(0);
         for (int i = lane; i < nu; i += 32) { act[i] = T(0); prev[i] = T(0); }
         if (lane == 0) {
@@ -2413,6 +2456,7 @@ __device__ __noinline__ void motion_post(const s3_model& m, const s3_task& tk, c
         }
     }
     __syncwarp();
+    events_interval(m, tk, s.qvel, w, ctr, lane);  // pushes after resets, like the velocity kind
     motion_observe(m, tk, L_, B_, w, ctr, cmd, act, lane);
     for (int i = lane; i < nq; i += 32) gq[i] = s.qpos[i];
     for (int i = lane; i < nv; i += 32) gv[i] = s.qvel[i];
@@ -2673,16 +2717,8 @@ __global__ void __launch_bounds__(32 * 16) env_kernel(const __grid_constant__ s3
             __syncwarp();
             task_reset(m, tk, L_, B_, w, 0, lane);
             task_resample(tk, cmd, w, 0, lane);
-            if (tk.events && lane == 0) {  // startup friction randomisation + first push timer (purpose 5)
-                uint64_t k5 = stream_key(tk.seed, tk.world_offset + w, 5);
-                static_cast<T*>(d.friction_scale)[w] =
-                    T(tk.friction_range[0]) + T(tk.friction_range[1] - tk.friction_range[0]) * uniform01<T>(k5, 0);
-                static_cast<T*>(d.mass_scale)[w] =
-                    T(tk.base_mass_range[0]) + T(tk.base_mass_range[1] - tk.base_mass_range[0]) * uniform01<T>(k5, 5);
-                static_cast<T*>(tk.event_timer)[w] =
-                    T(tk.push_interval[0]) + T(tk.push_interval[1] - tk.push_interval[0]) * uniform01<T>(k5, 1);
-            }
         }
+        if (tk.kind != 2) events_startup<T>(d, tk, w, lane);  // friction / mass scales, first push timer
         for (int i = lane; i < nv; i += 32) gw[i] = T(0);
         for (int i = lane; i < nu; i += 32) { act[i] = T(0); prev[i] = T(0); }
         if (lane == 0) {
@@ -2777,11 +2813,7 @@ __global__ void __launch_bounds__(32 * 16) env_kernel(const __grid_constant__ s3
     __syncwarp();
     if (term || trunc) {  // masked reset (warp-uniform)
         task_reset(m, tk, L_, B_, w, ctr, lane);
-        if (tk.events && lane == 0) {
-            uint64_t k5 = stream_key(tk.seed, tk.world_offset + w, 5);
-            static_cast<T*>(tk.event_timer)[w] =
-                T(tk.push_interval[0]) + T(tk.push_interval[1] - tk.push_interval[0]) * uniform01<T>(k5, ctr * 8 + 1);
-        }
+        events_reset<T>(tk, w, ctr, lane);
         for (int i = lane; i < nv; i += 32) gw[i] = T(0);
         for (int i = lane; i < nu; i += 32) { act[i] = T(0); prev[i] = T(0); }
         task_resample(tk, cmd, w, ctr, lane);
@@ -2800,21 +2832,7 @@ __global__ void __launch_bounds__(32 * 16) env_kernel(const __grid_constant__ s3
         if (lane == 0) tk.cmd_timer[w] = tm;
     }
     __syncwarp();
-    if (tk.events) {  // interval push: every world, after resets and commands (EventManager.apply_interval)
-        T tmr = static_cast<T*>(tk.event_timer)[w] - T(m.timestep) * T(tk.decimation);
-        __syncwarp();
-        if (lane == 0) {
-            uint64_t k5 = stream_key(tk.seed, tk.world_offset + w, 5);
-            if (tmr <= T(0)) {
-                T pv = T(tk.push_velocity);
-                s.qvel[0] += pv * (T(2) * uniform01<T>(k5, ctr * 8 + 2) - T(1));
-                s.qvel[1] += pv * (T(2) * uniform01<T>(k5, ctr * 8 + 3) - T(1));
-                tmr = T(tk.push_interval[0]) + T(tk.push_interval[1] - tk.push_interval[0]) * uniform01<T>(k5, ctr * 8 + 4);
-            }
-            static_cast<T*>(tk.event_timer)[w] = tmr;
-        }
-        __syncwarp();
-    }
+    events_interval(m, tk, s.qvel, w, ctr, lane);  // after resets and commands (EventManager.apply_interval)
     task_observe(m, tk, L_, B_, w, ctr, cmd, act, lane);
     if (d.geom_xpos) store_geom_frames(m, d, L_, B_, w, lane);  // sensors see the post-reset state, like obs
     for (int i = lane; i < nq; i += 32) gq[i] = s.qpos[i];
@@ -3268,7 +3286,7 @@ int s3_env_step(const s3_model* m, const s3_data* d, const s3_layout* l, const s
     if (d->nworld == 0) return S3_OK;
     if (!d->qpos || !d->qvel || !d->qacc_warmstart) return fail(S3_ERR_ARG, "qpos/qvel/qacc_warmstart required");
     if (mode == 0 && !actions) return fail(S3_ERR_ARG, "actions required");
-    if (t->kind == 0 && t->events && (!d->friction_scale || !d->mass_scale || !t->event_timer))
+    if (t->kind != 2 && t->events && (!d->friction_scale || !d->mass_scale || !t->event_timer))
         return fail(S3_ERR_ARG, "events need friction_scale, mass_scale and event_timer");
     const int want = t->kind == 1 ? 15 + 5 * m->nu : (t->kind == 2 ? 13 + 3 * m->nu : 12 + 3 * m->nu + t->nscan);
     if (t->obs_dim != want || t->nscan > S3_MAX_RAYS || t->decimation < 1 ||

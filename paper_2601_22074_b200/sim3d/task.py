@@ -197,6 +197,11 @@ class MotionTrackingCfg:
     adaptive_lambda: float = 0.8
     adaptive_uniform_ratio: float = 0.1
     adaptive_alpha: float = 0.001
+    # domain randomisation, as the velocity task's (None: off): startup friction / base-mass scales, pushes
+    friction_range: tuple = (0.6, 1.2)
+    base_mass_range: tuple = (0.8, 1.2)
+    push_interval: tuple | None = None
+    push_velocity: float = 0.5
 
     def n_bins(self) -> int:
         clip = (self.motion_qpos.shape[0] - 1) * self.motion_dt
@@ -395,16 +400,6 @@ class VelocityEnv3D:
                 raise ValueError(f"at most {N.S3_MAX_SENSOR} feet")
             t.nfeet = len(feet)
             t.foot_body[:len(feet)] = feet
-            if cfg.push_interval is not None:
-                t.events = 1
-                self.data.friction_scale = torch.ones(n, dtype=dt, device=dev)
-                self.event_timer = z(n)
-                t.event_timer = self.event_timer.data_ptr()
-                t.friction_range[:] = cfg.friction_range
-                t.base_mass_range[:] = cfg.base_mass_range
-                self.data.mass_scale = torch.ones(n, dtype=dt, device=dev)
-                t.push_interval[:] = cfg.push_interval
-                t.push_velocity = cfg.push_velocity
             if cfg.curriculum is not None:
                 rows, cols, patch = cfg.curriculum
                 t.curriculum, t.terrain_rows, t.terrain_cols, t.patch_size = 1, rows, cols, patch
@@ -421,6 +416,16 @@ class VelocityEnv3D:
                 cfg.reset_joint_jitter
             for i, (lo, hi) in enumerate(cfg.command_ranges):
                 t.cmd_lo[i], t.cmd_hi[i] = lo, hi
+        if not lift and cfg.push_interval is not None:  # domain randomisation events (velocity, motion kinds)
+            t.events = 1
+            self.data.friction_scale = torch.ones(n, dtype=dt, device=dev)
+            self.event_timer = z(n)
+            t.event_timer = self.event_timer.data_ptr()
+            t.friction_range[:] = cfg.friction_range
+            t.base_mass_range[:] = cfg.base_mass_range
+            self.data.mass_scale = torch.ones(n, dtype=dt, device=dev)
+            t.push_interval[:] = cfg.push_interval
+            t.push_velocity = cfg.push_velocity
         pts = cfg.scan_points() if getattr(cfg, "height_scan", False) else []
         if len(pts) > N.S3_MAX_RAYS:
             raise ValueError("height scan larger than S3_MAX_RAYS")

@@ -539,13 +539,17 @@ def test_ppo_trains_on_the_motion_and_lift_tasks(task):
 
 
 @pytest.mark.gpu
-def test_domain_randomisation_events_match_oracle():
-    """Startup friction and base-mass randomisation (per world) and interval pushes: pushes every 1-3
-    control steps here, so the kicked base velocities, timers and both scales are all compared."""
+@pytest.mark.parametrize("task", ["velocity", "motion"])
+def test_domain_randomisation_events_match_oracle(task):
+    """Startup friction and base-mass randomisation (per world) and interval pushes, on the velocity and the
+    motion-imitation tasks: pushes every 1-3 control steps here, so the kicked base velocities, timers and
+    both scales are all compared."""
     import torch
 
     n = 8
-    env, ref = _pair("g1_flat", n, push_interval=(0.02, 0.06), push_velocity=0.8)
+    kw = dict(push_interval=(0.02, 0.06), push_velocity=0.8)
+    env, ref = _pair("g1_flat", n, **kw) if task == "velocity" else _motion_pair(n, max_height_error=10.0,
+                                                                                 max_ori_error=10.0, **kw)
     np.testing.assert_allclose(env.reset().cpu().numpy(), ref.reset(), atol=1e-12)
     np.testing.assert_allclose(env.data.friction_scale.cpu().numpy(), ref.fscale, atol=1e-15)
     np.testing.assert_allclose(env.data.mass_scale.cpu().numpy(), ref.mscale, atol=1e-15)
