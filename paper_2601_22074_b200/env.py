@@ -576,8 +576,10 @@ class ManagerBasedRlEnv:
         crosses PCIe in one copy with it (two arenas per copy sustain ~6 % more
         bandwidth). ``step_wait()`` blocks until the oldest pending step's
         results are in host memory and returns its host views (obs groups,
-        reward, terminated, truncated), valid until ``step_async`` has been
-        called ``PIPE_SLOTS`` more times. At most ``PIPE_SLOTS`` steps may be
+        reward, terminated, truncated); ``PIPE_SLOTS + 2`` pinned host blocks
+        rotate, so the views stay valid through at least the next two
+        ``step_async`` calls, even with the pipeline full (the third may
+        reuse them). At most ``PIPE_SLOTS`` steps may be
         pending; with several in flight the host enqueues step i+1 while
         earlier steps run, hiding its own per-step cost. The action tensor is
         read asynchronously: do not overwrite it before that step's

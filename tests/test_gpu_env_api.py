@@ -870,8 +870,8 @@ def test_step_async_paired_and_sequential_waits(monkeypatch, n, group, slots):
 
 @pytest.mark.gpu
 def test_step_wait_view_survives_the_next_step_async():
-    """With the pipeline full (PIPE_SLOTS steps pending), the host view step_wait returned is not
-    overwritten by the following step_async (PIPE_SLOTS + 2 host blocks, ss_pipe_*)."""
+    """With the pipeline full (PIPE_SLOTS steps pending), the host view step_wait returned survives the
+    next two step_async calls (PIPE_SLOTS + 2 host blocks, ss_pipe_*)."""
     from paper_2601_22074_b200.env import PIPE_SLOTS, ManagerBasedRlEnv
     from paper_2601_22074_b200.tasks import make_env_cfg
 
@@ -881,20 +881,25 @@ def test_step_wait_view_survives_the_next_step_async():
     b.reset()
     rng = np.random.default_rng(8)
     acts = [torch.from_numpy(rng.uniform(-1, 1, size=(256, a.action_manager.total_dim))).pin_memory()
-            for _ in range(PIPE_SLOTS + 6)]
+            for _ in range(PIPE_SLOTS + 7)]
     want = []
     for x in acts:
         _, r, _, _, _ = a.step(x.cuda())
         want.append(r.cpu().clone())
     for i in range(PIPE_SLOTS):
         b.step_async(acts[i])
-    for i in range(PIPE_SLOTS, len(acts)):
-        view = b.step_wait()  # step i - PIPE_SLOTS
-        b.step_async(acts[i])  # the pipeline is full again
+    nxt, k = PIPE_SLOTS, 0  # next step to submit, next step to wait for
+    while nxt + 1 < len(acts):
+        view = b.step_wait()  # step k
+        b.step_async(acts[nxt])  # the pipeline is full again
+        view2 = b.step_wait()  # step k + 1
+        b.step_async(acts[nxt + 1])  # a second enqueue
         torch.cuda.synchronize()  # every copy issued so far has landed
-        assert torch.equal(view["reward"], want[i - PIPE_SLOTS]), i
-    for i in range(len(acts) - PIPE_SLOTS, len(acts)):
-        assert torch.equal(b.step_wait()["reward"], want[i])
+        assert torch.equal(view["reward"], want[k]) and torch.equal(view2["reward"], want[k + 1]), k
+        nxt, k = nxt + 2, k + 2
+    while k < nxt:  # drain the submitted steps
+        assert torch.equal(b.step_wait()["reward"], want[k]), k
+        k += 1
 
 
 @pytest.mark.gpu
