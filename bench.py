@@ -662,7 +662,8 @@ def run_ours(args):
         "d2h_bytes_per_step": int(env.step_outputs.numel()),
         "path": "pinned host actions -> env.step_async (H2D cudaMemcpyAsync on a copy-engine stream, the step "
                 "kernel waits on it; the output arena is snapshotted D2D and copied to pinned host memory on a "
-                "second copy-engine stream, overlapping the next step) -> env.step_wait (results in host memory)"}
+                "second copy-engine stream -- two consecutive steps' arenas per copy once both are submitted -- "
+                "overlapping the next steps) -> env.step_wait (results in host memory)"}
 
     scale = at_scale(args, flush, stream) if (world == 1 and args.scale_envs > 0) else None
     s3 = None if args.no_sim3d else sim3d_leg(args, flush, stream)
